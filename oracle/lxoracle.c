@@ -1,0 +1,516 @@
+/*
+ * lxoracle.c -- CPU ORACLE for the LeXInt hot path (arxiv 2310.08344).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference leg may load this library.
+ * The product (paper_2310_08344_b200/) never includes, links or calls it,
+ * and this file includes nothing from the product.
+ *
+ * Plain, slow, obviously-correct fp64 C: plain loops, no blocking, no fusion,
+ * no reordering beyond what the paper's definitions state.  Every function
+ * cites the passage it follows:
+ *   P:<line>  = /root/reference/PAPER.md line (section / equation / listing)
+ *   S:<line>  = /root/reference/SPEC.md line
+ *   R<k>      = reading k of DESIGN.md "Readings of the paper" (= SURVEY 8(c)).
+ *
+ * Pins (tests/test_oracle_*.py, -m "not gpu"): mpmath phi values, closed
+ * forms, brute-force Leja greedy property, dense expm / augmented-matrix phi,
+ * FFT-exact solutions of the circulant stencil operators, convergence orders.
+ */
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#include <float.h>
+
+#define OC_OK 0
+#define OC_ERR_ARG 1
+#define OC_ERR_UNSUPPORTED 4
+#define OC_ERR_NOCONV 5
+#define OC_ERR_NONFINITE 6
+
+/* ------------------------------------------------------------------------- */
+/* vector helpers ("vecops")                                          */
+/* ------------------------------------------------------------------------- */
+
+/* Pairwise sum of x[i]^2 over [lo, hi) (pairwise summation). */
+static double sumsq_pairwise(const double *x, long lo, long hi)
+{
+    if (hi - lo <= 8) {
+        double s = 0.0;
+        for (long i = lo; i < hi; i++) s += x[i] * x[i];
+        return s;
+    }
+    long mid = lo + (hi - lo) / 2;
+    return sumsq_pairwise(x, lo, mid) + sumsq_pairwise(x, mid, hi);
+}
+
+/* ||x||_2 / sqrt(N): "l2 norm normalised to sqrt(N)" (§2.2). */
+double oc_l2norm_scaled(const double *x, long n)
+{
+    if (n <= 0) return 0.0;
+    return sqrt(sumsq_pairwise(x, 0, n) / (double)n);
+}
+
+/* ------------------------------------------------------------------------- */
+/* phi_l scalar functions (§1)                                           */
+/*   phi_0 = exp, phi_{l+1}(z) = (phi_l(z) - 1/l!)/z.                         */
+/* Taylor phi_l(z) = sum_k z^k/(k+l)! for |z| < 2 (R: the recursion cancels   */
+/* catastrophically near 0); exp + the recursion otherwise.                   */
+/* ------------------------------------------------------------------------- */
+static double factorial(int l)
+{
+    double f = 1.0;
+    for (int i = 2; i <= l; i++) f *= (double)i;
+    return f;
+}
+
+double oc_phi(int l, double z)
+{
+    if (l < 0) return NAN;
+    if (fabs(z) < 2.0) {
+        double term = 1.0 / factorial(l);   /* k = 0 term: 1/l! */
+        double sum = term;
+        for (int k = 1; k <= 60; k++) {
+            term = term * z / (double)(k + l);
+            sum += term;
+            if (fabs(term) < 1e-18 * fabs(sum)) break;
+        }
+        return sum;
+    }
+    double p = exp(z);                       /* phi_0 */
+    for (int j = 0; j < l; j++)              /* phi_{j+1} = (phi_j - 1/j!)/z */
+        p = (p - 1.0 / factorial(j)) / z;
+    return p;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Leja points on K = [-2, 2] (§2.1):                                    */
+/*   prod_{k<j} |z_j - z_k| = max_{z in K} prod_{k<j} |z - z_k|,               */
+/*   |z_0| = max |z|  ->  z_0 = +2 (R7: sign +).                               */
+/* For j >= 2 every candidate lies strictly between two consecutive sorted    */
+/* nodes; on such a gap log prod|z - xi_k| is concave, so its maximiser is    */
+/* the root of g(z) = sum_k 1/(z - xi_k) (decreasing from +inf to -inf),      */
+/* found by bisection.  The largest gap maximum wins; ties (|dL| <= 1e-12)    */
+/* go to the larger z (R7).                                             */
+/* ------------------------------------------------------------------------- */
+static double leja_g(const double *xi, int j, double z)
+{
+    double s = 0.0;
+    for (int k = 0; k < j; k++) s += 1.0 / (z - xi[k]);
+    return s;
+}
+
+static double leja_logprod(const double *xi, int j, double z)
+{
+    double s = 0.0;
+    for (int k = 0; k < j; k++) s += log(fabs(z - xi[k]));
+    return s;
+}
+
+static int cmp_double(const void *a, const void *b)
+{
+    double x = *(const double *)a, y = *(const double *)b;
+    return (x > y) - (x < y);
+}
+
+int oc_leja_points(int count, double *xi)
+{
+    if (count < 1 || !xi) return OC_ERR_ARG;
+    xi[0] = 2.0;
+    if (count == 1) return OC_OK;
+    xi[1] = -2.0;                 /* argmax |z - 2| on [-2, 2] */
+    double *sorted = (double *)malloc(sizeof(double) * (size_t)count);
+    if (!sorted) return OC_ERR_ARG;
+    for (int j = 2; j < count; j++) {
+        memcpy(sorted, xi, sizeof(double) * (size_t)j);
+        qsort(sorted, (size_t)j, sizeof(double), cmp_double);
+        double best_z = 0.0, best_L = -INFINITY;
+        for (int gidx = 0; gidx + 1 < j; gidx++) {
+            double lo = sorted[gidx], hi = sorted[gidx + 1];
+            for (int it = 0; it < 200; it++) {
+                double mid = 0.5 * (lo + hi);
+                if (mid <= lo || mid >= hi) break;
+                double g = leja_g(xi, j, mid);
+                if (g == 0.0) { lo = hi = mid; break; }   /* exact root */
+                if (g > 0.0) lo = mid; else hi = mid;
+            }
+            double z = 0.5 * (lo + hi);
+            double L = leja_logprod(xi, j, z);
+            if (L > best_L + 1e-12 || (fabs(L - best_L) <= 1e-12 && z > best_z)) {
+                best_L = L;
+                best_z = z;
+            }
+        }
+        xi[j] = best_z;
+    }
+    free(sorted);
+    return OC_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Divided differences (R8):                                     */
+/*   d_k = h[xi_0, ..., xi_k] of h(xi) = phi_l(a * dt * (c + gamma * xi)),     */
+/* by the triangular recurrence d[i:] = (d[i:] - d[i-1]) / (xi[i:] - xi[i-1]). */
+/* a is the vertical coefficient (R14).                                 */
+/* ------------------------------------------------------------------------- */
+int oc_divided_differences(int l, const double *xi, int m, double dt, double c,
+                           double gamma, double a, double *d)
+{
+    if (m < 1 || !xi || !d) return OC_ERR_ARG;
+    if (l < 0 || l > 4) return OC_ERR_UNSUPPORTED;
+    for (int k = 0; k < m; k++) d[k] = oc_phi(l, a * dt * (c + gamma * xi[k]));
+    for (int i = 1; i < m; i++)
+        for (int j = i; j < m; j++)
+            d[j] = (d[j] - d[i - 1]) / (xi[j] - xi[i - 1]);
+    for (int k = 0; k < m; k++)
+        if (!isfinite(d[k])) return OC_ERR_NONFINITE;
+    return OC_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Problems (R5, R10, R16).                                         */
+/*   f(u) = diff * lap(u) + nu * sum_d D_d u + react * (u - u^3)               */
+/*   lap : second-order centred 5-/7-point Laplacian                   */
+/*   D_d : third-order upwind, +x-biased (R10):                                */
+/*         (-u[i+2] + 6u[i+1] - 3u[i] - 2u[i-1]) / (6 dx)                      */
+/*   periodic on [-1,1)^ndim, row-major, dim 0 slowest.                */
+/*   J(u) v = diff * lap(v) + nu * sum_d D_d v + react * (1 - 3u^2) v (exact,  */
+/*   R13).  Nonlinear remainder F(x) = f(x) - J(u) x with the linear  */
+/*   part cancelled exactly (R18):  F(x) = g(x) - g'(u) x,  g(x) = react(x-x^3)*/
+/* ------------------------------------------------------------------------- */
+typedef struct {
+    int ndim;        /* 2 or 3 */
+    long n[3];       /* points per dimension; n[2] = 1 when ndim = 2 */
+    double dx[3];    /* grid spacing per dimension */
+    double diff;     /* diffusion coefficient */
+    double nu;       /* advection velocity */
+    double react;    /* Allen-Cahn reaction weight (0 or 1) */
+} oc_problem;
+
+static long oc_npoints(const oc_problem *pb)
+{
+    long N = 1;
+    for (int d = 0; d < pb->ndim; d++) N *= pb->n[d];
+    return N;
+}
+
+static long wrap(long i, long n)
+{
+    while (i < 0) i += n;
+    while (i >= n) i -= n;
+    return i;
+}
+
+/* index of the point at (i0, i1, i2) with periodic wrap */
+static long pidx(const oc_problem *pb, long i0, long i1, long i2)
+{
+    long n1 = pb->n[1], n2 = pb->ndim == 3 ? pb->n[2] : 1;
+    i0 = wrap(i0, pb->n[0]);
+    i1 = wrap(i1, n1);
+    i2 = pb->ndim == 3 ? wrap(i2, n2) : 0;
+    return (i0 * n1 + i1) * n2 + i2;
+}
+
+/* value of y at offset o along dimension d from point (i0,i1,i2) */
+static double at(const oc_problem *pb, const double *y, long i0, long i1, long i2, int d, long o)
+{
+    if (d == 0) return y[pidx(pb, i0 + o, i1, i2)];
+    if (d == 1) return y[pidx(pb, i0, i1 + o, i2)];
+    return y[pidx(pb, i0, i1, i2 + o)];
+}
+
+/* Linear constant-coefficient part: w = diff * lap(y) + nu * sum_d D_d y. */
+static void apply_linear(const oc_problem *pb, const double *y, double *w)
+{
+    long n0 = pb->n[0], n1 = pb->n[1], n2 = pb->ndim == 3 ? pb->n[2] : 1;
+    for (long i0 = 0; i0 < n0; i0++)
+        for (long i1 = 0; i1 < n1; i1++)
+            for (long i2 = 0; i2 < n2; i2++) {
+                double lap = 0.0, adv = 0.0;
+                for (int d = 0; d < pb->ndim; d++) {
+                    double h = pb->dx[d];
+                    double um1 = at(pb, y, i0, i1, i2, d, -1);
+                    double u0 = at(pb, y, i0, i1, i2, d, 0);
+                    double up1 = at(pb, y, i0, i1, i2, d, 1);
+                    double up2 = at(pb, y, i0, i1, i2, d, 2);
+                    lap += (up1 - 2.0 * u0 + um1) / (h * h);
+                    adv += (-up2 + 6.0 * up1 - 3.0 * u0 - 2.0 * um1) / (6.0 * h);
+                }
+                w[pidx(pb, i0, i1, i2)] = pb->diff * lap + pb->nu * adv;
+            }
+}
+
+/* f(u) (Eq. (1); problems P:559; R16) */
+void oc_rhs(const oc_problem *pb, const double *u, double *f)
+{
+    long N = oc_npoints(pb);
+    apply_linear(pb, u, f);
+    if (pb->react != 0.0)
+        for (long i = 0; i < N; i++) f[i] += pb->react * (u[i] - u[i] * u[i] * u[i]);
+}
+
+/* w = J(u) y, exact Jacobian (R13). u may be NULL when react == 0. */
+void oc_jac_apply(const oc_problem *pb, const double *u, const double *y, double *w)
+{
+    long N = oc_npoints(pb);
+    apply_linear(pb, y, w);
+    if (pb->react != 0.0)
+        for (long i = 0; i < N; i++) w[i] += pb->react * (1.0 - 3.0 * u[i] * u[i]) * y[i];
+}
+
+/* F(x) = f(x) - J(u) x  =  g(x) - g'(u) x  (R18) */
+void oc_nonlinear_remainder(const oc_problem *pb, const double *u, const double *x, double *out)
+{
+    long N = oc_npoints(pb);
+    for (long i = 0; i < N; i++) {
+        if (pb->react != 0.0) {
+            double g = pb->react * (x[i] - x[i] * x[i] * x[i]);
+            double gp = pb->react * (1.0 - 3.0 * u[i] * u[i]);
+            out[i] = g - gp * x[i];
+        } else {
+            out[i] = 0.0;
+        }
+    }
+}
+
+/* Spectral bound |lambda_max| (R9, R16): Fourier symbol of the constant part
+ * at theta = pi in every dimension, sum_d (4 diff/dx_d^2 + 4|nu|/(3 dx_d)),
+ * plus the Gershgorin shift of the reaction, react * max(0, 3 max u^2 - 1). */
+double oc_spectrum_bound(const oc_problem *pb, const double *u)
+{
+    double b = 0.0;
+    for (int d = 0; d < pb->ndim; d++) {
+        double h = pb->dx[d];
+        b += 4.0 * pb->diff / (h * h) + 4.0 * fabs(pb->nu) / (3.0 * h);
+    }
+    if (pb->react != 0.0 && u) {
+        long N = oc_npoints(pb);
+        double m = 0.0;
+        for (long i = 0; i < N; i++) if (u[i] * u[i] > m) m = u[i] * u[i];
+        double s = 3.0 * m - 1.0;
+        if (s > 0.0) b += pb->react * s;
+    }
+    return b;
+}
+
+/* Power iteration (R9): v_0 = ones + e_0; k_pw iterations of
+ * w = J v, estimate = ||w|| / ||v||, v = w / ||w||.  Returns the last estimate. */
+double oc_power_iteration(const oc_problem *pb, const double *u, int iters)
+{
+    long N = oc_npoints(pb);
+    double *v = (double *)malloc(sizeof(double) * (size_t)N);
+    double *w = (double *)malloc(sizeof(double) * (size_t)N);
+    if (!v || !w) { free(v); free(w); return NAN; }
+    for (long i = 0; i < N; i++) v[i] = 1.0;
+    v[0] += 1.0;
+    double est = 0.0;
+    for (int k = 0; k < iters; k++) {
+        oc_jac_apply(pb, u, v, w);
+        double nw = oc_l2norm_scaled(w, N), nv = oc_l2norm_scaled(v, N);
+        est = nw / nv;
+        for (long i = 0; i < N; i++) v[i] = w[i] / nw;
+    }
+    free(v);
+    free(w);
+    return est;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Real Leja interpolation (Eq. (2); P:155 stopping rule;           */
+/* listings alg:leja_exp_int, alg:leja_phi_nl_int, alg:leja_phi; R1-R6, R14). */
+/*                                                                             */
+/*   y_0 = v,  p_0^{(k)} = d_0^{(k)} y_0                                        */
+/*   for m = 1, 2, ...:                                                        */
+/*     y_m = y_{m-1} * ((z - c)/gamma - xi_{m-1})   with z -> J(u)             */
+/*     p_m^{(k)} = p_{m-1}^{(k)} + d_m^{(k)} y_m        (active k only)        */
+/*     accumulator k converges when                                            */
+/*        ||d_m^{(k)} y_m|| <= rtol ||p_m^{(k)}|| + atol  (norms / sqrt(N))    */
+/*     and is frozen; stop when all K have converged (iters = m).             */
+/*   coeffs a_k: p^{(k)} ~ phi_l(a_k dt J(u)) v  (vertical).    */
+/*   margins[0] = min_k thr/err at acceptance; margins[1] = min over the      */
+/*   rejected checks of err/thr (how far the decisions were from flipping).   */
+/* ------------------------------------------------------------------------- */
+int oc_real_leja_phi(const oc_problem *pb, const double *u_lin, const double *v,
+                     double **outs, const double *coeffs, int K, double dt, double c,
+                     double gamma, int l, double rtol, double atol, const double *xi,
+                     int max_nodes, int *iters, double *margins)
+{
+    if (iters) *iters = 0;
+    if (margins) { margins[0] = INFINITY; margins[1] = INFINITY; }
+    if (K < 1 || K > 4 || !pb || !v || !outs || !coeffs || !xi || max_nodes < 2) return OC_ERR_ARG;
+    if (l < 0 || l > 4) return OC_ERR_UNSUPPORTED;
+    if (!(gamma > 0.0) && dt != 0.0) return OC_ERR_ARG;
+    for (int k = 0; k < K; k++)
+        if (!(coeffs[k] > 0.0 && coeffs[k] <= 1.0) || (k > 0 && !(coeffs[k] > coeffs[k - 1])))
+            return OC_ERR_ARG;
+
+    long N = oc_npoints(pb);
+    double *y = (double *)malloc(sizeof(double) * (size_t)N);
+    double *w = (double *)malloc(sizeof(double) * (size_t)N);
+    double *d = (double *)malloc(sizeof(double) * (size_t)max_nodes * (size_t)K);
+    if (!y || !w || !d) { free(y); free(w); free(d); return OC_ERR_ARG; }
+
+    int status = OC_OK;
+    for (int k = 0; k < K; k++) {
+        int s = oc_divided_differences(l, xi, max_nodes, dt, c, gamma, coeffs[k], d + (size_t)k * max_nodes);
+        if (s != OC_OK) { status = s; goto done; }
+    }
+
+    int active[4] = {0, 0, 0, 0};
+    for (long i = 0; i < N; i++) y[i] = v[i];
+    for (int k = 0; k < K; k++) {
+        active[k] = 1;
+        for (long i = 0; i < N; i++) outs[k][i] = d[(size_t)k * max_nodes + 0] * v[i];
+    }
+
+    status = OC_ERR_NOCONV;
+    for (int m = 1; m < max_nodes; m++) {
+        oc_jac_apply(pb, u_lin, y, w);                       /* w = J y */
+        for (long i = 0; i < N; i++)                         /* Eq. (2) */
+            y[i] = (w[i] - c * y[i]) / gamma - xi[m - 1] * y[i];
+        double ny = oc_l2norm_scaled(y, N);
+        int n_active = 0;
+        for (int k = 0; k < K; k++) {
+            if (!active[k]) continue;
+            double dm = d[(size_t)k * max_nodes + m];
+            for (long i = 0; i < N; i++) outs[k][i] = outs[k][i] + dm * y[i];
+            double np = oc_l2norm_scaled(outs[k], N);
+            double err = fabs(dm) * ny;
+            double thr = rtol * np + atol;
+            if (!isfinite(err) || !isfinite(thr)) { status = OC_ERR_NONFINITE; if (iters) *iters = m; goto done; }
+            if (err <= thr) {
+                active[k] = 0;
+                if (margins) { double r = err > 0.0 ? thr / err : INFINITY; if (r < margins[0]) margins[0] = r; }
+            } else {
+                n_active++;
+                if (margins) { double r = err / thr; if (r < margins[1]) margins[1] = r; }
+            }
+        }
+        if (iters) *iters = m;
+        if (n_active == 0) { status = OC_OK; break; }
+    }
+done:
+    free(y);
+    free(w);
+    free(d);
+    return status;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Exponential integrators (listings alg:Ros_Eu, alg:exprb32;      */
+/* EXPRB43 and EPIRK4s3A tableaux from P:83's citations, R17).                */
+/*   method 0 Rosenbrock-Euler, 1 EXPRB32, 2 EXPRB43, 3 EPIRK4s3A.             */
+/* u_low may be NULL for Rosenbrock-Euler (non-embedded, err = 0).            */
+/* ------------------------------------------------------------------------- */
+static void axpby(double a, const double *x, double b, const double *y, double *z, long N)
+{
+    for (long i = 0; i < N; i++) z[i] = a * x[i] + b * y[i];
+}
+
+int oc_step(const oc_problem *pb, int method, const double *u, double *u_low, double *u_high,
+            double *err, double dt, double c, double gamma, double rtol, double atol,
+            const double *xi, int max_nodes, int *iters)
+{
+    long N = oc_npoints(pb);
+    int it = 0, total = 0, s = OC_OK;
+    if (err) *err = 0.0;
+    if (iters) *iters = 0;
+    if (method < 0 || method > 3) return OC_ERR_ARG;
+    size_t bytes = sizeof(double) * (size_t)N;
+    double *f_u = (double *)malloc(bytes);
+    double *t1 = (double *)malloc(bytes), *t2 = (double *)malloc(bytes), *t3 = (double *)malloc(bytes);
+    double *t4 = (double *)malloc(bytes), *t5 = (double *)malloc(bytes), *t6 = (double *)malloc(bytes);
+    double *t7 = (double *)malloc(bytes);
+    if (!f_u || !t1 || !t2 || !t3 || !t4 || !t5 || !t6 || !t7) { s = OC_ERR_ARG; goto out; }
+
+    /* f_u = RHS(u) * dt  (alg:Ros_Eu P:468-469) */
+    oc_rhs(pb, u, f_u);
+    for (long i = 0; i < N; i++) f_u[i] = dt * f_u[i];
+
+    if (method == 0) {
+        /* u_exprb2 = u + phi_1(J dt) f_u dt */
+        double one = 1.0;
+        double *o[1] = {t1};
+        s = oc_real_leja_phi(pb, u, f_u, o, &one, 1, dt, c, gamma, 1, rtol, atol, xi, max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        axpby(1.0, u, 1.0, t1, u_high, N);
+        if (u_low) axpby(1.0, u, 1.0, t1, u_low, N);
+    } else if (method == 1) {
+        /* EXPRB32 (alg:exprb32 P:512-540) */
+        double one = 1.0;
+        double *o[1] = {t1};                                  /* u_flux */
+        s = oc_real_leja_phi(pb, u, f_u, o, &one, 1, dt, c, gamma, 1, rtol, atol, xi, max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        axpby(1.0, u, 1.0, t1, u_low, N);                     /* u_exprb2 = a */
+        oc_nonlinear_remainder(pb, u, u, t2);                 /* NL_u */
+        oc_nonlinear_remainder(pb, u, u_low, t3);             /* NL_a */
+        axpby(dt, t3, -dt, t2, t4, N);                        /* R_a = (NL_a - NL_u) dt */
+        double *o3[1] = {t5};                                 /* u_nl_3 */
+        s = oc_real_leja_phi(pb, u, t4, o3, &one, 1, dt, c, gamma, 3, rtol, atol, xi, max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        axpby(1.0, u_low, 2.0, t5, u_high, N);                /* u_exprb3 = a + 2 u_nl_3 */
+        for (long i = 0; i < N; i++) t6[i] = 2.0 * t5[i];      /* error_vector */
+        if (err) *err = oc_l2norm_scaled(t6, N);
+    } else {
+        /* EXPRB43 (method 2) / EPIRK4s3A (method 3) -- R17 tableaux:
+         *  EXPRB43:   a = u + 1/2 hphi_1(hJ/2) f;  b = u + hphi_1 f + hphi_1 D_a
+         *             u3 = u + hphi_1 f + hphi_3 (16 D_a - 2 D_b)
+         *             u4 = u3 + hphi_4 (-48 D_a + 12 D_b)
+         *  EPIRK4s3A: a = u + 1/2 hphi_1(hJ/2) f;  b = u + 2/3 hphi_1(2hJ/3) f
+         *             u3 = u + hphi_1 f + hphi_3 (32 D_a - 27/2 D_b)
+         *             u4 = u3 + hphi_4 (-144 D_a + 81 D_b)
+         *  D_x = dt (F(x) - F(u)); vertical phi_1 on f_u. */
+        int epirk = (method == 3);
+        double cf2[2] = {0.5, 1.0}, cf3[3] = {0.5, 2.0 / 3.0, 1.0};
+        double *pv[3] = {t1, t2, t3};
+        s = oc_real_leja_phi(pb, u, f_u, pv, epirk ? cf3 : cf2, epirk ? 3 : 2, dt, c, gamma, 1,
+                             rtol, atol, xi, max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        double *p_half = t1, *p_one = epirk ? t3 : t2;
+        double *NLu = t4, *Da = t5, *Db = t6, *tmp = t7;
+        oc_nonlinear_remainder(pb, u, u, NLu);
+        /* a = u + 1/2 p_half */
+        axpby(1.0, u, 0.5, p_half, u_low, N);
+        oc_nonlinear_remainder(pb, u, u_low, tmp);
+        axpby(dt, tmp, -dt, NLu, Da, N);                      /* D_a */
+        if (epirk) {
+            /* b = u + 2/3 p_twothirds */
+            axpby(1.0, u, 2.0 / 3.0, t2, u_low, N);
+        } else {
+            /* b = u + p_one + phi_1(hJ) D_a */
+            double one = 1.0;
+            double *o[1] = {u_high};
+            s = oc_real_leja_phi(pb, u, Da, o, &one, 1, dt, c, gamma, 1, rtol, atol, xi, max_nodes, &it, NULL);
+            total += it;
+            if (s) goto out;
+            for (long i = 0; i < N; i++) u_low[i] = u[i] + p_one[i] + u_high[i];
+        }
+        oc_nonlinear_remainder(pb, u, u_low, tmp);
+        axpby(dt, tmp, -dt, NLu, Db, N);                      /* D_b */
+        double a3 = epirk ? 32.0 : 16.0, b3 = epirk ? -13.5 : -2.0;
+        double a4 = epirk ? -144.0 : -48.0, b4 = epirk ? 81.0 : 12.0;
+        axpby(a3, Da, b3, Db, tmp, N);                        /* w3 */
+        axpby(a4, Da, b4, Db, NLu, N);                        /* w4 (NLu no longer needed) */
+        double one = 1.0;
+        double *o3[1] = {Da};
+        s = oc_real_leja_phi(pb, u, tmp, o3, &one, 1, dt, c, gamma, 3, rtol, atol, xi, max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        double *o4[1] = {Db};
+        s = oc_real_leja_phi(pb, u, NLu, o4, &one, 1, dt, c, gamma, 4, rtol, atol, xi, max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        for (long i = 0; i < N; i++) u_low[i] = u[i] + p_one[i] + Da[i];    /* u3 */
+        for (long i = 0; i < N; i++) u_high[i] = u_low[i] + Db[i];          /* u4 */
+        for (long i = 0; i < N; i++) tmp[i] = u_high[i] - u_low[i];
+        if (err) *err = oc_l2norm_scaled(tmp, N);
+    }
+out:
+    if (iters) *iters = total;
+    free(f_u); free(t1); free(t2); free(t3); free(t4); free(t5); free(t6); free(t7);
+    return s;
+}

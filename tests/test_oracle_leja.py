@@ -1,0 +1,214 @@
+"""Pins for the oracle's real Leja interpolation and integrators.
+
+Exactness references (never the oracle itself):
+  * FFT-exact phi_l(dt A) v for the circulant stencil operators, with the
+    spectrum taken from the FFT of the operator's impulse response;
+  * dense scipy expm / augmented-matrix phi on <= 16x16 grids;
+  * per-entry mpmath phi for diagonal operators;
+  * a mode-by-mode (Fourier) simulation of the Leja recurrence with 60-digit
+    divided differences, which must stop at the same iteration;
+  * convergence orders of the integrators against a scipy DOP853 reference.
+"""
+import math
+
+import numpy as np
+import pytest
+import scipy.integrate
+
+import oracle as O
+import workloads as W
+from tests import refs
+
+
+def _advdiff(n, nu=10.0):
+    return O.Problem((n, n), (2 / n, 2 / n), 1.0, nu, 0.0)
+
+
+def _cg(pb, u=None):
+    return O.shift_scale(O.spectrum_bound(pb, u))
+
+
+@pytest.mark.parametrize("l", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("mult", [1.0, 10.0, 100.0])
+def test_leja_vs_fft_exact(xi300, l, mult):
+    n = 64
+    pb = _advdiff(n)
+    dt = mult * W.dt_cfl(n, 10.0)
+    c, g = _cg(pb)
+    u0 = W.ic_problem1_2d(n)
+    r = O.real_leja_phi(pb, u0, dt, c, g, l, 1e-13, 1e-13, xi300)
+    assert r.status == O.OK
+    sym = refs.impulse_symbol(lambda v: O.jac_apply(pb, None, v), (n, n))
+    ex = refs.fft_apply_phi(sym, u0, dt, l)
+    rel = np.linalg.norm(r.outs[0] - ex) / np.linalg.norm(ex)
+    # a-posteriori stop is not a bound: allow 100x tol
+    assert rel <= 1e-11, rel
+
+
+@pytest.mark.parametrize("l", [0, 1, 3])
+def test_leja_iteration_count_matches_spectral_simulation(xi300, l):
+    # The stopping decision depends only on the recurrence; a Fourier-space
+    # simulation with 60-digit divided differences must stop at the same m.
+    for n, mult in [(64, 1.0), (64, 10.0), (64, 100.0), (128, 10.0)]:
+        pb = _advdiff(n)
+        dt = mult * W.dt_cfl(n, 10.0)
+        c, g = _cg(pb)
+        u0 = W.ic_problem1_2d(n)
+        r = O.real_leja_phi(pb, u0, dt, c, g, l, 1e-10, 1e-10, xi300)
+        sym = refs.impulse_symbol(lambda v: O.jac_apply(pb, None, v), (n, n))
+        m, p = refs.spectral_leja_iters(sym, u0, dt, c, g, l, 1e-10, 1e-10, xi300, max_nodes=160)
+        assert r.iters == m, (n, mult, r.iters, m)
+        assert np.linalg.norm(r.outs[0] - p) <= 1e-12 * np.linalg.norm(p)   # d_k conditioning at rho~60
+        assert min(r.margins) > 1.0
+
+
+@pytest.mark.parametrize("l", [0, 1, 3])
+@pytest.mark.parametrize("nu,mult", [(3.0, 5.0), (1.0, 20.0)])
+def test_leja_vs_dense_augmented(xi300, l, nu, mult):
+    # 12x12 grid, broadband random v.  (Real Leja needs a spectrum close to the
+    # real axis: at this coarse grid nu = 3, 20 x CFL diverges -- P:141's
+    # ellipse case, out of scope, so the cases here keep rho*|Im|/|Re| small.)
+    n = 12
+    pb = _advdiff(n, nu=nu)
+    M = refs.dense_matrix(lambda v: O.jac_apply(pb, None, v.reshape(n, n)), n * n)
+    v = W.random_vector((n, n), seed=11)
+    c, g = _cg(pb)
+    dt = mult * W.dt_cfl(n, nu)
+    r = O.real_leja_phi(pb, v, dt, c, g, l, 1e-14, 1e-14, xi300)
+    assert r.status == O.OK
+    ex = refs.dense_phi(M, v.ravel(), dt, l)
+    assert np.linalg.norm(r.outs[0].ravel() - ex) <= 1e-12 * np.linalg.norm(ex)
+
+
+def test_leja_diagonal_operator_per_entry(xi300):
+    # diagonal J = diag(1 - 3u^2) -> p_i = phi_l(dt J_ii) v_i.
+    u = np.linspace(0.6, 4.0, 64).reshape(8, 8)           # J_ii in [-47, -0.08]
+    pb = O.Problem((8, 8), (0.25, 0.25), 0.0, 0.0, 1.0)
+    v = W.random_vector((8, 8), seed=2)
+    c, g = _cg(pb, u)
+    dt = 0.5
+    for l in range(5):
+        r = O.real_leja_phi(pb, v, dt, c, g, l, 1e-14, 1e-15, xi300, u_lin=u)
+        assert r.status == O.OK
+        ex = np.array([float(refs.phi_mp(l, dt * (1 - 3 * ui * ui))) for ui in u.ravel()]) * v.ravel()
+        assert np.abs(r.outs[0].ravel() - ex).max() <= 1e-12 * np.abs(ex).max(), l
+
+
+def test_leja_zero_input_and_dt_zero(xi300):
+    pb = _advdiff(16)
+    c, g = _cg(pb)
+    r = O.real_leja_phi(pb, np.zeros((16, 16)), 1e-3, c, g, 1, 1e-10, 1e-10, xi300)
+    assert r.status == O.OK and r.iters == 1 and np.all(r.outs[0] == 0)
+    v = W.ic_problem1_2d(16)
+    for l in range(5):
+        r = O.real_leja_phi(pb, v, 0.0, c, g, l, 1e-10, 1e-10, xi300)
+        assert r.status == O.OK and r.iters == 1
+        np.testing.assert_array_equal(r.outs[0], v * (1.0 / math.factorial(l)))
+
+
+def test_leja_vertical_equals_separate_calls(xi300):
+    # coeffs {0.25, 0.5, 1} == three single-coefficient calls to 1e-11,
+    # shared-recurrence iters <= sum of separate iters.
+    n = 32
+    pb = _advdiff(n)
+    c, g = _cg(pb)
+    dt = 10 * W.dt_cfl(n, 10.0)
+    v = W.ic_problem1_2d(n)
+    cf = (0.25, 0.5, 1.0)
+    rv = O.real_leja_phi(pb, v, dt, c, g, 1, 1e-12, 1e-12, xi300, coeffs=cf)
+    total = 0
+    for k, a in enumerate(cf):
+        # phi_1(a dt A) v == single call with dt' = a dt
+        rs = O.real_leja_phi(pb, v, a * dt, c, g, 1, 1e-12, 1e-12, xi300)
+        total += rs.iters
+        # frozen accumulators stop at the same m as the separate call
+        assert np.linalg.norm(rv.outs[k] - rs.outs[0]) <= 1e-11 * np.linalg.norm(rs.outs[0])
+    assert rv.iters <= total
+
+
+def test_leja_interpolation_error_decays(xi300):
+    n = 64
+    pb = _advdiff(n)
+    c, g = _cg(pb)
+    dt = 10 * W.dt_cfl(n, 10.0)
+    v = W.ic_problem1_2d(n)
+    sym = refs.impulse_symbol(lambda x: O.jac_apply(pb, None, x), (n, n))
+    ex = refs.fft_apply_phi(sym, v, dt, 1)
+    errs, its = [], []
+    for tol in (1e-4, 1e-7, 1e-10, 1e-13):
+        r = O.real_leja_phi(pb, v, dt, c, g, 1, tol, tol, xi300)
+        errs.append(np.linalg.norm(r.outs[0] - ex) / np.linalg.norm(ex))
+        its.append(r.iters)
+    assert all(a > b for a, b in zip(errs, errs[1:])), errs
+    assert all(a < b for a, b in zip(its, its[1:])), its
+
+
+def test_leja_noconv_and_errors(xi300):
+    pb = _advdiff(16)
+    c, g = _cg(pb)
+    v = W.ic_problem1_2d(16)
+    r = O.real_leja_phi(pb, v, 1000 * W.dt_cfl(16, 10.0), c, g, 0, 1e-14, 0.0, xi300, max_nodes=20)
+    assert r.status == O.ERR_NOCONV and r.iters == 19
+    assert O.real_leja_phi(pb, v, 1e-3, c, g, 5, 1e-10, 1e-10, xi300).status == O.ERR_UNSUPPORTED
+    assert O.real_leja_phi(pb, v, 1e-3, c, g, 1, 1e-10, 1e-10, xi300, coeffs=(1.0, 0.5)).status == O.ERR_ARG
+    assert O.real_leja_phi(pb, v, 1e-3, c, -1.0, 1, 1e-10, 1e-10, xi300).status == O.ERR_ARG
+
+
+# ---------------------------------------------------------------- integrators
+@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a"])
+def test_integrator_linear_exactness(xi300, method):
+    # every exponential integrator is exact on linear homogeneous problems
+    n = 64
+    pb = _advdiff(n)
+    c, g = _cg(pb)
+    dt = 10 * W.dt_cfl(n, 10.0)
+    u0 = W.ic_problem1_2d(n)
+    r = O.step(pb, method, u0, dt, c, g, 1e-12, 1e-12, xi300)
+    assert r.status == O.OK
+    sym = refs.impulse_symbol(lambda x: O.jac_apply(pb, None, x), (n, n))
+    ex = refs.fft_apply_phi(sym, u0, dt, 0)
+    assert np.linalg.norm(r.u_high - ex) <= 1e-11 * np.linalg.norm(ex)
+    if method != "rosenbrock_euler":
+        assert r.err == 0.0       # R18: F == 0 exactly for linear f
+
+
+def test_exprb32_embedded_error_contract(xi300):
+    n = 16
+    pb = O.Problem((n, n), (2 / n, 2 / n), 1e-2, 0.0, 1.0)
+    u = W.ic_allen_cahn_2d(n)
+    c, g = _cg(pb, u)
+    r = O.step(pb, "exprb32", u, 0.05, c, g, 1e-12, 1e-12, xi300)
+    assert r.status == O.OK and r.err > 0
+    assert r.err == pytest.approx(O.l2norm_scaled(r.u_high - r.u_low), rel=1e-13)
+
+
+def _allen_cahn_reference(pb, u0, T):
+    n0, n1 = pb.shape
+
+    def f(t, y):
+        return O.rhs(pb, y.reshape(n0, n1)).ravel()
+
+    sol = scipy.integrate.solve_ivp(f, (0, T), u0.ravel(), method="DOP853", rtol=1e-13, atol=1e-13)
+    return sol.y[:, -1].reshape(n0, n1)
+
+
+@pytest.mark.parametrize("method,order", [("rosenbrock_euler", 2), ("exprb32", 3), ("exprb43", 4),
+                                          ("epirk4s3a", 4)])
+def test_integrator_convergence_order(xi300, method, order):
+    n = 16
+    pb = O.Problem((n, n), (2 / n, 2 / n), 2e-3, 0.0, 1.0)
+    u0 = W.ic_allen_cahn_2d(n)
+    T = 0.5
+    uref = _allen_cahn_reference(pb, u0, T)
+    errs = []
+    for nsteps in (4, 8, 16, 32):
+        h = T / nsteps
+        u = u0.copy()
+        for _ in range(nsteps):
+            c, g = _cg(pb, u)
+            r = O.step(pb, method, u, h, c, g, 1e-14, 1e-14, xi300)
+            assert r.status == O.OK
+            u = r.u_high
+        errs.append(np.linalg.norm(u - uref) / np.linalg.norm(uref))
+    orders = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+    assert abs(orders[-1] - order) < 0.3, (errs, orders)
