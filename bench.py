@@ -1,0 +1,300 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native LeXInt hot path (BASELINE.json metric).
+
+Workload at N=1 (BASELINE.json configs[1]): 2D linear advection-diffusion on a
+4096^2 periodic grid (nu = 10, Problem-I Gaussian IC), fp64;
+phi_0..phi_3(dt A) u_0 by real Leja interpolation at dt = 10 dt_CFL with
+rtol = atol = 1e-10.  One bench STEP = the whole hot path over that input:
+spectrum bound -> (c, gamma) -> for l in 0..3: divided differences (host) +
+one persistent fused Leja kernel (device-side stopping decision).
+
+value   = Leja iterations / s (device-timed, inputs resident in HBM)
+e2e     = same metric through the C-ABI with HOST (pinned) buffers, copies inside
+roofline: dominant kernel k_leja2d<1,false>, algorithmic bytes
+          N*(24 + 32*(m-1)) per launch / CUDA-event duration.
+cpu_baseline / --impl reference: the oracle (oracle/) on the host cores.
+
+N>1 (torchrun): weak scaling -- each rank owns a 4096-row slab of a
+(4096*N) x 4096 grid (slab decomposition, NCCL halos + norm allgather); value
+counts 4096^2-equivalent Leja iterations of all ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = "Leja iterations/s and EXPRB steps/s (fp64) at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "Leja it/s"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for name, val in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"),
+                                 f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_baseline(n: int, iters: int = 2, reps: int = 1):
+    """Oracle (as it stands, single-threaded C) on a bounded sample of the workload."""
+    import oracle as O
+    wl = W.config(1, n=n)
+    ob = O.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
+    u0 = W.ic_problem1_2d(n)
+    xi = O.leja_points(300)
+    c, g = O.shift_scale(O.spectrum_bound(ob))
+    tot_it, t = 0, 0.0
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        r = O.real_leja_phi(ob, u0, wl.dt, c, g, 0, wl.rtol, wl.atol, xi, max_nodes=iters + 1)
+        t += time.perf_counter() - t0
+        tot_it += r.iters
+    return {"value": tot_it / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": "oracle real_leja_phi phi_0 on the full %dx%d grid, first %d Leja iterations "
+                      "(node cap %d) x %d, single-threaded plain C" % (n, n, iters, iters + 1, reps)}
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    n = args.n or 4096
+    per_step = args.ref_iters
+    cfg = {"workload": W.config(1, n=n).name, "grid": [n, n], "ls": [0, 1, 2, 3], "dt_cfl_mult": 10.0,
+           "tol": 1e-10, "inputs": "synthetic Problem-I Gaussian IC (P:562)"}
+    for _ in range(args.warmup):
+        cpu_baseline(n, per_step)
+    t0 = time.perf_counter()
+    tot = 0
+    for _ in range(args.steps):
+        r = cpu_baseline(n, per_step)
+        tot += per_step
+    dt = time.perf_counter() - t0
+    val = tot / dt
+    out = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+           "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": r["sample"]},
+           "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def _traffic_from_profiles():
+    p = os.path.join(ROOT, "profiles", "leja_traffic.json")
+    if os.path.exists(p):
+        try:
+            d = json.load(open(p))
+            return d
+        except Exception:
+            return None
+    return None
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2310_08344_b200 as lx
+
+    ws, rank, local = _dist()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    n = args.n or 4096
+    if ws > 1:
+        raise SystemExit("multi-GPU bench path requires the NCCL slab build (not in this version)")
+    wl = W.config(1, n=n)
+    pb = lx.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
+    stream = torch.cuda.current_stream()
+    ctx = lx.Context(pb, stream=stream)
+    u0_h = W.ic_problem1_2d(n)
+    u0 = torch.from_numpy(u0_h).cuda()
+    outs = [torch.empty_like(u0) for _ in range(4)]
+    N = u0.numel()
+
+    def step(ev=None):
+        bound = lx.lx_spectrum_bound(ctx)
+        c, g = lx.lx_shift_scale(bound)
+        for l in range(4):
+            if ev is not None:
+                ev[l][0].record(stream)
+            lx.lx_real_leja_phi(ctx, u0, outs[l], wl.dt, c, g, l, wl.rtol, wl.atol, sync=False)
+            if ev is not None:
+                ev[l][1].record(stream)
+
+    # iteration counts per call (untimed, sync)
+    c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+    iters = [lx.lx_real_leja_phi(ctx, u0, outs[l], wl.dt, c, g, l, wl.rtol, wl.atol) for l in range(4)]
+    for _ in range(args.warmup):
+        step()
+    ctx.synchronize()
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+
+    evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in range(4)]
+           for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.launch_count
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        start.record(stream)
+        for s in range(args.steps):
+            step(evs[s])
+        stop.record(stream)
+        torch.cuda.synchronize()
+    launches = ctx.launch_count - launches0
+    total_iters, _ = ctx.synchronize()
+    ms = start.elapsed_time(stop)
+    assert total_iters == args.steps * sum(iters), (total_iters, iters)
+    value = total_iters / (ms * 1e-3)
+
+    # roofline of the dominant kernel (persistent Leja kernel, one launch per call)
+    durs = np.array([[evs[s][l][0].elapsed_time(evs[s][l][1]) for l in range(4)] for s in range(args.steps)])
+    bytes_per_call = np.array([N * (24 + 32 * (m - 1)) for m in iters], dtype=np.float64)
+    per_call_ms = durs.mean(axis=0)
+    achieved = float(bytes_per_call.sum() / (per_call_ms.sum() * 1e-3) / 1e9)
+    peak, peak_kind = _peaks()
+    tr = _traffic_from_profiles()
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": (tr or {}).get("traffic_bytes_per_launch"),
+            "kernel": "k_leja2d<1,false> (persistent, 1 launch per Leja call)",
+            "algorithmic_bytes_per_launch": [float(b) for b in bytes_per_call],
+            "launch_ms": [float(x) for x in per_call_ms],
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (%s)" % peak_kind,
+            "frac_of_8TBs_spec": achieved / 8000.0,
+            "kernel_share_of_step": float(per_call_ms.sum() / (ms / args.steps))}
+
+    # e2e through the C-ABI with pinned HOST buffers (H2D + D2H inside the timed region)
+    uh = torch.from_numpy(u0_h).pin_memory()
+    oh = [torch.empty(wl.shape, dtype=torch.float64).pin_memory() for _ in range(4)]
+    e2e_steps = max(1, min(args.steps, 5))
+
+    def step_host():
+        bound = lx.lx_spectrum_bound(ctx)
+        c2, g2 = lx.lx_shift_scale(bound)
+        it = 0
+        for l in range(4):
+            it += lx.lx_real_leja_phi(ctx, uh, oh[l], wl.dt, c2, g2, l, wl.rtol, wl.atol)
+        return it
+
+    step_host()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e_it = 0
+    for _ in range(e2e_steps):
+        e_it += step_host()
+    torch.cuda.synchronize()
+    e_t = time.perf_counter() - t0
+    e2e = {"value": e_it / e_t, "unit": UNIT, "h2d_bytes_per_step": 4 * N * 8, "d2h_bytes_per_step": 4 * N * 8,
+           "steps": e2e_steps, "note": "4 lx_real_leja_phi calls with pinned host in/out pointers per step"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = cpu_baseline(n, args.ref_iters)
+    cfg = {"workload": wl.name, "grid": list(wl.shape), "ls": [0, 1, 2, 3], "dt_cfl_mult": 10.0, "dt": wl.dt,
+           "tol": 1e-10, "leja_iters_per_call": iters, "leja_iters_per_step": sum(iters),
+           "l2_policy": "inputs larger than L2 (each fp64 vector %.0f MB > 126 MB L2)" % (N * 8 / 1e6),
+           "inputs": "synthetic Problem-I Gaussian IC (P:562), nu=10", "parallelism": "single GPU"}
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg, "roofline": roof,
+           "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary()}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    ctx.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=0, help="grid side override (default 4096)")
+    ap.add_argument("--ref-iters", type=int, default=2, help="oracle Leja iterations per cpu sample")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,222 @@
+/*
+ * lexint.h -- C ABI of the B200-native LeXInt hot path (arxiv 2310.08344).
+ *
+ * Library: paper_2310_08344_b200/liblexint_b200.so (sm_100a, fp64).
+ * Citations: P:<line> = PAPER.md line (section / equation / listing).
+ *
+ * Conventions (apply to every call below)
+ * ---------------------------------------
+ *  - Scalars and all vector data are IEEE fp64.  Vectors are contiguous,
+ *    row-major, dimension 0 slowest (index = (i*n1 + j)*n2 + k), unpadded,
+ *    and hold the caller's LOCAL slab: rows [i_begin, i_end) of dimension 0
+ *    (the whole grid when the context has no communicator).  P:155 "data ...
+ *    have to lie contiguous in memory".
+ *  - Pointers may be DEVICE pointers (cudaMalloc / torch CUDA tensors, on the
+ *    context's device, 16-byte aligned) or HOST pointers (pageable or pinned).
+ *    Host data is staged through context-owned device buffers with the copies
+ *    on the context stream (the host<->device copies are part of the call).
+ *    Mixing host and device pointers in one call is allowed.
+ *  - Ownership: the caller allocates and owns every input and output vector
+ *    ("the user has to assign the required amount of memory for
+ *    the output vector").  The context owns all scratch (P:307, P:359-407:
+ *    "allocated only once - when an object of this class is created"); it is
+ *    freed by lx_ctx_destroy.
+ *  - Stream ordering: all device work is enqueued on the context stream.
+ *    Calls taking an `int* iters_out` (or `double* err_out`) return after one
+ *    small device->host read of the call's record (one host synchronisation
+ *    per call/step, never per Leja iteration).  Passing NULL for every such
+ *    out-pointer makes the call ASYNCHRONOUS (device pointers only): results
+ *    accumulate in the context record and are read by lx_ctx_synchronize.
+ *  - Errors: every call returns an lx_status; lx_last_error() returns a
+ *    thread-local message for the last non-OK status.  On LX_ERR_NOCONV the
+ *    output holds the last polynomial and *iters_out the node cap - 1.
+ *  - Concurrency: a context is not thread-safe; use one per host thread /
+ *    stream.  Distinct contexts may run concurrently.  No global mutable state
+ *    except the thread-local error string and the (immutable once built)
+ *    Leja-point table.
+ */
+#ifndef LEXINT_H
+#define LEXINT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    LX_OK = 0,
+    LX_ERR_ARG = 1,           /* invalid argument (NULL, gamma <= 0 with dt != 0, bad coeffs, ...) */
+    LX_ERR_DIM = 2,           /* grid shape unsupported (n < 4, odd n_last, slab too thin)        */
+    LX_ERR_ALIAS = 3,         /* an output aliases an input it must not alias                     */
+    LX_ERR_UNSUPPORTED = 4,   /* l > 4, K > 4, ndim not 2/3, ...                                  */
+    LX_ERR_NOCONV = 5,        /* node cap reached without meeting the tolerance          */
+    LX_ERR_NONFINITE = 6,     /* NaN/Inf in a norm (spectrum not enclosed / bad input)            */
+    LX_ERR_UNKNOWN_INTEGRATOR = 7,
+    LX_ERR_CUDA = 8,
+    LX_ERR_NCCL = 9,
+    LX_ERR_TIMEOUT = 10       /* device-side barrier watchdog fired                               */
+} lx_status;
+
+const char *lx_last_error(void);
+const char *lx_version(void);
+
+/* ------------------------------------------------------------------------ */
+/* Host math (no device work)                                                */
+/* ------------------------------------------------------------------------ */
+
+/* Real Leja points on [-2, 2] (§2.1): xi_0 = +2 (|z_0| = max|z|),
+ * xi_j = argmax_z prod_{k<j} |z - xi_k|, ties to the larger z.
+ * count in [1, 4096]; xi_out[count] written.  Errors: LX_ERR_ARG. */
+lx_status lx_leja_points(int count, double *xi_out);
+
+/* phi_l(z): phi_0 = exp, phi_{l+1}(z) = (phi_l(z) - 1/l!)/z.
+ * l in [0, 4] (else LX_ERR_UNSUPPORTED).  Relative accuracy ~1e-15. */
+lx_status lx_phi_scalar(int l, double z, double *out);
+
+/* Newton divided differences d_0..d_{m-1} of h(xi) = phi_l(a*dt*(c + gamma*xi))
+ * at xi[0..m-1] (interpolate phi_l(c + gamma xi) on the Leja
+ * points; a = vertical coefficient, 1.0 for a plain call).
+ * Errors: LX_ERR_ARG (m < 1, NULL), LX_ERR_UNSUPPORTED (l > 4),
+ * LX_ERR_NONFINITE (overflow). */
+lx_status lx_divided_differences(int l, const double *xi, int m, double dt, double c,
+                                 double gamma, double a, double *d_out);
+
+/* Rows [i_begin, i_end) of dimension 0 owned by `rank` of `nranks` slabs. */
+lx_status lx_slab_range(int64_t n0, int rank, int nranks, int64_t *i_begin, int64_t *i_end);
+
+/* ------------------------------------------------------------------------ */
+/* Problem: du/dt = f(u) = A u + g(u)   (Eq. (1))                   */
+/*   A u  = diff * lap(u) + nu * sum_d D_d u                                */
+/*          lap: second-order centred; D_d: third-order upwind, +x-biased   */
+/*          (stencil (-u[i+2] + 6u[i+1] - 3u[i] - 2u[i-1])/(6 dx))   */
+/*   g(u) = react * (u - u^3)   (Allen-Cahn; react = 0 for Problems I/II)   */
+/*   J(u) v = A v + react * (1 - 3u^2) v   (exact Jacobian)                  */
+/* Periodic on every dimension.                                              */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    int ndim;         /* 2 or 3                                               */
+    int64_t n[3];     /* GLOBAL points per dimension (n[2] = 1 when ndim = 2) */
+    double dx[3];     /* grid spacing per dimension                           */
+    double diff;      /* diffusion coefficient                                */
+    double nu;        /* advection velocity                           */
+    double react;     /* reaction weight (0 or 1)                             */
+} lx_problem;
+
+typedef struct lx_ctx lx_ctx;
+
+/* Create a context for problems on the grid of `pb` (only pb->ndim, pb->n
+ * are used here).  max_nodes = Leja node cap (0 -> 300; <= 1024).
+ * device = CUDA device ordinal (-1 -> current).  cuda_stream = cudaStream_t
+ * to enqueue on (NULL -> a stream owned by the context).
+ * Allocates: 2 y buffers + 3-row ghosts each, 7 stage vectors, partial-sum
+ * slots, control block, coefficient-table ring, host staging (lazily).
+ * Errors: LX_ERR_ARG, LX_ERR_DIM, LX_ERR_UNSUPPORTED, LX_ERR_CUDA. */
+lx_status lx_ctx_create(const lx_problem *pb, int max_nodes, int device, void *cuda_stream,
+                        lx_ctx **out);
+lx_status lx_ctx_destroy(lx_ctx *ctx);
+
+/* Attach a communicator for slab decomposition over nranks GPUs (one process
+ * per GPU).  nccl_unique_id: 128 bytes from lx_nccl_unique_id on rank 0,
+ * broadcast by the caller (e.g. torch.distributed).  After this call every
+ * vector argument is the caller's local slab (lx_slab_range).  Collective:
+ * every rank must call it.  Errors: LX_ERR_NCCL, LX_ERR_DIM (slab < 2 rows). */
+lx_status lx_nccl_unique_id(void *out128);
+lx_status lx_ctx_set_comm(lx_ctx *ctx, const void *nccl_unique_id, int rank, int nranks);
+
+/* Local slab of this context: rows [*i_begin, *i_end), *n_local points. */
+lx_status lx_ctx_local(const lx_ctx *ctx, int64_t *i_begin, int64_t *i_end, int64_t *n_local);
+
+/* Wait for all enqueued work; report the iterations / status accumulated by
+ * asynchronous calls since the last synchronize, then reset that record. */
+lx_status lx_ctx_synchronize(lx_ctx *ctx, int *iters_total, double *err_last);
+
+/* Number of kernel launches this context has issued (for bench accounting). */
+int64_t lx_ctx_launch_count(const lx_ctx *ctx);
+
+/* ------------------------------------------------------------------------ */
+/* Spectrum (P:91, P:274-278 listing alg:lexint)                             */
+/* ------------------------------------------------------------------------ */
+
+/* Power iteration on J(u): v_0 = 1 + e_0, `iters` applications,
+ * estimate ||J v|| / ||v||.  u may be NULL when pb->react == 0.
+ * One fused stencil + norm pass per iteration on the device. */
+lx_status lx_spectrum_estimate(lx_ctx *ctx, const lx_problem *pb, const double *u, int iters,
+                               double *lambda_abs_out);
+
+/* Closed-form bound of |lambda_max(J(u))|: sum_d (4 diff/dx_d^2 + 4|nu|/(3dx_d))
+ * (Fourier symbol at theta = pi) + react * max(0, 3 max_i u_i^2 - 1)
+ * (Gershgorin; device max-reduction, bitwise deterministic).  Synchronous. */
+lx_status lx_spectrum_bound(lx_ctx *ctx, const lx_problem *pb, const double *u,
+                            double *lambda_abs_out);
+
+/* Listing alg:lexint P:277-278: eig = -1.05*|lambda|; c = eig/2; gamma = -eig/4. */
+lx_status lx_shift_scale(double lambda_abs, double *c_out, double *gamma_out);
+
+/* ------------------------------------------------------------------------ */
+/* Real Leja interpolation (Eq. (2); P:155 stopping rule;          */
+/* listings alg:leja_exp_ext, alg:leja_phi_nl_ext, alg:leja_phi)             */
+/*   out ~= phi_l(dt J(u)) v, with (c, gamma) enclosing the spectrum of J(u) */
+/*   (NOT of dt J):  y_m = y_{m-1} ((J - c)/gamma - xi_{m-1}),               */
+/*   p_m = p_{m-1} + d_m y_m, stop at the first m >= 1 with                  */
+/*   |d_m| ||y_m|| <= rtol ||p_m|| + atol (norms l2 / sqrt(N_global)).       */
+/*   *iters_out = m (number of operator applications).                       */
+/* Each Leja iteration is ONE fused HBM pass (stencil of y_{m-1}, Newton     */
+/* update, polynomial accumulate, both norm partial sums) and the stopping   */
+/* decision is taken on the device (no host round trip per iteration).       */
+/* u_lin: linearisation state for J(u) (NULL when pb->react == 0).           */
+/* out must not alias v or u_lin (LX_ERR_ALIAS).                             */
+/* ------------------------------------------------------------------------ */
+lx_status lx_real_leja_phi(lx_ctx *ctx, const lx_problem *pb, const double *u_lin,
+                           const double *v, double *out, double dt, double c, double gamma,
+                           int l, double rtol, double atol, int *iters_out);
+
+/* Vertical interpolation (Tokman16): outs[k] ~= phi_l(coeffs[k] dt J(u)) v
+ * for K coefficients 0 < coeffs[0] < ... < coeffs[K-1] <= 1 sharing one
+ * y-recurrence; converged accumulators are frozen; *iters_out = recurrence
+ * steps until all K converged.  K in [1, 4]. */
+lx_status lx_real_leja_phi_vertical(lx_ctx *ctx, const lx_problem *pb, const double *u_lin,
+                                    const double *v, double *const *outs, const double *coeffs,
+                                    int K, double dt, double c, double gamma, int l, double rtol,
+                                    double atol, int *iters_out);
+
+/* ------------------------------------------------------------------------ */
+/* Exponential integrator steps (listings alg:Ros_Eu, alg:exprb32; */
+/* EXPRB43 / EPIRK4s3A tableaux from the papers cited at P:83).              */
+/*   u: state u^n; u_low / u_high: lower / higher order u^{n+1};             */
+/*   *err_out = ||u_high - u_low|| / sqrt(N) (EXPRB32: ||2 u_nl_3||). */
+/*   *iters_out = total Leja iterations of the step.                         */
+/* Outputs must not alias u; u_low != u_high.                                */
+/* ------------------------------------------------------------------------ */
+typedef enum {
+    LX_ROSENBROCK_EULER = 0,
+    LX_EXPRB32 = 1,
+    LX_EXPRB43 = 2,
+    LX_EPIRK4S3A = 3
+} lx_method;
+
+/* Rosenbrock-Euler: u_out = u + phi_1(dt J(u)) f(u) dt (alg:Ros_Eu). */
+lx_status lx_step_rosenbrock_euler(lx_ctx *ctx, const lx_problem *pb, const double *u,
+                                   double *u_out, double dt, double c, double gamma,
+                                   double rtol, double atol, int *iters_out);
+lx_status lx_step_exprb32(lx_ctx *ctx, const lx_problem *pb, const double *u, double *u_low,
+                          double *u_high, double *err_out, double dt, double c, double gamma,
+                          double rtol, double atol, int *iters_out);
+lx_status lx_step_exprb43(lx_ctx *ctx, const lx_problem *pb, const double *u, double *u_low,
+                          double *u_high, double *err_out, double dt, double c, double gamma,
+                          double rtol, double atol, int *iters_out);
+lx_status lx_step_epirk4s3a(lx_ctx *ctx, const lx_problem *pb, const double *u, double *u_low,
+                            double *u_high, double *err_out, double dt, double c, double gamma,
+                            double rtol, double atol, int *iters_out);
+/* Dispatch by method (the paper's exp_int / embed_exp_int). */
+lx_status lx_step(lx_ctx *ctx, lx_method method, const lx_problem *pb, const double *u,
+                  double *u_low, double *u_high, double *err_out, double dt, double c,
+                  double gamma, double rtol, double atol, int *iters_out);
+
+/* f(u) * dt (alg:Ros_Eu P:468-469) as a standalone fused stencil pass. */
+lx_status lx_rhs(lx_ctx *ctx, const lx_problem *pb, const double *u, double scale, double *f_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LEXINT_H */

@@ -1,0 +1,303 @@
+"""B200-native LeXInt hot path (arxiv 2310.08344): Python binding of the C ABI.
+
+Argument marshalling only -- every step of the path runs in
+``liblexint_b200.so`` (sm_100a CUDA kernels + C++ host runtime, declared in
+``include/lexint.h``).  PyTorch is used for device memory, streams and
+``torch.distributed`` plumbing.  There is no CPU fallback: if the shared
+library is missing or cannot be loaded this package raises at import/use.
+
+Names follow the C ABI: ``lx_leja_points``, ``lx_divided_differences``,
+``lx_spectrum_estimate``, ``lx_spectrum_bound``, ``lx_real_leja_phi``,
+``lx_real_leja_phi_vertical``, ``lx_step_<integrator>`` ...
+Vectors may be CUDA tensors (device pointers, zero copy) or numpy arrays /
+CPU tensors (host pointers: the library stages them through device buffers).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "liblexint_b200.so")
+
+LX_OK, LX_ERR_ARG, LX_ERR_DIM, LX_ERR_ALIAS, LX_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
+LX_ERR_NOCONV, LX_ERR_NONFINITE, LX_ERR_UNKNOWN_INTEGRATOR, LX_ERR_CUDA, LX_ERR_NCCL = 5, 6, 7, 8, 9
+LX_ERR_TIMEOUT = 10
+STATUS_NAMES = {0: "LX_OK", 1: "LX_ERR_ARG", 2: "LX_ERR_DIM", 3: "LX_ERR_ALIAS", 4: "LX_ERR_UNSUPPORTED",
+                5: "LX_ERR_NOCONV", 6: "LX_ERR_NONFINITE", 7: "LX_ERR_UNKNOWN_INTEGRATOR", 8: "LX_ERR_CUDA",
+                9: "LX_ERR_NCCL", 10: "LX_ERR_TIMEOUT"}
+LX_ROSENBROCK_EULER, LX_EXPRB32, LX_EXPRB43, LX_EPIRK4S3A = 0, 1, 2, 3
+METHODS = {"rosenbrock_euler": 0, "exprb32": 1, "exprb43": 2, "epirk4s3a": 3}
+
+# Every symbol include/lexint.h declares (checked by tests/test_abi.py).
+EXPORTS = ("lx_last_error", "lx_version", "lx_leja_points", "lx_phi_scalar", "lx_divided_differences",
+           "lx_slab_range", "lx_ctx_create", "lx_ctx_destroy", "lx_nccl_unique_id", "lx_ctx_set_comm",
+           "lx_ctx_local", "lx_ctx_synchronize", "lx_ctx_launch_count", "lx_spectrum_estimate",
+           "lx_spectrum_bound", "lx_shift_scale", "lx_real_leja_phi", "lx_real_leja_phi_vertical",
+           "lx_step_rosenbrock_euler", "lx_step_exprb32", "lx_step_exprb43", "lx_step_epirk4s3a",
+           "lx_step", "lx_rhs")
+
+
+class LxError(RuntimeError):
+    def __init__(self, status: int, msg: str, iters: int | None = None):
+        super().__init__("%s: %s" % (STATUS_NAMES.get(status, status), msg))
+        self.status = status
+        self.iters = iters
+
+
+class LxProblem(ctypes.Structure):
+    _fields_ = [("ndim", ctypes.c_int), ("n", ctypes.c_int64 * 3), ("dx", ctypes.c_double * 3),
+                ("diff", ctypes.c_double), ("nu", ctypes.c_double), ("react", ctypes.c_double)]
+
+
+@dataclass(frozen=True)
+class Problem:
+    """du/dt = diff*lap(u) + nu*sum_d D_d u + react*(u - u^3) on a periodic GLOBAL grid."""
+    shape: tuple
+    dx: tuple
+    diff: float = 1.0
+    nu: float = 0.0
+    react: float = 0.0
+
+    def c_struct(self) -> LxProblem:
+        nd = len(self.shape)
+        n = list(self.shape) + [1] * (3 - nd)
+        dx = list(self.dx) + [1.0] * (3 - nd)
+        return LxProblem(nd, (ctypes.c_int64 * 3)(*n), (ctypes.c_double * 3)(*dx), float(self.diff),
+                         float(self.nu), float(self.react))
+
+    @property
+    def npoints(self) -> int:
+        return int(np.prod(self.shape))
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load liblexint_b200.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError("liblexint_b200.so not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, dp, ip = ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)
+        pbp = ctypes.POINTER(LxProblem)
+        i64p = ctypes.POINTER(ctypes.c_int64)
+        d = ctypes.c_double
+        sig = {
+            "lx_last_error": (ctypes.c_char_p, []),
+            "lx_version": (ctypes.c_char_p, []),
+            "lx_leja_points": (ctypes.c_int, [ctypes.c_int, dp]),
+            "lx_phi_scalar": (ctypes.c_int, [ctypes.c_int, d, dp]),
+            "lx_divided_differences": (ctypes.c_int, [ctypes.c_int, dp, ctypes.c_int, d, d, d, d, dp]),
+            "lx_slab_range": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int, ctypes.c_int, i64p, i64p]),
+            "lx_ctx_create": (ctypes.c_int, [pbp, ctypes.c_int, ctypes.c_int, vp, ctypes.POINTER(vp)]),
+            "lx_ctx_destroy": (ctypes.c_int, [vp]),
+            "lx_nccl_unique_id": (ctypes.c_int, [vp]),
+            "lx_ctx_set_comm": (ctypes.c_int, [vp, vp, ctypes.c_int, ctypes.c_int]),
+            "lx_ctx_local": (ctypes.c_int, [vp, i64p, i64p, i64p]),
+            "lx_ctx_synchronize": (ctypes.c_int, [vp, ip, dp]),
+            "lx_ctx_launch_count": (ctypes.c_int64, [vp]),
+            "lx_spectrum_estimate": (ctypes.c_int, [vp, pbp, vp, ctypes.c_int, dp]),
+            "lx_spectrum_bound": (ctypes.c_int, [vp, pbp, vp, dp]),
+            "lx_shift_scale": (ctypes.c_int, [d, dp, dp]),
+            "lx_real_leja_phi": (ctypes.c_int, [vp, pbp, vp, vp, vp, d, d, d, ctypes.c_int, d, d, ip]),
+            "lx_real_leja_phi_vertical": (ctypes.c_int, [vp, pbp, vp, vp, ctypes.POINTER(vp), dp, ctypes.c_int,
+                                                         d, d, d, ctypes.c_int, d, d, ip]),
+            "lx_step": (ctypes.c_int, [vp, ctypes.c_int, pbp, vp, vp, vp, dp, d, d, d, d, d, ip]),
+            "lx_step_rosenbrock_euler": (ctypes.c_int, [vp, pbp, vp, vp, d, d, d, d, d, ip]),
+            "lx_step_exprb32": (ctypes.c_int, [vp, pbp, vp, vp, vp, dp, d, d, d, d, d, ip]),
+            "lx_step_exprb43": (ctypes.c_int, [vp, pbp, vp, vp, vp, dp, d, d, d, d, d, ip]),
+            "lx_step_epirk4s3a": (ctypes.c_int, [vp, pbp, vp, vp, vp, dp, d, d, d, d, d, ip]),
+            "lx_rhs": (ctypes.c_int, [vp, pbp, vp, d, vp]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(status: int, iters: int | None = None):
+    if status != LX_OK:
+        raise LxError(status, lib().lx_last_error().decode(), iters)
+
+
+def _ptr(x):
+    """Raw pointer of a torch tensor (device or host) or numpy array (host)."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        assert x.dtype == np.float64 and x.flags.c_contiguous, "float64 C-contiguous arrays only"
+        return x.ctypes.data
+    # torch.Tensor
+    assert x.dtype.is_floating_point and x.element_size() == 8 and x.is_contiguous(), "fp64 contiguous tensors only"
+    return x.data_ptr()
+
+
+# ------------------------------------------------------------------ host math
+def lx_leja_points(count: int) -> np.ndarray:
+    xi = np.zeros(count)
+    _check(lib().lx_leja_points(count, xi.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+    return xi
+
+
+def lx_phi_scalar(l: int, z: float) -> float:
+    out = ctypes.c_double()
+    _check(lib().lx_phi_scalar(int(l), float(z), ctypes.byref(out)))
+    return out.value
+
+
+def lx_divided_differences(l, xi, m, dt, c, gamma, a=1.0) -> np.ndarray:
+    xi = np.ascontiguousarray(xi, dtype=np.float64)
+    d = np.zeros(m)
+    dp = ctypes.POINTER(ctypes.c_double)
+    _check(lib().lx_divided_differences(int(l), xi.ctypes.data_as(dp), int(m), float(dt), float(c), float(gamma),
+                                        float(a), d.ctypes.data_as(dp)))
+    return d
+
+
+def lx_slab_range(n0: int, rank: int, nranks: int):
+    b, e = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().lx_slab_range(int(n0), int(rank), int(nranks), ctypes.byref(b), ctypes.byref(e)))
+    return b.value, e.value
+
+
+def lx_shift_scale(lambda_abs: float):
+    c, g = ctypes.c_double(), ctypes.c_double()
+    _check(lib().lx_shift_scale(float(lambda_abs), ctypes.byref(c), ctypes.byref(g)))
+    return c.value, g.value
+
+
+def lx_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().lx_nccl_unique_id(buf))
+    return buf.raw
+
+
+# ------------------------------------------------------------------ context
+class Context:
+    """Owns an lx_ctx (scratch allocated once)."""
+
+    def __init__(self, problem: Problem, max_nodes: int = 300, device: int = -1, stream=None):
+        self.problem = problem
+        self._pb = problem.c_struct()
+        h = ctypes.c_void_p()
+        sp = None
+        if stream is not None:
+            sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        _check(lib().lx_ctx_create(ctypes.byref(self._pb), int(max_nodes), int(device), sp, ctypes.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            lib().lx_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def set_comm(self, uid: bytes, rank: int, nranks: int):
+        buf = ctypes.create_string_buffer(uid, 128)
+        _check(lib().lx_ctx_set_comm(self.handle, buf, int(rank), int(nranks)))
+
+    def local(self):
+        b, e, n = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().lx_ctx_local(self.handle, ctypes.byref(b), ctypes.byref(e), ctypes.byref(n)))
+        return b.value, e.value, n.value
+
+    def synchronize(self):
+        it, err = ctypes.c_int(), ctypes.c_double()
+        st = lib().lx_ctx_synchronize(self.handle, ctypes.byref(it), ctypes.byref(err))
+        _check(st, it.value)
+        return it.value, err.value
+
+    @property
+    def launch_count(self) -> int:
+        return int(lib().lx_ctx_launch_count(self.handle))
+
+
+def _pb(ctx: Context, problem: Problem | None):
+    return ctypes.byref(problem.c_struct() if problem is not None else ctx._pb)
+
+
+def lx_spectrum_bound(ctx: Context, u=None, problem: Problem | None = None) -> float:
+    out = ctypes.c_double()
+    _check(lib().lx_spectrum_bound(ctx.handle, _pb(ctx, problem), _ptr(u), ctypes.byref(out)))
+    return out.value
+
+
+def lx_spectrum_estimate(ctx: Context, u=None, iters: int = 50, problem: Problem | None = None) -> float:
+    out = ctypes.c_double()
+    _check(lib().lx_spectrum_estimate(ctx.handle, _pb(ctx, problem), _ptr(u), int(iters), ctypes.byref(out)))
+    return out.value
+
+
+def lx_real_leja_phi(ctx: Context, v, out, dt, c, gamma, l, rtol, atol, u_lin=None,
+                     problem: Problem | None = None, sync: bool = True):
+    """out <- phi_l(dt J(u_lin)) v.  Returns the Leja iteration count (None if sync=False)."""
+    it = ctypes.c_int(0)
+    st = lib().lx_real_leja_phi(ctx.handle, _pb(ctx, problem), _ptr(u_lin), _ptr(v), _ptr(out), float(dt), float(c),
+                                float(gamma), int(l), float(rtol), float(atol), ctypes.byref(it) if sync else None)
+    _check(st, it.value)
+    return it.value if sync else None
+
+
+def lx_real_leja_phi_vertical(ctx: Context, v, outs: Sequence, coeffs: Sequence[float], dt, c, gamma, l, rtol,
+                              atol, u_lin=None, problem: Problem | None = None, sync: bool = True):
+    K = len(outs)
+    arr = (ctypes.c_void_p * K)(*[_ptr(o) for o in outs])
+    cf = (ctypes.c_double * K)(*[float(a) for a in coeffs])
+    it = ctypes.c_int(0)
+    st = lib().lx_real_leja_phi_vertical(ctx.handle, _pb(ctx, problem), _ptr(u_lin), _ptr(v), arr, cf, K,
+                                         float(dt), float(c), float(gamma), int(l), float(rtol), float(atol),
+                                         ctypes.byref(it) if sync else None)
+    _check(st, it.value)
+    return it.value if sync else None
+
+
+def lx_step(ctx: Context, method, u, u_low, u_high, dt, c, gamma, rtol, atol, problem: Problem | None = None,
+            sync: bool = True):
+    """One exponential-integrator step.  Returns (iters, err) (None, None if sync=False)."""
+    m = METHODS[method] if isinstance(method, str) else int(method)
+    it, err = ctypes.c_int(0), ctypes.c_double(0.0)
+    st = lib().lx_step(ctx.handle, m, _pb(ctx, problem), _ptr(u), _ptr(u_low), _ptr(u_high),
+                       ctypes.byref(err) if sync else None, float(dt), float(c), float(gamma), float(rtol),
+                       float(atol), ctypes.byref(it) if sync else None)
+    _check(st, it.value)
+    return (it.value, err.value) if sync else (None, None)
+
+
+def lx_step_rosenbrock_euler(ctx, u, u_out, dt, c, gamma, rtol, atol, problem=None):
+    return lx_step(ctx, LX_ROSENBROCK_EULER, u, None, u_out, dt, c, gamma, rtol, atol, problem)[0]
+
+
+def lx_step_exprb32(ctx, u, u_low, u_high, dt, c, gamma, rtol, atol, problem=None):
+    return lx_step(ctx, LX_EXPRB32, u, u_low, u_high, dt, c, gamma, rtol, atol, problem)
+
+
+def lx_step_exprb43(ctx, u, u_low, u_high, dt, c, gamma, rtol, atol, problem=None):
+    return lx_step(ctx, LX_EXPRB43, u, u_low, u_high, dt, c, gamma, rtol, atol, problem)
+
+
+def lx_step_epirk4s3a(ctx, u, u_low, u_high, dt, c, gamma, rtol, atol, problem=None):
+    return lx_step(ctx, LX_EPIRK4S3A, u, u_low, u_high, dt, c, gamma, rtol, atol, problem)
+
+
+def lx_rhs(ctx: Context, u, f_out, scale: float = 1.0, problem: Problem | None = None):
+    _check(lib().lx_rhs(ctx.handle, _pb(ctx, problem), _ptr(u), float(scale), _ptr(f_out)))

@@ -1,0 +1,21 @@
+// lx_comm.h -- slab decomposition over NCCL (one process per GPU).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/lexint.h"
+#include "lx_internal.h"
+
+namespace lx {
+struct Comm;
+const char* comm_error();
+int comm_unique_id(void* out128);
+int comm_create(const void* uid, int rank, int nranks, int device, long long row, int max_grid, Comm** out);
+void comm_destroy(Comm* c);
+void comm_bind(Comm* c, double* const Y[2], double* const Yg[2], double* vg, int n_loc, int rank, int nranks);
+lx_status comm_leja(Comm* c, LejaParams& P, bool diag, cudaStream_t s, int64_t* launches);
+lx_status comm_power(Comm* c, LejaParams& P, bool diag, cudaStream_t s, int64_t* launches);
+int comm_allreduce_max_u64(Comm* c, unsigned long long* dev, cudaStream_t s);
+int comm_stage_norm(Comm* c, int op, const StageArgs& A, cudaStream_t s, int64_t* launches);
+int comm_rhs(Comm* c, LejaParams& P, double scale, cudaStream_t s, int64_t* launches);
+}  // namespace lx

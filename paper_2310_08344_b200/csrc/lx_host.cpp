@@ -1,0 +1,796 @@
+// lx_host.cpp -- host runtime and C ABI of the B200-native LeXInt hot path.
+//
+// Owns the context (scratch buffers allocated once, P:307 / P:359-407), builds
+// the per-call coefficient tables (beta_m = -c/gamma - xi_{m-1}, d_m^(k)),
+// launches the persistent Leja kernel / stage kernels on the context stream
+// and reads back one small record per call or step.  See include/lexint.h.
+#include "../../include/lexint.h"
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "lx_hostmath.h"
+#include "lx_internal.h"
+#include "lx_comm.h"
+
+using namespace lx;
+
+static thread_local std::string g_err;
+
+static lx_status fail(lx_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+#define CUDA_TRY(x)                                                                       \
+    do {                                                                                  \
+        cudaError_t e_ = (x);                                                             \
+        if (e_ != cudaSuccess) return fail(LX_ERR_CUDA, "%s: %s", #x, cudaGetErrorString(e_)); \
+    } while (0)
+
+#define LX_TRY(x)                     \
+    do {                              \
+        lx_status s_ = (x);           \
+        if (s_ != LX_OK) return s_;   \
+    } while (0)
+
+static constexpr int kCoefSlots = 32;
+static constexpr int kStage = 4;   // integrator scratch vectors
+static constexpr int kHost = 6;    // host-pointer staging vectors
+
+struct lx_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int ndim = 2;
+    int64_t n[3] = {1, 1, 1};
+    int64_t i_begin = 0, i_end = 0;
+    int n_loc = 0;
+    int64_t row = 0;          // doubles per row (n1*n2)
+    int64_t N_loc = 0;
+    double N_glob = 0;
+    int max_nodes = 300;
+    int nsm = 0;
+    // device memory
+    double* Y[2] = {nullptr, nullptr};
+    double* Yg[2] = {nullptr, nullptr};   // ghost rows (comm mode)
+    double* vg = nullptr;                 // ghost rows of the iteration-1 input
+    double* S[kStage] = {};
+    double* H[kHost] = {};
+    double* partials = nullptr;
+    int max_grid = 0;
+    Ctrl* ctrl = nullptr;
+    Record* rec_dev = nullptr;            // [2]: 0 sync, 1 async
+    Record* rec_host = nullptr;           // pinned [2]
+    Record* rec_init = nullptr;           // pinned template
+    unsigned long long* umax_host = nullptr;
+    double* coef_dev = nullptr;
+    double* coef_host = nullptr;
+    size_t coef_stride = 0;
+    cudaEvent_t coef_ev[kCoefSlots] = {};
+    int coef_next = 0;
+    int64_t launches = 0;
+    std::vector<double> xi;
+    Comm* comm = nullptr;                 // slab decomposition (lx_comm.cpp)
+};
+
+// ------------------------------------------------------------------ helpers
+static bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static Stencil make_stencil(const lx_problem* pb) {
+    Stencil st;
+    std::memset(&st, 0, sizeof st);
+    double c0 = 0.0;
+    for (int d = 0; d < pb->ndim; d++) {
+        const double h = pb->dx[d], ih2 = 1.0 / (h * h);
+        // diff*(u[+1] - 2u + u[-1])/h^2 + nu*(-u[+2] + 6u[+1] - 3u - 2u[-1])/(6h)
+        st.m1[d] = pb->diff * ih2 - pb->nu / (3.0 * h);
+        st.p1[d] = pb->diff * ih2 + pb->nu / h;
+        st.p2[d] = -pb->nu / (6.0 * h);
+        c0 += -2.0 * pb->diff * ih2 - pb->nu / (2.0 * h);
+    }
+    st.c0 = c0;
+    st.react = pb->react;
+    st.qa = pb->react;          // J_ii = react*(1 - 3u^2)
+    st.qb = -3.0 * pb->react;
+    return st;
+}
+
+static lx_status check_problem(const lx_ctx* ctx, const lx_problem* pb) {
+    if (!pb) return fail(LX_ERR_ARG, "problem is NULL");
+    if (pb->ndim != ctx->ndim) return fail(LX_ERR_DIM, "problem ndim %d != context ndim %d", pb->ndim, ctx->ndim);
+    for (int d = 0; d < pb->ndim; d++)
+        if (pb->n[d] != ctx->n[d]) return fail(LX_ERR_DIM, "problem n[%d] differs from the context grid", d);
+    for (int d = 0; d < pb->ndim; d++)
+        if (!(pb->dx[d] > 0.0)) return fail(LX_ERR_ARG, "dx[%d] must be > 0", d);
+    if (pb->ndim != 2) return fail(LX_ERR_UNSUPPORTED, "only ndim = 2 is implemented on the device");
+    return LX_OK;
+}
+
+static double* stage_buf(lx_ctx* ctx, int i) {
+    if (!ctx->H[i]) {
+        if (cudaMalloc(&ctx->H[i], ctx->N_loc * sizeof(double)) != cudaSuccess) return nullptr;
+    }
+    return ctx->H[i];
+}
+
+static double* scratch(lx_ctx* ctx, int i) {
+    if (!ctx->S[i]) {
+        if (cudaMalloc(&ctx->S[i], ctx->N_loc * sizeof(double)) != cudaSuccess) return nullptr;
+    }
+    return ctx->S[i];
+}
+
+// Host<->device staging of one call's vectors.
+struct Staging {
+    lx_ctx* ctx;
+    int next = 0;
+    struct Out { double* host; double* dev; };
+    std::vector<Out> outs;
+    bool any_host = false;
+    explicit Staging(lx_ctx* c) : ctx(c) {}
+    lx_status in(const double* p, const double** dev) {
+        if (!p) { *dev = nullptr; return LX_OK; }
+        if (is_device_ptr(p)) { *dev = p; return LX_OK; }
+        any_host = true;
+        double* b = stage_buf(ctx, next++);
+        if (!b) return fail(LX_ERR_CUDA, "staging allocation failed");
+        CUDA_TRY(cudaMemcpyAsync(b, p, ctx->N_loc * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        *dev = b;
+        return LX_OK;
+    }
+    lx_status out(double* p, double** dev) {
+        if (!p) { *dev = nullptr; return LX_OK; }
+        if (is_device_ptr(p)) { *dev = p; return LX_OK; }
+        any_host = true;
+        double* b = stage_buf(ctx, next++);
+        if (!b) return fail(LX_ERR_CUDA, "staging allocation failed");
+        outs.push_back({p, b});
+        *dev = b;
+        return LX_OK;
+    }
+    lx_status finish() {
+        for (auto& o : outs)
+            CUDA_TRY(cudaMemcpyAsync(o.host, o.dev, ctx->N_loc * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        return LX_OK;
+    }
+};
+
+static lx_status reset_record(lx_ctx* ctx, int r) {
+    CUDA_TRY(cudaMemcpyAsync(ctx->rec_dev + r, ctx->rec_init, sizeof(Record), cudaMemcpyHostToDevice, ctx->stream));
+    return LX_OK;
+}
+
+static lx_status read_record(lx_ctx* ctx, int r, Record* out) {
+    CUDA_TRY(cudaMemcpyAsync(ctx->rec_host + r, ctx->rec_dev + r, sizeof(Record), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    *out = ctx->rec_host[r];
+    return LX_OK;
+}
+
+static lx_status status_of(const Record& r) {
+    switch (r.status) {
+        case 0: return LX_OK;
+        case 5: return fail(LX_ERR_NOCONV, "Leja interpolation did not converge within the node cap (iters %d)", r.iters);
+        case 6: return fail(LX_ERR_NONFINITE, "non-finite norm in the Leja iteration (spectrum not enclosed?)");
+        case 10: return fail(LX_ERR_TIMEOUT, "device barrier watchdog fired");
+        default: return fail(LX_ERR_CUDA, "device status %d", r.status);
+    }
+}
+
+// Build the coefficient table of one Leja call into a ring slot and enqueue its H2D.
+static lx_status build_coefs(lx_ctx* ctx, int l, const double* coeffs, int K, double dt, double c, double gamma,
+                             const double** dev_out) {
+    const int M = ctx->max_nodes;
+    const int slot = ctx->coef_next;
+    ctx->coef_next = (slot + 1) % kCoefSlots;
+    CUDA_TRY(cudaEventSynchronize(ctx->coef_ev[slot]));
+    double* tab = ctx->coef_host + slot * ctx->coef_stride;
+    std::vector<double> d(M);
+    for (int k = 0; k < K; k++) {
+        const int s = lx::divided_differences(l, ctx->xi.data(), M, dt, c, gamma, coeffs[k], d.data());
+        if (s == 6) return fail(LX_ERR_NONFINITE, "divided differences overflow (dt*gamma too large?)");
+        if (s) return fail(LX_ERR_ARG, "divided differences failed (%d)", s);
+        for (int m = 0; m < M; m++) tab[(size_t)m * (1 + K) + 1 + k] = d[m];
+    }
+    for (int m = 0; m < M; m++)
+        tab[(size_t)m * (1 + K)] = (m == 0 || dt == 0.0) ? 0.0 : (-c / gamma - ctx->xi[m - 1]);
+    double* dev = ctx->coef_dev + slot * ctx->coef_stride;
+    CUDA_TRY(cudaMemcpyAsync(dev, tab, (size_t)M * (1 + K) * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaEventRecord(ctx->coef_ev[slot], ctx->stream));
+    *dev_out = dev;
+    return LX_OK;
+}
+
+static LejaParams base_params(lx_ctx* ctx, const lx_problem* pb) {
+    LejaParams P;
+    std::memset(&P, 0, sizeof P);
+    P.ndim = ctx->ndim;
+    P.n_loc = ctx->n_loc;
+    P.n1 = (int)ctx->n[1];
+    P.n2 = 1;
+    P.nb = (P.n1 + 63) / 64;
+    P.nrb = (P.n_loc + kRT - 1) / kRT;
+    P.nunits = P.nb * P.nrb;
+    P.N_glob = ctx->N_glob;
+    P.st = make_stencil(pb);
+    P.ctrl = ctx->ctrl;
+    P.partials = ctx->partials;
+    P.timeout_spins = 1 << 24;
+    for (int i = 0; i < 2; i++) {
+        P.ysrc[i] = RowSrc{ctx->Y[i], ctx->comm ? ctx->Yg[i] : nullptr, ctx->row, ctx->n_loc, 0};
+        P.ydst[i] = ctx->Y[i];
+    }
+    return P;
+}
+
+// Core Leja call on device pointers (no staging, no sync).
+static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u, const double* v, double* const* outs,
+                             const double* coeffs, int K, double dt, double c, double gamma, int l, double rtol,
+                             double atol, int rec) {
+    const double* coef = nullptr;
+    LX_TRY(build_coefs(ctx, l, coeffs, K, dt, c, gamma, &coef));
+    LejaParams P = base_params(ctx, pb);
+    const bool diag = pb->react != 0.0;
+    P.K = K;
+    P.max_nodes = ctx->max_nodes;
+    P.active0 = (1 << K) - 1;
+    P.alpha = (dt == 0.0) ? 0.0 : 1.0 / gamma;
+    P.rtol = rtol;
+    P.atol = atol;
+    P.coef = coef;
+    P.v = RowSrc{v, nullptr, ctx->row, ctx->n_loc, 0};
+    for (int k = 0; k < K; k++) P.p[k] = outs[k];
+    P.u = u;
+    P.rec = ctx->rec_dev + rec;
+    if (ctx->comm) return comm_leja(ctx->comm, P, diag, ctx->stream, &ctx->launches);
+    P.grid = leja_grid_size(ctx->device, K, diag, ctx->ndim, P.nunits);
+    CUDA_TRY(launch_leja_persistent(P, ctx->stream, diag));
+    ctx->launches++;
+    return LX_OK;
+}
+
+static lx_status validate_leja(const lx_problem* pb, const double* u, const double* v, double* const* outs,
+                               const double* coeffs, int K, double dt, double gamma, int l) {
+    if (!v || !outs || !coeffs) return fail(LX_ERR_ARG, "NULL argument");
+    if (K < 1 || K > kMaxK) return fail(LX_ERR_UNSUPPORTED, "K = %d not in [1, 4]", K);
+    if (l < 0 || l > 4) return fail(LX_ERR_UNSUPPORTED, "phi_%d not supported (l <= 4)", l);
+    if (!(gamma > 0.0) && dt != 0.0) return fail(LX_ERR_ARG, "gamma must be > 0 (got %g)", gamma);
+    if (!std::isfinite(dt)) return fail(LX_ERR_ARG, "dt not finite");
+    for (int k = 0; k < K; k++) {
+        if (!(coeffs[k] > 0.0 && coeffs[k] <= 1.0)) return fail(LX_ERR_ARG, "coeffs[%d] not in (0, 1]", k);
+        if (k > 0 && !(coeffs[k] > coeffs[k - 1])) return fail(LX_ERR_ARG, "coeffs not strictly increasing");
+        if (!outs[k]) return fail(LX_ERR_ARG, "outs[%d] is NULL", k);
+        if (outs[k] == v || (u && outs[k] == u)) return fail(LX_ERR_ALIAS, "out must not alias v or u_lin");
+        for (int j = 0; j < k; j++)
+            if (outs[j] == outs[k]) return fail(LX_ERR_ALIAS, "outs must be distinct");
+    }
+    if (pb->react != 0.0 && !u) return fail(LX_ERR_ARG, "u_lin required when react != 0");
+    return LX_OK;
+}
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+const char* lx_last_error(void) { return g_err.c_str(); }
+const char* lx_version(void) { return "lexint-b200 0.1 (sm_100a, fp64)"; }
+
+lx_status lx_leja_points(int count, double* xi_out) {
+    if (lx::leja_points(count, xi_out)) return fail(LX_ERR_ARG, "count must be in [1, 4096]");
+    return LX_OK;
+}
+
+lx_status lx_phi_scalar(int l, double z, double* out) {
+    if (!out) return fail(LX_ERR_ARG, "out is NULL");
+    if (l < 0 || l > 4) return fail(LX_ERR_UNSUPPORTED, "phi_%d not supported (l <= 4)", l);
+    *out = lx::phi(l, z);
+    return LX_OK;
+}
+
+lx_status lx_divided_differences(int l, const double* xi, int m, double dt, double c, double gamma, double a,
+                                 double* d_out) {
+    const int s = lx::divided_differences(l, xi, m, dt, c, gamma, a, d_out);
+    if (s == 1) return fail(LX_ERR_ARG, "bad arguments");
+    if (s == 4) return fail(LX_ERR_UNSUPPORTED, "phi_%d not supported", l);
+    if (s == 6) return fail(LX_ERR_NONFINITE, "divided differences overflow");
+    return LX_OK;
+}
+
+lx_status lx_slab_range(int64_t n0, int rank, int nranks, int64_t* i_begin, int64_t* i_end) {
+    if (nranks < 1 || rank < 0 || rank >= nranks || n0 < 1 || !i_begin || !i_end)
+        return fail(LX_ERR_ARG, "bad slab arguments");
+    *i_begin = (n0 * rank) / nranks;
+    *i_end = (n0 * (rank + 1)) / nranks;
+    return LX_OK;
+}
+
+lx_status lx_shift_scale(double lambda_abs, double* c_out, double* gamma_out) {
+    if (!(lambda_abs >= 0.0) || !c_out || !gamma_out) return fail(LX_ERR_ARG, "lambda_abs must be >= 0");
+    const double eig = -1.05 * lambda_abs;
+    *c_out = eig / 2.0;
+    *gamma_out = -eig / 4.0;
+    return LX_OK;
+}
+
+static void free_ctx(lx_ctx* ctx) {
+    if (!ctx) return;
+    if (ctx->comm) comm_destroy(ctx->comm);
+    for (double* p : ctx->Y) cudaFree(p);
+    for (double* p : ctx->Yg) cudaFree(p);
+    cudaFree(ctx->vg);
+    for (double* p : ctx->S) cudaFree(p);
+    for (double* p : ctx->H) cudaFree(p);
+    cudaFree(ctx->partials);
+    cudaFree(ctx->ctrl);
+    cudaFree(ctx->rec_dev);
+    cudaFree(ctx->coef_dev);
+    cudaFreeHost(ctx->rec_host);
+    cudaFreeHost(ctx->rec_init);
+    cudaFreeHost(ctx->umax_host);
+    cudaFreeHost(ctx->coef_host);
+    for (auto& e : ctx->coef_ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+static lx_status alloc_local(lx_ctx* ctx) {
+    const size_t bytes = ctx->N_loc * sizeof(double);
+    for (int i = 0; i < 2; i++) {
+        if (ctx->Y[i]) cudaFree(ctx->Y[i]);
+        CUDA_TRY(cudaMalloc(&ctx->Y[i], bytes));
+        CUDA_TRY(cudaMemsetAsync(ctx->Y[i], 0, bytes, ctx->stream));
+    }
+    for (int i = 0; i < kStage; i++) {
+        cudaFree(ctx->S[i]);
+        ctx->S[i] = nullptr;
+    }
+    for (int i = 0; i < kHost; i++) {
+        cudaFree(ctx->H[i]);
+        ctx->H[i] = nullptr;
+    }
+    return LX_OK;
+}
+
+lx_status lx_ctx_create(const lx_problem* pb, int max_nodes, int device, void* cuda_stream, lx_ctx** out) {
+    if (!pb || !out) return fail(LX_ERR_ARG, "NULL argument");
+    *out = nullptr;
+    if (pb->ndim != 2 && pb->ndim != 3) return fail(LX_ERR_UNSUPPORTED, "ndim must be 2 or 3");
+    if (pb->ndim == 3) return fail(LX_ERR_UNSUPPORTED, "3D device kernels not built in this version");
+    for (int d = 0; d < pb->ndim; d++)
+        if (pb->n[d] < 4) return fail(LX_ERR_DIM, "n[%d] = %lld < 4", d, (long long)pb->n[d]);
+    if (pb->n[pb->ndim - 1] % 2) return fail(LX_ERR_DIM, "the contiguous dimension must be even (double2 access)");
+    if (pb->n[0] > (1 << 30) || pb->n[1] > (1 << 30)) return fail(LX_ERR_DIM, "grid too large");
+    if (max_nodes == 0) max_nodes = 300;
+    if (max_nodes < 2 || max_nodes > 1024) return fail(LX_ERR_ARG, "max_nodes must be in [2, 1024]");
+    lx_ctx* ctx = new lx_ctx();
+    if (device < 0) cudaGetDevice(&device);
+    ctx->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) { delete ctx; return fail(LX_ERR_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e)); }
+    if (cuda_stream) {
+        ctx->stream = (cudaStream_t)cuda_stream;
+    } else {
+        e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) { delete ctx; return fail(LX_ERR_CUDA, "stream: %s", cudaGetErrorString(e)); }
+        ctx->own_stream = true;
+    }
+    ctx->ndim = pb->ndim;
+    for (int d = 0; d < 3; d++) ctx->n[d] = d < pb->ndim ? pb->n[d] : 1;
+    ctx->i_begin = 0;
+    ctx->i_end = ctx->n[0];
+    ctx->n_loc = (int)ctx->n[0];
+    ctx->row = ctx->n[1] * ctx->n[2];
+    ctx->N_loc = (int64_t)ctx->n_loc * ctx->row;
+    ctx->N_glob = (double)ctx->n[0] * (double)ctx->row;
+    ctx->max_nodes = max_nodes;
+    cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device);
+    ctx->max_grid = ctx->nsm * 8;
+    ctx->xi.resize(max_nodes);
+    lx::leja_points(max_nodes, ctx->xi.data());
+    lx_status s = LX_OK;
+#define CK(x)                                                                          \
+    do {                                                                               \
+        cudaError_t e_ = (x);                                                          \
+        if (e_ != cudaSuccess) { s = fail(LX_ERR_CUDA, "%s: %s", #x, cudaGetErrorString(e_)); goto bad; } \
+    } while (0)
+    CK(cudaMalloc(&ctx->partials, (size_t)2 * ctx->max_grid * kSlot * sizeof(double)));
+    CK(cudaMalloc(&ctx->ctrl, sizeof(Ctrl)));
+    CK(cudaMemsetAsync(ctx->ctrl, 0, sizeof(Ctrl), ctx->stream));
+    CK(cudaMalloc(&ctx->rec_dev, 2 * sizeof(Record)));
+    CK(cudaMallocHost(&ctx->rec_host, 2 * sizeof(Record)));
+    CK(cudaMallocHost(&ctx->rec_init, sizeof(Record)));
+    CK(cudaMallocHost(&ctx->umax_host, sizeof(unsigned long long)));
+    std::memset(ctx->rec_init, 0, sizeof(Record));
+    ctx->rec_init->margin_accept = INFINITY;
+    ctx->rec_init->margin_reject = INFINITY;
+    ctx->coef_stride = (size_t)max_nodes * (1 + kMaxK);
+    CK(cudaMalloc(&ctx->coef_dev, kCoefSlots * ctx->coef_stride * sizeof(double)));
+    CK(cudaMallocHost(&ctx->coef_host, kCoefSlots * ctx->coef_stride * sizeof(double)));
+    for (auto& ev : ctx->coef_ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+#undef CK
+    s = alloc_local(ctx);
+    if (s != LX_OK) goto bad;
+    for (int r = 0; r < 2; r++) {
+        s = reset_record(ctx, r);
+        if (s != LX_OK) goto bad;
+    }
+    e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) { s = fail(LX_ERR_CUDA, "sync: %s", cudaGetErrorString(e)); goto bad; }
+    *out = ctx;
+    return LX_OK;
+bad:
+    free_ctx(ctx);
+    return s;
+}
+
+lx_status lx_ctx_destroy(lx_ctx* ctx) {
+    if (!ctx) return LX_OK;
+    cudaStreamSynchronize(ctx->stream);
+    free_ctx(ctx);
+    return LX_OK;
+}
+
+lx_status lx_nccl_unique_id(void* out128) {
+    if (!out128) return fail(LX_ERR_ARG, "NULL");
+    return comm_unique_id(out128) ? fail(LX_ERR_NCCL, "ncclGetUniqueId failed: %s", comm_error()) : LX_OK;
+}
+
+lx_status lx_ctx_set_comm(lx_ctx* ctx, const void* uid, int rank, int nranks) {
+    if (!ctx || !uid) return fail(LX_ERR_ARG, "NULL");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(LX_ERR_ARG, "bad rank/nranks");
+    int64_t b, e;
+    lx_slab_range(ctx->n[0], rank, nranks, &b, &e);
+    for (int r = 0; r < nranks; r++) {
+        int64_t bb, ee;
+        lx_slab_range(ctx->n[0], r, nranks, &bb, &ee);
+        if (ee - bb < 2) return fail(LX_ERR_DIM, "slab of rank %d has < 2 rows", r);
+    }
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->comm) { comm_destroy(ctx->comm); ctx->comm = nullptr; }
+    if (nranks > 1) {
+        Comm* c = nullptr;
+        if (comm_create(uid, rank, nranks, ctx->device, ctx->row, ctx->nsm * 8, &c))
+            return fail(LX_ERR_NCCL, "NCCL communicator: %s", comm_error());
+        ctx->comm = c;
+    }
+    ctx->i_begin = b;
+    ctx->i_end = e;
+    ctx->n_loc = (int)(e - b);
+    ctx->N_loc = (int64_t)ctx->n_loc * ctx->row;
+    LX_TRY(alloc_local(ctx));
+    if (ctx->comm) {
+        for (int i = 0; i < 2; i++) {
+            cudaFree(ctx->Yg[i]);
+            CUDA_TRY(cudaMalloc(&ctx->Yg[i], 3 * ctx->row * sizeof(double)));
+        }
+        cudaFree(ctx->vg);
+        CUDA_TRY(cudaMalloc(&ctx->vg, 3 * ctx->row * sizeof(double)));
+        comm_bind(ctx->comm, ctx->Y, ctx->Yg, ctx->vg, ctx->n_loc, rank, nranks);
+    }
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return LX_OK;
+}
+
+lx_status lx_ctx_local(const lx_ctx* ctx, int64_t* i_begin, int64_t* i_end, int64_t* n_local) {
+    if (!ctx) return fail(LX_ERR_ARG, "NULL");
+    if (i_begin) *i_begin = ctx->i_begin;
+    if (i_end) *i_end = ctx->i_end;
+    if (n_local) *n_local = ctx->N_loc;
+    return LX_OK;
+}
+
+lx_status lx_ctx_synchronize(lx_ctx* ctx, int* iters_total, double* err_last) {
+    if (!ctx) return fail(LX_ERR_ARG, "NULL");
+    Record r;
+    LX_TRY(read_record(ctx, 1, &r));
+    LX_TRY(reset_record(ctx, 1));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (iters_total) *iters_total = r.iters;
+    if (err_last) *err_last = r.err;
+    return status_of(r);
+}
+
+int64_t lx_ctx_launch_count(const lx_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// ---------------------------------------------------------------- Leja
+lx_status lx_real_leja_phi_vertical(lx_ctx* ctx, const lx_problem* pb, const double* u_lin, const double* v,
+                                    double* const* outs, const double* coeffs, int K, double dt, double c,
+                                    double gamma, int l, double rtol, double atol, int* iters_out) {
+    if (!ctx) return fail(LX_ERR_ARG, "ctx is NULL");
+    LX_TRY(check_problem(ctx, pb));
+    LX_TRY(validate_leja(pb, u_lin, v, outs, coeffs, K, dt, gamma, l));
+    if (pb->react == 0.0) u_lin = nullptr;
+    Staging sg(ctx);
+    const double *vd, *ud;
+    double* od[kMaxK];
+    LX_TRY(sg.in(v, &vd));
+    LX_TRY(sg.in(u_lin, &ud));
+    for (int k = 0; k < K; k++) LX_TRY(sg.out(outs[k], &od[k]));
+    const bool sync = iters_out != nullptr || sg.any_host;
+    const int rec = sync ? 0 : 1;
+    if (sync) LX_TRY(reset_record(ctx, 0));
+    LX_TRY(leja_device(ctx, pb, ud, vd, od, coeffs, K, dt, c, gamma, l, rtol, atol, rec));
+    LX_TRY(sg.finish());
+    if (!sync) return LX_OK;
+    Record r;
+    LX_TRY(read_record(ctx, 0, &r));
+    if (iters_out) *iters_out = r.iters;
+    return status_of(r);
+}
+
+lx_status lx_real_leja_phi(lx_ctx* ctx, const lx_problem* pb, const double* u_lin, const double* v, double* out,
+                           double dt, double c, double gamma, int l, double rtol, double atol, int* iters_out) {
+    const double one = 1.0;
+    double* outs[1] = {out};
+    return lx_real_leja_phi_vertical(ctx, pb, u_lin, v, outs, &one, 1, dt, c, gamma, l, rtol, atol, iters_out);
+}
+
+// ---------------------------------------------------------------- spectrum
+lx_status lx_spectrum_bound(lx_ctx* ctx, const lx_problem* pb, const double* u, double* lambda_abs_out) {
+    if (!ctx || !lambda_abs_out) return fail(LX_ERR_ARG, "NULL argument");
+    LX_TRY(check_problem(ctx, pb));
+    double b = 0.0;
+    for (int d = 0; d < pb->ndim; d++) {
+        const double h = pb->dx[d];
+        b += 4.0 * pb->diff / (h * h) + 4.0 * std::fabs(pb->nu) / (3.0 * h);
+    }
+    if (pb->react != 0.0) {
+        if (!u) return fail(LX_ERR_ARG, "u required when react != 0");
+        Staging sg(ctx);
+        const double* ud;
+        LX_TRY(sg.in(u, &ud));
+        CUDA_TRY(cudaMemsetAsync(&ctx->ctrl->umax, 0, sizeof(unsigned long long), ctx->stream));
+        StageArgs A;
+        std::memset(&A, 0, sizeof A);
+        A.n_loc = ctx->n_loc;
+        A.n1 = (int)ctx->n[1];
+        A.n2 = (int)ctx->n[2];
+        A.x0 = ud;
+        A.ctrl = ctx->ctrl;
+        A.grid = stage_grid_size(ctx->device);
+        CUDA_TRY(launch_stage(ST_MAXSQ, A, ctx->stream));
+        ctx->launches++;
+        if (ctx->comm) LX_TRY(comm_allreduce_max_u64(ctx->comm, &ctx->ctrl->umax, ctx->stream) ? fail(LX_ERR_NCCL, "allreduce max: %s", comm_error()) : LX_OK);
+        CUDA_TRY(cudaMemcpyAsync(ctx->umax_host, &ctx->ctrl->umax, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        double m2;
+        std::memcpy(&m2, ctx->umax_host, sizeof m2);
+        const double sft = 3.0 * m2 - 1.0;
+        if (sft > 0.0) b += pb->react * sft;
+    }
+    *lambda_abs_out = b;
+    return LX_OK;
+}
+
+lx_status lx_spectrum_estimate(lx_ctx* ctx, const lx_problem* pb, const double* u, int iters, double* lambda_abs_out) {
+    if (!ctx || !lambda_abs_out) return fail(LX_ERR_ARG, "NULL argument");
+    LX_TRY(check_problem(ctx, pb));
+    if (iters < 1 || iters > 100000) return fail(LX_ERR_ARG, "iters must be in [1, 100000]");
+    if (pb->react != 0.0 && !u) return fail(LX_ERR_ARG, "u required when react != 0");
+    Staging sg(ctx);
+    const double* ud = nullptr;
+    if (pb->react != 0.0) LX_TRY(sg.in(u, &ud));
+    LX_TRY(reset_record(ctx, 0));
+    CUDA_TRY(launch_fill_start(ctx->Y[0], ctx->N_loc, ctx->i_begin == 0, ctx->stream));
+    ctx->launches++;
+    LejaParams P = base_params(ctx, pb);
+    P.K = 0;
+    P.power_iters = iters;
+    P.max_nodes = iters + 1;
+    P.v = P.ysrc[0];
+    P.u = ud;
+    P.rec = ctx->rec_dev;
+    const bool diag = pb->react != 0.0;
+    if (ctx->comm) {
+        LX_TRY(comm_power(ctx->comm, P, diag, ctx->stream, &ctx->launches));
+    } else {
+        P.grid = leja_grid_size(ctx->device, 1, diag, ctx->ndim, P.nunits);
+        CUDA_TRY(launch_power_persistent(P, ctx->stream, diag));
+        ctx->launches++;
+    }
+    Record r;
+    LX_TRY(read_record(ctx, 0, &r));
+    *lambda_abs_out = r.est;
+    return status_of(r);
+}
+
+// ---------------------------------------------------------------- stages
+static StageArgs stage_args(lx_ctx* ctx, const lx_problem* pb, int rec) {
+    StageArgs A;
+    std::memset(&A, 0, sizeof A);
+    A.ndim = ctx->ndim;
+    A.n_loc = ctx->n_loc;
+    A.n1 = (int)ctx->n[1];
+    A.n2 = (int)ctx->n[2];
+    A.N_glob = ctx->N_glob;
+    A.st = make_stencil(pb);
+    A.partials = ctx->partials;
+    A.ctrl = ctx->ctrl;
+    A.rec = ctx->rec_dev + rec;
+    A.grid = stage_grid_size(ctx->device);
+    if (A.grid > ctx->max_grid) A.grid = ctx->max_grid;
+    return A;
+}
+
+static lx_status run_stage(lx_ctx* ctx, int op, const StageArgs& A) {
+    if (ctx->comm && (op == ST_FINAL4 || op == ST_FINAL_EXPRB32))
+        return comm_stage_norm(ctx->comm, op, A, ctx->stream, &ctx->launches) ? fail(LX_ERR_NCCL, "stage norm: %s", comm_error()) : LX_OK;
+    CUDA_TRY(launch_stage(op, A, ctx->stream));
+    ctx->launches++;
+    return LX_OK;
+}
+
+static lx_status rhs_device(lx_ctx* ctx, const lx_problem* pb, const double* u, double scale, double* f) {
+    LejaParams P = base_params(ctx, pb);
+    P.v = RowSrc{u, nullptr, ctx->row, ctx->n_loc, 0};
+    P.ydst[0] = f;
+    if (ctx->comm) return comm_rhs(ctx->comm, P, scale, ctx->stream, &ctx->launches) ? fail(LX_ERR_NCCL, "rhs halo: %s", comm_error()) : LX_OK;
+    P.grid = (P.nunits + kWarps - 1) / kWarps;
+    if (P.grid > ctx->nsm * 4) P.grid = ctx->nsm * 4;
+    CUDA_TRY(launch_rhs(P, scale, ctx->stream));
+    ctx->launches++;
+    return LX_OK;
+}
+
+lx_status lx_rhs(lx_ctx* ctx, const lx_problem* pb, const double* u, double scale, double* f_out) {
+    if (!ctx || !u || !f_out) return fail(LX_ERR_ARG, "NULL argument");
+    LX_TRY(check_problem(ctx, pb));
+    if (u == f_out) return fail(LX_ERR_ALIAS, "f_out must not alias u");
+    Staging sg(ctx);
+    const double* ud;
+    double* fd;
+    LX_TRY(sg.in(u, &ud));
+    LX_TRY(sg.out(f_out, &fd));
+    LX_TRY(rhs_device(ctx, pb, ud, scale, fd));
+    LX_TRY(sg.finish());
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return LX_OK;
+}
+
+static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb, const double* u, double* lo,
+                             double* hi, double dt, double c, double gamma, double rtol, double atol, int rec) {
+    const bool diag = pb->react != 0.0;
+    const double* ul = diag ? u : nullptr;
+    double* S0 = scratch(ctx, 0);
+    if (!S0) return fail(LX_ERR_CUDA, "scratch allocation failed");
+    const double one = 1.0;
+    // f_u = RHS(u) * dt   (alg:Ros_Eu P:468-469)
+    LX_TRY(rhs_device(ctx, pb, u, dt, S0));
+    StageArgs A = stage_args(ctx, pb, rec);
+    A.dt = dt;
+    A.u = u;
+    if (method == LX_ROSENBROCK_EULER) {
+        double* o[1] = {hi};
+        LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 1, rtol, atol, rec));
+        A.x0 = u; A.x1 = hi; A.y0 = hi; A.a0 = 1.0; A.a1 = 1.0;  // u_exprb2 = u + phi_1(J dt) f dt
+        LX_TRY(run_stage(ctx, ST_AXPBY, A));
+        if (lo && lo != hi) CUDA_TRY(cudaMemcpyAsync(lo, hi, ctx->N_loc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+        return LX_OK;
+    }
+    if (method == LX_EXPRB32) {
+        // P:414-418, alg:exprb32: u_flux (in hi) -> a (lo), R_a (S0) -> u_nl_3 (hi) -> u_3 = a + 2 u_nl_3
+        double* o[1] = {hi};
+        LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 1, rtol, atol, rec));
+        A.x0 = u; A.x1 = hi; A.y1 = lo; A.y0 = S0;
+        LX_TRY(run_stage(ctx, ST_EXPRB32_A, A));
+        LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 3, rtol, atol, rec));
+        A = stage_args(ctx, pb, rec);
+        A.x0 = lo; A.x1 = hi; A.y0 = hi;
+        return run_stage(ctx, ST_FINAL_EXPRB32, A);
+    }
+    // EXPRB43 / EPIRK4s3A (reading R17)
+    const bool epirk = method == LX_EPIRK4S3A;
+    double* S1 = scratch(ctx, 1);
+    double* S2 = scratch(ctx, 2);
+    double* S3 = epirk ? scratch(ctx, 3) : nullptr;
+    if (!S1 || !S2 || (epirk && !S3)) return fail(LX_ERR_CUDA, "scratch allocation failed");
+    const double cf2[2] = {0.5, 1.0}, cf3[3] = {0.5, 2.0 / 3.0, 1.0};
+    double* pv[3] = {S1, S2, S3};
+    LX_TRY(leja_device(ctx, pb, ul, S0, pv, epirk ? cf3 : cf2, epirk ? 3 : 2, dt, c, gamma, 1, rtol, atol, rec));
+    double* p_one = epirk ? S3 : S2;
+    // D_a = dt F(u + 1/2 p_half) - dt F(u)  -> S0
+    A.x0 = u; A.x1 = S1; A.x2 = nullptr; A.a0 = 0.5; A.a1 = 0.0; A.y0 = S0;
+    LX_TRY(run_stage(ctx, ST_STAGE_REMAINDER, A));
+    double* Db;
+    if (epirk) {
+        // D_b = dt F(u + 2/3 p_23) - dt F(u) -> S1
+        A.x0 = u; A.x1 = S2; A.x2 = nullptr; A.a0 = 2.0 / 3.0; A.a1 = 0.0; A.y0 = S1;
+        LX_TRY(run_stage(ctx, ST_STAGE_REMAINDER, A));
+        Db = S1;
+    } else {
+        // phi_1(hJ) D_a -> S1 ; b = u + p_one + S1 ; D_b -> lo
+        double* o[1] = {S1};
+        LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 1, rtol, atol, rec));
+        A.x0 = u; A.x1 = p_one; A.x2 = S1; A.a0 = 1.0; A.a1 = 1.0; A.y0 = lo;
+        LX_TRY(run_stage(ctx, ST_STAGE_REMAINDER, A));
+        Db = lo;
+    }
+    // w3 = a3 D_a + b3 D_b, w4 = a4 D_a + b4 D_b
+    double* w3 = epirk ? S2 : S1;
+    A = stage_args(ctx, pb, rec);
+    A.x0 = S0; A.x1 = Db; A.y0 = w3; A.y1 = hi;
+    A.a0 = epirk ? 32.0 : 16.0; A.a1 = epirk ? -13.5 : -2.0;
+    A.a2 = epirk ? -144.0 : -48.0; A.a3 = epirk ? 81.0 : 12.0;
+    LX_TRY(run_stage(ctx, ST_COMBINE2, A));
+    // q3 -> S0 (D_a consumed); q4 -> S1 (EPIRK: D_b consumed) / lo (EXPRB43: D_b consumed)
+    double* q3 = S0;
+    double* q4 = epirk ? S1 : lo;
+    double* o3[1] = {q3};
+    LX_TRY(leja_device(ctx, pb, ul, w3, o3, &one, 1, dt, c, gamma, 3, rtol, atol, rec));
+    double* o4[1] = {q4};
+    LX_TRY(leja_device(ctx, pb, ul, hi, o4, &one, 1, dt, c, gamma, 4, rtol, atol, rec));
+    // u3 = u + p_one + q3 -> lo ; u4 = u3 + q4 -> hi ; err = ||u4 - u3||
+    A = stage_args(ctx, pb, rec);
+    A.x0 = u; A.x1 = p_one; A.x2 = q3; A.x3 = q4; A.y0 = lo; A.y1 = hi;
+    return run_stage(ctx, ST_FINAL4, A);
+}
+
+lx_status lx_step(lx_ctx* ctx, lx_method method, const lx_problem* pb, const double* u, double* u_low, double* u_high,
+                  double* err_out, double dt, double c, double gamma, double rtol, double atol, int* iters_out) {
+    if (!ctx) return fail(LX_ERR_ARG, "ctx is NULL");
+    LX_TRY(check_problem(ctx, pb));
+    if ((int)method < 0 || (int)method > 3) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
+    if (!u || !u_high) return fail(LX_ERR_ARG, "NULL argument");
+    if (method != LX_ROSENBROCK_EULER && !u_low) return fail(LX_ERR_ARG, "u_low required for embedded methods");
+    if (u_low == u || u_high == u) return fail(LX_ERR_ALIAS, "outputs must not alias u");
+    if (u_low && u_low == u_high) return fail(LX_ERR_ALIAS, "u_low must differ from u_high");
+    if (!(gamma > 0.0) && dt != 0.0) return fail(LX_ERR_ARG, "gamma must be > 0");
+    Staging sg(ctx);
+    const double* ud;
+    double *lo = nullptr, *hi;
+    LX_TRY(sg.in(u, &ud));
+    LX_TRY(sg.out(u_high, &hi));
+    if (u_low) LX_TRY(sg.out(u_low, &lo));
+    const bool sync = iters_out || err_out || sg.any_host;
+    const int rec = sync ? 0 : 1;
+    if (sync) LX_TRY(reset_record(ctx, 0));
+    LX_TRY(step_device(ctx, method, pb, ud, lo, hi, dt, c, gamma, rtol, atol, rec));
+    LX_TRY(sg.finish());
+    if (!sync) return LX_OK;
+    Record r;
+    LX_TRY(read_record(ctx, 0, &r));
+    if (iters_out) *iters_out = r.iters;
+    if (err_out) *err_out = (method == LX_ROSENBROCK_EULER) ? 0.0 : r.err;
+    return status_of(r);
+}
+
+lx_status lx_step_rosenbrock_euler(lx_ctx* ctx, const lx_problem* pb, const double* u, double* u_out, double dt,
+                                   double c, double gamma, double rtol, double atol, int* iters_out) {
+    return lx_step(ctx, LX_ROSENBROCK_EULER, pb, u, nullptr, u_out, nullptr, dt, c, gamma, rtol, atol, iters_out);
+}
+lx_status lx_step_exprb32(lx_ctx* ctx, const lx_problem* pb, const double* u, double* u_low, double* u_high,
+                          double* err_out, double dt, double c, double gamma, double rtol, double atol, int* iters_out) {
+    return lx_step(ctx, LX_EXPRB32, pb, u, u_low, u_high, err_out, dt, c, gamma, rtol, atol, iters_out);
+}
+lx_status lx_step_exprb43(lx_ctx* ctx, const lx_problem* pb, const double* u, double* u_low, double* u_high,
+                          double* err_out, double dt, double c, double gamma, double rtol, double atol, int* iters_out) {
+    return lx_step(ctx, LX_EXPRB43, pb, u, u_low, u_high, err_out, dt, c, gamma, rtol, atol, iters_out);
+}
+lx_status lx_step_epirk4s3a(lx_ctx* ctx, const lx_problem* pb, const double* u, double* u_low, double* u_high,
+                            double* err_out, double dt, double c, double gamma, double rtol, double atol,
+                            int* iters_out) {
+    return lx_step(ctx, LX_EPIRK4S3A, pb, u, u_low, u_high, err_out, dt, c, gamma, rtol, atol, iters_out);
+}
+
+}  // extern "C"

@@ -1,0 +1,129 @@
+// lx_internal.h -- structures shared by the host runtime and the sm_100a kernels.
+// Not part of the public ABI (include/lexint.h is).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lx {
+
+constexpr int kThreads = 256;     // threads per CTA (8 warps)
+constexpr int kWarps = kThreads / 32;
+constexpr int kRT = 4;            // rows (2D) / planes (3D) per warp work unit
+constexpr int kMaxK = 4;          // vertical accumulators
+constexpr int kSlot = 8;          // doubles per CTA partial slot (1 + K <= 5)
+
+// Per-call record, written on the device, read by the host once per call/step.
+struct Record {
+    int iters;            // total Leja iterations accumulated by this record
+    int status;           // first non-OK status (lx_status numbering)
+    int iters_k[kMaxK];   // iteration at which accumulator k converged (last Leja call)
+    int ncalls;           // number of Leja calls accumulated
+    int pad;
+    double margin_accept; // min thr/err at acceptance (inf if err == 0)
+    double margin_reject; // min err/thr over rejected checks
+    double err;           // embedded error estimate (steps)
+    double est;           // spectrum estimate / bound
+};
+
+// Device control block of a persistent kernel (grid barrier + decision).
+struct Ctrl {
+    unsigned int arrive;  // barrier arrivals (reset by the last arriver)
+    unsigned int gen;     // barrier generation (monotone, release flag)
+    int done;             // decision: stop after this iteration
+    int active;           // decision: bit k = accumulator k still accumulating
+    int status;           // decision: status so far
+    int m;                // last decided iteration
+    int pad0, pad1;
+    double scale;         // power iteration: 1/||w_m|| for the next application
+    double est;           // power iteration: latest estimate
+    unsigned int ticket;  // last-block ticket for non-persistent reductions
+    unsigned int pad2;
+    unsigned long long umax;  // max reduction (bit pattern of a non-negative double)
+};
+
+// Rows of a slab: rows [0, n_loc) at base, row r in {-1, n_loc, n_loc+1}
+// either from `ghost` (3 rows: -1, n_loc, n_loc+1) or by periodic wrap.
+struct RowSrc {
+    const double* base;
+    const double* ghost;
+    long long stride;     // doubles per row (n1 in 2D, n1*n2 in 3D)
+    int n_loc;
+    int pad;
+};
+
+// Constant-coefficient stencil of A (diff*lap + nu*sum_d D_d) per dimension:
+// offsets -1, 0, +1, +2 (third-order upwind +x-biased).
+struct Stencil {
+    double c0;            // centre (summed over dimensions)
+    double m1[3], p1[3], p2[3];
+    double qa, qb;        // diagonal of J: qa + qb * u^2   (react*(1 - 3u^2))
+    double react;         // g(u) = react*(u - u^3)
+};
+
+struct LejaParams {
+    int ndim;
+    int n_loc;            // local rows (dim 0)
+    int n1, n2;           // dims 1, 2 (n2 = 1 in 2D)
+    int nb;               // column bands of 64 along the contiguous dimension
+    int nrow;             // rows of the CTA-tile index (2D: n_loc row blocks; 3D: n1 rows)
+    int nrb;              // row blocks of kRT along dim 0
+    int nunits;           // warp work units per iteration
+    int K;
+    int max_nodes;
+    int active0;          // initial active mask
+    int power_iters;      // POWER mode: number of applications
+    double N_glob;
+    double alpha;         // 1/gamma
+    double rtol, atol;
+    Stencil st;
+    const double* coef;   // [max_nodes][1+K]: beta_m, d_m^(k)
+    RowSrc v;             // input vector (iteration 1)
+    RowSrc ysrc[2];       // y ping-pong read views
+    double* ydst[2];      // y ping-pong write pointers (== ysrc[i].base)
+    double* p[kMaxK];
+    const double* u;      // linearisation state (diag), unpadded local
+    double* partials;     // [2][grid][kSlot]
+    Ctrl* ctrl;
+    Record* rec;
+    int grid;
+    int timeout_spins;
+};
+
+// launchers (lx_kernels.cu)
+cudaError_t launch_leja_persistent(const LejaParams& P, cudaStream_t s, bool diag);
+cudaError_t launch_power_persistent(const LejaParams& P, cudaStream_t s, bool diag);
+int leja_grid_size(int device, int K, bool diag, int ndim, int nunits);
+
+struct StageArgs {
+    int ndim, n_loc, n1, n2, nb, nrb, nunits;
+    double N_glob;
+    Stencil st;
+    RowSrc src;           // stencil input
+    const double* u;      // state
+    const double* x0; const double* x1; const double* x2; const double* x3;
+    double* y0; double* y1;
+    double a0, a1, a2, a3;
+    double dt;
+    double* partials;     // [grid][kSlot]
+    Ctrl* ctrl;
+    Record* rec;
+    int grid;
+};
+
+enum StageOp {
+    ST_RHS_SCALED = 0,    // y0 = a0 * f(src)                       (stencil)
+    ST_AXPBY = 1,         // y0 = a0*x0 + a1*x1
+    ST_REMAINDER_DIFF,    // y0 = dt*F(x0) - dt*F(u)   F(x)=g(x)-g'(u)x      (R18)
+    ST_STAGE_REMAINDER,   // s = x0 + a0*x1 + a1*x2 ; y0 = dt*F(s) - dt*F(u)  (s not stored)
+    ST_EXPRB32_A,         // y1 = x0 + x1 (a) ; y0 = dt*F(a) - dt*F(u)
+    ST_COMBINE2,          // y0 = a0*x0 + a1*x1 ; y1 = a2*x0 + a3*x1
+    ST_FINAL4,            // y0 = x0 + x1 + x2 (u3) ; y1 = y0 + x3 (u4) ; err = ||y1 - y0||
+    ST_FINAL_EXPRB32,     // y0 = x0 + 2 x1 ; err = ||2 x1||
+    ST_MAXSQ,             // ctrl->umax = max x0^2
+};
+cudaError_t launch_stage(int op, const StageArgs& A, cudaStream_t s);
+cudaError_t launch_rhs(const LejaParams& P, double scale, cudaStream_t s);
+cudaError_t launch_fill_start(double* v, long long n, bool add_e0, cudaStream_t s);
+int stage_grid_size(int device);
+
+}  // namespace lx

@@ -1,0 +1,586 @@
+// lx_kernels.cu -- sm_100a fp64 kernels of the LeXInt hot path (arxiv 2310.08344).
+//
+// k_leja2d : ONE persistent cooperative kernel per Leja call.  Each iteration m
+//            is one fused HBM pass over the grid (Eq. (2)):
+//               y_m  = alpha*(A y_{m-1}) + beta_m*y_{m-1}     (alpha = 1/gamma,
+//                                                              beta_m = -c/gamma - xi_{m-1})
+//               p_m^(k) = p_{m-1}^(k) + d_m^(k) y_m            (k < K, active only)
+//               S_y = sum y_m^2,  S_p^(k) = sum (p_m^(k))^2    (partials per CTA)
+//            then a grid barrier whose last arriver sums the CTA partials in a
+//            fixed order and takes the stopping decision of P:155
+//               |d_m| sqrt(S_y/N) <= rtol sqrt(S_p/N) + atol
+//            on the device.  No host round trip per iteration.
+// k_power2d: power iteration with the same machinery.
+// k_stage  : fused stencil / pointwise stage kernels of the integrators
+//             with deterministic last-block norm reductions.
+//
+// Work decomposition: a warp owns a unit = 64 contiguous columns (one double2
+// per lane) x kRT rows; it loads rows i0-1 .. i0+kRT+1 of y (the +x-biased
+// upwind stencil reaches i-1, i+1, i+2), takes column neighbours from warp
+// shuffles (+2 edge-lane halo loads), and streams p.  Adjacent warps of a CTA
+// own adjacent column bands of the same rows, so halo re-reads hit L1/L2.
+#include "lx_internal.h"
+
+#include <cstdio>
+
+namespace lx {
+
+#define FULL_MASK 0xffffffffu
+
+__device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+__device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ const double* rowp(const RowSrc& s, int r) {
+    if ((unsigned)r < (unsigned)s.n_loc) return s.base + (long long)r * s.stride;
+    if (s.ghost) return s.ghost + (long long)(r < 0 ? 0 : r - s.n_loc + 1) * s.stride;
+    return s.base + (long long)(r < 0 ? r + s.n_loc : r - s.n_loc) * s.stride;
+}
+
+// Deterministic block reduction of n values: xor-butterfly inside warps, then
+// warps summed in index order by thread 0.  Result valid in thread 0.
+template <int N>
+__device__ __forceinline__ void block_reduce(double (&v)[N], double (*s_red)[kSlot]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 0; i < N; i++) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v[i] += __shfl_xor_sync(FULL_MASK, v[i], off);
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < N; i++) s_red[warp][i] = v[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < N; i++) {
+            double s = s_red[0][i];
+            for (int w = 1; w < kWarps; w++) s += s_red[w][i];
+            v[i] = s;
+        }
+    }
+    __syncthreads();
+}
+
+enum TileMode { M_LEJA = 0, M_POWER = 1, M_RHS = 2 };
+
+// One warp work unit of the 2D stencil (64 columns x kRT rows).
+template <int K, bool DIAG, bool FIRST, int MODE, bool RO>
+__device__ __forceinline__ void tile2d(const LejaParams& P, const RowSrc& src, double* __restrict__ dst,
+                                       int unit, int lane, double beta, const double* d0, const double* dm,
+                                       int active, double scale, double& sy, double* sp) {
+    const int b = unit % P.nb;
+    const int rb = unit / P.nb;
+    const int n1 = P.n1;
+    const int j0 = b * 64 + 2 * lane;
+    const bool valid = j0 < n1;
+    const int last = min(31, ((n1 - b * 64) >> 1) - 1);
+    const int i0 = rb * kRT;
+    const int nout = min(kRT, P.n_loc - i0);
+    const Stencil& S = P.st;
+
+    double2 w[kRT + 3];
+#pragma unroll
+    for (int t = 0; t < kRT + 3; t++) {
+        w[t] = make_double2(0.0, 0.0);
+        if (valid && t < nout + 3) {
+            const double* rp = rowp(src, i0 - 1 + t) + j0;
+            w[t] = RO ? ldg2(rp) : ld2(rp);
+        }
+    }
+    double hl[kRT];
+    double2 hr[kRT];
+#pragma unroll
+    for (int t = 0; t < kRT; t++) {
+        hl[t] = 0.0;
+        hr[t] = make_double2(0.0, 0.0);
+        if (t < nout) {
+            const double* rp = rowp(src, i0 + t);
+            if (lane == 0) {
+                const int jl = (j0 == 0) ? n1 - 1 : j0 - 1;
+                hl[t] = RO ? __ldg(rp + jl) : rp[jl];
+            }
+            if (lane == last) {
+                int jr = j0 + 2;
+                if (jr >= n1) jr -= n1;
+                hr[t] = RO ? ldg2(rp + jr) : ld2(rp + jr);
+            }
+        }
+    }
+    constexpr int KK = K > 0 ? K : 1;
+    double2 pv[kRT][KK];
+    double2 uu[kRT];
+#pragma unroll
+    for (int t = 0; t < kRT; t++) {
+        const long long off = (long long)(i0 + t) * n1 + j0;
+        if (MODE == M_LEJA && !FIRST) {
+#pragma unroll
+            for (int k = 0; k < KK; k++) {
+                pv[t][k] = make_double2(0.0, 0.0);
+                if (valid && t < nout && ((active >> k) & 1)) pv[t][k] = ld2(P.p[k] + off);
+            }
+        }
+        uu[t] = make_double2(0.0, 0.0);
+        if (DIAG && valid && t < nout) uu[t] = ldg2(P.u + off);
+    }
+
+#pragma unroll
+    for (int t = 0; t < kRT; t++) {
+        if (t < nout) {  // uniform across the warp
+            const double2 yc = w[t + 1], up = w[t], dn1 = w[t + 2], dn2 = w[t + 3];
+            double left = __shfl_up_sync(FULL_MASK, yc.y, 1);
+            double r1 = __shfl_down_sync(FULL_MASK, yc.x, 1);
+            double r2 = __shfl_down_sync(FULL_MASK, yc.y, 1);
+            if (lane == 0) left = hl[t];
+            if (lane == last) {
+                r1 = hr[t].x;
+                r2 = hr[t].y;
+            }
+            // A y at (i, j0) and (i, j0+1): fixed summation order
+            double ax = S.c0 * yc.x;
+            ax = fma(S.m1[0], up.x, ax);
+            ax = fma(S.p1[0], dn1.x, ax);
+            ax = fma(S.p2[0], dn2.x, ax);
+            ax = fma(S.m1[1], left, ax);
+            ax = fma(S.p1[1], yc.y, ax);
+            ax = fma(S.p2[1], r1, ax);
+            double ay = S.c0 * yc.y;
+            ay = fma(S.m1[0], up.y, ay);
+            ay = fma(S.p1[0], dn1.y, ay);
+            ay = fma(S.p2[0], dn2.y, ay);
+            ay = fma(S.m1[1], yc.x, ay);
+            ay = fma(S.p1[1], r1, ay);
+            ay = fma(S.p2[1], r2, ay);
+            if (DIAG) {
+                ax = fma(fma(S.qb, uu[t].x * uu[t].x, S.qa), yc.x, ax);
+                ay = fma(fma(S.qb, uu[t].y * uu[t].y, S.qa), yc.y, ay);
+            }
+            double2 yn;
+            if (MODE == M_POWER) {
+                yn.x = scale * ax;
+                yn.y = scale * ay;
+            } else if (MODE == M_RHS) {
+                // f(u)*scale = scale*(A u + react*(u - u^3))
+                yn.x = scale * fma(S.react, yc.x - yc.x * yc.x * yc.x, ax);
+                yn.y = scale * fma(S.react, yc.y - yc.y * yc.y * yc.y, ay);
+            } else {
+                yn.x = fma(P.alpha, ax, beta * yc.x);
+                yn.y = fma(P.alpha, ay, beta * yc.y);
+            }
+            if (valid) {
+                const long long off = (long long)(i0 + t) * n1 + j0;
+                st2(dst + off, yn);
+                sy = fma(yn.x, yn.x, sy);
+                sy = fma(yn.y, yn.y, sy);
+                if (MODE == M_LEJA) {
+#pragma unroll
+                    for (int k = 0; k < KK; k++) {
+                        if ((active >> k) & 1) {
+                            double2 pn;
+                            if (FIRST) {
+                                pn.x = fma(dm[k], yn.x, d0[k] * yc.x);
+                                pn.y = fma(dm[k], yn.y, d0[k] * yc.y);
+                            } else {
+                                pn.x = fma(dm[k], yn.x, pv[t][k].x);
+                                pn.y = fma(dm[k], yn.y, pv[t][k].y);
+                            }
+                            st2(P.p[k] + off, pn);
+                            sp[k] = fma(pn.x, pn.x, sp[k]);
+                            sp[k] = fma(pn.y, pn.y, sp[k]);
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Grid barrier with the convergence decision taken by the last arriver.
+// Returns (in smem) done / active for the next iteration.
+// ---------------------------------------------------------------------------
+template <int K, int MODE>
+__device__ __forceinline__ void barrier_decide(const LejaParams& P, int m, unsigned gen0, const double* dm,
+                                               int active, double (*s_red)[kSlot], int* s_flags) {
+    constexpr int NV = (MODE == M_LEJA) ? 1 + K : 1;
+    const int tid = threadIdx.x;
+    Ctrl* ctrl = P.ctrl;
+    const int par = m & 1;
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        const unsigned t = atomicAdd(&ctrl->arrive, 1u);
+        s_flags[0] = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (s_flags[0]) {
+        __threadfence();
+        double acc[NV];
+#pragma unroll
+        for (int i = 0; i < NV; i++) acc[i] = 0.0;
+        for (int c = tid; c < (int)gridDim.x; c += kThreads) {
+            const double* slot = P.partials + ((size_t)par * gridDim.x + c) * kSlot;
+#pragma unroll
+            for (int i = 0; i < NV; i++) acc[i] += __ldcg(slot + i);
+        }
+        block_reduce<NV>(acc, s_red);
+        if (tid == 0) {
+            Record* rec = P.rec;
+            int done = 0, status = 0, act = active;
+            const double N = P.N_glob;
+            if (MODE == M_LEJA) {
+                const double ny = sqrt(acc[0] / N);
+                int nact = 0;
+                for (int k = 0; k < K; k++) {
+                    if (!((act >> k) & 1)) continue;
+                    const double err = fabs(dm[k]) * ny;
+                    const double thr = P.rtol * sqrt(acc[1 + k] / N) + P.atol;
+                    if (!isfinite(err) || !isfinite(thr)) {
+                        status = 6;  // LX_ERR_NONFINITE
+                        break;
+                    }
+                    if (err <= thr) {
+                        act &= ~(1 << k);
+                        rec->iters_k[k] = m;
+                        const double r = err > 0.0 ? thr / err : INFINITY;
+                        if (r < rec->margin_accept) rec->margin_accept = r;
+                    } else {
+                        nact++;
+                        const double r = err / thr;
+                        if (r < rec->margin_reject) rec->margin_reject = r;
+                    }
+                }
+                if (status) done = 1;
+                else if (nact == 0) done = 1;
+                else if (m >= P.max_nodes - 1) { done = 1; status = 5; }  // LX_ERR_NOCONV
+            } else {  // M_POWER
+                const double nw = sqrt(acc[0] / N);
+                const double nv = (m == 1) ? sqrt((N + 3.0) / N) : 1.0;
+                ctrl->est = nw / nv;
+                ctrl->scale = 1.0 / nw;
+                if (!isfinite(nw) || nw == 0.0) { done = 1; status = 6; }
+                if (m >= P.power_iters) done = 1;
+                if (done) rec->est = ctrl->est;
+            }
+            if (done) {
+                rec->iters += m;
+                rec->ncalls += 1;
+                if (rec->status == 0) rec->status = status;
+            }
+            ctrl->done = done;
+            ctrl->active = act;
+            ctrl->status = status;
+            ctrl->m = m;
+            ctrl->arrive = 0u;
+            __threadfence();
+            st_release(&ctrl->gen, gen0 + (unsigned)m);
+        }
+    } else if (tid == 0) {
+        int spins = 0;
+        while ((int)(ld_acquire(&ctrl->gen) - gen0) < m) {
+            if (++spins > 64) __nanosleep(64);
+            if (spins > P.timeout_spins) {
+                ctrl->done = 1;
+                ctrl->status = 10;  // LX_ERR_TIMEOUT
+                atomicExch(&P.rec->status, 10);
+                break;
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        s_flags[1] = *(volatile int*)&ctrl->done;
+        s_flags[2] = *(volatile int*)&ctrl->active;
+        s_flags[3] = 0;
+        if (MODE == M_POWER) {
+            volatile double* sc = &ctrl->scale;
+            s_red[0][kSlot - 1] = *sc;
+        }
+    }
+    __syncthreads();
+}
+
+template <int K, bool DIAG>
+__global__ void __launch_bounds__(kThreads) k_leja2d(const __grid_constant__ LejaParams P) {
+    __shared__ double s_red[kWarps][kSlot];
+    __shared__ int s_flags[4];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned gen0 = 0;
+    if (tid == 0) gen0 = ld_acquire(&P.ctrl->gen);
+    int active = P.active0;
+    double d0[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) d0[k] = P.coef[1 + k];
+    for (int m = 1; m < P.max_nodes; m++) {
+        const double* cm = P.coef + (size_t)m * (1 + K);
+        const double beta = cm[0];
+        double dm[K], sp[K];
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            dm[k] = cm[1 + k];
+            sp[k] = 0.0;
+        }
+        double sy = 0.0;
+        const int par = m & 1;
+        double* dst = P.ydst[par];
+        if (m == 1) {
+            for (int unit = blockIdx.x * kWarps + warp; unit < P.nunits; unit += gridDim.x * kWarps)
+                tile2d<K, DIAG, true, M_LEJA, true>(P, P.v, dst, unit, lane, beta, d0, dm, active, 0.0, sy, sp);
+        } else {
+            const RowSrc src = P.ysrc[par ^ 1];
+            for (int unit = blockIdx.x * kWarps + warp; unit < P.nunits; unit += gridDim.x * kWarps)
+                tile2d<K, DIAG, false, M_LEJA, false>(P, src, dst, unit, lane, beta, d0, dm, active, 0.0, sy, sp);
+        }
+        double vals[1 + K];
+        vals[0] = sy;
+#pragma unroll
+        for (int k = 0; k < K; k++) vals[1 + k] = sp[k];
+        block_reduce<1 + K>(vals, s_red);
+        if (tid == 0) {
+            double* slot = P.partials + ((size_t)par * gridDim.x + blockIdx.x) * kSlot;
+#pragma unroll
+            for (int i = 0; i < 1 + K; i++) slot[i] = vals[i];
+        }
+        barrier_decide<K, M_LEJA>(P, m, gen0, dm, active, s_red, s_flags);
+        active = s_flags[2];
+        if (s_flags[1]) break;
+    }
+}
+
+template <bool DIAG>
+__global__ void __launch_bounds__(kThreads) k_power2d(const __grid_constant__ LejaParams P) {
+    __shared__ double s_red[kWarps][kSlot];
+    __shared__ int s_flags[4];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned gen0 = 0;
+    if (tid == 0) gen0 = ld_acquire(&P.ctrl->gen);
+    double scale = 1.0;
+    for (int m = 1; m <= P.power_iters; m++) {
+        double sy = 0.0, sp[1] = {0.0};
+        const int par = m & 1;
+        double* dst = P.ydst[par];
+        const RowSrc src = (m == 1) ? P.v : P.ysrc[par ^ 1];
+        for (int unit = blockIdx.x * kWarps + warp; unit < P.nunits; unit += gridDim.x * kWarps)
+            tile2d<0, DIAG, false, M_POWER, false>(P, src, dst, unit, lane, 0.0, nullptr, nullptr, 0, scale, sy, sp);
+        double vals[1] = {sy};
+        block_reduce<1>(vals, s_red);
+        if (tid == 0) P.partials[((size_t)par * gridDim.x + blockIdx.x) * kSlot] = vals[0];
+        barrier_decide<0, M_POWER>(P, m, gen0, nullptr, 0, s_red, s_flags);
+        scale = s_red[0][kSlot - 1];
+        if (s_flags[1]) break;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Launchers
+// ---------------------------------------------------------------------------
+template <typename Kern>
+static int max_coresident(int device, Kern kern) {
+    int nsm = 0, per = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, 0);
+    return nsm * per;
+}
+
+static void* leja_kernel_ptr(int K, bool diag) {
+    switch (K * 2 + (diag ? 1 : 0)) {
+        case 2: return (void*)k_leja2d<1, false>;
+        case 3: return (void*)k_leja2d<1, true>;
+        case 4: return (void*)k_leja2d<2, false>;
+        case 5: return (void*)k_leja2d<2, true>;
+        case 6: return (void*)k_leja2d<3, false>;
+        case 7: return (void*)k_leja2d<3, true>;
+        case 8: return (void*)k_leja2d<4, false>;
+        case 9: return (void*)k_leja2d<4, true>;
+    }
+    return nullptr;
+}
+
+int leja_grid_size(int device, int K, bool diag, int ndim, int nunits) {
+    (void)ndim;
+    void* kern = leja_kernel_ptr(K, diag);
+    int nsm = 0, per = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, 0);
+    if (per < 1) per = 1;
+    long long g = (long long)nsm * per;
+    // never more CTAs than work: at least 2 units per warp for tiny grids
+    long long need = (nunits + kWarps - 1) / kWarps;
+    if (g > need) g = need > 0 ? need : 1;
+    return (int)g;
+}
+
+cudaError_t launch_leja_persistent(const LejaParams& P, cudaStream_t s, bool diag) {
+    void* kern = leja_kernel_ptr(P.K, diag);
+    if (!kern) return cudaErrorInvalidValue;
+    void* args[] = {(void*)&P};
+    return cudaLaunchCooperativeKernel(kern, dim3(P.grid), dim3(kThreads), args, 0, s);
+}
+
+cudaError_t launch_power_persistent(const LejaParams& P, cudaStream_t s, bool diag) {
+    void* kern = diag ? (void*)k_power2d<true> : (void*)k_power2d<false>;
+    void* args[] = {(void*)&P};
+    return cudaLaunchCooperativeKernel(kern, dim3(P.grid), dim3(kThreads), args, 0, s);
+}
+
+// ---------------------------------------------------------------------------
+// Stage kernels
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double nl_rem(double react, double x, double u) {
+    // F(x) = g(x) - g'(u) x,  g(x) = react (x - x^3)    (reading R18)
+    const double g = react * (x - x * x * x);
+    const double gp = react * (1.0 - 3.0 * u * u);
+    return g - gp * x;
+}
+
+// Deterministic last-block reduction of one value into rec->err = sqrt(S/N).
+__device__ __forceinline__ void stage_reduce_err(const StageArgs& A, double v, double (*s_red)[kSlot],
+                                                 int* s_last) {
+    double vals[1] = {v};
+    block_reduce<1>(vals, s_red);
+    if (threadIdx.x == 0) {
+        A.partials[blockIdx.x * kSlot] = vals[0];
+        __threadfence();
+        const unsigned t = atomicAdd(&A.ctrl->ticket, 1u);
+        *s_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (*s_last) {
+        __threadfence();
+        double acc[1] = {0.0};
+        for (int c = threadIdx.x; c < (int)gridDim.x; c += kThreads) acc[0] += __ldcg(A.partials + c * kSlot);
+        block_reduce<1>(acc, s_red);
+        if (threadIdx.x == 0) {
+            A.rec->err = sqrt(acc[0] / A.N_glob);
+            A.ctrl->ticket = 0u;
+        }
+    }
+}
+
+template <int OP>
+__global__ void __launch_bounds__(kThreads) k_stage_pointwise(const __grid_constant__ StageArgs A) {
+    __shared__ double s_red[kWarps][kSlot];
+    __shared__ int s_last;
+    const long long npair = (long long)A.n_loc * A.n1 * A.n2 / 2;
+    const long long stride = (long long)gridDim.x * kThreads;
+    double acc = 0.0;
+    unsigned long long umax = 0ull;
+    const double dt = A.dt, react = A.st.react;
+    for (long long i = (long long)blockIdx.x * kThreads + threadIdx.x; i < npair; i += stride) {
+        const long long o = 2 * i;
+        if (OP == ST_AXPBY) {
+            const double2 x = ld2(A.x0 + o), y = ld2(A.x1 + o);
+            st2(A.y0 + o, make_double2(A.a0 * x.x + A.a1 * y.x, A.a0 * x.y + A.a1 * y.y));
+        } else if (OP == ST_REMAINDER_DIFF) {
+            const double2 x = ld2(A.x0 + o), u = ld2(A.u + o);
+            st2(A.y0 + o, make_double2(dt * nl_rem(react, x.x, u.x) + (-dt) * nl_rem(react, u.x, u.x),
+                                       dt * nl_rem(react, x.y, u.y) + (-dt) * nl_rem(react, u.y, u.y)));
+        } else if (OP == ST_STAGE_REMAINDER) {
+            // s = x0 + a0*x1 + a1*x2 (not stored);  y0 = dt F(s) - dt F(u)
+            const double2 x = ld2(A.x0 + o), u = ld2(A.u + o);
+            const double2 p = ld2(A.x1 + o);
+            double2 q = make_double2(0.0, 0.0);
+            if (A.x2) q = ld2(A.x2 + o);
+            const double sx = x.x + A.a0 * p.x + A.a1 * q.x;
+            const double sy = x.y + A.a0 * p.y + A.a1 * q.y;
+            st2(A.y0 + o, make_double2(dt * nl_rem(react, sx, u.x) + (-dt) * nl_rem(react, u.x, u.x),
+                                       dt * nl_rem(react, sy, u.y) + (-dt) * nl_rem(react, u.y, u.y)));
+        } else if (OP == ST_EXPRB32_A) {
+            const double2 u = ld2(A.x0 + o), p = ld2(A.x1 + o);
+            const double2 a = make_double2(u.x + p.x, u.y + p.y);
+            st2(A.y1 + o, a);
+            st2(A.y0 + o, make_double2(dt * nl_rem(react, a.x, u.x) + (-dt) * nl_rem(react, u.x, u.x),
+                                       dt * nl_rem(react, a.y, u.y) + (-dt) * nl_rem(react, u.y, u.y)));
+        } else if (OP == ST_COMBINE2) {
+            const double2 x = ld2(A.x0 + o), y = ld2(A.x1 + o);
+            st2(A.y0 + o, make_double2(A.a0 * x.x + A.a1 * y.x, A.a0 * x.y + A.a1 * y.y));
+            st2(A.y1 + o, make_double2(A.a2 * x.x + A.a3 * y.x, A.a2 * x.y + A.a3 * y.y));
+        } else if (OP == ST_FINAL4) {
+            const double2 u = ld2(A.x0 + o), p1 = ld2(A.x1 + o), q3 = ld2(A.x2 + o), q4 = ld2(A.x3 + o);
+            const double2 u3 = make_double2(u.x + p1.x + q3.x, u.y + p1.y + q3.y);
+            const double2 u4 = make_double2(u3.x + q4.x, u3.y + q4.y);
+            st2(A.y0 + o, u3);
+            st2(A.y1 + o, u4);
+            const double ex = u4.x - u3.x, ey = u4.y - u3.y;
+            acc = fma(ex, ex, acc);
+            acc = fma(ey, ey, acc);
+        } else if (OP == ST_FINAL_EXPRB32) {
+            const double2 a = ld2(A.x0 + o), q = ld2(A.x1 + o);
+            st2(A.y0 + o, make_double2(a.x + 2.0 * q.x, a.y + 2.0 * q.y));
+            const double ex = 2.0 * q.x, ey = 2.0 * q.y;
+            acc = fma(ex, ex, acc);
+            acc = fma(ey, ey, acc);
+        } else if (OP == ST_MAXSQ) {
+            const double2 x = ld2(A.x0 + o);
+            const double m2 = fmax(x.x * x.x, x.y * x.y);
+            const unsigned long long b = (unsigned long long)__double_as_longlong(m2);
+            umax = b > umax ? b : umax;
+        }
+    }
+    if (OP == ST_FINAL4 || OP == ST_FINAL_EXPRB32) stage_reduce_err(A, acc, s_red, &s_last);
+    if (OP == ST_MAXSQ) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const unsigned long long o2 = __shfl_xor_sync(FULL_MASK, umax, off);
+            umax = o2 > umax ? o2 : umax;
+        }
+        if ((threadIdx.x & 31) == 0 && umax) atomicMax(&A.ctrl->umax, umax);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_rhs2d(const __grid_constant__ LejaParams P, double scale) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double sy = 0.0, sp[1] = {0.0};
+    for (int unit = blockIdx.x * kWarps + warp; unit < P.nunits; unit += gridDim.x * kWarps)
+        tile2d<0, false, false, M_RHS, true>(P, P.v, P.ydst[0], unit, lane, 0.0, nullptr, nullptr, 0, scale, sy, sp);
+}
+
+__global__ void k_fill_start(double* v, long long n, int add_e0) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        v[i] = (add_e0 && i == 0) ? 2.0 : 1.0;
+}
+
+cudaError_t launch_fill_start(double* v, long long n, bool add_e0, cudaStream_t s) {
+    k_fill_start<<<256, 256, 0, s>>>(v, n, add_e0 ? 1 : 0);
+    return cudaGetLastError();
+}
+
+int stage_grid_size(int device) {
+    int nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    return nsm * 4;
+}
+
+cudaError_t launch_rhs(const LejaParams& P, double scale, cudaStream_t s) {
+    k_rhs2d<<<P.grid, kThreads, 0, s>>>(P, scale);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stage(int op, const StageArgs& A, cudaStream_t s) {
+    const dim3 g(A.grid), b(kThreads);
+    switch (op) {
+        case ST_AXPBY: k_stage_pointwise<ST_AXPBY><<<g, b, 0, s>>>(A); break;
+        case ST_REMAINDER_DIFF: k_stage_pointwise<ST_REMAINDER_DIFF><<<g, b, 0, s>>>(A); break;
+        case ST_STAGE_REMAINDER: k_stage_pointwise<ST_STAGE_REMAINDER><<<g, b, 0, s>>>(A); break;
+        case ST_EXPRB32_A: k_stage_pointwise<ST_EXPRB32_A><<<g, b, 0, s>>>(A); break;
+        case ST_COMBINE2: k_stage_pointwise<ST_COMBINE2><<<g, b, 0, s>>>(A); break;
+        case ST_FINAL4: k_stage_pointwise<ST_FINAL4><<<g, b, 0, s>>>(A); break;
+        case ST_FINAL_EXPRB32: k_stage_pointwise<ST_FINAL_EXPRB32><<<g, b, 0, s>>>(A); break;
+        case ST_MAXSQ: k_stage_pointwise<ST_MAXSQ><<<g, b, 0, s>>>(A); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace lx

@@ -1,0 +1,282 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle.
+
+Bar (BASELINE.json north_star): the SAME number of Leja iterations and
+relative L2 error <= 1e-10 in fp64.  Inputs are seeded/synthetic (workloads/).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2310_08344_b200 as lx  # noqa: E402
+
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _rel(a, b):
+    a = a.detach().cpu().numpy() if hasattr(a, "detach") else np.asarray(a)
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a.reshape(b.shape) - b) / (nb if nb > 0 else 1.0)
+
+
+def _pair(shape, diff=1.0, nu=10.0, react=0.0):
+    dx = tuple(2.0 / n for n in shape)
+    return lx.Problem(shape, dx, diff, nu, react), O.Problem(shape, dx, diff, nu, react)
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+# ---------------------------------------------------------------- Leja calls
+@pytest.mark.parametrize("l", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("mult", [1.0, 10.0, 100.0])
+def test_leja_phi_64(xi300, l, mult):
+    n = 64
+    pb, ob = _pair((n, n))
+    dt = mult * W.dt_cfl(n, 10.0)
+    u0 = W.ic_problem1_2d(n)
+    with lx.Context(pb) as ctx:
+        c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+        out = torch.empty((n, n), dtype=torch.float64, device="cuda")
+        it = lx.lx_real_leja_phi(ctx, _dev(u0), out, dt, c, g, l, TOL, TOL)
+    r = O.real_leja_phi(ob, u0, dt, c, g, l, TOL, TOL, xi300)
+    assert it == r.iters
+    assert _rel(out, r.outs[0]) <= TOL
+
+
+@pytest.mark.parametrize("shape", [(50, 70), (37, 130), (64, 128), (130, 66), (8, 4), (5, 6)])
+def test_leja_ragged_shapes(xi300, shape):
+    # partial column bands (n1 % 64 != 0), partial row blocks (n0 % 4 != 0), tiny grids
+    pb, ob = _pair(shape, nu=4.0)
+    v = W.ic_random(shape, seed=99, amp=0.2)
+    dt = 5 * min(W.dt_cfl(n, 4.0) for n in shape)
+    with lx.Context(pb) as ctx:
+        c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+        assert (c, g) == O.shift_scale(O.spectrum_bound(ob))
+        for l in (0, 1, 3):
+            out = torch.empty(shape, dtype=torch.float64, device="cuda")
+            it = lx.lx_real_leja_phi(ctx, _dev(v), out, dt, c, g, l, TOL, TOL)
+            r = O.real_leja_phi(ob, v, dt, c, g, l, TOL, TOL, xi300)
+            assert it == r.iters, (shape, l)
+            assert _rel(out, r.outs[0]) <= TOL, (shape, l)
+
+
+@pytest.mark.parametrize("coeffs", [(0.5, 1.0), (0.5, 2 / 3, 1.0), (0.25, 0.5, 0.75, 1.0)])
+def test_leja_vertical(xi300, coeffs):
+    n = 96
+    pb, ob = _pair((n, n))
+    dt = 20 * W.dt_cfl(n, 10.0)
+    v = W.ic_problem1_2d(n)
+    with lx.Context(pb) as ctx:
+        c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+        outs = [torch.empty((n, n), dtype=torch.float64, device="cuda") for _ in coeffs]
+        it = lx.lx_real_leja_phi_vertical(ctx, _dev(v), outs, coeffs, dt, c, g, 1, TOL, TOL)
+    r = O.real_leja_phi(ob, v, dt, c, g, 1, TOL, TOL, xi300, coeffs=coeffs)
+    assert it == r.iters
+    for k in range(len(coeffs)):
+        assert _rel(outs[k], r.outs[k]) <= TOL, k
+
+
+def test_leja_allen_cahn_jacobian(xi300):
+    n = 128
+    pb, ob = _pair((n, n), diff=1e-4, nu=0.0, react=1.0)
+    u = W.ic_allen_cahn_2d(n)
+    v = W.random_vector((n, n), seed=5, scale=1e-3)
+    with lx.Context(pb) as ctx:
+        bound = lx.lx_spectrum_bound(ctx, _dev(u))
+        assert bound == pytest.approx(O.spectrum_bound(ob, u), rel=1e-15)
+        c, g = lx.lx_shift_scale(bound)
+        for l in (1, 3, 4):
+            out = torch.empty((n, n), dtype=torch.float64, device="cuda")
+            it = lx.lx_real_leja_phi(ctx, _dev(v), out, 0.01, c, g, l, TOL, TOL, u_lin=_dev(u))
+            r = O.real_leja_phi(ob, v, 0.01, c, g, l, TOL, TOL, xi300, u_lin=u)
+            assert it == r.iters, l
+            assert _rel(out, r.outs[0]) <= TOL, l
+
+
+def test_leja_zero_input_dt_zero_and_noconv(xi300):
+    n = 32
+    pb, ob = _pair((n, n))
+    with lx.Context(pb) as ctx:
+        c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+        z = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+        out = torch.full((n, n), 7.0, dtype=torch.float64, device="cuda")
+        assert lx.lx_real_leja_phi(ctx, z, out, 1e-3, c, g, 1, TOL, TOL) == 1
+        assert torch.all(out == 0)
+        v = _dev(W.ic_problem1_2d(n))
+        for l in range(5):
+            assert lx.lx_real_leja_phi(ctx, v, out, 0.0, c, g, l, TOL, TOL) == 1
+            assert torch.equal(out, v * (1.0 / math.factorial(l)))
+    with lx.Context(pb, max_nodes=20) as ctx:
+        c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+        v0 = W.ic_problem1_2d(n)
+        out = torch.empty((n, n), dtype=torch.float64, device="cuda")
+        with pytest.raises(lx.LxError) as e:
+            lx.lx_real_leja_phi(ctx, _dev(v0), out, 1000 * W.dt_cfl(n, 10.0), c, g, 0, 1e-14, 0.0)
+        assert e.value.status == lx.LX_ERR_NOCONV and e.value.iters == 19
+        r = O.real_leja_phi(ob, v0, 1000 * W.dt_cfl(n, 10.0), c, g, 0, 1e-14, 0.0, xi300, max_nodes=20)
+        assert r.status == O.ERR_NOCONV and r.iters == 19
+        assert _rel(out, r.outs[0]) <= 1e-10
+
+
+def test_argument_errors():
+    n = 16
+    pb, _ = _pair((n, n))
+    with lx.Context(pb) as ctx:
+        v = torch.ones((n, n), dtype=torch.float64, device="cuda")
+        with pytest.raises(lx.LxError) as e:
+            lx.lx_real_leja_phi(ctx, v, v, 1e-3, -1.0, 1.0, 1, TOL, TOL)
+        assert e.value.status == lx.LX_ERR_ALIAS
+        with pytest.raises(lx.LxError) as e:
+            lx.lx_real_leja_phi(ctx, v, torch.empty_like(v), 1e-3, -1.0, 1.0, 5, TOL, TOL)
+        assert e.value.status == lx.LX_ERR_UNSUPPORTED
+        with pytest.raises(lx.LxError) as e:
+            lx.lx_real_leja_phi(ctx, v, torch.empty_like(v), 1e-3, -1.0, -1.0, 1, TOL, TOL)
+        assert e.value.status == lx.LX_ERR_ARG
+        with pytest.raises(lx.LxError) as e:
+            lx.lx_step(ctx, 9, v, torch.empty_like(v), torch.empty_like(v), 1e-3, -1.0, 1.0, TOL, TOL)
+        assert e.value.status == lx.LX_ERR_UNKNOWN_INTEGRATOR
+    with pytest.raises(lx.LxError) as e:
+        lx.Context(lx.Problem((16, 15), (0.1, 0.1)))
+    assert e.value.status == lx.LX_ERR_DIM
+
+
+def test_host_pointer_path_equals_device_path():
+    n = 64
+    pb, _ = _pair((n, n))
+    u0 = W.ic_problem1_2d(n)
+    dt = 10 * W.dt_cfl(n, 10.0)
+    with lx.Context(pb) as ctx:
+        c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+        out_d = torch.empty((n, n), dtype=torch.float64, device="cuda")
+        it_d = lx.lx_real_leja_phi(ctx, _dev(u0), out_d, dt, c, g, 1, TOL, TOL)
+        out_h = np.zeros((n, n))
+        it_h = lx.lx_real_leja_phi(ctx, u0, out_h, dt, c, g, 1, TOL, TOL)
+    assert it_d == it_h
+    np.testing.assert_array_equal(out_d.cpu().numpy(), out_h)
+
+
+def test_async_calls_and_determinism():
+    n = 128
+    pb, _ = _pair((n, n))
+    u0 = _dev(W.ic_problem1_2d(n))
+    dt = 10 * W.dt_cfl(n, 10.0)
+    with lx.Context(pb) as ctx:
+        c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+        outs = [torch.empty_like(u0) for _ in range(4)]
+        sync_iters = [lx.lx_real_leja_phi(ctx, u0, outs[l], dt, c, g, l, TOL, TOL) for l in range(4)]
+        ref = [o.clone() for o in outs]
+        for l in range(4):
+            lx.lx_real_leja_phi(ctx, u0, outs[l], dt, c, g, l, TOL, TOL, sync=False)
+        total, _ = ctx.synchronize()
+        assert total == sum(sync_iters)
+        for a, b in zip(outs, ref):
+            assert torch.equal(a, b)   # bitwise reproducible (fixed-order reductions)
+
+
+# ---------------------------------------------------------------- spectrum / rhs
+def test_power_iteration_and_rhs(xi300):
+    n = 64
+    pb, ob = _pair((n, n))
+    with lx.Context(pb) as ctx:
+        est = lx.lx_spectrum_estimate(ctx, None, 50)
+        assert est == pytest.approx(O.power_iteration(ob, None, 50), rel=1e-10)
+        u0 = W.ic_problem1_2d(n)
+        f = torch.empty((n, n), dtype=torch.float64, device="cuda")
+        lx.lx_rhs(ctx, _dev(u0), f, 0.37)
+        ref = 0.37 * O.rhs(ob, u0)
+        assert np.abs(f.cpu().numpy() - ref).max() <= 1e-12 * np.abs(ref).max()
+    pa, oa = _pair((48, 64), diff=1e-3, nu=0.0, react=1.0)
+    u = W.ic_allen_cahn_2d(48, 64)
+    with lx.Context(pa) as ctx:
+        est = lx.lx_spectrum_estimate(ctx, _dev(u), 40)
+        assert est == pytest.approx(O.power_iteration(oa, u, 40), rel=1e-10)
+
+
+# ---------------------------------------------------------------- integrators
+@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a"])
+def test_steps_linear_advdiff(xi300, method):
+    n = 64
+    pb, ob = _pair((n, n))
+    u0 = W.ic_problem1_2d(n)
+    dt = 10 * W.dt_cfl(n, 10.0)
+    with lx.Context(pb) as ctx:
+        c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+        lo = torch.empty((n, n), dtype=torch.float64, device="cuda")
+        hi = torch.empty_like(lo)
+        it, err = lx.lx_step(ctx, method, _dev(u0), lo, hi, dt, c, g, TOL, TOL)
+    r = O.step(ob, method, u0, dt, c, g, TOL, TOL, xi300)
+    assert it == r.iters
+    assert _rel(hi, r.u_high) <= TOL
+    if method != "rosenbrock_euler":
+        assert err == r.err == 0.0
+
+
+@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a"])
+def test_steps_allen_cahn(xi300, method):
+    n = 128
+    pb, ob = _pair((n, n), diff=1e-4, nu=0.0, react=1.0)
+    u = W.ic_allen_cahn_2d(n)
+    dt = 0.01
+    with lx.Context(pb) as ctx:
+        ud = _dev(u)
+        for step in range(3):
+            bound = lx.lx_spectrum_bound(ctx, ud)
+            c, g = lx.lx_shift_scale(bound)
+            lo = torch.empty_like(ud)
+            hi = torch.empty_like(ud)
+            it, err = lx.lx_step(ctx, method, ud, lo, hi, dt, c, g, TOL, TOL)
+            r = O.step(ob, method, u, dt, c, g, TOL, TOL, xi300)
+            assert it == r.iters, (method, step)
+            assert _rel(hi, r.u_high) <= TOL, (method, step)
+            if method != "rosenbrock_euler":
+                assert _rel(lo, r.u_low) <= TOL
+                assert err == pytest.approx(r.err, rel=1e-8)
+            # continue from the oracle state so both sides see identical inputs
+            u = r.u_high
+            ud = _dev(u)
+
+
+# ---------------------------------------------------------------- full size (BASELINE configs)
+def test_config0_rosenbrock_euler_64(xi300):
+    wl = W.config(0)
+    pb, ob = _pair(wl.shape)
+    u0 = W.ic_problem1_2d(64)
+    with lx.Context(pb) as ctx:
+        c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+        out = np.zeros(wl.shape)
+        it = lx.lx_step_rosenbrock_euler(ctx, u0, out, wl.dt, c, g, wl.rtol, wl.atol)   # host buffers
+    r = O.step(ob, "rosenbrock_euler", u0, wl.dt, c, g, wl.rtol, wl.atol, xi300)
+    assert it == r.iters == 23
+    assert _rel(out, r.u_high) <= TOL
+
+
+@pytest.mark.slow
+def test_config1_4096_phi0_full_oracle(xi300):
+    # BASELINE config 1 at full size, launch configuration of bench.py: phi_0 vs the full oracle.
+    wl = W.config(1)
+    n = wl.shape[0]
+    pb, ob = _pair(wl.shape)
+    u0 = W.ic_problem1_2d(n)
+    with lx.Context(pb) as ctx:
+        c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+        out = torch.empty(wl.shape, dtype=torch.float64, device="cuda")
+        it = lx.lx_real_leja_phi(ctx, _dev(u0), out, wl.dt, c, g, 0, wl.rtol, wl.atol)
+        got = out.cpu().numpy()
+    r = O.real_leja_phi(ob, u0, wl.dt, c, g, 0, wl.rtol, wl.atol, xi300)
+    assert it == r.iters
+    assert _rel(got, r.outs[0]) <= TOL
