@@ -178,7 +178,8 @@ def run_ours(args):
         raise SystemExit("multi-GPU bench path requires the NCCL slab build (not in this version)")
     wl = W.config(1, n=n)
     pb = lx.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     ctx = lx.Context(pb, stream=stream)
     u0_h = W.ic_problem1_2d(n)
     u0 = torch.from_numpy(u0_h).cuda()

@@ -108,7 +108,8 @@ typedef struct lx_ctx lx_ctx;
 /* Create a context for problems on the grid of `pb` (only pb->ndim, pb->n
  * are used here).  max_nodes = Leja node cap (0 -> 300; <= 1024).
  * device = CUDA device ordinal (-1 -> current).  cuda_stream = cudaStream_t
- * to enqueue on (NULL -> a stream owned by the context).
+ * to enqueue on (NULL -> a non-blocking stream owned by the context; pass
+ * cudaStreamLegacy = (void*)1 for the legacy default stream).
  * Allocates: 2 y buffers + 3-row ghosts each, 7 stage vectors, partial-sum
  * slots, control block, coefficient-table ring, host staging (lazily).
  * Errors: LX_ERR_ARG, LX_ERR_DIM, LX_ERR_UNSUPPORTED, LX_ERR_CUDA. */

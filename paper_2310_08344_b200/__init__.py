@@ -192,6 +192,8 @@ class Context:
         sp = None
         if stream is not None:
             sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+            if sp == 0:
+                sp = 1   # the legacy default stream (cudaStreamLegacy); NULL would mean "own stream"
         _check(lib().lx_ctx_create(ctypes.byref(self._pb), int(max_nodes), int(device), sp, ctypes.byref(h)))
         self.handle = h
 
