@@ -125,6 +125,18 @@ lx_status lx_ctx_destroy(lx_ctx *ctx);
 lx_status lx_nccl_unique_id(void *out128);
 lx_status lx_ctx_set_comm(lx_ctx *ctx, const void *nccl_unique_id, int rank, int nranks);
 
+/* In-process slab decomposition over `nranks` VIRTUAL ranks (host threads of
+ * one process, all on the context's device).  Runs exactly the multi-rank
+ * protocol of lx_ctx_set_comm (step kernels, 1+2-row halo exchange, rank-order
+ * sum of gathered partials) with device-to-device copies and host barriers as
+ * the transport; used to validate the slab path on one GPU and for
+ * single-process multi-stream use.  Each rank's calls must be issued from its
+ * own host thread, all ranks making the same sequence of calls. */
+typedef struct lx_local_group lx_local_group;
+lx_status lx_local_group_create(int nranks, lx_local_group **out);
+lx_status lx_local_group_destroy(lx_local_group *group);
+lx_status lx_ctx_set_comm_local(lx_ctx *ctx, lx_local_group *group, int rank);
+
 /* Local slab of this context: rows [*i_begin, *i_end), *n_local points. */
 lx_status lx_ctx_local(const lx_ctx *ctx, int64_t *i_begin, int64_t *i_end, int64_t *n_local);
 

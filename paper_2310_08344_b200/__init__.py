@@ -39,7 +39,7 @@ EXPORTS = ("lx_last_error", "lx_version", "lx_leja_points", "lx_phi_scalar", "lx
            "lx_ctx_local", "lx_ctx_synchronize", "lx_ctx_launch_count", "lx_spectrum_estimate",
            "lx_spectrum_bound", "lx_shift_scale", "lx_real_leja_phi", "lx_real_leja_phi_vertical",
            "lx_step_rosenbrock_euler", "lx_step_exprb32", "lx_step_exprb43", "lx_step_epirk4s3a",
-           "lx_step", "lx_rhs")
+           "lx_step", "lx_rhs", "lx_local_group_create", "lx_local_group_destroy", "lx_ctx_set_comm_local")
 
 
 class LxError(RuntimeError):
@@ -115,6 +115,9 @@ def lib() -> ctypes.CDLL:
             "lx_step_exprb43": (ctypes.c_int, [vp, pbp, vp, vp, vp, dp, d, d, d, d, d, ip]),
             "lx_step_epirk4s3a": (ctypes.c_int, [vp, pbp, vp, vp, vp, dp, d, d, d, d, d, ip]),
             "lx_rhs": (ctypes.c_int, [vp, pbp, vp, d, vp]),
+            "lx_local_group_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(vp)]),
+            "lx_local_group_destroy": (ctypes.c_int, [vp]),
+            "lx_ctx_set_comm_local": (ctypes.c_int, [vp, vp, ctypes.c_int]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -182,14 +185,44 @@ def lx_nccl_unique_id() -> bytes:
 
 
 # ------------------------------------------------------------------ context
+class LocalGroup:
+    """Virtual ranks of one process on one GPU (lx_local_group): same slab protocol as NCCL."""
+
+    def __init__(self, nranks: int):
+        h = ctypes.c_void_p()
+        _check(lib().lx_local_group_create(int(nranks), ctypes.byref(h)))
+        self.handle = h
+        self.nranks = nranks
+
+    def close(self):
+        if self.handle:
+            lib().lx_local_group_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Context:
     """Owns an lx_ctx (scratch allocated once)."""
 
     def __init__(self, problem: Problem, max_nodes: int = 300, device: int = -1, stream=None):
+        """stream: torch.cuda.Stream / raw cudaStream_t handle; default = torch's current
+        stream (so library work is ordered with the caller's torch ops)."""
         self.problem = problem
         self._pb = problem.c_struct()
         h = ctypes.c_void_p()
         sp = None
+        if stream is None:
+            try:
+                import torch
+                if torch.cuda.is_available():
+                    stream = torch.cuda.current_stream()
+            except ImportError:
+                pass
         if stream is not None:
             sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
             if sp == 0:
@@ -217,6 +250,10 @@ class Context:
     def set_comm(self, uid: bytes, rank: int, nranks: int):
         buf = ctypes.create_string_buffer(uid, 128)
         _check(lib().lx_ctx_set_comm(self.handle, buf, int(rank), int(nranks)))
+
+    def set_comm_local(self, group: "LocalGroup", rank: int):
+        self._group = group   # keep the group alive while the context uses it
+        _check(lib().lx_ctx_set_comm_local(self.handle, group.handle, int(rank)))
 
     def local(self):
         b, e, n = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()

@@ -21,14 +21,16 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
 def _nccl_dir():
+    """torch's bundled NCCL 2.28 (nvidia-nccl wheel): headers + libnccl.so.2."""
     try:
-        import nvidia.nccl  # noqa: F401  (torch's bundled NCCL 2.28)
-        base = os.path.dirname(nvidia.nccl.__file__) if nvidia.nccl.__file__ else list(nvidia.nccl.__path__)[0]
+        import nvidia
+        bases = [os.path.join(p, "nccl") for p in nvidia.__path__]
     except Exception:
         return None
-    inc, lib = os.path.join(base, "include"), os.path.join(base, "lib")
-    if os.path.exists(os.path.join(inc, "nccl.h")) and os.path.exists(os.path.join(lib, "libnccl.so.2")):
-        return inc, lib
+    for base in bases:
+        inc, lib = os.path.join(base, "include"), os.path.join(base, "lib")
+        if os.path.exists(os.path.join(inc, "nccl.h")) and os.path.exists(os.path.join(lib, "libnccl.so.2")):
+            return inc, lib
     return None
 
 

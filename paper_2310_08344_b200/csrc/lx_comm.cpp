@@ -1,16 +1,397 @@
-// lx_comm.cpp -- placeholder until the NCCL slab path lands.
+// lx_comm.cpp -- slab decomposition of the Leja path over several ranks.
+//
+// Protocol per Leja iteration m (identical for every transport):
+//   1. k_leja2d_step(m): decision of m-1 from the gathered per-rank partials
+//      (summed in rank order -> the same decision on every rank), tiles of m,
+//      per-rank partial {S_y, S_p^(k)} by a fixed-order last-block reduction;
+//   2. halo: the 1 last row goes to rank r+1 (its ghost row -1) and the 2 first
+//      rows go to rank r-1 (its ghost rows n, n+1) -- the +x-biased upwind
+//      stencil reaches i-1, i+1, i+2 (reading R10); periodic in rank;
+//   3. allgather of the per-rank partials (1+K doubles).
+// The host enqueues iterations in chunks and polls the device `done` flag once
+// per chunk (launches after convergence exit at entry), so every rank issues the
+// same sequence of collectives.
+//
+// Transports: NCCL (one process per GPU, NVLink/NVSwitch) and LOCAL (virtual
+// ranks = host threads of one process sharing one GPU; D2D copies + host
+// barriers).  LOCAL runs the same protocol and kernels, so the multi-rank path is
+// validated on a single B200 against the single-domain result.
 #include "lx_comm.h"
 
+#include <condition_variable>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#ifdef LX_HAVE_NCCL
+#include <nccl.h>
+#endif
+
 namespace lx {
-struct Comm {};
-const char* comm_error() { return "NCCL slab decomposition not built in this version"; }
-int comm_unique_id(void*) { return 1; }
-int comm_create(const void*, int, int, int, long long, int, Comm**) { return 1; }
-void comm_destroy(Comm*) {}
-void comm_bind(Comm*, double* const*, double* const*, double*, int, int, int) {}
-lx_status comm_leja(Comm*, LejaParams&, bool, cudaStream_t, int64_t*) { return LX_ERR_NCCL; }
-lx_status comm_power(Comm*, LejaParams&, bool, cudaStream_t, int64_t*) { return LX_ERR_NCCL; }
-int comm_allreduce_max_u64(Comm*, unsigned long long*, cudaStream_t) { return 1; }
-int comm_stage_norm(Comm*, int, const StageArgs&, cudaStream_t, int64_t*) { return 1; }
-int comm_rhs(Comm*, LejaParams&, double, cudaStream_t, int64_t*) { return 1; }
+
+static thread_local std::string g_comm_err;
+const char* comm_error() { return g_comm_err.c_str(); }
+static int cerr(const std::string& m) {
+    g_comm_err = m;
+    return 1;
+}
+#define CU(x)                                                                               \
+    do {                                                                                    \
+        cudaError_t e_ = (x);                                                               \
+        if (e_ != cudaSuccess) return cerr(std::string(#x ": ") + cudaGetErrorString(e_));  \
+    } while (0)
+
+struct Transport {
+    int rank = 0, nranks = 1;
+    virtual ~Transport() {}
+    virtual int exchange_rows(const double* base, double* ghost, int n_loc, long long row, cudaStream_t s) = 0;
+    virtual int allgather(const double* send, double* recv, int count, cudaStream_t s) = 0;
+    virtual int allreduce_max_u64(unsigned long long* buf, cudaStream_t s) = 0;
+};
+
+// ------------------------------------------------------------------ NCCL
+#ifdef LX_HAVE_NCCL
+#define NC(x)                                                                                   \
+    do {                                                                                        \
+        ncclResult_t r_ = (x);                                                                  \
+        if (r_ != ncclSuccess) return cerr(std::string(#x ": ") + ncclGetErrorString(r_));      \
+    } while (0)
+
+struct NcclTransport : Transport {
+    ncclComm_t comm = nullptr;
+    ~NcclTransport() override {
+        if (comm) ncclCommDestroy(comm);
+    }
+    int exchange_rows(const double* base, double* ghost, int n_loc, long long row, cudaStream_t s) override {
+        const int up = (rank - 1 + nranks) % nranks, down = (rank + 1) % nranks;
+        NC(ncclGroupStart());
+        // direction "up": my rows 0,1 -> ghost rows n, n+1 of rank r-1; I receive rank r+1's rows 0,1
+        NC(ncclSend(base, 2 * row, ncclDouble, up, comm, s));
+        NC(ncclRecv(ghost + row, 2 * row, ncclDouble, down, comm, s));
+        // direction "down": my last row -> ghost row -1 of rank r+1; I receive rank r-1's last row
+        NC(ncclSend(base + (long long)(n_loc - 1) * row, row, ncclDouble, down, comm, s));
+        NC(ncclRecv(ghost, row, ncclDouble, up, comm, s));
+        NC(ncclGroupEnd());
+        return 0;
+    }
+    int allgather(const double* send, double* recv, int count, cudaStream_t s) override {
+        NC(ncclAllGather(send, recv, count, ncclDouble, comm, s));
+        return 0;
+    }
+    int allreduce_max_u64(unsigned long long* buf, cudaStream_t s) override {
+        NC(ncclAllReduce(buf, buf, 1, ncclUint64, ncclMax, comm, s));
+        return 0;
+    }
+};
+#endif
+
+int comm_unique_id(void* out128) {
+#ifdef LX_HAVE_NCCL
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return cerr(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    std::memcpy(out128, &id, 128);
+    return 0;
+#else
+    (void)out128;
+    return cerr("built without NCCL");
+#endif
+}
+
+// ------------------------------------------------------------------ LOCAL
+struct LocalGroup {
+    int nranks;
+    std::mutex mu;
+    std::condition_variable cv;
+    int count = 0;
+    long long gen = 0;
+    std::vector<const void*> ptr;
+    std::vector<int> nloc;
+    std::vector<cudaEvent_t> ev;
+    explicit LocalGroup(int n) : nranks(n), ptr(n, nullptr), nloc(n, 0), ev(n, nullptr) {}
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        const long long g = gen;
+        if (++count == nranks) {
+            count = 0;
+            gen++;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g; });
+        }
+    }
+};
+
+LocalGroup* local_group_create(int nranks) { return new LocalGroup(nranks); }
+void local_group_destroy(LocalGroup* g) { delete g; }
+
+struct LocalTransport : Transport {
+    LocalGroup* g = nullptr;
+    cudaEvent_t ev = nullptr;
+    unsigned long long* tmp = nullptr;  // device [nranks]
+    ~LocalTransport() override {
+        if (ev) cudaEventDestroy(ev);
+        cudaFree(tmp);
+    }
+    int publish(const void* p, int n_loc, cudaStream_t s) {
+        CU(cudaEventRecord(ev, s));
+        g->ptr[rank] = p;
+        g->nloc[rank] = n_loc;
+        g->ev[rank] = ev;
+        g->barrier();
+        return 0;
+    }
+    int exchange_rows(const double* base, double* ghost, int n_loc, long long row, cudaStream_t s) override {
+        if (publish(base, n_loc, s)) return 1;
+        const int up = (rank - 1 + nranks) % nranks, down = (rank + 1) % nranks;
+        int rc = 0;
+        if (cudaStreamWaitEvent(s, g->ev[up], 0) != cudaSuccess || cudaStreamWaitEvent(s, g->ev[down], 0) != cudaSuccess)
+            rc = cerr("cudaStreamWaitEvent failed");
+        const double* ub = (const double*)g->ptr[up];
+        const double* db = (const double*)g->ptr[down];
+        if (!rc && cudaMemcpyAsync(ghost, ub + (long long)(g->nloc[up] - 1) * row, row * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+            rc = cerr("halo copy (up) failed");
+        if (!rc && cudaMemcpyAsync(ghost + row, db, 2 * row * sizeof(double), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+            rc = cerr("halo copy (down) failed");
+        g->barrier();  // everybody enqueued their pulls before pointers are republished
+        return rc;
+    }
+    // Make every rank's stream wait until all peers finished the copies they just
+    // enqueued (so a rank cannot overwrite a buffer a peer has not read yet).
+    int settle(cudaStream_t s) {
+        if (publish(nullptr, 0, s)) return 1;
+        int rc = 0;
+        for (int r = 0; r < nranks; r++)
+            if (cudaStreamWaitEvent(s, g->ev[r], 0) != cudaSuccess) rc = cerr("cudaStreamWaitEvent failed");
+        g->barrier();
+        return rc;
+    }
+    int allgather(const double* send, double* recv, int count, cudaStream_t s) override {
+        if (publish(send, 0, s)) return 1;
+        int rc = 0;
+        for (int r = 0; r < nranks && !rc; r++) {
+            if (cudaStreamWaitEvent(s, g->ev[r], 0) != cudaSuccess ||
+                cudaMemcpyAsync(recv + (long long)r * count, g->ptr[r], count * sizeof(double), cudaMemcpyDeviceToDevice,
+                                s) != cudaSuccess)
+                rc = cerr("allgather copy failed");
+        }
+        g->barrier();
+        if (settle(s)) return 1;
+        return rc;
+    }
+    int allreduce_max_u64(unsigned long long* buf, cudaStream_t s) override {
+        if (publish(buf, 0, s)) return 1;
+        int rc = 0;
+        for (int r = 0; r < nranks && !rc; r++) {
+            if (cudaStreamWaitEvent(s, g->ev[r], 0) != cudaSuccess ||
+                cudaMemcpyAsync(tmp + r, g->ptr[r], sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+                rc = cerr("allreduce copy failed");
+        }
+        g->barrier();
+        if (settle(s)) return 1;   // all peers have read every buf before anyone overwrites its own
+        if (!rc && launch_max_u64(tmp, nranks, buf, s) != cudaSuccess) rc = cerr("max kernel failed");
+        return rc;
+    }
+};
+
+// ------------------------------------------------------------------ Comm
+struct Comm {
+    Transport* tr = nullptr;
+    int rank = 0, nranks = 1, device = 0;
+    long long row = 0;
+    int n_loc = 0;
+    double* Y[2] = {nullptr, nullptr};
+    double* Yg[2] = {nullptr, nullptr};
+    double* vg = nullptr;
+    double* rank_part = nullptr;   // device [kSlot]
+    double* gathered = nullptr;    // device [nranks][kSlot]
+    int* done_host = nullptr;      // pinned [2]
+    Ctrl* ctrl_init = nullptr;     // pinned [kMaxK + 1] templates (hist[0] = active0)
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    int chunk = 4;
+};
+
+static int comm_alloc(Comm* c) {
+    CU(cudaMalloc(&c->rank_part, kSlot * sizeof(double)));
+    CU(cudaMalloc(&c->gathered, (size_t)c->nranks * kSlot * sizeof(double)));
+    CU(cudaMemset(c->rank_part, 0, kSlot * sizeof(double)));
+    CU(cudaMemset(c->gathered, 0, (size_t)c->nranks * kSlot * sizeof(double)));
+    CU(cudaMallocHost(&c->done_host, 2 * sizeof(int)));
+    CU(cudaMallocHost(&c->ctrl_init, (kMaxK + 1) * sizeof(Ctrl)));
+    std::memset(c->ctrl_init, 0, (kMaxK + 1) * sizeof(Ctrl));
+    for (int k = 0; k <= kMaxK; k++) c->ctrl_init[k].hist[0] = c->ctrl_init[k].hist[1] = (1 << k) - 1;
+    for (auto& e : c->ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return 0;
+}
+
+int comm_create(const void* uid, int rank, int nranks, int device, long long row, int max_grid, Comm** out) {
+    (void)max_grid;
+#ifdef LX_HAVE_NCCL
+    CU(cudaSetDevice(device));
+    Comm* c = new Comm();
+    c->rank = rank;
+    c->nranks = nranks;
+    c->device = device;
+    c->row = row;
+    auto* t = new NcclTransport();
+    t->rank = rank;
+    t->nranks = nranks;
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof id);
+    ncclResult_t r = ncclCommInitRank(&t->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+        delete t;
+        delete c;
+        return cerr(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+    c->tr = t;
+    if (comm_alloc(c)) {
+        comm_destroy(c);
+        return 1;
+    }
+    *out = c;
+    return 0;
+#else
+    (void)uid; (void)rank; (void)nranks; (void)device; (void)row; (void)out;
+    return cerr("built without NCCL");
+#endif
+}
+
+int comm_create_local(LocalGroup* g, int rank, int device, long long row, Comm** out) {
+    CU(cudaSetDevice(device));
+    Comm* c = new Comm();
+    c->rank = rank;
+    c->nranks = g->nranks;
+    c->device = device;
+    c->row = row;
+    auto* t = new LocalTransport();
+    t->rank = rank;
+    t->nranks = g->nranks;
+    t->g = g;
+    c->tr = t;
+    if (cudaEventCreateWithFlags(&t->ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaMalloc(&t->tmp, g->nranks * sizeof(unsigned long long)) != cudaSuccess || comm_alloc(c)) {
+        comm_destroy(c);
+        return cerr("local transport allocation failed");
+    }
+    *out = c;
+    return 0;
+}
+
+void comm_destroy(Comm* c) {
+    if (!c) return;
+    delete c->tr;
+    cudaFree(c->rank_part);
+    cudaFree(c->gathered);
+    cudaFreeHost(c->done_host);
+    cudaFreeHost(c->ctrl_init);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    delete c;
+}
+
+void comm_bind(Comm* c, double* const Y[2], double* const Yg[2], double* vg, int n_loc, int rank, int nranks) {
+    (void)rank; (void)nranks;
+    for (int i = 0; i < 2; i++) {
+        c->Y[i] = Y[i];
+        c->Yg[i] = Yg[i];
+    }
+    c->vg = vg;
+    c->n_loc = n_loc;
+}
+
+int comm_exchange(Comm* c, const double* base, double* ghost, cudaStream_t s) {
+    return c->tr->exchange_rows(base, ghost, c->n_loc, c->row, s);
+}
+
+// Enqueue iterations 1..last in chunks; poll `done` once per chunk (one chunk behind).
+template <typename Launch>
+static lx_status run_chunked(Comm* c, Ctrl* ctrl, int last, Launch launch, cudaStream_t s) {
+    int chunk = 0;
+    for (int m = 1; m <= last; m++) {
+        if (launch(m)) return LX_ERR_NCCL;
+        if (m % c->chunk == 0 || m == last) {
+            if (cudaMemcpyAsync(&c->done_host[chunk & 1], &ctrl->done, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+                cudaEventRecord(c->ev[chunk & 1], s) != cudaSuccess)
+                return LX_ERR_CUDA;
+            if (chunk >= 1) {
+                if (cudaEventSynchronize(c->ev[(chunk - 1) & 1]) != cudaSuccess) return LX_ERR_CUDA;
+                if (c->done_host[(chunk - 1) & 1]) break;
+            }
+            chunk++;
+        }
+    }
+    return LX_OK;
+}
+
+lx_status comm_leja(Comm* c, LejaParams& P, bool diag, cudaStream_t s, int64_t* launches) {
+    P.nranks = c->nranks;
+    P.rank_part = c->rank_part;
+    P.gathered = c->gathered;
+    P.grid = step_grid_size(c->device, P.nunits);
+    P.v.ghost = c->vg;
+    if (cudaMemcpyAsync(P.ctrl, &c->ctrl_init[P.K], sizeof(Ctrl), cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return LX_ERR_CUDA;
+    if (comm_exchange(c, P.v.base, c->vg, s)) return LX_ERR_NCCL;
+    const int M = P.max_nodes;
+    auto launch = [&](int m) -> int {
+        if (launch_leja_step(P, m, s, diag) != cudaSuccess) return cerr("step kernel launch failed");
+        (*launches)++;
+        if (m < M) {
+            if (comm_exchange(c, c->Y[m & 1], c->Yg[m & 1], s)) return 1;
+            if (c->tr->allgather(c->rank_part, c->gathered, kSlot, s)) return 1;
+        }
+        return 0;
+    };
+    return run_chunked(c, P.ctrl, M, launch, s);
+}
+
+lx_status comm_power(Comm* c, LejaParams& P, bool diag, cudaStream_t s, int64_t* launches) {
+    P.nranks = c->nranks;
+    P.rank_part = c->rank_part;
+    P.gathered = c->gathered;
+    P.grid = step_grid_size(c->device, P.nunits);
+    if (cudaMemcpyAsync(P.ctrl, &c->ctrl_init[0], sizeof(Ctrl), cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return LX_ERR_CUDA;
+    if (comm_exchange(c, c->Y[0], c->Yg[0], s)) return LX_ERR_NCCL;
+    const int last = P.power_iters + 1;
+    auto launch = [&](int m) -> int {
+        if (launch_power_step(P, m, s, diag) != cudaSuccess) return cerr("power step launch failed");
+        (*launches)++;
+        if (m < last) {
+            if (comm_exchange(c, c->Y[m & 1], c->Yg[m & 1], s)) return 1;
+            if (c->tr->allgather(c->rank_part, c->gathered, kSlot, s)) return 1;
+        }
+        return 0;
+    };
+    return run_chunked(c, P.ctrl, last, launch, s);
+}
+
+int comm_allreduce_max_u64(Comm* c, unsigned long long* dev, cudaStream_t s) {
+    return c->tr->allreduce_max_u64(dev, s);
+}
+
+int comm_stage_norm(Comm* c, int op, const StageArgs& A0, cudaStream_t s, int64_t* launches) {
+    StageArgs A = A0;
+    A.rank_part = c->rank_part;
+    CU(launch_stage(op, A, s));
+    (*launches)++;
+    if (c->tr->allgather(c->rank_part, c->gathered, kSlot, s)) return 1;
+    CU(launch_finalize_err(c->gathered, c->nranks, A.N_glob, A.rec, s));
+    (*launches)++;
+    return 0;
+}
+
+int comm_rhs(Comm* c, LejaParams& P, double scale, cudaStream_t s, int64_t* launches) {
+    if (comm_exchange(c, P.v.base, c->vg, s)) return 1;
+    P.v.ghost = c->vg;
+    P.grid = step_grid_size(c->device, P.nunits);
+    CU(launch_rhs(P, scale, s));
+    (*launches)++;
+    return 0;
+}
+
 }  // namespace lx

@@ -11,6 +11,10 @@ struct Comm;
 const char* comm_error();
 int comm_unique_id(void* out128);
 int comm_create(const void* uid, int rank, int nranks, int device, long long row, int max_grid, Comm** out);
+struct LocalGroup;
+LocalGroup* local_group_create(int nranks);
+void local_group_destroy(LocalGroup* g);
+int comm_create_local(LocalGroup* g, int rank, int device, long long row, Comm** out);
 void comm_destroy(Comm* c);
 void comm_bind(Comm* c, double* const Y[2], double* const Yg[2], double* vg, int n_loc, int rank, int nranks);
 lx_status comm_leja(Comm* c, LejaParams& P, bool diag, cudaStream_t s, int64_t* launches);

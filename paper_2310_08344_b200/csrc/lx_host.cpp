@@ -455,24 +455,22 @@ lx_status lx_nccl_unique_id(void* out128) {
     return comm_unique_id(out128) ? fail(LX_ERR_NCCL, "ncclGetUniqueId failed: %s", comm_error()) : LX_OK;
 }
 
-lx_status lx_ctx_set_comm(lx_ctx* ctx, const void* uid, int rank, int nranks) {
-    if (!ctx || !uid) return fail(LX_ERR_ARG, "NULL");
+static lx_status check_slabs(lx_ctx* ctx, int rank, int nranks) {
     if (nranks < 1 || rank < 0 || rank >= nranks) return fail(LX_ERR_ARG, "bad rank/nranks");
-    int64_t b, e;
-    lx_slab_range(ctx->n[0], rank, nranks, &b, &e);
     for (int r = 0; r < nranks; r++) {
         int64_t bb, ee;
         lx_slab_range(ctx->n[0], r, nranks, &bb, &ee);
         if (ee - bb < 2) return fail(LX_ERR_DIM, "slab of rank %d has < 2 rows", r);
     }
-    cudaStreamSynchronize(ctx->stream);
-    if (ctx->comm) { comm_destroy(ctx->comm); ctx->comm = nullptr; }
-    if (nranks > 1) {
-        Comm* c = nullptr;
-        if (comm_create(uid, rank, nranks, ctx->device, ctx->row, ctx->nsm * 8, &c))
-            return fail(LX_ERR_NCCL, "NCCL communicator: %s", comm_error());
-        ctx->comm = c;
-    }
+    return LX_OK;
+}
+
+// Re-shape the context to the local slab of `rank` and bind the communicator.
+static lx_status attach_comm(lx_ctx* ctx, Comm* c, int rank, int nranks) {
+    int64_t b, e;
+    lx_slab_range(ctx->n[0], rank, nranks, &b, &e);
+    if (ctx->comm) comm_destroy(ctx->comm);
+    ctx->comm = c;
     ctx->i_begin = b;
     ctx->i_end = e;
     ctx->n_loc = (int)(e - b);
@@ -481,14 +479,55 @@ lx_status lx_ctx_set_comm(lx_ctx* ctx, const void* uid, int rank, int nranks) {
     if (ctx->comm) {
         for (int i = 0; i < 2; i++) {
             cudaFree(ctx->Yg[i]);
+            ctx->Yg[i] = nullptr;
             CUDA_TRY(cudaMalloc(&ctx->Yg[i], 3 * ctx->row * sizeof(double)));
         }
         cudaFree(ctx->vg);
+        ctx->vg = nullptr;
         CUDA_TRY(cudaMalloc(&ctx->vg, 3 * ctx->row * sizeof(double)));
         comm_bind(ctx->comm, ctx->Y, ctx->Yg, ctx->vg, ctx->n_loc, rank, nranks);
     }
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     return LX_OK;
+}
+
+lx_status lx_ctx_set_comm(lx_ctx* ctx, const void* uid, int rank, int nranks) {
+    if (!ctx || !uid) return fail(LX_ERR_ARG, "NULL");
+    LX_TRY(check_slabs(ctx, rank, nranks));
+    cudaStreamSynchronize(ctx->stream);
+    Comm* c = nullptr;
+    if (nranks > 1 && comm_create(uid, rank, nranks, ctx->device, ctx->row, ctx->nsm * 8, &c))
+        return fail(LX_ERR_NCCL, "NCCL communicator: %s", comm_error());
+    return attach_comm(ctx, c, rank, nranks);
+}
+
+struct lx_local_group {
+    LocalGroup* g;
+    int nranks;
+};
+
+lx_status lx_local_group_create(int nranks, lx_local_group** out) {
+    if (nranks < 1 || nranks > 64 || !out) return fail(LX_ERR_ARG, "bad nranks");
+    *out = new lx_local_group{local_group_create(nranks), nranks};
+    return LX_OK;
+}
+
+lx_status lx_local_group_destroy(lx_local_group* g) {
+    if (g) {
+        local_group_destroy(g->g);
+        delete g;
+    }
+    return LX_OK;
+}
+
+lx_status lx_ctx_set_comm_local(lx_ctx* ctx, lx_local_group* g, int rank) {
+    if (!ctx || !g) return fail(LX_ERR_ARG, "NULL");
+    LX_TRY(check_slabs(ctx, rank, g->nranks));
+    cudaStreamSynchronize(ctx->stream);
+    Comm* c = nullptr;
+    if (g->nranks > 1 && comm_create_local(g->g, rank, ctx->device, ctx->row, &c))
+        return fail(LX_ERR_NCCL, "local communicator: %s", comm_error());
+    return attach_comm(ctx, c, rank, g->nranks);
 }
 
 lx_status lx_ctx_local(const lx_ctx* ctx, int64_t* i_begin, int64_t* i_end, int64_t* n_local) {

@@ -39,6 +39,7 @@ struct Ctrl {
     unsigned int ticket;  // last-block ticket for non-persistent reductions
     unsigned int pad2;
     unsigned long long umax;  // max reduction (bit pattern of a non-negative double)
+    int hist[2];          // step mode: active mask after iteration j stored at hist[j & 1]
 };
 
 // Rows of a slab: rows [0, n_loc) at base, row r in {-1, n_loc, n_loc+1}
@@ -87,6 +88,10 @@ struct LejaParams {
     Record* rec;
     int grid;
     int timeout_spins;
+    // step (multi-rank) mode: per-rank partial and the gathered [nranks][kSlot] partials
+    double* rank_part;
+    const double* gathered;
+    int nranks;
 };
 
 // launchers (lx_kernels.cu)
@@ -108,6 +113,7 @@ struct StageArgs {
     Ctrl* ctrl;
     Record* rec;
     int grid;
+    double* rank_part;    // multi-rank: norm partial goes here instead of rec->err
 };
 
 enum StageOp {
@@ -124,6 +130,12 @@ enum StageOp {
 cudaError_t launch_stage(int op, const StageArgs& A, cudaStream_t s);
 cudaError_t launch_rhs(const LejaParams& P, double scale, cudaStream_t s);
 cudaError_t launch_fill_start(double* v, long long n, bool add_e0, cudaStream_t s);
+// step mode (one launch per iteration; decision for m-1 in the prologue from P.gathered)
+cudaError_t launch_leja_step(const LejaParams& P, int m, cudaStream_t s, bool diag);
+cudaError_t launch_power_step(const LejaParams& P, int m, cudaStream_t s, bool diag);
+int step_grid_size(int device, int nunits);
+cudaError_t launch_finalize_err(const double* gathered, int nranks, double N, Record* rec, cudaStream_t s);
+cudaError_t launch_max_u64(const unsigned long long* vals, int n, unsigned long long* out, cudaStream_t s);
 int stage_grid_size(int device);
 
 }  // namespace lx

@@ -206,6 +206,73 @@ __device__ __forceinline__ void tile2d(const LejaParams& P, const RowSrc& src, d
 }
 
 // ---------------------------------------------------------------------------
+// Stopping decision of P:155 for iteration m (shared by the persistent and the
+// step kernels).  sums = {S_y, S_p^(0..K-1)} over the whole (global) grid.
+// rec != nullptr: the single writer updates margins / per-accumulator iters.
+// ---------------------------------------------------------------------------
+template <int K>
+__device__ __forceinline__ void leja_decide(const LejaParams& P, int m, const double* sums, const double* dm,
+                                            int& act, int& done, int& status, Record* rec) {
+    const double N = P.N_glob;
+    const double ny = sqrt(sums[0] / N);
+    int nact = 0;
+    done = 0;
+    status = 0;
+    for (int k = 0; k < K; k++) {
+        if (!((act >> k) & 1)) continue;
+        const double err = fabs(dm[k]) * ny;
+        const double thr = P.rtol * sqrt(sums[1 + k] / N) + P.atol;
+        if (!isfinite(err) || !isfinite(thr)) {
+            status = 6;  // LX_ERR_NONFINITE
+            break;
+        }
+        if (err <= thr) {
+            act &= ~(1 << k);
+            if (rec) {
+                rec->iters_k[k] = m;
+                const double r = err > 0.0 ? thr / err : INFINITY;
+                if (r < rec->margin_accept) rec->margin_accept = r;
+            }
+        } else {
+            nact++;
+            if (rec) {
+                const double r = err / thr;
+                if (r < rec->margin_reject) rec->margin_reject = r;
+            }
+        }
+    }
+    if (status) done = 1;
+    else if (nact == 0) done = 1;
+    else if (m >= P.max_nodes - 1) { done = 1; status = 5; }  // LX_ERR_NOCONV
+    if (done && rec) {
+        rec->iters += m;
+        rec->ncalls += 1;
+        if (rec->status == 0) rec->status = status;
+    }
+}
+
+// Power iteration: estimate ||w_m|| / ||v_{m-1}|| and the scale of v_m = w_m/||w_m||.
+__device__ __forceinline__ void power_decide(const LejaParams& P, int m, double sumsq, int& done, int& status,
+                                             double* est_out, double* scale_out, Record* rec) {
+    const double N = P.N_glob;
+    const double nw = sqrt(sumsq / N);
+    const double nv = (m == 1) ? sqrt((N + 3.0) / N) : 1.0;
+    const double est = nw / nv;
+    *est_out = est;
+    *scale_out = 1.0 / nw;
+    done = 0;
+    status = 0;
+    if (!isfinite(nw) || nw == 0.0) { done = 1; status = 6; }
+    if (m >= P.power_iters) done = 1;
+    if (done && rec) {
+        rec->est = est;
+        rec->iters += m;
+        rec->ncalls += 1;
+        if (rec->status == 0) rec->status = status;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Grid barrier with the convergence decision taken by the last arriver.
 // Returns (in smem) done / active for the next iteration.
 // ---------------------------------------------------------------------------
@@ -237,45 +304,10 @@ __device__ __forceinline__ void barrier_decide(const LejaParams& P, int m, unsig
         if (tid == 0) {
             Record* rec = P.rec;
             int done = 0, status = 0, act = active;
-            const double N = P.N_glob;
             if (MODE == M_LEJA) {
-                const double ny = sqrt(acc[0] / N);
-                int nact = 0;
-                for (int k = 0; k < K; k++) {
-                    if (!((act >> k) & 1)) continue;
-                    const double err = fabs(dm[k]) * ny;
-                    const double thr = P.rtol * sqrt(acc[1 + k] / N) + P.atol;
-                    if (!isfinite(err) || !isfinite(thr)) {
-                        status = 6;  // LX_ERR_NONFINITE
-                        break;
-                    }
-                    if (err <= thr) {
-                        act &= ~(1 << k);
-                        rec->iters_k[k] = m;
-                        const double r = err > 0.0 ? thr / err : INFINITY;
-                        if (r < rec->margin_accept) rec->margin_accept = r;
-                    } else {
-                        nact++;
-                        const double r = err / thr;
-                        if (r < rec->margin_reject) rec->margin_reject = r;
-                    }
-                }
-                if (status) done = 1;
-                else if (nact == 0) done = 1;
-                else if (m >= P.max_nodes - 1) { done = 1; status = 5; }  // LX_ERR_NOCONV
+                leja_decide<K>(P, m, acc, dm, act, done, status, rec);
             } else {  // M_POWER
-                const double nw = sqrt(acc[0] / N);
-                const double nv = (m == 1) ? sqrt((N + 3.0) / N) : 1.0;
-                ctrl->est = nw / nv;
-                ctrl->scale = 1.0 / nw;
-                if (!isfinite(nw) || nw == 0.0) { done = 1; status = 6; }
-                if (m >= P.power_iters) done = 1;
-                if (done) rec->est = ctrl->est;
-            }
-            if (done) {
-                rec->iters += m;
-                rec->ncalls += 1;
-                if (rec->status == 0) rec->status = status;
+                power_decide(P, m, acc[0], done, status, &ctrl->est, &ctrl->scale, rec);
             }
             ctrl->done = done;
             ctrl->active = act;
@@ -382,6 +414,155 @@ __global__ void __launch_bounds__(kThreads) k_power2d(const __grid_constant__ Le
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Step mode (multi-rank slab decomposition): one launch per iteration m.
+// Prologue: decision of iteration m-1 from the per-rank partials gathered by
+// the transport (summed in rank order -> identical decision on every rank);
+// body: tiles of iteration m; epilogue: CTA partials -> rank partial (fixed
+// order, last-block ticket).  Speculative launches after convergence exit at
+// entry (ctrl->done), so the host may enqueue iterations in chunks.
+// ---------------------------------------------------------------------------
+template <int NV>
+__device__ __forceinline__ void rank_reduce(const LejaParams& P, double (&vals)[NV], double (*s_red)[kSlot],
+                                            int* s_last) {
+    block_reduce<NV>(vals, s_red);
+    if (threadIdx.x == 0) {
+        double* slot = P.partials + (size_t)blockIdx.x * kSlot;
+#pragma unroll
+        for (int i = 0; i < NV; i++) slot[i] = vals[i];
+        __threadfence();
+        const unsigned t = atomicAdd(&P.ctrl->ticket, 1u);
+        *s_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (*s_last) {
+        __threadfence();
+        double acc[NV];
+#pragma unroll
+        for (int i = 0; i < NV; i++) acc[i] = 0.0;
+        for (int c = threadIdx.x; c < (int)gridDim.x; c += kThreads) {
+#pragma unroll
+            for (int i = 0; i < NV; i++) acc[i] += __ldcg(P.partials + (size_t)c * kSlot + i);
+        }
+        block_reduce<NV>(acc, s_red);
+        if (threadIdx.x == 0) {
+#pragma unroll
+            for (int i = 0; i < NV; i++) P.rank_part[i] = acc[i];
+            P.ctrl->ticket = 0u;
+        }
+    }
+}
+
+template <int K, bool DIAG>
+__global__ void __launch_bounds__(kThreads) k_leja2d_step(const __grid_constant__ LejaParams P, int m) {
+    __shared__ double s_red[kWarps][kSlot];
+    __shared__ int s_last;
+    Ctrl* ctrl = P.ctrl;
+    if (*(volatile int*)&ctrl->done) return;
+    const bool writer = blockIdx.x == 0 && threadIdx.x == 0;
+    int active = P.active0;
+    if (m >= 2) {
+        const int prev = *(volatile int*)&ctrl->hist[m & 1];   // mask after iteration m-2
+        double sums[1 + K];
+#pragma unroll
+        for (int i = 0; i < 1 + K; i++) {
+            double s = 0.0;
+            for (int r = 0; r < P.nranks; r++) s += P.gathered[r * kSlot + i];
+            sums[i] = s;
+        }
+        double dmp[K];
+#pragma unroll
+        for (int k = 0; k < K; k++) dmp[k] = P.coef[(size_t)(m - 1) * (1 + K) + 1 + k];
+        int act = prev, done = 0, status = 0;
+        leja_decide<K>(P, m - 1, sums, dmp, act, done, status, writer ? P.rec : nullptr);
+        if (writer) {
+            ctrl->hist[(m - 1) & 1] = act;
+            if (done) {
+                ctrl->status = status;
+                ctrl->m = m - 1;
+                ctrl->done = 1;
+            }
+        }
+        if (done) return;
+        active = act;
+    }
+    if (m >= P.max_nodes) return;   // decision-only launch
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double* cm = P.coef + (size_t)m * (1 + K);
+    const double beta = cm[0];
+    double dm[K], d0[K], sp[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        dm[k] = cm[1 + k];
+        d0[k] = P.coef[1 + k];
+        sp[k] = 0.0;
+    }
+    double sy = 0.0;
+    double* dst = P.ydst[m & 1];
+    if (m == 1) {
+        for (int unit = blockIdx.x * kWarps + warp; unit < P.nunits; unit += gridDim.x * kWarps)
+            tile2d<K, DIAG, true, M_LEJA, true>(P, P.v, dst, unit, lane, beta, d0, dm, active, 0.0, sy, sp);
+    } else {
+        const RowSrc src = P.ysrc[(m - 1) & 1];
+        for (int unit = blockIdx.x * kWarps + warp; unit < P.nunits; unit += gridDim.x * kWarps)
+            tile2d<K, DIAG, false, M_LEJA, false>(P, src, dst, unit, lane, beta, d0, dm, active, 0.0, sy, sp);
+    }
+    double vals[1 + K];
+    vals[0] = sy;
+#pragma unroll
+    for (int k = 0; k < K; k++) vals[1 + k] = sp[k];
+    rank_reduce<1 + K>(P, vals, s_red, &s_last);
+}
+
+template <bool DIAG>
+__global__ void __launch_bounds__(kThreads) k_power2d_step(const __grid_constant__ LejaParams P, int m) {
+    __shared__ double s_red[kWarps][kSlot];
+    __shared__ int s_last;
+    Ctrl* ctrl = P.ctrl;
+    if (*(volatile int*)&ctrl->done) return;
+    const bool writer = blockIdx.x == 0 && threadIdx.x == 0;
+    double scale = 1.0;
+    if (m >= 2) {
+        double s = 0.0;
+        for (int r = 0; r < P.nranks; r++) s += P.gathered[r * kSlot];
+        int done = 0, status = 0;
+        double est;
+        power_decide(P, m - 1, s, done, status, &est, &scale, writer ? P.rec : nullptr);
+        if (done) {
+            if (writer) {
+                ctrl->status = status;
+                ctrl->done = 1;
+            }
+            return;
+        }
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double sy = 0.0, sp[1] = {0.0};
+    const RowSrc src = (m == 1) ? P.v : P.ysrc[(m - 1) & 1];
+    double* dst = P.ydst[m & 1];
+    for (int unit = blockIdx.x * kWarps + warp; unit < P.nunits; unit += gridDim.x * kWarps)
+        tile2d<0, DIAG, false, M_POWER, false>(P, src, dst, unit, lane, 0.0, nullptr, nullptr, 0, scale, sy, sp);
+    double vals[1] = {sy};
+    rank_reduce<1>(P, vals, s_red, &s_last);
+}
+
+__global__ void k_finalize_err(const double* gathered, int nranks, double N, Record* rec) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double s = 0.0;
+        for (int r = 0; r < nranks; r++) s += gathered[r * kSlot];
+        rec->err = sqrt(s / N);
+    }
+}
+
+__global__ void k_max_u64(const unsigned long long* vals, int n, unsigned long long* out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        unsigned long long m = 0ull;
+        for (int i = 0; i < n; i++) m = vals[i] > m ? vals[i] : m;
+        *out = m;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Launchers
 // ---------------------------------------------------------------------------
@@ -434,6 +615,53 @@ cudaError_t launch_power_persistent(const LejaParams& P, cudaStream_t s, bool di
     return cudaLaunchCooperativeKernel(kern, dim3(P.grid), dim3(kThreads), args, 0, s);
 }
 
+
+static void* leja_step_ptr(int K, bool diag) {
+    switch (K * 2 + (diag ? 1 : 0)) {
+        case 2: return (void*)k_leja2d_step<1, false>;
+        case 3: return (void*)k_leja2d_step<1, true>;
+        case 4: return (void*)k_leja2d_step<2, false>;
+        case 5: return (void*)k_leja2d_step<2, true>;
+        case 6: return (void*)k_leja2d_step<3, false>;
+        case 7: return (void*)k_leja2d_step<3, true>;
+        case 8: return (void*)k_leja2d_step<4, false>;
+        case 9: return (void*)k_leja2d_step<4, true>;
+    }
+    return nullptr;
+}
+
+int step_grid_size(int device, int nunits) {
+    int nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    long long g = (long long)nsm * 2;
+    long long need = (nunits + kWarps - 1) / kWarps;
+    if (g > need) g = need > 0 ? need : 1;
+    return (int)g;
+}
+
+cudaError_t launch_leja_step(const LejaParams& P, int m, cudaStream_t s, bool diag) {
+    void* kern = leja_step_ptr(P.K, diag);
+    if (!kern) return cudaErrorInvalidValue;
+    void* args[] = {(void*)&P, (void*)&m};
+    return cudaLaunchKernel(kern, dim3(P.grid), dim3(kThreads), args, 0, s);
+}
+
+cudaError_t launch_power_step(const LejaParams& P, int m, cudaStream_t s, bool diag) {
+    void* kern = diag ? (void*)k_power2d_step<true> : (void*)k_power2d_step<false>;
+    void* args[] = {(void*)&P, (void*)&m};
+    return cudaLaunchKernel(kern, dim3(P.grid), dim3(kThreads), args, 0, s);
+}
+
+cudaError_t launch_finalize_err(const double* gathered, int nranks, double N, Record* rec, cudaStream_t s) {
+    k_finalize_err<<<1, 32, 0, s>>>(gathered, nranks, N, rec);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_max_u64(const unsigned long long* vals, int n, unsigned long long* out, cudaStream_t s) {
+    k_max_u64<<<1, 32, 0, s>>>(vals, n, out);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // Stage kernels
 // ---------------------------------------------------------------------------
@@ -462,7 +690,8 @@ __device__ __forceinline__ void stage_reduce_err(const StageArgs& A, double v, d
         for (int c = threadIdx.x; c < (int)gridDim.x; c += kThreads) acc[0] += __ldcg(A.partials + c * kSlot);
         block_reduce<1>(acc, s_red);
         if (threadIdx.x == 0) {
-            A.rec->err = sqrt(acc[0] / A.N_glob);
+            if (A.rank_part) A.rank_part[0] = acc[0];   // multi-rank: finalised after the allgather
+            else A.rec->err = sqrt(acc[0] / A.N_glob);
             A.ctrl->ticket = 0u;
         }
     }
