@@ -174,13 +174,22 @@ def run_ours(args):
         raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
     torch.cuda.set_device(local)
     n = args.n or 4096
-    if ws > 1:
-        raise SystemExit("multi-GPU bench path requires the NCCL slab build (not in this version)")
     wl = W.config(1, n=n)
-    pb = lx.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
+    if ws > 1:
+        import torch.distributed as dist
+        from paper_2310_08344_b200 import dist as lxd
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # weak scaling: a (n*ws) x n grid at the SAME spacing, Problem-I IC replicated per
+        # slab (x-periodic images) -> every rank does exactly the N=1 work + halos/gathers
+        pb = lx.Problem((n * ws, n), wl.dx, wl.diff, wl.nu, wl.react)
+    else:
+        pb = lx.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx = lx.Context(pb, stream=stream)
+    if ws > 1:
+        b, e = lxd.attach(ctx)
+        assert e - b == n, (b, e)
     u0_h = W.ic_problem1_2d(n)
     u0 = torch.from_numpy(u0_h).cuda()
     outs = [torch.empty_like(u0) for _ in range(4)]
@@ -205,6 +214,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
+        torch.cuda.synchronize()
 
     evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in range(4)]
            for _ in range(args.steps)]
@@ -212,16 +222,23 @@ def run_ours(args):
     launches0 = ctx.launch_count
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+            torch.cuda.synchronize()
         start.record(stream)
         for s in range(args.steps):
             step(evs[s])
         stop.record(stream)
         torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
     launches = ctx.launch_count - launches0
     total_iters, _ = ctx.synchronize()
     ms = start.elapsed_time(stop)
+    if ws > 1:
+        ms = lxd.max_over_ranks(ms, device=u0.device)
     assert total_iters == args.steps * sum(iters), (total_iters, iters)
-    value = total_iters / (ms * 1e-3)
+    value = ws * total_iters / (ms * 1e-3)   # 4096^2-equivalent Leja iterations of all ranks
 
     # roofline of the dominant kernel (persistent Leja kernel, one launch per call)
     durs = np.array([[evs[s][l][0].elapsed_time(evs[s][l][1]) for l in range(4)] for s in range(args.steps)])
@@ -260,16 +277,19 @@ def run_ours(args):
         e_it += step_host()
     torch.cuda.synchronize()
     e_t = time.perf_counter() - t0
-    e2e = {"value": e_it / e_t, "unit": UNIT, "h2d_bytes_per_step": 4 * N * 8, "d2h_bytes_per_step": 4 * N * 8,
+    if ws > 1:
+        e_t = lxd.max_over_ranks(e_t, device=u0.device)
+    e2e = {"value": ws * e_it / e_t, "unit": UNIT, "h2d_bytes_per_step": 4 * N * 8, "d2h_bytes_per_step": 4 * N * 8,
            "steps": e2e_steps, "note": "4 lx_real_leja_phi calls with pinned host in/out pointers per step"}
 
     cpu = None
     if rank == 0 and not args.no_cpu:
         cpu = cpu_baseline(n, args.ref_iters)
-    cfg = {"workload": wl.name, "grid": list(wl.shape), "ls": [0, 1, 2, 3], "dt_cfl_mult": 10.0, "dt": wl.dt,
+    cfg = {"workload": wl.name, "grid": list(pb.shape), "per_rank_grid": [n, n], "ls": [0, 1, 2, 3], "dt_cfl_mult": 10.0, "dt": wl.dt,
            "tol": 1e-10, "leja_iters_per_call": iters, "leja_iters_per_step": sum(iters),
            "l2_policy": "inputs larger than L2 (each fp64 vector %.0f MB > 126 MB L2)" % (N * 8 / 1e6),
-           "inputs": "synthetic Problem-I Gaussian IC (P:562), nu=10", "parallelism": "single GPU"}
+           "inputs": "synthetic Problem-I Gaussian IC (P:562), nu=10" + (" replicated per slab" if ws > 1 else ""),
+           "parallelism": ("slab%d (NCCL halos + partial allgather per Leja iteration)" % ws) if ws > 1 else "single GPU"}
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg, "roofline": roof,
@@ -277,6 +297,9 @@ def run_ours(args):
     if rank == 0:
         print(json.dumps(out), flush=True)
     ctx.close()
+    if ws > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
 
 
 def main():

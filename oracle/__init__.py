@@ -59,6 +59,7 @@ def lib():
         L.oc_rhs.argtypes = [pp, dp, dp]
         L.oc_jac_apply.argtypes = [pp, dp, dp, dp]
         L.oc_nonlinear_remainder.argtypes = [pp, dp, dp, dp]
+        L.oc_jac_apply_slab.argtypes = [pp, ctypes.c_long, dp, dp, dp]
         L.oc_spectrum_bound.restype = ctypes.c_double
         L.oc_spectrum_bound.argtypes = [pp, dp]
         L.oc_power_iteration.restype = ctypes.c_double
@@ -156,6 +157,17 @@ def jac_apply(pb: Problem, u, y) -> np.ndarray:
     w = np.zeros_like(y)
     lib().oc_jac_apply(ctypes.byref(pb.c_struct()), _dp(u), _dp(y), _dp(w))
     return w
+
+
+def jac_apply_slab(pb: Problem, n_loc: int, u_loc, y_ghosted) -> np.ndarray:
+    """J(u) y on a slab: y_ghosted has rows -1..n_loc+1 (1 ghost before, 2 after)."""
+    row = int(np.prod(pb.shape[1:]))
+    y = np.ascontiguousarray(y_ghosted, dtype=np.float64)
+    assert y.size == (n_loc + 3) * row
+    u = None if u_loc is None else np.ascontiguousarray(u_loc, dtype=np.float64)
+    w = np.zeros(n_loc * row)
+    lib().oc_jac_apply_slab(ctypes.byref(pb.c_struct()), int(n_loc), _dp(u), _dp(y), _dp(w))
+    return w.reshape((n_loc,) + tuple(pb.shape[1:]))
 
 
 def nonlinear_remainder(pb: Problem, u, x) -> np.ndarray:

@@ -240,6 +240,37 @@ static void apply_linear(const oc_problem *pb, const double *y, double *w)
             }
 }
 
+/* Slab form of J(u) y for the emulated slab decomposition:
+ * y_gh holds rows -1 .. n_loc+1 of dimension 0 (one ghost row before, two after,
+ * filled by the caller from the neighbouring slabs); w (rows 0..n_loc-1) gets
+ * J(u) y with NO wrap along dimension 0 (the ghost rows replace it) and periodic
+ * wrap along the other dimensions.  u: local rows only (NULL if react == 0). */
+void oc_jac_apply_slab(const oc_problem *pb, long n_loc, const double *u, const double *y_gh, double *w)
+{
+    long n1 = pb->n[1], n2 = pb->ndim == 3 ? pb->n[2] : 1;
+    long row = n1 * n2;
+    for (long i0 = 0; i0 < n_loc; i0++)
+        for (long i1 = 0; i1 < n1; i1++)
+            for (long i2 = 0; i2 < n2; i2++) {
+                double lap = 0.0, adv = 0.0;
+                for (int d = 0; d < pb->ndim; d++) {
+                    double h = pb->dx[d], v[4];
+                    for (int o = -1; o <= 2; o++) {
+                        long a0 = i0, a1 = i1, a2 = i2;
+                        if (d == 0) a0 += o;
+                        if (d == 1) a1 = wrap(i1 + o, n1);
+                        if (d == 2) a2 = wrap(i2 + o, n2);
+                        v[o + 1] = y_gh[(a0 + 1) * row + a1 * n2 + a2];
+                    }
+                    lap += (v[2] - 2.0 * v[1] + v[0]) / (h * h);
+                    adv += (-v[3] + 6.0 * v[2] - 3.0 * v[1] - 2.0 * v[0]) / (6.0 * h);
+                }
+                long idx = i0 * row + i1 * n2 + i2;
+                w[idx] = pb->diff * lap + pb->nu * adv;
+                if (pb->react != 0.0) w[idx] += pb->react * (1.0 - 3.0 * u[idx] * u[idx]) * y_gh[row + idx];
+            }
+}
+
 /* f(u) (Eq. (1); problems P:559; R16) */
 void oc_rhs(const oc_problem *pb, const double *u, double *f)
 {

@@ -1,0 +1,71 @@
+"""Multi-process plumbing of the slab decomposition (one process per GPU).
+
+torch.distributed is used only for bootstrap and timing: the NCCL unique id of
+the library's own communicator is broadcast with ``broadcast_object_list``,
+timings are reduced with MAX.  The per-iteration halo exchange and the partial
+gather run inside liblexint_b200.so (csrc/lx_comm.cpp) on the context stream.
+
+``halo_plan`` states the exchange protocol of csrc/lx_comm.cpp in host terms
+(which rows go to which peer, in which order); the CPU gloo tests drive an
+oracle-based emulation of the slab path with it.
+"""
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+
+from . import Context, lx_nccl_unique_id, lx_slab_range
+
+
+def env():
+    """(rank, world_size, local_rank) from the torchrun environment."""
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def share_unique_id() -> bytes:
+    """Rank 0 creates the NCCL unique id; every rank returns the same 128 bytes."""
+    import torch.distributed as dist
+    obj = [lx_nccl_unique_id() if dist.get_rank() == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def attach(ctx: Context) -> tuple:
+    """Attach the context to an NCCL communicator spanning the process group.
+    Returns this rank's slab (i_begin, i_end)."""
+    import torch.distributed as dist
+    uid = share_unique_id()
+    ctx.set_comm(uid, dist.get_rank(), dist.get_world_size())
+    b, e, _ = ctx.local()
+    return b, e
+
+
+def max_over_ranks(x: float, device=None) -> float:
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+@dataclass(frozen=True)
+class HaloOp:
+    kind: str        # "send" | "recv"
+    peer: int
+    rows: tuple      # local rows (send) or ghost slots (recv): ghost slot 0 = row -1, 1..2 = rows n, n+1
+
+
+def halo_plan(rank: int, world: int, n_loc: int) -> list:
+    """Ordered point-to-point operations of one halo exchange (csrc/lx_comm.cpp):
+    the +x-biased upwind stencil (reading R10) reaches rows i-1, i+1, i+2, so a
+    slab needs 1 ghost row from rank r-1 and 2 from rank r+1 (periodic in rank)."""
+    up, down = (rank - 1) % world, (rank + 1) % world
+    return [HaloOp("send", up, (0, 1)), HaloOp("recv", down, (1, 2)),
+            HaloOp("send", down, (n_loc - 1,)), HaloOp("recv", up, (0,))]
+
+
+def slabs(n0: int, world: int) -> list:
+    return [lx_slab_range(n0, r, world) for r in range(world)]
