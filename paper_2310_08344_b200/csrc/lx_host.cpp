@@ -122,7 +122,6 @@ static lx_status check_problem(const lx_ctx* ctx, const lx_problem* pb) {
         if (pb->n[d] != ctx->n[d]) return fail(LX_ERR_DIM, "problem n[%d] differs from the context grid", d);
     for (int d = 0; d < pb->ndim; d++)
         if (!(pb->dx[d] > 0.0)) return fail(LX_ERR_ARG, "dx[%d] must be > 0", d);
-    if (pb->ndim != 2) return fail(LX_ERR_UNSUPPORTED, "only ndim = 2 is implemented on the device");
     return LX_OK;
 }
 
@@ -227,10 +226,15 @@ static LejaParams base_params(lx_ctx* ctx, const lx_problem* pb) {
     P.ndim = ctx->ndim;
     P.n_loc = ctx->n_loc;
     P.n1 = (int)ctx->n[1];
-    P.n2 = 1;
-    P.nb = (P.n1 + 63) / 64;
+    P.n2 = (int)ctx->n[2];
     P.nrb = (P.n_loc + kRT - 1) / kRT;
-    P.nunits = P.nb * P.nrb;
+    if (ctx->ndim == 3) {
+        P.nb = (P.n2 + 63) / 64;                 // 64-wide bands along the contiguous dim 2
+        P.nunits = P.nb * P.n1 * P.nrb;          // u = (plane_block*nb + band)*n1 + j
+    } else {
+        P.nb = (P.n1 + 63) / 64;
+        P.nunits = P.nb * P.nrb;                 // u = row_block*nb + band
+    }
     P.N_glob = ctx->N_glob;
     P.st = make_stencil(pb);
     P.ctrl = ctx->ctrl;
@@ -375,11 +379,13 @@ lx_status lx_ctx_create(const lx_problem* pb, int max_nodes, int device, void* c
     if (!pb || !out) return fail(LX_ERR_ARG, "NULL argument");
     *out = nullptr;
     if (pb->ndim != 2 && pb->ndim != 3) return fail(LX_ERR_UNSUPPORTED, "ndim must be 2 or 3");
-    if (pb->ndim == 3) return fail(LX_ERR_UNSUPPORTED, "3D device kernels not built in this version");
     for (int d = 0; d < pb->ndim; d++)
         if (pb->n[d] < 4) return fail(LX_ERR_DIM, "n[%d] = %lld < 4", d, (long long)pb->n[d]);
     if (pb->n[pb->ndim - 1] % 2) return fail(LX_ERR_DIM, "the contiguous dimension must be even (double2 access)");
-    if (pb->n[0] > (1 << 30) || pb->n[1] > (1 << 30)) return fail(LX_ERR_DIM, "grid too large");
+    if (pb->n[0] > (1 << 30) || pb->n[1] > (1 << 30) || (pb->ndim == 3 && pb->n[2] > (1 << 30)))
+        return fail(LX_ERR_DIM, "grid too large");
+    if (pb->ndim == 3 && (double)pb->n[1] * (double)((pb->n[2] + 63) / 64) * (double)((pb->n[0] + 3) / 4) > 2e9)
+        return fail(LX_ERR_DIM, "grid too large for the 32-bit work-unit index");
     if (max_nodes == 0) max_nodes = 300;
     if (max_nodes < 2 || max_nodes > 1024) return fail(LX_ERR_ARG, "max_nodes must be in [2, 1024]");
     lx_ctx* ctx = new lx_ctx();

@@ -205,6 +205,164 @@ __device__ __forceinline__ void tile2d(const LejaParams& P, const RowSrc& src, d
     }
 }
 
+
+// One warp work unit of the 3D stencil: 64 contiguous k (dim 2) x one j row (dim 1)
+// x kRT planes (dim 0).  i-neighbours from the plane window, j-neighbours from
+// rows j-1, j+1, j+2 of the same plane (adjacent warps own adjacent j -> L1 hits),
+// k-neighbours by shuffles + edge-lane halo loads.  Units: u = (pb*nb + b)*n1 + j.
+template <int K, bool DIAG, bool FIRST, int MODE, bool RO>
+__device__ __forceinline__ void tile3d(const LejaParams& P, const RowSrc& src, double* __restrict__ dst,
+                                       int unit, int lane, double beta, const double* d0, const double* dm,
+                                       int active, double scale, double& sy, double* sp) {
+    const int n1 = P.n1, n2 = P.n2;
+    const int j = unit % n1;
+    const int t0 = unit / n1;
+    const int b = t0 % P.nb;
+    const int pb = t0 / P.nb;
+    const int k0 = b * 64 + 2 * lane;
+    const bool valid = k0 < n2;
+    const int last = min(31, ((n2 - b * 64) >> 1) - 1);
+    const int i0 = pb * kRT;
+    const int nout = min(kRT, P.n_loc - i0);
+    const int jm = (j == 0) ? n1 - 1 : j - 1;
+    const int jp1 = (j + 1 >= n1) ? j + 1 - n1 : j + 1;
+    const int jp2 = (j + 2 >= n1) ? j + 2 - n1 : j + 2;
+    const Stencil& S = P.st;
+    auto LD2 = [&](const double* q) { return RO ? ldg2(q) : ld2(q); };
+
+    double2 w[kRT + 3];
+#pragma unroll
+    for (int t = 0; t < kRT + 3; t++) {
+        w[t] = make_double2(0.0, 0.0);
+        if (valid && t < nout + 3) w[t] = LD2(rowp(src, i0 - 1 + t) + (long long)j * n2 + k0);
+    }
+    double2 wm[kRT], wp1[kRT], wp2[kRT];
+    double hl[kRT];
+    double2 hr[kRT];
+#pragma unroll
+    for (int t = 0; t < kRT; t++) {
+        wm[t] = wp1[t] = wp2[t] = hr[t] = make_double2(0.0, 0.0);
+        hl[t] = 0.0;
+        if (t < nout) {
+            const double* pl = rowp(src, i0 + t);
+            if (valid) {
+                wm[t] = LD2(pl + (long long)jm * n2 + k0);
+                wp1[t] = LD2(pl + (long long)jp1 * n2 + k0);
+                wp2[t] = LD2(pl + (long long)jp2 * n2 + k0);
+            }
+            const double* rp = pl + (long long)j * n2;
+            if (lane == 0) {
+                const int kl = (k0 == 0) ? n2 - 1 : k0 - 1;
+                hl[t] = RO ? __ldg(rp + kl) : rp[kl];
+            }
+            if (lane == last) {
+                int kr = k0 + 2;
+                if (kr >= n2) kr -= n2;
+                hr[t] = LD2(rp + kr);
+            }
+        }
+    }
+    constexpr int KK = K > 0 ? K : 1;
+    double2 pv[kRT][KK];
+    double2 uu[kRT];
+#pragma unroll
+    for (int t = 0; t < kRT; t++) {
+        const long long off = ((long long)(i0 + t) * n1 + j) * n2 + k0;
+        if (MODE == M_LEJA && !FIRST) {
+#pragma unroll
+            for (int k = 0; k < KK; k++) {
+                pv[t][k] = make_double2(0.0, 0.0);
+                if (valid && t < nout && ((active >> k) & 1)) pv[t][k] = ld2(P.p[k] + off);
+            }
+        }
+        uu[t] = make_double2(0.0, 0.0);
+        if (DIAG && valid && t < nout) uu[t] = ldg2(P.u + off);
+    }
+#pragma unroll
+    for (int t = 0; t < kRT; t++) {
+        if (t < nout) {
+            const double2 yc = w[t + 1], up = w[t], dn1 = w[t + 2], dn2 = w[t + 3];
+            double left = __shfl_up_sync(FULL_MASK, yc.y, 1);
+            double r1 = __shfl_down_sync(FULL_MASK, yc.x, 1);
+            double r2 = __shfl_down_sync(FULL_MASK, yc.y, 1);
+            if (lane == 0) left = hl[t];
+            if (lane == last) {
+                r1 = hr[t].x;
+                r2 = hr[t].y;
+            }
+            double ax = S.c0 * yc.x;
+            ax = fma(S.m1[0], up.x, ax);
+            ax = fma(S.p1[0], dn1.x, ax);
+            ax = fma(S.p2[0], dn2.x, ax);
+            ax = fma(S.m1[1], wm[t].x, ax);
+            ax = fma(S.p1[1], wp1[t].x, ax);
+            ax = fma(S.p2[1], wp2[t].x, ax);
+            ax = fma(S.m1[2], left, ax);
+            ax = fma(S.p1[2], yc.y, ax);
+            ax = fma(S.p2[2], r1, ax);
+            double ay = S.c0 * yc.y;
+            ay = fma(S.m1[0], up.y, ay);
+            ay = fma(S.p1[0], dn1.y, ay);
+            ay = fma(S.p2[0], dn2.y, ay);
+            ay = fma(S.m1[1], wm[t].y, ay);
+            ay = fma(S.p1[1], wp1[t].y, ay);
+            ay = fma(S.p2[1], wp2[t].y, ay);
+            ay = fma(S.m1[2], yc.x, ay);
+            ay = fma(S.p1[2], r1, ay);
+            ay = fma(S.p2[2], r2, ay);
+            if (DIAG) {
+                ax = fma(fma(S.qb, uu[t].x * uu[t].x, S.qa), yc.x, ax);
+                ay = fma(fma(S.qb, uu[t].y * uu[t].y, S.qa), yc.y, ay);
+            }
+            double2 yn;
+            if (MODE == M_POWER) {
+                yn.x = scale * ax;
+                yn.y = scale * ay;
+            } else if (MODE == M_RHS) {
+                yn.x = scale * fma(S.react, yc.x - yc.x * yc.x * yc.x, ax);
+                yn.y = scale * fma(S.react, yc.y - yc.y * yc.y * yc.y, ay);
+            } else {
+                yn.x = fma(P.alpha, ax, beta * yc.x);
+                yn.y = fma(P.alpha, ay, beta * yc.y);
+            }
+            if (valid) {
+                const long long off = ((long long)(i0 + t) * n1 + j) * n2 + k0;
+                st2(dst + off, yn);
+                sy = fma(yn.x, yn.x, sy);
+                sy = fma(yn.y, yn.y, sy);
+                if (MODE == M_LEJA) {
+#pragma unroll
+                    for (int k = 0; k < KK; k++) {
+                        if ((active >> k) & 1) {
+                            double2 pn;
+                            if (FIRST) {
+                                pn.x = fma(dm[k], yn.x, d0[k] * yc.x);
+                                pn.y = fma(dm[k], yn.y, d0[k] * yc.y);
+                            } else {
+                                pn.x = fma(dm[k], yn.x, pv[t][k].x);
+                                pn.y = fma(dm[k], yn.y, pv[t][k].y);
+                            }
+                            st2(P.p[k] + off, pn);
+                            sp[k] = fma(pn.x, pn.x, sp[k]);
+                            sp[k] = fma(pn.y, pn.y, sp[k]);
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
+template <int NDIM, int K, bool DIAG, bool FIRST, int MODE, bool RO>
+__device__ __forceinline__ void tile(const LejaParams& P, const RowSrc& src, double* __restrict__ dst, int unit,
+                                     int lane, double beta, const double* d0, const double* dm, int active,
+                                     double scale, double& sy, double* sp) {
+    if (NDIM == 2)
+        tile2d<K, DIAG, FIRST, MODE, RO>(P, src, dst, unit, lane, beta, d0, dm, active, scale, sy, sp);
+    else
+        tile3d<K, DIAG, FIRST, MODE, RO>(P, src, dst, unit, lane, beta, d0, dm, active, scale, sy, sp);
+}
+
 // ---------------------------------------------------------------------------
 // Stopping decision of P:155 for iteration m (shared by the persistent and the
 // step kernels).  sums = {S_y, S_p^(0..K-1)} over the whole (global) grid.
@@ -343,7 +501,7 @@ __device__ __forceinline__ void barrier_decide(const LejaParams& P, int m, unsig
     __syncthreads();
 }
 
-template <int K, bool DIAG>
+template <int NDIM, int K, bool DIAG>
 __global__ void __launch_bounds__(kThreads) k_leja2d(const __grid_constant__ LejaParams P) {
     __shared__ double s_red[kWarps][kSlot];
     __shared__ int s_flags[4];
@@ -368,11 +526,11 @@ __global__ void __launch_bounds__(kThreads) k_leja2d(const __grid_constant__ Lej
         double* dst = P.ydst[par];
         if (m == 1) {
             for (int unit = blockIdx.x * kWarps + warp; unit < P.nunits; unit += gridDim.x * kWarps)
-                tile2d<K, DIAG, true, M_LEJA, true>(P, P.v, dst, unit, lane, beta, d0, dm, active, 0.0, sy, sp);
+                tile<NDIM, K, DIAG, true, M_LEJA, true>(P, P.v, dst, unit, lane, beta, d0, dm, active, 0.0, sy, sp);
         } else {
             const RowSrc src = P.ysrc[par ^ 1];
             for (int unit = blockIdx.x * kWarps + warp; unit < P.nunits; unit += gridDim.x * kWarps)
-                tile2d<K, DIAG, false, M_LEJA, false>(P, src, dst, unit, lane, beta, d0, dm, active, 0.0, sy, sp);
+                tile<NDIM, K, DIAG, false, M_LEJA, false>(P, src, dst, unit, lane, beta, d0, dm, active, 0.0, sy, sp);
         }
         double vals[1 + K];
         vals[0] = sy;
@@ -390,7 +548,7 @@ __global__ void __launch_bounds__(kThreads) k_leja2d(const __grid_constant__ Lej
     }
 }
 
-template <bool DIAG>
+template <int NDIM, bool DIAG>
 __global__ void __launch_bounds__(kThreads) k_power2d(const __grid_constant__ LejaParams P) {
     __shared__ double s_red[kWarps][kSlot];
     __shared__ int s_flags[4];
@@ -404,7 +562,7 @@ __global__ void __launch_bounds__(kThreads) k_power2d(const __grid_constant__ Le
         double* dst = P.ydst[par];
         const RowSrc src = (m == 1) ? P.v : P.ysrc[par ^ 1];
         for (int unit = blockIdx.x * kWarps + warp; unit < P.nunits; unit += gridDim.x * kWarps)
-            tile2d<0, DIAG, false, M_POWER, false>(P, src, dst, unit, lane, 0.0, nullptr, nullptr, 0, scale, sy, sp);
+            tile<NDIM, 0, DIAG, false, M_POWER, false>(P, src, dst, unit, lane, 0.0, nullptr, nullptr, 0, scale, sy, sp);
         double vals[1] = {sy};
         block_reduce<1>(vals, s_red);
         if (tid == 0) P.partials[((size_t)par * gridDim.x + blockIdx.x) * kSlot] = vals[0];
@@ -454,7 +612,7 @@ __device__ __forceinline__ void rank_reduce(const LejaParams& P, double (&vals)[
     }
 }
 
-template <int K, bool DIAG>
+template <int NDIM, int K, bool DIAG>
 __global__ void __launch_bounds__(kThreads) k_leja2d_step(const __grid_constant__ LejaParams P, int m) {
     __shared__ double s_red[kWarps][kSlot];
     __shared__ int s_last;
@@ -502,11 +660,11 @@ __global__ void __launch_bounds__(kThreads) k_leja2d_step(const __grid_constant_
     double* dst = P.ydst[m & 1];
     if (m == 1) {
         for (int unit = blockIdx.x * kWarps + warp; unit < P.nunits; unit += gridDim.x * kWarps)
-            tile2d<K, DIAG, true, M_LEJA, true>(P, P.v, dst, unit, lane, beta, d0, dm, active, 0.0, sy, sp);
+            tile<NDIM, K, DIAG, true, M_LEJA, true>(P, P.v, dst, unit, lane, beta, d0, dm, active, 0.0, sy, sp);
     } else {
         const RowSrc src = P.ysrc[(m - 1) & 1];
         for (int unit = blockIdx.x * kWarps + warp; unit < P.nunits; unit += gridDim.x * kWarps)
-            tile2d<K, DIAG, false, M_LEJA, false>(P, src, dst, unit, lane, beta, d0, dm, active, 0.0, sy, sp);
+            tile<NDIM, K, DIAG, false, M_LEJA, false>(P, src, dst, unit, lane, beta, d0, dm, active, 0.0, sy, sp);
     }
     double vals[1 + K];
     vals[0] = sy;
@@ -515,7 +673,7 @@ __global__ void __launch_bounds__(kThreads) k_leja2d_step(const __grid_constant_
     rank_reduce<1 + K>(P, vals, s_red, &s_last);
 }
 
-template <bool DIAG>
+template <int NDIM, bool DIAG>
 __global__ void __launch_bounds__(kThreads) k_power2d_step(const __grid_constant__ LejaParams P, int m) {
     __shared__ double s_red[kWarps][kSlot];
     __shared__ int s_last;
@@ -542,7 +700,7 @@ __global__ void __launch_bounds__(kThreads) k_power2d_step(const __grid_constant
     const RowSrc src = (m == 1) ? P.v : P.ysrc[(m - 1) & 1];
     double* dst = P.ydst[m & 1];
     for (int unit = blockIdx.x * kWarps + warp; unit < P.nunits; unit += gridDim.x * kWarps)
-        tile2d<0, DIAG, false, M_POWER, false>(P, src, dst, unit, lane, 0.0, nullptr, nullptr, 0, scale, sy, sp);
+        tile<NDIM, 0, DIAG, false, M_POWER, false>(P, src, dst, unit, lane, 0.0, nullptr, nullptr, 0, scale, sy, sp);
     double vals[1] = {sy};
     rank_reduce<1>(P, vals, s_red, &s_last);
 }
@@ -574,23 +732,27 @@ static int max_coresident(int device, Kern kern) {
     return nsm * per;
 }
 
-static void* leja_kernel_ptr(int K, bool diag) {
+template <int NDIM>
+static void* leja_kernel_ptr_nd(int K, bool diag) {
     switch (K * 2 + (diag ? 1 : 0)) {
-        case 2: return (void*)k_leja2d<1, false>;
-        case 3: return (void*)k_leja2d<1, true>;
-        case 4: return (void*)k_leja2d<2, false>;
-        case 5: return (void*)k_leja2d<2, true>;
-        case 6: return (void*)k_leja2d<3, false>;
-        case 7: return (void*)k_leja2d<3, true>;
-        case 8: return (void*)k_leja2d<4, false>;
-        case 9: return (void*)k_leja2d<4, true>;
+        case 2: return (void*)k_leja2d<NDIM, 1, false>;
+        case 3: return (void*)k_leja2d<NDIM, 1, true>;
+        case 4: return (void*)k_leja2d<NDIM, 2, false>;
+        case 5: return (void*)k_leja2d<NDIM, 2, true>;
+        case 6: return (void*)k_leja2d<NDIM, 3, false>;
+        case 7: return (void*)k_leja2d<NDIM, 3, true>;
+        case 8: return (void*)k_leja2d<NDIM, 4, false>;
+        case 9: return (void*)k_leja2d<NDIM, 4, true>;
     }
     return nullptr;
 }
 
+static void* leja_kernel_ptr(int ndim, int K, bool diag) {
+    return ndim == 3 ? leja_kernel_ptr_nd<3>(K, diag) : leja_kernel_ptr_nd<2>(K, diag);
+}
+
 int leja_grid_size(int device, int K, bool diag, int ndim, int nunits) {
-    (void)ndim;
-    void* kern = leja_kernel_ptr(K, diag);
+    void* kern = leja_kernel_ptr(ndim, K, diag);
     int nsm = 0, per = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, 0);
@@ -603,31 +765,37 @@ int leja_grid_size(int device, int K, bool diag, int ndim, int nunits) {
 }
 
 cudaError_t launch_leja_persistent(const LejaParams& P, cudaStream_t s, bool diag) {
-    void* kern = leja_kernel_ptr(P.K, diag);
+    void* kern = leja_kernel_ptr(P.ndim, P.K, diag);
     if (!kern) return cudaErrorInvalidValue;
     void* args[] = {(void*)&P};
     return cudaLaunchCooperativeKernel(kern, dim3(P.grid), dim3(kThreads), args, 0, s);
 }
 
 cudaError_t launch_power_persistent(const LejaParams& P, cudaStream_t s, bool diag) {
-    void* kern = diag ? (void*)k_power2d<true> : (void*)k_power2d<false>;
+    void* kern = P.ndim == 3 ? (diag ? (void*)k_power2d<3, true> : (void*)k_power2d<3, false>)
+                             : (diag ? (void*)k_power2d<2, true> : (void*)k_power2d<2, false>);
     void* args[] = {(void*)&P};
     return cudaLaunchCooperativeKernel(kern, dim3(P.grid), dim3(kThreads), args, 0, s);
 }
 
 
-static void* leja_step_ptr(int K, bool diag) {
+template <int NDIM>
+static void* leja_step_ptr_nd(int K, bool diag) {
     switch (K * 2 + (diag ? 1 : 0)) {
-        case 2: return (void*)k_leja2d_step<1, false>;
-        case 3: return (void*)k_leja2d_step<1, true>;
-        case 4: return (void*)k_leja2d_step<2, false>;
-        case 5: return (void*)k_leja2d_step<2, true>;
-        case 6: return (void*)k_leja2d_step<3, false>;
-        case 7: return (void*)k_leja2d_step<3, true>;
-        case 8: return (void*)k_leja2d_step<4, false>;
-        case 9: return (void*)k_leja2d_step<4, true>;
+        case 2: return (void*)k_leja2d_step<NDIM, 1, false>;
+        case 3: return (void*)k_leja2d_step<NDIM, 1, true>;
+        case 4: return (void*)k_leja2d_step<NDIM, 2, false>;
+        case 5: return (void*)k_leja2d_step<NDIM, 2, true>;
+        case 6: return (void*)k_leja2d_step<NDIM, 3, false>;
+        case 7: return (void*)k_leja2d_step<NDIM, 3, true>;
+        case 8: return (void*)k_leja2d_step<NDIM, 4, false>;
+        case 9: return (void*)k_leja2d_step<NDIM, 4, true>;
     }
     return nullptr;
+}
+
+static void* leja_step_ptr(int ndim, int K, bool diag) {
+    return ndim == 3 ? leja_step_ptr_nd<3>(K, diag) : leja_step_ptr_nd<2>(K, diag);
 }
 
 int step_grid_size(int device, int nunits) {
@@ -640,14 +808,15 @@ int step_grid_size(int device, int nunits) {
 }
 
 cudaError_t launch_leja_step(const LejaParams& P, int m, cudaStream_t s, bool diag) {
-    void* kern = leja_step_ptr(P.K, diag);
+    void* kern = leja_step_ptr(P.ndim, P.K, diag);
     if (!kern) return cudaErrorInvalidValue;
     void* args[] = {(void*)&P, (void*)&m};
     return cudaLaunchKernel(kern, dim3(P.grid), dim3(kThreads), args, 0, s);
 }
 
 cudaError_t launch_power_step(const LejaParams& P, int m, cudaStream_t s, bool diag) {
-    void* kern = diag ? (void*)k_power2d_step<true> : (void*)k_power2d_step<false>;
+    void* kern = P.ndim == 3 ? (diag ? (void*)k_power2d_step<3, true> : (void*)k_power2d_step<3, false>)
+                             : (diag ? (void*)k_power2d_step<2, true> : (void*)k_power2d_step<2, false>);
     void* args[] = {(void*)&P, (void*)&m};
     return cudaLaunchKernel(kern, dim3(P.grid), dim3(kThreads), args, 0, s);
 }
@@ -768,11 +937,12 @@ __global__ void __launch_bounds__(kThreads) k_stage_pointwise(const __grid_const
     }
 }
 
+template <int NDIM>
 __global__ void __launch_bounds__(kThreads) k_rhs2d(const __grid_constant__ LejaParams P, double scale) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double sy = 0.0, sp[1] = {0.0};
     for (int unit = blockIdx.x * kWarps + warp; unit < P.nunits; unit += gridDim.x * kWarps)
-        tile2d<0, false, false, M_RHS, true>(P, P.v, P.ydst[0], unit, lane, 0.0, nullptr, nullptr, 0, scale, sy, sp);
+        tile<NDIM, 0, false, false, M_RHS, true>(P, P.v, P.ydst[0], unit, lane, 0.0, nullptr, nullptr, 0, scale, sy, sp);
 }
 
 __global__ void k_fill_start(double* v, long long n, int add_e0) {
@@ -792,7 +962,8 @@ int stage_grid_size(int device) {
 }
 
 cudaError_t launch_rhs(const LejaParams& P, double scale, cudaStream_t s) {
-    k_rhs2d<<<P.grid, kThreads, 0, s>>>(P, scale);
+    if (P.ndim == 3) k_rhs2d<3><<<P.grid, kThreads, 0, s>>>(P, scale);
+    else k_rhs2d<2><<<P.grid, kThreads, 0, s>>>(P, scale);
     return cudaGetLastError();
 }
 

@@ -280,3 +280,57 @@ def test_config1_4096_phi0_full_oracle(xi300):
     r = O.real_leja_phi(ob, u0, wl.dt, c, g, 0, wl.rtol, wl.atol, xi300)
     assert it == r.iters
     assert _rel(got, r.outs[0]) <= TOL
+
+
+# ---------------------------------------------------------------- 3D (config 5 shape family)
+@pytest.mark.parametrize("shape", [(16, 24, 32), (20, 12, 66), (9, 10, 130), (32, 32, 64)])
+def test_leja_3d(xi300, shape):
+    pb, ob = _pair(shape)
+    v = W.ic_random(shape, seed=7, amp=0.2)
+    dt = 5 * min(W.dt_cfl(n, 10.0, 3) for n in shape)
+    with lx.Context(pb) as ctx:
+        bound = lx.lx_spectrum_bound(ctx)
+        assert bound == O.spectrum_bound(ob)
+        c, g = lx.lx_shift_scale(bound)
+        for l in (0, 1, 4):
+            out = torch.empty(shape, dtype=torch.float64, device="cuda")
+            it = lx.lx_real_leja_phi(ctx, _dev(v), out, dt, c, g, l, TOL, TOL)
+            r = O.real_leja_phi(ob, v, dt, c, g, l, TOL, TOL, xi300)
+            assert it == r.iters, (shape, l)
+            assert _rel(out, r.outs[0]) <= TOL, (shape, l)
+        f = torch.empty(shape, dtype=torch.float64, device="cuda")
+        lx.lx_rhs(ctx, _dev(v), f, 0.5)
+        ref = 0.5 * O.rhs(ob, v)
+        assert np.abs(f.cpu().numpy() - ref).max() <= 1e-12 * np.abs(ref).max()
+        est = lx.lx_spectrum_estimate(ctx, None, 20)
+        assert est == pytest.approx(O.power_iteration(ob, None, 20), rel=1e-10)
+
+
+@pytest.mark.parametrize("method", ["epirk4s3a", "exprb43"])
+def test_steps_3d(xi300, method):
+    n = 32
+    shape = (n, n, n)
+    pb, ob = _pair(shape)
+    c1 = W.coords(n)
+    x, y, z = np.meshgrid(c1, c1, c1, indexing="ij")
+    u0 = np.ascontiguousarray(1.0 + np.exp(-((x + .5) ** 2 + (y + .5) ** 2 + (z + .5) ** 2) / 0.05))
+    dt = 10 * W.dt_cfl(n, 10.0, 3)
+    with lx.Context(pb) as ctx:
+        c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+        lo = torch.empty(shape, dtype=torch.float64, device="cuda")
+        hi = torch.empty_like(lo)
+        it, err = lx.lx_step(ctx, method, _dev(u0), lo, hi, dt, c, g, TOL, TOL)
+    r = O.step(ob, method, u0, dt, c, g, TOL, TOL, xi300)
+    assert it == r.iters
+    assert _rel(hi, r.u_high) <= TOL and _rel(lo, r.u_low) <= TOL
+    pa, oa = _pair((16, 16, 32), diff=1e-3, nu=0.0, react=1.0)
+    ua = W.ic_random((16, 16, 32), seed=3, amp=0.9) - 1.0
+    with lx.Context(pa) as ctx:
+        c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx, _dev(ua)))
+        lo = torch.empty((16, 16, 32), dtype=torch.float64, device="cuda")
+        hi = torch.empty_like(lo)
+        it, err = lx.lx_step(ctx, method, _dev(ua), lo, hi, 0.05, c, g, TOL, TOL)
+    r = O.step(oa, method, ua, 0.05, c, g, TOL, TOL, xi300)
+    assert it == r.iters
+    assert _rel(hi, r.u_high) <= TOL and _rel(lo, r.u_low) <= TOL
+    assert err == pytest.approx(r.err, rel=1e-8)

@@ -120,3 +120,30 @@ def test_slab_steps_allen_cahn(xi300, method):
     assert len({r[2] for r in res}) == 1 and res[0][2] == pytest.approx(ref.err, rel=1e-8)
     assert len({r[5] for r in res}) == 1
     assert res[0][5] == pytest.approx(O.power_iteration(ob, u, 30), rel=1e-10)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_slab_3d_epirk(xi300, P):
+    shape = (24, 16, 32)
+    dx = tuple(2.0 / n for n in shape)
+    pb = lx.Problem(shape, dx, 1.0, 10.0, 0.0)
+    ob = O.Problem(shape, dx, 1.0, 10.0, 0.0)
+    u = W.ic_random(shape, seed=11, amp=0.3)
+    dt = 5 * W.dt_cfl(32, 10.0, 3)
+    c, g = O.shift_scale(O.spectrum_bound(ob))
+
+    def rank_fn(r, group, s):
+        ctx = lx.Context(pb, stream=s)
+        ctx.set_comm_local(group, r)
+        b, e, _ = ctx.local()
+        ul = torch.from_numpy(u[b:e]).cuda()
+        lo, hi = torch.empty_like(ul), torch.empty_like(ul)
+        it, err = lx.lx_step(ctx, "epirk4s3a", ul, lo, hi, dt, c, g, TOL, TOL)
+        ctx.close()
+        return it, hi.cpu().numpy()
+
+    res = _run_ranks(P, rank_fn)
+    ref = O.step(ob, "epirk4s3a", u, dt, c, g, TOL, TOL, xi300)
+    assert {r[0] for r in res} == {ref.iters}
+    hi = np.concatenate([r[1] for r in res])
+    assert np.linalg.norm(hi - ref.u_high) <= TOL * np.linalg.norm(ref.u_high)

@@ -212,3 +212,18 @@ def test_integrator_convergence_order(xi300, method, order):
         errs.append(np.linalg.norm(u - uref) / np.linalg.norm(uref))
     orders = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
     assert abs(orders[-1] - order) < 0.3, (errs, orders)
+
+
+@pytest.mark.parametrize("l", [0, 1, 3])
+def test_leja_3d_vs_fft_exact(xi300, l):
+    n = 16
+    shape = (n, n, n)
+    pb = O.Problem(shape, (2 / n,) * 3, 1.0, 10.0, 0.0)
+    c, g = _cg(pb)
+    dt = 10 * W.dt_cfl(n, 10.0, 3)
+    v = W.ic_random(shape, seed=4, amp=0.5)
+    r = O.real_leja_phi(pb, v, dt, c, g, l, 1e-13, 1e-13, xi300)
+    assert r.status == O.OK
+    sym = refs.impulse_symbol(lambda x: O.jac_apply(pb, None, x), shape)
+    ex = refs.fft_apply_phi(sym, v, dt, l)
+    assert np.linalg.norm(r.outs[0] - ex) <= 1e-11 * np.linalg.norm(ex)
