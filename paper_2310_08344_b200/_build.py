@@ -51,6 +51,9 @@ def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
     hdr_mtime = max([os.path.getmtime(h) for h in _deps()] + [0])
+    src_mtime = max([os.path.getmtime(x) for x in srcs] + [hdr_mtime, os.path.getmtime(__file__)])
+    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= src_mtime:
+        return LIB   # up to date (objects may be absent, e.g. on a gpurun box)
     objs = []
     flags = _flags()
     for s in srcs:

@@ -220,8 +220,8 @@ def test_leja_3d_vs_fft_exact(xi300, l):
     shape = (n, n, n)
     pb = O.Problem(shape, (2 / n,) * 3, 1.0, 10.0, 0.0)
     c, g = _cg(pb)
-    dt = 10 * W.dt_cfl(n, 10.0, 3)
-    v = W.ic_random(shape, seed=4, amp=0.5)
+    dt = 5 * W.dt_cfl(n, 10.0, 3)
+    v = W.ic_random(shape, seed=4, amp=0.2)
     r = O.real_leja_phi(pb, v, dt, c, g, l, 1e-13, 1e-13, xi300)
     assert r.status == O.OK
     sym = refs.impulse_symbol(lambda x: O.jac_apply(pb, None, x), shape)

@@ -1,0 +1,152 @@
+#!/usr/bin/env python
+"""Measure every BASELINE.json config on one GPU (device-timed, CUDA events).
+
+Prints one JSON object per config: Leja iterations, time, achieved algorithmic
+GB/s of the Leja kernels and the fraction of the measured HBM copy peak.
+Not the driver's bench line (bench.py is); used to fill profiles/.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2310_08344_b200 as lx  # noqa: E402
+import workloads as W  # noqa: E402
+
+PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+
+
+def timed(stream, fn, reps):
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(stream)
+    out = [fn() for _ in range(reps)]
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps, out
+
+
+def cfg0(stream):
+    wl = W.config(0)
+    pb = lx.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
+    ctx = lx.Context(pb, stream=stream)
+    u = torch.from_numpy(W.ic_problem1_2d(64)).cuda()
+    out = torch.empty_like(u)
+    c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+    for _ in range(5):
+        it = lx.lx_step_rosenbrock_euler(ctx, u, out, wl.dt, c, g, wl.rtol, wl.atol)
+    ms, _ = timed(stream, lambda: lx.lx_step(ctx, "rosenbrock_euler", u, None, out, wl.dt, c, g, wl.rtol,
+                                             wl.atol, sync=False), 50)
+    ctx.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(50):
+        lx.lx_step_rosenbrock_euler(ctx, u, out, wl.dt, c, g, wl.rtol, wl.atol)
+    host_us = (time.perf_counter() - t0) / 50 * 1e6
+    return {"config": 0, "workload": wl.name, "grid": [64, 64], "leja_iters": it, "device_us_per_step": ms * 1e3,
+            "sync_us_per_step": host_us, "note": "L1/L2 resident, launch/latency bound: no roofline claim"}
+
+
+def cfg_leja(stream, n, ls, name, reps=3):
+    wl = W.config(1, n=n)
+    pb = lx.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
+    ctx = lx.Context(pb, stream=stream)
+    u = torch.from_numpy(W.ic_problem1_2d(n)).cuda()
+    out = torch.empty_like(u)
+    c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+    res = []
+    for l in ls:
+        it = lx.lx_real_leja_phi(ctx, u, out, wl.dt, c, g, l, wl.rtol, wl.atol)
+        ms, _ = timed(stream, lambda: lx.lx_real_leja_phi(ctx, u, out, wl.dt, c, g, l, wl.rtol, wl.atol,
+                                                           sync=False), reps)
+        ctx.synchronize()
+        byt = u.numel() * (24 + 32 * (it - 1))
+        res.append({"l": l, "iters": it, "ms": ms, "GBps": byt / ms / 1e6, "frac": byt / ms / 1e6 / PEAK})
+    ctx.close()
+    return {"config": name, "grid": [n, n], "calls": res,
+            "leja_it_per_s": sum(r["iters"] for r in res) / sum(r["ms"] for r in res) * 1e3}
+
+
+def cfg2(stream, n=2048, steps=20):
+    wl = W.config(2, n=n)
+    pb = lx.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
+    ctx = lx.Context(pb, stream=stream)
+    u = torch.from_numpy(W.ic_allen_cahn_2d(n)).cuda()
+    lo, hi = torch.empty_like(u), torch.empty_like(u)
+    its, errs = [], []
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for s in range(steps):
+        c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx, u))
+        it, err = lx.lx_step(ctx, "exprb43", u, lo, hi, wl.dt, c, g, wl.rtol, wl.atol)
+        its.append(it)
+        errs.append(err)
+        u, hi = hi, u
+    b.record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    ms = a.elapsed_time(b)
+    ctx.close()
+    return {"config": 2, "workload": wl.name, "grid": [n, n], "steps": steps, "leja_iters_per_step": its,
+            "err": errs[-1], "steps_per_s_device": steps / (ms * 1e-3), "steps_per_s_wall": steps / wall,
+            "ms_per_step": ms / steps}
+
+
+def cfg4(stream, n=512):
+    wl = W.config(4, n=n)
+    pb = lx.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
+    ctx = lx.Context(pb, stream=stream)
+    c1 = W.coords(n)
+    u = torch.empty(wl.shape, dtype=torch.float64, device="cuda")
+    for i in range(n):   # 3D Gaussian built slab by slab (host memory)
+        x = c1[i]
+        y, z = np.meshgrid(c1, c1, indexing="ij")
+        u[i] = torch.from_numpy(1.0 + np.exp(-((x + .5) ** 2 + (y + .5) ** 2 + (z + .5) ** 2) / 0.01))
+    lo, hi = torch.empty_like(u), torch.empty_like(u)
+    c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+    it, err = lx.lx_step(ctx, "epirk4s3a", u, lo, hi, wl.dt, c, g, wl.rtol, wl.atol)
+    ms, _ = timed(stream, lambda: lx.lx_step(ctx, "epirk4s3a", u, lo, hi, wl.dt, c, g, wl.rtol, wl.atol,
+                                             sync=False), 2)
+    ctx.synchronize()
+    out = torch.empty_like(u)
+    it0 = lx.lx_real_leja_phi(ctx, u, out, wl.dt, c, g, 0, wl.rtol, wl.atol)
+    ms0, _ = timed(stream, lambda: lx.lx_real_leja_phi(ctx, u, out, wl.dt, c, g, 0, wl.rtol, wl.atol, sync=False), 2)
+    ctx.synchronize()
+    byt = u.numel() * (24 + 32 * (it0 - 1))
+    ctx.close()
+    return {"config": 4, "workload": wl.name, "grid": list(wl.shape), "epirk4s3a_iters": it, "epirk4s3a_ms": ms,
+            "phi0_iters": it0, "phi0_ms": ms0, "phi0_GBps": byt / ms0 / 1e6, "phi0_frac": byt / ms0 / 1e6 / PEAK}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="0,1,2,3,4")
+    a = ap.parse_args()
+    torch.cuda.set_device(0)
+    s = torch.cuda.Stream()
+    torch.cuda.set_stream(s)
+    want = set(int(x) for x in a.only.split(","))
+    if 0 in want:
+        print(json.dumps(cfg0(s)), flush=True)
+    if 1 in want:
+        print(json.dumps(cfg_leja(s, 4096, (0, 1, 2, 3), 1)), flush=True)
+    if 2 in want:
+        print(json.dumps(cfg2(s)), flush=True)
+    if 3 in want:
+        print(json.dumps(cfg_leja(s, 16384, (0,), "3 (N=1)", reps=2)), flush=True)
+    if 4 in want:
+        print(json.dumps(cfg4(s)), flush=True)
+
+
+if __name__ == "__main__":
+    main()
