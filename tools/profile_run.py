@@ -1,0 +1,58 @@
+#!/usr/bin/env python
+"""Small driver for ncu captures: runs one workload a few times (first call = warm-up).
+
+  python tools/profile_run.py leja2d 4096 0      # phi_0 Leja call, 2D
+  python tools/profile_run.py leja3d 512 0       # phi_0 Leja call, 3D
+  python tools/profile_run.py ac 2048 2          # Allen-Cahn EXPRB43, 2 steps
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2310_08344_b200 as lx  # noqa: E402
+import workloads as W  # noqa: E402
+
+
+def main():
+    what, n, arg = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
+    reps = int(sys.argv[4]) if len(sys.argv) > 4 else 2
+    torch.cuda.set_device(0)
+    if what in ("leja2d", "leja3d"):
+        if what == "leja2d":
+            wl = W.config(1, n=n)
+            u = torch.from_numpy(W.ic_problem1_2d(n)).cuda()
+        else:
+            wl = W.config(4, n=n)
+            c1 = W.coords(n)
+            u = torch.empty(wl.shape, dtype=torch.float64, device="cuda")
+            y, z = np.meshgrid(c1, c1, indexing="ij")
+            for i in range(n):
+                u[i] = torch.from_numpy(1.0 + np.exp(-((c1[i] + .5) ** 2 + (y + .5) ** 2 + (z + .5) ** 2) / 0.01))
+        pb = lx.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
+        ctx = lx.Context(pb)
+        c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+        out = torch.empty_like(u)
+        for _ in range(reps):
+            it = lx.lx_real_leja_phi(ctx, u, out, wl.dt, c, g, arg, wl.rtol, wl.atol)
+        print("iters", it)
+    elif what == "ac":
+        wl = W.config(2, n=n)
+        pb = lx.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
+        ctx = lx.Context(pb)
+        u = torch.from_numpy(W.ic_allen_cahn_2d(n)).cuda()
+        lo, hi = torch.empty_like(u), torch.empty_like(u)
+        for _ in range(arg):
+            c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx, u))
+            it, err = lx.lx_step(ctx, "exprb43", u, lo, hi, wl.dt, c, g, wl.rtol, wl.atol)
+            u, hi = hi, u
+            print("iters", it, "err", err)
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    main()
