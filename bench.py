@@ -164,6 +164,36 @@ def _traffic_from_profiles():
     return None
 
 
+def exprb43_steps(lx, torch, stream, n=2048, warm=2, steps=10):
+    wl = W.config(2, n=n)
+    pb = lx.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
+    ctx = lx.Context(pb, stream=stream)
+    u = torch.from_numpy(W.ic_allen_cahn_2d(n)).cuda()
+    lo, hi = torch.empty_like(u), torch.empty_like(u)
+    its = []
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = 0
+    for s in range(warm + steps):
+        if s == warm:
+            torch.cuda.synchronize()
+            l0 = ctx.launch_count
+            a.record(stream)
+        c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx, u))
+        it, err = lx.lx_step(ctx, "exprb43", u, lo, hi, wl.dt, c, g, wl.rtol, wl.atol)
+        if s >= warm:
+            its.append(it)
+        u, hi = hi, u
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    launches = ctx.launch_count - l0
+    ctx.close()
+    return {"metric": "EXPRB43 steps/s", "value": steps / (ms * 1e-3), "unit": "steps/s",
+            "workload": wl.name, "grid": [n, n], "steps_timed": steps, "after_steps": warm,
+            "ms_per_step": ms / steps, "leja_iters_per_step": its, "gpu_launches": launches,
+            "note": "device-timed incl. per-step Gershgorin bound readback (2 host syncs/step)"}
+
+
 def run_ours(args):
     import torch
 
@@ -282,6 +312,12 @@ def run_ours(args):
     e2e = {"value": ws * e_it / e_t, "unit": UNIT, "h2d_bytes_per_step": 4 * N * 8, "d2h_bytes_per_step": 4 * N * 8,
            "steps": e2e_steps, "note": "4 lx_real_leja_phi calls with pinned host in/out pointers per step"}
 
+    # secondary metric of BASELINE.json: EXPRB steps/s (config 2 shape: Allen-Cahn 2048^2, EXPRB43,
+    # Gershgorin (c, gamma) recomputed every step).  Single-GPU only.
+    exprb = None
+    if ws == 1 and not args.no_exprb:
+        exprb = exprb43_steps(lx, torch, stream)
+
     cpu = None
     if rank == 0 and not args.no_cpu:
         cpu = cpu_baseline(n, args.ref_iters)
@@ -293,7 +329,8 @@ def run_ours(args):
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg, "roofline": roof,
-           "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary()}
+           "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
+           "exprb43": exprb}
     if rank == 0:
         print(json.dumps(out), flush=True)
     ctx.close()
@@ -311,6 +348,7 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="grid side override (default 4096)")
     ap.add_argument("--ref-iters", type=int, default=2, help="oracle Leja iterations per cpu sample")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-exprb", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -229,6 +229,7 @@ static LejaParams base_params(lx_ctx* ctx, const lx_problem* pb) {
     P.n2 = (int)ctx->n[2];
     P.nrb = (P.n_loc + kRT - 1) / kRT;
     if (ctx->ndim == 3) {
+        P.nrb = (P.n_loc + kRT3 - 1) / kRT3;
         P.nb = (P.n2 + 63) / 64;                 // 64-wide bands along the contiguous dim 2
         P.nunits = P.nb * P.n1 * P.nrb;          // u = (plane_block*nb + band)*n1 + j
     } else {
@@ -384,7 +385,7 @@ lx_status lx_ctx_create(const lx_problem* pb, int max_nodes, int device, void* c
     if (pb->n[pb->ndim - 1] % 2) return fail(LX_ERR_DIM, "the contiguous dimension must be even (double2 access)");
     if (pb->n[0] > (1 << 30) || pb->n[1] > (1 << 30) || (pb->ndim == 3 && pb->n[2] > (1 << 30)))
         return fail(LX_ERR_DIM, "grid too large");
-    if (pb->ndim == 3 && (double)pb->n[1] * (double)((pb->n[2] + 63) / 64) * (double)((pb->n[0] + 3) / 4) > 2e9)
+    if (pb->ndim == 3 && (double)pb->n[1] * (double)((pb->n[2] + 63) / 64) * (double)((pb->n[0] + 1) / 2) > 2e9)
         return fail(LX_ERR_DIM, "grid too large for the 32-bit work-unit index");
     if (max_nodes == 0) max_nodes = 300;
     if (max_nodes < 2 || max_nodes > 1024) return fail(LX_ERR_ARG, "max_nodes must be in [2, 1024]");
@@ -612,7 +613,7 @@ lx_status lx_spectrum_bound(lx_ctx* ctx, const lx_problem* pb, const double* u, 
         A.n2 = (int)ctx->n[2];
         A.x0 = ud;
         A.ctrl = ctx->ctrl;
-        A.grid = stage_grid_size(ctx->device);
+        A.grid = stage_grid_size(ctx->device, ST_MAXSQ);
         CUDA_TRY(launch_stage(ST_MAXSQ, A, ctx->stream));
         ctx->launches++;
         if (ctx->comm) LX_TRY(comm_allreduce_max_u64(ctx->comm, &ctx->ctrl->umax, ctx->stream) ? fail(LX_ERR_NCCL, "allreduce max: %s", comm_error()) : LX_OK);
@@ -673,12 +674,14 @@ static StageArgs stage_args(lx_ctx* ctx, const lx_problem* pb, int rec) {
     A.partials = ctx->partials;
     A.ctrl = ctx->ctrl;
     A.rec = ctx->rec_dev + rec;
-    A.grid = stage_grid_size(ctx->device);
-    if (A.grid > ctx->max_grid) A.grid = ctx->max_grid;
+    A.grid = 0;   // chosen per op in run_stage
     return A;
 }
 
-static lx_status run_stage(lx_ctx* ctx, int op, const StageArgs& A) {
+static lx_status run_stage(lx_ctx* ctx, int op, const StageArgs& A0) {
+    StageArgs A = A0;
+    A.grid = stage_grid_size(ctx->device, op);
+    if (A.grid > ctx->max_grid) A.grid = ctx->max_grid;
     if (ctx->comm && (op == ST_FINAL4 || op == ST_FINAL_EXPRB32))
         return comm_stage_norm(ctx->comm, op, A, ctx->stream, &ctx->launches) ? fail(LX_ERR_NCCL, "stage norm: %s", comm_error()) : LX_OK;
     CUDA_TRY(launch_stage(op, A, ctx->stream));

@@ -8,7 +8,8 @@ namespace lx {
 
 constexpr int kThreads = 256;     // threads per CTA (8 warps)
 constexpr int kWarps = kThreads / 32;
-constexpr int kRT = 4;            // rows (2D) / planes (3D) per warp work unit
+constexpr int kRT = 4;            // rows per warp work unit (2D)
+constexpr int kRT3 = 2;           // planes per warp work unit (3D)
 constexpr int kMaxK = 4;          // vertical accumulators
 constexpr int kSlot = 8;          // doubles per CTA partial slot (1 + K <= 5)
 
@@ -136,6 +137,6 @@ cudaError_t launch_power_step(const LejaParams& P, int m, cudaStream_t s, bool d
 int step_grid_size(int device, int nunits);
 cudaError_t launch_finalize_err(const double* gathered, int nranks, double N, Record* rec, cudaStream_t s);
 cudaError_t launch_max_u64(const unsigned long long* vals, int n, unsigned long long* out, cudaStream_t s);
-int stage_grid_size(int device);
+int stage_grid_size(int device, int op);
 
 }  // namespace lx

@@ -207,7 +207,7 @@ __device__ __forceinline__ void tile2d(const LejaParams& P, const RowSrc& src, d
 
 
 // One warp work unit of the 3D stencil: 64 contiguous k (dim 2) x one j row (dim 1)
-// x kRT planes (dim 0).  i-neighbours from the plane window, j-neighbours from
+// x kRT3 planes (dim 0).  i-neighbours from the plane window, j-neighbours from
 // rows j-1, j+1, j+2 of the same plane (adjacent warps own adjacent j -> L1 hits),
 // k-neighbours by shuffles + edge-lane halo loads.  Units: u = (pb*nb + b)*n1 + j.
 template <int K, bool DIAG, bool FIRST, int MODE, bool RO>
@@ -222,25 +222,25 @@ __device__ __forceinline__ void tile3d(const LejaParams& P, const RowSrc& src, d
     const int k0 = b * 64 + 2 * lane;
     const bool valid = k0 < n2;
     const int last = min(31, ((n2 - b * 64) >> 1) - 1);
-    const int i0 = pb * kRT;
-    const int nout = min(kRT, P.n_loc - i0);
+    const int i0 = pb * kRT3;
+    const int nout = min(kRT3, P.n_loc - i0);
     const int jm = (j == 0) ? n1 - 1 : j - 1;
     const int jp1 = (j + 1 >= n1) ? j + 1 - n1 : j + 1;
     const int jp2 = (j + 2 >= n1) ? j + 2 - n1 : j + 2;
     const Stencil& S = P.st;
     auto LD2 = [&](const double* q) { return RO ? ldg2(q) : ld2(q); };
 
-    double2 w[kRT + 3];
+    double2 w[kRT3 + 3];
 #pragma unroll
-    for (int t = 0; t < kRT + 3; t++) {
+    for (int t = 0; t < kRT3 + 3; t++) {
         w[t] = make_double2(0.0, 0.0);
         if (valid && t < nout + 3) w[t] = LD2(rowp(src, i0 - 1 + t) + (long long)j * n2 + k0);
     }
-    double2 wm[kRT], wp1[kRT], wp2[kRT];
-    double hl[kRT];
-    double2 hr[kRT];
+    double2 wm[kRT3], wp1[kRT3], wp2[kRT3];
+    double hl[kRT3];
+    double2 hr[kRT3];
 #pragma unroll
-    for (int t = 0; t < kRT; t++) {
+    for (int t = 0; t < kRT3; t++) {
         wm[t] = wp1[t] = wp2[t] = hr[t] = make_double2(0.0, 0.0);
         hl[t] = 0.0;
         if (t < nout) {
@@ -263,10 +263,10 @@ __device__ __forceinline__ void tile3d(const LejaParams& P, const RowSrc& src, d
         }
     }
     constexpr int KK = K > 0 ? K : 1;
-    double2 pv[kRT][KK];
-    double2 uu[kRT];
+    double2 pv[kRT3][KK];
+    double2 uu[kRT3];
 #pragma unroll
-    for (int t = 0; t < kRT; t++) {
+    for (int t = 0; t < kRT3; t++) {
         const long long off = ((long long)(i0 + t) * n1 + j) * n2 + k0;
         if (MODE == M_LEJA && !FIRST) {
 #pragma unroll
@@ -279,7 +279,7 @@ __device__ __forceinline__ void tile3d(const LejaParams& P, const RowSrc& src, d
         if (DIAG && valid && t < nout) uu[t] = ldg2(P.u + off);
     }
 #pragma unroll
-    for (int t = 0; t < kRT; t++) {
+    for (int t = 0; t < kRT3; t++) {
         if (t < nout) {
             const double2 yc = w[t + 1], up = w[t], dn1 = w[t + 2], dn2 = w[t + 3];
             double left = __shfl_up_sync(FULL_MASK, yc.y, 1);
@@ -502,7 +502,7 @@ __device__ __forceinline__ void barrier_decide(const LejaParams& P, int m, unsig
 }
 
 template <int NDIM, int K, bool DIAG>
-__global__ void __launch_bounds__(kThreads) k_leja2d(const __grid_constant__ LejaParams P) {
+__global__ void __launch_bounds__(kThreads, 2) k_leja2d(const __grid_constant__ LejaParams P) {
     __shared__ double s_red[kWarps][kSlot];
     __shared__ int s_flags[4];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(kThreads) k_leja2d(const __grid_constant__ Lej
 }
 
 template <int NDIM, bool DIAG>
-__global__ void __launch_bounds__(kThreads) k_power2d(const __grid_constant__ LejaParams P) {
+__global__ void __launch_bounds__(kThreads, 2) k_power2d(const __grid_constant__ LejaParams P) {
     __shared__ double s_red[kWarps][kSlot];
     __shared__ int s_flags[4];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -613,7 +613,7 @@ __device__ __forceinline__ void rank_reduce(const LejaParams& P, double (&vals)[
 }
 
 template <int NDIM, int K, bool DIAG>
-__global__ void __launch_bounds__(kThreads) k_leja2d_step(const __grid_constant__ LejaParams P, int m) {
+__global__ void __launch_bounds__(kThreads, 2) k_leja2d_step(const __grid_constant__ LejaParams P, int m) {
     __shared__ double s_red[kWarps][kSlot];
     __shared__ int s_last;
     Ctrl* ctrl = P.ctrl;
@@ -674,7 +674,7 @@ __global__ void __launch_bounds__(kThreads) k_leja2d_step(const __grid_constant_
 }
 
 template <int NDIM, bool DIAG>
-__global__ void __launch_bounds__(kThreads) k_power2d_step(const __grid_constant__ LejaParams P, int m) {
+__global__ void __launch_bounds__(kThreads, 2) k_power2d_step(const __grid_constant__ LejaParams P, int m) {
     __shared__ double s_red[kWarps][kSlot];
     __shared__ int s_last;
     Ctrl* ctrl = P.ctrl;
@@ -938,7 +938,7 @@ __global__ void __launch_bounds__(kThreads) k_stage_pointwise(const __grid_const
 }
 
 template <int NDIM>
-__global__ void __launch_bounds__(kThreads) k_rhs2d(const __grid_constant__ LejaParams P, double scale) {
+__global__ void __launch_bounds__(kThreads, 2) k_rhs2d(const __grid_constant__ LejaParams P, double scale) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double sy = 0.0, sp[1] = {0.0};
     for (int unit = blockIdx.x * kWarps + warp; unit < P.nunits; unit += gridDim.x * kWarps)
@@ -955,10 +955,29 @@ cudaError_t launch_fill_start(double* v, long long n, bool add_e0, cudaStream_t 
     return cudaGetLastError();
 }
 
-int stage_grid_size(int device) {
-    int nsm = 0;
+static void* stage_kernel_ptr(int op) {
+    switch (op) {
+        case ST_AXPBY: return (void*)k_stage_pointwise<ST_AXPBY>;
+        case ST_REMAINDER_DIFF: return (void*)k_stage_pointwise<ST_REMAINDER_DIFF>;
+        case ST_STAGE_REMAINDER: return (void*)k_stage_pointwise<ST_STAGE_REMAINDER>;
+        case ST_EXPRB32_A: return (void*)k_stage_pointwise<ST_EXPRB32_A>;
+        case ST_COMBINE2: return (void*)k_stage_pointwise<ST_COMBINE2>;
+        case ST_FINAL4: return (void*)k_stage_pointwise<ST_FINAL4>;
+        case ST_FINAL_EXPRB32: return (void*)k_stage_pointwise<ST_FINAL_EXPRB32>;
+        case ST_MAXSQ: return (void*)k_stage_pointwise<ST_MAXSQ>;
+    }
+    return nullptr;
+}
+
+// One full wave of resident CTAs (never more: a partial second wave doubles the time).
+int stage_grid_size(int device, int op) {
+    int nsm = 0, per = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
-    return nsm * 4;
+    void* k = stage_kernel_ptr(op);
+    if (k) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kThreads, 0);
+    if (per < 1) per = 1;
+    if (per > 8) per = 8;
+    return nsm * per;
 }
 
 cudaError_t launch_rhs(const LejaParams& P, double scale, cudaStream_t s) {
