@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -83,6 +84,7 @@ struct lx_ctx {
     int64_t launches = 0;
     std::vector<double> xi;
     Comm* comm = nullptr;                 // slab decomposition (lx_comm.cpp)
+    int variant = 1;                      // 2D single-GPU Leja kernel: 0 = register tiles, 1 = TMA marching
 };
 
 // ------------------------------------------------------------------ helpers
@@ -268,6 +270,14 @@ static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u,
     P.u = u;
     P.rec = ctx->rec_dev + rec;
     if (ctx->comm) return comm_leja(ctx->comm, P, diag, ctx->stream, &ctx->launches);
+    if (ctx->ndim == 2 && ctx->variant == 1) {
+        P.grid = leja_tma_grid_size(ctx->device, K, diag, (long long)P.nb * P.n_loc);
+        if (P.grid > 0) {
+            CUDA_TRY(launch_leja_tma(P, ctx->stream, diag));
+            ctx->launches++;
+            return LX_OK;
+        }
+    }
     P.grid = leja_grid_size(ctx->device, K, diag, ctx->ndim, P.nunits);
     CUDA_TRY(launch_leja_persistent(P, ctx->stream, diag));
     ctx->launches++;
@@ -410,6 +420,7 @@ lx_status lx_ctx_create(const lx_problem* pb, int max_nodes, int device, void* c
     ctx->N_loc = (int64_t)ctx->n_loc * ctx->row;
     ctx->N_glob = (double)ctx->n[0] * (double)ctx->row;
     ctx->max_nodes = max_nodes;
+    if (const char* ev = std::getenv("LX_LEJA_KERNEL")) ctx->variant = (std::strcmp(ev, "tile") == 0) ? 0 : 1;
     cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device);
     ctx->max_grid = ctx->nsm * 8;
     ctx->xi.resize(max_nodes);

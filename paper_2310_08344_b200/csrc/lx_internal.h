@@ -99,6 +99,9 @@ struct LejaParams {
 cudaError_t launch_leja_persistent(const LejaParams& P, cudaStream_t s, bool diag);
 cudaError_t launch_power_persistent(const LejaParams& P, cudaStream_t s, bool diag);
 int leja_grid_size(int device, int K, bool diag, int ndim, int nunits);
+// TMA-pipelined marching variant (2D, single GPU)
+int leja_tma_grid_size(int device, int K, bool diag, long long band_rows);
+cudaError_t launch_leja_tma(const LejaParams& P, cudaStream_t s, bool diag);
 
 struct StageArgs {
     int ndim, n_loc, n1, n2, nb, nrb, nunits;

@@ -721,6 +721,255 @@ __global__ void k_max_u64(const unsigned long long* vals, int n, unsigned long l
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// TMA-pipelined marching variant of the 2D Leja iteration (k_leja2d_tma).
+//
+// Each warp owns a contiguous run of rows of one 64-column band ("segment";
+// the band-rows of the grid are split evenly over all warps) and marches down
+// it.  Row data arrive in a per-warp shared-memory ring through bulk async
+// copies (cp.async.bulk, TMA engine) completing on one mbarrier per ring slot:
+// entry e = {y row r+2 (+16-byte halos on both sides), p row r, u row r}.
+// The stencil for row r reads y rows r-1..r+2 from the last 4 entries, so every
+// y row crosses HBM once per iteration (+3 preamble rows per segment) with no
+// register-held tiles; D = RS-4 entries are in flight ahead of the consumer.
+// Same arithmetic order, reductions and device-side decision as k_leja2d.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <int K, bool DIAG>
+struct TmaCfg {
+    static constexpr int RS = (K <= 1) ? 8 : 6;             // ring slots per warp
+    static constexpr int D = RS - 4;                        // entries in flight ahead of the consumer
+    static constexpr int YS = 68;                           // y slot: [j0-2, j0+64) + right halo
+    static constexpr int ES = YS + 64 * K + (DIAG ? 64 : 0);  // doubles per entry
+    static constexpr int WARP_BYTES = RS * (ES * 8 + 8);
+    static constexpr int SMEM = kWarps * WARP_BYTES;
+};
+
+// Warp work list: band-rows [t0, t1) in band-major order (t -> band t / n, row t % n).
+struct SegIter {
+    long long t0, t1;
+    int n_loc;
+};
+
+template <int K, bool DIAG>
+__global__ void __launch_bounds__(kThreads, (K <= 1 ? 3 : 2)) k_leja2d_tma(const __grid_constant__ LejaParams P) {
+    using C = TmaCfg<K, DIAG>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ double s_red[kWarps][kSlot];
+    __shared__ int s_flags[4];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned char* wbase = smem + warp * C::WARP_BYTES;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(wbase);
+    double* ring = reinterpret_cast<double*>(wbase + C::RS * 8);
+    if (lane == 0)
+        for (int i = 0; i < C::RS; i++) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+
+    const int n1 = P.n1, n_loc = P.n_loc;
+    const long long T = (long long)P.nb * n_loc;
+    const long long W = (long long)gridDim.x * kWarps;
+    const long long gw = (long long)blockIdx.x * kWarps + warp;
+    const long long t0 = T * gw / W, t1 = T * (gw + 1) / W;
+    // entries of this warp per iteration: rows + 3 preamble entries per segment
+    int nseg = 0;
+    for (long long t = t0; t < t1;) {
+        const long long len = min(t1 - t, (long long)(n_loc - (int)(t % n_loc)));
+        nseg++;
+        t += len;
+    }
+    const int NE = (int)(t1 - t0) + 3 * nseg;
+
+    unsigned gen0 = 0;
+    if (tid == 0) gen0 = ld_acquire(&P.ctrl->gen);
+    int active = P.active0;
+    double d0[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) d0[k] = P.coef[1 + k];
+    unsigned long long qbase = 0;
+    const Stencil& S = P.st;
+
+    for (int m = 1; m < P.max_nodes; m++) {
+        const double* cm = P.coef + (size_t)m * (1 + K);
+        const double beta = cm[0];
+        double dm[K], sp[K];
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            dm[k] = cm[1 + k];
+            sp[k] = 0.0;
+        }
+        double sy = 0.0;
+        const int par = m & 1;
+        const bool first = (m == 1);
+        const RowSrc src = first ? P.v : P.ysrc[par ^ 1];
+        double* dst = P.ydst[par];
+        // producer cursor over (segment, position) in entry order
+        long long pt = t0;     // band-row of the producer's current segment start
+        int ppos = 0;          // position within segment (0..2 preamble, then rows)
+        long long ct = t0;     // consumer's current segment start
+        int cpos = 0;
+        int e_p = 0;
+        for (int e = 0; e < NE; e++) {
+            // ---- producer: keep D entries in flight
+            while (e_p < NE && e_p <= e + C::D) {
+                const int b = (int)(pt / n_loc);
+                const int i0 = (int)(pt % n_loc);
+                const int len = (int)min(t1 - pt, (long long)(n_loc - i0));
+                if (lane == 0) {
+                    const unsigned long long q = qbase + e_p;
+                    const int slot = (int)(q % C::RS);
+                    double* ent = ring + slot * C::ES;
+                    uint64_t* bar = &bars[slot];
+                    const int j0 = b * 64;
+                    const int vc = min(64, n1 - j0);
+                    const int jl = (j0 == 0) ? n1 - 2 : j0 - 2;
+                    const int jr = (j0 + vc >= n1) ? 0 : j0 + vc;
+                    const int yrow = (ppos < 3) ? i0 - 1 + ppos : i0 + (ppos - 3) + 2;
+                    const double* rp = rowp(src, yrow);
+                    uint32_t bytes = (uint32_t)(vc * 8 + 32);
+                    const bool full = ppos >= 3;
+                    const int prow = i0 + (ppos - 3);
+                    int nact = 0;
+                    if (full && !first) {
+#pragma unroll
+                        for (int k = 0; k < K; k++) nact += (active >> k) & 1;
+                    }
+                    if (full) bytes += (uint32_t)(vc * 8) * (uint32_t)(nact + (DIAG ? 1 : 0));
+                    fence_proxy_async();
+                    mbar_expect_tx(bar, bytes);
+                    bulk_g2s(ent, rp + jl, 16, bar);
+                    bulk_g2s(ent + 2, rp + j0, vc * 8, bar);
+                    bulk_g2s(ent + 2 + vc, rp + jr, 16, bar);
+                    if (full) {
+                        const long long off = (long long)prow * n1 + j0;
+                        if (!first) {
+#pragma unroll
+                            for (int k = 0; k < K; k++)
+                                if ((active >> k) & 1) bulk_g2s(ent + C::YS + 64 * k, P.p[k] + off, vc * 8, bar);
+                        }
+                        if (DIAG) bulk_g2s(ent + C::YS + 64 * K, P.u + off, vc * 8, bar);
+                    }
+                }
+                e_p++;
+                if (++ppos == 3 + len) {
+                    pt += len;
+                    ppos = 0;
+                }
+            }
+            // ---- consumer
+            const unsigned long long q = qbase + e;
+            mbar_wait(&bars[q % C::RS], (uint32_t)((q / C::RS) & 1));
+            const int b = (int)(ct / n_loc);
+            const int i0 = (int)(ct % n_loc);
+            const int len = (int)min(t1 - ct, (long long)(n_loc - i0));
+            if (cpos >= 3) {
+                const int r = i0 + (cpos - 3);
+                const double* Ed2 = ring + (int)(q % C::RS) * C::ES;
+                const double* Ed1 = ring + (int)((q + C::RS - 1) % C::RS) * C::ES;
+                const double* Ec = ring + (int)((q + C::RS - 2) % C::RS) * C::ES;
+                const double* Eu = ring + (int)((q + C::RS - 3) % C::RS) * C::ES;
+                const int j0 = b * 64;
+                const int j = j0 + 2 * lane;
+                if (j < n1) {
+                    const double2 yc = *reinterpret_cast<const double2*>(Ec + 2 + 2 * lane);
+                    const double left = Ec[1 + 2 * lane];
+                    const double2 rr = *reinterpret_cast<const double2*>(Ec + 4 + 2 * lane);
+                    const double2 up = *reinterpret_cast<const double2*>(Eu + 2 + 2 * lane);
+                    const double2 dn1 = *reinterpret_cast<const double2*>(Ed1 + 2 + 2 * lane);
+                    const double2 dn2 = *reinterpret_cast<const double2*>(Ed2 + 2 + 2 * lane);
+                    double ax = S.c0 * yc.x;
+                    ax = fma(S.m1[0], up.x, ax);
+                    ax = fma(S.p1[0], dn1.x, ax);
+                    ax = fma(S.p2[0], dn2.x, ax);
+                    ax = fma(S.m1[1], left, ax);
+                    ax = fma(S.p1[1], yc.y, ax);
+                    ax = fma(S.p2[1], rr.x, ax);
+                    double ay = S.c0 * yc.y;
+                    ay = fma(S.m1[0], up.y, ay);
+                    ay = fma(S.p1[0], dn1.y, ay);
+                    ay = fma(S.p2[0], dn2.y, ay);
+                    ay = fma(S.m1[1], yc.x, ay);
+                    ay = fma(S.p1[1], rr.x, ay);
+                    ay = fma(S.p2[1], rr.y, ay);
+                    if (DIAG) {
+                        const double2 uu = *reinterpret_cast<const double2*>(Ed2 + C::YS + 64 * K + 2 * lane);
+                        ax = fma(fma(S.qb, uu.x * uu.x, S.qa), yc.x, ax);
+                        ay = fma(fma(S.qb, uu.y * uu.y, S.qa), yc.y, ay);
+                    }
+                    double2 yn;
+                    yn.x = fma(P.alpha, ax, beta * yc.x);
+                    yn.y = fma(P.alpha, ay, beta * yc.y);
+                    const long long off = (long long)r * n1 + j;
+                    st2(dst + off, yn);
+                    sy = fma(yn.x, yn.x, sy);
+                    sy = fma(yn.y, yn.y, sy);
+#pragma unroll
+                    for (int k = 0; k < K; k++) {
+                        if ((active >> k) & 1) {
+                            double2 pn;
+                            if (first) {
+                                pn.x = fma(dm[k], yn.x, d0[k] * yc.x);
+                                pn.y = fma(dm[k], yn.y, d0[k] * yc.y);
+                            } else {
+                                const double2 pv = *reinterpret_cast<const double2*>(Ed2 + C::YS + 64 * k + 2 * lane);
+                                pn.x = fma(dm[k], yn.x, pv.x);
+                                pn.y = fma(dm[k], yn.y, pv.y);
+                            }
+                            st2(P.p[k] + off, pn);
+                            sp[k] = fma(pn.x, pn.x, sp[k]);
+                            sp[k] = fma(pn.y, pn.y, sp[k]);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            if (++cpos == 3 + len) {
+                ct += len;
+                cpos = 0;
+            }
+        }
+        qbase += NE;
+        double vals[1 + K];
+        vals[0] = sy;
+#pragma unroll
+        for (int k = 0; k < K; k++) vals[1 + k] = sp[k];
+        block_reduce<1 + K>(vals, s_red);
+        if (tid == 0) {
+            double* slot = P.partials + ((size_t)par * gridDim.x + blockIdx.x) * kSlot;
+#pragma unroll
+            for (int i = 0; i < 1 + K; i++) slot[i] = vals[i];
+        }
+        barrier_decide<K, M_LEJA>(P, m, gen0, dm, active, s_red, s_flags);
+        active = s_flags[2];
+        if (s_flags[1]) break;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Launchers
 // ---------------------------------------------------------------------------
@@ -829,6 +1078,46 @@ cudaError_t launch_finalize_err(const double* gathered, int nranks, double N, Re
 cudaError_t launch_max_u64(const unsigned long long* vals, int n, unsigned long long* out, cudaStream_t s) {
     k_max_u64<<<1, 32, 0, s>>>(vals, n, out);
     return cudaGetLastError();
+}
+
+
+// ---- TMA marching kernel launch
+template <int K, bool DIAG>
+static cudaError_t tma_prepare(int device, int* per_sm) {
+    using C = TmaCfg<K, DIAG>;
+    cudaError_t e = cudaFuncSetAttribute(k_leja2d_tma<K, DIAG>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_leja2d_tma<K, DIAG>, kThreads, C::SMEM);
+}
+
+template <int K, bool DIAG>
+static cudaError_t tma_launch(const LejaParams& P, cudaStream_t s) {
+    using C = TmaCfg<K, DIAG>;
+    void* args[] = {(void*)&P};
+    return cudaLaunchCooperativeKernel((void*)k_leja2d_tma<K, DIAG>, dim3(P.grid), dim3(kThreads), args, C::SMEM, s);
+}
+
+static cudaError_t tma_dispatch(int K, bool diag, int device, int* per_sm, const LejaParams* P, cudaStream_t s) {
+#define LX_TMA_CASE(KK, DD)                                                    \
+    if (K == KK && diag == DD) return P ? tma_launch<KK, DD>(*P, s) : tma_prepare<KK, DD>(device, per_sm);
+    LX_TMA_CASE(1, false) LX_TMA_CASE(1, true) LX_TMA_CASE(2, false) LX_TMA_CASE(2, true)
+    LX_TMA_CASE(3, false) LX_TMA_CASE(3, true) LX_TMA_CASE(4, false) LX_TMA_CASE(4, true)
+#undef LX_TMA_CASE
+    return cudaErrorInvalidValue;
+}
+
+int leja_tma_grid_size(int device, int K, bool diag, long long band_rows) {
+    int nsm = 0, per = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    if (tma_dispatch(K, diag, device, &per, nullptr, nullptr) != cudaSuccess || per < 1) return 0;
+    long long g = (long long)nsm * per;
+    const long long need = (band_rows + kWarps * 8 - 1) / (kWarps * 8);   // >= 8 rows per warp
+    if (g > need) g = need > 0 ? need : 1;
+    return (int)g;
+}
+
+cudaError_t launch_leja_tma(const LejaParams& P, cudaStream_t s, bool diag) {
+    return tma_dispatch(P.K, diag, 0, nullptr, &P, s);
 }
 
 // ---------------------------------------------------------------------------

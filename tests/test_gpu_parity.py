@@ -334,3 +334,30 @@ def test_steps_3d(xi300, method):
     assert it == r.iters
     assert _rel(hi, r.u_high) <= TOL and _rel(lo, r.u_low) <= TOL
     assert err == pytest.approx(r.err, rel=1e-8)
+
+
+@pytest.mark.parametrize("shape,K,react", [((64, 64), 1, 0.0), ((50, 70), 2, 0.0), ((130, 66), 3, 1.0),
+                                           ((4096, 256), 1, 1.0)])
+def test_kernel_variants_bitwise_equal(xi300, monkeypatch, shape, K, react):
+    # register-tile kernel (LX_LEJA_KERNEL=tile) and TMA marching kernel (default) do the same
+    # per-point arithmetic in the same order: identical iterations and bitwise-identical output.
+    diff, nu = (1e-4, 0.0) if react else (1.0, 10.0)
+    pb, ob = _pair(shape, diff=diff, nu=nu, react=react)
+    u = W.ic_allen_cahn_2d(*shape) if react else None
+    v = W.ic_random(shape, seed=21, amp=0.2)
+    dt = 0.01 if react else 10 * min(W.dt_cfl(n, 10.0) for n in shape)
+    coeffs = (0.5, 2 / 3, 0.9, 1.0)[-K:]
+    res = {}
+    for variant in ("tile", "tma"):
+        monkeypatch.setenv("LX_LEJA_KERNEL", variant)
+        with lx.Context(pb) as ctx:
+            ud = _dev(u) if react else None
+            c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx, ud))
+            outs = [torch.empty(shape, dtype=torch.float64, device="cuda") for _ in range(K)]
+            it = lx.lx_real_leja_phi_vertical(ctx, _dev(v), outs, coeffs, dt, c, g, 1, TOL, TOL, u_lin=ud)
+            res[variant] = (it, [o.cpu().numpy() for o in outs])
+    assert res["tile"][0] == res["tma"][0]
+    for a, b in zip(res["tile"][1], res["tma"][1]):
+        np.testing.assert_array_equal(a, b)
+    r = O.real_leja_phi(ob, v, dt, c, g, 1, TOL, TOL, xi300, coeffs=coeffs, u_lin=u)
+    assert res["tma"][0] == r.iters
