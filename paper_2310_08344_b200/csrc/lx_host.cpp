@@ -84,7 +84,7 @@ struct lx_ctx {
     int64_t launches = 0;
     std::vector<double> xi;
     Comm* comm = nullptr;                 // slab decomposition (lx_comm.cpp)
-    int variant = 1;                      // 2D single-GPU Leja kernel: 0 = register tiles, 1 = TMA marching
+    int variant = 0;                      // 2D single-GPU Leja kernel: 0 = register tiles, 1 = TMA marching
 };
 
 // ------------------------------------------------------------------ helpers
@@ -420,7 +420,7 @@ lx_status lx_ctx_create(const lx_problem* pb, int max_nodes, int device, void* c
     ctx->N_loc = (int64_t)ctx->n_loc * ctx->row;
     ctx->N_glob = (double)ctx->n[0] * (double)ctx->row;
     ctx->max_nodes = max_nodes;
-    if (const char* ev = std::getenv("LX_LEJA_KERNEL")) ctx->variant = (std::strcmp(ev, "tile") == 0) ? 0 : 1;
+    if (const char* ev = std::getenv("LX_LEJA_KERNEL")) ctx->variant = (std::strcmp(ev, "tma") == 0) ? 1 : 0;
     cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device);
     ctx->max_grid = ctx->nsm * 8;
     ctx->xi.resize(max_nodes);

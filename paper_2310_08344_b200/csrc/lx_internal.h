@@ -41,6 +41,9 @@ struct Ctrl {
     unsigned int pad2;
     unsigned long long umax;  // max reduction (bit pattern of a non-negative double)
     int hist[2];          // step mode: active mask after iteration j stored at hist[j & 1]
+    // persistent kernels: packed decision word released by the barrier's last arriver
+    // [63:32] generation (gen0 + m), [31:16] status, [15:8] done, [7:0] active mask
+    unsigned long long word;
 };
 
 // Rows of a slab: rows [0, n_loc) at base, row r in {-1, n_loc, n_loc+1}

@@ -40,6 +40,20 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
 __device__ __forceinline__ const double* rowp(const RowSrc& s, int r) {
     if ((unsigned)r < (unsigned)s.n_loc) return s.base + (long long)r * s.stride;
     if (s.ghost) return s.ghost + (long long)(r < 0 ? 0 : r - s.n_loc + 1) * s.stride;
@@ -437,19 +451,22 @@ __device__ __forceinline__ void power_decide(const LejaParams& P, int m, double 
 template <int K, int MODE>
 __device__ __forceinline__ void barrier_decide(const LejaParams& P, int m, unsigned gen0, const double* dm,
                                                int active, double (*s_red)[kSlot], int* s_flags) {
+    // Grid barrier + device-side decision.  Arrival = one acq_rel atomic per CTA
+    // (releases this CTA's y/p stores and its partial slot, ordered before it by
+    // bar.sync); the last arriver sums the slots in fixed order, decides, and
+    // publishes {generation, status, done, active} in ONE st.release of a 64-bit
+    // word, which the waiters acquire (no further fences or control reads).
     constexpr int NV = (MODE == M_LEJA) ? 1 + K : 1;
     const int tid = threadIdx.x;
     Ctrl* ctrl = P.ctrl;
     const int par = m & 1;
     __syncthreads();
     if (tid == 0) {
-        __threadfence();
-        const unsigned t = atomicAdd(&ctrl->arrive, 1u);
+        const unsigned t = atom_add_acq_rel(&ctrl->arrive, 1u);
         s_flags[0] = (t == gridDim.x - 1);
     }
     __syncthreads();
     if (s_flags[0]) {
-        __threadfence();
         double acc[NV];
 #pragma unroll
         for (int i = 0; i < NV; i++) acc[i] = 0.0;
@@ -462,41 +479,37 @@ __device__ __forceinline__ void barrier_decide(const LejaParams& P, int m, unsig
         if (tid == 0) {
             Record* rec = P.rec;
             int done = 0, status = 0, act = active;
+            double scale = 0.0;
             if (MODE == M_LEJA) {
                 leja_decide<K>(P, m, acc, dm, act, done, status, rec);
-            } else {  // M_POWER
-                power_decide(P, m, acc[0], done, status, &ctrl->est, &ctrl->scale, rec);
+            } else {
+                power_decide(P, m, acc[0], done, status, &ctrl->est, &scale, rec);
+                ctrl->scale = scale;
             }
-            ctrl->done = done;
-            ctrl->active = act;
-            ctrl->status = status;
-            ctrl->m = m;
             ctrl->arrive = 0u;
-            __threadfence();
-            st_release(&ctrl->gen, gen0 + (unsigned)m);
+            const unsigned long long w = ((unsigned long long)(gen0 + (unsigned)m) << 32) |
+                                         ((unsigned long long)(status & 0xffff) << 16) |
+                                         ((unsigned long long)(done & 0xff) << 8) | (unsigned long long)(act & 0xff);
+            st_release64(&ctrl->word, w);
+            s_flags[1] = done;
+            s_flags[2] = act;
+            s_red[0][kSlot - 1] = scale;
         }
     } else if (tid == 0) {
+        unsigned long long w = ld_acquire64(&ctrl->word);
         int spins = 0;
-        while ((int)(ld_acquire(&ctrl->gen) - gen0) < m) {
-            if (++spins > 64) __nanosleep(64);
+        while ((int)((unsigned)(w >> 32) - gen0) < m) {
+            if (++spins > 32) __nanosleep(32);
             if (spins > P.timeout_spins) {
-                ctrl->done = 1;
-                ctrl->status = 10;  // LX_ERR_TIMEOUT
-                atomicExch(&P.rec->status, 10);
+                atomicExch(&P.rec->status, 10);  // LX_ERR_TIMEOUT
+                w = (1ull << 8);
                 break;
             }
+            w = ld_acquire64(&ctrl->word);
         }
-        __threadfence();
-    }
-    __syncthreads();
-    if (tid == 0) {
-        s_flags[1] = *(volatile int*)&ctrl->done;
-        s_flags[2] = *(volatile int*)&ctrl->active;
-        s_flags[3] = 0;
-        if (MODE == M_POWER) {
-            volatile double* sc = &ctrl->scale;
-            s_red[0][kSlot - 1] = *sc;
-        }
+        s_flags[1] = (int)((w >> 8) & 0xff);
+        s_flags[2] = (int)(w & 0xff);
+        if (MODE == M_POWER) s_red[0][kSlot - 1] = *(volatile double*)&ctrl->scale;
     }
     __syncthreads();
 }
@@ -507,7 +520,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d(const __grid_constant__ 
     __shared__ int s_flags[4];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     unsigned gen0 = 0;
-    if (tid == 0) gen0 = ld_acquire(&P.ctrl->gen);
+    if (tid == 0) gen0 = (unsigned)(ld_acquire64(&P.ctrl->word) >> 32);
     int active = P.active0;
     double d0[K];
 #pragma unroll
@@ -554,7 +567,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_power2d(const __grid_constant__
     __shared__ int s_flags[4];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     unsigned gen0 = 0;
-    if (tid == 0) gen0 = ld_acquire(&P.ctrl->gen);
+    if (tid == 0) gen0 = (unsigned)(ld_acquire64(&P.ctrl->word) >> 32);
     double scale = 1.0;
     for (int m = 1; m <= P.power_iters; m++) {
         double sy = 0.0, sp[1] = {0.0};
@@ -806,7 +819,7 @@ __global__ void __launch_bounds__(kThreads, (K <= 1 ? 3 : 2)) k_leja2d_tma(const
     const int NE = (int)(t1 - t0) + 3 * nseg;
 
     unsigned gen0 = 0;
-    if (tid == 0) gen0 = ld_acquire(&P.ctrl->gen);
+    if (tid == 0) gen0 = (unsigned)(ld_acquire64(&P.ctrl->word) >> 32);
     int active = P.active0;
     double d0[K];
 #pragma unroll
