@@ -83,6 +83,7 @@ struct lx_ctx {
     int coef_next = 0;
     int64_t launches = 0;
     std::vector<double> xi;
+    double* xi_dev = nullptr;             // Leja points on the device
     Comm* comm = nullptr;                 // slab decomposition (lx_comm.cpp)
     int variant = 0;                      // 2D single-GPU Leja kernel: 0 = register tiles, 1 = TMA marching
 };
@@ -198,26 +199,19 @@ static lx_status status_of(const Record& r) {
     }
 }
 
-// Build the coefficient table of one Leja call into a ring slot and enqueue its H2D.
+// Coefficient table of one Leja call ({beta_m, d_m^(k)}, m < max_nodes), built ON THE DEVICE by
+// k_coef_table (one CTA per accumulator) on the context stream: no host arithmetic, no H2D copy.
+// Ring slots keep tables of in-flight asynchronous calls apart (stream order makes reuse safe).
 static lx_status build_coefs(lx_ctx* ctx, int l, const double* coeffs, int K, double dt, double c, double gamma,
-                             const double** dev_out) {
-    const int M = ctx->max_nodes;
+                             int rec, const double** dev_out) {
     const int slot = ctx->coef_next;
     ctx->coef_next = (slot + 1) % kCoefSlots;
-    CUDA_TRY(cudaEventSynchronize(ctx->coef_ev[slot]));
-    double* tab = ctx->coef_host + slot * ctx->coef_stride;
-    std::vector<double> d(M);
-    for (int k = 0; k < K; k++) {
-        const int s = lx::divided_differences(l, ctx->xi.data(), M, dt, c, gamma, coeffs[k], d.data());
-        if (s == 6) return fail(LX_ERR_NONFINITE, "divided differences overflow (dt*gamma too large?)");
-        if (s) return fail(LX_ERR_ARG, "divided differences failed (%d)", s);
-        for (int m = 0; m < M; m++) tab[(size_t)m * (1 + K) + 1 + k] = d[m];
-    }
-    for (int m = 0; m < M; m++)
-        tab[(size_t)m * (1 + K)] = (m == 0 || dt == 0.0) ? 0.0 : (-c / gamma - ctx->xi[m - 1]);
     double* dev = ctx->coef_dev + slot * ctx->coef_stride;
-    CUDA_TRY(cudaMemcpyAsync(dev, tab, (size_t)M * (1 + K) * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    CUDA_TRY(cudaEventRecord(ctx->coef_ev[slot], ctx->stream));
+    Coef4 a;
+    for (int k = 0; k < kMaxK; k++) a.a[k] = k < K ? coeffs[k] : 1.0;
+    CUDA_TRY(launch_coef_table(ctx->xi_dev, ctx->max_nodes, l, K, a, dt, c, gamma, nullptr, dev,
+                               &ctx->rec_dev[rec].status, ctx->stream));
+    ctx->launches++;
     *dev_out = dev;
     return LX_OK;
 }
@@ -255,7 +249,7 @@ static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u,
                              const double* coeffs, int K, double dt, double c, double gamma, int l, double rtol,
                              double atol, int rec) {
     const double* coef = nullptr;
-    LX_TRY(build_coefs(ctx, l, coeffs, K, dt, c, gamma, &coef));
+    LX_TRY(build_coefs(ctx, l, coeffs, K, dt, c, gamma, rec, &coef));
     LejaParams P = base_params(ctx, pb);
     const bool diag = pb->react != 0.0;
     P.K = K;
@@ -358,6 +352,7 @@ static void free_ctx(lx_ctx* ctx) {
     cudaFree(ctx->ctrl);
     cudaFree(ctx->rec_dev);
     cudaFree(ctx->coef_dev);
+    cudaFree(ctx->xi_dev);
     cudaFreeHost(ctx->rec_host);
     cudaFreeHost(ctx->rec_init);
     cudaFreeHost(ctx->umax_host);
@@ -445,6 +440,8 @@ lx_status lx_ctx_create(const lx_problem* pb, int max_nodes, int device, void* c
     CK(cudaMalloc(&ctx->coef_dev, kCoefSlots * ctx->coef_stride * sizeof(double)));
     CK(cudaMallocHost(&ctx->coef_host, kCoefSlots * ctx->coef_stride * sizeof(double)));
     for (auto& ev : ctx->coef_ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CK(cudaMalloc(&ctx->xi_dev, max_nodes * sizeof(double)));
+    CK(cudaMemcpy(ctx->xi_dev, ctx->xi.data(), max_nodes * sizeof(double), cudaMemcpyHostToDevice));
 #undef CK
     s = alloc_local(ctx);
     if (s != LX_OK) goto bad;

@@ -144,5 +144,9 @@ int step_grid_size(int device, int nunits);
 cudaError_t launch_finalize_err(const double* gathered, int nranks, double N, Record* rec, cudaStream_t s);
 cudaError_t launch_max_u64(const unsigned long long* vals, int n, unsigned long long* out, cudaStream_t s);
 int stage_grid_size(int device, int op);
+// device coefficient table: [M][1+K] = {beta_m, d_m^(k)}; a[K] device array of vertical coefficients
+struct Coef4 { double a[kMaxK]; };
+cudaError_t launch_coef_table(const double* xi, int M, int l, int K, const Coef4& a, double dt, double c,
+                              double gamma, const double* cg_dev, double* table, int* status, cudaStream_t s);
 
 }  // namespace lx

@@ -525,13 +525,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d(const __grid_constant__ 
     double d0[K];
 #pragma unroll
     for (int k = 0; k < K; k++) d0[k] = P.coef[1 + k];
+    // coefficients of the next iteration are fetched before the barrier (off the critical path)
+    double beta_n = P.coef[1 + K], dm_n[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) dm_n[k] = P.coef[(1 + K) + 1 + k];
     for (int m = 1; m < P.max_nodes; m++) {
-        const double* cm = P.coef + (size_t)m * (1 + K);
-        const double beta = cm[0];
+        const double beta = beta_n;
         double dm[K], sp[K];
 #pragma unroll
         for (int k = 0; k < K; k++) {
-            dm[k] = cm[1 + k];
+            dm[k] = dm_n[k];
             sp[k] = 0.0;
         }
         double sy = 0.0;
@@ -549,6 +552,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d(const __grid_constant__ 
         vals[0] = sy;
 #pragma unroll
         for (int k = 0; k < K; k++) vals[1 + k] = sp[k];
+        if (m + 1 < P.max_nodes) {
+            const double* cn = P.coef + (size_t)(m + 1) * (1 + K);
+            beta_n = cn[0];
+#pragma unroll
+            for (int k = 0; k < K; k++) dm_n[k] = cn[1 + k];
+        }
         block_reduce<1 + K>(vals, s_red);
         if (tid == 0) {
             double* slot = P.partials + ((size_t)par * gridDim.x + blockIdx.x) * kSlot;
@@ -1131,6 +1140,71 @@ int leja_tma_grid_size(int device, int K, bool diag, long long band_rows) {
 
 cudaError_t launch_leja_tma(const LejaParams& P, cudaStream_t s, bool diag) {
     return tma_dispatch(P.K, diag, 0, nullptr, &P, s);
+}
+
+
+// ---------------------------------------------------------------------------
+// Coefficient table on the device: beta_m = -c/gamma - xi_{m-1} and the Newton
+// divided differences d_m^(k) of h_k(xi) = phi_l(a_k dt (c + gamma xi)) at the
+// Leja points (reading R8: triangular recurrence
+// d[i:] = (d[i:] - d[i-1]) / (xi[i:] - xi[i-1])).  One CTA per accumulator,
+// thread j owns d_j; one barrier per recurrence step.  No host work, no H2D.
+// ---------------------------------------------------------------------------
+__device__ double phi_dev(int l, double z) {
+    const double inv_fact[6] = {1.0, 1.0, 0.5, 1.0 / 6.0, 1.0 / 24.0, 1.0 / 120.0};
+    if (fabs(z) < 2.0) {
+        constexpr int NT = 34;
+        double c[NT];
+        double f = inv_fact[l];
+        c[0] = f;
+        for (int k = 1; k < NT; k++) {
+            f /= (double)(k + l);
+            c[k] = f;
+        }
+        double s = c[NT - 1];
+        for (int k = NT - 2; k >= 0; k--) s = fma(s, z, c[k]);
+        return s;
+    }
+    double p = exp(z);
+    for (int j = 0; j < l; j++) p = (p - inv_fact[j]) / z;
+    return p;
+}
+
+__global__ void k_coef_table(const double* xi, int M, int l, int K, Coef4 a, double dt, double c, double gamma,
+                             const double* cg_dev, double* table, int* status) {
+    extern __shared__ double sh[];
+    double* d = sh;        // [M]
+    double* x = sh + M;    // [M]
+    const int k = blockIdx.x;
+    if (cg_dev) {          // (c, gamma) computed on the device (spectrum kernel)
+        c = cg_dev[0];
+        gamma = cg_dev[1];
+    }
+    const double ak = a.a[k];
+    for (int j = threadIdx.x; j < M; j += blockDim.x) {
+        x[j] = xi[j];
+        d[j] = phi_dev(l, ak * dt * (c + gamma * xi[j]));
+    }
+    for (int i = 1; i < M; i++) {
+        __syncthreads();   // d[i-1] final (written at step i-1); not modified during step i
+        const double di = d[i - 1], xi_i = x[i - 1];
+        for (int j = threadIdx.x; j < M; j += blockDim.x)
+            if (j >= i) d[j] = (d[j] - di) / (x[j] - xi_i);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < M; j += blockDim.x) {
+        const double v = d[j];
+        table[(size_t)j * (1 + K) + 1 + k] = v;
+        if (!isfinite(v)) atomicExch(status, 6);
+        if (k == 0) table[(size_t)j * (1 + K)] = (j == 0 || dt == 0.0) ? 0.0 : (-c / gamma - x[j - 1]);
+    }
+}
+
+cudaError_t launch_coef_table(const double* xi, int M, int l, int K, const Coef4& a, double dt, double c,
+                              double gamma, const double* cg_dev, double* table, int* status, cudaStream_t s) {
+    const int threads = M < 1024 ? ((M + 31) / 32) * 32 : 1024;
+    k_coef_table<<<K, threads, 2 * M * sizeof(double), s>>>(xi, M, l, K, a, dt, c, gamma, cg_dev, table, status);
+    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
