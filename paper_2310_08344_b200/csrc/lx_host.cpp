@@ -199,20 +199,33 @@ static lx_status status_of(const Record& r) {
     }
 }
 
-// Coefficient table of one Leja call ({beta_m, d_m^(k)}, m < max_nodes), built ON THE DEVICE by
-// k_coef_table (one CTA per accumulator) on the context stream: no host arithmetic, no H2D copy.
-// Ring slots keep tables of in-flight asynchronous calls apart (stream order makes reuse safe).
-static lx_status build_coefs(lx_ctx* ctx, int l, const double* coeffs, int K, double dt, double c, double gamma,
-                             int rec, const double** dev_out) {
-    const int slot = ctx->coef_next;
-    ctx->coef_next = (slot + 1) % kCoefSlots;
-    double* dev = ctx->coef_dev + slot * ctx->coef_stride;
-    Coef4 a;
-    for (int k = 0; k < kMaxK; k++) a.a[k] = k < K ? coeffs[k] : 1.0;
-    CUDA_TRY(launch_coef_table(ctx->xi_dev, ctx->max_nodes, l, K, a, dt, c, gamma, nullptr, dev,
-                               &ctx->rec_dev[rec].status, ctx->stream));
+// Coefficient tables ({beta_m, d_m^(k)}, m < max_nodes) of one or several Leja calls, built ON THE
+// DEVICE by one k_coef_tables launch (one CTA per accumulator) on the context stream: no host
+// arithmetic, no H2D copy.  Ring slots keep tables of in-flight calls apart (stream order makes
+// reuse safe).
+struct TableSpec {
+    int l;
+    int K;
+    const double* coeffs;
+};
+
+static lx_status build_tables(lx_ctx* ctx, const TableSpec* specs, int n, double dt, double c, double gamma, int rec,
+                              const double** tables_out) {
+    CoefJobs jobs;
+    std::memset(&jobs, 0, sizeof jobs);
+    for (int t = 0; t < n; t++) {
+        const int slot = ctx->coef_next;
+        ctx->coef_next = (slot + 1) % kCoefSlots;
+        double* dev = ctx->coef_dev + slot * ctx->coef_stride;
+        tables_out[t] = dev;
+        for (int k = 0; k < specs[t].K; k++) {
+            if (jobs.n >= 16) return fail(LX_ERR_ARG, "too many coefficient tables in one batch");
+            jobs.j[jobs.n++] = CoefJob{dev, specs[t].coeffs[k], specs[t].l, specs[t].K, k};
+        }
+    }
+    CUDA_TRY(launch_coef_tables(ctx->xi_dev, ctx->max_nodes, jobs, dt, c, gamma, nullptr, &ctx->rec_dev[rec].status,
+                                ctx->stream));
     ctx->launches++;
-    *dev_out = dev;
     return LX_OK;
 }
 
@@ -247,9 +260,12 @@ static LejaParams base_params(lx_ctx* ctx, const lx_problem* pb) {
 // Core Leja call on device pointers (no staging, no sync).
 static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u, const double* v, double* const* outs,
                              const double* coeffs, int K, double dt, double c, double gamma, int l, double rtol,
-                             double atol, int rec) {
-    const double* coef = nullptr;
-    LX_TRY(build_coefs(ctx, l, coeffs, K, dt, c, gamma, rec, &coef));
+                             double atol, int rec, const double* table = nullptr) {
+    const double* coef = table;
+    if (!coef) {
+        const TableSpec spec{l, K, coeffs};
+        LX_TRY(build_tables(ctx, &spec, 1, dt, c, gamma, rec, &coef));
+    }
     LejaParams P = base_params(ctx, pb);
     const bool diag = pb->react != 0.0;
     P.K = K;
@@ -731,6 +747,29 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
     double* S0 = scratch(ctx, 0);
     if (!S0) return fail(LX_ERR_CUDA, "scratch allocation failed");
     const double one = 1.0;
+    // all coefficient tables of the step in one device launch
+    static const double c1[1] = {1.0}, c2[2] = {0.5, 1.0}, c3[3] = {0.5, 2.0 / 3.0, 1.0};
+    const double* tab[4] = {nullptr, nullptr, nullptr, nullptr};
+    {
+        TableSpec specs[4];
+        int n = 0;
+        if (method == LX_ROSENBROCK_EULER) {
+            specs[n++] = {1, 1, c1};
+        } else if (method == LX_EXPRB32) {
+            specs[n++] = {1, 1, c1};
+            specs[n++] = {3, 1, c1};
+        } else if (method == LX_EXPRB43) {
+            specs[n++] = {1, 2, c2};
+            specs[n++] = {1, 1, c1};
+            specs[n++] = {3, 1, c1};
+            specs[n++] = {4, 1, c1};
+        } else {
+            specs[n++] = {1, 3, c3};
+            specs[n++] = {3, 1, c1};
+            specs[n++] = {4, 1, c1};
+        }
+        LX_TRY(build_tables(ctx, specs, n, dt, c, gamma, rec, tab));
+    }
     // f_u = RHS(u) * dt   (alg:Ros_Eu P:468-469)
     LX_TRY(rhs_device(ctx, pb, u, dt, S0));
     StageArgs A = stage_args(ctx, pb, rec);
@@ -738,7 +777,7 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
     A.u = u;
     if (method == LX_ROSENBROCK_EULER) {
         double* o[1] = {hi};
-        LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 1, rtol, atol, rec));
+        LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 1, rtol, atol, rec, tab[0]));
         A.x0 = u; A.x1 = hi; A.y0 = hi; A.a0 = 1.0; A.a1 = 1.0;  // u_exprb2 = u + phi_1(J dt) f dt
         LX_TRY(run_stage(ctx, ST_AXPBY, A));
         if (lo && lo != hi) CUDA_TRY(cudaMemcpyAsync(lo, hi, ctx->N_loc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
@@ -747,10 +786,10 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
     if (method == LX_EXPRB32) {
         // P:414-418, alg:exprb32: u_flux (in hi) -> a (lo), R_a (S0) -> u_nl_3 (hi) -> u_3 = a + 2 u_nl_3
         double* o[1] = {hi};
-        LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 1, rtol, atol, rec));
+        LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 1, rtol, atol, rec, tab[0]));
         A.x0 = u; A.x1 = hi; A.y1 = lo; A.y0 = S0;
         LX_TRY(run_stage(ctx, ST_EXPRB32_A, A));
-        LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 3, rtol, atol, rec));
+        LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 3, rtol, atol, rec, tab[1]));
         A = stage_args(ctx, pb, rec);
         A.x0 = lo; A.x1 = hi; A.y0 = hi;
         return run_stage(ctx, ST_FINAL_EXPRB32, A);
@@ -763,7 +802,7 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
     if (!S1 || !S2 || (epirk && !S3)) return fail(LX_ERR_CUDA, "scratch allocation failed");
     const double cf2[2] = {0.5, 1.0}, cf3[3] = {0.5, 2.0 / 3.0, 1.0};
     double* pv[3] = {S1, S2, S3};
-    LX_TRY(leja_device(ctx, pb, ul, S0, pv, epirk ? cf3 : cf2, epirk ? 3 : 2, dt, c, gamma, 1, rtol, atol, rec));
+    LX_TRY(leja_device(ctx, pb, ul, S0, pv, epirk ? cf3 : cf2, epirk ? 3 : 2, dt, c, gamma, 1, rtol, atol, rec, tab[0]));
     double* p_one = epirk ? S3 : S2;
     // D_a = dt F(u + 1/2 p_half) - dt F(u)  -> S0
     A.x0 = u; A.x1 = S1; A.x2 = nullptr; A.a0 = 0.5; A.a1 = 0.0; A.y0 = S0;
@@ -777,7 +816,7 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
     } else {
         // phi_1(hJ) D_a -> S1 ; b = u + p_one + S1 ; D_b -> lo
         double* o[1] = {S1};
-        LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 1, rtol, atol, rec));
+        LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 1, rtol, atol, rec, tab[1]));
         A.x0 = u; A.x1 = p_one; A.x2 = S1; A.a0 = 1.0; A.a1 = 1.0; A.y0 = lo;
         LX_TRY(run_stage(ctx, ST_STAGE_REMAINDER, A));
         Db = lo;
@@ -793,9 +832,9 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
     double* q3 = S0;
     double* q4 = epirk ? S1 : lo;
     double* o3[1] = {q3};
-    LX_TRY(leja_device(ctx, pb, ul, w3, o3, &one, 1, dt, c, gamma, 3, rtol, atol, rec));
+    LX_TRY(leja_device(ctx, pb, ul, w3, o3, &one, 1, dt, c, gamma, 3, rtol, atol, rec, tab[epirk ? 1 : 2]));
     double* o4[1] = {q4};
-    LX_TRY(leja_device(ctx, pb, ul, hi, o4, &one, 1, dt, c, gamma, 4, rtol, atol, rec));
+    LX_TRY(leja_device(ctx, pb, ul, hi, o4, &one, 1, dt, c, gamma, 4, rtol, atol, rec, tab[epirk ? 2 : 3]));
     // u3 = u + p_one + q3 -> lo ; u4 = u3 + q4 -> hi ; err = ||u4 - u3||
     A = stage_args(ctx, pb, rec);
     A.x0 = u; A.x1 = p_one; A.x2 = q3; A.x3 = q4; A.y0 = lo; A.y1 = hi;

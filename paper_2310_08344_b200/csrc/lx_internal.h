@@ -145,8 +145,16 @@ cudaError_t launch_finalize_err(const double* gathered, int nranks, double N, Re
 cudaError_t launch_max_u64(const unsigned long long* vals, int n, unsigned long long* out, cudaStream_t s);
 int stage_grid_size(int device, int op);
 // device coefficient table: [M][1+K] = {beta_m, d_m^(k)}; a[K] device array of vertical coefficients
-struct Coef4 { double a[kMaxK]; };
-cudaError_t launch_coef_table(const double* xi, int M, int l, int K, const Coef4& a, double dt, double c,
-                              double gamma, const double* cg_dev, double* table, int* status, cudaStream_t s);
+struct CoefJob {
+    double* table;   // [M][1+K]
+    double a;        // vertical coefficient of accumulator k
+    int l, K, k;
+};
+struct CoefJobs {
+    CoefJob j[16];
+    int n;
+};
+cudaError_t launch_coef_tables(const double* xi, int M, const CoefJobs& jobs, double dt, double c, double gamma,
+                               const double* cg_dev, int* status, cudaStream_t s);
 
 }  // namespace lx

@@ -1170,40 +1170,49 @@ __device__ double phi_dev(int l, double z) {
     return p;
 }
 
-__global__ void k_coef_table(const double* xi, int M, int l, int K, Coef4 a, double dt, double c, double gamma,
-                             const double* cg_dev, double* table, int* status) {
+// Critical path per recurrence step: one bar.sync, one shared load of d_{i-1},
+// one subtract and one multiply; the reciprocal 1/(xi_j - xi_{i-1}) of the
+// next step is computed meanwhile.  Thread j publishes d_j when it becomes final
+// (step j).  Rounding differs from the host division form by <= 1 ulp per step.
+__global__ void k_coef_tables(const double* xi, int M, CoefJobs jobs, double dt, double c, double gamma,
+                              const double* cg_dev, int* status) {
     extern __shared__ double sh[];
-    double* d = sh;        // [M]
-    double* x = sh + M;    // [M]
-    const int k = blockIdx.x;
-    if (cg_dev) {          // (c, gamma) computed on the device (spectrum kernel)
+    double* dsh = sh;        // [M] published final values
+    double* x = sh + M;      // [M]
+    const CoefJob J = jobs.j[blockIdx.x];
+    if (cg_dev) {
         c = cg_dev[0];
         gamma = cg_dev[1];
     }
-    const double ak = a.a[k];
-    for (int j = threadIdx.x; j < M; j += blockDim.x) {
-        x[j] = xi[j];
-        d[j] = phi_dev(l, ak * dt * (c + gamma * xi[j]));
-    }
-    for (int i = 1; i < M; i++) {
-        __syncthreads();   // d[i-1] final (written at step i-1); not modified during step i
-        const double di = d[i - 1], xi_i = x[i - 1];
-        for (int j = threadIdx.x; j < M; j += blockDim.x)
-            if (j >= i) d[j] = (d[j] - di) / (x[j] - xi_i);
-    }
+    const int j = threadIdx.x;
+    for (int t = threadIdx.x; t < M; t += blockDim.x) x[t] = xi[t];
     __syncthreads();
-    for (int j = threadIdx.x; j < M; j += blockDim.x) {
-        const double v = d[j];
-        table[(size_t)j * (1 + K) + 1 + k] = v;
-        if (!isfinite(v)) atomicExch(status, 6);
-        if (k == 0) table[(size_t)j * (1 + K)] = (j == 0 || dt == 0.0) ? 0.0 : (-c / gamma - x[j - 1]);
+    const bool own = j < M;
+    const double xj = own ? x[j] : 0.0;
+    double dj = own ? phi_dev(J.l, J.a * dt * (c + gamma * xj)) : 0.0;
+    if (j == 0) dsh[0] = dj;                       // d_0 = h(xi_0) is final
+    double r = (own && j >= 1) ? __drcp_rn(xj - x[0]) : 0.0;
+    for (int i = 1; i < M; i++) {
+        __syncthreads();                           // d_{i-1} published at step i-1
+        const double di = dsh[i - 1];
+        if (own && j >= i) {
+            dj = (dj - di) * r;
+            if (j == i) dsh[j] = dj;
+            if (j > i) r = __drcp_rn(xj - x[i]);  // for step i+1
+        }
+    }
+    if (own) {
+        J.table[(size_t)j * (1 + J.K) + 1 + J.k] = dj;
+        if (!isfinite(dj)) atomicExch(status, 6);
+        if (J.k == 0) J.table[(size_t)j * (1 + J.K)] = (j == 0 || dt == 0.0) ? 0.0 : (-c / gamma - x[j - 1]);
     }
 }
 
-cudaError_t launch_coef_table(const double* xi, int M, int l, int K, const Coef4& a, double dt, double c,
-                              double gamma, const double* cg_dev, double* table, int* status, cudaStream_t s) {
-    const int threads = M < 1024 ? ((M + 31) / 32) * 32 : 1024;
-    k_coef_table<<<K, threads, 2 * M * sizeof(double), s>>>(xi, M, l, K, a, dt, c, gamma, cg_dev, table, status);
+cudaError_t launch_coef_tables(const double* xi, int M, const CoefJobs& jobs, double dt, double c, double gamma,
+                               const double* cg_dev, int* status, cudaStream_t s) {
+    const int threads = ((M + 31) / 32) * 32;
+    if (threads > 1024 || jobs.n < 1) return cudaErrorInvalidValue;
+    k_coef_tables<<<jobs.n, threads, 2 * M * sizeof(double), s>>>(xi, M, jobs, dt, c, gamma, cg_dev, status);
     return cudaGetLastError();
 }
 
