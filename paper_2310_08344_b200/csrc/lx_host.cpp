@@ -84,6 +84,7 @@ struct lx_ctx {
     int64_t launches = 0;
     std::vector<double> xi;
     double* xi_dev = nullptr;             // Leja points on the device
+    double* rcp_dev = nullptr;            // [M][M]: 1/(xi_j - xi_i), j > i (divided-difference recurrence)
     Comm* comm = nullptr;                 // slab decomposition (lx_comm.cpp)
     int variant = 0;                      // 2D single-GPU Leja kernel: 0 = register tiles, 1 = TMA marching
 };
@@ -223,8 +224,8 @@ static lx_status build_tables(lx_ctx* ctx, const TableSpec* specs, int n, double
             jobs.j[jobs.n++] = CoefJob{dev, specs[t].coeffs[k], specs[t].l, specs[t].K, k};
         }
     }
-    CUDA_TRY(launch_coef_tables(ctx->xi_dev, ctx->max_nodes, jobs, dt, c, gamma, nullptr, &ctx->rec_dev[rec].status,
-                                ctx->stream));
+    CUDA_TRY(launch_coef_tables(ctx->xi_dev, ctx->rcp_dev, ctx->max_nodes, jobs, dt, c, gamma, nullptr,
+                                &ctx->rec_dev[rec].status, ctx->stream));
     ctx->launches++;
     return LX_OK;
 }
@@ -369,6 +370,7 @@ static void free_ctx(lx_ctx* ctx) {
     cudaFree(ctx->rec_dev);
     cudaFree(ctx->coef_dev);
     cudaFree(ctx->xi_dev);
+    cudaFree(ctx->rcp_dev);
     cudaFreeHost(ctx->rec_host);
     cudaFreeHost(ctx->rec_init);
     cudaFreeHost(ctx->umax_host);
@@ -458,6 +460,13 @@ lx_status lx_ctx_create(const lx_problem* pb, int max_nodes, int device, void* c
     for (auto& ev : ctx->coef_ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     CK(cudaMalloc(&ctx->xi_dev, max_nodes * sizeof(double)));
     CK(cudaMemcpy(ctx->xi_dev, ctx->xi.data(), max_nodes * sizeof(double), cudaMemcpyHostToDevice));
+    {
+        std::vector<double> R((size_t)max_nodes * max_nodes, 0.0);
+        for (int i = 0; i < max_nodes; i++)
+            for (int j = i + 1; j < max_nodes; j++) R[(size_t)i * max_nodes + j] = 1.0 / (ctx->xi[j] - ctx->xi[i]);
+        CK(cudaMalloc(&ctx->rcp_dev, R.size() * sizeof(double)));
+        CK(cudaMemcpy(ctx->rcp_dev, R.data(), R.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
 #undef CK
     s = alloc_local(ctx);
     if (s != LX_OK) goto bad;

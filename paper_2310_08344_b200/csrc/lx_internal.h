@@ -154,7 +154,8 @@ struct CoefJobs {
     CoefJob j[16];
     int n;
 };
-cudaError_t launch_coef_tables(const double* xi, int M, const CoefJobs& jobs, double dt, double c, double gamma,
-                               const double* cg_dev, int* status, cudaStream_t s);
+// R[i*M + j] = 1/(xi_j - xi_i) for j > i (per-context table)
+cudaError_t launch_coef_tables(const double* xi, const double* R, int M, const CoefJobs& jobs, double dt, double c,
+                               double gamma, const double* cg_dev, int* status, cudaStream_t s);
 
 }  // namespace lx

@@ -1152,17 +1152,13 @@ cudaError_t launch_leja_tma(const LejaParams& P, cudaStream_t s, bool diag) {
 // ---------------------------------------------------------------------------
 __device__ double phi_dev(int l, double z) {
     const double inv_fact[6] = {1.0, 1.0, 0.5, 1.0 / 6.0, 1.0 / 24.0, 1.0 / 120.0};
-    if (fabs(z) < 2.0) {
-        constexpr int NT = 34;
-        double c[NT];
-        double f = inv_fact[l];
-        c[0] = f;
-        for (int k = 1; k < NT; k++) {
-            f /= (double)(k + l);
-            c[k] = f;
+    if (fabs(z) < 2.0) {   // Taylor: sum_k z^k/(k+l)!  (34 terms: 2^34/34! ~ 1e-29)
+        double term = inv_fact[l], s = term;
+#pragma unroll
+        for (int k = 1; k < 34; k++) {
+            term *= z / (double)(k + l);
+            s += term;
         }
-        double s = c[NT - 1];
-        for (int k = NT - 2; k >= 0; k--) s = fma(s, z, c[k]);
         return s;
     }
     double p = exp(z);
@@ -1170,49 +1166,55 @@ __device__ double phi_dev(int l, double z) {
     return p;
 }
 
-// Critical path per recurrence step: one bar.sync, one shared load of d_{i-1},
-// one subtract and one multiply; the reciprocal 1/(xi_j - xi_{i-1}) of the
-// next step is computed meanwhile.  Thread j publishes d_j when it becomes final
-// (step j).  Rounding differs from the host division form by <= 1 ulp per step.
-__global__ void k_coef_tables(const double* xi, int M, CoefJobs jobs, double dt, double c, double gamma,
-                              const double* cg_dev, int* status) {
-    extern __shared__ double sh[];
-    double* dsh = sh;        // [M] published final values
-    double* x = sh + M;      // [M]
+// Critical path per recurrence step: one bar.sync, one shared load of the
+// published d_{i-1}, one subtract, one multiply by the precomputed reciprocal
+// R[i-1][j] = 1/(xi_j - xi_{i-1}) (per-context table, prefetched 4 steps ahead).
+// Thread j publishes d_j when it becomes final (step j).
+__global__ void k_coef_tables(const double* xi, const double* R, int M, CoefJobs jobs, double dt, double c,
+                              double gamma, const double* cg_dev, int* status) {
+    extern __shared__ double dsh[];   // [M] published final values
     const CoefJob J = jobs.j[blockIdx.x];
     if (cg_dev) {
         c = cg_dev[0];
         gamma = cg_dev[1];
     }
     const int j = threadIdx.x;
-    for (int t = threadIdx.x; t < M; t += blockDim.x) x[t] = xi[t];
-    __syncthreads();
     const bool own = j < M;
-    const double xj = own ? x[j] : 0.0;
+    const double xj = own ? xi[j] : 0.0;
     double dj = own ? phi_dev(J.l, J.a * dt * (c + gamma * xj)) : 0.0;
-    if (j == 0) dsh[0] = dj;                       // d_0 = h(xi_0) is final
-    double r = (own && j >= 1) ? __drcp_rn(xj - x[0]) : 0.0;
-    for (int i = 1; i < M; i++) {
-        __syncthreads();                           // d_{i-1} published at step i-1
-        const double di = dsh[i - 1];
-        if (own && j >= i) {
-            dj = (dj - di) * r;
-            if (j == i) dsh[j] = dj;
-            if (j > i) r = __drcp_rn(xj - x[i]);  // for step i+1
+    if (j == 0) dsh[0] = dj;   // d_0 = h(xi_0) is final
+    double rr[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) rr[q] = (own && q + 1 < M && j > q) ? __ldg(R + (size_t)q * M + j) : 0.0;
+    for (int i0 = 1; i0 < M; i0 += 4) {
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const int i = i0 + q;
+            if (i < M) {
+                const double r = rr[q];
+                const int ip = i + 3;   // row of step i + 4
+                rr[q] = (own && ip + 1 < M && j > ip) ? __ldg(R + (size_t)ip * M + j) : 0.0;
+                __syncthreads();
+                const double di = dsh[i - 1];
+                if (own && j >= i) {
+                    dj = (dj - di) * r;
+                    if (j == i) dsh[j] = dj;
+                }
+            }
         }
     }
     if (own) {
         J.table[(size_t)j * (1 + J.K) + 1 + J.k] = dj;
         if (!isfinite(dj)) atomicExch(status, 6);
-        if (J.k == 0) J.table[(size_t)j * (1 + J.K)] = (j == 0 || dt == 0.0) ? 0.0 : (-c / gamma - x[j - 1]);
+        if (J.k == 0) J.table[(size_t)j * (1 + J.K)] = (j == 0 || dt == 0.0) ? 0.0 : (-c / gamma - xi[j - 1]);
     }
 }
 
-cudaError_t launch_coef_tables(const double* xi, int M, const CoefJobs& jobs, double dt, double c, double gamma,
-                               const double* cg_dev, int* status, cudaStream_t s) {
+cudaError_t launch_coef_tables(const double* xi, const double* R, int M, const CoefJobs& jobs, double dt, double c,
+                               double gamma, const double* cg_dev, int* status, cudaStream_t s) {
     const int threads = ((M + 31) / 32) * 32;
     if (threads > 1024 || jobs.n < 1) return cudaErrorInvalidValue;
-    k_coef_tables<<<jobs.n, threads, 2 * M * sizeof(double), s>>>(xi, M, jobs, dt, c, gamma, cg_dev, status);
+    k_coef_tables<<<jobs.n, threads, M * sizeof(double), s>>>(xi, R, M, jobs, dt, c, gamma, cg_dev, status);
     return cudaGetLastError();
 }
 
