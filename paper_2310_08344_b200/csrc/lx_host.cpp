@@ -262,13 +262,30 @@ static LejaParams base_params(lx_ctx* ctx, const lx_problem* pb) {
 static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u, const double* v, double* const* outs,
                              const double* coeffs, int K, double dt, double c, double gamma, int l, double rtol,
                              double atol, int rec, const double* table = nullptr) {
+    const bool tma = ctx->ndim == 2 && ctx->variant == 1 && !ctx->comm;
     const double* coef = table;
-    if (!coef) {
+    if (!coef && tma) {   // the experimental TMA kernel reads a prebuilt table
         const TableSpec spec{l, K, coeffs};
         LX_TRY(build_tables(ctx, &spec, 1, dt, c, gamma, rec, &coef));
     }
     LejaParams P = base_params(ctx, pb);
     const bool diag = pb->react != 0.0;
+    if (!coef) {
+        // the Leja kernels compute their own Newton coefficients (coefficient warp) into a ring slot
+        const int slot = ctx->coef_next;
+        ctx->coef_next = (slot + 1) % kCoefSlots;
+        double* tab = ctx->coef_dev + slot * ctx->coef_stride;
+        P.coef_gen = 1;
+        P.l = l;
+        P.cdt = dt;
+        P.cc = c;
+        P.cgamma = gamma;
+        for (int k = 0; k < kMaxK; k++) P.ak[k] = k < K ? coeffs[k] : 1.0;
+        P.xi = ctx->xi_dev;
+        P.R = ctx->rcp_dev;
+        P.table = tab;
+        coef = tab;
+    }
     P.K = K;
     P.max_nodes = ctx->max_nodes;
     P.active0 = (1 << K) - 1;
@@ -759,7 +776,7 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
     // all coefficient tables of the step in one device launch
     static const double c1[1] = {1.0}, c2[2] = {0.5, 1.0}, c3[3] = {0.5, 2.0 / 3.0, 1.0};
     const double* tab[4] = {nullptr, nullptr, nullptr, nullptr};
-    {
+    if (ctx->ndim == 2 && ctx->variant == 1 && !ctx->comm) {   // experimental TMA kernel: prebuilt tables
         TableSpec specs[4];
         int n = 0;
         if (method == LX_ROSENBROCK_EULER) {

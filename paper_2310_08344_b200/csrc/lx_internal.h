@@ -96,6 +96,15 @@ struct LejaParams {
     double* rank_part;
     const double* gathered;
     int nranks;
+    // In-kernel coefficients: the kernel fills `table` ([max_nodes][1+K]: beta_m,
+    // d_m^(k)) itself, two iterations ahead, on a dedicated coefficient warp (CTA 0, warp 0).
+    int coef_gen;
+    int l;
+    double cdt, cc, cgamma;
+    double ak[kMaxK];
+    const double* xi;     // [max_nodes] Leja points
+    const double* R;      // [max_nodes][max_nodes]: 1/(xi_j - xi_i), j > i
+    double* table;        // == coef
 };
 
 // launchers (lx_kernels.cu)

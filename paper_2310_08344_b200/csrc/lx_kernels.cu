@@ -60,6 +60,75 @@ __device__ __forceinline__ const double* rowp(const RowSrc& s, int r) {
     return s.base + (long long)(r < 0 ? r + s.n_loc : r - s.n_loc) * s.stride;
 }
 
+__device__ double phi_dev(int l, double z) {
+    const double inv_fact[6] = {1.0, 1.0, 0.5, 1.0 / 6.0, 1.0 / 24.0, 1.0 / 120.0};
+    if (fabs(z) < 2.0) {   // Taylor: sum_k z^k/(k+l)!  (34 terms: 2^34/34! ~ 1e-29)
+        double term = inv_fact[l], s = term;
+#pragma unroll
+        for (int k = 1; k < 34; k++) {
+            term *= z / (double)(k + l);
+            s += term;
+        }
+        return s;
+    }
+    double p = exp(z);
+    for (int j = 0; j < l; j++) p = (p - inv_fact[j]) / z;
+    return p;
+}
+
+// ---------------------------------------------------------------------------
+// In-kernel Newton divided differences (reading R8).  Column form
+// of the triangular recurrence: d_j = fold_{i<j} (d - d_i) * R[i][j] starting at
+// d = h_j = phi_l(a dt (c + gamma xi_j)); it needs only the FINAL d_0..d_{j-1},
+// so the coefficient warp computes d_{m+2} during iteration m (reading its own
+// earlier rows of the table) -- overlapped with the stencil work, no table
+// launch and no host arithmetic.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double coef_h(const LejaParams& P, int k, int j) {
+    return phi_dev(P.l, P.ak[k] * P.cdt * (P.cc + P.cgamma * P.xi[j]));
+}
+
+__device__ __forceinline__ double coef_fold(const LejaParams& P, int K, int k, int j) {
+    double d = coef_h(P, k, j);
+    const int M = P.max_nodes;
+    const double* tab = P.table + 1 + k;
+    const double* Rc = P.R + j;
+    int i = 0;
+    for (; i + 4 <= j; i += 4) {
+        const double t0 = tab[(size_t)i * (1 + K)], t1 = tab[(size_t)(i + 1) * (1 + K)];
+        const double t2 = tab[(size_t)(i + 2) * (1 + K)], t3 = tab[(size_t)(i + 3) * (1 + K)];
+        const double r0 = Rc[(size_t)i * M], r1 = Rc[(size_t)(i + 1) * M];
+        const double r2 = Rc[(size_t)(i + 2) * M], r3 = Rc[(size_t)(i + 3) * M];
+        d = (d - t0) * r0;
+        d = (d - t1) * r1;
+        d = (d - t2) * r2;
+        d = (d - t3) * r3;
+    }
+    for (; i < j; i++) d = (d - tab[(size_t)i * (1 + K)]) * Rc[(size_t)i * M];
+    return d;
+}
+
+// d_0, d_1, d_2 of accumulator k (computed redundantly by every thread in the prologue).
+__device__ __forceinline__ void coef_first3(const LejaParams& P, int k, double& d0, double& d1, double& d2) {
+    const int M = P.max_nodes;
+    d0 = coef_h(P, k, 0);
+    d1 = M > 1 ? (coef_h(P, k, 1) - d0) * P.R[1] : 0.0;
+    d2 = M > 2 ? ((coef_h(P, k, 2) - d0) * P.R[2] - d1) * P.R[M + 2] : 0.0;
+}
+
+// Coefficient warp: write rows 0..2 (prologue) or row j (>= 3) of the table.
+template <int K>
+__device__ __forceinline__ void coef_write_row(const LejaParams& P, int j, int lane, int active, const double* dk) {
+    if (j >= P.max_nodes) return;
+    double* row = P.table + (size_t)j * (1 + K);
+    if (lane == 0) row[0] = (j == 0 || P.cdt == 0.0) ? 0.0 : (-P.cc / P.cgamma - P.xi[j - 1]);
+    if (lane < K && ((active >> lane) & 1)) row[1 + lane] = dk ? dk[lane] : coef_fold(P, K, lane, j);
+}
+
+__device__ __forceinline__ double coef_beta(const LejaParams& P, int m) {
+    return (P.cdt == 0.0) ? 0.0 : (-P.cc / P.cgamma - P.xi[m - 1]);
+}
+
 // Deterministic block reduction of n values: xor-butterfly inside warps, then
 // warps summed in index order by thread 0.  Result valid in thread 0.
 template <int N>
@@ -519,17 +588,27 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d(const __grid_constant__ 
     __shared__ double s_red[kWarps][kSlot];
     __shared__ int s_flags[4];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // warp 0 of CTA 0 computes the Newton coefficients two iterations ahead; all
+    // other warps share the stencil units
+    const bool cwarp = (blockIdx.x == 0 && warp == 0);
+    const int gw = blockIdx.x * kWarps + warp - 1;
+    const int W = gridDim.x * kWarps - 1;
     unsigned gen0 = 0;
     if (tid == 0) gen0 = (unsigned)(ld_acquire64(&P.ctrl->word) >> 32);
     int active = P.active0;
-    double d0[K];
+    const int M = P.max_nodes;
+    double d0[K], d1[K], d2[K];
 #pragma unroll
-    for (int k = 0; k < K; k++) d0[k] = P.coef[1 + k];
-    // coefficients of the next iteration are fetched before the barrier (off the critical path)
-    double beta_n = P.coef[1 + K], dm_n[K];
+    for (int k = 0; k < K; k++) coef_first3(P, k, d0[k], d1[k], d2[k]);
+    if (cwarp) {
+        coef_write_row<K>(P, 0, lane, active, d0);
+        coef_write_row<K>(P, 1, lane, active, d1);
+        coef_write_row<K>(P, 2, lane, active, d2);
+    }
+    double beta_n = coef_beta(P, 1), dm_n[K];
 #pragma unroll
-    for (int k = 0; k < K; k++) dm_n[k] = P.coef[(1 + K) + 1 + k];
-    for (int m = 1; m < P.max_nodes; m++) {
+    for (int k = 0; k < K; k++) dm_n[k] = d1[k];
+    for (int m = 1; m < M; m++) {
         const double beta = beta_n;
         double dm[K], sp[K];
 #pragma unroll
@@ -540,23 +619,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d(const __grid_constant__ 
         double sy = 0.0;
         const int par = m & 1;
         double* dst = P.ydst[par];
-        if (m == 1) {
-            for (int unit = blockIdx.x * kWarps + warp; unit < P.nunits; unit += gridDim.x * kWarps)
+        if (cwarp) {
+            if (m + 2 < M) coef_write_row<K>(P, m + 2, lane, active, nullptr);
+        } else if (m == 1) {
+            for (int unit = gw; unit < P.nunits; unit += W)
                 tile<NDIM, K, DIAG, true, M_LEJA, true>(P, P.v, dst, unit, lane, beta, d0, dm, active, 0.0, sy, sp);
         } else {
             const RowSrc src = P.ysrc[par ^ 1];
-            for (int unit = blockIdx.x * kWarps + warp; unit < P.nunits; unit += gridDim.x * kWarps)
+            for (int unit = gw; unit < P.nunits; unit += W)
                 tile<NDIM, K, DIAG, false, M_LEJA, false>(P, src, dst, unit, lane, beta, d0, dm, active, 0.0, sy, sp);
         }
         double vals[1 + K];
         vals[0] = sy;
 #pragma unroll
         for (int k = 0; k < K; k++) vals[1 + k] = sp[k];
-        if (m + 1 < P.max_nodes) {
-            const double* cn = P.coef + (size_t)(m + 1) * (1 + K);
-            beta_n = cn[0];
+        // coefficients of iteration m+1, fetched before the barrier: row m+1 was written during
+        // iteration m-1 and released by barrier m-1
+        if (m + 1 < M) {
+            beta_n = coef_beta(P, m + 1);
 #pragma unroll
-            for (int k = 0; k < K; k++) dm_n[k] = cn[1 + k];
+            for (int k = 0; k < K; k++) dm_n[k] = (m + 1 == 2) ? d2[k] : P.table[(size_t)(m + 1) * (1 + K) + 1 + k];
         }
         block_reduce<1 + K>(vals, s_red);
         if (tid == 0) {
@@ -641,6 +723,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d_step(const __grid_consta
     Ctrl* ctrl = P.ctrl;
     if (*(volatile int*)&ctrl->done) return;
     const bool writer = blockIdx.x == 0 && threadIdx.x == 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool cwarp = (blockIdx.x == 0 && warp == 0);   // coefficient warp: row m+2 of the table
+    const int M = P.max_nodes;
     int active = P.active0;
     if (m >= 2) {
         const int prev = *(volatile int*)&ctrl->hist[m & 1];   // mask after iteration m-2
@@ -651,9 +736,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d_step(const __grid_consta
             for (int r = 0; r < P.nranks; r++) s += P.gathered[r * kSlot + i];
             sums[i] = s;
         }
-        double dmp[K];
+        double dmp[K];   // d_{m-1}: row written by launch 1 (m-1 <= 2) or launch m-3
 #pragma unroll
-        for (int k = 0; k < K; k++) dmp[k] = P.coef[(size_t)(m - 1) * (1 + K) + 1 + k];
+        for (int k = 0; k < K; k++) dmp[k] = P.table[(size_t)(m - 1) * (1 + K) + 1 + k];
         int act = prev, done = 0, status = 0;
         leja_decide<K>(P, m - 1, sums, dmp, act, done, status, writer ? P.rec : nullptr);
         if (writer) {
@@ -667,26 +752,48 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d_step(const __grid_consta
         if (done) return;
         active = act;
     }
-    if (m >= P.max_nodes) return;   // decision-only launch
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const double* cm = P.coef + (size_t)m * (1 + K);
-    const double beta = cm[0];
-    double dm[K], d0[K], sp[K];
+    if (m >= M) return;   // decision-only launch
+    double d0[K], dm[K], sp[K];
+    if (m <= 2 || cwarp) {
+        double e0[K], e1[K], e2[K];
 #pragma unroll
-    for (int k = 0; k < K; k++) {
-        dm[k] = cm[1 + k];
-        d0[k] = P.coef[1 + k];
-        sp[k] = 0.0;
+        for (int k = 0; k < K; k++) coef_first3(P, k, e0[k], e1[k], e2[k]);
+        if (cwarp && m == 1) {
+            coef_write_row<K>(P, 0, lane, active, e0);
+            coef_write_row<K>(P, 1, lane, active, e1);
+            coef_write_row<K>(P, 2, lane, active, e2);
+        }
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            d0[k] = e0[k];
+            dm[k] = (m == 1) ? e1[k] : e2[k];
+        }
     }
+    if (m >= 3) {
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            d0[k] = P.table[1 + k];
+            dm[k] = P.table[(size_t)m * (1 + K) + 1 + k];   // written by launch m-2
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < K; k++) sp[k] = 0.0;
+    const double beta = coef_beta(P, m);
     double sy = 0.0;
     double* dst = P.ydst[m & 1];
-    if (m == 1) {
-        for (int unit = blockIdx.x * kWarps + warp; unit < P.nunits; unit += gridDim.x * kWarps)
-            tile<NDIM, K, DIAG, true, M_LEJA, true>(P, P.v, dst, unit, lane, beta, d0, dm, active, 0.0, sy, sp);
+    if (cwarp) {
+        if (m + 2 < M) coef_write_row<K>(P, m + 2, lane, active, nullptr);
     } else {
-        const RowSrc src = P.ysrc[(m - 1) & 1];
-        for (int unit = blockIdx.x * kWarps + warp; unit < P.nunits; unit += gridDim.x * kWarps)
-            tile<NDIM, K, DIAG, false, M_LEJA, false>(P, src, dst, unit, lane, beta, d0, dm, active, 0.0, sy, sp);
+        const int gw = blockIdx.x * kWarps + warp - 1;
+        const int W = gridDim.x * kWarps - 1;
+        if (m == 1) {
+            for (int unit = gw; unit < P.nunits; unit += W)
+                tile<NDIM, K, DIAG, true, M_LEJA, true>(P, P.v, dst, unit, lane, beta, d0, dm, active, 0.0, sy, sp);
+        } else {
+            const RowSrc src = P.ysrc[(m - 1) & 1];
+            for (int unit = gw; unit < P.nunits; unit += W)
+                tile<NDIM, K, DIAG, false, M_LEJA, false>(P, src, dst, unit, lane, beta, d0, dm, active, 0.0, sy, sp);
+        }
     }
     double vals[1 + K];
     vals[0] = sy;
@@ -1150,21 +1257,6 @@ cudaError_t launch_leja_tma(const LejaParams& P, cudaStream_t s, bool diag) {
 // d[i:] = (d[i:] - d[i-1]) / (xi[i:] - xi[i-1])).  One CTA per accumulator,
 // thread j owns d_j; one barrier per recurrence step.  No host work, no H2D.
 // ---------------------------------------------------------------------------
-__device__ double phi_dev(int l, double z) {
-    const double inv_fact[6] = {1.0, 1.0, 0.5, 1.0 / 6.0, 1.0 / 24.0, 1.0 / 120.0};
-    if (fabs(z) < 2.0) {   // Taylor: sum_k z^k/(k+l)!  (34 terms: 2^34/34! ~ 1e-29)
-        double term = inv_fact[l], s = term;
-#pragma unroll
-        for (int k = 1; k < 34; k++) {
-            term *= z / (double)(k + l);
-            s += term;
-        }
-        return s;
-    }
-    double p = exp(z);
-    for (int j = 0; j < l; j++) p = (p - inv_fact[j]) / z;
-    return p;
-}
 
 // Critical path per recurrence step: one bar.sync, one shared load of the
 // published d_{i-1}, one subtract, one multiply by the precomputed reciprocal
