@@ -339,8 +339,10 @@ def test_steps_3d(xi300, method):
 @pytest.mark.parametrize("shape,K,react", [((64, 64), 1, 0.0), ((50, 70), 2, 0.0), ((130, 66), 3, 1.0),
                                            ((4096, 256), 1, 1.0)])
 def test_kernel_variants_bitwise_equal(xi300, monkeypatch, shape, K, react):
-    # register-tile kernel (LX_LEJA_KERNEL=tile) and TMA marching kernel (default) do the same
-    # per-point arithmetic in the same order: identical iterations and bitwise-identical output.
+    # register-tile kernel (default; Newton coefficients computed in-kernel) and the experimental
+    # TMA marching kernel (LX_LEJA_KERNEL=tma; coefficients from the table kernel) do the same
+    # per-point stencil arithmetic; their coefficient tables differ only by FMA contraction in the
+    # divided-difference recurrence -> identical iterations, outputs equal to ~1e-14.
     diff, nu = (1e-4, 0.0) if react else (1.0, 10.0)
     pb, ob = _pair(shape, diff=diff, nu=nu, react=react)
     u = W.ic_allen_cahn_2d(*shape) if react else None
@@ -348,7 +350,7 @@ def test_kernel_variants_bitwise_equal(xi300, monkeypatch, shape, K, react):
     dt = 0.01 if react else 10 * min(W.dt_cfl(n, 10.0) for n in shape)
     coeffs = (0.5, 2 / 3, 0.9, 1.0)[-K:]
     res = {}
-    for variant in ("tile", "tma"):
+    for variant in ("tile", "tma"):   # LX_LEJA_KERNEL values
         monkeypatch.setenv("LX_LEJA_KERNEL", variant)
         with lx.Context(pb) as ctx:
             ud = _dev(u) if react else None
@@ -358,6 +360,6 @@ def test_kernel_variants_bitwise_equal(xi300, monkeypatch, shape, K, react):
             res[variant] = (it, [o.cpu().numpy() for o in outs])
     assert res["tile"][0] == res["tma"][0]
     for a, b in zip(res["tile"][1], res["tma"][1]):
-        np.testing.assert_array_equal(a, b)
+        assert np.linalg.norm(a - b) <= 1e-13 * np.linalg.norm(b)
     r = O.real_leja_phi(ob, v, dt, c, g, 1, TOL, TOL, xi300, coeffs=coeffs, u_lin=u)
     assert res["tma"][0] == r.iters
