@@ -87,6 +87,7 @@ struct lx_ctx {
     double* rcp_dev = nullptr;            // [M][M]: 1/(xi_j - xi_i), j > i (divided-difference recurrence)
     Comm* comm = nullptr;                 // slab decomposition (lx_comm.cpp)
     int variant = 0;                      // 2D single-GPU Leja kernel: 0 = register tiles, 1 = TMA marching
+    bool coef_table = false;              // LX_COEF=table: prebuilt coefficient table instead of in-kernel
 };
 
 // ------------------------------------------------------------------ helpers
@@ -264,25 +265,27 @@ static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u,
                              double atol, int rec, const double* table = nullptr) {
     const bool tma = ctx->ndim == 2 && ctx->variant == 1 && !ctx->comm;
     const double* coef = table;
-    if (!coef && tma) {   // the experimental TMA kernel reads a prebuilt table
+    if (!coef && (tma || ctx->coef_table)) {   // prebuilt table (TMA kernel / LX_COEF=table)
         const TableSpec spec{l, K, coeffs};
         LX_TRY(build_tables(ctx, &spec, 1, dt, c, gamma, rec, &coef));
     }
     LejaParams P = base_params(ctx, pb);
     const bool diag = pb->react != 0.0;
+    // coefficient description (read by the prologue of every Leja kernel)
+    P.l = l;
+    P.cdt = dt;
+    P.cc = c;
+    P.cgamma = gamma;
+    for (int k = 0; k < kMaxK; k++) P.ak[k] = k < K ? coeffs[k] : 1.0;
+    P.xi = ctx->xi_dev;
+    P.R = ctx->rcp_dev;
+    P.table = const_cast<double*>(coef);
     if (!coef) {
         // the Leja kernels compute their own Newton coefficients (coefficient warp) into a ring slot
         const int slot = ctx->coef_next;
         ctx->coef_next = (slot + 1) % kCoefSlots;
         double* tab = ctx->coef_dev + slot * ctx->coef_stride;
         P.coef_gen = 1;
-        P.l = l;
-        P.cdt = dt;
-        P.cc = c;
-        P.cgamma = gamma;
-        for (int k = 0; k < kMaxK; k++) P.ak[k] = k < K ? coeffs[k] : 1.0;
-        P.xi = ctx->xi_dev;
-        P.R = ctx->rcp_dev;
         P.table = tab;
         coef = tab;
     }
@@ -451,6 +454,7 @@ lx_status lx_ctx_create(const lx_problem* pb, int max_nodes, int device, void* c
     ctx->N_glob = (double)ctx->n[0] * (double)ctx->row;
     ctx->max_nodes = max_nodes;
     if (const char* ev = std::getenv("LX_LEJA_KERNEL")) ctx->variant = (std::strcmp(ev, "tma") == 0) ? 1 : 0;
+    if (const char* ev = std::getenv("LX_COEF")) ctx->coef_table = (std::strcmp(ev, "table") == 0);
     cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device);
     ctx->max_grid = ctx->nsm * 8;
     ctx->xi.resize(max_nodes);
@@ -776,7 +780,7 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
     // all coefficient tables of the step in one device launch
     static const double c1[1] = {1.0}, c2[2] = {0.5, 1.0}, c3[3] = {0.5, 2.0 / 3.0, 1.0};
     const double* tab[4] = {nullptr, nullptr, nullptr, nullptr};
-    if (ctx->ndim == 2 && ctx->variant == 1 && !ctx->comm) {   // experimental TMA kernel: prebuilt tables
+    if ((ctx->ndim == 2 && ctx->variant == 1 && !ctx->comm) || ctx->coef_table) {   // prebuilt tables
         TableSpec specs[4];
         int n = 0;
         if (method == LX_ROSENBROCK_EULER) {

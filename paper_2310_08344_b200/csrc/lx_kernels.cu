@@ -60,19 +60,21 @@ __device__ __forceinline__ const double* rowp(const RowSrc& s, int r) {
     return s.base + (long long)(r < 0 ? r + s.n_loc : r - s.n_loc) * s.stride;
 }
 
+// phi_l with explicitly rounded operations (no FMA contraction), so every kernel
+// that evaluates it -- and every coefficient derived from it -- is bitwise reproducible.
 __device__ double phi_dev(int l, double z) {
     const double inv_fact[6] = {1.0, 1.0, 0.5, 1.0 / 6.0, 1.0 / 24.0, 1.0 / 120.0};
     if (fabs(z) < 2.0) {   // Taylor: sum_k z^k/(k+l)!  (34 terms: 2^34/34! ~ 1e-29)
         double term = inv_fact[l], s = term;
 #pragma unroll
         for (int k = 1; k < 34; k++) {
-            term *= z / (double)(k + l);
-            s += term;
+            term = __dmul_rn(term, __ddiv_rn(z, (double)(k + l)));
+            s = __dadd_rn(s, term);
         }
         return s;
     }
     double p = exp(z);
-    for (int j = 0; j < l; j++) p = (p - inv_fact[j]) / z;
+    for (int j = 0; j < l; j++) p = __ddiv_rn(__dsub_rn(p, inv_fact[j]), z);
     return p;
 }
 
@@ -84,9 +86,17 @@ __device__ double phi_dev(int l, double z) {
 // earlier rows of the table) -- overlapped with the stencil work, no table
 // launch and no host arithmetic.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double coef_h(const LejaParams& P, int k, int j) {
-    return phi_dev(P.l, P.ak[k] * P.cdt * (P.cc + P.cgamma * P.xi[j]));
+__device__ __forceinline__ double coef_arg(double a, double dt, double c, double gamma, double x) {
+    // a*dt*(c + gamma*x), explicitly rounded (no contraction)
+    return __dmul_rn(__dmul_rn(a, dt), __dadd_rn(c, __dmul_rn(gamma, x)));
 }
+
+__device__ __forceinline__ double coef_h(const LejaParams& P, int k, int j) {
+    return phi_dev(P.l, coef_arg(P.ak[k], P.cdt, P.cc, P.cgamma, P.xi[j]));
+}
+
+// one step of the recurrence: (d - d_i) * 1/(xi_j - xi_i), explicitly rounded
+__device__ __forceinline__ double dd_step(double d, double di, double r) { return __dmul_rn(__dsub_rn(d, di), r); }
 
 __device__ __forceinline__ double coef_fold(const LejaParams& P, int K, int k, int j) {
     double d = coef_h(P, k, j);
@@ -99,12 +109,12 @@ __device__ __forceinline__ double coef_fold(const LejaParams& P, int K, int k, i
         const double t2 = tab[(size_t)(i + 2) * (1 + K)], t3 = tab[(size_t)(i + 3) * (1 + K)];
         const double r0 = Rc[(size_t)i * M], r1 = Rc[(size_t)(i + 1) * M];
         const double r2 = Rc[(size_t)(i + 2) * M], r3 = Rc[(size_t)(i + 3) * M];
-        d = (d - t0) * r0;
-        d = (d - t1) * r1;
-        d = (d - t2) * r2;
-        d = (d - t3) * r3;
+        d = dd_step(d, t0, r0);
+        d = dd_step(d, t1, r1);
+        d = dd_step(d, t2, r2);
+        d = dd_step(d, t3, r3);
     }
-    for (; i < j; i++) d = (d - tab[(size_t)i * (1 + K)]) * Rc[(size_t)i * M];
+    for (; i < j; i++) d = dd_step(d, tab[(size_t)i * (1 + K)], Rc[(size_t)i * M]);
     return d;
 }
 
@@ -112,8 +122,8 @@ __device__ __forceinline__ double coef_fold(const LejaParams& P, int K, int k, i
 __device__ __forceinline__ void coef_first3(const LejaParams& P, int k, double& d0, double& d1, double& d2) {
     const int M = P.max_nodes;
     d0 = coef_h(P, k, 0);
-    d1 = M > 1 ? (coef_h(P, k, 1) - d0) * P.R[1] : 0.0;
-    d2 = M > 2 ? ((coef_h(P, k, 2) - d0) * P.R[2] - d1) * P.R[M + 2] : 0.0;
+    d1 = M > 1 ? dd_step(coef_h(P, k, 1), d0, P.R[1]) : 0.0;
+    d2 = M > 2 ? dd_step(dd_step(coef_h(P, k, 2), d0, P.R[2]), d1, P.R[M + 2]) : 0.0;
 }
 
 // Coefficient warp: write rows 0..2 (prologue) or row j (>= 3) of the table.
@@ -600,7 +610,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d(const __grid_constant__ 
     double d0[K], d1[K], d2[K];
 #pragma unroll
     for (int k = 0; k < K; k++) coef_first3(P, k, d0[k], d1[k], d2[k]);
-    if (cwarp) {
+    if (cwarp && P.coef_gen) {
         coef_write_row<K>(P, 0, lane, active, d0);
         coef_write_row<K>(P, 1, lane, active, d1);
         coef_write_row<K>(P, 2, lane, active, d2);
@@ -620,7 +630,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d(const __grid_constant__ 
         const int par = m & 1;
         double* dst = P.ydst[par];
         if (cwarp) {
-            if (m + 2 < M) coef_write_row<K>(P, m + 2, lane, active, nullptr);
+            if (P.coef_gen && m + 2 < M) coef_write_row<K>(P, m + 2, lane, active, nullptr);
         } else if (m == 1) {
             for (int unit = gw; unit < P.nunits; unit += W)
                 tile<NDIM, K, DIAG, true, M_LEJA, true>(P, P.v, dst, unit, lane, beta, d0, dm, active, 0.0, sy, sp);
@@ -758,7 +768,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d_step(const __grid_consta
         double e0[K], e1[K], e2[K];
 #pragma unroll
         for (int k = 0; k < K; k++) coef_first3(P, k, e0[k], e1[k], e2[k]);
-        if (cwarp && m == 1) {
+        if (cwarp && m == 1 && P.coef_gen) {
             coef_write_row<K>(P, 0, lane, active, e0);
             coef_write_row<K>(P, 1, lane, active, e1);
             coef_write_row<K>(P, 2, lane, active, e2);
@@ -782,7 +792,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d_step(const __grid_consta
     double sy = 0.0;
     double* dst = P.ydst[m & 1];
     if (cwarp) {
-        if (m + 2 < M) coef_write_row<K>(P, m + 2, lane, active, nullptr);
+        if (P.coef_gen && m + 2 < M) coef_write_row<K>(P, m + 2, lane, active, nullptr);
     } else {
         const int gw = blockIdx.x * kWarps + warp - 1;
         const int W = gridDim.x * kWarps - 1;
@@ -1273,7 +1283,7 @@ __global__ void k_coef_tables(const double* xi, const double* R, int M, CoefJobs
     const int j = threadIdx.x;
     const bool own = j < M;
     const double xj = own ? xi[j] : 0.0;
-    double dj = own ? phi_dev(J.l, J.a * dt * (c + gamma * xj)) : 0.0;
+    double dj = own ? phi_dev(J.l, coef_arg(J.a, dt, c, gamma, xj)) : 0.0;
     if (j == 0) dsh[0] = dj;   // d_0 = h(xi_0) is final
     double rr[4];
 #pragma unroll
@@ -1289,7 +1299,7 @@ __global__ void k_coef_tables(const double* xi, const double* R, int M, CoefJobs
                 __syncthreads();
                 const double di = dsh[i - 1];
                 if (own && j >= i) {
-                    dj = (dj - di) * r;
+                    dj = dd_step(dj, di, r);
                     if (j == i) dsh[j] = dj;
                 }
             }
