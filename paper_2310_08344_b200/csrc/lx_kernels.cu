@@ -62,13 +62,20 @@ __device__ __forceinline__ const double* rowp(const RowSrc& s, int r) {
 
 // phi_l with explicitly rounded operations (no FMA contraction), so every kernel
 // that evaluates it -- and every coefficient derived from it -- is bitwise reproducible.
+// Taylor terms use the constant reciprocals 1/n (one multiply instead of a division).
+__constant__ double c_inv_int[40] = {
+    0.0, 1.0, 1.0 / 2, 1.0 / 3, 1.0 / 4, 1.0 / 5, 1.0 / 6, 1.0 / 7, 1.0 / 8, 1.0 / 9, 1.0 / 10,
+    1.0 / 11, 1.0 / 12, 1.0 / 13, 1.0 / 14, 1.0 / 15, 1.0 / 16, 1.0 / 17, 1.0 / 18, 1.0 / 19, 1.0 / 20,
+    1.0 / 21, 1.0 / 22, 1.0 / 23, 1.0 / 24, 1.0 / 25, 1.0 / 26, 1.0 / 27, 1.0 / 28, 1.0 / 29, 1.0 / 30,
+    1.0 / 31, 1.0 / 32, 1.0 / 33, 1.0 / 34, 1.0 / 35, 1.0 / 36, 1.0 / 37, 1.0 / 38, 1.0 / 39};
+
 __device__ double phi_dev(int l, double z) {
     const double inv_fact[6] = {1.0, 1.0, 0.5, 1.0 / 6.0, 1.0 / 24.0, 1.0 / 120.0};
     if (fabs(z) < 2.0) {   // Taylor: sum_k z^k/(k+l)!  (34 terms: 2^34/34! ~ 1e-29)
         double term = inv_fact[l], s = term;
 #pragma unroll
         for (int k = 1; k < 34; k++) {
-            term = __dmul_rn(term, __ddiv_rn(z, (double)(k + l)));
+            term = __dmul_rn(term, __dmul_rn(z, c_inv_int[k + l]));
             s = __dadd_rn(s, term);
         }
         return s;
@@ -78,14 +85,6 @@ __device__ double phi_dev(int l, double z) {
     return p;
 }
 
-// ---------------------------------------------------------------------------
-// In-kernel Newton divided differences (reading R8).  Column form
-// of the triangular recurrence: d_j = fold_{i<j} (d - d_i) * R[i][j] starting at
-// d = h_j = phi_l(a dt (c + gamma xi_j)); it needs only the FINAL d_0..d_{j-1},
-// so the coefficient warp computes d_{m+2} during iteration m (reading its own
-// earlier rows of the table) -- overlapped with the stencil work, no table
-// launch and no host arithmetic.
-// ---------------------------------------------------------------------------
 __device__ __forceinline__ double coef_arg(double a, double dt, double c, double gamma, double x) {
     // a*dt*(c + gamma*x), explicitly rounded (no contraction)
     return __dmul_rn(__dmul_rn(a, dt), __dadd_rn(c, __dmul_rn(gamma, x)));
@@ -118,12 +117,19 @@ __device__ __forceinline__ double coef_fold(const LejaParams& P, int K, int k, i
     return d;
 }
 
-// d_0, d_1, d_2 of accumulator k (computed redundantly by every thread in the prologue).
+// d_0, d_1, d_2 of accumulator k: computed by lane 0 of every warp, broadcast by shuffle
+// (all lanes of the warp must call it).
 __device__ __forceinline__ void coef_first3(const LejaParams& P, int k, double& d0, double& d1, double& d2) {
     const int M = P.max_nodes;
-    d0 = coef_h(P, k, 0);
-    d1 = M > 1 ? dd_step(coef_h(P, k, 1), d0, P.R[1]) : 0.0;
-    d2 = M > 2 ? dd_step(dd_step(coef_h(P, k, 2), d0, P.R[2]), d1, P.R[M + 2]) : 0.0;
+    double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+    if ((threadIdx.x & 31) == 0) {
+        e0 = coef_h(P, k, 0);
+        e1 = M > 1 ? dd_step(coef_h(P, k, 1), e0, P.R[1]) : 0.0;
+        e2 = M > 2 ? dd_step(dd_step(coef_h(P, k, 2), e0, P.R[2]), e1, P.R[M + 2]) : 0.0;
+    }
+    d0 = __shfl_sync(0xffffffffu, e0, 0);
+    d1 = __shfl_sync(0xffffffffu, e1, 0);
+    d2 = __shfl_sync(0xffffffffu, e2, 0);
 }
 
 // Coefficient warp: write rows 0..2 (prologue) or row j (>= 3) of the table.
