@@ -1363,6 +1363,11 @@ __device__ __forceinline__ void stage_reduce_err(const StageArgs& A, double v, d
 
 template <int OP>
 __global__ void __launch_bounds__(kThreads) k_stage_pointwise(const __grid_constant__ StageArgs A) {
+    // Each loop trip handles UN independent element pairs; all loads of the trip are issued
+    // before any store (outputs may alias inputs element-wise, which blocks the compiler from
+    // overlapping trips on its own), so every thread keeps UN x (inputs) 16-byte loads in flight.
+    constexpr int UN = 4;
+    constexpr int NIN = (OP == ST_FINAL4) ? 4 : (OP == ST_STAGE_REMAINDER) ? 4 : (OP == ST_MAXSQ) ? 1 : 2;
     __shared__ double s_red[kWarps][kSlot];
     __shared__ int s_last;
     const long long npair = (long long)A.n_loc * A.n1 * A.n2 / 2;
@@ -1370,55 +1375,72 @@ __global__ void __launch_bounds__(kThreads) k_stage_pointwise(const __grid_const
     double acc = 0.0;
     unsigned long long umax = 0ull;
     const double dt = A.dt, react = A.st.react;
-    for (long long i = (long long)blockIdx.x * kThreads + threadIdx.x; i < npair; i += stride) {
-        const long long o = 2 * i;
-        if (OP == ST_AXPBY) {
-            const double2 x = ld2(A.x0 + o), y = ld2(A.x1 + o);
-            st2(A.y0 + o, make_double2(A.a0 * x.x + A.a1 * y.x, A.a0 * x.y + A.a1 * y.y));
-        } else if (OP == ST_REMAINDER_DIFF) {
-            const double2 x = ld2(A.x0 + o), u = ld2(A.u + o);
-            st2(A.y0 + o, make_double2(dt * nl_rem(react, x.x, u.x) + (-dt) * nl_rem(react, u.x, u.x),
-                                       dt * nl_rem(react, x.y, u.y) + (-dt) * nl_rem(react, u.y, u.y)));
-        } else if (OP == ST_STAGE_REMAINDER) {
-            // s = x0 + a0*x1 + a1*x2 (not stored);  y0 = dt F(s) - dt F(u)
-            const double2 x = ld2(A.x0 + o), u = ld2(A.u + o);
-            const double2 p = ld2(A.x1 + o);
-            double2 q = make_double2(0.0, 0.0);
-            if (A.x2) q = ld2(A.x2 + o);
-            const double sx = x.x + A.a0 * p.x + A.a1 * q.x;
-            const double sy = x.y + A.a0 * p.y + A.a1 * q.y;
-            st2(A.y0 + o, make_double2(dt * nl_rem(react, sx, u.x) + (-dt) * nl_rem(react, u.x, u.x),
-                                       dt * nl_rem(react, sy, u.y) + (-dt) * nl_rem(react, u.y, u.y)));
-        } else if (OP == ST_EXPRB32_A) {
-            const double2 u = ld2(A.x0 + o), p = ld2(A.x1 + o);
-            const double2 a = make_double2(u.x + p.x, u.y + p.y);
-            st2(A.y1 + o, a);
-            st2(A.y0 + o, make_double2(dt * nl_rem(react, a.x, u.x) + (-dt) * nl_rem(react, u.x, u.x),
-                                       dt * nl_rem(react, a.y, u.y) + (-dt) * nl_rem(react, u.y, u.y)));
-        } else if (OP == ST_COMBINE2) {
-            const double2 x = ld2(A.x0 + o), y = ld2(A.x1 + o);
-            st2(A.y0 + o, make_double2(A.a0 * x.x + A.a1 * y.x, A.a0 * x.y + A.a1 * y.y));
-            st2(A.y1 + o, make_double2(A.a2 * x.x + A.a3 * y.x, A.a2 * x.y + A.a3 * y.y));
-        } else if (OP == ST_FINAL4) {
-            const double2 u = ld2(A.x0 + o), p1 = ld2(A.x1 + o), q3 = ld2(A.x2 + o), q4 = ld2(A.x3 + o);
-            const double2 u3 = make_double2(u.x + p1.x + q3.x, u.y + p1.y + q3.y);
-            const double2 u4 = make_double2(u3.x + q4.x, u3.y + q4.y);
-            st2(A.y0 + o, u3);
-            st2(A.y1 + o, u4);
-            const double ex = u4.x - u3.x, ey = u4.y - u3.y;
-            acc = fma(ex, ex, acc);
-            acc = fma(ey, ey, acc);
-        } else if (OP == ST_FINAL_EXPRB32) {
-            const double2 a = ld2(A.x0 + o), q = ld2(A.x1 + o);
-            st2(A.y0 + o, make_double2(a.x + 2.0 * q.x, a.y + 2.0 * q.y));
-            const double ex = 2.0 * q.x, ey = 2.0 * q.y;
-            acc = fma(ex, ex, acc);
-            acc = fma(ey, ey, acc);
-        } else if (OP == ST_MAXSQ) {
-            const double2 x = ld2(A.x0 + o);
-            const double m2 = fmax(x.x * x.x, x.y * x.y);
-            const unsigned long long b = (unsigned long long)__double_as_longlong(m2);
-            umax = b > umax ? b : umax;
+    const double* in[4];
+    if (OP == ST_REMAINDER_DIFF) { in[0] = A.x0; in[1] = A.u; }
+    else if (OP == ST_STAGE_REMAINDER) { in[0] = A.x0; in[1] = A.u; in[2] = A.x1; in[3] = A.x2; }
+    else if (OP == ST_EXPRB32_A) { in[0] = A.x0; in[1] = A.x1; }
+    else { in[0] = A.x0; in[1] = A.x1; in[2] = A.x2; in[3] = A.x3; }
+    for (long long i0 = (long long)blockIdx.x * kThreads + threadIdx.x; i0 < npair; i0 += UN * stride) {
+        double2 v[UN][NIN];
+#pragma unroll
+        for (int q = 0; q < UN; q++) {
+            const long long o = 2 * (i0 + q * stride);
+            const bool ok = i0 + q * stride < npair;
+#pragma unroll
+            for (int t = 0; t < NIN; t++) {
+                v[q][t] = make_double2(0.0, 0.0);
+                if (ok && !(OP == ST_STAGE_REMAINDER && t == 3 && !in[3])) v[q][t] = ld2(in[t] + o);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < UN; q++) {
+            const long long o = 2 * (i0 + q * stride);
+            if (i0 + q * stride >= npair) break;
+            if (OP == ST_AXPBY) {
+                const double2 x = v[q][0], y = v[q][1];
+                st2(A.y0 + o, make_double2(A.a0 * x.x + A.a1 * y.x, A.a0 * x.y + A.a1 * y.y));
+            } else if (OP == ST_REMAINDER_DIFF) {
+                const double2 x = v[q][0], u = v[q][1];
+                st2(A.y0 + o, make_double2(dt * nl_rem(react, x.x, u.x) + (-dt) * nl_rem(react, u.x, u.x),
+                                           dt * nl_rem(react, x.y, u.y) + (-dt) * nl_rem(react, u.y, u.y)));
+            } else if (OP == ST_STAGE_REMAINDER) {
+                // s = x0 + a0*x1 + a1*x2 (not stored);  y0 = dt F(s) - dt F(u)
+                const double2 x = v[q][0], u = v[q][1], p = v[q][2], r = v[q][3];
+                const double sx = x.x + A.a0 * p.x + A.a1 * r.x;
+                const double sy = x.y + A.a0 * p.y + A.a1 * r.y;
+                st2(A.y0 + o, make_double2(dt * nl_rem(react, sx, u.x) + (-dt) * nl_rem(react, u.x, u.x),
+                                           dt * nl_rem(react, sy, u.y) + (-dt) * nl_rem(react, u.y, u.y)));
+            } else if (OP == ST_EXPRB32_A) {
+                const double2 u = v[q][0], p = v[q][1];
+                const double2 a = make_double2(u.x + p.x, u.y + p.y);
+                st2(A.y1 + o, a);
+                st2(A.y0 + o, make_double2(dt * nl_rem(react, a.x, u.x) + (-dt) * nl_rem(react, u.x, u.x),
+                                           dt * nl_rem(react, a.y, u.y) + (-dt) * nl_rem(react, u.y, u.y)));
+            } else if (OP == ST_COMBINE2) {
+                const double2 x = v[q][0], y = v[q][1];
+                st2(A.y0 + o, make_double2(A.a0 * x.x + A.a1 * y.x, A.a0 * x.y + A.a1 * y.y));
+                st2(A.y1 + o, make_double2(A.a2 * x.x + A.a3 * y.x, A.a2 * x.y + A.a3 * y.y));
+            } else if (OP == ST_FINAL4) {
+                const double2 u = v[q][0], p1 = v[q][1], q3 = v[q][2], q4 = v[q][3];
+                const double2 u3 = make_double2(u.x + p1.x + q3.x, u.y + p1.y + q3.y);
+                const double2 u4 = make_double2(u3.x + q4.x, u3.y + q4.y);
+                st2(A.y0 + o, u3);
+                st2(A.y1 + o, u4);
+                const double ex = u4.x - u3.x, ey = u4.y - u3.y;
+                acc = fma(ex, ex, acc);
+                acc = fma(ey, ey, acc);
+            } else if (OP == ST_FINAL_EXPRB32) {
+                const double2 a = v[q][0], qq = v[q][1];
+                st2(A.y0 + o, make_double2(a.x + 2.0 * qq.x, a.y + 2.0 * qq.y));
+                const double ex = 2.0 * qq.x, ey = 2.0 * qq.y;
+                acc = fma(ex, ex, acc);
+                acc = fma(ey, ey, acc);
+            } else if (OP == ST_MAXSQ) {
+                const double2 x = v[q][0];
+                const double m2 = fmax(x.x * x.x, x.y * x.y);
+                const unsigned long long bb = (unsigned long long)__double_as_longlong(m2);
+                umax = bb > umax ? bb : umax;
+            }
         }
     }
     if (OP == ST_FINAL4 || OP == ST_FINAL_EXPRB32) stage_reduce_err(A, acc, s_red, &s_last);
