@@ -226,6 +226,16 @@ lx_status lx_step(lx_ctx *ctx, lx_method method, const lx_problem *pb, const dou
                   double *u_low, double *u_high, double *err_out, double dt, double c,
                   double gamma, double rtol, double atol, int *iters_out);
 
+/* The paper's time loop (listing alg:lexint) run on the device: nsteps steps of
+ * `method` from the state in u (overwritten with u^{n+nsteps}).  Before every step the spectrum
+ * bound of J(u^n) is recomputed ON THE DEVICE (closed form + Gershgorin max-reduction,
+ * eig = -1.05 |lambda|, c = eig/2, gamma = -eig/4) and the Leja kernels read (c, gamma)
+ * from device memory, so the whole run is enqueued without host round trips.  *iters_out = total
+ * Leja iterations, *err_out = embedded error of the last step.  NULL out-pointers -> asynchronous
+ * (device u only).  Uses 3 extra context state vectors. */
+lx_status lx_integrate(lx_ctx *ctx, lx_method method, const lx_problem *pb, double *u, double dt, int nsteps,
+                       double rtol, double atol, int *iters_out, double *err_out);
+
 /* f(u) * dt (alg:Ros_Eu P:468-469) as a standalone fused stencil pass. */
 lx_status lx_rhs(lx_ctx *ctx, const lx_problem *pb, const double *u, double scale, double *f_out);
 

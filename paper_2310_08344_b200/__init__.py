@@ -39,7 +39,7 @@ EXPORTS = ("lx_last_error", "lx_version", "lx_leja_points", "lx_phi_scalar", "lx
            "lx_ctx_local", "lx_ctx_synchronize", "lx_ctx_launch_count", "lx_spectrum_estimate",
            "lx_spectrum_bound", "lx_shift_scale", "lx_real_leja_phi", "lx_real_leja_phi_vertical",
            "lx_step_rosenbrock_euler", "lx_step_exprb32", "lx_step_exprb43", "lx_step_epirk4s3a",
-           "lx_step", "lx_rhs", "lx_local_group_create", "lx_local_group_destroy", "lx_ctx_set_comm_local")
+           "lx_step", "lx_rhs", "lx_integrate", "lx_local_group_create", "lx_local_group_destroy", "lx_ctx_set_comm_local")
 
 
 class LxError(RuntimeError):
@@ -115,6 +115,7 @@ def lib() -> ctypes.CDLL:
             "lx_step_exprb43": (ctypes.c_int, [vp, pbp, vp, vp, vp, dp, d, d, d, d, d, ip]),
             "lx_step_epirk4s3a": (ctypes.c_int, [vp, pbp, vp, vp, vp, dp, d, d, d, d, d, ip]),
             "lx_rhs": (ctypes.c_int, [vp, pbp, vp, d, vp]),
+            "lx_integrate": (ctypes.c_int, [vp, ctypes.c_int, pbp, vp, d, ctypes.c_int, d, d, ip, dp]),
             "lx_local_group_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(vp)]),
             "lx_local_group_destroy": (ctypes.c_int, [vp]),
             "lx_ctx_set_comm_local": (ctypes.c_int, [vp, vp, ctypes.c_int]),
@@ -336,6 +337,18 @@ def lx_step_exprb43(ctx, u, u_low, u_high, dt, c, gamma, rtol, atol, problem=Non
 
 def lx_step_epirk4s3a(ctx, u, u_low, u_high, dt, c, gamma, rtol, atol, problem=None):
     return lx_step(ctx, LX_EPIRK4S3A, u, u_low, u_high, dt, c, gamma, rtol, atol, problem)
+
+
+def lx_integrate(ctx: Context, method, u, dt, nsteps, rtol, atol, problem: Problem | None = None,
+                 sync: bool = True):
+    """nsteps exponential-integrator steps in place on u with the spectrum (c, gamma) recomputed on the
+    device every step (the paper's time loop).  Returns (total Leja iterations, last err)."""
+    m = METHODS[method] if isinstance(method, str) else int(method)
+    it, err = ctypes.c_int(0), ctypes.c_double(0.0)
+    st = lib().lx_integrate(ctx.handle, m, _pb(ctx, problem), _ptr(u), float(dt), int(nsteps), float(rtol),
+                            float(atol), ctypes.byref(it) if sync else None, ctypes.byref(err) if sync else None)
+    _check(st, it.value)
+    return (it.value, err.value) if sync else (None, None)
 
 
 def lx_rhs(ctx: Context, u, f_out, scale: float = 1.0, problem: Problem | None = None):

@@ -47,7 +47,7 @@ static lx_status fail(lx_status s, const char* fmt, ...) {
     } while (0)
 
 static constexpr int kCoefSlots = 32;
-static constexpr int kStage = 4;   // integrator scratch vectors
+static constexpr int kStage = 7;   // integrator scratch vectors (4 stages + 3 states for lx_integrate)
 static constexpr int kHost = 6;    // host-pointer staging vectors
 
 struct lx_ctx {
@@ -88,6 +88,8 @@ struct lx_ctx {
     Comm* comm = nullptr;                 // slab decomposition (lx_comm.cpp)
     int variant = 0;                      // 2D single-GPU Leja kernel: 0 = register tiles, 1 = TMA marching
     bool coef_table = false;              // LX_COEF=table: prebuilt coefficient table instead of in-kernel
+    double* cg_dev = nullptr;             // device (c, gamma, bound) of lx_integrate
+    const double* cg_active = nullptr;    // when set, Leja kernels take (c, gamma) from here
 };
 
 // ------------------------------------------------------------------ helpers
@@ -263,9 +265,9 @@ static LejaParams base_params(lx_ctx* ctx, const lx_problem* pb) {
 static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u, const double* v, double* const* outs,
                              const double* coeffs, int K, double dt, double c, double gamma, int l, double rtol,
                              double atol, int rec, const double* table = nullptr) {
-    const bool tma = ctx->ndim == 2 && ctx->variant == 1 && !ctx->comm;
+    const bool tma = ctx->ndim == 2 && ctx->variant == 1 && !ctx->comm && !ctx->cg_active;
     const double* coef = table;
-    if (!coef && (tma || ctx->coef_table)) {   // prebuilt table (TMA kernel / LX_COEF=table)
+    if (!coef && (tma || (ctx->coef_table && !ctx->cg_active))) {   // prebuilt table (TMA / LX_COEF=table)
         const TableSpec spec{l, K, coeffs};
         LX_TRY(build_tables(ctx, &spec, 1, dt, c, gamma, rec, &coef));
     }
@@ -280,6 +282,7 @@ static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u,
     P.xi = ctx->xi_dev;
     P.R = ctx->rcp_dev;
     P.table = const_cast<double*>(coef);
+    P.cg_dev = ctx->cg_active;
     if (!coef) {
         // the Leja kernels compute their own Newton coefficients (coefficient warp) into a ring slot
         const int slot = ctx->coef_next;
@@ -391,6 +394,7 @@ static void free_ctx(lx_ctx* ctx) {
     cudaFree(ctx->coef_dev);
     cudaFree(ctx->xi_dev);
     cudaFree(ctx->rcp_dev);
+    cudaFree(ctx->cg_dev);
     cudaFreeHost(ctx->rec_host);
     cudaFreeHost(ctx->rec_init);
     cudaFreeHost(ctx->umax_host);
@@ -479,6 +483,7 @@ lx_status lx_ctx_create(const lx_problem* pb, int max_nodes, int device, void* c
     CK(cudaMalloc(&ctx->coef_dev, kCoefSlots * ctx->coef_stride * sizeof(double)));
     CK(cudaMallocHost(&ctx->coef_host, kCoefSlots * ctx->coef_stride * sizeof(double)));
     for (auto& ev : ctx->coef_ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CK(cudaMalloc(&ctx->cg_dev, 4 * sizeof(double)));
     CK(cudaMalloc(&ctx->xi_dev, max_nodes * sizeof(double)));
     CK(cudaMemcpy(ctx->xi_dev, ctx->xi.data(), max_nodes * sizeof(double), cudaMemcpyHostToDevice));
     {
@@ -780,7 +785,7 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
     // all coefficient tables of the step in one device launch
     static const double c1[1] = {1.0}, c2[2] = {0.5, 1.0}, c3[3] = {0.5, 2.0 / 3.0, 1.0};
     const double* tab[4] = {nullptr, nullptr, nullptr, nullptr};
-    if ((ctx->ndim == 2 && ctx->variant == 1 && !ctx->comm) || ctx->coef_table) {   // prebuilt tables
+    if (!ctx->cg_active && ((ctx->ndim == 2 && ctx->variant == 1 && !ctx->comm) || ctx->coef_table)) {
         TableSpec specs[4];
         int n = 0;
         if (method == LX_ROSENBROCK_EULER) {
@@ -892,6 +897,75 @@ lx_status lx_step(lx_ctx* ctx, lx_method method, const lx_problem* pb, const dou
     if (sync) LX_TRY(reset_record(ctx, 0));
     LX_TRY(step_device(ctx, method, pb, ud, lo, hi, dt, c, gamma, rtol, atol, rec));
     LX_TRY(sg.finish());
+    if (!sync) return LX_OK;
+    Record r;
+    LX_TRY(read_record(ctx, 0, &r));
+    if (iters_out) *iters_out = r.iters;
+    if (err_out) *err_out = (method == LX_ROSENBROCK_EULER) ? 0.0 : r.err;
+    return status_of(r);
+}
+
+// The paper's time loop (listing alg:lexint) on the device: every step recomputes the
+// spectrum bound (Gershgorin / closed form, x1.05, c = eig/2, gamma = -eig/4) with a
+// device max-reduction + k_shift_scale, so the whole run is enqueued without host round trips.
+lx_status lx_integrate(lx_ctx* ctx, lx_method method, const lx_problem* pb, double* u, double dt, int nsteps,
+                       double rtol, double atol, int* iters_out, double* err_out) {
+    if (!ctx || !u) return fail(LX_ERR_ARG, "NULL argument");
+    LX_TRY(check_problem(ctx, pb));
+    if ((int)method < 0 || (int)method > 3) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
+    if (nsteps < 0) return fail(LX_ERR_ARG, "nsteps < 0");
+    if (!std::isfinite(dt)) return fail(LX_ERR_ARG, "dt not finite");
+    Staging sg(ctx);
+    const double* uin;
+    double* ud;
+    LX_TRY(sg.in(u, &uin));
+    ud = const_cast<double*>(uin);
+    double* st[2] = {scratch(ctx, 4), scratch(ctx, 5)};
+    double* lo = scratch(ctx, 6);   // lower-order solution (discarded)
+    if (!st[0] || !st[1] || !lo) return fail(LX_ERR_CUDA, "scratch allocation failed");
+    double bound_const = 0.0;
+    for (int d = 0; d < pb->ndim; d++) {
+        const double h = pb->dx[d];
+        bound_const += 4.0 * pb->diff / (h * h) + 4.0 * std::fabs(pb->nu) / (3.0 * h);
+    }
+    const bool sync = iters_out || err_out || sg.any_host;
+    const int rec = sync ? 0 : 1;
+    if (sync) LX_TRY(reset_record(ctx, 0));
+    StageArgs A = stage_args(ctx, pb, rec);
+    A.ctrl = ctx->ctrl;
+    double* cur = ud;
+    ctx->cg_active = ctx->cg_dev;
+    lx_status status = LX_OK;
+    for (int n = 0; n < nsteps && status == LX_OK; n++) {
+        // spectrum of J(u_n) on the device
+        if (pb->react != 0.0) {
+            if (cudaMemsetAsync(&ctx->ctrl->umax, 0, sizeof(unsigned long long), ctx->stream) != cudaSuccess) {
+                status = fail(LX_ERR_CUDA, "memset");
+                break;
+            }
+            StageArgs B = A;
+            B.x0 = cur;
+            B.grid = stage_grid_size(ctx->device, ST_MAXSQ);
+            if (launch_stage(ST_MAXSQ, B, ctx->stream) != cudaSuccess) { status = fail(LX_ERR_CUDA, "maxsq"); break; }
+            ctx->launches++;
+            if (ctx->comm && comm_allreduce_max_u64(ctx->comm, &ctx->ctrl->umax, ctx->stream)) {
+                status = fail(LX_ERR_NCCL, "allreduce max: %s", comm_error());
+                break;
+            }
+        }
+        if (launch_shift_scale(&ctx->ctrl->umax, bound_const, pb->react, ctx->cg_dev, ctx->stream) != cudaSuccess) {
+            status = fail(LX_ERR_CUDA, "shift_scale");
+            break;
+        }
+        ctx->launches++;
+        double* hi = (cur == st[0]) ? st[1] : st[0];
+        status = step_device(ctx, method, pb, cur, lo, hi, dt, 0.0, 1.0, rtol, atol, rec);
+        cur = hi;
+    }
+    ctx->cg_active = nullptr;
+    if (status != LX_OK) return status;
+    if (cur != ud) CUDA_TRY(cudaMemcpyAsync(ud, cur, ctx->N_loc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    if (sg.any_host) CUDA_TRY(cudaMemcpyAsync(u, ud, ctx->N_loc * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     if (!sync) return LX_OK;
     Record r;
     LX_TRY(read_record(ctx, 0, &r));

@@ -105,6 +105,9 @@ struct LejaParams {
     const double* xi;     // [max_nodes] Leja points
     const double* R;      // [max_nodes][max_nodes]: 1/(xi_j - xi_i), j > i
     double* table;        // == coef
+    // device-resident (c, gamma) (lx_integrate: spectrum recomputed on the device every step);
+    // nullptr -> cc / cgamma / alpha from the host
+    const double* cg_dev;
 };
 
 // launchers (lx_kernels.cu)
@@ -152,6 +155,9 @@ cudaError_t launch_power_step(const LejaParams& P, int m, cudaStream_t s, bool d
 int step_grid_size(int device, int nunits);
 cudaError_t launch_finalize_err(const double* gathered, int nranks, double N, Record* rec, cudaStream_t s);
 cudaError_t launch_max_u64(const unsigned long long* vals, int n, unsigned long long* out, cudaStream_t s);
+// (c, gamma) on the device from the bound const_part + react*max(0, 3*max u^2 - 1)
+cudaError_t launch_shift_scale(const unsigned long long* umax, double const_part, double react, double* cg_out,
+                               cudaStream_t s);
 int stage_grid_size(int device, int op);
 // device coefficient table: [M][1+K] = {beta_m, d_m^(k)}; a[K] device array of vertical coefficients
 struct CoefJob {

@@ -90,8 +90,14 @@ __device__ __forceinline__ double coef_arg(double a, double dt, double c, double
     return __dmul_rn(__dmul_rn(a, dt), __dadd_rn(c, __dmul_rn(gamma, x)));
 }
 
+__device__ __forceinline__ double P_c(const LejaParams& P) { return P.cg_dev ? P.cg_dev[0] : P.cc; }
+__device__ __forceinline__ double P_g(const LejaParams& P) { return P.cg_dev ? P.cg_dev[1] : P.cgamma; }
+__device__ __forceinline__ double P_alpha(const LejaParams& P) {
+    return P.cg_dev ? (P.cdt == 0.0 ? 0.0 : 1.0 / P.cg_dev[1]) : P.alpha;
+}
+
 __device__ __forceinline__ double coef_h(const LejaParams& P, int k, int j) {
-    return phi_dev(P.l, coef_arg(P.ak[k], P.cdt, P.cc, P.cgamma, P.xi[j]));
+    return phi_dev(P.l, coef_arg(P.ak[k], P.cdt, P_c(P), P_g(P), P.xi[j]));
 }
 
 // one step of the recurrence: (d - d_i) * 1/(xi_j - xi_i), explicitly rounded
@@ -137,12 +143,12 @@ template <int K>
 __device__ __forceinline__ void coef_write_row(const LejaParams& P, int j, int lane, int active, const double* dk) {
     if (j >= P.max_nodes) return;
     double* row = P.table + (size_t)j * (1 + K);
-    if (lane == 0) row[0] = (j == 0 || P.cdt == 0.0) ? 0.0 : (-P.cc / P.cgamma - P.xi[j - 1]);
+    if (lane == 0) row[0] = (j == 0 || P.cdt == 0.0) ? 0.0 : (-P_c(P) / P_g(P) - P.xi[j - 1]);
     if (lane < K && ((active >> lane) & 1)) row[1 + lane] = dk ? dk[lane] : coef_fold(P, K, lane, j);
 }
 
 __device__ __forceinline__ double coef_beta(const LejaParams& P, int m) {
-    return (P.cdt == 0.0) ? 0.0 : (-P.cc / P.cgamma - P.xi[m - 1]);
+    return (P.cdt == 0.0) ? 0.0 : (-P_c(P) / P_g(P) - P.xi[m - 1]);
 }
 
 // Deterministic block reduction of n values: xor-butterfly inside warps, then
@@ -273,8 +279,8 @@ __device__ __forceinline__ void tile2d(const LejaParams& P, const RowSrc& src, d
                 yn.x = scale * fma(S.react, yc.x - yc.x * yc.x * yc.x, ax);
                 yn.y = scale * fma(S.react, yc.y - yc.y * yc.y * yc.y, ay);
             } else {
-                yn.x = fma(P.alpha, ax, beta * yc.x);
-                yn.y = fma(P.alpha, ay, beta * yc.y);
+                yn.x = fma(scale, ax, beta * yc.x);   // M_LEJA: scale = alpha = 1/gamma
+                yn.y = fma(scale, ay, beta * yc.y);
             }
             if (valid) {
                 const long long off = (long long)(i0 + t) * n1 + j0;
@@ -421,8 +427,8 @@ __device__ __forceinline__ void tile3d(const LejaParams& P, const RowSrc& src, d
                 yn.x = scale * fma(S.react, yc.x - yc.x * yc.x * yc.x, ax);
                 yn.y = scale * fma(S.react, yc.y - yc.y * yc.y * yc.y, ay);
             } else {
-                yn.x = fma(P.alpha, ax, beta * yc.x);
-                yn.y = fma(P.alpha, ay, beta * yc.y);
+                yn.x = fma(scale, ax, beta * yc.x);   // M_LEJA: scale = alpha = 1/gamma
+                yn.y = fma(scale, ay, beta * yc.y);
             }
             if (valid) {
                 const long long off = ((long long)(i0 + t) * n1 + j) * n2 + k0;
@@ -613,6 +619,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d(const __grid_constant__ 
     if (tid == 0) gen0 = (unsigned)(ld_acquire64(&P.ctrl->word) >> 32);
     int active = P.active0;
     const int M = P.max_nodes;
+    const double alpha = P_alpha(P);
     double d0[K], d1[K], d2[K];
 #pragma unroll
     for (int k = 0; k < K; k++) coef_first3(P, k, d0[k], d1[k], d2[k]);
@@ -639,11 +646,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d(const __grid_constant__ 
             if (P.coef_gen && m + 2 < M) coef_write_row<K>(P, m + 2, lane, active, nullptr);
         } else if (m == 1) {
             for (int unit = gw; unit < P.nunits; unit += W)
-                tile<NDIM, K, DIAG, true, M_LEJA, true>(P, P.v, dst, unit, lane, beta, d0, dm, active, 0.0, sy, sp);
+                tile<NDIM, K, DIAG, true, M_LEJA, true>(P, P.v, dst, unit, lane, beta, d0, dm, active, alpha, sy, sp);
         } else {
             const RowSrc src = P.ysrc[par ^ 1];
             for (int unit = gw; unit < P.nunits; unit += W)
-                tile<NDIM, K, DIAG, false, M_LEJA, false>(P, src, dst, unit, lane, beta, d0, dm, active, 0.0, sy, sp);
+                tile<NDIM, K, DIAG, false, M_LEJA, false>(P, src, dst, unit, lane, beta, d0, dm, active, alpha, sy, sp);
         }
         double vals[1 + K];
         vals[0] = sy;
@@ -795,6 +802,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d_step(const __grid_consta
 #pragma unroll
     for (int k = 0; k < K; k++) sp[k] = 0.0;
     const double beta = coef_beta(P, m);
+    const double alpha = P_alpha(P);
     double sy = 0.0;
     double* dst = P.ydst[m & 1];
     if (cwarp) {
@@ -804,11 +812,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d_step(const __grid_consta
         const int W = gridDim.x * kWarps - 1;
         if (m == 1) {
             for (int unit = gw; unit < P.nunits; unit += W)
-                tile<NDIM, K, DIAG, true, M_LEJA, true>(P, P.v, dst, unit, lane, beta, d0, dm, active, 0.0, sy, sp);
+                tile<NDIM, K, DIAG, true, M_LEJA, true>(P, P.v, dst, unit, lane, beta, d0, dm, active, alpha, sy, sp);
         } else {
             const RowSrc src = P.ysrc[(m - 1) & 1];
             for (int unit = gw; unit < P.nunits; unit += W)
-                tile<NDIM, K, DIAG, false, M_LEJA, false>(P, src, dst, unit, lane, beta, d0, dm, active, 0.0, sy, sp);
+                tile<NDIM, K, DIAG, false, M_LEJA, false>(P, src, dst, unit, lane, beta, d0, dm, active, alpha, sy, sp);
         }
     }
     double vals[1 + K];
@@ -1323,6 +1331,28 @@ cudaError_t launch_coef_tables(const double* xi, const double* R, int M, const C
     const int threads = ((M + 31) / 32) * 32;
     if (threads > 1024 || jobs.n < 1) return cudaErrorInvalidValue;
     k_coef_tables<<<jobs.n, threads, M * sizeof(double), s>>>(xi, R, M, jobs, dt, c, gamma, cg_dev, status);
+    return cudaGetLastError();
+}
+
+
+__global__ void k_shift_scale(const unsigned long long* umax, double const_part, double react, double* cg) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double b = const_part;
+        if (react != 0.0) {
+            const double m2 = __longlong_as_double((long long)*umax);
+            const double sft = __dsub_rn(__dmul_rn(3.0, m2), 1.0);
+            if (sft > 0.0) b = __dadd_rn(b, __dmul_rn(react, sft));
+        }
+        const double eig = __dmul_rn(-1.05, b);
+        cg[0] = eig / 2.0;
+        cg[1] = -eig / 4.0;
+        cg[2] = b;
+    }
+}
+
+cudaError_t launch_shift_scale(const unsigned long long* umax, double const_part, double react, double* cg_out,
+                               cudaStream_t s) {
+    k_shift_scale<<<1, 32, 0, s>>>(umax, const_part, react, cg_out);
     return cudaGetLastError();
 }
 

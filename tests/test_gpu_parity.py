@@ -363,3 +363,26 @@ def test_kernel_variants_bitwise_equal(xi300, monkeypatch, shape, K, react):
         np.testing.assert_array_equal(a, b)
     r = O.real_leja_phi(ob, v, dt, c, g, 1, TOL, TOL, xi300, coeffs=coeffs, u_lin=u)
     assert res["tma"][0] == r.iters
+
+
+@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a"])
+def test_integrate_device_spectrum(xi300, method):
+    # lx_integrate: the paper's time loop with (c, gamma) recomputed ON THE DEVICE every
+    # step; the oracle recomputes them from its own state with the same formula (R16).
+    n = 96
+    pb, ob = _pair((n, n), diff=1e-4, nu=0.0, react=1.0)
+    u = W.ic_allen_cahn_2d(n)
+    dt, nsteps = 0.01, 4
+    ud = _dev(u)
+    with lx.Context(pb) as ctx:
+        it, err = lx.lx_integrate(ctx, method, ud, dt, nsteps, TOL, TOL)
+    tot = 0
+    for _ in range(nsteps):
+        c, g = O.shift_scale(O.spectrum_bound(ob, u))
+        r = O.step(ob, method, u, dt, c, g, TOL, TOL, xi300)
+        tot += r.iters
+        u = r.u_high
+    assert it == tot
+    assert _rel(ud, u) <= TOL
+    if method != "rosenbrock_euler":
+        assert err == pytest.approx(r.err, rel=1e-8)
