@@ -79,24 +79,31 @@ def lib():
 
 class OcProblem(ctypes.Structure):
     _fields_ = [("ndim", ctypes.c_int), ("n", ctypes.c_long * 3), ("dx", ctypes.c_double * 3),
-                ("diff", ctypes.c_double), ("nu", ctypes.c_double), ("react", ctypes.c_double)]
+                ("diff", ctypes.c_double), ("nu", ctypes.c_double), ("react", ctypes.c_double),
+                ("source", ctypes.POINTER(ctypes.c_double))]
 
 
-@dataclass(frozen=True)
+@dataclass(frozen=True, eq=False)
 class Problem:
-    """f(u) = diff*lap(u) + nu*sum_d D_d u + react*(u - u^3) on a periodic grid."""
+    """f(u) = diff*lap(u) + nu*sum_d D_d u + react*(u - u^3) [+ source] on a periodic grid."""
     shape: tuple
     dx: tuple
     diff: float = 1.0
     nu: float = 0.0
     react: float = 0.0
+    source: np.ndarray | None = None
 
     def c_struct(self) -> OcProblem:
         nd = len(self.shape)
         n = list(self.shape) + [1] * (3 - nd)
         dx = list(self.dx) + [1.0] * (3 - nd)
+        src = None
+        if self.source is not None:
+            src = np.ascontiguousarray(self.source, dtype=np.float64)
+            assert src.size == self.npoints
+            object.__setattr__(self, "_src_keep", src)
         return OcProblem(nd, (ctypes.c_long * 3)(*n), (ctypes.c_double * 3)(*dx),
-                         float(self.diff), float(self.nu), float(self.react))
+                         float(self.diff), float(self.nu), float(self.react), _dp(src))
 
     @property
     def npoints(self) -> int:

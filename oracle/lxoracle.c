@@ -185,6 +185,7 @@ typedef struct {
     double diff;     /* diffusion coefficient */
     double nu;       /* advection velocity */
     double react;    /* Allen-Cahn reaction weight (0 or 1) */
+    const double *source;  /* optional time-independent source S (Problem II); NULL = none */
 } oc_problem;
 
 static long oc_npoints(const oc_problem *pb)
@@ -278,6 +279,8 @@ void oc_rhs(const oc_problem *pb, const double *u, double *f)
     apply_linear(pb, u, f);
     if (pb->react != 0.0)
         for (long i = 0; i < N; i++) f[i] += pb->react * (u[i] - u[i] * u[i] * u[i]);
+    if (pb->source)   /* Problem II: f(u) = A u + S */
+        for (long i = 0; i < N; i++) f[i] += pb->source[i];
 }
 
 /* w = J(u) y, exact Jacobian (R13). u may be NULL when react == 0. */
@@ -289,7 +292,9 @@ void oc_jac_apply(const oc_problem *pb, const double *u, const double *y, double
         for (long i = 0; i < N; i++) w[i] += pb->react * (1.0 - 3.0 * u[i] * u[i]) * y[i];
 }
 
-/* F(x) = f(x) - J(u) x  =  g(x) - g'(u) x  (R18) */
+/* F(x) = f(x) - J(u) x  =  g(x) - g'(u) x  (R18).  A source S would add the same
+ * constant to every F(x); it cancels in every difference F(x) - F(u) the integrators use,
+ * so it is left out (R21). */
 void oc_nonlinear_remainder(const oc_problem *pb, const double *u, const double *x, double *out)
 {
     long N = oc_npoints(pb);

@@ -51,24 +51,27 @@ class LxError(RuntimeError):
 
 class LxProblem(ctypes.Structure):
     _fields_ = [("ndim", ctypes.c_int), ("n", ctypes.c_int64 * 3), ("dx", ctypes.c_double * 3),
-                ("diff", ctypes.c_double), ("nu", ctypes.c_double), ("react", ctypes.c_double)]
+                ("diff", ctypes.c_double), ("nu", ctypes.c_double), ("react", ctypes.c_double),
+                ("source", ctypes.c_void_p)]
 
 
-@dataclass(frozen=True)
+@dataclass(frozen=True, eq=False)
 class Problem:
-    """du/dt = diff*lap(u) + nu*sum_d D_d u + react*(u - u^3) on a periodic GLOBAL grid."""
+    """du/dt = diff*lap(u) + nu*sum_d D_d u + react*(u - u^3) [+ source] on a periodic GLOBAL grid.
+    source: optional time-independent S (Problem II), the caller's local slab (tensor or ndarray)."""
     shape: tuple
     dx: tuple
     diff: float = 1.0
     nu: float = 0.0
     react: float = 0.0
+    source: object = None
 
     def c_struct(self) -> LxProblem:
         nd = len(self.shape)
         n = list(self.shape) + [1] * (3 - nd)
         dx = list(self.dx) + [1.0] * (3 - nd)
         return LxProblem(nd, (ctypes.c_int64 * 3)(*n), (ctypes.c_double * 3)(*dx), float(self.diff),
-                         float(self.nu), float(self.react))
+                         float(self.nu), float(self.react), _ptr(self.source))
 
     @property
     def npoints(self) -> int:

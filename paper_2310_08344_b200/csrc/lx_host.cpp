@@ -750,6 +750,7 @@ static lx_status run_stage(lx_ctx* ctx, int op, const StageArgs& A0) {
 
 static lx_status rhs_device(lx_ctx* ctx, const lx_problem* pb, const double* u, double scale, double* f) {
     LejaParams P = base_params(ctx, pb);
+    P.source = pb->source;   // device pointer (staged by the caller)
     P.v = RowSrc{u, nullptr, ctx->row, ctx->n_loc, 0};
     P.ydst[0] = f;
     if (ctx->comm) return comm_rhs(ctx->comm, P, scale, ctx->stream, &ctx->launches) ? fail(LX_ERR_NCCL, "rhs halo: %s", comm_error()) : LX_OK;
@@ -760,11 +761,14 @@ static lx_status rhs_device(lx_ctx* ctx, const lx_problem* pb, const double* u, 
     return LX_OK;
 }
 
-lx_status lx_rhs(lx_ctx* ctx, const lx_problem* pb, const double* u, double scale, double* f_out) {
+lx_status lx_rhs(lx_ctx* ctx, const lx_problem* pb0, const double* u, double scale, double* f_out) {
     if (!ctx || !u || !f_out) return fail(LX_ERR_ARG, "NULL argument");
-    LX_TRY(check_problem(ctx, pb));
+    LX_TRY(check_problem(ctx, pb0));
     if (u == f_out) return fail(LX_ERR_ALIAS, "f_out must not alias u");
     Staging sg(ctx);
+    lx_problem pbs = *pb0;
+    const lx_problem* pb = &pbs;
+    LX_TRY(sg.in(pb0->source, &pbs.source));
     const double* ud;
     double* fd;
     LX_TRY(sg.in(u, &ud));
@@ -876,8 +880,11 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
     return run_stage(ctx, ST_FINAL4, A);
 }
 
-lx_status lx_step(lx_ctx* ctx, lx_method method, const lx_problem* pb, const double* u, double* u_low, double* u_high,
+lx_status lx_step(lx_ctx* ctx, lx_method method, const lx_problem* pb0, const double* u, double* u_low, double* u_high,
                   double* err_out, double dt, double c, double gamma, double rtol, double atol, int* iters_out) {
+    if (!pb0) return fail(LX_ERR_ARG, "problem is NULL");
+    lx_problem pbs = *pb0;
+    const lx_problem* pb = &pbs;
     if (!ctx) return fail(LX_ERR_ARG, "ctx is NULL");
     LX_TRY(check_problem(ctx, pb));
     if ((int)method < 0 || (int)method > 3) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
@@ -887,6 +894,7 @@ lx_status lx_step(lx_ctx* ctx, lx_method method, const lx_problem* pb, const dou
     if (u_low && u_low == u_high) return fail(LX_ERR_ALIAS, "u_low must differ from u_high");
     if (!(gamma > 0.0) && dt != 0.0) return fail(LX_ERR_ARG, "gamma must be > 0");
     Staging sg(ctx);
+    LX_TRY(sg.in(pb0->source, &pbs.source));
     const double* ud;
     double *lo = nullptr, *hi;
     LX_TRY(sg.in(u, &ud));
@@ -908,14 +916,17 @@ lx_status lx_step(lx_ctx* ctx, lx_method method, const lx_problem* pb, const dou
 // The paper's time loop (listing alg:lexint) on the device: every step recomputes the
 // spectrum bound (Gershgorin / closed form, x1.05, c = eig/2, gamma = -eig/4) with a
 // device max-reduction + k_shift_scale, so the whole run is enqueued without host round trips.
-lx_status lx_integrate(lx_ctx* ctx, lx_method method, const lx_problem* pb, double* u, double dt, int nsteps,
+lx_status lx_integrate(lx_ctx* ctx, lx_method method, const lx_problem* pb0, double* u, double dt, int nsteps,
                        double rtol, double atol, int* iters_out, double* err_out) {
-    if (!ctx || !u) return fail(LX_ERR_ARG, "NULL argument");
+    if (!ctx || !u || !pb0) return fail(LX_ERR_ARG, "NULL argument");
+    lx_problem pbs = *pb0;
+    const lx_problem* pb = &pbs;
     LX_TRY(check_problem(ctx, pb));
     if ((int)method < 0 || (int)method > 3) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
     if (nsteps < 0) return fail(LX_ERR_ARG, "nsteps < 0");
     if (!std::isfinite(dt)) return fail(LX_ERR_ARG, "dt not finite");
     Staging sg(ctx);
+    LX_TRY(sg.in(pb0->source, &pbs.source));
     const double* uin;
     double* ud;
     LX_TRY(sg.in(u, &uin));

@@ -108,6 +108,7 @@ struct LejaParams {
     // device-resident (c, gamma) (lx_integrate: spectrum recomputed on the device every step);
     // nullptr -> cc / cgamma / alpha from the host
     const double* cg_dev;
+    const double* source;  // optional source S added by the f(u) (M_RHS) tiles (Problem II)
 };
 
 // launchers (lx_kernels.cu)

@@ -275,9 +275,16 @@ __device__ __forceinline__ void tile2d(const LejaParams& P, const RowSrc& src, d
                 yn.x = scale * ax;
                 yn.y = scale * ay;
             } else if (MODE == M_RHS) {
-                // f(u)*scale = scale*(A u + react*(u - u^3))
-                yn.x = scale * fma(S.react, yc.x - yc.x * yc.x * yc.x, ax);
-                yn.y = scale * fma(S.react, yc.y - yc.y * yc.y * yc.y, ay);
+                // f(u)*scale = scale*(A u + react*(u - u^3) [+ S])
+                double fx = fma(S.react, yc.x - yc.x * yc.x * yc.x, ax);
+                double fy = fma(S.react, yc.y - yc.y * yc.y * yc.y, ay);
+                if (P.source && valid) {
+                    const double2 sv = ldg2(P.source + (long long)(i0 + t) * n1 + j0);
+                    fx += sv.x;
+                    fy += sv.y;
+                }
+                yn.x = scale * fx;
+                yn.y = scale * fy;
             } else {
                 yn.x = fma(scale, ax, beta * yc.x);   // M_LEJA: scale = alpha = 1/gamma
                 yn.y = fma(scale, ay, beta * yc.y);
@@ -424,8 +431,15 @@ __device__ __forceinline__ void tile3d(const LejaParams& P, const RowSrc& src, d
                 yn.x = scale * ax;
                 yn.y = scale * ay;
             } else if (MODE == M_RHS) {
-                yn.x = scale * fma(S.react, yc.x - yc.x * yc.x * yc.x, ax);
-                yn.y = scale * fma(S.react, yc.y - yc.y * yc.y * yc.y, ay);
+                double fx = fma(S.react, yc.x - yc.x * yc.x * yc.x, ax);
+                double fy = fma(S.react, yc.y - yc.y * yc.y * yc.y, ay);
+                if (P.source && valid) {
+                    const double2 sv = ldg2(P.source + ((long long)(i0 + t) * n1 + j) * n2 + k0);
+                    fx += sv.x;
+                    fy += sv.y;
+                }
+                yn.x = scale * fx;
+                yn.y = scale * fy;
             } else {
                 yn.x = fma(scale, ax, beta * yc.x);   // M_LEJA: scale = alpha = 1/gamma
                 yn.y = fma(scale, ay, beta * yc.y);

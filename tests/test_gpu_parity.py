@@ -386,3 +386,33 @@ def test_integrate_device_spectrum(xi300, method):
     assert _rel(ud, u) <= TOL
     if method != "rosenbrock_euler":
         assert err == pytest.approx(r.err, rel=1e-8)
+
+
+@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb43"])
+def test_problem2_source(xi300, method):
+    # Problem II: f(u) = A u + S, time-independent source
+    n = 128
+    S = W.source_problem2_2d(n)
+    dx = (2 / n, 2 / n)
+    ob = O.Problem((n, n), dx, 1.0, 10.0, 0.0, S)
+    u0 = W.ic_problem1_2d(n)
+    dt = 10 * W.dt_cfl(n, 10.0)
+    for src in (_dev(S), S):   # device and host source pointers
+        pb = lx.Problem((n, n), dx, 1.0, 10.0, 0.0, src)
+        with lx.Context(pb) as ctx:
+            c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+            lo = torch.empty((n, n), dtype=torch.float64, device="cuda")
+            hi = torch.empty_like(lo)
+            it, err = lx.lx_step(ctx, method, _dev(u0), lo, hi, dt, c, g, TOL, TOL)
+            r = O.step(ob, method, u0, dt, c, g, TOL, TOL, xi300)
+            assert it == r.iters
+            assert _rel(hi, r.u_high) <= TOL
+            ud = _dev(u0)
+            it2, _ = lx.lx_integrate(ctx, method, ud, dt, 2, TOL, TOL)
+            u = u0
+            tot = 0
+            for _ in range(2):
+                r = O.step(ob, method, u, dt, c, g, TOL, TOL, xi300)
+                tot += r.iters
+                u = r.u_high
+            assert it2 == tot and _rel(ud, u) <= TOL

@@ -227,3 +227,23 @@ def test_leja_3d_vs_fft_exact(xi300, l):
     sym = refs.impulse_symbol(lambda x: O.jac_apply(pb, None, x), shape)
     ex = refs.fft_apply_phi(sym, v, dt, l)
     assert np.linalg.norm(r.outs[0] - ex) <= 1e-11 * np.linalg.norm(ex)
+
+
+def test_problem2_rosenbrock_euler_exact(xi300):
+    # Problem II: u' = A u + S.  Rosenbrock-Euler with the source in f is the exact update
+    # u(dt) = exp(dt A) u0 + dt phi_1(dt A) S  (P:586 with the dt factor, reading R12).
+    n = 64
+    S = W.source_problem2_2d(n)
+    pb = O.Problem((n, n), (2 / n, 2 / n), 1.0, 10.0, 0.0, S)
+    c, g = _cg(pb)
+    dt = 10 * W.dt_cfl(n, 10.0)
+    u0 = W.ic_problem1_2d(n)
+    r = O.step(pb, "rosenbrock_euler", u0, dt, c, g, 1e-13, 1e-13, xi300)
+    assert r.status == O.OK
+    sym = refs.impulse_symbol(lambda x: O.jac_apply(pb, None, x), (n, n))
+    ex = refs.fft_apply_phi(sym, u0, dt, 0) + dt * refs.fft_apply_phi(sym, S, dt, 1)
+    assert np.linalg.norm(r.u_high - ex) <= 1e-11 * np.linalg.norm(ex)
+    # higher-order integrators are exact too: their remainders vanish (S cancels in F(x) - F(u), R21)
+    for m in ("exprb32", "exprb43", "epirk4s3a"):
+        rm = O.step(pb, m, u0, dt, c, g, 1e-13, 1e-13, xi300)
+        assert np.linalg.norm(rm.u_high - ex) <= 1e-11 * np.linalg.norm(ex)
