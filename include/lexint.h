@@ -210,7 +210,8 @@ typedef enum {
     LX_ROSENBROCK_EULER = 0,
     LX_EXPRB32 = 1,
     LX_EXPRB43 = 2,
-    LX_EPIRK4S3A = 3
+    LX_EPIRK4S3A = 3,
+    LX_EXPRB42 = 4        /* Luan 2017 (cited at P:83), 4th order, non-embedded (err = 0) */
 } lx_method;
 
 /* Rosenbrock-Euler: u_out = u + phi_1(dt J(u)) f(u) dt (alg:Ros_Eu). */
@@ -226,6 +227,9 @@ lx_status lx_step_exprb43(lx_ctx *ctx, const lx_problem *pb, const double *u, do
 lx_status lx_step_epirk4s3a(lx_ctx *ctx, const lx_problem *pb, const double *u, double *u_low,
                             double *u_high, double *err_out, double dt, double c, double gamma,
                             double rtol, double atol, int *iters_out);
+/* EXPRB42 (reading R22): a = u + 3/4 hphi_1(3/4 hJ) f; u_out = u + hphi_1(hJ) f + 32/9 hphi_3(hJ) D_a. */
+lx_status lx_step_exprb42(lx_ctx *ctx, const lx_problem *pb, const double *u, double *u_out, double dt,
+                          double c, double gamma, double rtol, double atol, int *iters_out);
 /* Dispatch by method (the paper's exp_int / embed_exp_int). */
 lx_status lx_step(lx_ctx *ctx, lx_method method, const lx_problem *pb, const double *u,
                   double *u_low, double *u_high, double *err_out, double dt, double c,

@@ -435,7 +435,7 @@ done:
 /* ------------------------------------------------------------------------- */
 /* Exponential integrators (listings alg:Ros_Eu, alg:exprb32;      */
 /* EXPRB43 and EPIRK4s3A tableaux from P:83's citations, R17).                */
-/*   method 0 Rosenbrock-Euler, 1 EXPRB32, 2 EXPRB43, 3 EPIRK4s3A.             */
+/*   method 0 Rosenbrock-Euler, 1 EXPRB32, 2 EXPRB43, 3 EPIRK4s3A, 4 EXPRB42.   */
 /* u_low may be NULL for Rosenbrock-Euler (non-embedded, err = 0).            */
 /* ------------------------------------------------------------------------- */
 static void axpby(double a, const double *x, double b, const double *y, double *z, long N)
@@ -451,7 +451,7 @@ int oc_step(const oc_problem *pb, int method, const double *u, double *u_low, do
     int it = 0, total = 0, s = OC_OK;
     if (err) *err = 0.0;
     if (iters) *iters = 0;
-    if (method < 0 || method > 3) return OC_ERR_ARG;
+    if (method < 0 || method > 4) return OC_ERR_ARG;
     size_t bytes = sizeof(double) * (size_t)N;
     double *f_u = (double *)malloc(bytes);
     double *t1 = (double *)malloc(bytes), *t2 = (double *)malloc(bytes), *t3 = (double *)malloc(bytes);
@@ -490,6 +490,28 @@ int oc_step(const oc_problem *pb, int method, const double *u, double *u_low, do
         axpby(1.0, u_low, 2.0, t5, u_high, N);                /* u_exprb3 = a + 2 u_nl_3 */
         for (long i = 0; i < N; i++) t6[i] = 2.0 * t5[i];      /* error_vector */
         if (err) *err = oc_l2norm_scaled(t6, N);
+    } else if (method == 4) {
+        /* EXPRB42 (Luan 2017, cited at P:83; reading R22):
+         *   a = u + 3/4 h phi_1(3/4 hJ) f(u)
+         *   u_{n+1} = u + h phi_1(hJ) f(u) + 32/9 h phi_3(hJ) D_a,   D_a = dt (F(a) - F(u))
+         * non-embedded (u_low = u_high, err = 0). */
+        double cf[2] = {0.75, 1.0};
+        double *pv[2] = {t1, t2};
+        s = oc_real_leja_phi(pb, u, f_u, pv, cf, 2, dt, c, gamma, 1, rtol, atol, xi, max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        axpby(1.0, u, 0.75, t1, t3, N);                       /* a */
+        oc_nonlinear_remainder(pb, u, u, t4);                 /* NL_u */
+        oc_nonlinear_remainder(pb, u, t3, t5);                /* NL_a */
+        axpby(dt, t5, -dt, t4, t6, N);                        /* D_a */
+        for (long i = 0; i < N; i++) t6[i] = (32.0 / 9.0) * t6[i];
+        double one = 1.0;
+        double *o3[1] = {t7};
+        s = oc_real_leja_phi(pb, u, t6, o3, &one, 1, dt, c, gamma, 3, rtol, atol, xi, max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        for (long i = 0; i < N; i++) u_high[i] = u[i] + t2[i] + t7[i];
+        if (u_low) for (long i = 0; i < N; i++) u_low[i] = u_high[i];
     } else {
         /* EXPRB43 (method 2) / EPIRK4s3A (method 3) -- R17 tableaux:
          *  EXPRB43:   a = u + 1/2 hphi_1(hJ/2) f;  b = u + hphi_1 f + hphi_1 D_a

@@ -787,7 +787,7 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
     if (!S0) return fail(LX_ERR_CUDA, "scratch allocation failed");
     const double one = 1.0;
     // all coefficient tables of the step in one device launch
-    static const double c1[1] = {1.0}, c2[2] = {0.5, 1.0}, c3[3] = {0.5, 2.0 / 3.0, 1.0};
+    static const double c1[1] = {1.0}, c2[2] = {0.5, 1.0}, c3[3] = {0.5, 2.0 / 3.0, 1.0}, c42[2] = {0.75, 1.0};
     const double* tab[4] = {nullptr, nullptr, nullptr, nullptr};
     if (!ctx->cg_active && ((ctx->ndim == 2 && ctx->variant == 1 && !ctx->comm) || ctx->coef_table)) {
         TableSpec specs[4];
@@ -796,6 +796,9 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
             specs[n++] = {1, 1, c1};
         } else if (method == LX_EXPRB32) {
             specs[n++] = {1, 1, c1};
+            specs[n++] = {3, 1, c1};
+        } else if (method == LX_EXPRB42) {
+            specs[n++] = {1, 2, c42};
             specs[n++] = {3, 1, c1};
         } else if (method == LX_EXPRB43) {
             specs[n++] = {1, 2, c2};
@@ -833,6 +836,23 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
         A.x0 = lo; A.x1 = hi; A.y0 = hi;
         return run_stage(ctx, ST_FINAL_EXPRB32, A);
     }
+    if (method == LX_EXPRB42) {
+        // EXPRB42 (reading R22): a = u + 3/4 p_34 ; u+ = u + p_1 + phi_3(hJ) (32/9 D_a)
+        double* S1 = scratch(ctx, 1);
+        double* S2 = scratch(ctx, 2);
+        if (!S1 || !S2) return fail(LX_ERR_CUDA, "scratch allocation failed");
+        double* pv[2] = {S1, S2};
+        LX_TRY(leja_device(ctx, pb, ul, S0, pv, c42, 2, dt, c, gamma, 1, rtol, atol, rec, tab[0]));
+        A.x0 = u; A.x1 = S1; A.x2 = nullptr; A.a0 = 0.75; A.a1 = 0.0; A.a2 = 32.0 / 9.0; A.y0 = S0;
+        LX_TRY(run_stage(ctx, ST_STAGE_REMAINDER, A));
+        double* o3[1] = {S1};
+        LX_TRY(leja_device(ctx, pb, ul, S0, o3, &one, 1, dt, c, gamma, 3, rtol, atol, rec, tab[1]));
+        A = stage_args(ctx, pb, rec);
+        A.x0 = u; A.x1 = S2; A.x2 = S1; A.y0 = hi;
+        LX_TRY(run_stage(ctx, ST_SUM3, A));
+        if (lo && lo != hi) CUDA_TRY(cudaMemcpyAsync(lo, hi, ctx->N_loc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+        return LX_OK;
+    }
     // EXPRB43 / EPIRK4s3A (reading R17)
     const bool epirk = method == LX_EPIRK4S3A;
     double* S1 = scratch(ctx, 1);
@@ -844,19 +864,19 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
     LX_TRY(leja_device(ctx, pb, ul, S0, pv, epirk ? cf3 : cf2, epirk ? 3 : 2, dt, c, gamma, 1, rtol, atol, rec, tab[0]));
     double* p_one = epirk ? S3 : S2;
     // D_a = dt F(u + 1/2 p_half) - dt F(u)  -> S0
-    A.x0 = u; A.x1 = S1; A.x2 = nullptr; A.a0 = 0.5; A.a1 = 0.0; A.y0 = S0;
+    A.x0 = u; A.x1 = S1; A.x2 = nullptr; A.a0 = 0.5; A.a1 = 0.0; A.a2 = 1.0; A.y0 = S0;
     LX_TRY(run_stage(ctx, ST_STAGE_REMAINDER, A));
     double* Db;
     if (epirk) {
         // D_b = dt F(u + 2/3 p_23) - dt F(u) -> S1
-        A.x0 = u; A.x1 = S2; A.x2 = nullptr; A.a0 = 2.0 / 3.0; A.a1 = 0.0; A.y0 = S1;
+        A.x0 = u; A.x1 = S2; A.x2 = nullptr; A.a0 = 2.0 / 3.0; A.a1 = 0.0; A.a2 = 1.0; A.y0 = S1;
         LX_TRY(run_stage(ctx, ST_STAGE_REMAINDER, A));
         Db = S1;
     } else {
         // phi_1(hJ) D_a -> S1 ; b = u + p_one + S1 ; D_b -> lo
         double* o[1] = {S1};
         LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 1, rtol, atol, rec, tab[1]));
-        A.x0 = u; A.x1 = p_one; A.x2 = S1; A.a0 = 1.0; A.a1 = 1.0; A.y0 = lo;
+        A.x0 = u; A.x1 = p_one; A.x2 = S1; A.a0 = 1.0; A.a1 = 1.0; A.a2 = 1.0; A.y0 = lo;
         LX_TRY(run_stage(ctx, ST_STAGE_REMAINDER, A));
         Db = lo;
     }
@@ -887,9 +907,10 @@ lx_status lx_step(lx_ctx* ctx, lx_method method, const lx_problem* pb0, const do
     const lx_problem* pb = &pbs;
     if (!ctx) return fail(LX_ERR_ARG, "ctx is NULL");
     LX_TRY(check_problem(ctx, pb));
-    if ((int)method < 0 || (int)method > 3) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
+    if ((int)method < 0 || (int)method > 4) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
     if (!u || !u_high) return fail(LX_ERR_ARG, "NULL argument");
-    if (method != LX_ROSENBROCK_EULER && !u_low) return fail(LX_ERR_ARG, "u_low required for embedded methods");
+    if (method != LX_ROSENBROCK_EULER && method != LX_EXPRB42 && !u_low)
+        return fail(LX_ERR_ARG, "u_low required for embedded methods");
     if (u_low == u || u_high == u) return fail(LX_ERR_ALIAS, "outputs must not alias u");
     if (u_low && u_low == u_high) return fail(LX_ERR_ALIAS, "u_low must differ from u_high");
     if (!(gamma > 0.0) && dt != 0.0) return fail(LX_ERR_ARG, "gamma must be > 0");
@@ -909,7 +930,7 @@ lx_status lx_step(lx_ctx* ctx, lx_method method, const lx_problem* pb0, const do
     Record r;
     LX_TRY(read_record(ctx, 0, &r));
     if (iters_out) *iters_out = r.iters;
-    if (err_out) *err_out = (method == LX_ROSENBROCK_EULER) ? 0.0 : r.err;
+    if (err_out) *err_out = (method == LX_ROSENBROCK_EULER || method == LX_EXPRB42) ? 0.0 : r.err;
     return status_of(r);
 }
 
@@ -922,7 +943,7 @@ lx_status lx_integrate(lx_ctx* ctx, lx_method method, const lx_problem* pb0, dou
     lx_problem pbs = *pb0;
     const lx_problem* pb = &pbs;
     LX_TRY(check_problem(ctx, pb));
-    if ((int)method < 0 || (int)method > 3) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
+    if ((int)method < 0 || (int)method > 4) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
     if (nsteps < 0) return fail(LX_ERR_ARG, "nsteps < 0");
     if (!std::isfinite(dt)) return fail(LX_ERR_ARG, "dt not finite");
     Staging sg(ctx);
@@ -981,8 +1002,13 @@ lx_status lx_integrate(lx_ctx* ctx, lx_method method, const lx_problem* pb0, dou
     Record r;
     LX_TRY(read_record(ctx, 0, &r));
     if (iters_out) *iters_out = r.iters;
-    if (err_out) *err_out = (method == LX_ROSENBROCK_EULER) ? 0.0 : r.err;
+    if (err_out) *err_out = (method == LX_ROSENBROCK_EULER || method == LX_EXPRB42) ? 0.0 : r.err;
     return status_of(r);
+}
+
+lx_status lx_step_exprb42(lx_ctx* ctx, const lx_problem* pb, const double* u, double* u_out, double dt, double c,
+                          double gamma, double rtol, double atol, int* iters_out) {
+    return lx_step(ctx, LX_EXPRB42, pb, u, nullptr, u_out, nullptr, dt, c, gamma, rtol, atol, iters_out);
 }
 
 lx_status lx_step_rosenbrock_euler(lx_ctx* ctx, const lx_problem* pb, const double* u, double* u_out, double dt,

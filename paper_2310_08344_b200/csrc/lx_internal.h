@@ -140,12 +140,13 @@ enum StageOp {
     ST_RHS_SCALED = 0,    // y0 = a0 * f(src)                       (stencil)
     ST_AXPBY = 1,         // y0 = a0*x0 + a1*x1
     ST_REMAINDER_DIFF,    // y0 = dt*F(x0) - dt*F(u)   F(x)=g(x)-g'(u)x      (R18)
-    ST_STAGE_REMAINDER,   // s = x0 + a0*x1 + a1*x2 ; y0 = dt*F(s) - dt*F(u)  (s not stored)
+    ST_STAGE_REMAINDER,   // s = x0 + a0*x1 + a1*x2 ; y0 = a2*(dt*F(s) - dt*F(u))  (s not stored)
     ST_EXPRB32_A,         // y1 = x0 + x1 (a) ; y0 = dt*F(a) - dt*F(u)
     ST_COMBINE2,          // y0 = a0*x0 + a1*x1 ; y1 = a2*x0 + a3*x1
     ST_FINAL4,            // y0 = x0 + x1 + x2 (u3) ; y1 = y0 + x3 (u4) ; err = ||y1 - y0||
     ST_FINAL_EXPRB32,     // y0 = x0 + 2 x1 ; err = ||2 x1||
     ST_MAXSQ,             // ctrl->umax = max x0^2
+    ST_SUM3,              // y0 = x0 + x1 + x2
 };
 cudaError_t launch_stage(int op, const StageArgs& A, cudaStream_t s);
 cudaError_t launch_rhs(const LejaParams& P, double scale, cudaStream_t s);

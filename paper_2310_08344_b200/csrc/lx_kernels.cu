@@ -1411,7 +1411,8 @@ __global__ void __launch_bounds__(kThreads) k_stage_pointwise(const __grid_const
     // before any store (outputs may alias inputs element-wise, which blocks the compiler from
     // overlapping trips on its own), so every thread keeps UN x (inputs) 16-byte loads in flight.
     constexpr int UN = 4;
-    constexpr int NIN = (OP == ST_FINAL4) ? 4 : (OP == ST_STAGE_REMAINDER) ? 4 : (OP == ST_MAXSQ) ? 1 : 2;
+    constexpr int NIN = (OP == ST_FINAL4) ? 4 : (OP == ST_STAGE_REMAINDER) ? 4 : (OP == ST_SUM3) ? 3
+                                                                                : (OP == ST_MAXSQ) ? 1 : 2;
     __shared__ double s_red[kWarps][kSlot];
     __shared__ int s_last;
     const long long npair = (long long)A.n_loc * A.n1 * A.n2 / 2;
@@ -1452,8 +1453,9 @@ __global__ void __launch_bounds__(kThreads) k_stage_pointwise(const __grid_const
                 const double2 x = v[q][0], u = v[q][1], p = v[q][2], r = v[q][3];
                 const double sx = x.x + A.a0 * p.x + A.a1 * r.x;
                 const double sy = x.y + A.a0 * p.y + A.a1 * r.y;
-                st2(A.y0 + o, make_double2(dt * nl_rem(react, sx, u.x) + (-dt) * nl_rem(react, u.x, u.x),
-                                           dt * nl_rem(react, sy, u.y) + (-dt) * nl_rem(react, u.y, u.y)));
+                const double Dx = dt * nl_rem(react, sx, u.x) + (-dt) * nl_rem(react, u.x, u.x);
+                const double Dy = dt * nl_rem(react, sy, u.y) + (-dt) * nl_rem(react, u.y, u.y);
+                st2(A.y0 + o, make_double2(A.a2 * Dx, A.a2 * Dy));
             } else if (OP == ST_EXPRB32_A) {
                 const double2 u = v[q][0], p = v[q][1];
                 const double2 a = make_double2(u.x + p.x, u.y + p.y);
@@ -1479,6 +1481,9 @@ __global__ void __launch_bounds__(kThreads) k_stage_pointwise(const __grid_const
                 const double ex = 2.0 * qq.x, ey = 2.0 * qq.y;
                 acc = fma(ex, ex, acc);
                 acc = fma(ey, ey, acc);
+            } else if (OP == ST_SUM3) {
+                const double2 x = v[q][0], y = v[q][1], z = v[q][2];
+                st2(A.y0 + o, make_double2(x.x + y.x + z.x, x.y + y.y + z.y));
             } else if (OP == ST_MAXSQ) {
                 const double2 x = v[q][0];
                 const double m2 = fmax(x.x * x.x, x.y * x.y);
@@ -1526,6 +1531,7 @@ static void* stage_kernel_ptr(int op) {
         case ST_FINAL4: return (void*)k_stage_pointwise<ST_FINAL4>;
         case ST_FINAL_EXPRB32: return (void*)k_stage_pointwise<ST_FINAL_EXPRB32>;
         case ST_MAXSQ: return (void*)k_stage_pointwise<ST_MAXSQ>;
+        case ST_SUM3: return (void*)k_stage_pointwise<ST_SUM3>;
     }
     return nullptr;
 }
@@ -1558,6 +1564,7 @@ cudaError_t launch_stage(int op, const StageArgs& A, cudaStream_t s) {
         case ST_FINAL4: k_stage_pointwise<ST_FINAL4><<<g, b, 0, s>>>(A); break;
         case ST_FINAL_EXPRB32: k_stage_pointwise<ST_FINAL_EXPRB32><<<g, b, 0, s>>>(A); break;
         case ST_MAXSQ: k_stage_pointwise<ST_MAXSQ><<<g, b, 0, s>>>(A); break;
+        case ST_SUM3: k_stage_pointwise<ST_SUM3><<<g, b, 0, s>>>(A); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
