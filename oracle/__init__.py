@@ -80,7 +80,7 @@ def lib():
 class OcProblem(ctypes.Structure):
     _fields_ = [("ndim", ctypes.c_int), ("n", ctypes.c_long * 3), ("dx", ctypes.c_double * 3),
                 ("diff", ctypes.c_double), ("nu", ctypes.c_double), ("react", ctypes.c_double),
-                ("source", ctypes.POINTER(ctypes.c_double))]
+                ("flux", ctypes.c_double), ("source", ctypes.POINTER(ctypes.c_double))]
 
 
 @dataclass(frozen=True, eq=False)
@@ -92,6 +92,7 @@ class Problem:
     nu: float = 0.0
     react: float = 0.0
     source: np.ndarray | None = None
+    flux: float = 0.0
 
     def c_struct(self) -> OcProblem:
         nd = len(self.shape)
@@ -103,7 +104,7 @@ class Problem:
             assert src.size == self.npoints
             object.__setattr__(self, "_src_keep", src)
         return OcProblem(nd, (ctypes.c_long * 3)(*n), (ctypes.c_double * 3)(*dx),
-                         float(self.diff), float(self.nu), float(self.react), _dp(src))
+                         float(self.diff), float(self.nu), float(self.react), float(self.flux), _dp(src))
 
     @property
     def npoints(self) -> int:

@@ -185,6 +185,7 @@ typedef struct {
     double diff;     /* diffusion coefficient */
     double nu;       /* advection velocity */
     double react;    /* Allen-Cahn reaction weight (0 or 1) */
+    double flux;     /* Burgers flux weight beta: f += (beta/2) sum_d D_d(u^2) (Problem III) */
     const double *source;  /* optional time-independent source S (Problem II); NULL = none */
 } oc_problem;
 
@@ -270,6 +271,41 @@ void oc_jac_apply_slab(const oc_problem *pb, long n_loc, const double *u, const 
                 w[idx] = pb->diff * lap + pb->nu * adv;
                 if (pb->react != 0.0) w[idx] += pb->react * (1.0 - 3.0 * u[idx] * u[idx]) * y_gh[row + idx];
             }
+    /* (flux problems are not supported by the slab emulation) */
+}
+
+/* sum_d D_d w (third-order upwind, +x-biased, R10) of a pointwise field w */
+static void apply_upwind_sum(const oc_problem *pb, const double *w, double *out)
+{
+    long n0 = pb->n[0], n1 = pb->n[1], n2 = pb->ndim == 3 ? pb->n[2] : 1;
+    for (long i0 = 0; i0 < n0; i0++)
+        for (long i1 = 0; i1 < n1; i1++)
+            for (long i2 = 0; i2 < n2; i2++) {
+                double adv = 0.0;
+                for (int d = 0; d < pb->ndim; d++) {
+                    double h = pb->dx[d];
+                    double um1 = at(pb, w, i0, i1, i2, d, -1);
+                    double u0 = at(pb, w, i0, i1, i2, d, 0);
+                    double up1 = at(pb, w, i0, i1, i2, d, 1);
+                    double up2 = at(pb, w, i0, i1, i2, d, 2);
+                    adv += (-up2 + 6.0 * up1 - 3.0 * u0 - 2.0 * um1) / (6.0 * h);
+                }
+                out[pidx(pb, i0, i1, i2)] = adv;
+            }
+}
+
+/* Burgers flux part of f and J (Problem III): (beta/2) sum_d D_d(u^2) and its exact
+ * Jacobian beta sum_d D_d(u y) (R13).  out += beta * scale * sum_d D_d(a .* b). */
+static void add_flux(const oc_problem *pb, const double *a, const double *b, double scale, double *out)
+{
+    long N = oc_npoints(pb);
+    double *w = (double *)malloc(sizeof(double) * (size_t)N);
+    double *t = (double *)malloc(sizeof(double) * (size_t)N);
+    for (long i = 0; i < N; i++) w[i] = a[i] * b[i];
+    apply_upwind_sum(pb, w, t);
+    for (long i = 0; i < N; i++) out[i] += pb->flux * scale * t[i];
+    free(w);
+    free(t);
 }
 
 /* f(u) (Eq. (1); problems P:559; R16) */
@@ -277,6 +313,7 @@ void oc_rhs(const oc_problem *pb, const double *u, double *f)
 {
     long N = oc_npoints(pb);
     apply_linear(pb, u, f);
+    if (pb->flux != 0.0) add_flux(pb, u, u, 0.5, f);     /* (beta/2) sum_d D_d(u^2) */
     if (pb->react != 0.0)
         for (long i = 0; i < N; i++) f[i] += pb->react * (u[i] - u[i] * u[i] * u[i]);
     if (pb->source)   /* Problem II: f(u) = A u + S */
@@ -288,6 +325,7 @@ void oc_jac_apply(const oc_problem *pb, const double *u, const double *y, double
 {
     long N = oc_npoints(pb);
     apply_linear(pb, y, w);
+    if (pb->flux != 0.0) add_flux(pb, u, y, 1.0, w);     /* beta sum_d D_d(u y) */
     if (pb->react != 0.0)
         for (long i = 0; i < N; i++) w[i] += pb->react * (1.0 - 3.0 * u[i] * u[i]) * y[i];
 }
@@ -307,6 +345,17 @@ void oc_nonlinear_remainder(const oc_problem *pb, const double *u, const double 
             out[i] = 0.0;
         }
     }
+    if (pb->flux != 0.0) {
+        /* Burgers: F(x) = sum_d D_d(beta/2 x^2 - beta u x)  (f(x) - J(u)x, diffusion and linear
+         * advection cancelled exactly, R18) */
+        double *w = (double *)malloc(sizeof(double) * (size_t)N);
+        double *t = (double *)malloc(sizeof(double) * (size_t)N);
+        for (long i = 0; i < N; i++) w[i] = 0.5 * pb->flux * x[i] * x[i] - pb->flux * u[i] * x[i];
+        apply_upwind_sum(pb, w, t);
+        for (long i = 0; i < N; i++) out[i] += t[i];
+        free(w);
+        free(t);
+    }
 }
 
 /* Spectral bound |lambda_max| (R9, R16): Fourier symbol of the constant part
@@ -314,10 +363,17 @@ void oc_nonlinear_remainder(const oc_problem *pb, const double *u, const double 
  * plus the Gershgorin shift of the reaction, react * max(0, 3 max u^2 - 1). */
 double oc_spectrum_bound(const oc_problem *pb, const double *u)
 {
+    double vmax = fabs(pb->nu);
+    if (pb->flux != 0.0 && u) {   /* Burgers: frozen-coefficient speed |nu| + |beta| max|u| (R23) */
+        long N = oc_npoints(pb);
+        double m = 0.0;
+        for (long i = 0; i < N; i++) if (u[i] * u[i] > m) m = u[i] * u[i];
+        vmax = fabs(pb->nu) + fabs(pb->flux) * sqrt(m);
+    }
     double b = 0.0;
     for (int d = 0; d < pb->ndim; d++) {
         double h = pb->dx[d];
-        b += 4.0 * pb->diff / (h * h) + 4.0 * fabs(pb->nu) / (3.0 * h);
+        b += 4.0 * pb->diff / (h * h) + 4.0 * vmax / (3.0 * h);
     }
     if (pb->react != 0.0 && u) {
         long N = oc_npoints(pb);

@@ -247,3 +247,29 @@ def test_problem2_rosenbrock_euler_exact(xi300):
     for m in ("exprb32", "exprb43", "epirk4s3a"):
         rm = O.step(pb, m, u0, dt, c, g, 1e-13, 1e-13, xi300)
         assert np.linalg.norm(rm.u_high - ex) <= 1e-11 * np.linalg.norm(ex)
+
+
+@pytest.mark.parametrize("method,order", [("rosenbrock_euler", 2), ("exprb32", 3), ("exprb43", 4),
+                                          ("epirk4s3a", 4), ("exprb42", 4)])
+def test_integrator_order_burgers(xi300, method, order):
+    # Problem III: viscous Burgers, exact Jacobian (R13), P:593 initial condition
+    n, T = 24, 0.005
+    pb = O.Problem((n, n), (2 / n, 2 / n), 1.0, 0.0, 0.0, None, 10.0)
+    u0 = W.ic_burgers_2d(n)
+
+    def f(t, y):
+        return O.rhs(pb, y.reshape(n, n)).ravel()
+
+    ref = scipy.integrate.solve_ivp(f, (0, T), u0.ravel(), method="DOP853", rtol=1e-13, atol=1e-13).y[:, -1]
+    errs = []
+    for ns in (4, 8, 16):
+        h = T / ns
+        u = u0.copy()
+        for _ in range(ns):
+            c, g = _cg(pb, u)
+            r = O.step(pb, method, u, h, c, g, 1e-14, 1e-14, xi300)
+            assert r.status == O.OK
+            u = r.u_high
+        errs.append(np.linalg.norm(u.ravel() - ref) / np.linalg.norm(ref))
+    orders = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+    assert abs(orders[-1] - order) < 0.3, (errs, orders)

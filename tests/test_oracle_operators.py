@@ -147,3 +147,47 @@ def test_l2norm_scaled():
     assert O.l2norm_scaled(np.array([3.0, 4.0])) == pytest.approx(5 / np.sqrt(2), rel=1e-16)
     assert O.l2norm_scaled(np.zeros(7)) == 0.0
     assert O.l2norm_scaled(np.full(1001, -2.5)) == pytest.approx(2.5, rel=1e-15)
+
+
+# ---------------------------------------------------------------- Problem III: viscous Burgers
+def _burgers(n, beta=10.0):
+    return O.Problem((n, n), (2 / n, 2 / n), 1.0, 0.0, 0.0, None, beta)
+
+
+def test_burgers_flux_third_order():
+    # (beta/2) sum_d D_d(u^2) -> beta u (u_x + u_y) at third order (P:549 upwind, R10)
+    errs = []
+    for n in (32, 64, 128):
+        x, y = W.grid_2d(n)
+        k = 2 * np.pi
+        u = 2.0 + 0.3 * np.sin(k * x) * np.cos(k * y)
+        ux = 0.3 * k * np.cos(k * x) * np.cos(k * y)
+        uy = -0.3 * k * np.sin(k * x) * np.sin(k * y)
+        pb = O.Problem((n, n), (2 / n, 2 / n), 0.0, 0.0, 0.0, None, 1.0)
+        errs.append(np.abs(O.rhs(pb, u) - u * (ux + uy)).max())
+    orders = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+    assert np.all(np.abs(orders - 3.0) < 0.2), orders
+
+
+def test_burgers_jacobian_and_remainder():
+    n = 32
+    pb = _burgers(n)
+    u = W.ic_burgers_2d(n)
+    v = W.random_vector((n, n), seed=3)
+    eps = 1e-6
+    fd = (O.rhs(pb, u + eps * v) - O.rhs(pb, u - eps * v)) / (2 * eps)
+    jv = O.jac_apply(pb, u, v)
+    assert np.linalg.norm(jv - fd) <= 1e-8 * np.linalg.norm(jv)          # exact J (R13)
+    x = u + 0.01 * v
+    lit = O.rhs(pb, x) - O.jac_apply(pb, u, x)
+    assert np.abs(O.nonlinear_remainder(pb, u, x) - lit).max() <= 1e-13 * np.abs(O.rhs(pb, x)).max()
+
+
+def test_burgers_bound_encloses_power_iteration():
+    for n in (16, 32):
+        pb = _burgers(n)
+        u = W.ic_burgers_2d(n)
+        M = refs.dense_matrix(lambda v: O.jac_apply(pb, u, v.reshape(n, n)), n * n)
+        lam = np.abs(np.linalg.eigvals(M)).max()
+        assert lam <= O.spectrum_bound(pb, u) * (1 + 1e-12)
+        assert O.power_iteration(pb, u, 200) <= O.spectrum_bound(pb, u)
