@@ -91,8 +91,9 @@ lx_status lx_slab_range(int64_t n0, int rank, int nranks, int64_t *i_begin, int6
 /*          lap: second-order centred; D_d: third-order upwind, +x-biased   */
 /*          (stencil (-u[i+2] + 6u[i+1] - 3u[i] - 2u[i-1])/(6 dx))   */
 /*   g(u) = react * (u - u^3)   (Allen-Cahn; react = 0 for Problems I/II)   */
+/*        + (flux/2) sum_d D_d(u^2)   (viscous Burgers, Problem III)          */
 /*   + S   (optional source, Problem II)                                     */
-/*   J(u) v = A v + react * (1 - 3u^2) v   (exact Jacobian)                  */
+/*   J(u) v = A v + react * (1 - 3u^2) v + flux sum_d D_d(u v)  (exact J)     */
 /* Periodic on every dimension.                                              */
 /* ------------------------------------------------------------------------ */
 typedef struct {
@@ -102,6 +103,8 @@ typedef struct {
     double diff;      /* diffusion coefficient                                */
     double nu;        /* advection velocity                           */
     double react;     /* reaction weight (0 or 1)                             */
+    double flux;      /* Burgers flux weight beta (Problem III): f += (beta/2) sum_d D_d(u^2),
+                         J(u) v += beta sum_d D_d(u v); 2D single-GPU contexts only               */
     const double *source; /* optional time-independent source S added to f (Problem II,
                              P:583-586: f(u) = A u + S); caller's local slab, device or host
                              pointer; NULL -> no source.  S does not enter J(u) and cancels in

@@ -53,12 +53,13 @@ class LxError(RuntimeError):
 class LxProblem(ctypes.Structure):
     _fields_ = [("ndim", ctypes.c_int), ("n", ctypes.c_int64 * 3), ("dx", ctypes.c_double * 3),
                 ("diff", ctypes.c_double), ("nu", ctypes.c_double), ("react", ctypes.c_double),
-                ("source", ctypes.c_void_p)]
+                ("flux", ctypes.c_double), ("source", ctypes.c_void_p)]
 
 
 @dataclass(frozen=True, eq=False)
 class Problem:
-    """du/dt = diff*lap(u) + nu*sum_d D_d u + react*(u - u^3) [+ source] on a periodic GLOBAL grid.
+    """du/dt = diff*lap(u) + nu*sum_d D_d u + (flux/2) sum_d D_d(u^2) + react*(u - u^3) [+ source]
+    on a periodic GLOBAL grid (flux: viscous Burgers, Problem III).
     source: optional time-independent S (Problem II), the caller's local slab (tensor or ndarray)."""
     shape: tuple
     dx: tuple
@@ -66,13 +67,14 @@ class Problem:
     nu: float = 0.0
     react: float = 0.0
     source: object = None
+    flux: float = 0.0
 
     def c_struct(self) -> LxProblem:
         nd = len(self.shape)
         n = list(self.shape) + [1] * (3 - nd)
         dx = list(self.dx) + [1.0] * (3 - nd)
         return LxProblem(nd, (ctypes.c_int64 * 3)(*n), (ctypes.c_double * 3)(*dx), float(self.diff),
-                         float(self.nu), float(self.react), _ptr(self.source))
+                         float(self.nu), float(self.react), float(self.flux), _ptr(self.source))
 
     @property
     def npoints(self) -> int:

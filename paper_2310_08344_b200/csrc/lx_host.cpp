@@ -119,6 +119,19 @@ static Stencil make_stencil(const lx_problem* pb) {
     st.react = pb->react;
     st.qa = pb->react;          // J_ii = react*(1 - 3u^2)
     st.qb = -3.0 * pb->react;
+    // flux form (Burgers): diffusion and upwind kept apart, velocity field nu + beta*u
+    st.flux = pb->flux;
+    st.nu = pb->nu;
+    for (int d = 0; d < pb->ndim; d++) {
+        const double h = pb->dx[d], ih2 = 1.0 / (h * h);
+        st.dm1[d] = pb->diff * ih2;
+        st.dp1[d] = pb->diff * ih2;
+        st.dd0 += -2.0 * pb->diff * ih2;
+        st.am1[d] = -2.0 / (6.0 * h);
+        st.a0[d] = -3.0 / (6.0 * h);
+        st.ap1[d] = 6.0 / (6.0 * h);
+        st.ap2[d] = -1.0 / (6.0 * h);
+    }
     return st;
 }
 
@@ -129,6 +142,8 @@ static lx_status check_problem(const lx_ctx* ctx, const lx_problem* pb) {
         if (pb->n[d] != ctx->n[d]) return fail(LX_ERR_DIM, "problem n[%d] differs from the context grid", d);
     for (int d = 0; d < pb->ndim; d++)
         if (!(pb->dx[d] > 0.0)) return fail(LX_ERR_ARG, "dx[%d] must be > 0", d);
+    if (pb->flux != 0.0 && (pb->ndim != 2 || ctx->comm))
+        return fail(LX_ERR_UNSUPPORTED, "flux (Burgers) problems: 2D single-GPU contexts only");
     return LX_OK;
 }
 
@@ -251,6 +266,7 @@ static LejaParams base_params(lx_ctx* ctx, const lx_problem* pb) {
     }
     P.N_glob = ctx->N_glob;
     P.st = make_stencil(pb);
+    if (pb->flux != 0.0) P.ndim = 4;   // flux-form (Burgers) tile variant of the 2D kernels
     P.ctrl = ctx->ctrl;
     P.partials = ctx->partials;
     P.timeout_spins = 1 << 24;
@@ -265,7 +281,7 @@ static LejaParams base_params(lx_ctx* ctx, const lx_problem* pb) {
 static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u, const double* v, double* const* outs,
                              const double* coeffs, int K, double dt, double c, double gamma, int l, double rtol,
                              double atol, int rec, const double* table = nullptr) {
-    const bool tma = ctx->ndim == 2 && ctx->variant == 1 && !ctx->comm && !ctx->cg_active;
+    const bool tma = ctx->ndim == 2 && ctx->variant == 1 && !ctx->comm && !ctx->cg_active && pb->flux == 0.0;
     const double* coef = table;
     if (!coef && (tma || (ctx->coef_table && !ctx->cg_active))) {   // prebuilt table (TMA / LX_COEF=table)
         const TableSpec spec{l, K, coeffs};
@@ -312,7 +328,7 @@ static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u,
             return LX_OK;
         }
     }
-    P.grid = leja_grid_size(ctx->device, K, diag, ctx->ndim, P.nunits);
+    P.grid = leja_grid_size(ctx->device, K, diag, P.ndim, P.nunits);
     CUDA_TRY(launch_leja_persistent(P, ctx->stream, diag));
     ctx->launches++;
     return LX_OK;
@@ -333,7 +349,7 @@ static lx_status validate_leja(const lx_problem* pb, const double* u, const doub
         for (int j = 0; j < k; j++)
             if (outs[j] == outs[k]) return fail(LX_ERR_ALIAS, "outs must be distinct");
     }
-    if (pb->react != 0.0 && !u) return fail(LX_ERR_ARG, "u_lin required when react != 0");
+    if ((pb->react != 0.0 || pb->flux != 0.0) && !u) return fail(LX_ERR_ARG, "u_lin required when react/flux != 0");
     return LX_OK;
 }
 
@@ -624,7 +640,7 @@ lx_status lx_real_leja_phi_vertical(lx_ctx* ctx, const lx_problem* pb, const dou
     if (!ctx) return fail(LX_ERR_ARG, "ctx is NULL");
     LX_TRY(check_problem(ctx, pb));
     LX_TRY(validate_leja(pb, u_lin, v, outs, coeffs, K, dt, gamma, l));
-    if (pb->react == 0.0) u_lin = nullptr;
+    if (pb->react == 0.0 && pb->flux == 0.0) u_lin = nullptr;
     Staging sg(ctx);
     const double *vd, *ud;
     double* od[kMaxK];
@@ -654,13 +670,9 @@ lx_status lx_real_leja_phi(lx_ctx* ctx, const lx_problem* pb, const double* u_li
 lx_status lx_spectrum_bound(lx_ctx* ctx, const lx_problem* pb, const double* u, double* lambda_abs_out) {
     if (!ctx || !lambda_abs_out) return fail(LX_ERR_ARG, "NULL argument");
     LX_TRY(check_problem(ctx, pb));
-    double b = 0.0;
-    for (int d = 0; d < pb->ndim; d++) {
-        const double h = pb->dx[d];
-        b += 4.0 * pb->diff / (h * h) + 4.0 * std::fabs(pb->nu) / (3.0 * h);
-    }
-    if (pb->react != 0.0) {
-        if (!u) return fail(LX_ERR_ARG, "u required when react != 0");
+    double m2 = 0.0;   // max u^2 (Gershgorin shift / Burgers speed)
+    if (pb->react != 0.0 || pb->flux != 0.0) {
+        if (!u) return fail(LX_ERR_ARG, "u required when react/flux != 0");
         Staging sg(ctx);
         const double* ud;
         LX_TRY(sg.in(u, &ud));
@@ -679,8 +691,17 @@ lx_status lx_spectrum_bound(lx_ctx* ctx, const lx_problem* pb, const double* u, 
         CUDA_TRY(cudaMemcpyAsync(ctx->umax_host, &ctx->ctrl->umax, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                  ctx->stream));
         CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-        double m2;
         std::memcpy(&m2, ctx->umax_host, sizeof m2);
+    }
+    // closed form (Fourier symbol at theta = pi), frozen-coefficient speed for Burgers (R9, R23)
+    double vmax = std::fabs(pb->nu);
+    if (pb->flux != 0.0) vmax = std::fabs(pb->nu) + std::fabs(pb->flux) * std::sqrt(m2);
+    double b = 0.0;
+    for (int d = 0; d < pb->ndim; d++) {
+        const double h = pb->dx[d];
+        b += 4.0 * pb->diff / (h * h) + 4.0 * vmax / (3.0 * h);
+    }
+    if (pb->react != 0.0) {   // Gershgorin shift of the reaction (R16)
         const double sft = 3.0 * m2 - 1.0;
         if (sft > 0.0) b += pb->react * sft;
     }
@@ -692,10 +713,10 @@ lx_status lx_spectrum_estimate(lx_ctx* ctx, const lx_problem* pb, const double* 
     if (!ctx || !lambda_abs_out) return fail(LX_ERR_ARG, "NULL argument");
     LX_TRY(check_problem(ctx, pb));
     if (iters < 1 || iters > 100000) return fail(LX_ERR_ARG, "iters must be in [1, 100000]");
-    if (pb->react != 0.0 && !u) return fail(LX_ERR_ARG, "u required when react != 0");
+    if ((pb->react != 0.0 || pb->flux != 0.0) && !u) return fail(LX_ERR_ARG, "u required when react/flux != 0");
     Staging sg(ctx);
     const double* ud = nullptr;
-    if (pb->react != 0.0) LX_TRY(sg.in(u, &ud));
+    if (pb->react != 0.0 || pb->flux != 0.0) LX_TRY(sg.in(u, &ud));
     LX_TRY(reset_record(ctx, 0));
     CUDA_TRY(launch_fill_start(ctx->Y[0], ctx->N_loc, ctx->i_begin == 0, ctx->stream));
     ctx->launches++;
@@ -710,7 +731,7 @@ lx_status lx_spectrum_estimate(lx_ctx* ctx, const lx_problem* pb, const double* 
     if (ctx->comm) {
         LX_TRY(comm_power(ctx->comm, P, diag, ctx->stream, &ctx->launches));
     } else {
-        P.grid = leja_grid_size(ctx->device, 1, diag, ctx->ndim, P.nunits);
+        P.grid = leja_grid_size(ctx->device, 1, diag, P.ndim, P.nunits);
         CUDA_TRY(launch_power_persistent(P, ctx->stream, diag));
         ctx->launches++;
     }
@@ -751,6 +772,7 @@ static lx_status run_stage(lx_ctx* ctx, int op, const StageArgs& A0) {
 static lx_status rhs_device(lx_ctx* ctx, const lx_problem* pb, const double* u, double scale, double* f) {
     LejaParams P = base_params(ctx, pb);
     P.source = pb->source;   // device pointer (staged by the caller)
+    P.u = u;
     P.v = RowSrc{u, nullptr, ctx->row, ctx->n_loc, 0};
     P.ydst[0] = f;
     if (ctx->comm) return comm_rhs(ctx->comm, P, scale, ctx->stream, &ctx->launches) ? fail(LX_ERR_NCCL, "rhs halo: %s", comm_error()) : LX_OK;
@@ -779,10 +801,39 @@ lx_status lx_rhs(lx_ctx* ctx, const lx_problem* pb0, const double* u, double sca
     return LX_OK;
 }
 
+// Remainder difference y0 = a2 * (dt F(s) - dt F(u)), s = x0 + a0 x1 + a1 x2.  Pointwise problems use
+// one fused kernel; flux (Burgers) problems materialise s into `tmp` and apply the stencil remainder.
+static lx_status stage_remainder(lx_ctx* ctx, const lx_problem* pb, int rec, const double* u, const double* x0,
+                           const double* x1, double a0, const double* x2, double a1, double a2, double dt,
+                           double* y0, double* tmp) {
+    StageArgs A = stage_args(ctx, pb, rec);
+    A.dt = dt;
+    A.u = u;
+    if (pb->flux == 0.0) {
+        A.x0 = x0; A.x1 = x1; A.x2 = x2; A.a0 = a0; A.a1 = a1; A.a2 = a2; A.y0 = y0;
+        return run_stage(ctx, ST_STAGE_REMAINDER, A);
+    }
+    const double* sfield = x0;
+    if (x1 || x2) {
+        A.x0 = x0; A.x1 = x1; A.x2 = x2; A.a0 = a0; A.a1 = x2 ? a1 : 0.0; A.y0 = tmp;
+        LX_TRY(run_stage(ctx, ST_LIN3, A));
+        sfield = tmp;
+    }
+    LejaParams P = base_params(ctx, pb);
+    P.v = RowSrc{sfield, nullptr, ctx->row, ctx->n_loc, 0};
+    P.u = u;
+    P.grid = (P.nunits + kWarps - 1) / kWarps;
+    if (P.grid > ctx->nsm * 2) P.grid = ctx->nsm * 2;
+    CUDA_TRY(launch_rem_flux(P, dt, a2, y0, ctx->stream));
+    ctx->launches++;
+    return LX_OK;
+}
+
 static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb, const double* u, double* lo,
                              double* hi, double dt, double c, double gamma, double rtol, double atol, int rec) {
     const bool diag = pb->react != 0.0;
-    const double* ul = diag ? u : nullptr;
+    const bool flux = pb->flux != 0.0;
+    const double* ul = (diag || flux) ? u : nullptr;
     double* S0 = scratch(ctx, 0);
     if (!S0) return fail(LX_ERR_CUDA, "scratch allocation failed");
     const double one = 1.0;
@@ -829,8 +880,14 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
         // P:414-418, alg:exprb32: u_flux (in hi) -> a (lo), R_a (S0) -> u_nl_3 (hi) -> u_3 = a + 2 u_nl_3
         double* o[1] = {hi};
         LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 1, rtol, atol, rec, tab[0]));
-        A.x0 = u; A.x1 = hi; A.y1 = lo; A.y0 = S0;
-        LX_TRY(run_stage(ctx, ST_EXPRB32_A, A));
+        if (!flux) {
+            A.x0 = u; A.x1 = hi; A.y1 = lo; A.y0 = S0;
+            LX_TRY(run_stage(ctx, ST_EXPRB32_A, A));
+        } else {   // a = u + u_flux -> lo ; R_a = dt F(a) - dt F(u) (stencil remainder)
+            A.x0 = u; A.x1 = hi; A.a0 = 1.0; A.a1 = 1.0; A.y0 = lo;
+            LX_TRY(run_stage(ctx, ST_AXPBY, A));
+            LX_TRY(stage_remainder(ctx, pb, rec, u, lo, nullptr, 0.0, nullptr, 0.0, 1.0, dt, S0, nullptr));
+        }
         LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 3, rtol, atol, rec, tab[1]));
         A = stage_args(ctx, pb, rec);
         A.x0 = lo; A.x1 = hi; A.y0 = hi;
@@ -843,8 +900,7 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
         if (!S1 || !S2) return fail(LX_ERR_CUDA, "scratch allocation failed");
         double* pv[2] = {S1, S2};
         LX_TRY(leja_device(ctx, pb, ul, S0, pv, c42, 2, dt, c, gamma, 1, rtol, atol, rec, tab[0]));
-        A.x0 = u; A.x1 = S1; A.x2 = nullptr; A.a0 = 0.75; A.a1 = 0.0; A.a2 = 32.0 / 9.0; A.y0 = S0;
-        LX_TRY(run_stage(ctx, ST_STAGE_REMAINDER, A));
+        LX_TRY(stage_remainder(ctx, pb, rec, u, u, S1, 0.75, nullptr, 0.0, 32.0 / 9.0, dt, S0, hi));
         double* o3[1] = {S1};
         LX_TRY(leja_device(ctx, pb, ul, S0, o3, &one, 1, dt, c, gamma, 3, rtol, atol, rec, tab[1]));
         A = stage_args(ctx, pb, rec);
@@ -864,20 +920,17 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
     LX_TRY(leja_device(ctx, pb, ul, S0, pv, epirk ? cf3 : cf2, epirk ? 3 : 2, dt, c, gamma, 1, rtol, atol, rec, tab[0]));
     double* p_one = epirk ? S3 : S2;
     // D_a = dt F(u + 1/2 p_half) - dt F(u)  -> S0
-    A.x0 = u; A.x1 = S1; A.x2 = nullptr; A.a0 = 0.5; A.a1 = 0.0; A.a2 = 1.0; A.y0 = S0;
-    LX_TRY(run_stage(ctx, ST_STAGE_REMAINDER, A));
+    LX_TRY(stage_remainder(ctx, pb, rec, u, u, S1, 0.5, nullptr, 0.0, 1.0, dt, S0, hi));
     double* Db;
     if (epirk) {
         // D_b = dt F(u + 2/3 p_23) - dt F(u) -> S1
-        A.x0 = u; A.x1 = S2; A.x2 = nullptr; A.a0 = 2.0 / 3.0; A.a1 = 0.0; A.a2 = 1.0; A.y0 = S1;
-        LX_TRY(run_stage(ctx, ST_STAGE_REMAINDER, A));
+        LX_TRY(stage_remainder(ctx, pb, rec, u, u, S2, 2.0 / 3.0, nullptr, 0.0, 1.0, dt, S1, hi));
         Db = S1;
     } else {
         // phi_1(hJ) D_a -> S1 ; b = u + p_one + S1 ; D_b -> lo
         double* o[1] = {S1};
         LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 1, rtol, atol, rec, tab[1]));
-        A.x0 = u; A.x1 = p_one; A.x2 = S1; A.a0 = 1.0; A.a1 = 1.0; A.a2 = 1.0; A.y0 = lo;
-        LX_TRY(run_stage(ctx, ST_STAGE_REMAINDER, A));
+        LX_TRY(stage_remainder(ctx, pb, rec, u, u, p_one, 1.0, S1, 1.0, 1.0, dt, lo, hi));
         Db = lo;
     }
     // w3 = a3 D_a + b3 D_b, w4 = a4 D_a + b4 D_b
@@ -955,11 +1008,14 @@ lx_status lx_integrate(lx_ctx* ctx, lx_method method, const lx_problem* pb0, dou
     double* st[2] = {scratch(ctx, 4), scratch(ctx, 5)};
     double* lo = scratch(ctx, 6);   // lower-order solution (discarded)
     if (!st[0] || !st[1] || !lo) return fail(LX_ERR_CUDA, "scratch allocation failed");
-    double bound_const = 0.0;
-    for (int d = 0; d < pb->ndim; d++) {
-        const double h = pb->dx[d];
-        bound_const += 4.0 * pb->diff / (h * h) + 4.0 * std::fabs(pb->nu) / (3.0 * h);
-    }
+    ShiftArgs sa;
+    std::memset(&sa, 0, sizeof sa);
+    sa.ndim = pb->ndim;
+    for (int d = 0; d < pb->ndim; d++) sa.h[d] = pb->dx[d];
+    sa.diff = pb->diff;
+    sa.nu = pb->nu;
+    sa.flux = pb->flux;
+    sa.react = pb->react;
     const bool sync = iters_out || err_out || sg.any_host;
     const int rec = sync ? 0 : 1;
     if (sync) LX_TRY(reset_record(ctx, 0));
@@ -970,7 +1026,7 @@ lx_status lx_integrate(lx_ctx* ctx, lx_method method, const lx_problem* pb0, dou
     lx_status status = LX_OK;
     for (int n = 0; n < nsteps && status == LX_OK; n++) {
         // spectrum of J(u_n) on the device
-        if (pb->react != 0.0) {
+        if (pb->react != 0.0 || pb->flux != 0.0) {
             if (cudaMemsetAsync(&ctx->ctrl->umax, 0, sizeof(unsigned long long), ctx->stream) != cudaSuccess) {
                 status = fail(LX_ERR_CUDA, "memset");
                 break;
@@ -985,7 +1041,7 @@ lx_status lx_integrate(lx_ctx* ctx, lx_method method, const lx_problem* pb0, dou
                 break;
             }
         }
-        if (launch_shift_scale(&ctx->ctrl->umax, bound_const, pb->react, ctx->cg_dev, ctx->stream) != cudaSuccess) {
+        if (launch_shift_scale(&ctx->ctrl->umax, sa, ctx->cg_dev, ctx->stream) != cudaSuccess) {
             status = fail(LX_ERR_CUDA, "shift_scale");
             break;
         }

@@ -63,6 +63,10 @@ struct Stencil {
     double m1[3], p1[3], p2[3];
     double qa, qb;        // diagonal of J: qa + qb * u^2   (react*(1 - 3u^2))
     double react;         // g(u) = react*(u - u^3)
+    // flux form (Burgers, Problem III): diffusion and upwind coefficients kept separate
+    double flux, nu;      // beta, nu:  J y = diff lap y + sum_d D_d((nu + beta u) y)
+    double dd0, dm1[3], dp1[3];             // diff*lap: centre, -1, +1
+    double a0[3], am1[3], ap1[3], ap2[3];   // D_d: centre, -1, +1, +2
 };
 
 struct LejaParams {
@@ -147,9 +151,12 @@ enum StageOp {
     ST_FINAL_EXPRB32,     // y0 = x0 + 2 x1 ; err = ||2 x1||
     ST_MAXSQ,             // ctrl->umax = max x0^2
     ST_SUM3,              // y0 = x0 + x1 + x2
+    ST_LIN3,              // y0 = x0 + a0*x1 + a1*x2
 };
 cudaError_t launch_stage(int op, const StageArgs& A, cudaStream_t s);
 cudaError_t launch_rhs(const LejaParams& P, double scale, cudaStream_t s);
+// Burgers remainder difference (stencil): y = a2 * (dt F(x) - dt F(u)), x = P.v (with halo), u = P.u
+cudaError_t launch_rem_flux(const LejaParams& P, double dt, double a2, double* out, cudaStream_t s);
 cudaError_t launch_fill_start(double* v, long long n, bool add_e0, cudaStream_t s);
 // step mode (one launch per iteration; decision for m-1 in the prologue from P.gathered)
 cudaError_t launch_leja_step(const LejaParams& P, int m, cudaStream_t s, bool diag);
@@ -157,9 +164,14 @@ cudaError_t launch_power_step(const LejaParams& P, int m, cudaStream_t s, bool d
 int step_grid_size(int device, int nunits);
 cudaError_t launch_finalize_err(const double* gathered, int nranks, double N, Record* rec, cudaStream_t s);
 cudaError_t launch_max_u64(const unsigned long long* vals, int n, unsigned long long* out, cudaStream_t s);
-// (c, gamma) on the device from the bound const_part + react*max(0, 3*max u^2 - 1)
-cudaError_t launch_shift_scale(const unsigned long long* umax, double const_part, double react, double* cg_out,
-                               cudaStream_t s);
+// (c, gamma) on the device from the spectrum bound of J(u): sum_d (4 diff/h^2 + 4 vmax/(3h)),
+// vmax = |nu| + |beta| max|u|, + react*max(0, 3 max u^2 - 1)  (readings R9, R16, R23)
+struct ShiftArgs {
+    int ndim;
+    double h[3];
+    double diff, nu, flux, react;
+};
+cudaError_t launch_shift_scale(const unsigned long long* umax, const ShiftArgs& a, double* cg_out, cudaStream_t s);
 int stage_grid_size(int device, int op);
 // device coefficient table: [M][1+K] = {beta_m, d_m^(k)}; a[K] device array of vertical coefficients
 struct CoefJob {

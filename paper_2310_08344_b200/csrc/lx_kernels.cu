@@ -177,7 +177,14 @@ __device__ __forceinline__ void block_reduce(double (&v)[N], double (*s_red)[kSl
     __syncthreads();
 }
 
-enum TileMode { M_LEJA = 0, M_POWER = 1, M_RHS = 2 };
+__device__ __forceinline__ double nl_rem(double react, double x, double u) {
+    // F(x) = g(x) - g'(u) x,  g(x) = react (x - x^3)    (P:416, reading R18)
+    const double g = react * (x - x * x * x);
+    const double gp = react * (1.0 - 3.0 * u * u);
+    return g - gp * x;
+}
+
+enum TileMode { M_LEJA = 0, M_POWER = 1, M_RHS = 2, M_REM = 3 };
 
 // One warp work unit of the 2D stencil (64 columns x kRT rows).
 template <int K, bool DIAG, bool FIRST, int MODE, bool RO>
@@ -472,11 +479,205 @@ __device__ __forceinline__ void tile3d(const LejaParams& P, const RowSrc& src, d
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Flux-form 2D tile (Problem III, viscous Burgers; exact Jacobian R13):
+//   M_LEJA/M_POWER: A y = diff lap(y) + sum_d D_d((nu + beta u) y)      (J(u) y)
+//   M_RHS:          f(u) = diff lap(u) + sum_d D_d((nu + beta/2 u) u) [+ react g(u) + S]
+//   M_REM:          a2 * (dt F(x) - dt F(u)),  F(x) = sum_d D_d(beta/2 x^2 - beta u x) + g-part
+// Two register windows (the field y/x and u) with the same row / shuffle / halo
+// pattern as tile2d.  Single GPU (u is read with periodic wrap).  For M_REM the
+// `beta` argument carries dt and `scale` carries a2.
+// ---------------------------------------------------------------------------
+template <int K, bool FIRST, int MODE, bool RO>
+__device__ __forceinline__ void tile2d_flux(const LejaParams& P, const RowSrc& src, double* __restrict__ dst,
+                                            int unit, int lane, double beta, const double* d0, const double* dm,
+                                            int active, double scale, double& sy, double* sp) {
+    constexpr bool TWO = (MODE != M_RHS);   // RHS: the coefficient field is the input itself
+    const int b = unit % P.nb;
+    const int rb = unit / P.nb;
+    const int n1 = P.n1;
+    const int j0 = b * 64 + 2 * lane;
+    const bool valid = j0 < n1;
+    const int last = min(31, ((n1 - b * 64) >> 1) - 1);
+    const int i0 = rb * kRT;
+    const int nout = min(kRT, P.n_loc - i0);
+    const Stencil& S = P.st;
+    const RowSrc us{P.u, nullptr, (long long)n1, P.n_loc, 0};
+    auto LD2 = [&](const double* q) { return RO ? ldg2(q) : ld2(q); };
+    auto LD1 = [&](const double* q) { return RO ? __ldg(q) : *q; };
+
+    double2 w[kRT + 3], uw[kRT + 3];
+#pragma unroll
+    for (int t = 0; t < kRT + 3; t++) {
+        w[t] = uw[t] = make_double2(0.0, 0.0);
+        if (valid && t < nout + 3) {
+            w[t] = LD2(rowp(src, i0 - 1 + t) + j0);
+            if (TWO) uw[t] = ldg2(rowp(us, i0 - 1 + t) + j0);
+        }
+    }
+    double hl[kRT], uhl[kRT];
+    double2 hr[kRT], uhr[kRT];
+#pragma unroll
+    for (int t = 0; t < kRT; t++) {
+        hl[t] = uhl[t] = 0.0;
+        hr[t] = uhr[t] = make_double2(0.0, 0.0);
+        if (t < nout) {
+            const double* rp = rowp(src, i0 + t);
+            const double* rq = rowp(us, i0 + t);
+            const int jl = (j0 == 0) ? n1 - 1 : j0 - 1;
+            int jr = j0 + 2;
+            if (jr >= n1) jr -= n1;
+            if (lane == 0) {
+                hl[t] = LD1(rp + jl);
+                if (TWO) uhl[t] = __ldg(rq + jl);
+            }
+            if (lane == last) {
+                hr[t] = LD2(rp + jr);
+                if (TWO) uhr[t] = ldg2(rq + jr);
+            }
+        }
+    }
+    constexpr int KK = K > 0 ? K : 1;
+    double2 pv[kRT][KK];
+#pragma unroll
+    for (int t = 0; t < kRT; t++) {
+        const long long off = (long long)(i0 + t) * n1 + j0;
+        if (MODE == M_LEJA && !FIRST) {
+#pragma unroll
+            for (int k = 0; k < KK; k++) {
+                pv[t][k] = make_double2(0.0, 0.0);
+                if (valid && t < nout && ((active >> k) & 1)) pv[t][k] = ld2(P.p[k] + off);
+            }
+        }
+    }
+    const double nu = S.nu, bt = S.flux;
+#pragma unroll
+    for (int t = 0; t < kRT; t++) {
+        if (t < nout) {
+            const double2 yc = w[t + 1], up = w[t], dn1 = w[t + 2], dn2 = w[t + 3];
+            const double2 uc = TWO ? uw[t + 1] : yc, uu = TWO ? uw[t] : up;
+            const double2 ud1 = TWO ? uw[t + 2] : dn1, ud2 = TWO ? uw[t + 3] : dn2;
+            double yl = __shfl_up_sync(FULL_MASK, yc.y, 1);
+            double yr1 = __shfl_down_sync(FULL_MASK, yc.x, 1);
+            double yr2 = __shfl_down_sync(FULL_MASK, yc.y, 1);
+            double ul = __shfl_up_sync(FULL_MASK, uc.y, 1);
+            double ur1 = __shfl_down_sync(FULL_MASK, uc.x, 1);
+            double ur2 = __shfl_down_sync(FULL_MASK, uc.y, 1);
+            if (lane == 0) {
+                yl = hl[t];
+                ul = TWO ? uhl[t] : hl[t];
+            }
+            if (lane == last) {
+                yr1 = hr[t].x;
+                yr2 = hr[t].y;
+                ur1 = TWO ? uhr[t].x : hr[t].x;
+                ur2 = TWO ? uhr[t].y : hr[t].y;
+            }
+            // pointwise flux field w(y, u) at the stencil points
+            auto wf = [&](double yv, double uv) -> double {
+                if (MODE == M_RHS) return (nu + 0.5 * bt * uv) * uv;
+                if (MODE == M_REM) return 0.5 * bt * yv * yv - bt * uv * yv;
+                return (nu + bt * uv) * yv;
+            };
+            auto wu = [&](double uv) -> double { return -0.5 * bt * uv * uv; };   // M_REM: F(u) field
+            // value at point x=(i,j0) and y=(i,j0+1)
+            double res[2];
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const double y0 = h ? yc.y : yc.x, u0 = h ? uc.y : uc.x;
+                const double ymr = h ? up.y : up.x, ypr = h ? dn1.y : dn1.x, yp2r = h ? dn2.y : dn2.x;
+                const double umr = h ? uu.y : uu.x, upr = h ? ud1.y : ud1.x, up2r = h ? ud2.y : ud2.x;
+                const double ymc = h ? yc.x : yl, ypc = h ? yr1 : yc.y, yp2c = h ? yr2 : yr1;
+                const double umc = h ? uc.x : ul, upc = h ? ur1 : uc.y, up2c = h ? ur2 : ur1;
+                double adv = (S.a0[0] + S.a0[1]) * wf(y0, u0);
+                adv = fma(S.am1[0], wf(ymr, umr), adv);
+                adv = fma(S.ap1[0], wf(ypr, upr), adv);
+                adv = fma(S.ap2[0], wf(yp2r, up2r), adv);
+                adv = fma(S.am1[1], wf(ymc, umc), adv);
+                adv = fma(S.ap1[1], wf(ypc, upc), adv);
+                adv = fma(S.ap2[1], wf(yp2c, up2c), adv);
+                if (MODE == M_REM) {
+                    double advu = (S.a0[0] + S.a0[1]) * wu(u0);
+                    advu = fma(S.am1[0], wu(umr), advu);
+                    advu = fma(S.ap1[0], wu(upr), advu);
+                    advu = fma(S.ap2[0], wu(up2r), advu);
+                    advu = fma(S.am1[1], wu(umc), advu);
+                    advu = fma(S.ap1[1], wu(upc), advu);
+                    advu = fma(S.ap2[1], wu(up2c), advu);
+                    const double Fx = adv + nl_rem(S.react, y0, u0);
+                    const double Fu = advu + nl_rem(S.react, u0, u0);
+                    res[h] = scale * (beta * Fx + (-beta) * Fu);   // a2 * (dt F(x) - dt F(u))
+                } else {
+                    double lap = S.dd0 * y0;
+                    lap = fma(S.dm1[0], ymr, lap);
+                    lap = fma(S.dp1[0], ypr, lap);
+                    lap = fma(S.dm1[1], ymc, lap);
+                    lap = fma(S.dp1[1], ypc, lap);
+                    double a = lap + adv;
+                    if (MODE == M_RHS) {
+                        a = fma(S.react, y0 - y0 * y0 * y0, a);
+                    } else if (S.react != 0.0) {
+                        a = fma(fma(S.qb, u0 * u0, S.qa), y0, a);
+                    }
+                    res[h] = a;
+                }
+            }
+            double2 yn;
+            if (MODE == M_POWER) {
+                yn.x = scale * res[0];
+                yn.y = scale * res[1];
+            } else if (MODE == M_RHS) {
+                double fx = res[0], fy = res[1];
+                if (P.source && valid) {
+                    const double2 sv = ldg2(P.source + (long long)(i0 + t) * n1 + j0);
+                    fx += sv.x;
+                    fy += sv.y;
+                }
+                yn.x = scale * fx;
+                yn.y = scale * fy;
+            } else if (MODE == M_REM) {
+                yn.x = res[0];
+                yn.y = res[1];
+            } else {
+                yn.x = fma(scale, res[0], beta * yc.x);
+                yn.y = fma(scale, res[1], beta * yc.y);
+            }
+            if (valid) {
+                const long long off = (long long)(i0 + t) * n1 + j0;
+                st2(dst + off, yn);
+                sy = fma(yn.x, yn.x, sy);
+                sy = fma(yn.y, yn.y, sy);
+                if (MODE == M_LEJA) {
+#pragma unroll
+                    for (int k = 0; k < KK; k++) {
+                        if ((active >> k) & 1) {
+                            double2 pn;
+                            if (FIRST) {
+                                pn.x = fma(dm[k], yn.x, d0[k] * yc.x);
+                                pn.y = fma(dm[k], yn.y, d0[k] * yc.y);
+                            } else {
+                                pn.x = fma(dm[k], yn.x, pv[t][k].x);
+                                pn.y = fma(dm[k], yn.y, pv[t][k].y);
+                            }
+                            st2(P.p[k] + off, pn);
+                            sp[k] = fma(pn.x, pn.x, sp[k]);
+                            sp[k] = fma(pn.y, pn.y, sp[k]);
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
 template <int NDIM, int K, bool DIAG, bool FIRST, int MODE, bool RO>
 __device__ __forceinline__ void tile(const LejaParams& P, const RowSrc& src, double* __restrict__ dst, int unit,
                                      int lane, double beta, const double* d0, const double* dm, int active,
                                      double scale, double& sy, double* sp) {
-    if (NDIM == 2)
+    if (NDIM == 4)   // flux form (Burgers), 2D
+        tile2d_flux<K, FIRST, MODE, RO>(P, src, dst, unit, lane, beta, d0, dm, active, scale, sy, sp);
+    else if (NDIM == 2)
         tile2d<K, DIAG, FIRST, MODE, RO>(P, src, dst, unit, lane, beta, d0, dm, active, scale, sy, sp);
     else
         tile3d<K, DIAG, FIRST, MODE, RO>(P, src, dst, unit, lane, beta, d0, dm, active, scale, sy, sp);
@@ -620,7 +821,7 @@ __device__ __forceinline__ void barrier_decide(const LejaParams& P, int m, unsig
 }
 
 template <int NDIM, int K, bool DIAG>
-__global__ void __launch_bounds__(kThreads, 2) k_leja2d(const __grid_constant__ LejaParams P) {
+__global__ void __launch_bounds__(kThreads, (NDIM == 4 ? 1 : 2)) k_leja2d(const __grid_constant__ LejaParams P) {
     __shared__ double s_red[kWarps][kSlot];
     __shared__ int s_flags[4];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -690,7 +891,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d(const __grid_constant__ 
 }
 
 template <int NDIM, bool DIAG>
-__global__ void __launch_bounds__(kThreads, 2) k_power2d(const __grid_constant__ LejaParams P) {
+__global__ void __launch_bounds__(kThreads, (NDIM == 4 ? 1 : 2)) k_power2d(const __grid_constant__ LejaParams P) {
     __shared__ double s_red[kWarps][kSlot];
     __shared__ int s_flags[4];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1164,6 +1365,15 @@ static void* leja_kernel_ptr_nd(int K, bool diag) {
 }
 
 static void* leja_kernel_ptr(int ndim, int K, bool diag) {
+    if (ndim == 4) {   // flux form (Burgers, 2D); react handled at run time inside the tile
+        switch (K) {
+            case 1: return (void*)k_leja2d<4, 1, false>;
+            case 2: return (void*)k_leja2d<4, 2, false>;
+            case 3: return (void*)k_leja2d<4, 3, false>;
+            case 4: return (void*)k_leja2d<4, 4, false>;
+        }
+        return nullptr;
+    }
     return ndim == 3 ? leja_kernel_ptr_nd<3>(K, diag) : leja_kernel_ptr_nd<2>(K, diag);
 }
 
@@ -1188,8 +1398,9 @@ cudaError_t launch_leja_persistent(const LejaParams& P, cudaStream_t s, bool dia
 }
 
 cudaError_t launch_power_persistent(const LejaParams& P, cudaStream_t s, bool diag) {
-    void* kern = P.ndim == 3 ? (diag ? (void*)k_power2d<3, true> : (void*)k_power2d<3, false>)
-                             : (diag ? (void*)k_power2d<2, true> : (void*)k_power2d<2, false>);
+    void* kern = P.ndim == 4 ? (void*)k_power2d<4, false>
+                 : P.ndim == 3 ? (diag ? (void*)k_power2d<3, true> : (void*)k_power2d<3, false>)
+                               : (diag ? (void*)k_power2d<2, true> : (void*)k_power2d<2, false>);
     void* args[] = {(void*)&P};
     return cudaLaunchCooperativeKernel(kern, dim3(P.grid), dim3(kThreads), args, 0, s);
 }
@@ -1349,13 +1560,21 @@ cudaError_t launch_coef_tables(const double* xi, const double* R, int M, const C
 }
 
 
-__global__ void k_shift_scale(const unsigned long long* umax, double const_part, double react, double* cg) {
+__global__ void k_shift_scale(const unsigned long long* umax, ShiftArgs a, double* cg) {
+    // the bound of oracle/lxoracle.c oc_spectrum_bound, operation by operation (no contraction)
     if (threadIdx.x == 0 && blockIdx.x == 0) {
-        double b = const_part;
-        if (react != 0.0) {
-            const double m2 = __longlong_as_double((long long)*umax);
+        const double m2 = __longlong_as_double((long long)*umax);
+        double vmax = fabs(a.nu);
+        if (a.flux != 0.0) vmax = __dadd_rn(fabs(a.nu), __dmul_rn(fabs(a.flux), sqrt(m2)));
+        double b = 0.0;
+        for (int d = 0; d < a.ndim; d++) {
+            const double h = a.h[d];
+            b = __dadd_rn(b, __dadd_rn(__ddiv_rn(__dmul_rn(4.0, a.diff), __dmul_rn(h, h)),
+                                       __ddiv_rn(__dmul_rn(4.0, vmax), __dmul_rn(3.0, h))));
+        }
+        if (a.react != 0.0) {
             const double sft = __dsub_rn(__dmul_rn(3.0, m2), 1.0);
-            if (sft > 0.0) b = __dadd_rn(b, __dmul_rn(react, sft));
+            if (sft > 0.0) b = __dadd_rn(b, __dmul_rn(a.react, sft));
         }
         const double eig = __dmul_rn(-1.05, b);
         cg[0] = eig / 2.0;
@@ -1364,21 +1583,14 @@ __global__ void k_shift_scale(const unsigned long long* umax, double const_part,
     }
 }
 
-cudaError_t launch_shift_scale(const unsigned long long* umax, double const_part, double react, double* cg_out,
-                               cudaStream_t s) {
-    k_shift_scale<<<1, 32, 0, s>>>(umax, const_part, react, cg_out);
+cudaError_t launch_shift_scale(const unsigned long long* umax, const ShiftArgs& a, double* cg_out, cudaStream_t s) {
+    k_shift_scale<<<1, 32, 0, s>>>(umax, a, cg_out);
     return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
 // Stage kernels
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double nl_rem(double react, double x, double u) {
-    // F(x) = g(x) - g'(u) x,  g(x) = react (x - x^3)    (P:416, reading R18)
-    const double g = react * (x - x * x * x);
-    const double gp = react * (1.0 - 3.0 * u * u);
-    return g - gp * x;
-}
 
 // Deterministic last-block reduction of one value into rec->err = sqrt(S/N).
 __device__ __forceinline__ void stage_reduce_err(const StageArgs& A, double v, double (*s_red)[kSlot],
@@ -1411,8 +1623,8 @@ __global__ void __launch_bounds__(kThreads) k_stage_pointwise(const __grid_const
     // before any store (outputs may alias inputs element-wise, which blocks the compiler from
     // overlapping trips on its own), so every thread keeps UN x (inputs) 16-byte loads in flight.
     constexpr int UN = 4;
-    constexpr int NIN = (OP == ST_FINAL4) ? 4 : (OP == ST_STAGE_REMAINDER) ? 4 : (OP == ST_SUM3) ? 3
-                                                                                : (OP == ST_MAXSQ) ? 1 : 2;
+    constexpr int NIN = (OP == ST_FINAL4) ? 4 : (OP == ST_STAGE_REMAINDER) ? 4
+                        : (OP == ST_SUM3 || OP == ST_LIN3) ? 3 : (OP == ST_MAXSQ) ? 1 : 2;
     __shared__ double s_red[kWarps][kSlot];
     __shared__ int s_last;
     const long long npair = (long long)A.n_loc * A.n1 * A.n2 / 2;
@@ -1434,7 +1646,7 @@ __global__ void __launch_bounds__(kThreads) k_stage_pointwise(const __grid_const
 #pragma unroll
             for (int t = 0; t < NIN; t++) {
                 v[q][t] = make_double2(0.0, 0.0);
-                if (ok && !(OP == ST_STAGE_REMAINDER && t == 3 && !in[3])) v[q][t] = ld2(in[t] + o);
+                if (ok && in[t]) v[q][t] = ld2(in[t] + o);
             }
         }
 #pragma unroll
@@ -1481,6 +1693,9 @@ __global__ void __launch_bounds__(kThreads) k_stage_pointwise(const __grid_const
                 const double ex = 2.0 * qq.x, ey = 2.0 * qq.y;
                 acc = fma(ex, ex, acc);
                 acc = fma(ey, ey, acc);
+            } else if (OP == ST_LIN3) {
+                const double2 x = v[q][0], y = v[q][1], z = v[q][2];
+                st2(A.y0 + o, make_double2(x.x + A.a0 * y.x + A.a1 * z.x, x.y + A.a0 * y.y + A.a1 * z.y));
             } else if (OP == ST_SUM3) {
                 const double2 x = v[q][0], y = v[q][1], z = v[q][2];
                 st2(A.y0 + o, make_double2(x.x + y.x + z.x, x.y + y.y + z.y));
@@ -1532,11 +1747,25 @@ static void* stage_kernel_ptr(int op) {
         case ST_FINAL_EXPRB32: return (void*)k_stage_pointwise<ST_FINAL_EXPRB32>;
         case ST_MAXSQ: return (void*)k_stage_pointwise<ST_MAXSQ>;
         case ST_SUM3: return (void*)k_stage_pointwise<ST_SUM3>;
+        case ST_LIN3: return (void*)k_stage_pointwise<ST_LIN3>;
     }
     return nullptr;
 }
 
 // One full wave of resident CTAs (never more: a partial second wave doubles the time).
+__global__ void __launch_bounds__(kThreads, 2) k_rem2d_flux(const __grid_constant__ LejaParams P, double dt, double a2,
+                                                              double* out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double sy = 0.0, sp[1] = {0.0};
+    for (int unit = blockIdx.x * kWarps + warp; unit < P.nunits; unit += gridDim.x * kWarps)
+        tile2d_flux<0, false, M_REM, true>(P, P.v, out, unit, lane, dt, nullptr, nullptr, 0, a2, sy, sp);
+}
+
+cudaError_t launch_rem_flux(const LejaParams& P, double dt, double a2, double* out, cudaStream_t s) {
+    k_rem2d_flux<<<P.grid, kThreads, 0, s>>>(P, dt, a2, out);
+    return cudaGetLastError();
+}
+
 int stage_grid_size(int device, int op) {
     int nsm = 0, per = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
@@ -1548,7 +1777,8 @@ int stage_grid_size(int device, int op) {
 }
 
 cudaError_t launch_rhs(const LejaParams& P, double scale, cudaStream_t s) {
-    if (P.ndim == 3) k_rhs2d<3><<<P.grid, kThreads, 0, s>>>(P, scale);
+    if (P.ndim == 4) k_rhs2d<4><<<P.grid, kThreads, 0, s>>>(P, scale);
+    else if (P.ndim == 3) k_rhs2d<3><<<P.grid, kThreads, 0, s>>>(P, scale);
     else k_rhs2d<2><<<P.grid, kThreads, 0, s>>>(P, scale);
     return cudaGetLastError();
 }
@@ -1565,6 +1795,7 @@ cudaError_t launch_stage(int op, const StageArgs& A, cudaStream_t s) {
         case ST_FINAL_EXPRB32: k_stage_pointwise<ST_FINAL_EXPRB32><<<g, b, 0, s>>>(A); break;
         case ST_MAXSQ: k_stage_pointwise<ST_MAXSQ><<<g, b, 0, s>>>(A); break;
         case ST_SUM3: k_stage_pointwise<ST_SUM3><<<g, b, 0, s>>>(A); break;
+        case ST_LIN3: k_stage_pointwise<ST_LIN3><<<g, b, 0, s>>>(A); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

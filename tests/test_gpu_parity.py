@@ -416,3 +416,62 @@ def test_problem2_source(xi300, method):
                 tot += r.iters
                 u = r.u_high
             assert it2 == tot and _rel(ud, u) <= TOL
+
+
+# ---------------------------------------------------------------- Problem III: viscous Burgers
+def _burgers_pair(n, beta=10.0):
+    dx = (2 / n, 2 / n)
+    return lx.Problem((n, n), dx, 1.0, 0.0, 0.0, None, beta), O.Problem((n, n), dx, 1.0, 0.0, 0.0, None, beta)
+
+
+@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42"])
+def test_burgers_steps(xi300, method):
+    n = 128
+    pb, ob = _burgers_pair(n)
+    u = W.ic_burgers_2d(n)
+    dt = 10 * W.dt_cfl(n, 20.0)
+    with lx.Context(pb) as ctx:
+        ud = _dev(u)
+        bound = lx.lx_spectrum_bound(ctx, ud)
+        assert bound == pytest.approx(O.spectrum_bound(ob, u), rel=1e-14)
+        c, g = O.shift_scale(O.spectrum_bound(ob, u))
+        lo = torch.empty_like(ud)
+        hi = torch.empty_like(ud)
+        it, err = lx.lx_step(ctx, method, ud, lo, hi, dt, c, g, TOL, TOL)
+        r = O.step(ob, method, u, dt, c, g, TOL, TOL, xi300)
+        assert it == r.iters
+        assert _rel(hi, r.u_high) <= TOL
+        if method not in ("rosenbrock_euler", "exprb42"):
+            assert _rel(lo, r.u_low) <= TOL
+            assert err == pytest.approx(r.err, rel=1e-8)
+
+
+def test_burgers_leja_power_rhs_integrate(xi300):
+    n = 96
+    pb, ob = _burgers_pair(n)
+    u = W.ic_burgers_2d(n)
+    v = W.random_vector((n, n), seed=8, scale=0.01)
+    dt = 10 * W.dt_cfl(n, 20.0)
+    c, g = O.shift_scale(O.spectrum_bound(ob, u))
+    with lx.Context(pb) as ctx:
+        ud = _dev(u)
+        outs = [torch.empty_like(ud) for _ in range(2)]
+        it = lx.lx_real_leja_phi_vertical(ctx, _dev(v), outs, (0.5, 1.0), dt, c, g, 1, TOL, TOL, u_lin=ud)
+        r = O.real_leja_phi(ob, v, dt, c, g, 1, TOL, TOL, xi300, u_lin=u, coeffs=(0.5, 1.0))
+        assert it == r.iters
+        for k in range(2):
+            assert _rel(outs[k], r.outs[k]) <= TOL
+        f = torch.empty_like(ud)
+        lx.lx_rhs(ctx, ud, f, 0.25)
+        ref = 0.25 * O.rhs(ob, u)
+        assert np.abs(f.cpu().numpy() - ref).max() <= 1e-12 * np.abs(ref).max()
+        est = lx.lx_spectrum_estimate(ctx, ud, 30)
+        assert est == pytest.approx(O.power_iteration(ob, u, 30), rel=1e-10)
+        it2, err2 = lx.lx_integrate(ctx, "exprb32", ud, dt, 3, TOL, TOL)
+    tot = 0
+    for _ in range(3):
+        cc, gg = O.shift_scale(O.spectrum_bound(ob, u))
+        rr = O.step(ob, "exprb32", u, dt, cc, gg, TOL, TOL, xi300)
+        tot += rr.iters
+        u = rr.u_high
+    assert it2 == tot and _rel(ud, u) <= TOL
