@@ -138,9 +138,42 @@ def cfg4(stream, n=512):
             "phi0_iters": it0, "phi0_ms": ms0, "phi0_GBps": byt / ms0 / 1e6, "phi0_frac": byt / ms0 / 1e6 / PEAK}
 
 
+def cfg_burgers(stream, n=4096, mult=10.0, steps=3):
+    """Problem III: viscous Burgers, EXPRB32 (the paper's Table 2 integrators)."""
+    dx = (2.0 / n, 2.0 / n)
+    pb = lx.Problem((n, n), dx, 1.0, 0.0, 0.0, None, 10.0)
+    ctx = lx.Context(pb, stream=stream)
+    u = torch.from_numpy(W.ic_burgers_2d(n)).cuda()
+    dt = mult * W.dt_cfl(n, 20.0)
+    it, _ = lx.lx_integrate(ctx, "exprb32", u, dt, 1, 1e-10, 1e-10)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(stream)
+    lx.lx_integrate(ctx, "exprb32", u, dt, steps, 1e-10, 1e-10, sync=False)
+    b.record(stream)
+    torch.cuda.synchronize()
+    its, err = ctx.synchronize()
+    ms = a.elapsed_time(b)
+    # one Burgers Leja call (J(u) flux form), phi_1 of f*dt
+    c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx, u))
+    f = torch.empty_like(u)
+    lx.lx_rhs(ctx, u, f, dt)
+    out = torch.empty_like(u)
+    m = lx.lx_real_leja_phi(ctx, f, out, dt, c, g, 1, 1e-10, 1e-10, u_lin=u)
+    ms1, _ = timed(stream, lambda: lx.lx_real_leja_phi(ctx, f, out, dt, c, g, 1, 1e-10, 1e-10, u_lin=u,
+                                                        sync=False), 3)
+    ctx.synchronize()
+    byt = u.numel() * (32 + 40 * (m - 1))   # iteration 1: v, u read, y, p written; then y, p, u read, y, p written
+    ctx.close()
+    return {"config": "Problem III (Burgers) exprb32", "grid": [n, n], "dt_cfl_mult": mult, "steps": steps,
+            "leja_iters": its, "ms_per_step": ms / steps, "steps_per_s": steps / (ms * 1e-3), "err": err,
+            "phi1_iters": m, "phi1_ms": ms1, "phi1_GBps": byt / ms1 / 1e6, "phi1_frac": byt / ms1 / 1e6 / PEAK,
+            "algorithmic_bytes_note": "40 B/pt per iteration (y, p, u reads; y, p writes)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="0,1,2,3,4")
+    ap.add_argument("--only", default="0,1,2,3,4,5")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     s = torch.cuda.Stream()
@@ -156,6 +189,8 @@ def main():
         print(json.dumps(cfg_leja(s, 16384, (0,), "3 (N=1)", reps=2)), flush=True)
     if 4 in want:
         print(json.dumps(cfg4(s)), flush=True)
+    if 5 in want:
+        print(json.dumps(cfg_burgers(s)), flush=True)
 
 
 if __name__ == "__main__":
