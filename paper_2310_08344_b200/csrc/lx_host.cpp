@@ -87,6 +87,7 @@ struct lx_ctx {
     double* rcp_dev = nullptr;            // [M][M]: 1/(xi_j - xi_i), j > i (divided-difference recurrence)
     Comm* comm = nullptr;                 // slab decomposition (lx_comm.cpp)
     int variant = 0;                      // 2D single-GPU Leja kernel: 0 = register tiles, 1 = TMA marching
+    int tblock = 2;                       // 2D single-GPU: Leja iterations per HBM pass (1 or 2; LX_TBLOCK)
     bool coef_table = false;              // LX_COEF=table: prebuilt coefficient table instead of in-kernel
     double* cg_dev = nullptr;             // device (c, gamma, bound) of lx_integrate
     const double* cg_active = nullptr;    // when set, Leja kernels take (c, gamma) from here
@@ -328,6 +329,16 @@ static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u,
             return LX_OK;
         }
     }
+    if (P.ndim == 2 && ctx->tblock == 2 && P.n_loc >= 16 && P.n1 >= 64) {
+        // temporally blocked kernel: two iterations per pass; work items = (60-column band, RT-row chunk)
+        P.nb = (P.n1 + kBand2 - 1) / kBand2;
+        P.nrb = (P.n_loc + tb2_rt(K) - 1) / tb2_rt(K);
+        P.nunits = P.nb * P.nrb;
+        P.grid = leja_tb2_grid_size(ctx->device, K, diag, P.nunits);
+        CUDA_TRY(launch_leja_tb2(P, ctx->stream, diag));
+        ctx->launches++;
+        return LX_OK;
+    }
     P.grid = leja_grid_size(ctx->device, K, diag, P.ndim, P.nunits);
     CUDA_TRY(launch_leja_persistent(P, ctx->stream, diag));
     ctx->launches++;
@@ -474,6 +485,7 @@ lx_status lx_ctx_create(const lx_problem* pb, int max_nodes, int device, void* c
     ctx->N_glob = (double)ctx->n[0] * (double)ctx->row;
     ctx->max_nodes = max_nodes;
     if (const char* ev = std::getenv("LX_LEJA_KERNEL")) ctx->variant = (std::strcmp(ev, "tma") == 0) ? 1 : 0;
+    if (const char* ev = std::getenv("LX_TBLOCK")) ctx->tblock = (std::atoi(ev) == 1) ? 1 : 2;
     if (const char* ev = std::getenv("LX_COEF")) ctx->coef_table = (std::strcmp(ev, "table") == 0);
     cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device);
     ctx->max_grid = ctx->nsm * 8;

@@ -10,8 +10,11 @@ constexpr int kThreads = 256;     // threads per CTA (8 warps)
 constexpr int kWarps = kThreads / 32;
 constexpr int kRT = 4;            // rows per warp work unit (2D)
 constexpr int kRT3 = 2;           // planes per warp work unit (3D)
+// rows per chunk of the two-step (temporally blocked) kernel, by the number of accumulators K
+__host__ __device__ constexpr int tb2_rt(int K) { return K <= 2 ? 4 : 2; }
+constexpr int kBand2 = 60;        // output columns per warp band of the two-step kernel (64 loaded)
 constexpr int kMaxK = 4;          // vertical accumulators
-constexpr int kSlot = 8;          // doubles per CTA partial slot (1 + K <= 5)
+constexpr int kSlot = 12;         // doubles per CTA partial slot (2 (1 + K) <= 10 for two-step passes)
 
 // Per-call record, written on the device, read by the host once per call/step.
 struct Record {
@@ -119,6 +122,9 @@ struct LejaParams {
 cudaError_t launch_leja_persistent(const LejaParams& P, cudaStream_t s, bool diag);
 cudaError_t launch_power_persistent(const LejaParams& P, cudaStream_t s, bool diag);
 int leja_grid_size(int device, int K, bool diag, int ndim, int nunits);
+// temporally blocked 2D kernel: two Leja iterations per HBM pass (single GPU, constant coefficients + diag)
+int leja_tb2_grid_size(int device, int K, bool diag, int nunits);
+cudaError_t launch_leja_tb2(const LejaParams& P, cudaStream_t s, bool diag);
 // TMA-pipelined marching variant (2D, single GPU)
 int leja_tma_grid_size(int device, int K, bool diag, long long band_rows);
 cudaError_t launch_leja_tma(const LejaParams& P, cudaStream_t s, bool diag);

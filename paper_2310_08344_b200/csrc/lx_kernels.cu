@@ -22,6 +22,8 @@
 #include "lx_internal.h"
 
 #include <cstdio>
+#include <map>
+#include <mutex>
 
 namespace lx {
 
@@ -1338,15 +1340,408 @@ __global__ void __launch_bounds__(kThreads, (K <= 1 ? 3 : 2)) k_leja2d_tma(const
     }
 }
 
+
+// ===========================================================================
+// Temporal blocking: TWO Leja iterations per HBM pass.
+//   pass (m, m+1): read y_{m-1}, p_{m-1};  y_m is formed in registers on a
+//   widened halo (rows i0-1 .. i0+RT+1, columns j0-2 .. j0+61 of a 64-column
+//   warp window whose 60 inner columns are outputs);  y_{m+1} and p_{m+1} are
+//   written.  -> 32 B/pt per TWO iterations (16 B/pt per iteration) and one grid
+//   barrier per two iterations.  Both iterations' norms are reduced, and the
+//   stopping rule of P:155 is applied to m and then m+1 exactly as in the
+//   one-step kernel (same decisions, same iteration counts).  If an accumulator
+//   converges at the first iteration of a pass, its p_{m+1} is rolled back to
+//   p_m = p_{m+1} - d_{m+1} y_{m+1} (<= 1 ulp from the one-step value) in the
+//   next pass, or in a final pointwise pass when the call ends.
+// ===========================================================================
+// stencil of the constant-coefficient operator at the two columns of a lane (same order as tile2d)
+__device__ __forceinline__ void stencil2(const Stencil& S, const double2 yc, const double2 up, const double2 dn1,
+                                         const double2 dn2, double left, double r1, double r2, double& ax, double& ay) {
+    ax = S.c0 * yc.x;
+    ax = fma(S.m1[0], up.x, ax);
+    ax = fma(S.p1[0], dn1.x, ax);
+    ax = fma(S.p2[0], dn2.x, ax);
+    ax = fma(S.m1[1], left, ax);
+    ax = fma(S.p1[1], yc.y, ax);
+    ax = fma(S.p2[1], r1, ax);
+    ay = S.c0 * yc.y;
+    ay = fma(S.m1[0], up.y, ay);
+    ay = fma(S.p1[0], dn1.y, ay);
+    ay = fma(S.p2[0], dn2.y, ay);
+    ay = fma(S.m1[1], yc.x, ay);
+    ay = fma(S.p1[1], r1, ay);
+    ay = fma(S.p2[1], r2, ay);
+}
+
+// y_m = alpha (A + diag) y_{m-1} + beta y_{m-1} at one row of the lane's two columns.
+// r1/r2 come from the next lane; lane 31 uses its halo pair h (columns c0+62, c0+63).
+template <bool DIAG>
+__device__ __forceinline__ double2 leja_row(const Stencil& S, double alpha, double beta, const double2 up,
+                                            const double2 yc, const double2 dn1, const double2 dn2, const double2 h,
+                                            const double2 uu, int lane) {
+    const double left = __shfl_up_sync(FULL_MASK, yc.y, 1);
+    double r1 = __shfl_down_sync(FULL_MASK, yc.x, 1);
+    double r2 = __shfl_down_sync(FULL_MASK, yc.y, 1);
+    if (lane == 31) {
+        r1 = h.x;
+        r2 = h.y;
+    }
+    double ax, ay;
+    stencil2(S, yc, up, dn1, dn2, left, r1, r2, ax, ay);
+    if (DIAG) {
+        ax = fma(fma(S.qb, uu.x * uu.x, S.qa), yc.x, ax);
+        ay = fma(fma(S.qb, uu.y * uu.y, S.qa), yc.y, ay);
+    }
+    return make_double2(fma(alpha, ax, beta * yc.x), fma(alpha, ay, beta * yc.y));
+}
+
+// Temporally blocked pass over a contiguous range [cbeg, cend) of (band, chunk) work items in
+// band-major order (chunk = RT rows of a 60-column band).  A warp marches down its rows with
+// register windows: y_{m-1} rows [i0, i0+RT+4), y_m rows [i0-1, i0+RT+2), u rows [i0, i0+RT+2);
+// per chunk it loads RT new rows of y_{m-1} (and u), forms RT new rows of y_m (one row of the
+// halo recomputation per RT rows happens only at a strip start) and writes RT rows of y_{m+1}
+// and p_{m+1}.  Lanes 1..30 own the band's 60 output columns; lanes 0 and 31 carry halo columns.
+// Requires n_loc >= 16, n1 >= 64 (single wrap of every index; host-checked).
+template <int K, int RT, bool DIAG, bool FIRST, bool TWO>
+__device__ __forceinline__ void strip2d_tb2(const LejaParams& P, const double* __restrict__ src,
+                                            double* __restrict__ dst, int cbeg, int cend, int lane, double alpha,
+                                            double b1, double b2, const double* d0, const double* da,
+                                            const double* db, int active, int rbmask, const double* rbd,
+                                            double* acc) {
+    const int n1 = P.n1, n = P.n_loc, nc = P.nrb;
+    const Stencil& S = P.st;
+    auto wrap = [n](int r) { return r < 0 ? r + n : (r >= n ? r - n : r); };
+    auto LD = [](const double* q) { return FIRST ? ldg2(q) : ld2(q); };
+    constexpr int KK = K > 0 ? K : 1;
+    double2 aw[RT + 4], yw[RT + 3], uw[RT + 2];
+    const double2 z2 = make_double2(0.0, 0.0);
+    int ci = cbeg;
+#pragma unroll 1
+    while (ci < cend) {
+        const int b = ci / nc;
+        const int cseg = min(cend, (b + 1) * nc);   // this band's part of the range
+        const int c0 = b * kBand2;
+        const int jraw = c0 - 2 + 2 * lane;
+        const int j = jraw < 0 ? jraw + n1 : (jraw >= n1 ? jraw - n1 : jraw);
+        const int jh = jraw + 2 >= n1 ? jraw + 2 - n1 : jraw + 2;
+        const bool outl = lane >= 1 && lane <= 30 && jraw < n1 && jraw < c0 + kBand2;
+        {
+            const int i0 = (ci - b * nc) * RT;
+            // y_{m-1} rows i0-2 .. i0+3, y_m rows i0-1 .. i0+1
+            double2 t6[6], h3[3], u3[3];
+#pragma unroll
+            for (int q = 0; q < 6; q++) t6[q] = LD(src + (size_t)wrap(i0 - 2 + q) * n1 + j);
+#pragma unroll
+            for (int q = 0; q < 3; q++) {
+                h3[q] = (lane == 31) ? LD(src + (size_t)wrap(i0 - 1 + q) * n1 + jh) : z2;
+                u3[q] = DIAG ? ldg2(P.u + (size_t)wrap(i0 - 1 + q) * n1 + j) : z2;
+            }
+#pragma unroll
+            for (int q = 0; q < 3; q++)
+                yw[q] = leja_row<DIAG>(S, alpha, b1, t6[q], t6[q + 1], t6[q + 2], t6[q + 3], h3[q], u3[q], lane);
+#pragma unroll
+            for (int q = 0; q < 4; q++) aw[q] = t6[q + 2];
+            uw[0] = u3[1];
+            uw[1] = u3[2];
+        }
+#pragma unroll 1
+        for (int i0 = (ci - b * nc) * RT; ci < cseg; ci++, i0 += RT) {
+        const int nout = min(RT, n - i0);
+        double2 ah[RT];
+        double2 pv[RT][KK];
+#pragma unroll
+        for (int q = 0; q < RT; q++) {
+            aw[4 + q] = LD(src + (size_t)wrap(i0 + 4 + q) * n1 + j);
+            ah[q] = (lane == 31) ? LD(src + (size_t)wrap(i0 + 2 + q) * n1 + jh) : z2;
+            if (DIAG) uw[2 + q] = ldg2(P.u + (size_t)wrap(i0 + 2 + q) * n1 + j);
+        }
+#pragma unroll
+        for (int t = 0; t < RT; t++) {
+#pragma unroll
+            for (int k = 0; k < KK; k++) {
+                pv[t][k] = z2;
+                const bool need = ((active >> k) & 1) ? !FIRST : (K > 1 && ((rbmask >> k) & 1));
+                if (outl && t < nout && need) pv[t][k] = ld2(P.p[k] + (size_t)(i0 + t) * n1 + j);
+            }
+        }
+        // step 1: y_m rows i0+2 .. i0+RT+1
+#pragma unroll
+        for (int q = 0; q < RT; q++)
+            yw[3 + q] = leja_row<DIAG>(S, alpha, b1, aw[1 + q], aw[2 + q], aw[3 + q], aw[4 + q], ah[q],
+                                       DIAG ? uw[2 + q] : z2, lane);
+        // step 2: y_{m+1} on the output rows; p updates and norms
+#pragma unroll
+        for (int t = 0; t < RT; t++) {
+            if (t < nout) {
+                const double2 yc = yw[t + 1];
+                double2 zz = yc;
+                if (TWO) zz = leja_row<DIAG>(S, alpha, b2, yw[t], yc, yw[t + 2], yw[t + 3], z2, uw[t], lane);
+                if (outl) {
+                    const size_t off = (size_t)(i0 + t) * n1 + j;
+                    st2(dst + off, zz);
+                    acc[0] = fma(yc.y, yc.y, fma(yc.x, yc.x, acc[0]));
+                    if (TWO) acc[1 + K] = fma(zz.y, zz.y, fma(zz.x, zz.x, acc[1 + K]));
+                    const double2 yprev = aw[t];   // y_{m-1} (= v on the first pass)
+#pragma unroll
+                    for (int k = 0; k < KK; k++) {
+                        if ((active >> k) & 1) {
+                            double2 pm;
+                            if (FIRST) {
+                                pm.x = fma(da[k], yc.x, d0[k] * yprev.x);
+                                pm.y = fma(da[k], yc.y, d0[k] * yprev.y);
+                            } else {
+                                pm.x = fma(da[k], yc.x, pv[t][k].x);
+                                pm.y = fma(da[k], yc.y, pv[t][k].y);
+                            }
+                            acc[1 + k] = fma(pm.y, pm.y, fma(pm.x, pm.x, acc[1 + k]));
+                            double2 pn = pm;
+                            if (TWO) {
+                                pn.x = fma(db[k], zz.x, pm.x);
+                                pn.y = fma(db[k], zz.y, pm.y);
+                                acc[2 + K + k] = fma(pn.y, pn.y, fma(pn.x, pn.x, acc[2 + K + k]));
+                            }
+                            st2(P.p[k] + off, pn);
+                        } else if (K > 1 && ((rbmask >> k) & 1)) {
+                            // roll back the speculative last update of the previous pass (K = 1: the
+                            // call ends at that decision -> final rollback pass instead)
+                            st2(P.p[k] + off, make_double2(fma(-rbd[k], yprev.x, pv[t][k].x),
+                                                           fma(-rbd[k], yprev.y, pv[t][k].y)));
+                        }
+                    }
+                }
+            }
+        }
+        // advance the windows by RT rows
+#pragma unroll
+        for (int q = 0; q < 4; q++) aw[q] = aw[RT + q];
+#pragma unroll
+        for (int q = 0; q < 3; q++) yw[q] = yw[RT + q];
+#pragma unroll
+        for (int q = 0; q < 2; q++) uw[q] = uw[RT + q];
+        }
+    }
+}
+
+// Final rollback pass: p_k -= rbd[k] * y (y = the last written y_{m+1}) on the strip's output points.
+template <int K, int RT>
+__device__ __forceinline__ void strip2d_tb2_rollback(const LejaParams& P, const double* y, int cbeg, int cend,
+                                                     int lane, int rbmask, const double* rbd) {
+    const int n1 = P.n1, n = P.n_loc, nc = P.nrb;
+    for (int ci = cbeg; ci < cend; ci++) {
+        const int b = ci / nc, ic = ci - b * nc;
+        const int c0 = b * kBand2;
+        const int jraw = c0 - 2 + 2 * lane;
+        if (!(lane >= 1 && lane <= 30 && jraw < n1 && jraw < c0 + kBand2)) continue;
+        const int i0 = ic * RT;
+        const int nout = min(RT, n - i0);
+        for (int t = 0; t < nout; t++) {
+            const size_t off = (size_t)(i0 + t) * n1 + jraw;
+            const double2 yy = ld2(y + off);
+#pragma unroll
+            for (int k = 0; k < K; k++) {
+                if ((rbmask >> k) & 1) {
+                    const double2 pp = ld2(P.p[k] + off);
+                    st2(P.p[k] + off, make_double2(fma(-rbd[k], yy.x, pp.x), fma(-rbd[k], yy.y, pp.y)));
+                }
+            }
+        }
+    }
+}
+
+// grid barrier + decisions of iterations m (and m+1): flags[1] done, [2] active, [3] rollback mask
+template <int K>
+__device__ __forceinline__ void barrier_decide_tb2(const LejaParams& P, int m, bool two, unsigned gen0, const double* da,
+                                                   const double* db, int active, double (*s_red)[kSlot],
+                                                   int* s_flags) {
+    constexpr int NV = 2 * (1 + K);
+    const int tid = threadIdx.x;
+    Ctrl* ctrl = P.ctrl;
+    const int par = ((m - 1) / 2) & 1;
+    __syncthreads();
+    if (tid == 0) {
+        const unsigned t = atom_add_acq_rel(&ctrl->arrive, 1u);
+        s_flags[0] = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (s_flags[0]) {
+        double acc[NV];
+#pragma unroll
+        for (int i = 0; i < NV; i++) acc[i] = 0.0;
+        for (int c = tid; c < (int)gridDim.x; c += kThreads) {
+            const double* slot = P.partials + ((size_t)par * gridDim.x + c) * kSlot;
+#pragma unroll
+            for (int i = 0; i < NV; i++) acc[i] += __ldcg(slot + i);
+        }
+        block_reduce<NV>(acc, s_red);
+        if (tid == 0) {
+            int act = active, done = 0, status = 0;
+            leja_decide<K>(P, m, acc, da, act, done, status, P.rec);
+            const int rb = active & ~act;   // converged at the first iteration of the pass -> roll back
+            if (!done && two) leja_decide<K>(P, m + 1, acc + 1 + K, db, act, done, status, P.rec);
+            ctrl->arrive = 0u;
+            const unsigned long long w = ((unsigned long long)(gen0 + (unsigned)m) << 32) |
+                                         ((unsigned long long)(status & 0xff) << 16) |
+                                         ((unsigned long long)(rb & 0xf) << 12) |
+                                         ((unsigned long long)(done & 0xf) << 8) | (unsigned long long)(act & 0xff);
+            st_release64(&ctrl->word, w);
+            s_flags[1] = done;
+            s_flags[2] = act;
+            s_flags[3] = two ? rb : 0;
+        }
+    } else if (tid == 0) {
+        unsigned long long w = ld_acquire64(&ctrl->word);
+        int spins = 0;
+        while ((int)((unsigned)(w >> 32) - gen0) < m) {
+            if (++spins > 32) __nanosleep(32);
+            if (spins > P.timeout_spins) {
+                atomicExch(&P.rec->status, 10);
+                w = (1ull << 8);
+                break;
+            }
+            w = ld_acquire64(&ctrl->word);
+        }
+        s_flags[1] = (int)((w >> 8) & 0xf);
+        s_flags[2] = (int)(w & 0xff);
+        s_flags[3] = two ? (int)((w >> 12) & 0xf) : 0;
+    }
+    __syncthreads();
+}
+
+template <int K>
+__device__ __forceinline__ void coef_first5(const LejaParams& P, int k, double* d) {
+    // d_0..d_4 of accumulator k by lane 0 of the warp (column form, explicitly rounded), broadcast
+    const int M = P.max_nodes;
+    double e[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int jj = 0; jj < 5; jj++) {
+            if (jj < M) {
+                double v = coef_h(P, k, jj);
+#pragma unroll
+                for (int i = 0; i < jj; i++) v = dd_step(v, e[i], P.R[(size_t)i * M + jj]);
+                e[jj] = v;
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 5; i++) d[i] = __shfl_sync(0xffffffffu, e[i], 0);
+}
+
+template <int K, bool DIAG>
+__global__ void __launch_bounds__(kThreads, (K == 1 ? 2 : 1)) k_leja2d_tb2(const __grid_constant__ LejaParams P) {
+    __shared__ double s_red[kWarps][kSlot];
+    __shared__ int s_flags[4];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool cwarp = (blockIdx.x == 0 && warp == 0);
+    const int gw = blockIdx.x * kWarps + warp - 1;
+    const int W = gridDim.x * kWarps - 1;
+    constexpr int RT = tb2_rt(K);
+    const int cbeg = cwarp ? 0 : (int)((long long)gw * P.nunits / W);
+    const int cend = cwarp ? 0 : (int)((long long)(gw + 1) * P.nunits / W);
+    unsigned gen0 = 0;
+    if (tid == 0) gen0 = (unsigned)(ld_acquire64(&P.ctrl->word) >> 32);
+    int active = P.active0, rbmask = 0;
+    const int M = P.max_nodes;
+    const double alpha = P_alpha(P);
+    double dd[K][5];
+#pragma unroll
+    for (int k = 0; k < K; k++) coef_first5<K>(P, k, dd[k]);
+    if (cwarp && P.coef_gen) {
+        for (int r = 0; r < 5 && r < M; r++) {
+            double row[K];
+#pragma unroll
+            for (int k = 0; k < K; k++) row[k] = dd[k][r];
+            coef_write_row<K>(P, r, lane, active, row);
+        }
+    }
+    double d0[K], da[K], db[K], rbd[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        d0[k] = dd[k][0];
+        da[k] = dd[k][1];
+        db[k] = dd[k][2];
+        rbd[k] = 0.0;
+    }
+    double na[K], nb[K];   // rows m+2, m+3 (rows 3, 4 from the prologue for the first pass)
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+        na[k] = dd[k][3];
+        nb[k] = dd[k][4];
+    }
+    int m = 1;
+    for (; m < M; m += 2) {
+        const bool two = (m + 1 < M);
+        const double b1 = coef_beta(P, m), b2 = two ? coef_beta(P, m + 1) : 0.0;
+        const int pass = (m - 1) >> 1;
+        double* dst = P.ydst[pass & 1];
+        double acc[2 * (1 + K)];
+#pragma unroll
+        for (int i = 0; i < 2 * (1 + K); i++) acc[i] = 0.0;
+        if (cwarp) {
+            if (P.coef_gen) {
+                if (m + 4 < M) coef_write_row<K>(P, m + 4, lane, active, nullptr);
+                if (m + 5 < M) coef_write_row<K>(P, m + 5, lane, active, nullptr);
+            }
+        } else {
+            const double* src = (m == 1) ? P.v.base : P.ysrc[(pass & 1) ^ 1].base;
+            if (m == 1) {
+                if (two) strip2d_tb2<K, RT, DIAG, true, true>(P, src, dst, cbeg, cend, lane, alpha, b1, b2, d0, da, db,
+                                                             active, rbmask, rbd, acc);
+                else strip2d_tb2<K, RT, DIAG, true, false>(P, src, dst, cbeg, cend, lane, alpha, b1, b2, d0, da, db,
+                                                           active, rbmask, rbd, acc);
+            } else {
+                if (two) strip2d_tb2<K, RT, DIAG, false, true>(P, src, dst, cbeg, cend, lane, alpha, b1, b2, d0, da,
+                                                              db, active, rbmask, rbd, acc);
+                else strip2d_tb2<K, RT, DIAG, false, false>(P, src, dst, cbeg, cend, lane, alpha, b1, b2, d0, da, db,
+                                                            active, rbmask, rbd, acc);
+            }
+        }
+        block_reduce<2 * (1 + K)>(acc, s_red);
+        if (tid == 0) {
+            double* slot = P.partials + ((size_t)(pass & 1) * gridDim.x + blockIdx.x) * kSlot;
+#pragma unroll
+            for (int i = 0; i < 2 * (1 + K); i++) slot[i] = acc[i];
+        }
+        barrier_decide_tb2<K>(P, m, two, gen0, da, db, active, s_red, s_flags);
+        active = s_flags[2];
+        rbmask = s_flags[3];
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            rbd[k] = db[k];
+            da[k] = na[k];
+            db[k] = nb[k];
+            // rows m+4, m+5 (written by the coefficient warp during pass m-2... visible after this barrier)
+            na[k] = (m + 4 < M) ? P.table[(size_t)(m + 4) * (1 + K) + 1 + k] : 0.0;
+            nb[k] = (m + 5 < M) ? P.table[(size_t)(m + 5) * (1 + K) + 1 + k] : 0.0;
+        }
+        if (s_flags[1]) break;
+    }
+    // the call ended on the first iteration of a pass for some accumulators: final rollback
+    if (rbmask && !cwarp && m < M) strip2d_tb2_rollback<K, RT>(P, P.ydst[((m - 1) >> 1) & 1], cbeg, cend, lane, rbmask, rbd);
+}
+
 // ---------------------------------------------------------------------------
 // Launchers
 // ---------------------------------------------------------------------------
-template <typename Kern>
-static int max_coresident(int device, Kern kern) {
+// Co-resident CTAs (kThreads each, no dynamic smem) of a kernel on a device: SMs x blocks per SM,
+// cached per (device, kernel) -- occupancy queries cost host microseconds on every Leja call.
+static int coresident(int device, const void* kern) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, int> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find({device, kern});
+    if (it != cache.end()) return it->second;
     int nsm = 0, per = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, 0);
+    if (per < 1) per = 1;
+    cache[{device, kern}] = nsm * per;
     return nsm * per;
+}
+
+template <typename Kern>
+static int max_coresident(int device, Kern kern) {
+    return coresident(device, (const void*)kern);
 }
 
 template <int NDIM>
@@ -1378,12 +1773,7 @@ static void* leja_kernel_ptr(int ndim, int K, bool diag) {
 }
 
 int leja_grid_size(int device, int K, bool diag, int ndim, int nunits) {
-    void* kern = leja_kernel_ptr(ndim, K, diag);
-    int nsm = 0, per = 0;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, 0);
-    if (per < 1) per = 1;
-    long long g = (long long)nsm * per;
+    long long g = coresident(device, leja_kernel_ptr(ndim, K, diag));
     // never more CTAs than work: at least 2 units per warp for tiny grids
     long long need = (nunits + kWarps - 1) / kWarps;
     if (g > need) g = need > 0 ? need : 1;
@@ -1588,6 +1978,35 @@ cudaError_t launch_shift_scale(const unsigned long long* umax, const ShiftArgs& 
     return cudaGetLastError();
 }
 
+
+static void* leja_tb2_ptr(int K, bool diag) {
+    switch (K * 2 + (diag ? 1 : 0)) {
+        case 2: return (void*)k_leja2d_tb2<1, false>;
+        case 3: return (void*)k_leja2d_tb2<1, true>;
+        case 4: return (void*)k_leja2d_tb2<2, false>;
+        case 5: return (void*)k_leja2d_tb2<2, true>;
+        case 6: return (void*)k_leja2d_tb2<3, false>;
+        case 7: return (void*)k_leja2d_tb2<3, true>;
+        case 8: return (void*)k_leja2d_tb2<4, false>;
+        case 9: return (void*)k_leja2d_tb2<4, true>;
+    }
+    return nullptr;
+}
+
+int leja_tb2_grid_size(int device, int K, bool diag, int nunits) {
+    long long g = coresident(device, leja_tb2_ptr(K, diag));
+    long long need = (nunits + kWarps - 1) / kWarps + 1;
+    if (g > need) g = need;
+    return (int)g;
+}
+
+cudaError_t launch_leja_tb2(const LejaParams& P, cudaStream_t s, bool diag) {
+    void* kern = leja_tb2_ptr(P.K, diag);
+    if (!kern) return cudaErrorInvalidValue;
+    void* args[] = {(void*)&P};
+    return cudaLaunchCooperativeKernel(kern, dim3(P.grid), dim3(kThreads), args, 0, s);
+}
+
 // ---------------------------------------------------------------------------
 // Stage kernels
 // ---------------------------------------------------------------------------
@@ -1767,13 +2186,11 @@ cudaError_t launch_rem_flux(const LejaParams& P, double dt, double a2, double* o
 }
 
 int stage_grid_size(int device, int op) {
-    int nsm = 0, per = 0;
+    int nsm = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     void* k = stage_kernel_ptr(op);
-    if (k) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kThreads, 0);
-    if (per < 1) per = 1;
-    if (per > 8) per = 8;
-    return nsm * per;
+    const int g = k ? coresident(device, k) : nsm;
+    return g > 8 * nsm ? 8 * nsm : g;
 }
 
 cudaError_t launch_rhs(const LejaParams& P, double scale, cudaStream_t s) {

@@ -350,6 +350,7 @@ def test_kernel_variants_bitwise_equal(xi300, monkeypatch, shape, K, react):
     dt = 0.01 if react else 10 * min(W.dt_cfl(n, 10.0) for n in shape)
     coeffs = (0.5, 2 / 3, 0.9, 1.0)[-K:]
     res = {}
+    monkeypatch.setenv("LX_TBLOCK", "1")   # one iteration per pass (the two-step kernel: test_tblock2_*)
     for variant in ("tile", "tma"):   # LX_LEJA_KERNEL values
         monkeypatch.setenv("LX_LEJA_KERNEL", variant)
         with lx.Context(pb) as ctx:
@@ -475,3 +476,35 @@ def test_burgers_leja_power_rhs_integrate(xi300):
         tot += rr.iters
         u = rr.u_high
     assert it2 == tot and _rel(ud, u) <= TOL
+
+
+@pytest.mark.parametrize("shape,K,react,l", [((64, 64), 1, 0.0, 0), ((66, 62), 2, 0.0, 1), ((7, 24), 1, 0.0, 2),
+                                             ((130, 122), 3, 1.0, 1), ((131, 182), 4, 0.0, 1),
+                                             ((200, 60), 4, 1.0, 3), ((4096, 256), 1, 1.0, 0)])
+def test_tblock2_matches_oracle_and_one_step(xi300, monkeypatch, shape, K, react, l):
+    # two Leja iterations per HBM pass: ragged 60-column bands (n1 = 62, 122,
+    # 182, 24 < 64), odd row counts, K = 1..4 (accumulators converging at different m, i.e. on
+    # either half of a pass -> rollback), with and without the diagonal term.  Same iteration
+    # counts as the oracle and as the one-step kernel; y_m, p_m are bitwise those of the one-step
+    # kernel except after a rollback p_m = p_{m+1} - d_{m+1} y_{m+1} (a few ulp).
+    diff, nu = (1e-4, 0.0) if react else (1.0, 10.0)
+    pb, ob = _pair(shape, diff=diff, nu=nu, react=react)
+    u = W.ic_allen_cahn_2d(*shape) if react else None
+    v = W.ic_random(shape, seed=23, amp=0.2)
+    dt = 0.01 if react else 10 * min(W.dt_cfl(n, 10.0) for n in shape)
+    coeffs = (0.25, 0.5, 0.75, 1.0)[-K:]
+    res = {}
+    for tb in ("1", "2"):
+        monkeypatch.setenv("LX_TBLOCK", tb)
+        with lx.Context(pb) as ctx:
+            ud = _dev(u) if react else None
+            c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx, ud))
+            outs = [torch.full(shape, float("nan"), dtype=torch.float64, device="cuda") for _ in range(K)]
+            it = lx.lx_real_leja_phi_vertical(ctx, _dev(v), outs, coeffs, dt, c, g, l, TOL, TOL, u_lin=ud)
+            res[tb] = (it, [o.cpu().numpy() for o in outs])
+    r = O.real_leja_phi(ob, v, dt, c, g, l, TOL, TOL, xi300, coeffs=coeffs, u_lin=u)
+    assert res["2"][0] == res["1"][0] == r.iters
+    for a, b, ref in zip(res["2"][1], res["1"][1], r.outs):
+        assert np.isfinite(a).all()
+        np.testing.assert_allclose(a, b, rtol=0, atol=8 * np.finfo(float).eps * np.abs(b).max())
+        assert np.linalg.norm(a - ref) <= TOL * np.linalg.norm(ref)

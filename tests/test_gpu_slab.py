@@ -52,7 +52,8 @@ def _run_ranks(P, fn):
 
 
 @pytest.mark.parametrize("P,shape", [(2, (64, 64)), (3, (50, 70)), (4, (130, 66)), (8, (64, 128))])
-def test_slab_leja_matches_oracle_and_single_domain(xi300, P, shape):
+def test_slab_leja_matches_oracle_and_single_domain(xi300, monkeypatch, P, shape):
+    monkeypatch.setenv("LX_TBLOCK", "1")   # single-domain reference: the one-step kernel (same arithmetic)
     dx = tuple(2.0 / n for n in shape)
     pb = lx.Problem(shape, dx, 1.0, 10.0, 0.0)
     ob = O.Problem(shape, dx, 1.0, 10.0, 0.0)

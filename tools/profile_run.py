@@ -4,6 +4,7 @@
   python tools/profile_run.py leja2d 4096 0      # phi_0 Leja call, 2D
   python tools/profile_run.py leja3d 512 0       # phi_0 Leja call, 3D
   python tools/profile_run.py ac 2048 2          # Allen-Cahn EXPRB43, 2 steps
+  python tools/profile_run.py aci 2048 2         # the same through lx_integrate
 """
 import os
 import sys
@@ -51,6 +52,13 @@ def main():
             it, err = lx.lx_step(ctx, "exprb43", u, lo, hi, wl.dt, c, g, wl.rtol, wl.atol)
             u, hi = hi, u
             print("iters", it, "err", err)
+    elif what == "aci":   # the same through lx_integrate (device-side spectrum)
+        wl = W.config(2, n=n)
+        pb = lx.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
+        ctx = lx.Context(pb)
+        u = torch.from_numpy(W.ic_allen_cahn_2d(n)).cuda()
+        it, err = lx.lx_integrate(ctx, "exprb43", u, wl.dt, arg, wl.rtol, wl.atol)
+        print("iters", it, "err", err)
     torch.cuda.synchronize()
 
 

@@ -96,15 +96,17 @@ def cfg2(stream, n=2048, steps=20):
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     ms = a.elapsed_time(b)
-    # the same run through lx_integrate (device-side spectrum, no host round trips)
-    u2 = torch.from_numpy(W.ic_allen_cahn_2d(n)).cuda()
-    torch.cuda.synchronize()
-    a.record(stream)
-    lx.lx_integrate(ctx, "exprb43", u2, wl.dt, steps, wl.rtol, wl.atol, sync=False)
-    b.record(stream)
-    torch.cuda.synchronize()
-    it2, err2 = ctx.synchronize()
-    ms2 = a.elapsed_time(b)
+    # the same run through lx_integrate (device-side spectrum, no host round trips); twice, the
+    # second timed
+    for _ in range(2):
+        u2 = torch.from_numpy(W.ic_allen_cahn_2d(n)).cuda()
+        torch.cuda.synchronize()
+        a.record(stream)
+        lx.lx_integrate(ctx, "exprb43", u2, wl.dt, steps, wl.rtol, wl.atol, sync=False)
+        b.record(stream)
+        torch.cuda.synchronize()
+        it2, err2 = ctx.synchronize()
+        ms2 = a.elapsed_time(b)
     ctx.close()
     return {"config": 2, "workload": wl.name, "grid": [n, n], "steps": steps, "leja_iters_per_step": its,
             "err": errs[-1], "steps_per_s_device": steps / (ms * 1e-3), "steps_per_s_wall": steps / wall,
