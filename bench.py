@@ -10,8 +10,10 @@ one persistent fused Leja kernel (device-side stopping decision).
 
 value   = Leja iterations / s (device-timed, inputs resident in HBM)
 e2e     = same metric through the C-ABI with HOST (pinned) buffers, copies inside
-roofline: dominant kernel k_leja2d<1,false>, algorithmic bytes
-          N*(24 + 32*(m-1)) per launch / CUDA-event duration.
+roofline: dominant kernel k_leja2d_tb2<1,false> (two Leja iterations per HBM pass),
+          algorithmic bytes N*(24 + 32*(ceil(m/2)-1) [+24 if m odd]) per launch
+          (leja_bytes_per_point; one-step schedule: N*(24 + 32*(m-1)))
+          / CUDA-event duration.
 cpu_baseline / --impl reference: the oracle (oracle/) on the host cores.
 
 N>1 (torchrun): weak scaling -- each rank owns a 4096-row slab of a
@@ -153,6 +155,19 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+def leja_bytes_per_point(m, tb2):
+    """Algorithmic HBM bytes per grid point of one Leja call with m iterations (roofline).
+
+    one-step kernel: iteration 1 reads v, writes y, p (24 B); every later one reads y, p and writes
+    y, p (32 B).  two-step kernel (temporal blocking): pass 1 = iterations 1, 2 reads v, writes y, p
+    (24 B); each later pass (two iterations) reads y, p and writes y, p (32 B); a call that stops on
+    the first iteration of its last pass adds the rollback pass (read y, p; write p: 24 B)."""
+    if not tb2:
+        return 24 + 32 * (m - 1)
+    passes = (m + 1) // 2
+    return 24 + 32 * (passes - 1) + (24 if m % 2 == 1 else 0)
+
+
 def _traffic_from_profiles():
     p = os.path.join(ROOT, "profiles", "leja_traffic.json")
     if os.path.exists(p):
@@ -269,14 +284,18 @@ def run_ours(args):
 
     # roofline of the dominant kernel (persistent Leja kernel, one launch per call)
     durs = np.array([[evs[s][l][0].elapsed_time(evs[s][l][1]) for l in range(4)] for s in range(args.steps)])
-    bytes_per_call = np.array([N * (24 + 32 * (m - 1)) for m in iters], dtype=np.float64)
+    tb2 = ws == 1 and os.environ.get("LX_TBLOCK", "2") != "1"
+    bytes_per_call = np.array([N * leja_bytes_per_point(m, tb2) for m in iters], dtype=np.float64)
     per_call_ms = durs.mean(axis=0)
     achieved = float(bytes_per_call.sum() / (per_call_ms.sum() * 1e-3) / 1e9)
     peak, peak_kind = _peaks()
     tr = _traffic_from_profiles()
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": (tr or {}).get("traffic_bytes_per_launch"),
-            "kernel": "k_leja2d<1,false> (persistent, 1 launch per Leja call)",
+            "kernel": ("k_leja2d_tb2<1,false> (persistent, 2 Leja iterations per HBM pass, 1 launch per call)"
+                       if tb2 else "k_leja2d<1,false> (persistent, 1 launch per Leja call)"),
+            "one_step_equivalent_frac": float(N * sum(leja_bytes_per_point(m, False) for m in iters)
+                                              / (per_call_ms.sum() * 1e-3) / 1e9 / peak),
             "algorithmic_bytes_per_launch": [float(b) for b in bytes_per_call],
             "launch_ms": [float(x) for x in per_call_ms],
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (%s)" % peak_kind,

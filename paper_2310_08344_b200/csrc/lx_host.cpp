@@ -88,6 +88,11 @@ struct lx_ctx {
     Comm* comm = nullptr;                 // slab decomposition (lx_comm.cpp)
     int variant = 0;                      // 2D single-GPU Leja kernel: 0 = register tiles, 1 = TMA marching
     int tblock = 2;                       // 2D single-GPU: Leja iterations per HBM pass (1 or 2; LX_TBLOCK)
+    int tb2_seg = 8;                      // two-step kernel: dynamic segment length in chunks (LX_TB2_SEG; 0 static)
+    int tb2_cap = 0;                      // segments the buffers below can hold
+    double* tb2_seg_part = nullptr;       // [cap][2(1+kMaxK)]
+    double* tb2_grp_part = nullptr;       // [cap/32+1][2(1+kMaxK)]
+    unsigned* tb2_grp_cnt = nullptr;      // [cap/32+1]
     bool coef_table = false;              // LX_COEF=table: prebuilt coefficient table instead of in-kernel
     double* cg_dev = nullptr;             // device (c, gamma, bound) of lx_integrate
     const double* cg_active = nullptr;    // when set, Leja kernels take (c, gamma) from here
@@ -335,6 +340,29 @@ static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u,
         P.nrb = (P.n_loc + tb2_rt(K) - 1) / tb2_rt(K);
         P.nunits = P.nb * P.nrb;
         P.grid = leja_tb2_grid_size(ctx->device, K, diag, P.nunits);
+        P.seg = ctx->tb2_seg;
+        if (P.seg > 0) {
+            P.nseg = (P.nunits + P.seg - 1) / P.seg;
+            P.ngrp = (P.nseg + 31) / 32;
+            if (P.nseg > ctx->tb2_cap) {
+                cudaFree(ctx->tb2_seg_part);
+                cudaFree(ctx->tb2_grp_part);
+                cudaFree(ctx->tb2_grp_cnt);
+                ctx->tb2_seg_part = nullptr;
+                ctx->tb2_grp_part = nullptr;
+                ctx->tb2_grp_cnt = nullptr;
+                ctx->tb2_cap = 0;
+                const size_t nv = 2 * (1 + kMaxK);
+                CUDA_TRY(cudaMalloc(&ctx->tb2_seg_part, (size_t)P.nseg * nv * sizeof(double)));
+                CUDA_TRY(cudaMalloc(&ctx->tb2_grp_part, (size_t)P.ngrp * nv * sizeof(double)));
+                CUDA_TRY(cudaMalloc(&ctx->tb2_grp_cnt, (size_t)P.ngrp * sizeof(unsigned)));
+                CUDA_TRY(cudaMemsetAsync(ctx->tb2_grp_cnt, 0, (size_t)P.ngrp * sizeof(unsigned), ctx->stream));
+                ctx->tb2_cap = P.nseg;
+            }
+            P.seg_part = ctx->tb2_seg_part;
+            P.grp_part = ctx->tb2_grp_part;
+            P.grp_cnt = ctx->tb2_grp_cnt;
+        }
         CUDA_TRY(launch_leja_tb2(P, ctx->stream, diag));
         ctx->launches++;
         return LX_OK;
@@ -416,6 +444,9 @@ static void free_ctx(lx_ctx* ctx) {
     for (double* p : ctx->S) cudaFree(p);
     for (double* p : ctx->H) cudaFree(p);
     cudaFree(ctx->partials);
+    cudaFree(ctx->tb2_seg_part);
+    cudaFree(ctx->tb2_grp_part);
+    cudaFree(ctx->tb2_grp_cnt);
     cudaFree(ctx->ctrl);
     cudaFree(ctx->rec_dev);
     cudaFree(ctx->coef_dev);
@@ -486,6 +517,7 @@ lx_status lx_ctx_create(const lx_problem* pb, int max_nodes, int device, void* c
     ctx->max_nodes = max_nodes;
     if (const char* ev = std::getenv("LX_LEJA_KERNEL")) ctx->variant = (std::strcmp(ev, "tma") == 0) ? 1 : 0;
     if (const char* ev = std::getenv("LX_TBLOCK")) ctx->tblock = (std::atoi(ev) == 1) ? 1 : 2;
+    if (const char* ev = std::getenv("LX_TB2_SEG")) ctx->tb2_seg = std::atoi(ev) > 0 ? std::atoi(ev) : 0;
     if (const char* ev = std::getenv("LX_COEF")) ctx->coef_table = (std::strcmp(ev, "table") == 0);
     cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device);
     ctx->max_grid = ctx->nsm * 8;

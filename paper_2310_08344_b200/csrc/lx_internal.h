@@ -10,8 +10,14 @@ constexpr int kThreads = 256;     // threads per CTA (8 warps)
 constexpr int kWarps = kThreads / 32;
 constexpr int kRT = 4;            // rows per warp work unit (2D)
 constexpr int kRT3 = 2;           // planes per warp work unit (3D)
-// rows per chunk of the two-step (temporally blocked) kernel, by the number of accumulators K
-__host__ __device__ constexpr int tb2_rt(int K) { return K <= 2 ? 4 : 2; }
+// two-step (temporally blocked) kernel: rows per chunk, bytes of one staged chunk, ring depth
+// (chunks per warp ring; 8 warps x depth x stage <= 110 KB so that two CTAs fit on an SM)
+__host__ __device__ constexpr int tb2_rt(int K) { return K == 1 ? 4 : 2; }
+__host__ __device__ constexpr int tb2_stage_bytes(int K, bool diag) {
+    return 16 * (tb2_rt(K) * 32 * (1 + K + (diag ? 1 : 0)) + tb2_rt(K));
+}
+__host__ __device__ constexpr int tb2_depth(int K, bool diag) { return tb2_stage_bytes(K, diag) * 24 <= 112640 ? 3 : 2; }
+__host__ __device__ constexpr int tb2_smem_bytes(int K, bool diag) { return 8 * tb2_depth(K, diag) * tb2_stage_bytes(K, diag); }
 constexpr int kBand2 = 60;        // output columns per warp band of the two-step kernel (64 loaded)
 constexpr int kMaxK = 4;          // vertical accumulators
 constexpr int kSlot = 12;         // doubles per CTA partial slot (2 (1 + K) <= 10 for two-step passes)
@@ -47,6 +53,8 @@ struct Ctrl {
     // persistent kernels: packed decision word released by the barrier's last arriver
     // [63:32] generation (gen0 + m), [31:16] status, [15:8] done, [7:0] active mask
     unsigned long long word;
+    unsigned int work[2];  // two-step kernel: dynamic segment counters of even / odd passes
+    unsigned int pad3[2];
 };
 
 // Rows of a slab: rows [0, n_loc) at base, row r in {-1, n_loc, n_loc+1}
@@ -116,6 +124,13 @@ struct LejaParams {
     // nullptr -> cc / cgamma / alpha from the host
     const double* cg_dev;
     const double* source;  // optional source S added by the f(u) (M_RHS) tiles (Problem II)
+    // two-step kernel, dynamic segments of `seg` chunks (0 = static ranges): per-segment norm partials,
+    // reduced in fixed order per group of 32 segments by the group's last finisher, then over groups
+    int seg;
+    int nseg, ngrp;
+    double* seg_part;     // [nseg][2(1+K)]
+    double* grp_part;     // [ngrp][2(1+K)]
+    unsigned* grp_cnt;    // [ngrp] finished segments of the group (reset by its last finisher)
 };
 
 // launchers (lx_kernels.cu)

@@ -1395,45 +1395,109 @@ __device__ __forceinline__ double2 leja_row(const Stencil& S, double alpha, doub
     return make_double2(fma(alpha, ax, beta * yc.x), fma(alpha, ay, beta * yc.y));
 }
 
+// xor-butterfly sum of N values over the warp (fixed order: every lane ends with the same bits)
+template <int N>
+__device__ __forceinline__ void warp_sum(double* v) {
+#pragma unroll
+    for (int i = 0; i < N; i++) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v[i] += __shfl_xor_sync(FULL_MASK, v[i], off);
+    }
+}
+
+// Shared-memory staging of the two-step kernel: per warp a ring of tb2_depth stages, one stage =
+// the global rows one chunk consumes (16 B per lane per row, lane-private: every lane reads back only
+// what its own cp.async wrote -> no warp synchronisation needed):
+//   y_{m-1} rows i0+4 .. i0+RT+3 | halo pair of lane 31 for rows i0+2 .. i0+RT+1 |
+//   p_k rows i0 .. i0+RT-1 (k < K) | u rows i0+2 .. i0+RT+1 (DIAG)
+template <int K, bool DIAG>
+struct Tb2Stage {
+    static constexpr int RT = tb2_rt(K);
+    static constexpr int Y = 0;
+    static constexpr int H = RT * 32;
+    static constexpr int PP = H + RT;
+    static constexpr int U = PP + RT * K * 32;
+    static constexpr int SIZE = U + (DIAG ? RT * 32 : 0);          // double2 per stage
+    static constexpr int DEPTH = tb2_depth(K, DIAG);
+    static constexpr int WARP = SIZE * DEPTH;                        // double2 per warp
+};
+
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // Temporally blocked pass over a contiguous range [cbeg, cend) of (band, chunk) work items in
 // band-major order (chunk = RT rows of a 60-column band).  A warp marches down its rows with
 // register windows: y_{m-1} rows [i0, i0+RT+4), y_m rows [i0-1, i0+RT+2), u rows [i0, i0+RT+2);
-// per chunk it loads RT new rows of y_{m-1} (and u), forms RT new rows of y_m (one row of the
-// halo recomputation per RT rows happens only at a strip start) and writes RT rows of y_{m+1}
-// and p_{m+1}.  Lanes 1..30 own the band's 60 output columns; lanes 0 and 31 carry halo columns.
-// Requires n_loc >= 16, n1 >= 64 (single wrap of every index; host-checked).
-template <int K, int RT, bool DIAG, bool FIRST, bool TWO>
+// per chunk it consumes RT new rows of y_{m-1} (and p, u) staged DEPTH-1 chunks ahead by
+// cp.async, forms RT new rows of y_m (the 3-row halo recomputation happens only at a strip start)
+// and writes RT rows of y_{m+1} and p_{m+1}.  Lanes 1..30 own the band's 60 output columns;
+// lanes 0 and 31 carry halo columns.  Requires n_loc >= 16, n1 >= 64 (host-checked).
+template <int K, bool DIAG, bool FIRST, bool TWO>
 __device__ __forceinline__ void strip2d_tb2(const LejaParams& P, const double* __restrict__ src,
                                             double* __restrict__ dst, int cbeg, int cend, int lane, double alpha,
                                             double b1, double b2, const double* d0, const double* da,
                                             const double* db, int active, int rbmask, const double* rbd,
-                                            double* acc) {
+                                            double* acc, double2* __restrict__ ring) {
+    using L = Tb2Stage<K, DIAG>;
+    constexpr int RT = L::RT, D = L::DEPTH;
     const int n1 = P.n1, n = P.n_loc, nc = P.nrb;
     const Stencil& S = P.st;
     auto wrap = [n](int r) { return r < 0 ? r + n : (r >= n ? r - n : r); };
-    auto LD = [](const double* q) { return FIRST ? ldg2(q) : ld2(q); };
+    auto colw = [n1](int c) { return c < 0 ? c + n1 : (c >= n1 ? c - n1 : c); };
     constexpr int KK = K > 0 ? K : 1;
+    // stage the global rows of chunk ci into ring stage st (every lane: its own 16-byte pieces)
+    auto issue = [&](int ci, int st) {
+        const int b = ci / nc;
+        const int i0 = (ci - b * nc) * RT;
+        const int jraw = b * kBand2 - 2 + 2 * lane;
+        const int j = colw(jraw);
+        double2* sg = ring + st * L::SIZE;
+#pragma unroll
+        for (int q = 0; q < RT; q++) {
+            cp_async16(sg + L::Y + q * 32 + lane, src + (size_t)wrap(i0 + 4 + q) * n1 + j);
+            if (lane == 31) cp_async16(sg + L::H + q, src + (size_t)wrap(i0 + 2 + q) * n1 + colw(jraw + 2));
+            if (DIAG) cp_async16(sg + L::U + q * 32 + lane, P.u + (size_t)wrap(i0 + 2 + q) * n1 + j);
+        }
+#pragma unroll
+        for (int t = 0; t < RT; t++) {
+#pragma unroll
+            for (int k = 0; k < KK; k++) {
+                const bool need = ((active >> k) & 1) ? !FIRST : (K > 1 && ((rbmask >> k) & 1));
+                if (need) cp_async16(sg + L::PP + (t * K + k) * 32 + lane, P.p[k] + (size_t)wrap(i0 + t) * n1 + j);
+            }
+        }
+    };
     double2 aw[RT + 4], yw[RT + 3], uw[RT + 2];
     const double2 z2 = make_double2(0.0, 0.0);
-    int ci = cbeg;
+    // prime the ring: chunks cbeg .. cbeg+D-2
+#pragma unroll
+    for (int d = 0; d < D - 1; d++) {
+        if (cbeg + d < cend) issue(cbeg + d, d);
+        cp_async_commit();
+    }
+    int ci = cbeg, st = 0;
 #pragma unroll 1
     while (ci < cend) {
         const int b = ci / nc;
         const int cseg = min(cend, (b + 1) * nc);   // this band's part of the range
         const int c0 = b * kBand2;
         const int jraw = c0 - 2 + 2 * lane;
-        const int j = jraw < 0 ? jraw + n1 : (jraw >= n1 ? jraw - n1 : jraw);
-        const int jh = jraw + 2 >= n1 ? jraw + 2 - n1 : jraw + 2;
+        const int j = colw(jraw);
+        const int jh = colw(jraw + 2);
         const bool outl = lane >= 1 && lane <= 30 && jraw < n1 && jraw < c0 + kBand2;
         {
+            // strip start: y_{m-1} rows i0-2 .. i0+3 (direct loads), y_m rows i0-1 .. i0+1
             const int i0 = (ci - b * nc) * RT;
-            // y_{m-1} rows i0-2 .. i0+3, y_m rows i0-1 .. i0+1
             double2 t6[6], h3[3], u3[3];
 #pragma unroll
-            for (int q = 0; q < 6; q++) t6[q] = LD(src + (size_t)wrap(i0 - 2 + q) * n1 + j);
+            for (int q = 0; q < 6; q++) t6[q] = ld2(src + (size_t)wrap(i0 - 2 + q) * n1 + j);
 #pragma unroll
             for (int q = 0; q < 3; q++) {
-                h3[q] = (lane == 31) ? LD(src + (size_t)wrap(i0 - 1 + q) * n1 + jh) : z2;
+                h3[q] = (lane == 31) ? ld2(src + (size_t)wrap(i0 - 1 + q) * n1 + jh) : z2;
                 u3[q] = DIAG ? ldg2(P.u + (size_t)wrap(i0 - 1 + q) * n1 + j) : z2;
             }
 #pragma unroll
@@ -1446,80 +1510,83 @@ __device__ __forceinline__ void strip2d_tb2(const LejaParams& P, const double* _
         }
 #pragma unroll 1
         for (int i0 = (ci - b * nc) * RT; ci < cseg; ci++, i0 += RT) {
-        const int nout = min(RT, n - i0);
-        double2 ah[RT];
-        double2 pv[RT][KK];
-#pragma unroll
-        for (int q = 0; q < RT; q++) {
-            aw[4 + q] = LD(src + (size_t)wrap(i0 + 4 + q) * n1 + j);
-            ah[q] = (lane == 31) ? LD(src + (size_t)wrap(i0 + 2 + q) * n1 + jh) : z2;
-            if (DIAG) uw[2 + q] = ldg2(P.u + (size_t)wrap(i0 + 2 + q) * n1 + j);
-        }
-#pragma unroll
-        for (int t = 0; t < RT; t++) {
-#pragma unroll
-            for (int k = 0; k < KK; k++) {
-                pv[t][k] = z2;
-                const bool need = ((active >> k) & 1) ? !FIRST : (K > 1 && ((rbmask >> k) & 1));
-                if (outl && t < nout && need) pv[t][k] = ld2(P.p[k] + (size_t)(i0 + t) * n1 + j);
+            // keep D-1 chunks in flight: stage chunk ci+D-1, then wait for chunk ci's group
+            {
+                int sn = st + D - 1;
+                if (sn >= D) sn -= D;
+                if (ci + D - 1 < cend) issue(ci + D - 1, sn);
+                cp_async_commit();
+                cp_async_wait<D - 1>();
             }
-        }
-        // step 1: y_m rows i0+2 .. i0+RT+1
+            const double2* sg = ring + st * L::SIZE;
+            if (++st == D) st = 0;
+            const int nout = min(RT, n - i0);
+            double2 ah[RT];
 #pragma unroll
-        for (int q = 0; q < RT; q++)
-            yw[3 + q] = leja_row<DIAG>(S, alpha, b1, aw[1 + q], aw[2 + q], aw[3 + q], aw[4 + q], ah[q],
-                                       DIAG ? uw[2 + q] : z2, lane);
-        // step 2: y_{m+1} on the output rows; p updates and norms
+            for (int q = 0; q < RT; q++) {
+                aw[4 + q] = sg[L::Y + q * 32 + lane];
+                ah[q] = (lane == 31) ? sg[L::H + q] : z2;
+                if (DIAG) uw[2 + q] = sg[L::U + q * 32 + lane];
+            }
+            // step 1: y_m rows i0+2 .. i0+RT+1
 #pragma unroll
-        for (int t = 0; t < RT; t++) {
-            if (t < nout) {
-                const double2 yc = yw[t + 1];
-                double2 zz = yc;
-                if (TWO) zz = leja_row<DIAG>(S, alpha, b2, yw[t], yc, yw[t + 2], yw[t + 3], z2, uw[t], lane);
-                if (outl) {
-                    const size_t off = (size_t)(i0 + t) * n1 + j;
-                    st2(dst + off, zz);
-                    acc[0] = fma(yc.y, yc.y, fma(yc.x, yc.x, acc[0]));
-                    if (TWO) acc[1 + K] = fma(zz.y, zz.y, fma(zz.x, zz.x, acc[1 + K]));
-                    const double2 yprev = aw[t];   // y_{m-1} (= v on the first pass)
+            for (int q = 0; q < RT; q++)
+                yw[3 + q] = leja_row<DIAG>(S, alpha, b1, aw[1 + q], aw[2 + q], aw[3 + q], aw[4 + q], ah[q],
+                                           DIAG ? uw[2 + q] : z2, lane);
+            // step 2: y_{m+1} on the output rows; p updates and norms
 #pragma unroll
-                    for (int k = 0; k < KK; k++) {
-                        if ((active >> k) & 1) {
-                            double2 pm;
-                            if (FIRST) {
-                                pm.x = fma(da[k], yc.x, d0[k] * yprev.x);
-                                pm.y = fma(da[k], yc.y, d0[k] * yprev.y);
-                            } else {
-                                pm.x = fma(da[k], yc.x, pv[t][k].x);
-                                pm.y = fma(da[k], yc.y, pv[t][k].y);
+            for (int t = 0; t < RT; t++) {
+                if (t < nout) {
+                    const double2 yc = yw[t + 1];
+                    double2 zz = yc;
+                    if (TWO) zz = leja_row<DIAG>(S, alpha, b2, yw[t], yc, yw[t + 2], yw[t + 3], z2, uw[t], lane);
+                    if (outl) {
+                        const size_t off = (size_t)(i0 + t) * n1 + j;
+                        st2(dst + off, zz);
+                        acc[0] = fma(yc.y, yc.y, fma(yc.x, yc.x, acc[0]));
+                        if (TWO) acc[1 + K] = fma(zz.y, zz.y, fma(zz.x, zz.x, acc[1 + K]));
+                        const double2 yprev = aw[t];   // y_{m-1} (= v on the first pass)
+#pragma unroll
+                        for (int k = 0; k < KK; k++) {
+                            if ((active >> k) & 1) {
+                                double2 pm;
+                                if (FIRST) {
+                                    pm.x = fma(da[k], yc.x, d0[k] * yprev.x);
+                                    pm.y = fma(da[k], yc.y, d0[k] * yprev.y);
+                                } else {
+                                    const double2 pv = sg[L::PP + (t * K + k) * 32 + lane];
+                                    pm.x = fma(da[k], yc.x, pv.x);
+                                    pm.y = fma(da[k], yc.y, pv.y);
+                                }
+                                acc[1 + k] = fma(pm.y, pm.y, fma(pm.x, pm.x, acc[1 + k]));
+                                double2 pn = pm;
+                                if (TWO) {
+                                    pn.x = fma(db[k], zz.x, pm.x);
+                                    pn.y = fma(db[k], zz.y, pm.y);
+                                    acc[2 + K + k] = fma(pn.y, pn.y, fma(pn.x, pn.x, acc[2 + K + k]));
+                                }
+                                st2(P.p[k] + off, pn);
+                            } else if (K > 1 && ((rbmask >> k) & 1)) {
+                                // roll back the speculative last update of the previous pass (K = 1: the
+                                // call ends at that decision -> final rollback pass instead)
+                                const double2 pv = sg[L::PP + (t * K + k) * 32 + lane];
+                                st2(P.p[k] + off, make_double2(fma(-rbd[k], yprev.x, pv.x),
+                                                               fma(-rbd[k], yprev.y, pv.y)));
                             }
-                            acc[1 + k] = fma(pm.y, pm.y, fma(pm.x, pm.x, acc[1 + k]));
-                            double2 pn = pm;
-                            if (TWO) {
-                                pn.x = fma(db[k], zz.x, pm.x);
-                                pn.y = fma(db[k], zz.y, pm.y);
-                                acc[2 + K + k] = fma(pn.y, pn.y, fma(pn.x, pn.x, acc[2 + K + k]));
-                            }
-                            st2(P.p[k] + off, pn);
-                        } else if (K > 1 && ((rbmask >> k) & 1)) {
-                            // roll back the speculative last update of the previous pass (K = 1: the
-                            // call ends at that decision -> final rollback pass instead)
-                            st2(P.p[k] + off, make_double2(fma(-rbd[k], yprev.x, pv[t][k].x),
-                                                           fma(-rbd[k], yprev.y, pv[t][k].y)));
                         }
                     }
                 }
             }
-        }
-        // advance the windows by RT rows
+            // advance the windows by RT rows
 #pragma unroll
-        for (int q = 0; q < 4; q++) aw[q] = aw[RT + q];
+            for (int q = 0; q < 4; q++) aw[q] = aw[RT + q];
 #pragma unroll
-        for (int q = 0; q < 3; q++) yw[q] = yw[RT + q];
+            for (int q = 0; q < 3; q++) yw[q] = yw[RT + q];
 #pragma unroll
-        for (int q = 0; q < 2; q++) uw[q] = uw[RT + q];
+            for (int q = 0; q < 2; q++) uw[q] = uw[RT + q];
         }
     }
+    cp_async_wait<0>();
 }
 
 // Final rollback pass: p_k -= rbd[k] * y (y = the last written y_{m+1}) on the strip's output points.
@@ -1567,10 +1634,17 @@ __device__ __forceinline__ void barrier_decide_tb2(const LejaParams& P, int m, b
         double acc[NV];
 #pragma unroll
         for (int i = 0; i < NV; i++) acc[i] = 0.0;
-        for (int c = tid; c < (int)gridDim.x; c += kThreads) {
-            const double* slot = P.partials + ((size_t)par * gridDim.x + c) * kSlot;
+        if (P.seg > 0) {
+            for (int g = tid; g < P.ngrp; g += kThreads) {
 #pragma unroll
-            for (int i = 0; i < NV; i++) acc[i] += __ldcg(slot + i);
+                for (int i = 0; i < NV; i++) acc[i] += __ldcg(P.grp_part + (size_t)g * NV + i);
+            }
+        } else {
+            for (int c = tid; c < (int)gridDim.x; c += kThreads) {
+                const double* slot = P.partials + ((size_t)par * gridDim.x + c) * kSlot;
+#pragma unroll
+                for (int i = 0; i < NV; i++) acc[i] += __ldcg(slot + i);
+            }
         }
         block_reduce<NV>(acc, s_red);
         if (tid == 0) {
@@ -1579,6 +1653,9 @@ __device__ __forceinline__ void barrier_decide_tb2(const LejaParams& P, int m, b
             const int rb = active & ~act;   // converged at the first iteration of the pass -> roll back
             if (!done && two) leja_decide<K>(P, m + 1, acc + 1 + K, db, act, done, status, P.rec);
             ctrl->arrive = 0u;
+            const int pass = (m - 1) >> 1;
+            ctrl->work[(pass + 1) & 1] = 0u;     // segment counter of the next pass
+            if (done) ctrl->work[pass & 1] = 0u;  // ... and of this one for the next call
             const unsigned long long w = ((unsigned long long)(gen0 + (unsigned)m) << 32) |
                                          ((unsigned long long)(status & 0xff) << 16) |
                                          ((unsigned long long)(rb & 0xf) << 12) |
@@ -1628,14 +1705,17 @@ __device__ __forceinline__ void coef_first5(const LejaParams& P, int k, double* 
 }
 
 template <int K, bool DIAG>
-__global__ void __launch_bounds__(kThreads, (K == 1 ? 2 : 1)) k_leja2d_tb2(const __grid_constant__ LejaParams P) {
+__global__ void __launch_bounds__(kThreads, 2) k_leja2d_tb2(const __grid_constant__ LejaParams P) {
     __shared__ double s_red[kWarps][kSlot];
+    extern __shared__ double2 tb2_ring[];
     __shared__ int s_flags[4];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool cwarp = (blockIdx.x == 0 && warp == 0);
     const int gw = blockIdx.x * kWarps + warp - 1;
     const int W = gridDim.x * kWarps - 1;
     constexpr int RT = tb2_rt(K);
+    constexpr int NV = 2 * (1 + K);
+    double2* ring = tb2_ring + (size_t)warp * Tb2Stage<K, DIAG>::WARP;
     const int cbeg = cwarp ? 0 : (int)((long long)gw * P.nunits / W);
     const int cend = cwarp ? 0 : (int)((long long)(gw + 1) * P.nunits / W);
     unsigned gen0 = 0;
@@ -1684,23 +1764,72 @@ __global__ void __launch_bounds__(kThreads, (K == 1 ? 2 : 1)) k_leja2d_tb2(const
             }
         } else {
             const double* src = (m == 1) ? P.v.base : P.ysrc[(pass & 1) ^ 1].base;
-            if (m == 1) {
-                if (two) strip2d_tb2<K, RT, DIAG, true, true>(P, src, dst, cbeg, cend, lane, alpha, b1, b2, d0, da, db,
-                                                             active, rbmask, rbd, acc);
-                else strip2d_tb2<K, RT, DIAG, true, false>(P, src, dst, cbeg, cend, lane, alpha, b1, b2, d0, da, db,
-                                                           active, rbmask, rbd, acc);
+            auto run = [&](int c_b, int c_e, double* acc) {
+                if (m == 1) {
+                    if (two) strip2d_tb2<K, DIAG, true, true>(P, src, dst, c_b, c_e, lane, alpha, b1, b2, d0, da, db,
+                                                             active, rbmask, rbd, acc, ring);
+                    else strip2d_tb2<K, DIAG, true, false>(P, src, dst, c_b, c_e, lane, alpha, b1, b2, d0, da, db,
+                                                           active, rbmask, rbd, acc, ring);
+                } else {
+                    if (two) strip2d_tb2<K, DIAG, false, true>(P, src, dst, c_b, c_e, lane, alpha, b1, b2, d0, da,
+                                                              db, active, rbmask, rbd, acc, ring);
+                    else strip2d_tb2<K, DIAG, false, false>(P, src, dst, c_b, c_e, lane, alpha, b1, b2, d0, da,
+                                                            db, active, rbmask, rbd, acc, ring);
+                }
+            };
+            if (P.seg > 0) {
+                // dynamic segments of P.seg chunks (balances the end-of-pass tail).  The norm partials
+                // stay deterministic: each segment's sums are formed by one warp in a fixed order and
+                // stored by segment index; the last finisher of each group of 32 segments sums the
+                // group in index order (fixed butterfly); the barrier sums the groups in order.
+                unsigned* ctr = &P.ctrl->work[pass & 1];
+#pragma unroll 1
+                for (;;) {
+                    int sg = 0;
+                    if (lane == 0) sg = (int)atomicAdd(ctr, 1u);
+                    sg = __shfl_sync(FULL_MASK, sg, 0);
+                    if (sg >= P.nseg) break;
+                    const int c_b = sg * P.seg;
+                    double sacc[NV];
+#pragma unroll
+                    for (int i = 0; i < NV; i++) sacc[i] = 0.0;
+                    run(c_b, min(P.nunits, c_b + P.seg), sacc);
+                    warp_sum<NV>(sacc);
+                    int last = 0;
+                    const int g = sg >> 5;
+                    if (lane == 0) {
+#pragma unroll
+                        for (int i = 0; i < NV; i++) P.seg_part[(size_t)sg * NV + i] = sacc[i];
+                        __threadfence();
+                        const unsigned t = atomicAdd(&P.grp_cnt[g], 1u);
+                        last = (int)(t == (unsigned)(min(32, P.nseg - g * 32) - 1));
+                    }
+                    last = __shfl_sync(FULL_MASK, last, 0);
+                    if (last) {
+                        __threadfence();
+                        const int s2 = g * 32 + lane;
+                        double gv[NV];
+#pragma unroll
+                        for (int i = 0; i < NV; i++) gv[i] = (s2 < P.nseg) ? __ldcg(P.seg_part + (size_t)s2 * NV + i) : 0.0;
+                        warp_sum<NV>(gv);
+                        if (lane == 0) {
+#pragma unroll
+                            for (int i = 0; i < NV; i++) P.grp_part[(size_t)g * NV + i] = gv[i];
+                            P.grp_cnt[g] = 0u;
+                        }
+                    }
+                }
             } else {
-                if (two) strip2d_tb2<K, RT, DIAG, false, true>(P, src, dst, cbeg, cend, lane, alpha, b1, b2, d0, da,
-                                                              db, active, rbmask, rbd, acc);
-                else strip2d_tb2<K, RT, DIAG, false, false>(P, src, dst, cbeg, cend, lane, alpha, b1, b2, d0, da, db,
-                                                            active, rbmask, rbd, acc);
+                run(cbeg, cend, acc);
             }
         }
-        block_reduce<2 * (1 + K)>(acc, s_red);
-        if (tid == 0) {
-            double* slot = P.partials + ((size_t)(pass & 1) * gridDim.x + blockIdx.x) * kSlot;
+        if (P.seg == 0) {
+            block_reduce<2 * (1 + K)>(acc, s_red);
+            if (tid == 0) {
+                double* slot = P.partials + ((size_t)(pass & 1) * gridDim.x + blockIdx.x) * kSlot;
 #pragma unroll
-            for (int i = 0; i < 2 * (1 + K); i++) slot[i] = acc[i];
+                for (int i = 0; i < 2 * (1 + K); i++) slot[i] = acc[i];
+            }
         }
         barrier_decide_tb2<K>(P, m, two, gen0, da, db, active, s_red, s_flags);
         active = s_flags[2];
@@ -1993,8 +2122,27 @@ static void* leja_tb2_ptr(int K, bool diag) {
     return nullptr;
 }
 
+static int tb2_prepare(int device, int K, bool diag) {
+    // dynamic shared memory opt-in (once per kernel) + co-resident CTAs with that smem, cached
+    static std::mutex mu;
+    static std::map<std::pair<int, int>, int> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    const int key = K * 2 + (diag ? 1 : 0);
+    auto it = cache.find({device, key});
+    if (it != cache.end()) return it->second;
+    const void* kern = leja_tb2_ptr(K, diag);
+    const int smem = tb2_smem_bytes(K, diag);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int nsm = 0, per = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, smem);
+    if (per < 1) per = 1;
+    cache[{device, key}] = nsm * per;
+    return nsm * per;
+}
+
 int leja_tb2_grid_size(int device, int K, bool diag, int nunits) {
-    long long g = coresident(device, leja_tb2_ptr(K, diag));
+    long long g = tb2_prepare(device, K, diag);
     long long need = (nunits + kWarps - 1) / kWarps + 1;
     if (g > need) g = need;
     return (int)g;
@@ -2004,7 +2152,7 @@ cudaError_t launch_leja_tb2(const LejaParams& P, cudaStream_t s, bool diag) {
     void* kern = leja_tb2_ptr(P.K, diag);
     if (!kern) return cudaErrorInvalidValue;
     void* args[] = {(void*)&P};
-    return cudaLaunchCooperativeKernel(kern, dim3(P.grid), dim3(kThreads), args, 0, s);
+    return cudaLaunchCooperativeKernel(kern, dim3(P.grid), dim3(kThreads), args, tb2_smem_bytes(P.K, diag), s);
 }
 
 // ---------------------------------------------------------------------------

@@ -482,6 +482,7 @@ def test_burgers_leja_power_rhs_integrate(xi300):
                                              ((130, 122), 3, 1.0, 1), ((131, 182), 4, 0.0, 1),
                                              ((200, 60), 4, 1.0, 3), ((4096, 256), 1, 1.0, 0)])
 def test_tblock2_matches_oracle_and_one_step(xi300, monkeypatch, shape, K, react, l):
+    # (also: dynamic segments (LX_TB2_SEG=8, default) and static ranges (0) give bitwise-equal fields)
     # two Leja iterations per HBM pass: ragged 60-column bands (n1 = 62, 122,
     # 182, 24 < 64), odd row counts, K = 1..4 (accumulators converging at different m, i.e. on
     # either half of a pass -> rollback), with and without the diagonal term.  Same iteration
@@ -494,8 +495,9 @@ def test_tblock2_matches_oracle_and_one_step(xi300, monkeypatch, shape, K, react
     dt = 0.01 if react else 10 * min(W.dt_cfl(n, 10.0) for n in shape)
     coeffs = (0.25, 0.5, 0.75, 1.0)[-K:]
     res = {}
-    for tb in ("1", "2"):
-        monkeypatch.setenv("LX_TBLOCK", tb)
+    for tb, seg in (("1", "8"), ("2", "8"), ("2s", "0")):   # one-step; two-step dynamic / static segments
+        monkeypatch.setenv("LX_TBLOCK", tb[0])
+        monkeypatch.setenv("LX_TB2_SEG", seg)
         with lx.Context(pb) as ctx:
             ud = _dev(u) if react else None
             c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx, ud))
@@ -503,8 +505,30 @@ def test_tblock2_matches_oracle_and_one_step(xi300, monkeypatch, shape, K, react
             it = lx.lx_real_leja_phi_vertical(ctx, _dev(v), outs, coeffs, dt, c, g, l, TOL, TOL, u_lin=ud)
             res[tb] = (it, [o.cpu().numpy() for o in outs])
     r = O.real_leja_phi(ob, v, dt, c, g, l, TOL, TOL, xi300, coeffs=coeffs, u_lin=u)
-    assert res["2"][0] == res["1"][0] == r.iters
-    for a, b, ref in zip(res["2"][1], res["1"][1], r.outs):
+    assert res["2"][0] == res["2s"][0] == res["1"][0] == r.iters
+    for a, s_, b, ref in zip(res["2"][1], res["2s"][1], res["1"][1], r.outs):
+        np.testing.assert_array_equal(a, s_)   # work partition does not change any point's arithmetic
         assert np.isfinite(a).all()
         np.testing.assert_allclose(a, b, rtol=0, atol=8 * np.finfo(float).eps * np.abs(b).max())
         assert np.linalg.norm(a - ref) <= TOL * np.linalg.norm(ref)
+
+
+def test_tblock2_dynamic_segments_reproducible(xi300):
+    # dynamic work assignment (atomic segment counter) must not leak into the results: per-segment
+    # norm partials are reduced in segment order -> identical iterations and bitwise-equal outputs
+    # over repeated calls, at a size with thousands of segments (n = 1536: 26 bands x 384 chunks)
+    n = 1536
+    pb, _ = _pair((n, n))
+    u0 = _dev(W.ic_random((n, n), seed=5, amp=0.3))
+    dt = 10 * W.dt_cfl(n, 10.0)
+    with lx.Context(pb) as ctx:
+        c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+        runs = []
+        for _ in range(4):
+            outs = [torch.empty_like(u0) for _ in range(2)]
+            it = lx.lx_real_leja_phi_vertical(ctx, u0, outs, (0.5, 1.0), dt, c, g, 1, TOL, TOL)
+            runs.append((it, outs))
+    for it, outs in runs[1:]:
+        assert it == runs[0][0]
+        for a, b in zip(outs, runs[0][1]):
+            assert torch.equal(a, b)

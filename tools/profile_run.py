@@ -4,6 +4,7 @@
   python tools/profile_run.py leja2d 4096 0      # phi_0 Leja call, 2D
   python tools/profile_run.py leja3d 512 0       # phi_0 Leja call, 3D
   python tools/profile_run.py ac 2048 2          # Allen-Cahn EXPRB43, 2 steps
+  python tools/profile_run.py step 4096 0        # bench step (phi_0..phi_3), warm-up + 1
   python tools/profile_run.py aci 2048 2         # the same through lx_integrate
 """
 import os
@@ -52,6 +53,16 @@ def main():
             it, err = lx.lx_step(ctx, "exprb43", u, lo, hi, wl.dt, c, g, wl.rtol, wl.atol)
             u, hi = hi, u
             print("iters", it, "err", err)
+    elif what == "step":   # one bench step after a warm-up step: phi_0..phi_3 at n^2 (config 1)
+        wl = W.config(1, n=n)
+        u = torch.from_numpy(W.ic_problem1_2d(n)).cuda()
+        pb = lx.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
+        ctx = lx.Context(pb)
+        c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+        outs = [torch.empty_like(u) for _ in range(4)]
+        for _ in range(reps):
+            its = [lx.lx_real_leja_phi(ctx, u, outs[l], wl.dt, c, g, l, wl.rtol, wl.atol) for l in range(4)]
+        print("iters", its)
     elif what == "aci":   # the same through lx_integrate (device-side spectrum)
         wl = W.config(2, n=n)
         pb = lx.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
