@@ -22,7 +22,8 @@ from typing import Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "liblexint_b200.so")
+# LX_LIBRARY: load another build of the same library (A/B performance experiments only)
+LIB_PATH = os.environ.get("LX_LIBRARY") or os.path.join(_PKG, "liblexint_b200.so")
 
 LX_OK, LX_ERR_ARG, LX_ERR_DIM, LX_ERR_ALIAS, LX_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 LX_ERR_NOCONV, LX_ERR_NONFINITE, LX_ERR_UNKNOWN_INTEGRATOR, LX_ERR_CUDA, LX_ERR_NCCL = 5, 6, 7, 8, 9

@@ -88,7 +88,9 @@ struct lx_ctx {
     Comm* comm = nullptr;                 // slab decomposition (lx_comm.cpp)
     int variant = 0;                      // 2D single-GPU Leja kernel: 0 = register tiles, 1 = TMA marching
     int tblock = 2;                       // 2D single-GPU: Leja iterations per HBM pass (1 or 2; LX_TBLOCK)
-    int tb2_seg = 8;                      // two-step kernel: dynamic segment length in chunks (LX_TB2_SEG; 0 static)
+    int tb2_seg = -1;                     // two-step kernel: max segment length in chunks (LX_TB2_SEG; 0 static
+                                          // ranges; default 32 rows)
+    int tb2_order = 1;                    // two-step kernel: segment order (LX_TB2_ORDER)
     int tb2_cap = 0;                      // segments the buffers below can hold
     double* tb2_seg_part = nullptr;       // [cap][2(1+kMaxK)]
     double* tb2_grp_part = nullptr;       // [cap/32+1][2(1+kMaxK)]
@@ -340,9 +342,14 @@ static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u,
         P.nrb = (P.n_loc + tb2_rt(K) - 1) / tb2_rt(K);
         P.nunits = P.nb * P.nrb;
         P.grid = leja_tb2_grid_size(ctx->device, K, diag, P.nunits);
-        P.seg = ctx->tb2_seg;
-        if (P.seg > 0) {
+        P.seg = ctx->tb2_seg < 0 ? 32 / tb2_rt(K) : ctx->tb2_seg;   // default: 32-row segments
+        P.order = ctx->tb2_order;
+        if (P.seg > 0 && P.order) {
+            P.nseg = P.nb * ((P.nrb + P.seg - 1) / P.seg);
+        } else if (P.seg > 0) {
             P.nseg = (P.nunits + P.seg - 1) / P.seg;
+        }
+        if (P.seg > 0) {
             P.ngrp = (P.nseg + 31) / 32;
             if (P.nseg > ctx->tb2_cap) {
                 cudaFree(ctx->tb2_seg_part);
@@ -517,6 +524,7 @@ lx_status lx_ctx_create(const lx_problem* pb, int max_nodes, int device, void* c
     ctx->max_nodes = max_nodes;
     if (const char* ev = std::getenv("LX_LEJA_KERNEL")) ctx->variant = (std::strcmp(ev, "tma") == 0) ? 1 : 0;
     if (const char* ev = std::getenv("LX_TBLOCK")) ctx->tblock = (std::atoi(ev) == 1) ? 1 : 2;
+    if (const char* ev = std::getenv("LX_TB2_ORDER")) ctx->tb2_order = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("LX_TB2_SEG")) ctx->tb2_seg = std::atoi(ev) > 0 ? std::atoi(ev) : 0;
     if (const char* ev = std::getenv("LX_COEF")) ctx->coef_table = (std::strcmp(ev, "table") == 0);
     cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device);
@@ -545,13 +553,18 @@ lx_status lx_ctx_create(const lx_problem* pb, int max_nodes, int device, void* c
     for (auto& ev : ctx->coef_ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     CK(cudaMalloc(&ctx->cg_dev, 4 * sizeof(double)));
     CK(cudaMalloc(&ctx->xi_dev, max_nodes * sizeof(double)));
-    CK(cudaMemcpy(ctx->xi_dev, ctx->xi.data(), max_nodes * sizeof(double), cudaMemcpyHostToDevice));
+    // stream-ordered uploads: the context's stream may be non-blocking, and a pageable cudaMemcpy
+    // may return before its DMA lands
+    CK(cudaMemcpyAsync(ctx->xi_dev, ctx->xi.data(), max_nodes * sizeof(double), cudaMemcpyHostToDevice,
+                       ctx->stream));
     {
         std::vector<double> R((size_t)max_nodes * max_nodes, 0.0);
         for (int i = 0; i < max_nodes; i++)
             for (int j = i + 1; j < max_nodes; j++) R[(size_t)i * max_nodes + j] = 1.0 / (ctx->xi[j] - ctx->xi[i]);
         CK(cudaMalloc(&ctx->rcp_dev, R.size() * sizeof(double)));
-        CK(cudaMemcpy(ctx->rcp_dev, R.data(), R.size() * sizeof(double), cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(ctx->rcp_dev, R.data(), R.size() * sizeof(double), cudaMemcpyHostToDevice,
+                           ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));   // R is a local buffer
     }
 #undef CK
     s = alloc_local(ctx);

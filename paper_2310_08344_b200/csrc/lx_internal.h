@@ -127,6 +127,7 @@ struct LejaParams {
     // two-step kernel, dynamic segments of `seg` chunks (0 = static ranges): per-segment norm partials,
     // reduced in fixed order per group of 32 segments by the group's last finisher, then over groups
     int seg;
+    int order;            // 0: segments band-major (vertical strips); 1: band fastest (row-major)
     int nseg, ngrp;
     double* seg_part;     // [nseg][2(1+K)]
     double* grp_part;     // [ngrp][2(1+K)]

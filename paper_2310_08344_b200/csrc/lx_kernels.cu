@@ -1789,11 +1789,19 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d_tb2(const __grid_constan
                     if (lane == 0) sg = (int)atomicAdd(ctr, 1u);
                     sg = __shfl_sync(FULL_MASK, sg, 0);
                     if (sg >= P.nseg) break;
-                    const int c_b = sg * P.seg;
+                    int c_b, c_e;
+                    if (P.order) {   // band fastest: adjacent bands of the same rows run together
+                        const int rs = sg / P.nb, b = sg - rs * P.nb;
+                        c_b = b * P.nrb + rs * P.seg;
+                        c_e = b * P.nrb + min(P.nrb, rs * P.seg + P.seg);
+                    } else {
+                        c_b = sg * P.seg;
+                        c_e = min(P.nunits, c_b + P.seg);
+                    }
                     double sacc[NV];
 #pragma unroll
                     for (int i = 0; i < NV; i++) sacc[i] = 0.0;
-                    run(c_b, min(P.nunits, c_b + P.seg), sacc);
+                    run(c_b, c_e, sacc);
                     warp_sum<NV>(sacc);
                     int last = 0;
                     const int g = sg >> 5;
