@@ -47,6 +47,14 @@ __device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long l
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+// spin-wait read: relaxed (no L1 invalidation per poll); the waiter issues one fence_acquire() after
+// it has seen the released value (relaxed load + fence.acq_rel = acquire pattern)
+__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void st_release64(unsigned long long* p, unsigned long long v) {
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -804,7 +812,7 @@ __device__ __forceinline__ void barrier_decide(const LejaParams& P, int m, unsig
             s_red[0][kSlot - 1] = scale;
         }
     } else if (tid == 0) {
-        unsigned long long w = ld_acquire64(&ctrl->word);
+        unsigned long long w = ld_relaxed64(&ctrl->word);
         int spins = 0;
         while ((int)((unsigned)(w >> 32) - gen0) < m) {
             if (++spins > 32) __nanosleep(32);
@@ -813,8 +821,9 @@ __device__ __forceinline__ void barrier_decide(const LejaParams& P, int m, unsig
                 w = (1ull << 8);
                 break;
             }
-            w = ld_acquire64(&ctrl->word);
+            w = ld_relaxed64(&ctrl->word);
         }
+        fence_acquire();
         s_flags[1] = (int)((w >> 8) & 0xff);
         s_flags[2] = (int)(w & 0xff);
         if (MODE == M_POWER) s_red[0][kSlot - 1] = *(volatile double*)&ctrl->scale;
@@ -1425,9 +1434,46 @@ struct Tb2Stage {
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
 }
+__device__ __forceinline__ double2 lds2(uint32_t addr) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+    return v;
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// stage the global rows of chunk ci into ring stage st (every lane: its own 16-byte pieces)
+template <int K, bool DIAG, bool FIRST>
+__device__ __forceinline__ void tb2_issue(const LejaParams& P, const double* __restrict__ src,
+                                          double2* __restrict__ ring, int ci, int st, int lane, int active,
+                                          int rbmask) {
+    using L = Tb2Stage<K, DIAG>;
+    constexpr int RT = L::RT;
+    constexpr int KK = K > 0 ? K : 1;
+    const int n1 = P.n1, n = P.n_loc, nc = P.nrb;
+    auto wrap = [n](int r) { return r < 0 ? r + n : (r >= n ? r - n : r); };
+    auto colw = [n1](int c) { return c < 0 ? c + n1 : (c >= n1 ? c - n1 : c); };
+    const int b = ci / nc;
+    const int i0 = (ci - b * nc) * RT;
+    const int jraw = b * kBand2 - 2 + 2 * lane;
+    const int j = colw(jraw);
+    double2* sg = ring + st * L::SIZE;
+#pragma unroll
+    for (int q = 0; q < RT; q++) {
+        cp_async16(sg + L::Y + q * 32 + lane, src + (size_t)wrap(i0 + 4 + q) * n1 + j);
+        if (lane == 31) cp_async16(sg + L::H + q, src + (size_t)wrap(i0 + 2 + q) * n1 + colw(jraw + 2));
+        if (DIAG) cp_async16(sg + L::U + q * 32 + lane, P.u + (size_t)wrap(i0 + 2 + q) * n1 + j);
+    }
+#pragma unroll
+    for (int t = 0; t < RT; t++) {
+#pragma unroll
+        for (int k = 0; k < KK; k++) {
+            const bool need = ((active >> k) & 1) ? !FIRST : (K > 1 && ((rbmask >> k) & 1));
+            if (need) cp_async16(sg + L::PP + (t * K + k) * 32 + lane, P.p[k] + (size_t)wrap(i0 + t) * n1 + j);
+        }
+    }
+}
 
 // Temporally blocked pass over a contiguous range [cbeg, cend) of (band, chunk) work items in
 // band-major order (chunk = RT rows of a 60-column band).  A warp marches down its rows with
@@ -1441,7 +1487,7 @@ __device__ __forceinline__ void strip2d_tb2(const LejaParams& P, const double* _
                                             double* __restrict__ dst, int cbeg, int cend, int lane, double alpha,
                                             double b1, double b2, const double* d0, const double* da,
                                             const double* db, int active, int rbmask, const double* rbd,
-                                            double* acc, double2* __restrict__ ring) {
+                                            double (&acc)[2 * (1 + K)], double2* __restrict__ ring) {
     using L = Tb2Stage<K, DIAG>;
     constexpr int RT = L::RT, D = L::DEPTH;
     const int n1 = P.n1, n = P.n_loc, nc = P.nrb;
@@ -1449,34 +1495,12 @@ __device__ __forceinline__ void strip2d_tb2(const LejaParams& P, const double* _
     auto wrap = [n](int r) { return r < 0 ? r + n : (r >= n ? r - n : r); };
     auto colw = [n1](int c) { return c < 0 ? c + n1 : (c >= n1 ? c - n1 : c); };
     constexpr int KK = K > 0 ? K : 1;
-    // stage the global rows of chunk ci into ring stage st (every lane: its own 16-byte pieces)
-    auto issue = [&](int ci, int st) {
-        const int b = ci / nc;
-        const int i0 = (ci - b * nc) * RT;
-        const int jraw = b * kBand2 - 2 + 2 * lane;
-        const int j = colw(jraw);
-        double2* sg = ring + st * L::SIZE;
-#pragma unroll
-        for (int q = 0; q < RT; q++) {
-            cp_async16(sg + L::Y + q * 32 + lane, src + (size_t)wrap(i0 + 4 + q) * n1 + j);
-            if (lane == 31) cp_async16(sg + L::H + q, src + (size_t)wrap(i0 + 2 + q) * n1 + colw(jraw + 2));
-            if (DIAG) cp_async16(sg + L::U + q * 32 + lane, P.u + (size_t)wrap(i0 + 2 + q) * n1 + j);
-        }
-#pragma unroll
-        for (int t = 0; t < RT; t++) {
-#pragma unroll
-            for (int k = 0; k < KK; k++) {
-                const bool need = ((active >> k) & 1) ? !FIRST : (K > 1 && ((rbmask >> k) & 1));
-                if (need) cp_async16(sg + L::PP + (t * K + k) * 32 + lane, P.p[k] + (size_t)wrap(i0 + t) * n1 + j);
-            }
-        }
-    };
     double2 aw[RT + 4], yw[RT + 3], uw[RT + 2];
     const double2 z2 = make_double2(0.0, 0.0);
     // prime the ring: chunks cbeg .. cbeg+D-2
 #pragma unroll
     for (int d = 0; d < D - 1; d++) {
-        if (cbeg + d < cend) issue(cbeg + d, d);
+        if (cbeg + d < cend) tb2_issue<K, DIAG, FIRST>(P, src, ring, cbeg + d, d, lane, active, rbmask);
         cp_async_commit();
     }
     int ci = cbeg, st = 0;
@@ -1514,19 +1538,21 @@ __device__ __forceinline__ void strip2d_tb2(const LejaParams& P, const double* _
             {
                 int sn = st + D - 1;
                 if (sn >= D) sn -= D;
-                if (ci + D - 1 < cend) issue(ci + D - 1, sn);
+                if (ci + D - 1 < cend) tb2_issue<K, DIAG, FIRST>(P, src, ring, ci + D - 1, sn, lane, active, rbmask);
                 cp_async_commit();
                 cp_async_wait<D - 1>();
             }
-            const double2* sg = ring + st * L::SIZE;
+            // shared-space loads (ld.shared, not generic): 32-bit address of this stage
+            const uint32_t sgb = smem_u32(ring) + (uint32_t)(st * L::SIZE) * 16u;
+            auto sg = [sgb](int i) { return lds2(sgb + (uint32_t)i * 16u); };
             if (++st == D) st = 0;
             const int nout = min(RT, n - i0);
             double2 ah[RT];
 #pragma unroll
             for (int q = 0; q < RT; q++) {
-                aw[4 + q] = sg[L::Y + q * 32 + lane];
-                ah[q] = (lane == 31) ? sg[L::H + q] : z2;
-                if (DIAG) uw[2 + q] = sg[L::U + q * 32 + lane];
+                aw[4 + q] = sg(L::Y + q * 32 + lane);
+                ah[q] = (lane == 31) ? sg(L::H + q) : z2;
+                if (DIAG) uw[2 + q] = sg(L::U + q * 32 + lane);
             }
             // step 1: y_m rows i0+2 .. i0+RT+1
 #pragma unroll
@@ -1554,7 +1580,7 @@ __device__ __forceinline__ void strip2d_tb2(const LejaParams& P, const double* _
                                     pm.x = fma(da[k], yc.x, d0[k] * yprev.x);
                                     pm.y = fma(da[k], yc.y, d0[k] * yprev.y);
                                 } else {
-                                    const double2 pv = sg[L::PP + (t * K + k) * 32 + lane];
+                                    const double2 pv = sg(L::PP + (t * K + k) * 32 + lane);
                                     pm.x = fma(da[k], yc.x, pv.x);
                                     pm.y = fma(da[k], yc.y, pv.y);
                                 }
@@ -1569,7 +1595,7 @@ __device__ __forceinline__ void strip2d_tb2(const LejaParams& P, const double* _
                             } else if (K > 1 && ((rbmask >> k) & 1)) {
                                 // roll back the speculative last update of the previous pass (K = 1: the
                                 // call ends at that decision -> final rollback pass instead)
-                                const double2 pv = sg[L::PP + (t * K + k) * 32 + lane];
+                                const double2 pv = sg(L::PP + (t * K + k) * 32 + lane);
                                 st2(P.p[k] + off, make_double2(fma(-rbd[k], yprev.x, pv.x),
                                                                fma(-rbd[k], yprev.y, pv.y)));
                             }
@@ -1587,6 +1613,26 @@ __device__ __forceinline__ void strip2d_tb2(const LejaParams& P, const double* _
         }
     }
     cp_async_wait<0>();
+}
+
+// the four (first pass, two iterations) instantiations of strip2d_tb2
+template <int K, bool DIAG>
+__device__ __forceinline__ void tb2_strip(const LejaParams& P, bool first, bool two, const double* __restrict__ src,
+                                          double* __restrict__ dst, int c_b, int c_e, int lane, double alpha,
+                                          double b1, double b2, const double* d0, const double* da, const double* db,
+                                          int active, int rbmask, const double* rbd, double (&acc)[2 * (1 + K)],
+                                          double2* __restrict__ ring) {
+    if (first) {
+        if (two) strip2d_tb2<K, DIAG, true, true>(P, src, dst, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active,
+                                                 rbmask, rbd, acc, ring);
+        else strip2d_tb2<K, DIAG, true, false>(P, src, dst, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active,
+                                               rbmask, rbd, acc, ring);
+    } else {
+        if (two) strip2d_tb2<K, DIAG, false, true>(P, src, dst, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active,
+                                                  rbmask, rbd, acc, ring);
+        else strip2d_tb2<K, DIAG, false, false>(P, src, dst, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active,
+                                                rbmask, rbd, acc, ring);
+    }
 }
 
 // Final rollback pass: p_k -= rbd[k] * y (y = the last written y_{m+1}) on the strip's output points.
@@ -1666,7 +1712,7 @@ __device__ __forceinline__ void barrier_decide_tb2(const LejaParams& P, int m, b
             s_flags[3] = two ? rb : 0;
         }
     } else if (tid == 0) {
-        unsigned long long w = ld_acquire64(&ctrl->word);
+        unsigned long long w = ld_relaxed64(&ctrl->word);
         int spins = 0;
         while ((int)((unsigned)(w >> 32) - gen0) < m) {
             if (++spins > 32) __nanosleep(32);
@@ -1675,8 +1721,9 @@ __device__ __forceinline__ void barrier_decide_tb2(const LejaParams& P, int m, b
                 w = (1ull << 8);
                 break;
             }
-            w = ld_acquire64(&ctrl->word);
+            w = ld_relaxed64(&ctrl->word);
         }
+        fence_acquire();
         s_flags[1] = (int)((w >> 8) & 0xf);
         s_flags[2] = (int)(w & 0xff);
         s_flags[3] = two ? (int)((w >> 12) & 0xf) : 0;
@@ -1764,19 +1811,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d_tb2(const __grid_constan
             }
         } else {
             const double* src = (m == 1) ? P.v.base : P.ysrc[(pass & 1) ^ 1].base;
-            auto run = [&](int c_b, int c_e, double* acc) {
-                if (m == 1) {
-                    if (two) strip2d_tb2<K, DIAG, true, true>(P, src, dst, c_b, c_e, lane, alpha, b1, b2, d0, da, db,
-                                                             active, rbmask, rbd, acc, ring);
-                    else strip2d_tb2<K, DIAG, true, false>(P, src, dst, c_b, c_e, lane, alpha, b1, b2, d0, da, db,
-                                                           active, rbmask, rbd, acc, ring);
-                } else {
-                    if (two) strip2d_tb2<K, DIAG, false, true>(P, src, dst, c_b, c_e, lane, alpha, b1, b2, d0, da,
-                                                              db, active, rbmask, rbd, acc, ring);
-                    else strip2d_tb2<K, DIAG, false, false>(P, src, dst, c_b, c_e, lane, alpha, b1, b2, d0, da,
-                                                            db, active, rbmask, rbd, acc, ring);
-                }
-            };
             if (P.seg > 0) {
                 // dynamic segments of P.seg chunks (balances the end-of-pass tail).  The norm partials
                 // stay deterministic: each segment's sums are formed by one warp in a fixed order and
@@ -1798,10 +1832,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d_tb2(const __grid_constan
                         c_b = sg * P.seg;
                         c_e = min(P.nunits, c_b + P.seg);
                     }
+#pragma unroll
+                    for (int i = 0; i < NV; i++) acc[i] = 0.0;
+                    tb2_strip<K, DIAG>(P, m == 1, two, src, dst, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active,
+                                       rbmask, rbd, acc, ring);
                     double sacc[NV];
 #pragma unroll
-                    for (int i = 0; i < NV; i++) sacc[i] = 0.0;
-                    run(c_b, c_e, sacc);
+                    for (int i = 0; i < NV; i++) sacc[i] = acc[i];
                     warp_sum<NV>(sacc);
                     int last = 0;
                     const int g = sg >> 5;
@@ -1828,7 +1865,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d_tb2(const __grid_constan
                     }
                 }
             } else {
-                run(cbeg, cend, acc);
+                tb2_strip<K, DIAG>(P, m == 1, two, src, dst, cbeg, cend, lane, alpha, b1, b2, d0, da, db, active,
+                                   rbmask, rbd, acc, ring);
             }
         }
         if (P.seg == 0) {
