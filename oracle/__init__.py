@@ -25,6 +25,7 @@ _LIB = os.path.join(_HERE, "liblxoracle.so")
 
 OK, ERR_ARG, ERR_UNSUPPORTED, ERR_NOCONV, ERR_NONFINITE = 0, 1, 4, 5, 6
 METHODS = {"rosenbrock_euler": 0, "exprb32": 1, "exprb43": 2, "epirk4s3a": 3, "exprb42": 4}
+JAC = {"exact": 0, "fd": 1, "linear_f": 2}     # lxoracle.c OC_JAC_* (black-box RHS modes, reading R25)
 
 
 def ensure_built(force: bool = False) -> str:
@@ -69,6 +70,17 @@ def lib():
                                        ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
                                        ctypes.c_double, ctypes.c_double, dp, ctypes.c_int,
                                        ctypes.POINTER(ctypes.c_int), dp]
+        L.oc_real_leja_phi_ex.restype = ctypes.c_int
+        L.oc_real_leja_phi_ex.argtypes = [pp, ctypes.c_int, dp, dp, dp, ctypes.POINTER(dp), dp, ctypes.c_int,
+                                          ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                          ctypes.c_double, ctypes.c_double, dp, ctypes.c_int,
+                                          ctypes.POINTER(ctypes.c_int), dp]
+        L.oc_jac_apply_fd.argtypes = [pp, dp, dp, dp, dp]
+        L.oc_nonlinear_remainder_fd.argtypes = [pp, dp, dp, dp, dp]
+        L.oc_step_ex.restype = ctypes.c_int
+        L.oc_step_ex.argtypes = [pp, ctypes.c_int, ctypes.c_int, dp, dp, dp, dp, ctypes.c_double,
+                                 ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, dp,
+                                 ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
         L.oc_step.restype = ctypes.c_int
         L.oc_step.argtypes = [pp, ctypes.c_int, dp, dp, dp, dp, ctypes.c_double, ctypes.c_double,
                               ctypes.c_double, ctypes.c_double, ctypes.c_double, dp, ctypes.c_int,
@@ -178,6 +190,26 @@ def jac_apply_slab(pb: Problem, n_loc: int, u_loc, y_ghosted) -> np.ndarray:
     return w.reshape((n_loc,) + tuple(pb.shape[1:]))
 
 
+def jac_apply_fd(pb: Problem, u, y, f_u=None) -> np.ndarray:
+    """J(u) y by forward differences of f (reading R25)."""
+    y = _vec(y, pb)
+    u = _vec(u, pb)
+    f_u = rhs(pb, u) if f_u is None else _vec(f_u, pb)
+    w = np.zeros_like(y)
+    lib().oc_jac_apply_fd(ctypes.byref(pb.c_struct()), _dp(u), _dp(f_u), _dp(y), _dp(w))
+    return w
+
+
+def nonlinear_remainder_fd(pb: Problem, u, x, f_u=None) -> np.ndarray:
+    """F(x) = f(x) - J_FD(u) x, literally (alg:exprb32 Nonlinear_remainder)."""
+    x = _vec(x, pb)
+    u = _vec(u, pb)
+    f_u = rhs(pb, u) if f_u is None else _vec(f_u, pb)
+    out = np.zeros_like(x)
+    lib().oc_nonlinear_remainder_fd(ctypes.byref(pb.c_struct()), _dp(u), _dp(f_u), _dp(x), _dp(out))
+    return out
+
+
 def nonlinear_remainder(pb: Problem, u, x) -> np.ndarray:
     x = _vec(x, pb)
     u = _vec(u, pb)
@@ -211,7 +243,10 @@ class LejaResult:
 
 
 def real_leja_phi(pb: Problem, v, dt, c, gamma, l, rtol, atol, xi, *, u_lin=None,
-                  coeffs: Sequence[float] = (1.0,), max_nodes: int | None = None) -> LejaResult:
+                  coeffs: Sequence[float] = (1.0,), max_nodes: int | None = None,
+                  jac: str = "exact") -> LejaResult:
+    """jac: "exact" (J(u_lin) exact), "fd" (J(u_lin) by differences of f),
+    "linear_f" (the operator is f itself: a linear black-box RHS)."""
     v = _vec(v, pb)
     u_lin = None if u_lin is None else _vec(u_lin, pb)
     xi = _vec(xi)
@@ -222,9 +257,9 @@ def real_leja_phi(pb: Problem, v, dt, c, gamma, l, rtol, atol, xi, *, u_lin=None
     cf = np.asarray(coeffs, dtype=np.float64)
     it = ctypes.c_int(0)
     mg = np.zeros(2)
-    s = lib().oc_real_leja_phi(ctypes.byref(pb.c_struct()), _dp(u_lin), _dp(v), optr, _dp(cf), K,
-                               float(dt), float(c), float(gamma), int(l), float(rtol), float(atol),
-                               _dp(xi), int(max_nodes), ctypes.byref(it), _dp(mg))
+    s = lib().oc_real_leja_phi_ex(ctypes.byref(pb.c_struct()), JAC[jac], _dp(u_lin), _dp(None), _dp(v), optr,
+                                  _dp(cf), K, float(dt), float(c), float(gamma), int(l), float(rtol),
+                                  float(atol), _dp(xi), int(max_nodes), ctypes.byref(it), _dp(mg))
     return LejaResult(outs, it.value, s, (float(mg[0]), float(mg[1])))
 
 
@@ -237,14 +272,17 @@ class StepResult:
     status: int
 
 
-def step(pb: Problem, method: str, u, dt, c, gamma, rtol, atol, xi, max_nodes=None) -> StepResult:
+def step(pb: Problem, method: str, u, dt, c, gamma, rtol, atol, xi, max_nodes=None,
+         jac: str = "exact") -> StepResult:
+    """jac: "exact" (exact J, analytic remainders R18) or "fd" (black-box f: J and the
+    remainders F(x) = f(x) - J(u)x by finite differences)."""
     u = _vec(u, pb)
     xi = _vec(xi)
     max_nodes = len(xi) if max_nodes is None else max_nodes
     lo, hi = np.zeros_like(u), np.zeros_like(u)
     err = np.zeros(1)
     it = ctypes.c_int(0)
-    s = lib().oc_step(ctypes.byref(pb.c_struct()), METHODS[method], _dp(u), _dp(lo), _dp(hi), _dp(err),
+    s = lib().oc_step_ex(ctypes.byref(pb.c_struct()), JAC[jac], METHODS[method], _dp(u), _dp(lo), _dp(hi), _dp(err),
                       float(dt), float(c), float(gamma), float(rtol), float(atol), _dp(xi),
                       int(max_nodes), ctypes.byref(it))
     return StepResult(lo, hi, float(err[0]), it.value, s)

@@ -422,10 +422,89 @@ double oc_power_iteration(const oc_problem *pb, const double *u, int iters)
 /*   margins[0] = min_k thr/err at acceptance; margins[1] = min over the      */
 /*   rejected checks of err/thr (how far the decisions were from flipping).   */
 /* ------------------------------------------------------------------------- */
+/* ------------------------------------------------------------------------- */
+/* Black-box right-hand side (P:120-133 listing alg:RHS):    */
+/* the method only calls f.  Jacobian-vector products by forward finite        */
+/* differences ("computed numerically using finite differences"):       */
+/*   J(u) y ~ (f(u + eps y) - f(u)) / eps,                                     */
+/*   eps = sqrt(DBL_EPSILON) (1 + ||u||_inf) / ||y||_inf   (reading R25),       */
+/* J(u) y = 0 when y = 0.  For a LINEAR f (Problem I, P:161-171 real_Leja_exp  */
+/* with RHS = A) the operator is applied as f(y) itself (OC_JAC_LINEAR_F).     */
+/* ------------------------------------------------------------------------- */
+#define OC_JAC_EXACT 0
+#define OC_JAC_FD 1
+#define OC_JAC_LINEAR_F 2
+#define OC_FD_EPS0 1.4901161193847656e-08   /* sqrt(DBL_EPSILON) = 2^-26 */
+
+static double maxabs(const double *x, long N)
+{
+    double m = 0.0;
+    for (long i = 0; i < N; i++) if (fabs(x[i]) > m) m = fabs(x[i]);
+    return m;
+}
+
+/* w = J(u) y by forward differences; f_u = f(u) (unscaled). */
+void oc_jac_apply_fd(const oc_problem *pb, const double *u, const double *f_u, const double *y, double *w)
+{
+    long N = oc_npoints(pb);
+    double ymax = maxabs(y, N);
+    if (ymax == 0.0) {
+        for (long i = 0; i < N; i++) w[i] = 0.0;
+        return;
+    }
+    double eps = OC_FD_EPS0 * (1.0 + maxabs(u, N)) / ymax;
+    double *t = (double *)malloc(sizeof(double) * (size_t)N);
+    double *ft = (double *)malloc(sizeof(double) * (size_t)N);
+    for (long i = 0; i < N; i++) t[i] = u[i] + eps * y[i];
+    oc_rhs(pb, t, ft);
+    for (long i = 0; i < N; i++) w[i] = (ft[i] - f_u[i]) / eps;
+    free(t);
+    free(ft);
+}
+
+/* F(x) = f(x) - J(u) x with the finite-difference J (the listing's
+ * Nonlinear_remainder(RHS, u, x, NL_x), alg:exprb32 P:530-531), literally. */
+void oc_nonlinear_remainder_fd(const oc_problem *pb, const double *u, const double *f_u, const double *x,
+                               double *out)
+{
+    long N = oc_npoints(pb);
+    double *fx = (double *)malloc(sizeof(double) * (size_t)N);
+    double *jx = (double *)malloc(sizeof(double) * (size_t)N);
+    oc_rhs(pb, x, fx);
+    oc_jac_apply_fd(pb, u, f_u, x, jx);
+    for (long i = 0; i < N; i++) out[i] = fx[i] - jx[i];
+    free(fx);
+    free(jx);
+}
+
+static void jac_mode_apply(const oc_problem *pb, int mode, const double *u, const double *f_u, const double *y,
+                           double *w)
+{
+    if (mode == OC_JAC_FD) oc_jac_apply_fd(pb, u, f_u, y, w);
+    else if (mode == OC_JAC_LINEAR_F) oc_rhs(pb, y, w);
+    else oc_jac_apply(pb, u, y, w);
+}
+
+int oc_real_leja_phi_ex(const oc_problem *pb, int jac_mode, const double *u_lin, const double *f_u,
+                        const double *v, double **outs, const double *coeffs, int K, double dt, double c,
+                        double gamma, int l, double rtol, double atol, const double *xi,
+                        int max_nodes, int *iters, double *margins);
+
 int oc_real_leja_phi(const oc_problem *pb, const double *u_lin, const double *v,
                      double **outs, const double *coeffs, int K, double dt, double c,
                      double gamma, int l, double rtol, double atol, const double *xi,
                      int max_nodes, int *iters, double *margins)
+{
+    return oc_real_leja_phi_ex(pb, OC_JAC_EXACT, u_lin, NULL, v, outs, coeffs, K, dt, c, gamma, l, rtol, atol,
+                               xi, max_nodes, iters, margins);
+}
+
+/* jac_mode: OC_JAC_EXACT (J(u_lin) exact), OC_JAC_FD (J(u_lin) by differences of f;
+ * f_u = f(u_lin) or NULL to compute it here), OC_JAC_LINEAR_F (operator = f itself). */
+int oc_real_leja_phi_ex(const oc_problem *pb, int jac_mode, const double *u_lin, const double *f_u,
+                        const double *v, double **outs, const double *coeffs, int K, double dt, double c,
+                        double gamma, int l, double rtol, double atol, const double *xi,
+                        int max_nodes, int *iters, double *margins)
 {
     if (iters) *iters = 0;
     if (margins) { margins[0] = INFINITY; margins[1] = INFINITY; }
@@ -443,6 +522,13 @@ int oc_real_leja_phi(const oc_problem *pb, const double *u_lin, const double *v,
     if (!y || !w || !d) { free(y); free(w); free(d); return OC_ERR_ARG; }
 
     int status = OC_OK;
+    double *fu_own = NULL;
+    if (jac_mode == OC_JAC_FD && !f_u) {
+        if (!u_lin) { free(y); free(w); free(d); return OC_ERR_ARG; }
+        fu_own = (double *)malloc(sizeof(double) * (size_t)N);
+        oc_rhs(pb, u_lin, fu_own);
+        f_u = fu_own;
+    }
     for (int k = 0; k < K; k++) {
         int s = oc_divided_differences(l, xi, max_nodes, dt, c, gamma, coeffs[k], d + (size_t)k * max_nodes);
         if (s != OC_OK) { status = s; goto done; }
@@ -457,7 +543,7 @@ int oc_real_leja_phi(const oc_problem *pb, const double *u_lin, const double *v,
 
     status = OC_ERR_NOCONV;
     for (int m = 1; m < max_nodes; m++) {
-        oc_jac_apply(pb, u_lin, y, w);                       /* w = J y */
+        jac_mode_apply(pb, jac_mode, u_lin, f_u, y, w);      /* w = J y */
         for (long i = 0; i < N; i++)                         /* Eq. (2) */
             y[i] = (w[i] - c * y[i]) / gamma - xi[m - 1] * y[i];
         double ny = oc_l2norm_scaled(y, N);
@@ -485,6 +571,7 @@ done:
     free(y);
     free(w);
     free(d);
+    free(fu_own);
     return status;
 }
 
@@ -499,16 +586,27 @@ static void axpby(double a, const double *x, double b, const double *y, double *
     for (long i = 0; i < N; i++) z[i] = a * x[i] + b * y[i];
 }
 
-int oc_step(const oc_problem *pb, int method, const double *u, double *u_low, double *u_high,
-            double *err, double dt, double c, double gamma, double rtol, double atol,
-            const double *xi, int max_nodes, int *iters)
+/* F(x): analytic (R18) for the exact-Jacobian contract, literal f(x) - J_FD(u) x
+ * for the black-box finite-difference mode. */
+static void remainder_mode(const oc_problem *pb, int jac_mode, const double *u, const double *fu_raw,
+                           const double *x, double *out)
+{
+    if (jac_mode == OC_JAC_FD) oc_nonlinear_remainder_fd(pb, u, fu_raw, x, out);
+    else oc_nonlinear_remainder(pb, u, x, out);
+}
+
+int oc_step_ex(const oc_problem *pb, int jac_mode, int method, const double *u, double *u_low,
+               double *u_high, double *err, double dt, double c, double gamma, double rtol, double atol,
+               const double *xi, int max_nodes, int *iters)
 {
     long N = oc_npoints(pb);
     int it = 0, total = 0, s = OC_OK;
     if (err) *err = 0.0;
     if (iters) *iters = 0;
     if (method < 0 || method > 4) return OC_ERR_ARG;
+    if (jac_mode != OC_JAC_EXACT && jac_mode != OC_JAC_FD) return OC_ERR_ARG;
     size_t bytes = sizeof(double) * (size_t)N;
+    double *fu_raw = NULL;
     double *f_u = (double *)malloc(bytes);
     double *t1 = (double *)malloc(bytes), *t2 = (double *)malloc(bytes), *t3 = (double *)malloc(bytes);
     double *t4 = (double *)malloc(bytes), *t5 = (double *)malloc(bytes), *t6 = (double *)malloc(bytes);
@@ -517,13 +615,18 @@ int oc_step(const oc_problem *pb, int method, const double *u, double *u_low, do
 
     /* f_u = RHS(u) * dt  (alg:Ros_Eu P:468-469) */
     oc_rhs(pb, u, f_u);
+    if (jac_mode == OC_JAC_FD) {   /* unscaled f(u) for the difference quotients */
+        fu_raw = (double *)malloc(bytes);
+        if (!fu_raw) { s = OC_ERR_ARG; goto out; }
+        memcpy(fu_raw, f_u, bytes);
+    }
     for (long i = 0; i < N; i++) f_u[i] = dt * f_u[i];
 
     if (method == 0) {
         /* u_exprb2 = u + phi_1(J dt) f_u dt */
         double one = 1.0;
         double *o[1] = {t1};
-        s = oc_real_leja_phi(pb, u, f_u, o, &one, 1, dt, c, gamma, 1, rtol, atol, xi, max_nodes, &it, NULL);
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, f_u, o, &one, 1, dt, c, gamma, 1, rtol, atol, xi, max_nodes, &it, NULL);
         total += it;
         if (s) goto out;
         axpby(1.0, u, 1.0, t1, u_high, N);
@@ -532,15 +635,15 @@ int oc_step(const oc_problem *pb, int method, const double *u, double *u_low, do
         /* EXPRB32 (alg:exprb32 P:512-540) */
         double one = 1.0;
         double *o[1] = {t1};                                  /* u_flux */
-        s = oc_real_leja_phi(pb, u, f_u, o, &one, 1, dt, c, gamma, 1, rtol, atol, xi, max_nodes, &it, NULL);
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, f_u, o, &one, 1, dt, c, gamma, 1, rtol, atol, xi, max_nodes, &it, NULL);
         total += it;
         if (s) goto out;
         axpby(1.0, u, 1.0, t1, u_low, N);                     /* u_exprb2 = a */
-        oc_nonlinear_remainder(pb, u, u, t2);                 /* NL_u */
-        oc_nonlinear_remainder(pb, u, u_low, t3);             /* NL_a */
+        remainder_mode(pb, jac_mode, u, fu_raw, u, t2);                 /* NL_u */
+        remainder_mode(pb, jac_mode, u, fu_raw, u_low, t3);             /* NL_a */
         axpby(dt, t3, -dt, t2, t4, N);                        /* R_a = (NL_a - NL_u) dt */
         double *o3[1] = {t5};                                 /* u_nl_3 */
-        s = oc_real_leja_phi(pb, u, t4, o3, &one, 1, dt, c, gamma, 3, rtol, atol, xi, max_nodes, &it, NULL);
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, t4, o3, &one, 1, dt, c, gamma, 3, rtol, atol, xi, max_nodes, &it, NULL);
         total += it;
         if (s) goto out;
         axpby(1.0, u_low, 2.0, t5, u_high, N);                /* u_exprb3 = a + 2 u_nl_3 */
@@ -553,17 +656,17 @@ int oc_step(const oc_problem *pb, int method, const double *u, double *u_low, do
          * non-embedded (u_low = u_high, err = 0). */
         double cf[2] = {0.75, 1.0};
         double *pv[2] = {t1, t2};
-        s = oc_real_leja_phi(pb, u, f_u, pv, cf, 2, dt, c, gamma, 1, rtol, atol, xi, max_nodes, &it, NULL);
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, f_u, pv, cf, 2, dt, c, gamma, 1, rtol, atol, xi, max_nodes, &it, NULL);
         total += it;
         if (s) goto out;
         axpby(1.0, u, 0.75, t1, t3, N);                       /* a */
-        oc_nonlinear_remainder(pb, u, u, t4);                 /* NL_u */
-        oc_nonlinear_remainder(pb, u, t3, t5);                /* NL_a */
+        remainder_mode(pb, jac_mode, u, fu_raw, u, t4);                 /* NL_u */
+        remainder_mode(pb, jac_mode, u, fu_raw, t3, t5);                /* NL_a */
         axpby(dt, t5, -dt, t4, t6, N);                        /* D_a */
         for (long i = 0; i < N; i++) t6[i] = (32.0 / 9.0) * t6[i];
         double one = 1.0;
         double *o3[1] = {t7};
-        s = oc_real_leja_phi(pb, u, t6, o3, &one, 1, dt, c, gamma, 3, rtol, atol, xi, max_nodes, &it, NULL);
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, t6, o3, &one, 1, dt, c, gamma, 3, rtol, atol, xi, max_nodes, &it, NULL);
         total += it;
         if (s) goto out;
         for (long i = 0; i < N; i++) u_high[i] = u[i] + t2[i] + t7[i];
@@ -580,16 +683,16 @@ int oc_step(const oc_problem *pb, int method, const double *u, double *u_low, do
         int epirk = (method == 3);
         double cf2[2] = {0.5, 1.0}, cf3[3] = {0.5, 2.0 / 3.0, 1.0};
         double *pv[3] = {t1, t2, t3};
-        s = oc_real_leja_phi(pb, u, f_u, pv, epirk ? cf3 : cf2, epirk ? 3 : 2, dt, c, gamma, 1,
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, f_u, pv, epirk ? cf3 : cf2, epirk ? 3 : 2, dt, c, gamma, 1,
                              rtol, atol, xi, max_nodes, &it, NULL);
         total += it;
         if (s) goto out;
         double *p_half = t1, *p_one = epirk ? t3 : t2;
         double *NLu = t4, *Da = t5, *Db = t6, *tmp = t7;
-        oc_nonlinear_remainder(pb, u, u, NLu);
+        remainder_mode(pb, jac_mode, u, fu_raw, u, NLu);
         /* a = u + 1/2 p_half */
         axpby(1.0, u, 0.5, p_half, u_low, N);
-        oc_nonlinear_remainder(pb, u, u_low, tmp);
+        remainder_mode(pb, jac_mode, u, fu_raw, u_low, tmp);
         axpby(dt, tmp, -dt, NLu, Da, N);                      /* D_a */
         if (epirk) {
             /* b = u + 2/3 p_twothirds */
@@ -598,12 +701,12 @@ int oc_step(const oc_problem *pb, int method, const double *u, double *u_low, do
             /* b = u + p_one + phi_1(hJ) D_a */
             double one = 1.0;
             double *o[1] = {u_high};
-            s = oc_real_leja_phi(pb, u, Da, o, &one, 1, dt, c, gamma, 1, rtol, atol, xi, max_nodes, &it, NULL);
+            s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, Da, o, &one, 1, dt, c, gamma, 1, rtol, atol, xi, max_nodes, &it, NULL);
             total += it;
             if (s) goto out;
             for (long i = 0; i < N; i++) u_low[i] = u[i] + p_one[i] + u_high[i];
         }
-        oc_nonlinear_remainder(pb, u, u_low, tmp);
+        remainder_mode(pb, jac_mode, u, fu_raw, u_low, tmp);
         axpby(dt, tmp, -dt, NLu, Db, N);                      /* D_b */
         double a3 = epirk ? 32.0 : 16.0, b3 = epirk ? -13.5 : -2.0;
         double a4 = epirk ? -144.0 : -48.0, b4 = epirk ? 81.0 : 12.0;
@@ -611,11 +714,11 @@ int oc_step(const oc_problem *pb, int method, const double *u, double *u_low, do
         axpby(a4, Da, b4, Db, NLu, N);                        /* w4 (NLu no longer needed) */
         double one = 1.0;
         double *o3[1] = {Da};
-        s = oc_real_leja_phi(pb, u, tmp, o3, &one, 1, dt, c, gamma, 3, rtol, atol, xi, max_nodes, &it, NULL);
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, tmp, o3, &one, 1, dt, c, gamma, 3, rtol, atol, xi, max_nodes, &it, NULL);
         total += it;
         if (s) goto out;
         double *o4[1] = {Db};
-        s = oc_real_leja_phi(pb, u, NLu, o4, &one, 1, dt, c, gamma, 4, rtol, atol, xi, max_nodes, &it, NULL);
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, NLu, o4, &one, 1, dt, c, gamma, 4, rtol, atol, xi, max_nodes, &it, NULL);
         total += it;
         if (s) goto out;
         for (long i = 0; i < N; i++) u_low[i] = u[i] + p_one[i] + Da[i];    /* u3 */
@@ -626,5 +729,15 @@ int oc_step(const oc_problem *pb, int method, const double *u, double *u_low, do
 out:
     if (iters) *iters = total;
     free(f_u); free(t1); free(t2); free(t3); free(t4); free(t5); free(t6); free(t7);
+    free(fu_raw);
     return s;
+}
+
+/* Exact-Jacobian steps (R13, R18): the contract the device hot path follows. */
+int oc_step(const oc_problem *pb, int method, const double *u, double *u_low, double *u_high,
+            double *err, double dt, double c, double gamma, double rtol, double atol,
+            const double *xi, int max_nodes, int *iters)
+{
+    return oc_step_ex(pb, OC_JAC_EXACT, method, u, u_low, u_high, err, dt, c, gamma, rtol, atol, xi, max_nodes,
+                      iters);
 }
