@@ -251,6 +251,51 @@ lx_status lx_integrate(lx_ctx *ctx, lx_method method, const lx_problem *pb, doub
 /* f(u) * dt (alg:Ros_Eu P:468-469) as a standalone fused stencil pass. */
 lx_status lx_rhs(lx_ctx *ctx, const lx_problem *pb, const double *u, double scale, double *f_out);
 
+/* ------------------------------------------------------------------------ */
+/* Black-box right-hand side.                              */
+/* The paper's interface: the user supplies only f (listing       */
+/* alg:RHS: a functor taking an input and an output pointer to contiguous    */
+/* data) and the Jacobian action is "computed numerically using finite       */
+/* differences".  Reading R25:                           */
+/*   J(u) y = (f(u + eps y) - f(u)) / eps,                                   */
+/*   eps = 2^-26 (1 + ||u||_inf) / ||y||_inf,  J(u) 0 = 0;                    */
+/*   nonlinear remainder F(x) = f(x) - J(u) x literally (alg:exprb32).        */
+/* ------------------------------------------------------------------------ */
+/* f(in) -> out on the device: in / out are N_loc contiguous doubles on the
+ * context's device (in read-only; out never aliases in).  f must enqueue its
+ * work on cuda_stream (the context stream) or complete it before returning;
+ * it must not call back into the same context except through lx_builtin_rhs. */
+typedef void (*lx_rhs_fn)(const double *in, double *out, void *user, void *cuda_stream);
+
+/* phi_l(a_k dt J) v for a black-box operator (P:175-191 real_Leja_phi_nl(RHS, ...),
+ * P:421-443 real_Leja_phi; recurrence P:142-147 Eq. (2); stopping rule P:155):
+ *   u != NULL: J = J(u) by finite differences of f (R25);
+ *   u == NULL: J y = f(y) -- f must then be LINEAR (Problem I's RHS = A).
+ * Same argument meaning, layout, ownership and errors as lx_real_leja_phi_vertical.
+ * Per Leja iteration: one f call (plus one for f(u)), a perturbation kernel (FD) and one
+ * fused update kernel (Newton update + K accumulators + norms + device decision); the host
+ * waits for the decision of iteration m-1 while iteration m runs (one extra f call at the
+ * end, whose kernels return at entry).  Single-GPU contexts only (LX_ERR_UNSUPPORTED). */
+lx_status lx_real_leja_phi_cb(lx_ctx *ctx, lx_rhs_fn f, void *user, const double *u, const double *v,
+                              double *const *outs, const double *coeffs, int K, double dt, double c,
+                              double gamma, int l, double rtol, double atol, int *iters_out);
+
+/* One integrator step with a black-box f (the paper's exp_int / embed_exp_int on a user
+ * RHS; listings alg:Ros_Eu, alg:exprb32; R17, R22 tableaux), Jacobian actions and
+ * nonlinear remainders by finite differences (R25).  Arguments and errors as lx_step. */
+lx_status lx_step_cb(lx_ctx *ctx, lx_method method, lx_rhs_fn f, void *user, const double *u,
+                     double *u_low, double *u_high, double *err_out, double dt, double c, double gamma,
+                     double rtol, double atol, int *iters_out);
+
+/* The built-in stencil f of a problem packaged as an lx_rhs_fn (user points to this struct;
+ * pb->source, if any, must be a device pointer).  Lets the black-box path be checked against
+ * the same operator the fused kernels apply. */
+typedef struct {
+    lx_ctx *ctx;
+    const lx_problem *pb;
+} lx_builtin_rhs_user;
+void lx_builtin_rhs(const double *in, double *out, void *user, void *cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

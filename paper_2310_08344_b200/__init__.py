@@ -41,7 +41,11 @@ EXPORTS = ("lx_last_error", "lx_version", "lx_leja_points", "lx_phi_scalar", "lx
            "lx_spectrum_bound", "lx_shift_scale", "lx_real_leja_phi", "lx_real_leja_phi_vertical",
            "lx_step_rosenbrock_euler", "lx_step_exprb32", "lx_step_exprb43", "lx_step_epirk4s3a",
            "lx_step_exprb42",
-           "lx_step", "lx_rhs", "lx_integrate", "lx_local_group_create", "lx_local_group_destroy", "lx_ctx_set_comm_local")
+           "lx_step", "lx_rhs", "lx_integrate", "lx_local_group_create", "lx_local_group_destroy", "lx_ctx_set_comm_local",
+           "lx_real_leja_phi_cb", "lx_step_cb", "lx_builtin_rhs")
+
+# void f(const double* in, double* out, void* user, void* cuda_stream)  (include/lexint.h lx_rhs_fn)
+RHS_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
 
 
 class LxError(RuntimeError):
@@ -127,6 +131,10 @@ def lib() -> ctypes.CDLL:
             "lx_local_group_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(vp)]),
             "lx_local_group_destroy": (ctypes.c_int, [vp]),
             "lx_ctx_set_comm_local": (ctypes.c_int, [vp, vp, ctypes.c_int]),
+            "lx_real_leja_phi_cb": (ctypes.c_int, [vp, vp, vp, vp, vp, ctypes.POINTER(vp), dp, ctypes.c_int,
+                                                   d, d, d, ctypes.c_int, d, d, ip]),
+            "lx_step_cb": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, vp, vp, vp, dp, d, d, d, d, d, ip]),
+            "lx_builtin_rhs": (None, [vp, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -365,3 +373,93 @@ def lx_integrate(ctx: Context, method, u, dt, nsteps, rtol, atol, problem: Probl
 
 def lx_rhs(ctx: Context, u, f_out, scale: float = 1.0, problem: Problem | None = None):
     _check(lib().lx_rhs(ctx.handle, _pb(ctx, problem), _ptr(u), float(scale), _ptr(f_out)))
+
+
+# ------------------------------------------------------------------ black-box RHS
+class LxBuiltinRhsUser(ctypes.Structure):
+    _fields_ = [("ctx", ctypes.c_void_p), ("pb", ctypes.POINTER(LxProblem))]
+
+
+class Rhs:
+    """A black-box right-hand side f for lx_real_leja_phi_cb / lx_step_cb.
+
+    Rhs.builtin(ctx): the library's own stencil f of ctx's problem, called natively (no Python
+    in the loop).  Rhs.from_python(fn): fn(in_ptr, out_ptr, stream_handle) is called from the
+    library through a ctypes trampoline; it must enqueue its device work on that stream."""
+
+    def __init__(self, fn_ptr, user_ptr, keep=()):
+        self.fn = fn_ptr
+        self.user = user_ptr
+        self._keep = keep
+        self.error = None     # first exception raised inside a Python callback (re-raised after the call)
+
+    def _raise(self):
+        if self.error is not None:
+            e, self.error = self.error, None
+            raise RuntimeError("black-box RHS callback failed") from e
+
+    @classmethod
+    def builtin(cls, ctx: "Context", problem: Problem | None = None) -> "Rhs":
+        pb = problem.c_struct() if problem is not None else ctx._pb
+        u = LxBuiltinRhsUser(ctx.handle.value, ctypes.pointer(pb))
+        fn = ctypes.cast(lib().lx_builtin_rhs, ctypes.c_void_p).value
+        return cls(fn, ctypes.addressof(u), keep=(u, pb))
+
+    @classmethod
+    def from_torch(cls, fn, shape) -> "Rhs":
+        """fn(x, out): a torch implementation of f on CUDA tensors of `shape` (fp64); it runs on the
+        library's stream (torch.cuda.ExternalStream).  User code -- the library only calls it."""
+        import torch
+
+        class _View:
+            def __init__(self, ptr):
+                self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f8", "data": (ptr, False),
+                                                 "version": 3, "strides": None, "stream": None}
+
+        def call(inp, out, stream):
+            # the legacy default stream (handle 0 or cudaStreamLegacy = 1) is torch's default stream
+            st = torch.cuda.default_stream() if not stream or stream == 1 else torch.cuda.ExternalStream(stream)
+            with torch.cuda.stream(st):
+                fn(torch.as_tensor(_View(inp), device="cuda"), torch.as_tensor(_View(out), device="cuda"))
+        return cls.from_python(call)
+
+    @classmethod
+    def from_python(cls, fn) -> "Rhs":
+        holder = []
+
+        def tramp(inp, out, user, stream):
+            try:
+                fn(inp, out, stream)
+            except BaseException as e:   # never unwind through the C frames
+                if holder and holder[0].error is None:
+                    holder[0].error = e
+        cb = RHS_FN(tramp)
+        r = cls(ctypes.cast(cb, ctypes.c_void_p).value, None, keep=(cb,))
+        holder.append(r)
+        return r
+
+
+def lx_real_leja_phi_cb(ctx: Context, rhs: Rhs, v, outs: Sequence, coeffs: Sequence[float], dt, c, gamma, l,
+                        rtol, atol, u=None) -> int:
+    """phi_l(a_k dt J) v with J known only through rhs: J(u) by finite differences when u is
+    given, else J y = f(y) (linear f).  Returns the Leja iteration count."""
+    K = len(outs)
+    arr = (ctypes.c_void_p * K)(*[_ptr(o) for o in outs])
+    cf = (ctypes.c_double * K)(*[float(a) for a in coeffs])
+    it = ctypes.c_int(0)
+    st = lib().lx_real_leja_phi_cb(ctx.handle, rhs.fn, rhs.user, _ptr(u), _ptr(v), arr, cf, K, float(dt), float(c),
+                                   float(gamma), int(l), float(rtol), float(atol), ctypes.byref(it))
+    rhs._raise()
+    _check(st, it.value)
+    return it.value
+
+
+def lx_step_cb(ctx: Context, method, rhs: Rhs, u, u_low, u_high, dt, c, gamma, rtol, atol):
+    """One integrator step on a black-box f (FD Jacobians and remainders).  Returns (iters, err)."""
+    m = METHODS[method] if isinstance(method, str) else int(method)
+    it, err = ctypes.c_int(0), ctypes.c_double(0.0)
+    st = lib().lx_step_cb(ctx.handle, m, rhs.fn, rhs.user, _ptr(u), _ptr(u_low), _ptr(u_high), ctypes.byref(err),
+                          float(dt), float(c), float(gamma), float(rtol), float(atol), ctypes.byref(it))
+    rhs._raise()
+    _check(st, it.value)
+    return it.value, err.value

@@ -1,0 +1,307 @@
+// lx_blackbox.cu -- sm_100a kernels of the black-box right-hand-side path.
+//
+// The paper's LeXInt only calls a user RHS functor f (listing alg:RHS) and forms
+// Jacobian-vector products by finite differences: J(u) y ~ (f(u + eps y) - f(u)) / eps.
+// Here the user's f is a host callback that enqueues device work on the context stream; every
+// other step of the Leja iteration (Eq. (2)) and of the stopping test runs in
+// the kernels below.  Per Leja iteration m:
+//   k_bb_perturb(m)  : w = u + eps_m y_{m-1},  eps_m = 2^-26 (1 + ||u||_inf) / ||y_{m-1}||_inf   (R25)
+//   user f(w) -> fw   (or f(y_{m-1}) for a linear black-box operator)
+//   k_bb_update(m)   : J y = (fw - f(u)) / eps_m ; y_m = alpha J y + beta_m y_{m-1} ;
+//                      p_k += d_m^(k) y_m ; per-CTA partials (sum y^2, sum p_k^2), max|y_m| ;
+//                      the last CTA sums the partials in CTA order and takes the decision.
+// All kernels return at entry once the decision says "done", so the host may enqueue one
+// iteration ahead of the flag it reads.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "lx_internal.h"
+
+namespace lx {
+
+namespace {
+
+constexpr double kFdEps0 = 1.4901161193847656e-08;   // 2^-26 = sqrt(DBL_EPSILON)  (R25)
+
+__device__ __forceinline__ double u64_as_double(unsigned long long b) { return __longlong_as_double((long long)b); }
+__device__ __forceinline__ unsigned long long double_as_u64(double x) {
+    return (unsigned long long)__double_as_longlong(x);
+}
+
+// block sum of NV values (fixed order: warp butterfly, then warps in index order)
+template <int NV>
+__device__ __forceinline__ void block_sum(double* v, double (*s)[NV]) {
+#pragma unroll
+    for (int i = 0; i < NV; i++)
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], off);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0)
+#pragma unroll
+        for (int i = 0; i < NV; i++) s[warp][i] = v[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; i++) {
+            double a = 0.0;
+            for (int w = 0; w < kWarps; w++) a += s[w][i];
+            v[i] = a;
+        }
+    }
+}
+
+__device__ __forceinline__ double block_max(double v, double* s) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) s[warp] = v;
+    __syncthreads();
+    double m = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < kWarps; w++) m = fmax(m, s[w]);
+    return m;
+}
+
+__device__ __forceinline__ double fd_eps(const BbCtrl* c, int slot) {
+    const double ym = u64_as_double(c->maxbits[slot]);
+    if (ym == 0.0) return 0.0;                 // J(u) 0 = 0
+    return kFdEps0 * (1.0 + u64_as_double(c->umaxbits)) / ym;
+}
+
+// p_k = d_0^(k) v ; max|v| -> maxbits[0] ; max|u| -> umaxbits (FD) ; decision state reset by the host
+__global__ void __launch_bounds__(kThreads) k_bb_init(BbArgs A) {
+    __shared__ double s[kWarps];
+    double mv = 0.0, mu = 0.0;
+    const long long N = A.N;
+    const int K = A.K;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+        const double v = A.y_in[i];
+        mv = fmax(mv, fabs(v));
+        if (A.u) mu = fmax(mu, fabs(A.u[i]));
+        for (int k = 0; k < K; k++) A.p[k][i] = A.table[1 + k] * v;
+    }
+    mv = block_max(mv, s);
+    __syncthreads();
+    mu = block_max(mu, s);
+    if (threadIdx.x == 0) {
+        atomicMax(&A.ctrl->maxbits[0], double_as_u64(mv));
+        if (A.u) atomicMax(&A.ctrl->umaxbits, double_as_u64(mu));
+    }
+}
+
+// w = u + eps_m y_{m-1}; block 0 also clears the max slot iteration m will fill
+__global__ void __launch_bounds__(kThreads) k_bb_perturb(BbArgs A, int m) {
+    BbCtrl* c = A.ctrl;
+    if (*(volatile int*)&c->done) return;
+    const double eps = fd_eps(c, (m - 1) & 1);
+    const long long N = A.N;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x)
+        A.w[i] = A.u[i] + eps * A.y_in[i];
+    if (blockIdx.x == 0 && threadIdx.x == 0) c->maxbits[m & 1] = 0ull;
+}
+
+template <int K>
+__global__ void __launch_bounds__(kThreads) k_bb_update(BbArgs A, int m) {
+    constexpr int NV = 1 + K;
+    __shared__ double s_red[kWarps][NV];
+    __shared__ double s_max[kWarps];
+    __shared__ int s_last;
+    BbCtrl* c = A.ctrl;
+    if (*(volatile int*)&c->done) return;
+    const int act = c->active;
+    const double* row = A.table + (size_t)m * (1 + A.K);
+    const double beta = row[0];
+    double dm[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) dm[k] = row[1 + k];
+    const double alpha = A.alpha;
+    const bool fd = A.mode == 1;
+    const double eps = fd ? fd_eps(c, (m - 1) & 1) : 1.0;
+    const double ieps = (fd && eps != 0.0) ? 1.0 / eps : 0.0;
+    double acc[NV];
+#pragma unroll
+    for (int i = 0; i < NV; i++) acc[i] = 0.0;
+    double my = 0.0;
+    const long long N = A.N;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+        const double yp = A.y_in[i];
+        double jy;
+        if (fd) jy = (eps == 0.0) ? 0.0 : (A.fw[i] - A.fu[i]) * ieps;
+        else jy = A.fw[i];
+        const double y = fma(alpha, jy, beta * yp);
+        A.y_out[i] = y;
+        acc[0] = fma(y, y, acc[0]);
+        my = fmax(my, fabs(y));
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            if ((act >> k) & 1) {
+                const double p = fma(dm[k], y, A.p[k][i]);
+                A.p[k][i] = p;
+                acc[1 + k] = fma(p, p, acc[1 + k]);
+            }
+        }
+    }
+    block_sum<NV>(acc, s_red);
+    __syncthreads();
+    my = block_max(my, s_max);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; i++) A.partials[(size_t)blockIdx.x * NV + i] = acc[i];
+        atomicMax(&c->maxbits[m & 1], double_as_u64(my));
+        __threadfence();
+        const unsigned t = atomicAdd(&c->ticket, 1u);
+        s_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    // last CTA: fixed-order sum of the CTA partials, then the P:155 test (R3, R4)
+    __threadfence();
+    double sums[NV];
+#pragma unroll
+    for (int i = 0; i < NV; i++) sums[i] = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+#pragma unroll
+        for (int i = 0; i < NV; i++) sums[i] += __ldcg(A.partials + (size_t)b * NV + i);
+    block_sum<NV>(sums, s_red);
+    if (threadIdx.x == 0) {
+        c->ticket = 0u;
+        Record* rec = A.rec;
+        const double Ng = A.N_glob;
+        const double ny = sqrt(sums[0] / Ng);
+        int a = act, nact = 0, status = 0, done = 0;
+        for (int k = 0; k < K; k++) {
+            if (!((a >> k) & 1)) continue;
+            const double err = fabs(dm[k]) * ny;
+            const double thr = A.rtol * sqrt(sums[1 + k] / Ng) + A.atol;
+            if (!isfinite(err) || !isfinite(thr)) { status = 6; break; }
+            if (err <= thr) {
+                a &= ~(1 << k);
+                rec->iters_k[k] = m;
+                const double r = err > 0.0 ? thr / err : INFINITY;
+                if (r < rec->margin_accept) rec->margin_accept = r;
+            } else {
+                nact++;
+                const double r = err / thr;
+                if (r < rec->margin_reject) rec->margin_reject = r;
+            }
+        }
+        if (status) done = 1;
+        else if (nact == 0) done = 1;
+        else if (m >= A.max_nodes - 1) { done = 1; status = 5; }
+        c->active = a;
+        c->m = m;
+        if (done) {
+            rec->iters += m;
+            rec->ncalls += 1;
+            if (rec->status == 0) rec->status = status;
+            c->status = status;
+            __threadfence_system();
+            c->done = 1;
+            if (A.done_host) *(volatile int*)A.done_host = m;
+        }
+    }
+}
+
+// max |x| -> ctrl->maxbits[2] (host clears it first)
+__global__ void __launch_bounds__(kThreads) k_bb_maxabs(const double* x, long long N, BbCtrl* c) {
+    __shared__ double s[kWarps];
+    double mx = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x)
+        mx = fmax(mx, fabs(x[i]));
+    mx = block_max(mx, s);
+    if (threadIdx.x == 0) atomicMax(&c->maxbits[2], double_as_u64(mx));
+}
+
+// FD remainder pieces (alg:exprb32 Nonlinear_remainder), eps from maxbits[2]:
+//   PERTURB: y0 = u + eps x0 ;  REMAINDER: y0 = x0 - (x1 - fu) / eps   (F(x) = f(x) - J_FD(u) x)
+__global__ void __launch_bounds__(kThreads) k_bb_fdpiece(BbLin L, int op) {
+    const double ym = u64_as_double(L.ctrl->maxbits[2]);
+    const double eps = ym == 0.0 ? 0.0 : kFdEps0 * (1.0 + u64_as_double(L.ctrl->umaxbits)) / ym;
+    const long long N = L.N;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+        if (op == 0) L.y0[i] = L.u[i] + eps * L.x0[i];
+        else L.y0[i] = L.x0[i] - (eps == 0.0 ? 0.0 : (L.x1[i] - L.fu[i]) / eps);
+    }
+}
+
+// y0 = a0 x0 + a1 x1 + a2 x2 + a3 x3 (absent inputs skipped, evaluated left to right)
+__global__ void __launch_bounds__(kThreads) k_bb_lincomb(BbLin L) {
+    const long long N = L.N;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+        double s = L.a0 * L.x0[i];
+        if (L.x1) s += L.a1 * L.x1[i];
+        if (L.x2) s += L.a2 * L.x2[i];
+        if (L.x3) s += L.a3 * L.x3[i];
+        L.y0[i] = s;
+    }
+}
+
+// rec->err = || a0 x0 + a1 x1 || / sqrt(N), CTA partials summed in CTA order by the last CTA
+__global__ void __launch_bounds__(kThreads) k_bb_norm(BbLin L) {
+    __shared__ double s_red[kWarps][1];
+    __shared__ int s_last;
+    double acc[1] = {0.0};
+    const long long N = L.N;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+        double e = L.a0 * L.x0[i];
+        if (L.x1) e += L.a1 * L.x1[i];
+        acc[0] = fma(e, e, acc[0]);
+    }
+    block_sum<1>(acc, s_red);
+    if (threadIdx.x == 0) {
+        L.partials[blockIdx.x] = acc[0];
+        __threadfence();
+        s_last = (atomicAdd(&L.ctrl->ticket, 1u) == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    double t[1] = {0.0};
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) t[0] += __ldcg(L.partials + b);
+    block_sum<1>(t, s_red);
+    if (threadIdx.x == 0) {
+        L.ctrl->ticket = 0u;
+        L.rec->err = sqrt(t[0] / L.N_glob);
+    }
+}
+
+}  // namespace
+
+int bb_grid(int nsm) { return nsm * 2; }
+
+cudaError_t launch_bb_init(const BbArgs& A, cudaStream_t s) {
+    k_bb_init<<<A.grid, kThreads, 0, s>>>(A);
+    return cudaGetLastError();
+}
+cudaError_t launch_bb_perturb(const BbArgs& A, int m, cudaStream_t s) {
+    k_bb_perturb<<<A.grid, kThreads, 0, s>>>(A, m);
+    return cudaGetLastError();
+}
+cudaError_t launch_bb_update(const BbArgs& A, int m, cudaStream_t s) {
+    switch (A.K) {
+        case 1: k_bb_update<1><<<A.grid, kThreads, 0, s>>>(A, m); break;
+        case 2: k_bb_update<2><<<A.grid, kThreads, 0, s>>>(A, m); break;
+        case 3: k_bb_update<3><<<A.grid, kThreads, 0, s>>>(A, m); break;
+        case 4: k_bb_update<4><<<A.grid, kThreads, 0, s>>>(A, m); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+cudaError_t launch_bb_maxabs(const double* x, long long N, BbCtrl* c, int grid, cudaStream_t s) {
+    k_bb_maxabs<<<grid, kThreads, 0, s>>>(x, N, c);
+    return cudaGetLastError();
+}
+cudaError_t launch_bb_fdpiece(const BbLin& L, int op, cudaStream_t s) {
+    k_bb_fdpiece<<<L.grid, kThreads, 0, s>>>(L, op);
+    return cudaGetLastError();
+}
+cudaError_t launch_bb_lincomb(const BbLin& L, cudaStream_t s) {
+    k_bb_lincomb<<<L.grid, kThreads, 0, s>>>(L);
+    return cudaGetLastError();
+}
+cudaError_t launch_bb_norm(const BbLin& L, cudaStream_t s) {
+    k_bb_norm<<<L.grid, kThreads, 0, s>>>(L);
+    return cudaGetLastError();
+}
+
+}  // namespace lx

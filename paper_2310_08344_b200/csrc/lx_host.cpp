@@ -49,6 +49,7 @@ static lx_status fail(lx_status s, const char* fmt, ...) {
 static constexpr int kCoefSlots = 32;
 static constexpr int kStage = 7;   // integrator scratch vectors (4 stages + 3 states for lx_integrate)
 static constexpr int kHost = 6;    // host-pointer staging vectors
+static constexpr int kBb = 11;     // black-box path vectors
 
 struct lx_ctx {
     int device = 0;
@@ -98,6 +99,12 @@ struct lx_ctx {
     bool coef_table = false;              // LX_COEF=table: prebuilt coefficient table instead of in-kernel
     double* cg_dev = nullptr;             // device (c, gamma, bound) of lx_integrate
     const double* cg_active = nullptr;    // when set, Leja kernels take (c, gamma) from here
+    // black-box RHS path (lx_real_leja_phi_cb / lx_step_cb)
+    BbCtrl* bb = nullptr;                 // device control block
+    int* bb_done_host = nullptr;          // mapped pinned word written by the deciding CTA
+    int* bb_done_dev = nullptr;           // its device alias
+    cudaEvent_t bb_ev[2] = {};
+    double* B[kBb] = {};                  // black-box vectors: f(u), f_u dt, t1..t7, w, f(w)
 };
 
 // ------------------------------------------------------------------ helpers
@@ -465,6 +472,11 @@ static void free_ctx(lx_ctx* ctx) {
     cudaFreeHost(ctx->umax_host);
     cudaFreeHost(ctx->coef_host);
     for (auto& e : ctx->coef_ev)
+        if (e) cudaEventDestroy(e);
+    for (double* p : ctx->B) cudaFree(p);
+    cudaFree(ctx->bb);
+    cudaFreeHost(ctx->bb_done_host);
+    for (auto& e : ctx->bb_ev)
         if (e) cudaEventDestroy(e);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -1140,6 +1152,328 @@ lx_status lx_step_epirk4s3a(lx_ctx* ctx, const lx_problem* pb, const double* u, 
                             double* err_out, double dt, double c, double gamma, double rtol, double atol,
                             int* iters_out) {
     return lx_step(ctx, LX_EPIRK4S3A, pb, u, u_low, u_high, err_out, dt, c, gamma, rtol, atol, iters_out);
+}
+
+
+// ============================================================== black-box right-hand side
+// (P:120-133 listing alg:RHS; P:416 finite-difference Jacobian; reading R25)
+}  // extern "C"
+
+static lx_status bb_ensure(lx_ctx* ctx) {
+    if (ctx->comm) return fail(LX_ERR_UNSUPPORTED, "black-box RHS path: single-GPU contexts only");
+    if (!ctx->bb) {
+        CUDA_TRY(cudaMalloc(&ctx->bb, sizeof(BbCtrl)));
+        CUDA_TRY(cudaHostAlloc(&ctx->bb_done_host, sizeof(int), cudaHostAllocMapped));
+        CUDA_TRY(cudaHostGetDevicePointer((void**)&ctx->bb_done_dev, ctx->bb_done_host, 0));
+        for (auto& e : ctx->bb_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    return LX_OK;
+}
+
+static double* bb_vec(lx_ctx* ctx, int i) {
+    if (!ctx->B[i]) {
+        if (cudaMalloc(&ctx->B[i], ctx->N_loc * sizeof(double)) != cudaSuccess) return nullptr;
+    }
+    return ctx->B[i];
+}
+
+namespace {
+enum { BB_FU = 0, BB_FDT = 1, BB_T1 = 2, BB_W = 9, BB_FW = 10 };
+
+struct BbRun {
+    lx_ctx* ctx;
+    lx_rhs_fn f;
+    void* user;
+    const double* u;     // linearisation state (FD) or nullptr (linear operator)
+    const double* fu;    // f(u) (FD)
+    int rec;
+
+    lx_status call_f(const double* in, double* out) {
+        f(in, out, user, (void*)ctx->stream);
+        CUDA_TRY(cudaGetLastError());
+        return LX_OK;
+    }
+    BbLin lin() const {
+        BbLin L;
+        std::memset(&L, 0, sizeof L);
+        L.N = ctx->N_loc;
+        L.N_glob = ctx->N_glob;
+        L.grid = bb_grid(ctx->nsm);
+        L.u = u;
+        L.fu = fu;
+        L.partials = ctx->partials;
+        L.ctrl = ctx->bb;
+        L.rec = ctx->rec_dev + rec;
+        return L;
+    }
+    // y = a0 x0 + a1 x1 + a2 x2 + a3 x3
+    lx_status comb(double* y, double a0, const double* x0, double a1 = 0.0, const double* x1 = nullptr,
+                   double a2 = 0.0, const double* x2 = nullptr, double a3 = 0.0, const double* x3 = nullptr) {
+        BbLin L = lin();
+        L.y0 = y;
+        L.x0 = x0; L.x1 = x1; L.x2 = x2; L.x3 = x3;
+        L.a0 = a0; L.a1 = a1; L.a2 = a2; L.a3 = a3;
+        CUDA_TRY(launch_bb_lincomb(L, ctx->stream));
+        ctx->launches++;
+        return LX_OK;
+    }
+    // F(x) = f(x) - J_FD(u) x -> out (the listing's Nonlinear_remainder, alg:exprb32)
+    lx_status remainder(const double* x, double* out) {
+        double* w = bb_vec(ctx, BB_W);
+        double* fw = bb_vec(ctx, BB_FW);
+        if (!w || !fw) return fail(LX_ERR_CUDA, "black-box buffer allocation failed");
+        LX_TRY(call_f(x, out));
+        CUDA_TRY(cudaMemsetAsync(&ctx->bb->maxbits[2], 0, sizeof(unsigned long long), ctx->stream));
+        CUDA_TRY(launch_bb_maxabs(x, ctx->N_loc, ctx->bb, bb_grid(ctx->nsm), ctx->stream));
+        BbLin L = lin();
+        L.x0 = x;
+        L.y0 = w;
+        CUDA_TRY(launch_bb_fdpiece(L, 0, ctx->stream));
+        LX_TRY(call_f(w, fw));
+        L = lin();
+        L.x0 = out;
+        L.x1 = fw;
+        L.y0 = out;
+        CUDA_TRY(launch_bb_fdpiece(L, 1, ctx->stream));
+        ctx->launches += 3;
+        return LX_OK;
+    }
+    // phi_l(a_k dt J) v -> outs[k]  (Eq. (2), stopping rule P:155)
+    lx_status leja(const double* v, double* const* outs, const double* coeffs, int K, double dt, double c,
+                   double gamma, int l, double rtol, double atol) {
+        double* w = bb_vec(ctx, BB_W);
+        double* fw = bb_vec(ctx, BB_FW);
+        if (!w || !fw) return fail(LX_ERR_CUDA, "black-box buffer allocation failed");
+        TableSpec spec{l, K, coeffs};
+        const double* tab = nullptr;
+        LX_TRY(build_tables(ctx, &spec, 1, dt, c, gamma, rec, &tab));
+        BbArgs A;
+        std::memset(&A, 0, sizeof A);
+        A.N = ctx->N_loc;
+        A.N_glob = ctx->N_glob;
+        A.K = K;
+        A.mode = u ? 1 : 2;
+        A.max_nodes = ctx->max_nodes;
+        A.grid = bb_grid(ctx->nsm);
+        A.alpha = (dt == 0.0) ? 0.0 : 1.0 / gamma;
+        A.rtol = rtol;
+        A.atol = atol;
+        A.table = tab;
+        A.u = u;
+        A.fu = fu;
+        A.w = w;
+        A.fw = fw;
+        for (int k = 0; k < K; k++) A.p[k] = outs[k];
+        A.partials = ctx->partials;
+        A.ctrl = ctx->bb;
+        A.rec = ctx->rec_dev + rec;
+        A.done_host = ctx->bb_done_dev;
+        // decision state: everything but max|u| (kept for the remainders of a step)
+        CUDA_TRY(cudaMemsetAsync(ctx->bb, 0, offsetof(BbCtrl, umaxbits), ctx->stream));
+        const int act0 = (1 << K) - 1;
+        CUDA_TRY(cudaMemcpyAsync(&ctx->bb->active, &act0, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));   // host word reset below must not race the previous call
+        *(volatile int*)ctx->bb_done_host = 0;
+        A.y_in = v;
+        CUDA_TRY(launch_bb_init(A, ctx->stream));
+        ctx->launches++;
+        for (int m = 1; m < ctx->max_nodes; m++) {
+            A.y_in = (m == 1) ? v : ctx->Y[(m - 1) & 1];
+            A.y_out = ctx->Y[m & 1];
+            if (u) {
+                CUDA_TRY(launch_bb_perturb(A, m, ctx->stream));
+                LX_TRY(call_f(w, fw));
+            } else {
+                LX_TRY(call_f(A.y_in, fw));
+            }
+            CUDA_TRY(launch_bb_update(A, m, ctx->stream));
+            ctx->launches += u ? 2 : 1;
+            CUDA_TRY(cudaEventRecord(ctx->bb_ev[m & 1], ctx->stream));
+            // one iteration in flight: wait for the decision of m - 1 while m runs
+            if (m >= 2) {
+                CUDA_TRY(cudaEventSynchronize(ctx->bb_ev[(m - 1) & 1]));
+                if (*(volatile int*)ctx->bb_done_host) break;
+            }
+        }
+        return LX_OK;
+    }
+};
+}  // namespace
+
+static lx_status bb_setup(lx_ctx* ctx, BbRun& R, lx_rhs_fn f, void* user, const double* u) {
+    LX_TRY(bb_ensure(ctx));
+    R.ctx = ctx;
+    R.f = f;
+    R.user = user;
+    R.u = u;
+    R.fu = nullptr;
+    R.rec = 0;
+    CUDA_TRY(cudaMemsetAsync(ctx->bb, 0, sizeof(BbCtrl), ctx->stream));
+    if (u) {
+        double* fu = bb_vec(ctx, BB_FU);
+        if (!fu) return fail(LX_ERR_CUDA, "black-box buffer allocation failed");
+        LX_TRY(R.call_f(u, fu));                      // f(u), unscaled (FD base point)
+        R.fu = fu;
+        // max|u| (FD scaling, R25) -> umaxbits
+        CUDA_TRY(launch_bb_maxabs(u, ctx->N_loc, ctx->bb, bb_grid(ctx->nsm), ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(&ctx->bb->umaxbits, &ctx->bb->maxbits[2], sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToDevice, ctx->stream));
+        ctx->launches++;
+    }
+    return LX_OK;
+}
+
+static lx_status bb_step(BbRun& R, lx_method method, const double* u, double* lo, double* hi, double dt, double c,
+                         double gamma, double rtol, double atol) {
+    lx_ctx* ctx = R.ctx;
+    double* t[8];
+    for (int i = 1; i <= 7; i++) {
+        t[i] = bb_vec(ctx, BB_T1 + i - 1);
+        if (!t[i]) return fail(LX_ERR_CUDA, "black-box buffer allocation failed");
+    }
+    double* f_u = bb_vec(ctx, BB_FDT);
+    if (!f_u) return fail(LX_ERR_CUDA, "black-box buffer allocation failed");
+    const double one = 1.0;
+    LX_TRY(R.comb(f_u, dt, R.fu));                    // f_u = RHS(u) dt  (alg:Ros_Eu P:468-469)
+    if (method == LX_ROSENBROCK_EULER) {
+        double* o[1] = {t[1]};
+        LX_TRY(R.leja(f_u, o, &one, 1, dt, c, gamma, 1, rtol, atol));
+        LX_TRY(R.comb(hi, 1.0, u, 1.0, t[1]));        // u + phi_1(J dt) f_u
+        if (lo && lo != hi) LX_TRY(R.comb(lo, 1.0, hi));
+        return LX_OK;
+    }
+    if (method == LX_EXPRB32) {                        // P:414-418, alg:exprb32
+        double* o[1] = {t[1]};
+        LX_TRY(R.leja(f_u, o, &one, 1, dt, c, gamma, 1, rtol, atol));
+        LX_TRY(R.comb(lo, 1.0, u, 1.0, t[1]));        // a = u_exprb2
+        LX_TRY(R.remainder(u, t[2]));                 // NL_u
+        LX_TRY(R.remainder(lo, t[3]));                // NL_a
+        LX_TRY(R.comb(t[4], dt, t[3], -dt, t[2]));    // R_a = (NL_a - NL_u) dt
+        double* o3[1] = {t[5]};
+        LX_TRY(R.leja(t[4], o3, &one, 1, dt, c, gamma, 3, rtol, atol));
+        LX_TRY(R.comb(hi, 1.0, lo, 2.0, t[5]));       // u_exprb3 = a + 2 u_nl_3
+        BbLin L = R.lin();
+        L.x0 = t[5];
+        L.a0 = 2.0;
+        CUDA_TRY(launch_bb_norm(L, ctx->stream));     // error = ||2 u_nl_3||
+        ctx->launches++;
+        return LX_OK;
+    }
+    if (method == LX_EXPRB42) {                        // reading R22
+        const double cf[2] = {0.75, 1.0};
+        double* pv[2] = {t[1], t[2]};
+        LX_TRY(R.leja(f_u, pv, cf, 2, dt, c, gamma, 1, rtol, atol));
+        LX_TRY(R.comb(t[3], 1.0, u, 0.75, t[1]));     // a
+        LX_TRY(R.remainder(u, t[4]));
+        LX_TRY(R.remainder(t[3], t[5]));
+        LX_TRY(R.comb(t[6], dt, t[5], -dt, t[4]));    // D_a
+        LX_TRY(R.comb(t[6], 32.0 / 9.0, t[6]));
+        double* o3[1] = {t[7]};
+        LX_TRY(R.leja(t[6], o3, &one, 1, dt, c, gamma, 3, rtol, atol));
+        LX_TRY(R.comb(hi, 1.0, u, 1.0, t[2], 1.0, t[7]));
+        if (lo && lo != hi) LX_TRY(R.comb(lo, 1.0, hi));
+        return LX_OK;
+    }
+    // EXPRB43 / EPIRK4s3A (reading R17)
+    const bool epirk = method == LX_EPIRK4S3A;
+    const double cf2[2] = {0.5, 1.0}, cf3[3] = {0.5, 2.0 / 3.0, 1.0};
+    double* pv[3] = {t[1], t[2], t[3]};
+    LX_TRY(R.leja(f_u, pv, epirk ? cf3 : cf2, epirk ? 3 : 2, dt, c, gamma, 1, rtol, atol));
+    double* p_half = t[1];
+    double* p_one = epirk ? t[3] : t[2];
+    double *NLu = t[4], *Da = t[5], *Db = t[6], *tmp = t[7];
+    LX_TRY(R.remainder(u, NLu));
+    LX_TRY(R.comb(lo, 1.0, u, 0.5, p_half));          // a
+    LX_TRY(R.remainder(lo, tmp));
+    LX_TRY(R.comb(Da, dt, tmp, -dt, NLu));
+    if (epirk) {
+        LX_TRY(R.comb(lo, 1.0, u, 2.0 / 3.0, t[2]));  // b
+    } else {
+        double* o[1] = {hi};
+        LX_TRY(R.leja(Da, o, &one, 1, dt, c, gamma, 1, rtol, atol));
+        LX_TRY(R.comb(lo, 1.0, u, 1.0, p_one, 1.0, hi));   // b = u + p_one + phi_1 D_a
+    }
+    LX_TRY(R.remainder(lo, tmp));
+    LX_TRY(R.comb(Db, dt, tmp, -dt, NLu));
+    const double a3 = epirk ? 32.0 : 16.0, b3 = epirk ? -13.5 : -2.0;
+    const double a4 = epirk ? -144.0 : -48.0, b4 = epirk ? 81.0 : 12.0;
+    LX_TRY(R.comb(tmp, a3, Da, b3, Db));              // w3
+    LX_TRY(R.comb(NLu, a4, Da, b4, Db));              // w4
+    double* o3[1] = {Da};
+    LX_TRY(R.leja(tmp, o3, &one, 1, dt, c, gamma, 3, rtol, atol));
+    double* o4[1] = {Db};
+    LX_TRY(R.leja(NLu, o4, &one, 1, dt, c, gamma, 4, rtol, atol));
+    LX_TRY(R.comb(lo, 1.0, u, 1.0, p_one, 1.0, Da));  // u3
+    LX_TRY(R.comb(hi, 1.0, lo, 1.0, Db));             // u4
+    BbLin L = R.lin();
+    L.x0 = hi;
+    L.a0 = 1.0;
+    L.x1 = lo;
+    L.a1 = -1.0;
+    CUDA_TRY(launch_bb_norm(L, ctx->stream));         // err = ||u4 - u3||
+    ctx->launches++;
+    return LX_OK;
+}
+
+extern "C" {
+
+void lx_builtin_rhs(const double* in, double* out, void* user, void* cuda_stream) {
+    (void)cuda_stream;
+    const lx_builtin_rhs_user* b = (const lx_builtin_rhs_user*)user;
+    if (!b || !b->ctx || !b->pb) return;
+    rhs_device(b->ctx, b->pb, in, 1.0, out);
+}
+
+lx_status lx_real_leja_phi_cb(lx_ctx* ctx, lx_rhs_fn f, void* user, const double* u, const double* v,
+                              double* const* outs, const double* coeffs, int K, double dt, double c, double gamma,
+                              int l, double rtol, double atol, int* iters_out) {
+    if (!ctx || !f) return fail(LX_ERR_ARG, "NULL argument");
+    lx_problem pb;
+    std::memset(&pb, 0, sizeof pb);
+    LX_TRY(validate_leja(&pb, u, v, outs, coeffs, K, dt, gamma, l));
+    Staging sg(ctx);
+    const double *vd, *ud;
+    double* od[kMaxK];
+    LX_TRY(sg.in(v, &vd));
+    LX_TRY(sg.in(u, &ud));
+    for (int k = 0; k < K; k++) LX_TRY(sg.out(outs[k], &od[k]));
+    BbRun R;
+    LX_TRY(bb_setup(ctx, R, f, user, ud));
+    LX_TRY(reset_record(ctx, 0));
+    LX_TRY(R.leja(vd, od, coeffs, K, dt, c, gamma, l, rtol, atol));
+    LX_TRY(sg.finish());
+    Record r;
+    LX_TRY(read_record(ctx, 0, &r));
+    if (iters_out) *iters_out = r.iters;
+    return status_of(r);
+}
+
+lx_status lx_step_cb(lx_ctx* ctx, lx_method method, lx_rhs_fn f, void* user, const double* u, double* u_low,
+                     double* u_high, double* err_out, double dt, double c, double gamma, double rtol, double atol,
+                     int* iters_out) {
+    if (!ctx || !f || !u || !u_high) return fail(LX_ERR_ARG, "NULL argument");
+    if ((int)method < 0 || (int)method > 4) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
+    if (method != LX_ROSENBROCK_EULER && method != LX_EXPRB42 && !u_low)
+        return fail(LX_ERR_ARG, "u_low required for embedded methods");
+    if (u_low == u || u_high == u) return fail(LX_ERR_ALIAS, "outputs must not alias u");
+    if (u_low && u_low == u_high) return fail(LX_ERR_ALIAS, "u_low must differ from u_high");
+    if (!(gamma > 0.0) && dt != 0.0) return fail(LX_ERR_ARG, "gamma must be > 0 (got %g)", gamma);
+    Staging sg(ctx);
+    const double* ud;
+    double *lo, *hi;
+    LX_TRY(sg.in(u, &ud));
+    LX_TRY(sg.out(u_low, &lo));
+    LX_TRY(sg.out(u_high, &hi));
+    BbRun R;
+    LX_TRY(bb_setup(ctx, R, f, user, ud));
+    LX_TRY(reset_record(ctx, 0));
+    LX_TRY(bb_step(R, method, ud, lo, hi, dt, c, gamma, rtol, atol));
+    LX_TRY(sg.finish());
+    Record r;
+    LX_TRY(read_record(ctx, 0, &r));
+    if (iters_out) *iters_out = r.iters;
+    if (err_out) *err_out = (method == LX_ROSENBROCK_EULER || method == LX_EXPRB42) ? 0.0 : r.err;
+    return status_of(r);
 }
 
 }  // extern "C"

@@ -209,4 +209,57 @@ struct CoefJobs {
 cudaError_t launch_coef_tables(const double* xi, const double* R, int M, const CoefJobs& jobs, double dt, double c,
                                double gamma, const double* cg_dev, int* status, cudaStream_t s);
 
+// ---------------------------------------------------------------- black-box RHS path (lx_blackbox.cu)
+// Control block of the callback-driven Leja loop: decision + FD scaling state.
+struct BbCtrl {
+    int done;                          // decision: stop (kernels of later iterations return at entry)
+    int active;                        // bit k = accumulator k still accumulating
+    int status;
+    int m;                             // last decided iteration
+    unsigned int ticket;               // last-CTA ticket
+    unsigned int pad;
+    unsigned long long maxbits[3];     // max|y| of y_{m} at [m & 1]; [2]: remainder direction (bit patterns)
+    unsigned long long umaxbits;       // max|u| (FD scaling, R25)
+};
+struct BbArgs {
+    long long N;                       // local points
+    double N_glob;
+    int K, mode;                       // mode 1 = FD Jacobian, 2 = linear operator (J y = f(y))
+    int max_nodes, grid;
+    double alpha, rtol, atol;
+    const double* table;               // [max_nodes][1+K]: beta_m, d_m^(k) (k_coef_tables)
+    const double* u;                   // linearisation state (FD)
+    const double* fu;                  // f(u) (FD)
+    const double* y_in;                // y_{m-1} (v at m = 1)
+    double* y_out;                     // y_m
+    double* w;                         // perturbed state u + eps y_{m-1}
+    const double* fw;                  // f(w) (FD) or f(y_{m-1}) (linear)
+    double* p[kMaxK];
+    double* partials;                  // [grid][1+K]
+    BbCtrl* ctrl;
+    Record* rec;
+    int* done_host;                    // mapped pinned word: iteration at which the loop stopped
+};
+struct BbLin {
+    long long N;
+    double N_glob;
+    int grid;
+    const double* x0; const double* x1; const double* x2; const double* x3;
+    double a0, a1, a2, a3;
+    double* y0;
+    const double* u;
+    const double* fu;
+    double* partials;
+    BbCtrl* ctrl;
+    Record* rec;
+};
+int bb_grid(int nsm);
+cudaError_t launch_bb_init(const BbArgs& A, cudaStream_t s);
+cudaError_t launch_bb_perturb(const BbArgs& A, int m, cudaStream_t s);
+cudaError_t launch_bb_update(const BbArgs& A, int m, cudaStream_t s);
+cudaError_t launch_bb_maxabs(const double* x, long long N, BbCtrl* c, int grid, cudaStream_t s);
+cudaError_t launch_bb_fdpiece(const BbLin& L, int op, cudaStream_t s);   // 0: u + eps x0 ; 1: x0 - (x1 - fu)/eps
+cudaError_t launch_bb_lincomb(const BbLin& L, cudaStream_t s);
+cudaError_t launch_bb_norm(const BbLin& L, cudaStream_t s);
+
 }  // namespace lx
