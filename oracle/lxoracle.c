@@ -578,7 +578,8 @@ done:
 /* ------------------------------------------------------------------------- */
 /* Exponential integrators (listings alg:Ros_Eu, alg:exprb32;      */
 /* EXPRB43 and EPIRK4s3A tableaux from P:83's citations, R17).                */
-/*   method 0 Rosenbrock-Euler, 1 EXPRB32, 2 EXPRB43, 3 EPIRK4s3A, 4 EXPRB42.   */
+/*   method 0 Rosenbrock-Euler, 1 EXPRB32, 2 EXPRB43, 3 EPIRK4s3A, 4 EXPRB42,    */
+/*   5 EPIRK5P1.                                                               */
 /* u_low may be NULL for Rosenbrock-Euler (non-embedded, err = 0).            */
 /* ------------------------------------------------------------------------- */
 static void axpby(double a, const double *x, double b, const double *y, double *z, long N)
@@ -603,7 +604,7 @@ int oc_step_ex(const oc_problem *pb, int jac_mode, int method, const double *u, 
     int it = 0, total = 0, s = OC_OK;
     if (err) *err = 0.0;
     if (iters) *iters = 0;
-    if (method < 0 || method > 4) return OC_ERR_ARG;
+    if (method < 0 || method > 5) return OC_ERR_ARG;
     if (jac_mode != OC_JAC_EXACT && jac_mode != OC_JAC_FD) return OC_ERR_ARG;
     size_t bytes = sizeof(double) * (size_t)N;
     double *fu_raw = NULL;
@@ -670,6 +671,45 @@ int oc_step_ex(const oc_problem *pb, int jac_mode, int method, const double *u, 
         total += it;
         if (s) goto out;
         for (long i = 0; i < N; i++) u_high[i] = u[i] + t2[i] + t7[i];
+        if (u_low) for (long i = 0; i < N; i++) u_low[i] = u_high[i];
+    } else if (method == 5) {
+        /* EPIRK5P1 (Tokman, Loffeld & Tranquilli 2012, cited at P:83 and run in Table 2, P:616-634;
+         * reading R26), psi functions = (phi_1, phi_1, phi_3), R(x) = h (F(x) - F(u)):
+         *   Y1 = u + a11 h phi_1(g11 hJ) f
+         *   Y2 = u + a21 h phi_1(g21 hJ) f + a22 phi_1(g22 hJ) R(Y1)
+         *   u+ = u + b1 h phi_1(g31 hJ) f + b2 phi_1(g32 hJ) R(Y1) + b3 phi_3(g33 hJ) (R(Y2) - 2 R(Y1))
+         * non-embedded here (u_low = u_high, err = 0). */
+        const double a11 = 0.35129592695058193092, a21 = 0.84405472011657126298, a22 = 1.6905891609568963624;
+        const double b1 = 1.0, b2 = 1.2727127317356892397, b3 = 2.2714599265422622275;
+        const double g11 = 0.35129592695058193092, g21 = 0.84405472011657126298, g22 = 1.0;
+        const double g31 = 1.0, g32 = 0.71111095364366870359, g33 = 0.62378111953371494809;
+        double cf3[3] = {g11, g21, g31};                     /* vertical phi_1 on f h */
+        double *pv[3] = {t1, t2, t3};
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, f_u, pv, cf3, 3, dt, c, gamma, 1, rtol, atol, xi,
+                                max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        remainder_mode(pb, jac_mode, u, fu_raw, u, t4);      /* NL_u */
+        axpby(1.0, u, a11, t1, t5, N);                       /* Y1 */
+        remainder_mode(pb, jac_mode, u, fu_raw, t5, t6);     /* NL_Y1 */
+        axpby(dt, t6, -dt, t4, t5, N);                       /* R1 = h (F(Y1) - F(u)) */
+        double cf2[2] = {g32, g22};                          /* vertical phi_1 on R1 */
+        double *qv[2] = {t6, t7};
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, t5, qv, cf2, 2, dt, c, gamma, 1, rtol, atol, xi,
+                                max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        for (long i = 0; i < N; i++) t1[i] = u[i] + a21 * t2[i] + a22 * t7[i];   /* Y2 */
+        remainder_mode(pb, jac_mode, u, fu_raw, t1, t2);     /* NL_Y2 */
+        axpby(dt, t2, -dt, t4, t7, N);                       /* R2 */
+        axpby(1.0, t7, -2.0, t5, t2, N);                     /* R2 - 2 R1 */
+        double one33 = g33;
+        double *o3[1] = {t7};
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, t2, o3, &one33, 1, dt, c, gamma, 3, rtol, atol, xi,
+                                max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        for (long i = 0; i < N; i++) u_high[i] = u[i] + b1 * t3[i] + b2 * t6[i] + b3 * t7[i];
         if (u_low) for (long i = 0; i < N; i++) u_low[i] = u_high[i];
     } else {
         /* EXPRB43 (method 2) / EPIRK4s3A (method 3) -- R17 tableaux:

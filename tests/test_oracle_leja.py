@@ -155,7 +155,7 @@ def test_leja_noconv_and_errors(xi300):
 
 
 # ---------------------------------------------------------------- integrators
-@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42"])
+@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1"])
 def test_integrator_linear_exactness(xi300, method):
     # every exponential integrator is exact on linear homogeneous problems
     n = 64
@@ -168,7 +168,7 @@ def test_integrator_linear_exactness(xi300, method):
     sym = refs.impulse_symbol(lambda x: O.jac_apply(pb, None, x), (n, n))
     ex = refs.fft_apply_phi(sym, u0, dt, 0)
     assert np.linalg.norm(r.u_high - ex) <= 1e-11 * np.linalg.norm(ex)
-    if method not in ("rosenbrock_euler", "exprb42"):
+    if method not in ("rosenbrock_euler", "exprb42", "epirk5p1"):
         assert r.err == 0.0       # R18: F == 0 exactly for linear f
 
 
@@ -273,3 +273,44 @@ def test_integrator_order_burgers(xi300, method, order):
         errs.append(np.linalg.norm(u.ravel() - ref) / np.linalg.norm(ref))
     orders = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
     assert abs(orders[-1] - order) < 0.3, (errs, orders)
+
+
+def test_epirk5p1_fifth_order(xi300):
+    # EPIRK5P1 (reading R26): fifth order on Allen-Cahn (exact Jacobian) against scipy DOP853;
+    # a mistyped tableau constant drops the observed order to ~2 (survey of perturbed b3)
+    n = 16
+    pb = O.Problem((n, n), (2 / n, 2 / n), 2e-3, 0.0, 1.0)
+    u0 = W.ic_allen_cahn_2d(n)
+    T = 0.5
+    uref = _allen_cahn_reference(pb, u0, T)
+    errs = []
+    for nsteps in (4, 8, 16):
+        h = T / nsteps
+        u = u0.copy()
+        for _ in range(nsteps):
+            c, g = _cg(pb, u)
+            r = O.step(pb, "epirk5p1", u, h, c, g, 1e-14, 1e-14, xi300)
+            assert r.status == O.OK and r.err == 0.0
+            u = r.u_high
+        errs.append(np.linalg.norm(u - uref) / np.linalg.norm(uref))
+    orders = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+    assert np.all(orders > 4.7) and np.all(orders < 6.0), (errs, orders)
+
+
+def test_epirk5p1_fifth_order_burgers(xi300):
+    n, T = 24, 0.005
+    pb = O.Problem((n, n), (2 / n, 2 / n), 1.0, 0.0, 0.0, None, 10.0)
+    u0 = W.ic_burgers_2d(n)
+    ref = scipy.integrate.solve_ivp(lambda t, y: O.rhs(pb, y.reshape(n, n)).ravel(), (0, T), u0.ravel(),
+                                    method="DOP853", rtol=1e-13, atol=1e-13).y[:, -1]
+    errs = []
+    for ns in (2, 4, 8):
+        u = u0.copy()
+        for _ in range(ns):
+            c, g = _cg(pb, u)
+            r = O.step(pb, "epirk5p1", u, T / ns, c, g, 1e-14, 1e-14, xi300)
+            assert r.status == O.OK
+            u = r.u_high
+        errs.append(np.linalg.norm(u.ravel() - ref) / np.linalg.norm(ref))
+    orders = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+    assert orders[-1] > 4.5, (errs, orders)
