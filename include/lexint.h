@@ -214,7 +214,8 @@ typedef enum {
     LX_EXPRB32 = 1,
     LX_EXPRB43 = 2,
     LX_EPIRK4S3A = 3,
-    LX_EXPRB42 = 4        /* Luan 2017 (cited at P:83), 4th order, non-embedded (err = 0) */
+    LX_EXPRB42 = 4,       /* Luan 2017 (cited at P:83), 4th order, non-embedded (err = 0) */
+    LX_EPIRK5P1 = 5       /* Tokman et al. 2012 (cited at P:83, Table 2), 5th order, non-embedded (R26) */
 } lx_method;
 
 /* Rosenbrock-Euler: u_out = u + phi_1(dt J(u)) f(u) dt (alg:Ros_Eu). */
@@ -233,6 +234,10 @@ lx_status lx_step_epirk4s3a(lx_ctx *ctx, const lx_problem *pb, const double *u, 
 /* EXPRB42 (reading R22): a = u + 3/4 hphi_1(3/4 hJ) f; u_out = u + hphi_1(hJ) f + 32/9 hphi_3(hJ) D_a. */
 lx_status lx_step_exprb42(lx_ctx *ctx, const lx_problem *pb, const double *u, double *u_out, double dt,
                           double c, double gamma, double rtol, double atol, int *iters_out);
+/* EPIRK5P1 (reading R26): Y1 = u + a11 hphi_1(g11 hJ) f; Y2 = u + a21 hphi_1(g21 hJ) f + a22 phi_1(hJ) R(Y1);
+ * u_out = u + hphi_1(hJ) f + b2 phi_1(g32 hJ) R(Y1) + b3 phi_3(g33 hJ)(R(Y2) - 2R(Y1)), R(x) = h(F(x) - F(u)). */
+lx_status lx_step_epirk5p1(lx_ctx *ctx, const lx_problem *pb, const double *u, double *u_out, double dt,
+                           double c, double gamma, double rtol, double atol, int *iters_out);
 /* Dispatch by method (the paper's exp_int / embed_exp_int). */
 lx_status lx_step(lx_ctx *ctx, lx_method method, const lx_problem *pb, const double *u,
                   double *u_low, double *u_high, double *err_out, double dt, double c,

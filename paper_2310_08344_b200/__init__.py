@@ -31,8 +31,8 @@ LX_ERR_TIMEOUT = 10
 STATUS_NAMES = {0: "LX_OK", 1: "LX_ERR_ARG", 2: "LX_ERR_DIM", 3: "LX_ERR_ALIAS", 4: "LX_ERR_UNSUPPORTED",
                 5: "LX_ERR_NOCONV", 6: "LX_ERR_NONFINITE", 7: "LX_ERR_UNKNOWN_INTEGRATOR", 8: "LX_ERR_CUDA",
                 9: "LX_ERR_NCCL", 10: "LX_ERR_TIMEOUT"}
-LX_ROSENBROCK_EULER, LX_EXPRB32, LX_EXPRB43, LX_EPIRK4S3A, LX_EXPRB42 = 0, 1, 2, 3, 4
-METHODS = {"rosenbrock_euler": 0, "exprb32": 1, "exprb43": 2, "epirk4s3a": 3, "exprb42": 4}
+LX_ROSENBROCK_EULER, LX_EXPRB32, LX_EXPRB43, LX_EPIRK4S3A, LX_EXPRB42, LX_EPIRK5P1 = 0, 1, 2, 3, 4, 5
+METHODS = {"rosenbrock_euler": 0, "exprb32": 1, "exprb43": 2, "epirk4s3a": 3, "exprb42": 4, "epirk5p1": 5}
 
 # Every symbol include/lexint.h declares (checked by tests/test_abi.py).
 EXPORTS = ("lx_last_error", "lx_version", "lx_leja_points", "lx_phi_scalar", "lx_divided_differences",
@@ -40,7 +40,7 @@ EXPORTS = ("lx_last_error", "lx_version", "lx_leja_points", "lx_phi_scalar", "lx
            "lx_ctx_local", "lx_ctx_synchronize", "lx_ctx_launch_count", "lx_spectrum_estimate",
            "lx_spectrum_bound", "lx_shift_scale", "lx_real_leja_phi", "lx_real_leja_phi_vertical",
            "lx_step_rosenbrock_euler", "lx_step_exprb32", "lx_step_exprb43", "lx_step_epirk4s3a",
-           "lx_step_exprb42",
+           "lx_step_exprb42", "lx_step_epirk5p1",
            "lx_step", "lx_rhs", "lx_integrate", "lx_local_group_create", "lx_local_group_destroy", "lx_ctx_set_comm_local",
            "lx_real_leja_phi_cb", "lx_step_cb", "lx_builtin_rhs")
 
@@ -126,6 +126,7 @@ def lib() -> ctypes.CDLL:
             "lx_step_exprb43": (ctypes.c_int, [vp, pbp, vp, vp, vp, dp, d, d, d, d, d, ip]),
             "lx_step_epirk4s3a": (ctypes.c_int, [vp, pbp, vp, vp, vp, dp, d, d, d, d, d, ip]),
             "lx_step_exprb42": (ctypes.c_int, [vp, pbp, vp, vp, d, d, d, d, d, ip]),
+            "lx_step_epirk5p1": (ctypes.c_int, [vp, pbp, vp, vp, d, d, d, d, d, ip]),
             "lx_rhs": (ctypes.c_int, [vp, pbp, vp, d, vp]),
             "lx_integrate": (ctypes.c_int, [vp, ctypes.c_int, pbp, vp, d, ctypes.c_int, d, d, ip, dp]),
             "lx_local_group_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(vp)]),
@@ -345,6 +346,10 @@ def lx_step_rosenbrock_euler(ctx, u, u_out, dt, c, gamma, rtol, atol, problem=No
 
 def lx_step_exprb42(ctx, u, u_out, dt, c, gamma, rtol, atol, problem=None):
     return lx_step(ctx, LX_EXPRB42, u, None, u_out, dt, c, gamma, rtol, atol, problem)[0]
+
+
+def lx_step_epirk5p1(ctx, u, u_out, dt, c, gamma, rtol, atol, problem=None):
+    return lx_step(ctx, LX_EPIRK5P1, u, None, u_out, dt, c, gamma, rtol, atol, problem)[0]
 
 
 def lx_step_exprb32(ctx, u, u_low, u_high, dt, c, gamma, rtol, atol, problem=None):

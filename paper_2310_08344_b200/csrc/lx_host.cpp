@@ -47,7 +47,7 @@ static lx_status fail(lx_status s, const char* fmt, ...) {
     } while (0)
 
 static constexpr int kCoefSlots = 32;
-static constexpr int kStage = 7;   // integrator scratch vectors (4 stages + 3 states for lx_integrate)
+static constexpr int kStage = 8;   // integrator scratch vectors (4 stages + 3 states for lx_integrate + 1 EPIRK5P1)
 static constexpr int kHost = 6;    // host-pointer staging vectors
 static constexpr int kBb = 11;     // black-box path vectors
 
@@ -898,6 +898,17 @@ static lx_status stage_remainder(lx_ctx* ctx, const lx_problem* pb, int rec, con
     return LX_OK;
 }
 
+// Non-embedded methods: err = 0, u_low optional (a copy of u_high).
+static bool nonembedded(lx_method m) { return m == LX_ROSENBROCK_EULER || m == LX_EXPRB42 || m == LX_EPIRK5P1; }
+
+// EPIRK5P1 tableau (reading R26; Tokman, Loffeld & Tranquilli 2012, cited at P:83)
+namespace epirk5 {
+constexpr double a11 = 0.35129592695058193092, a21 = 0.84405472011657126298, a22 = 1.6905891609568963624;
+constexpr double b1 = 1.0, b2 = 1.2727127317356892397, b3 = 2.2714599265422622275;
+constexpr double g11 = 0.35129592695058193092, g21 = 0.84405472011657126298, g22 = 1.0;
+constexpr double g31 = 1.0, g32 = 0.71111095364366870359, g33 = 0.62378111953371494809;
+}  // namespace epirk5
+
 static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb, const double* u, double* lo,
                              double* hi, double dt, double c, double gamma, double rtol, double atol, int rec) {
     const bool diag = pb->react != 0.0;
@@ -920,6 +931,13 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
         } else if (method == LX_EXPRB42) {
             specs[n++] = {1, 2, c42};
             specs[n++] = {3, 1, c1};
+        } else if (method == LX_EPIRK5P1) {
+            static const double e3[3] = {epirk5::g11, epirk5::g21, epirk5::g31};
+            static const double e2[2] = {epirk5::g32, epirk5::g22};
+            static const double e1[1] = {epirk5::g33};
+            specs[n++] = {1, 3, e3};
+            specs[n++] = {1, 2, e2};
+            specs[n++] = {3, 1, e1};
         } else if (method == LX_EXPRB43) {
             specs[n++] = {1, 2, c2};
             specs[n++] = {1, 1, c1};
@@ -978,6 +996,35 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
         if (lo && lo != hi) CUDA_TRY(cudaMemcpyAsync(lo, hi, ctx->N_loc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
         return LX_OK;
     }
+    if (method == LX_EPIRK5P1) {
+        // reading R26: R(x) = dt (F(x) - F(u)); vertical phi_1 {g11, g21, 1} on f dt, vertical phi_1 {g32, 1}
+        // on R(Y1), phi_3(g33 hJ) on R(Y2) - 2 R(Y1)
+        using namespace epirk5;
+        double* S1 = scratch(ctx, 1);
+        double* S2 = scratch(ctx, 2);
+        double* S3 = scratch(ctx, 3);
+        double* S7 = scratch(ctx, 7);
+        if (!S1 || !S2 || !S3 || !S7) return fail(LX_ERR_CUDA, "scratch allocation failed");
+        const double e3[3] = {g11, g21, g31}, e2[2] = {g32, g22}, e1[1] = {g33};
+        double* pv[3] = {S1, S2, S3};
+        LX_TRY(leja_device(ctx, pb, ul, S0, pv, e3, 3, dt, c, gamma, 1, rtol, atol, rec, tab[0]));
+        // R1 = dt F(u + a11 P1) - dt F(u) -> S0 (f dt consumed)
+        LX_TRY(stage_remainder(ctx, pb, rec, u, u, S1, a11, nullptr, 0.0, 1.0, dt, S0, hi));
+        double* qv[2] = {S1, hi};                            // Q1 = phi_1(g32 hJ) R1, Q2 = phi_1(hJ) R1
+        LX_TRY(leja_device(ctx, pb, ul, S0, qv, e2, 2, dt, c, gamma, 1, rtol, atol, rec, tab[1]));
+        // R2 = dt F(u + a21 P2 + a22 Q2) - dt F(u) -> S2
+        LX_TRY(stage_remainder(ctx, pb, rec, u, u, S2, a21, hi, a22, 1.0, dt, S7, S2));
+        A = stage_args(ctx, pb, rec);
+        A.x0 = S7; A.x1 = S0; A.a0 = 1.0; A.a1 = -2.0; A.y0 = S0;  // R2 - 2 R1
+        LX_TRY(run_stage(ctx, ST_AXPBY, A));
+        double* o3[1] = {S2};
+        LX_TRY(leja_device(ctx, pb, ul, S0, o3, e1, 1, dt, c, gamma, 3, rtol, atol, rec, tab[2]));
+        A = stage_args(ctx, pb, rec);
+        A.x0 = u; A.x1 = S3; A.x2 = S1; A.x3 = S2; A.a0 = b1; A.a1 = b2; A.a2 = b3; A.y0 = hi;
+        LX_TRY(run_stage(ctx, ST_LIN4, A));
+        if (lo && lo != hi) CUDA_TRY(cudaMemcpyAsync(lo, hi, ctx->N_loc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+        return LX_OK;
+    }
     // EXPRB43 / EPIRK4s3A (reading R17)
     const bool epirk = method == LX_EPIRK4S3A;
     double* S1 = scratch(ctx, 1);
@@ -1029,9 +1076,9 @@ lx_status lx_step(lx_ctx* ctx, lx_method method, const lx_problem* pb0, const do
     const lx_problem* pb = &pbs;
     if (!ctx) return fail(LX_ERR_ARG, "ctx is NULL");
     LX_TRY(check_problem(ctx, pb));
-    if ((int)method < 0 || (int)method > 4) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
+    if ((int)method < 0 || (int)method > 5) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
     if (!u || !u_high) return fail(LX_ERR_ARG, "NULL argument");
-    if (method != LX_ROSENBROCK_EULER && method != LX_EXPRB42 && !u_low)
+    if (!nonembedded(method) && !u_low)
         return fail(LX_ERR_ARG, "u_low required for embedded methods");
     if (u_low == u || u_high == u) return fail(LX_ERR_ALIAS, "outputs must not alias u");
     if (u_low && u_low == u_high) return fail(LX_ERR_ALIAS, "u_low must differ from u_high");
@@ -1052,7 +1099,7 @@ lx_status lx_step(lx_ctx* ctx, lx_method method, const lx_problem* pb0, const do
     Record r;
     LX_TRY(read_record(ctx, 0, &r));
     if (iters_out) *iters_out = r.iters;
-    if (err_out) *err_out = (method == LX_ROSENBROCK_EULER || method == LX_EXPRB42) ? 0.0 : r.err;
+    if (err_out) *err_out = nonembedded(method) ? 0.0 : r.err;
     return status_of(r);
 }
 
@@ -1065,7 +1112,7 @@ lx_status lx_integrate(lx_ctx* ctx, lx_method method, const lx_problem* pb0, dou
     lx_problem pbs = *pb0;
     const lx_problem* pb = &pbs;
     LX_TRY(check_problem(ctx, pb));
-    if ((int)method < 0 || (int)method > 4) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
+    if ((int)method < 0 || (int)method > 5) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
     if (nsteps < 0) return fail(LX_ERR_ARG, "nsteps < 0");
     if (!std::isfinite(dt)) return fail(LX_ERR_ARG, "dt not finite");
     Staging sg(ctx);
@@ -1127,13 +1174,18 @@ lx_status lx_integrate(lx_ctx* ctx, lx_method method, const lx_problem* pb0, dou
     Record r;
     LX_TRY(read_record(ctx, 0, &r));
     if (iters_out) *iters_out = r.iters;
-    if (err_out) *err_out = (method == LX_ROSENBROCK_EULER || method == LX_EXPRB42) ? 0.0 : r.err;
+    if (err_out) *err_out = nonembedded(method) ? 0.0 : r.err;
     return status_of(r);
 }
 
 lx_status lx_step_exprb42(lx_ctx* ctx, const lx_problem* pb, const double* u, double* u_out, double dt, double c,
                           double gamma, double rtol, double atol, int* iters_out) {
     return lx_step(ctx, LX_EXPRB42, pb, u, nullptr, u_out, nullptr, dt, c, gamma, rtol, atol, iters_out);
+}
+
+lx_status lx_step_epirk5p1(lx_ctx* ctx, const lx_problem* pb, const double* u, double* u_out, double dt, double c,
+                           double gamma, double rtol, double atol, int* iters_out) {
+    return lx_step(ctx, LX_EPIRK5P1, pb, u, nullptr, u_out, nullptr, dt, c, gamma, rtol, atol, iters_out);
 }
 
 lx_status lx_step_rosenbrock_euler(lx_ctx* ctx, const lx_problem* pb, const double* u, double* u_out, double dt,
@@ -1374,6 +1426,27 @@ static lx_status bb_step(BbRun& R, lx_method method, const double* u, double* lo
         if (lo && lo != hi) LX_TRY(R.comb(lo, 1.0, hi));
         return LX_OK;
     }
+    if (method == LX_EPIRK5P1) {                       // reading R26
+        using namespace epirk5;
+        const double e3[3] = {g11, g21, g31}, e2[2] = {g32, g22}, e1[1] = {g33};
+        double* pv[3] = {t[1], t[2], t[3]};
+        LX_TRY(R.leja(f_u, pv, e3, 3, dt, c, gamma, 1, rtol, atol));
+        LX_TRY(R.remainder(u, t[4]));                 // NL_u
+        LX_TRY(R.comb(t[5], 1.0, u, a11, t[1]));      // Y1
+        LX_TRY(R.remainder(t[5], t[6]));
+        LX_TRY(R.comb(t[5], dt, t[6], -dt, t[4]));    // R1
+        double* qv[2] = {t[6], t[7]};
+        LX_TRY(R.leja(t[5], qv, e2, 2, dt, c, gamma, 1, rtol, atol));
+        LX_TRY(R.comb(t[1], 1.0, u, a21, t[2], a22, t[7]));   // Y2
+        LX_TRY(R.remainder(t[1], t[2]));
+        LX_TRY(R.comb(t[7], dt, t[2], -dt, t[4]));    // R2
+        LX_TRY(R.comb(t[2], 1.0, t[7], -2.0, t[5]));  // R2 - 2 R1
+        double* o3[1] = {t[7]};
+        LX_TRY(R.leja(t[2], o3, e1, 1, dt, c, gamma, 3, rtol, atol));
+        LX_TRY(R.comb(hi, 1.0, u, b1, t[3], b2, t[6], b3, t[7]));
+        if (lo && lo != hi) LX_TRY(R.comb(lo, 1.0, hi));
+        return LX_OK;
+    }
     // EXPRB43 / EPIRK4s3A (reading R17)
     const bool epirk = method == LX_EPIRK4S3A;
     const double cf2[2] = {0.5, 1.0}, cf3[3] = {0.5, 2.0 / 3.0, 1.0};
@@ -1452,8 +1525,8 @@ lx_status lx_step_cb(lx_ctx* ctx, lx_method method, lx_rhs_fn f, void* user, con
                      double* u_high, double* err_out, double dt, double c, double gamma, double rtol, double atol,
                      int* iters_out) {
     if (!ctx || !f || !u || !u_high) return fail(LX_ERR_ARG, "NULL argument");
-    if ((int)method < 0 || (int)method > 4) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
-    if (method != LX_ROSENBROCK_EULER && method != LX_EXPRB42 && !u_low)
+    if ((int)method < 0 || (int)method > 5) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
+    if (!nonembedded(method) && !u_low)
         return fail(LX_ERR_ARG, "u_low required for embedded methods");
     if (u_low == u || u_high == u) return fail(LX_ERR_ALIAS, "outputs must not alias u");
     if (u_low && u_low == u_high) return fail(LX_ERR_ALIAS, "u_low must differ from u_high");
@@ -1472,7 +1545,7 @@ lx_status lx_step_cb(lx_ctx* ctx, lx_method method, lx_rhs_fn f, void* user, con
     Record r;
     LX_TRY(read_record(ctx, 0, &r));
     if (iters_out) *iters_out = r.iters;
-    if (err_out) *err_out = (method == LX_ROSENBROCK_EULER || method == LX_EXPRB42) ? 0.0 : r.err;
+    if (err_out) *err_out = nonembedded(method) ? 0.0 : r.err;
     return status_of(r);
 }
 

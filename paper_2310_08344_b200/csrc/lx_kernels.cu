@@ -2236,7 +2236,7 @@ __global__ void __launch_bounds__(kThreads) k_stage_pointwise(const __grid_const
     // before any store (outputs may alias inputs element-wise, which blocks the compiler from
     // overlapping trips on its own), so every thread keeps UN x (inputs) 16-byte loads in flight.
     constexpr int UN = 4;
-    constexpr int NIN = (OP == ST_FINAL4) ? 4 : (OP == ST_STAGE_REMAINDER) ? 4
+    constexpr int NIN = (OP == ST_FINAL4 || OP == ST_LIN4) ? 4 : (OP == ST_STAGE_REMAINDER) ? 4
                         : (OP == ST_SUM3 || OP == ST_LIN3) ? 3 : (OP == ST_MAXSQ) ? 1 : 2;
     __shared__ double s_red[kWarps][kSlot];
     __shared__ int s_last;
@@ -2309,6 +2309,10 @@ __global__ void __launch_bounds__(kThreads) k_stage_pointwise(const __grid_const
             } else if (OP == ST_LIN3) {
                 const double2 x = v[q][0], y = v[q][1], z = v[q][2];
                 st2(A.y0 + o, make_double2(x.x + A.a0 * y.x + A.a1 * z.x, x.y + A.a0 * y.y + A.a1 * z.y));
+            } else if (OP == ST_LIN4) {
+                const double2 x = v[q][0], y = v[q][1], z = v[q][2], w = v[q][3];
+                st2(A.y0 + o, make_double2(x.x + A.a0 * y.x + A.a1 * z.x + A.a2 * w.x,
+                                           x.y + A.a0 * y.y + A.a1 * z.y + A.a2 * w.y));
             } else if (OP == ST_SUM3) {
                 const double2 x = v[q][0], y = v[q][1], z = v[q][2];
                 st2(A.y0 + o, make_double2(x.x + y.x + z.x, x.y + y.y + z.y));
@@ -2361,6 +2365,7 @@ static void* stage_kernel_ptr(int op) {
         case ST_MAXSQ: return (void*)k_stage_pointwise<ST_MAXSQ>;
         case ST_SUM3: return (void*)k_stage_pointwise<ST_SUM3>;
         case ST_LIN3: return (void*)k_stage_pointwise<ST_LIN3>;
+        case ST_LIN4: return (void*)k_stage_pointwise<ST_LIN4>;
     }
     return nullptr;
 }
@@ -2407,6 +2412,7 @@ cudaError_t launch_stage(int op, const StageArgs& A, cudaStream_t s) {
         case ST_MAXSQ: k_stage_pointwise<ST_MAXSQ><<<g, b, 0, s>>>(A); break;
         case ST_SUM3: k_stage_pointwise<ST_SUM3><<<g, b, 0, s>>>(A); break;
         case ST_LIN3: k_stage_pointwise<ST_LIN3><<<g, b, 0, s>>>(A); break;
+        case ST_LIN4: k_stage_pointwise<ST_LIN4><<<g, b, 0, s>>>(A); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
