@@ -579,7 +579,7 @@ done:
 /* Exponential integrators (listings alg:Ros_Eu, alg:exprb32;      */
 /* EXPRB43 and EPIRK4s3A tableaux from P:83's citations, R17).                */
 /*   method 0 Rosenbrock-Euler, 1 EXPRB32, 2 EXPRB43, 3 EPIRK4s3A, 4 EXPRB42,    */
-/*   5 EPIRK5P1.                                                               */
+/*   5 EPIRK5P1, 6 EXPRB53s3.                                                  */
 /* u_low may be NULL for Rosenbrock-Euler (non-embedded, err = 0).            */
 /* ------------------------------------------------------------------------- */
 static void axpby(double a, const double *x, double b, const double *y, double *z, long N)
@@ -604,7 +604,7 @@ int oc_step_ex(const oc_problem *pb, int jac_mode, int method, const double *u, 
     int it = 0, total = 0, s = OC_OK;
     if (err) *err = 0.0;
     if (iters) *iters = 0;
-    if (method < 0 || method > 5) return OC_ERR_ARG;
+    if (method < 0 || method > 6) return OC_ERR_ARG;
     if (jac_mode != OC_JAC_EXACT && jac_mode != OC_JAC_FD) return OC_ERR_ARG;
     size_t bytes = sizeof(double) * (size_t)N;
     double *fu_raw = NULL;
@@ -711,6 +711,50 @@ int oc_step_ex(const oc_problem *pb, int jac_mode, int method, const double *u, 
         if (s) goto out;
         for (long i = 0; i < N; i++) u_high[i] = u[i] + b1 * t3[i] + b2 * t6[i] + b3 * t7[i];
         if (u_low) for (long i = 0; i < N; i++) u_low[i] = u_high[i];
+    } else if (method == 6) {
+        /* EXPRB53s3 (Luan & Ostermann 2014, cited at P:83; reading R27), D_x = h (F(x) - F(u)):
+         *   U2 = u + c2 h phi_1(c2 hJ) f                                  c2 = 1/2
+         *   U3 = u + c3 h phi_1(c3 hJ) f + (27/25 phi_3(c2 hJ) + 729/125 phi_3(c3 hJ)) D2   c3 = 9/10
+         *   u5 = u + h phi_1(hJ) f + (18 phi_3 - 60 phi_4)(hJ) D2 + (-250/81 phi_3 + 500/27 phi_4)(hJ) D3
+         *   u3 = u + h phi_1(hJ) f + 8 phi_3(hJ) D2        (embedded, order 3)
+         *   err = ||u5 - u3|| */
+        const double c2 = 0.5, c3 = 0.9;
+        double cf3[3] = {c2, c3, 1.0};
+        double *pv[3] = {t1, t2, t3};                        /* phi_1(c2 hJ) hf, phi_1(c3 hJ) hf, phi_1(hJ) hf */
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, f_u, pv, cf3, 3, dt, c, gamma, 1, rtol, atol, xi,
+                                max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        remainder_mode(pb, jac_mode, u, fu_raw, u, t4);      /* NL_u */
+        axpby(1.0, u, c2, t1, t5, N);                        /* U2 */
+        remainder_mode(pb, jac_mode, u, fu_raw, t5, t6);
+        axpby(dt, t6, -dt, t4, t5, N);                       /* D2 */
+        double *qv[3] = {t1, t6, t7};                        /* phi_3(c2 hJ) D2, phi_3(c3 hJ) D2, phi_3(hJ) D2 */
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, t5, qv, cf3, 3, dt, c, gamma, 3, rtol, atol, xi,
+                                max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        for (long i = 0; i < N; i++)                         /* U3 */
+            t1[i] = u[i] + c3 * t2[i] + (27.0 / 25.0) * t1[i] + (729.0 / 125.0) * t6[i];
+        remainder_mode(pb, jac_mode, u, fu_raw, t1, t2);
+        axpby(dt, t2, -dt, t4, t6, N);                       /* D3 */
+        axpby(18.0, t5, -250.0 / 81.0, t6, t1, N);           /* w3 */
+        axpby(-60.0, t5, 500.0 / 27.0, t6, t2, N);           /* w4 */
+        double one = 1.0;
+        double *o3[1] = {t4};
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, t1, o3, &one, 1, dt, c, gamma, 3, rtol, atol, xi,
+                                max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        double *o4[1] = {t5};
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, t2, o4, &one, 1, dt, c, gamma, 4, rtol, atol, xi,
+                                max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        for (long i = 0; i < N; i++) u_high[i] = u[i] + t3[i] + t4[i] + t5[i];   /* u5 */
+        for (long i = 0; i < N; i++) u_low[i] = u[i] + t3[i] + 8.0 * t7[i];      /* u3 */
+        for (long i = 0; i < N; i++) t1[i] = u_high[i] - u_low[i];
+        if (err) *err = oc_l2norm_scaled(t1, N);
     } else {
         /* EXPRB43 (method 2) / EPIRK4s3A (method 3) -- R17 tableaux:
          *  EXPRB43:   a = u + 1/2 hphi_1(hJ/2) f;  b = u + hphi_1 f + hphi_1 D_a

@@ -155,7 +155,7 @@ def test_leja_noconv_and_errors(xi300):
 
 
 # ---------------------------------------------------------------- integrators
-@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1"])
+@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3"])
 def test_integrator_linear_exactness(xi300, method):
     # every exponential integrator is exact on linear homogeneous problems
     n = 64
@@ -314,3 +314,26 @@ def test_epirk5p1_fifth_order_burgers(xi300):
         errs.append(np.linalg.norm(u.ravel() - ref) / np.linalg.norm(ref))
     orders = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
     assert orders[-1] > 4.5, (errs, orders)
+
+
+def test_exprb53s3_orders(xi300):
+    # EXPRB53s3 (reading R27): fifth-order solution and third-order embedded solution on Allen-Cahn;
+    # with a32 = 729/125 phi_3(c3 hJ) alone (dropping 27/25 phi_3(c2 hJ)) the order falls to ~3.5
+    n = 16
+    pb = O.Problem((n, n), (2 / n, 2 / n), 2e-3, 0.0, 1.0)
+    u0 = W.ic_allen_cahn_2d(n)
+    T = 0.5
+    uref = _allen_cahn_reference(pb, u0, T)
+    for attr, order in (("u_high", 5), ("u_low", 3)):
+        errs = []
+        for nsteps in (4, 8, 16):
+            u = u0.copy()
+            for _ in range(nsteps):
+                c, g = _cg(pb, u)
+                r = O.step(pb, "exprb53s3", u, T / nsteps, c, g, 1e-14, 1e-14, xi300)
+                assert r.status == O.OK
+                assert r.err == pytest.approx(O.l2norm_scaled(r.u_high - r.u_low), rel=1e-12)
+                u = getattr(r, attr)
+            errs.append(np.linalg.norm(u - uref) / np.linalg.norm(uref))
+        orders = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+        assert np.all(np.abs(orders - order) < 0.35), (attr, errs, orders)
