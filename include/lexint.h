@@ -215,7 +215,8 @@ typedef enum {
     LX_EXPRB43 = 2,
     LX_EPIRK4S3A = 3,
     LX_EXPRB42 = 4,       /* Luan 2017 (cited at P:83), 4th order, non-embedded (err = 0) */
-    LX_EPIRK5P1 = 5       /* Tokman et al. 2012 (cited at P:83, Table 2), 5th order, non-embedded (R26) */
+    LX_EPIRK5P1 = 5,      /* Tokman et al. 2012 (cited at P:83, Table 2), 5th order, non-embedded (R26) */
+    LX_EXPRB53S3 = 6      /* Luan & Ostermann 2014 (cited at P:83), 5th order, embedded 3rd (R27)      */
 } lx_method;
 
 /* Rosenbrock-Euler: u_out = u + phi_1(dt J(u)) f(u) dt (alg:Ros_Eu). */

@@ -931,6 +931,12 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
         } else if (method == LX_EXPRB42) {
             specs[n++] = {1, 2, c42};
             specs[n++] = {3, 1, c1};
+        } else if (method == LX_EXPRB53S3) {
+            static const double e3[3] = {0.5, 0.9, 1.0};
+            specs[n++] = {1, 3, e3};
+            specs[n++] = {3, 3, e3};
+            specs[n++] = {3, 1, c1};
+            specs[n++] = {4, 1, c1};
         } else if (method == LX_EPIRK5P1) {
             static const double e3[3] = {epirk5::g11, epirk5::g21, epirk5::g31};
             static const double e2[2] = {epirk5::g32, epirk5::g22};
@@ -995,6 +1001,41 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
         LX_TRY(run_stage(ctx, ST_SUM3, A));
         if (lo && lo != hi) CUDA_TRY(cudaMemcpyAsync(lo, hi, ctx->N_loc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
         return LX_OK;
+    }
+    if (method == LX_EXPRB53S3) {
+        // reading R27: c2 = 1/2, c3 = 9/10, D_x = dt (F(x) - F(u))
+        double* S1 = scratch(ctx, 1);
+        double* S2 = scratch(ctx, 2);
+        double* S3 = scratch(ctx, 3);
+        double* S7 = scratch(ctx, 7);
+        if (!S1 || !S2 || !S3 || !S7) return fail(LX_ERR_CUDA, "scratch allocation failed");
+        const double e3[3] = {0.5, 0.9, 1.0};
+        double* pv[3] = {S1, S2, S3};                        // phi_1(c hJ) hf, c = 1/2, 9/10, 1
+        LX_TRY(leja_device(ctx, pb, ul, S0, pv, e3, 3, dt, c, gamma, 1, rtol, atol, rec, tab[0]));
+        LX_TRY(stage_remainder(ctx, pb, rec, u, u, S1, 0.5, nullptr, 0.0, 1.0, dt, S0, hi));   // D2 -> S0
+        double* qv[3] = {S1, hi, lo};                        // phi_3(c hJ) D2, c = 1/2, 9/10, 1
+        LX_TRY(leja_device(ctx, pb, ul, S0, qv, e3, 3, dt, c, gamma, 3, rtol, atol, rec, tab[1]));
+        A = stage_args(ctx, pb, rec);                        // U3 = u + c3 P09 + 27/25 Q05 + 729/125 Q09
+        A.x0 = u; A.x1 = S2; A.x2 = S1; A.x3 = hi; A.a0 = 0.9; A.a1 = 27.0 / 25.0; A.a2 = 729.0 / 125.0; A.y0 = S7;
+        LX_TRY(run_stage(ctx, ST_LIN4, A));
+        LX_TRY(stage_remainder(ctx, pb, rec, u, S7, nullptr, 0.0, nullptr, 0.0, 1.0, dt, S2, nullptr));  // D3 -> S2
+        A = stage_args(ctx, pb, rec);                        // w3 -> S1, w4 -> S7
+        A.x0 = S0; A.x1 = S2; A.y0 = S1; A.y1 = S7;
+        A.a0 = 18.0; A.a1 = -250.0 / 81.0; A.a2 = -60.0; A.a3 = 500.0 / 27.0;
+        LX_TRY(run_stage(ctx, ST_COMBINE2, A));
+        double* o3[1] = {hi};
+        LX_TRY(leja_device(ctx, pb, ul, S1, o3, &one, 1, dt, c, gamma, 3, rtol, atol, rec, tab[2]));
+        double* o4[1] = {S0};
+        LX_TRY(leja_device(ctx, pb, ul, S7, o4, &one, 1, dt, c, gamma, 4, rtol, atol, rec, tab[3]));
+        A = stage_args(ctx, pb, rec);                        // d = Z3 + Z4 - 8 Q1 -> S2
+        A.x0 = hi; A.x1 = S0; A.x2 = lo; A.a0 = 1.0; A.a1 = -8.0; A.y0 = S2;
+        LX_TRY(run_stage(ctx, ST_LIN3, A));
+        A = stage_args(ctx, pb, rec);                        // q8 = 8 Q1 (in place)
+        A.x0 = lo; A.a0 = 8.0; A.y0 = lo;
+        LX_TRY(run_stage(ctx, ST_AXPBY, A));
+        A = stage_args(ctx, pb, rec);                        // u3 = u + P1 + q8 ; u5 = u3 + d ; err = ||d||
+        A.x0 = u; A.x1 = S3; A.x2 = lo; A.x3 = S2; A.y0 = lo; A.y1 = hi;
+        return run_stage(ctx, ST_FINAL4, A);
     }
     if (method == LX_EPIRK5P1) {
         // reading R26: R(x) = dt (F(x) - F(u)); vertical phi_1 {g11, g21, 1} on f dt, vertical phi_1 {g32, 1}
@@ -1076,7 +1117,7 @@ lx_status lx_step(lx_ctx* ctx, lx_method method, const lx_problem* pb0, const do
     const lx_problem* pb = &pbs;
     if (!ctx) return fail(LX_ERR_ARG, "ctx is NULL");
     LX_TRY(check_problem(ctx, pb));
-    if ((int)method < 0 || (int)method > 5) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
+    if ((int)method < 0 || (int)method > 6) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
     if (!u || !u_high) return fail(LX_ERR_ARG, "NULL argument");
     if (!nonembedded(method) && !u_low)
         return fail(LX_ERR_ARG, "u_low required for embedded methods");
@@ -1112,7 +1153,7 @@ lx_status lx_integrate(lx_ctx* ctx, lx_method method, const lx_problem* pb0, dou
     lx_problem pbs = *pb0;
     const lx_problem* pb = &pbs;
     LX_TRY(check_problem(ctx, pb));
-    if ((int)method < 0 || (int)method > 5) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
+    if ((int)method < 0 || (int)method > 6) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
     if (nsteps < 0) return fail(LX_ERR_ARG, "nsteps < 0");
     if (!std::isfinite(dt)) return fail(LX_ERR_ARG, "dt not finite");
     Staging sg(ctx);
@@ -1426,6 +1467,36 @@ static lx_status bb_step(BbRun& R, lx_method method, const double* u, double* lo
         if (lo && lo != hi) LX_TRY(R.comb(lo, 1.0, hi));
         return LX_OK;
     }
+    if (method == LX_EXPRB53S3) {                      // reading R27
+        const double e3[3] = {0.5, 0.9, 1.0};
+        double* pv[3] = {t[1], t[2], t[3]};
+        LX_TRY(R.leja(f_u, pv, e3, 3, dt, c, gamma, 1, rtol, atol));
+        LX_TRY(R.remainder(u, t[4]));                 // NL_u
+        LX_TRY(R.comb(t[5], 1.0, u, 0.5, t[1]));      // U2
+        LX_TRY(R.remainder(t[5], t[6]));
+        LX_TRY(R.comb(t[5], dt, t[6], -dt, t[4]));    // D2
+        double* qv[3] = {t[1], t[6], t[7]};
+        LX_TRY(R.leja(t[5], qv, e3, 3, dt, c, gamma, 3, rtol, atol));
+        LX_TRY(R.comb(t[1], 1.0, u, 0.9, t[2], 27.0 / 25.0, t[1], 729.0 / 125.0, t[6]));   // U3
+        LX_TRY(R.remainder(t[1], t[2]));
+        LX_TRY(R.comb(t[6], dt, t[2], -dt, t[4]));    // D3
+        LX_TRY(R.comb(t[1], 18.0, t[5], -250.0 / 81.0, t[6]));   // w3
+        LX_TRY(R.comb(t[2], -60.0, t[5], 500.0 / 27.0, t[6]));   // w4
+        double* o3[1] = {t[4]};
+        LX_TRY(R.leja(t[1], o3, &one, 1, dt, c, gamma, 3, rtol, atol));
+        double* o4[1] = {t[5]};
+        LX_TRY(R.leja(t[2], o4, &one, 1, dt, c, gamma, 4, rtol, atol));
+        LX_TRY(R.comb(hi, 1.0, u, 1.0, t[3], 1.0, t[4], 1.0, t[5]));   // u5
+        LX_TRY(R.comb(lo, 1.0, u, 1.0, t[3], 8.0, t[7]));              // u3
+        BbLin L = R.lin();
+        L.x0 = hi;
+        L.a0 = 1.0;
+        L.x1 = lo;
+        L.a1 = -1.0;
+        CUDA_TRY(launch_bb_norm(L, ctx->stream));
+        ctx->launches++;
+        return LX_OK;
+    }
     if (method == LX_EPIRK5P1) {                       // reading R26
         using namespace epirk5;
         const double e3[3] = {g11, g21, g31}, e2[2] = {g32, g22}, e1[1] = {g33};
@@ -1525,7 +1596,7 @@ lx_status lx_step_cb(lx_ctx* ctx, lx_method method, lx_rhs_fn f, void* user, con
                      double* u_high, double* err_out, double dt, double c, double gamma, double rtol, double atol,
                      int* iters_out) {
     if (!ctx || !f || !u || !u_high) return fail(LX_ERR_ARG, "NULL argument");
-    if ((int)method < 0 || (int)method > 5) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
+    if ((int)method < 0 || (int)method > 6) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
     if (!nonembedded(method) && !u_low)
         return fail(LX_ERR_ARG, "u_low required for embedded methods");
     if (u_low == u || u_high == u) return fail(LX_ERR_ALIAS, "outputs must not alias u");
