@@ -96,6 +96,10 @@ struct lx_ctx {
     double* tb2_seg_part = nullptr;       // [cap][2(1+kMaxK)]
     double* tb2_grp_part = nullptr;       // [cap/32+1][2(1+kMaxK)]
     unsigned* tb2_grp_cnt = nullptr;      // [cap/32+1]
+    int* tb2_segrow = nullptr;            // guided segment-row table (device) for tb2_key
+    long long tb2_key = -1;               // (nrb, nb, grid) the table was built for
+    int tb2_nsrow = 0;
+    bool tb2_guided = false;              // LX_TB2_GUIDED=min_rows,max_rows,k: guided segment rows
     bool coef_table = false;              // LX_COEF=table: prebuilt coefficient table instead of in-kernel
     double* cg_dev = nullptr;             // device (c, gamma, bound) of lx_integrate
     const double* cg_active = nullptr;    // when set, Leja kernels take (c, gamma) from here
@@ -351,7 +355,39 @@ static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u,
         P.grid = leja_tb2_grid_size(ctx->device, K, diag, P.nunits);
         P.seg = ctx->tb2_seg < 0 ? 32 / tb2_rt(K) : ctx->tb2_seg;   // default: 32-row segments
         P.order = ctx->tb2_order;
-        if (P.seg > 0 && P.order) {
+        P.segrow = nullptr;
+        if (ctx->tb2_seg < 0 && P.order && ctx->tb2_guided) {
+            // guided self-scheduling: a segment row of length L chunks per band, L = remaining work /
+            // (2 x working warps), clamped to [8, 64] rows: large segments (few strip starts) early,
+            // short ones at the end of the pass (short tail before the grid barrier)
+            const long long key = ((long long)P.nrb << 40) ^ ((long long)P.nb << 20) ^ (long long)P.grid;
+            if (key != ctx->tb2_key) {
+                const int rt = tb2_rt(K);
+                const long long warps = (long long)P.grid * kWarps - 1;
+                int gmin = 16, gmax = 32, gk = 2;
+                if (const char* ev = std::getenv("LX_TB2_GUIDED")) std::sscanf(ev, "%d,%d,%d", &gmin, &gmax, &gk);
+                const int lmin = (gmin + rt - 1) / rt, lmax = gmax / rt;
+                std::vector<int> rows(1, 0);
+                int r = 0;
+                while (r < P.nrb) {
+                    const long long rem = (long long)(P.nrb - r) * P.nb;
+                    long long L = (rem + gk * warps - 1) / (gk * warps);
+                    L = L < lmin ? lmin : (L > lmax ? lmax : L);
+                    r = (int)std::min<long long>(P.nrb, r + L);
+                    rows.push_back(r);
+                }
+                cudaFree(ctx->tb2_segrow);
+                ctx->tb2_segrow = nullptr;
+                CUDA_TRY(cudaMalloc(&ctx->tb2_segrow, rows.size() * sizeof(int)));
+                CUDA_TRY(cudaMemcpyAsync(ctx->tb2_segrow, rows.data(), rows.size() * sizeof(int),
+                                         cudaMemcpyHostToDevice, ctx->stream));
+                CUDA_TRY(cudaStreamSynchronize(ctx->stream));   // rows is a host temporary
+                ctx->tb2_key = key;
+                ctx->tb2_nsrow = (int)rows.size() - 1;
+            }
+            P.segrow = ctx->tb2_segrow;
+            P.nseg = P.nb * ctx->tb2_nsrow;
+        } else if (P.seg > 0 && P.order) {
             P.nseg = P.nb * ((P.nrb + P.seg - 1) / P.seg);
         } else if (P.seg > 0) {
             P.nseg = (P.nunits + P.seg - 1) / P.seg;
@@ -461,6 +497,7 @@ static void free_ctx(lx_ctx* ctx) {
     cudaFree(ctx->tb2_seg_part);
     cudaFree(ctx->tb2_grp_part);
     cudaFree(ctx->tb2_grp_cnt);
+    cudaFree(ctx->tb2_segrow);
     cudaFree(ctx->ctrl);
     cudaFree(ctx->rec_dev);
     cudaFree(ctx->coef_dev);
@@ -537,6 +574,7 @@ lx_status lx_ctx_create(const lx_problem* pb, int max_nodes, int device, void* c
     if (const char* ev = std::getenv("LX_LEJA_KERNEL")) ctx->variant = (std::strcmp(ev, "tma") == 0) ? 1 : 0;
     if (const char* ev = std::getenv("LX_TBLOCK")) ctx->tblock = (std::atoi(ev) == 1) ? 1 : 2;
     if (const char* ev = std::getenv("LX_TB2_ORDER")) ctx->tb2_order = std::atoi(ev) != 0;
+    if (std::getenv("LX_TB2_GUIDED")) ctx->tb2_guided = true;
     if (const char* ev = std::getenv("LX_TB2_SEG")) ctx->tb2_seg = std::atoi(ev) > 0 ? std::atoi(ev) : 0;
     if (const char* ev = std::getenv("LX_COEF")) ctx->coef_table = (std::strcmp(ev, "table") == 0);
     cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device);

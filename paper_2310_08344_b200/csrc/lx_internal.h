@@ -132,6 +132,9 @@ struct LejaParams {
     double* seg_part;     // [nseg][2(1+K)]
     double* grp_part;     // [ngrp][2(1+K)]
     unsigned* grp_cnt;    // [ngrp] finished segments of the group (reset by its last finisher)
+    // guided segment rows (order 1): segment row r covers chunks [segrow[r], segrow[r+1]) of every band;
+    // lengths shrink towards the end of a pass (guided self-scheduling) so the end-of-pass tail is short
+    const int* segrow;    // nullptr -> fixed rows of `seg` chunks
 };
 
 // launchers (lx_kernels.cu)

@@ -1826,8 +1826,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d_tb2(const __grid_constan
                     int c_b, c_e;
                     if (P.order) {   // band fastest: adjacent bands of the same rows run together
                         const int rs = sg / P.nb, b = sg - rs * P.nb;
-                        c_b = b * P.nrb + rs * P.seg;
-                        c_e = b * P.nrb + min(P.nrb, rs * P.seg + P.seg);
+                        if (P.segrow) {
+                            c_b = b * P.nrb + __ldg(P.segrow + rs);
+                            c_e = b * P.nrb + __ldg(P.segrow + rs + 1);
+                        } else {
+                            c_b = b * P.nrb + rs * P.seg;
+                            c_e = b * P.nrb + min(P.nrb, rs * P.seg + P.seg);
+                        }
                     } else {
                         c_b = sg * P.seg;
                         c_e = min(P.nunits, c_b + P.seg);
