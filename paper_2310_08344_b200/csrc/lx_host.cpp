@@ -99,7 +99,7 @@ struct lx_ctx {
     int* tb2_segrow = nullptr;            // guided segment-row table (device) for tb2_key
     long long tb2_key = -1;               // (nrb, nb, grid) the table was built for
     int tb2_nsrow = 0;
-    bool tb2_guided = false;              // LX_TB2_GUIDED=min_rows,max_rows,k: guided segment rows
+    int tb2_sched = 0;                    // LX_TB2_SCHED: 0 fixed 32-row segments, 1 balanced, 2 guided
     bool coef_table = false;              // LX_COEF=table: prebuilt coefficient table instead of in-kernel
     double* cg_dev = nullptr;             // device (c, gamma, bound) of lx_integrate
     const double* cg_active = nullptr;    // when set, Leja kernels take (c, gamma) from here
@@ -356,18 +356,31 @@ static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u,
         P.seg = ctx->tb2_seg < 0 ? 32 / tb2_rt(K) : ctx->tb2_seg;   // default: 32-row segments
         P.order = ctx->tb2_order;
         P.segrow = nullptr;
-        if (ctx->tb2_seg < 0 && P.order && ctx->tb2_guided) {
+        if (ctx->tb2_seg < 0 && P.order && ctx->tb2_sched != 0) {
             // guided self-scheduling: a segment row of length L chunks per band, L = remaining work /
             // (2 x working warps), clamped to [8, 64] rows: large segments (few strip starts) early,
             // short ones at the end of the pass (short tail before the grid barrier)
-            const long long key = ((long long)P.nrb << 40) ^ ((long long)P.nb << 20) ^ (long long)P.grid;
+            const long long key = ((((long long)P.nrb << 40) ^ ((long long)P.nb << 20) ^ (long long)P.grid) << 2) |
+                                  ctx->tb2_sched;
             if (key != ctx->tb2_key) {
                 const int rt = tb2_rt(K);
                 const long long warps = (long long)P.grid * kWarps - 1;
+                std::vector<int> rows(1, 0);
+                if (ctx->tb2_sched == 1) {
+                    // balanced: a whole number k of ~32-row segments per working warp, so the last round of
+                    // the dynamic schedule keeps (almost) every warp busy: nsrow = floor(k warps / nb)
+                    // segment rows of nrb/nsrow chunks (lengths differ by <= 1 chunk)
+                    const long long units = (long long)P.nrb * P.nb;
+                    long long k = (units + (32 / rt) * warps / 2) / ((32 / rt) * warps);   // round(units / (32-row segment x warps))
+                    if (k < 1) k = 1;
+                    long long nsrow = k * warps / P.nb;
+                    if (nsrow < 1) nsrow = 1;
+                    if (nsrow > P.nrb) nsrow = P.nrb;
+                    for (long long i = 1; i <= nsrow; i++) rows.push_back((int)(i * P.nrb / nsrow));
+                } else {
                 int gmin = 16, gmax = 32, gk = 2;
                 if (const char* ev = std::getenv("LX_TB2_GUIDED")) std::sscanf(ev, "%d,%d,%d", &gmin, &gmax, &gk);
                 const int lmin = (gmin + rt - 1) / rt, lmax = gmax / rt;
-                std::vector<int> rows(1, 0);
                 int r = 0;
                 while (r < P.nrb) {
                     const long long rem = (long long)(P.nrb - r) * P.nb;
@@ -375,6 +388,7 @@ static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u,
                     L = L < lmin ? lmin : (L > lmax ? lmax : L);
                     r = (int)std::min<long long>(P.nrb, r + L);
                     rows.push_back(r);
+                }
                 }
                 cudaFree(ctx->tb2_segrow);
                 ctx->tb2_segrow = nullptr;
@@ -574,7 +588,9 @@ lx_status lx_ctx_create(const lx_problem* pb, int max_nodes, int device, void* c
     if (const char* ev = std::getenv("LX_LEJA_KERNEL")) ctx->variant = (std::strcmp(ev, "tma") == 0) ? 1 : 0;
     if (const char* ev = std::getenv("LX_TBLOCK")) ctx->tblock = (std::atoi(ev) == 1) ? 1 : 2;
     if (const char* ev = std::getenv("LX_TB2_ORDER")) ctx->tb2_order = std::atoi(ev) != 0;
-    if (std::getenv("LX_TB2_GUIDED")) ctx->tb2_guided = true;
+    if (const char* ev = std::getenv("LX_TB2_SCHED"))
+        ctx->tb2_sched = std::strcmp(ev, "balanced") == 0 ? 1 : (std::strcmp(ev, "guided") == 0 ? 2 : 0);
+    if (std::getenv("LX_TB2_GUIDED")) ctx->tb2_sched = 2;
     if (const char* ev = std::getenv("LX_TB2_SEG")) ctx->tb2_seg = std::atoi(ev) > 0 ? std::atoi(ev) : 0;
     if (const char* ev = std::getenv("LX_COEF")) ctx->coef_table = (std::strcmp(ev, "table") == 0);
     cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device);
