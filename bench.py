@@ -284,7 +284,7 @@ def run_ours(args):
 
     # roofline of the dominant kernel (persistent Leja kernel, one launch per call)
     durs = np.array([[evs[s][l][0].elapsed_time(evs[s][l][1]) for l in range(4)] for s in range(args.steps)])
-    tb2 = ws == 1 and os.environ.get("LX_TBLOCK", "2") != "1"
+    tb2 = ctx.iterations_per_pass == 2   # the library's kernel choice for this context (lexint.h)
     bytes_per_call = np.array([N * leja_bytes_per_point(m, tb2) for m in iters], dtype=np.float64)
     per_call_ms = durs.mean(axis=0)
     achieved = float(bytes_per_call.sum() / (per_call_ms.sum() * 1e-3) / 1e9)

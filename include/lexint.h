@@ -154,6 +154,10 @@ lx_status lx_ctx_synchronize(lx_ctx *ctx, int *iters_total, double *err_last);
 
 /* Number of kernel launches this context has issued (for bench accounting). */
 int64_t lx_ctx_launch_count(const lx_ctx *ctx);
+/* Leja iterations per HBM pass of this context's Leja calls: 2 = the temporally blocked 2D kernel
+ * (single GPU, >= 3*2^20 local points, or LX_TBLOCK=2), 1 = one pass per iteration.
+ * Determines the algorithmic bytes of a call.  0 for a NULL context. */
+int lx_ctx_iterations_per_pass(const lx_ctx *ctx);
 
 /* ------------------------------------------------------------------------ */
 /* Spectrum (P:91, P:274-278 listing alg:lexint)                             */

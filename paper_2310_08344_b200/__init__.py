@@ -38,7 +38,7 @@ METHODS = {"rosenbrock_euler": 0, "exprb32": 1, "exprb43": 2, "epirk4s3a": 3, "e
 # Every symbol include/lexint.h declares (checked by tests/test_abi.py).
 EXPORTS = ("lx_last_error", "lx_version", "lx_leja_points", "lx_phi_scalar", "lx_divided_differences",
            "lx_slab_range", "lx_ctx_create", "lx_ctx_destroy", "lx_nccl_unique_id", "lx_ctx_set_comm",
-           "lx_ctx_local", "lx_ctx_synchronize", "lx_ctx_launch_count", "lx_spectrum_estimate",
+           "lx_ctx_local", "lx_ctx_synchronize", "lx_ctx_launch_count", "lx_ctx_iterations_per_pass", "lx_spectrum_estimate",
            "lx_spectrum_bound", "lx_shift_scale", "lx_real_leja_phi", "lx_real_leja_phi_vertical",
            "lx_step_rosenbrock_euler", "lx_step_exprb32", "lx_step_exprb43", "lx_step_epirk4s3a",
            "lx_step_exprb42", "lx_step_epirk5p1",
@@ -115,6 +115,7 @@ def lib() -> ctypes.CDLL:
             "lx_ctx_local": (ctypes.c_int, [vp, i64p, i64p, i64p]),
             "lx_ctx_synchronize": (ctypes.c_int, [vp, ip, dp]),
             "lx_ctx_launch_count": (ctypes.c_int64, [vp]),
+            "lx_ctx_iterations_per_pass": (ctypes.c_int, [vp]),
             "lx_spectrum_estimate": (ctypes.c_int, [vp, pbp, vp, ctypes.c_int, dp]),
             "lx_spectrum_bound": (ctypes.c_int, [vp, pbp, vp, dp]),
             "lx_shift_scale": (ctypes.c_int, [d, dp, dp]),
@@ -284,6 +285,11 @@ class Context:
         st = lib().lx_ctx_synchronize(self.handle, ctypes.byref(it), ctypes.byref(err))
         _check(st, it.value)
         return it.value, err.value
+
+    @property
+    def iterations_per_pass(self) -> int:
+        """2 when this context's Leja calls use the temporally blocked kernel, else 1."""
+        return int(lib().lx_ctx_iterations_per_pass(self.handle))
 
     @property
     def launch_count(self) -> int:

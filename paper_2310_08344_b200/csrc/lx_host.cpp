@@ -50,6 +50,9 @@ static constexpr int kCoefSlots = 32;
 static constexpr int kStage = 8;   // integrator scratch vectors (4 stages + 3 states for lx_integrate + 1 EPIRK5P1)
 static constexpr int kHost = 6;    // host-pointer staging vectors
 static constexpr int kBb = 11;     // black-box path vectors
+// Auto policy of the two-step kernel (measured round 1): its per-pass latency chain (~27 us)
+// loses to the one-pass kernel below ~1700^2 points (Leja calls and Allen-Cahn EXPRB43 alike).
+static constexpr int64_t kTb2MinPoints = 3 << 20;
 
 struct lx_ctx {
     int device = 0;
@@ -88,7 +91,8 @@ struct lx_ctx {
     double* rcp_dev = nullptr;            // [M][M]: 1/(xi_j - xi_i), j > i (divided-difference recurrence)
     Comm* comm = nullptr;                 // slab decomposition (lx_comm.cpp)
     int variant = 0;                      // 2D single-GPU Leja kernel: 0 = register tiles, 1 = TMA marching
-    int tblock = 2;                       // 2D single-GPU: Leja iterations per HBM pass (1 or 2; LX_TBLOCK)
+    int tblock = 0;                       // 2D single-GPU: Leja iterations per HBM pass (LX_TBLOCK=1 or 2;
+                                          // 0 = auto: two-step from kTb2MinPoints local points on)
     int tb2_seg = -1;                     // two-step kernel: max segment length in chunks (LX_TB2_SEG; 0 static
                                           // ranges; default 32 rows)
     int tb2_order = 1;                    // two-step kernel: segment order (LX_TB2_ORDER)
@@ -247,6 +251,14 @@ struct TableSpec {
     const double* coeffs;
 };
 
+// Leja iterations per HBM pass of this context's 2D single-GPU Leja calls (1 or 2).
+static int ctx_tblock(const lx_ctx* ctx) {
+    if (ctx->ndim != 2 || ctx->comm || ctx->variant == 1 || ctx->n_loc < 16 || ctx->n[1] < 64) return 1;
+    if (ctx->tblock == 1) return 1;
+    if (ctx->tblock == 2) return 2;
+    return ctx->N_loc >= kTb2MinPoints ? 2 : 1;
+}
+
 static lx_status build_tables(lx_ctx* ctx, const TableSpec* specs, int n, double dt, double c, double gamma, int rec,
                               const double** tables_out) {
     CoefJobs jobs;
@@ -347,7 +359,7 @@ static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u,
             return LX_OK;
         }
     }
-    if (P.ndim == 2 && ctx->tblock == 2 && P.n_loc >= 16 && P.n1 >= 64) {
+    if (P.ndim == 2 && ctx_tblock(ctx) == 2) {
         // temporally blocked kernel: two iterations per pass; work items = (60-column band, RT-row chunk)
         P.nb = (P.n1 + kBand2 - 1) / kBand2;
         P.nrb = (P.n_loc + tb2_rt(K) - 1) / tb2_rt(K);
@@ -586,7 +598,7 @@ lx_status lx_ctx_create(const lx_problem* pb, int max_nodes, int device, void* c
     ctx->N_glob = (double)ctx->n[0] * (double)ctx->row;
     ctx->max_nodes = max_nodes;
     if (const char* ev = std::getenv("LX_LEJA_KERNEL")) ctx->variant = (std::strcmp(ev, "tma") == 0) ? 1 : 0;
-    if (const char* ev = std::getenv("LX_TBLOCK")) ctx->tblock = (std::atoi(ev) == 1) ? 1 : 2;
+    if (const char* ev = std::getenv("LX_TBLOCK")) ctx->tblock = std::atoi(ev) == 1 ? 1 : (std::atoi(ev) == 2 ? 2 : 0);
     if (const char* ev = std::getenv("LX_TB2_ORDER")) ctx->tb2_order = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("LX_TB2_SCHED"))
         ctx->tb2_sched = std::strcmp(ev, "balanced") == 0 ? 1 : (std::strcmp(ev, "guided") == 0 ? 2 : 0);
@@ -755,6 +767,8 @@ lx_status lx_ctx_synchronize(lx_ctx* ctx, int* iters_total, double* err_last) {
 }
 
 int64_t lx_ctx_launch_count(const lx_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int lx_ctx_iterations_per_pass(const lx_ctx* ctx) { return ctx ? ctx_tblock(ctx) : 0; }
 
 // ---------------------------------------------------------------- Leja
 lx_status lx_real_leja_phi_vertical(lx_ctx* ctx, const lx_problem* pb, const double* u_lin, const double* v,

@@ -4,12 +4,15 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#ifndef LX_KRT3
+#define LX_KRT3 2
+#endif
 namespace lx {
 
 constexpr int kThreads = 256;     // threads per CTA (8 warps)
 constexpr int kWarps = kThreads / 32;
 constexpr int kRT = 4;            // rows per warp work unit (2D)
-constexpr int kRT3 = 2;           // planes per warp work unit (3D)
+constexpr int kRT3 = LX_KRT3;         // planes per warp work unit (3D)
 // two-step (temporally blocked) kernel: rows per chunk, bytes of one staged chunk, ring depth
 // (chunks per warp ring; 8 warps x depth x stage <= 110 KB so that two CTAs fit on an SM)
 __host__ __device__ constexpr int tb2_rt(int K) { return K == 1 ? 4 : 2; }

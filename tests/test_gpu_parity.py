@@ -513,11 +513,12 @@ def test_tblock2_matches_oracle_and_one_step(xi300, monkeypatch, shape, K, react
         assert np.linalg.norm(a - ref) <= TOL * np.linalg.norm(ref)
 
 
-def test_tblock2_dynamic_segments_reproducible(xi300):
+def test_tblock2_dynamic_segments_reproducible(xi300, monkeypatch):
     # dynamic work assignment (atomic segment counter) must not leak into the results: per-segment
     # norm partials are reduced in segment order -> identical iterations and bitwise-equal outputs
     # over repeated calls, at a size with thousands of segments (n = 1536: 26 bands x 384 chunks)
     n = 1536
+    monkeypatch.setenv("LX_TBLOCK", "2")   # below the auto threshold: force the two-step kernel
     pb, _ = _pair((n, n))
     u0 = _dev(W.ic_random((n, n), seed=5, amp=0.3))
     dt = 10 * W.dt_cfl(n, 10.0)
@@ -532,3 +533,17 @@ def test_tblock2_dynamic_segments_reproducible(xi300):
         assert it == runs[0][0]
         for a, b in zip(outs, runs[0][1]):
             assert torch.equal(a, b)
+
+
+def test_tblock_auto_policy(monkeypatch):
+    # two-step kernel from 3*2^20 local points on (2D single GPU), one-pass below; LX_TBLOCK forces
+    monkeypatch.delenv("LX_TBLOCK", raising=False)
+    for shape, want in (((1536, 1536), 1), ((2048, 2048), 2), ((64, 64), 1)):
+        pb, _ = _pair(shape)
+        with lx.Context(pb) as ctx:
+            assert ctx.iterations_per_pass == want, shape
+    monkeypatch.setenv("LX_TBLOCK", "2")
+    with lx.Context(_pair((64, 64))[0]) as ctx:
+        assert ctx.iterations_per_pass == 2
+    with lx.Context(_pair((8, 8, 64))[0]) as ctx:
+        assert ctx.iterations_per_pass == 1        # 3D: one pass per iteration

@@ -69,7 +69,7 @@ def cfg_leja(stream, n, ls, name, reps=3):
         ms, _ = timed(stream, lambda: lx.lx_real_leja_phi(ctx, u, out, wl.dt, c, g, l, wl.rtol, wl.atol,
                                                            sync=False), reps)
         ctx.synchronize()
-        tb2 = os.environ.get("LX_TBLOCK", "2") != "1"
+        tb2 = ctx.iterations_per_pass == 2
         byt = u.numel() * leja_bytes_per_point(it, tb2)        # the kernel's own algorithmic bytes
         byt1 = u.numel() * leja_bytes_per_point(it, False)     # one-pass accounting (32 B/pt per iteration)
         res.append({"l": l, "iters": it, "ms": ms, "GBps": byt / ms / 1e6, "frac": byt / ms / 1e6 / PEAK,
