@@ -439,8 +439,28 @@ static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u,
             P.grp_part = ctx->tb2_grp_part;
             P.grp_cnt = ctx->tb2_grp_cnt;
         }
+        static const char* trace_path = std::getenv("LX_TB2_TRACE");   // diagnostics only
+        unsigned long long* tr = nullptr;
+        if (trace_path) {
+            CUDA_TRY(cudaMalloc(&tr, (size_t)160 * P.grid * 3 * sizeof(unsigned long long)));
+            CUDA_TRY(cudaMemsetAsync(tr, 0, (size_t)160 * P.grid * 3 * sizeof(unsigned long long), ctx->stream));
+            P.trace = tr;
+        }
         CUDA_TRY(launch_leja_tb2(P, ctx->stream, diag));
         ctx->launches++;
+        if (tr) {
+            std::vector<unsigned long long> h((size_t)160 * P.grid * 3);
+            CUDA_TRY(cudaMemcpyAsync(h.data(), tr, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+            CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+            cudaFree(tr);
+            if (FILE* f = std::fopen(trace_path, "ab")) {
+                const int hdr[2] = {P.grid, 160};
+                std::fwrite(hdr, sizeof hdr, 1, f);
+                std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+                std::fclose(f);
+            }
+        }
         return LX_OK;
     }
     P.grid = leja_grid_size(ctx->device, K, diag, P.ndim, P.nunits);

@@ -138,6 +138,7 @@ struct LejaParams {
     // guided segment rows (order 1): segment row r covers chunks [segrow[r], segrow[r+1]) of every band;
     // lengths shrink towards the end of a pass (guided self-scheduling) so the end-of-pass tail is short
     const int* segrow;    // nullptr -> fixed rows of `seg` chunks
+    unsigned long long* trace;   // diagnostics (LX_TB2_TRACE): [pass][grid][3] globaltimer start/arrive/exit
 };
 
 // launchers (lx_kernels.cu)

@@ -1715,7 +1715,7 @@ __device__ __forceinline__ void barrier_decide_tb2(const LejaParams& P, int m, b
         unsigned long long w = ld_relaxed64(&ctrl->word);
         int spins = 0;
         while ((int)((unsigned)(w >> 32) - gen0) < m) {
-            if (++spins > 32) __nanosleep(32);
+            if (++spins > 4096) __nanosleep(32);
             if (spins > P.timeout_spins) {
                 atomicExch(&P.rec->status, 10);
                 w = (1ull << 8);
@@ -1749,6 +1749,12 @@ __device__ __forceinline__ void coef_first5(const LejaParams& P, int k, double* 
     }
 #pragma unroll
     for (int i = 0; i < 5; i++) d[i] = __shfl_sync(0xffffffffu, e[i], 0);
+}
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
 }
 
 template <int K, bool DIAG>
@@ -1796,10 +1802,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d_tb2(const __grid_constan
         nb[k] = dd[k][4];
     }
     int m = 1;
+    double nb1 = coef_beta(P, 1), nb2 = (2 < M) ? coef_beta(P, 2) : 0.0;
     for (; m < M; m += 2) {
         const bool two = (m + 1 < M);
-        const double b1 = coef_beta(P, m), b2 = two ? coef_beta(P, m + 1) : 0.0;
+        const double b1 = nb1, b2 = two ? nb2 : 0.0;
+        // next pass's shifts (constant inputs): loaded now, off the post-barrier critical path
+        nb1 = (m + 2 < M) ? coef_beta(P, m + 2) : 0.0;
+        nb2 = (m + 3 < M) ? coef_beta(P, m + 3) : 0.0;
         const int pass = (m - 1) >> 1;
+        if (P.trace && tid == 0 && pass < 160) P.trace[((size_t)pass * gridDim.x + blockIdx.x) * 3] = globaltimer_ns();
         double* dst = P.ydst[pass & 1];
         double acc[2 * (1 + K)];
 #pragma unroll
@@ -1882,7 +1893,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d_tb2(const __grid_constan
                 for (int i = 0; i < 2 * (1 + K); i++) slot[i] = acc[i];
             }
         }
+        if (P.trace) {
+            __syncthreads();
+            if (tid == 0 && pass < 160) P.trace[((size_t)pass * gridDim.x + blockIdx.x) * 3 + 1] = globaltimer_ns();
+        }
         barrier_decide_tb2<K>(P, m, two, gen0, da, db, active, s_red, s_flags);
+        if (P.trace && tid == 0 && pass < 160) P.trace[((size_t)pass * gridDim.x + blockIdx.x) * 3 + 2] = globaltimer_ns();
         active = s_flags[2];
         rbmask = s_flags[3];
 #pragma unroll
