@@ -62,6 +62,10 @@ __device__ __forceinline__ double block_max(double v, double* s) {
     return m;
 }
 
+// 16-byte global accesses (cudaMalloc'd vectors and caller tensors are 16-byte aligned: lexint.h)
+__device__ __forceinline__ double2 ld2g(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ void st2g(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
+
 __device__ __forceinline__ double fd_eps(const BbCtrl* c, int slot) {
     const double ym = u64_as_double(c->maxbits[slot]);
     if (ym == 0.0) return 0.0;                 // J(u) 0 = 0
@@ -95,9 +99,15 @@ __global__ void __launch_bounds__(kThreads) k_bb_perturb(BbArgs A, int m) {
     if (*(volatile int*)&c->done) return;
     const double eps = fd_eps(c, (m - 1) & 1);
     const long long N = A.N;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x)
-        A.w[i] = A.u[i] + eps * A.y_in[i];
-    if (blockIdx.x == 0 && threadIdx.x == 0) c->maxbits[m & 1] = 0ull;
+    const long long npair = N >> 1;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < npair; i += (long long)gridDim.x * blockDim.x) {
+        const double2 u = ld2g(A.u + 2 * i), y = ld2g(A.y_in + 2 * i);
+        st2g(A.w + 2 * i, make_double2(u.x + eps * y.x, u.y + eps * y.y));
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (N & 1) A.w[N - 1] = A.u[N - 1] + eps * A.y_in[N - 1];
+        c->maxbits[m & 1] = 0ull;
+    }
 }
 
 template <int K>
@@ -123,7 +133,54 @@ __global__ void __launch_bounds__(kThreads) k_bb_update(BbArgs A, int m) {
     for (int i = 0; i < NV; i++) acc[i] = 0.0;
     double my = 0.0;
     const long long N = A.N;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+    // pairs (16-byte loads/stores), UN independent pairs per trip with every load issued before any
+    // store; the scalar tail (odd N) afterwards
+    constexpr int UN = 2;
+    const long long npair = N >> 1;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < npair; i0 += UN * stride) {
+        double2 yp[UN], fw[UN], fu[UN], pv[UN][K];
+#pragma unroll
+        for (int q = 0; q < UN; q++) {
+            const long long i = i0 + q * stride;
+            const bool ok = i < npair;
+            yp[q] = ok ? ld2g(A.y_in + 2 * i) : make_double2(0.0, 0.0);
+            fw[q] = ok ? ld2g(A.fw + 2 * i) : make_double2(0.0, 0.0);
+            fu[q] = (ok && fd) ? ld2g(A.fu + 2 * i) : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int k = 0; k < K; k++)
+                pv[q][k] = (ok && ((act >> k) & 1)) ? ld2g(A.p[k] + 2 * i) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int q = 0; q < UN; q++) {
+            const long long i = i0 + q * stride;
+            if (i >= npair) break;
+            double jx, jyy;
+            if (fd) {
+                jx = (eps == 0.0) ? 0.0 : (fw[q].x - fu[q].x) * ieps;
+                jyy = (eps == 0.0) ? 0.0 : (fw[q].y - fu[q].y) * ieps;
+            } else {
+                jx = fw[q].x;
+                jyy = fw[q].y;
+            }
+            const double2 y = make_double2(fma(alpha, jx, beta * yp[q].x), fma(alpha, jyy, beta * yp[q].y));
+            st2g(A.y_out + 2 * i, y);
+            acc[0] = fma(y.x, y.x, acc[0]);
+            acc[0] = fma(y.y, y.y, acc[0]);
+            my = fmax(my, fmax(fabs(y.x), fabs(y.y)));
+#pragma unroll
+            for (int k = 0; k < K; k++) {
+                if ((act >> k) & 1) {
+                    const double2 p = make_double2(fma(dm[k], y.x, pv[q][k].x), fma(dm[k], y.y, pv[q][k].y));
+                    st2g(A.p[k] + 2 * i, p);
+                    acc[1 + k] = fma(p.x, p.x, acc[1 + k]);
+                    acc[1 + k] = fma(p.y, p.y, acc[1 + k]);
+                }
+            }
+        }
+    }
+    if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {   // odd tail element
+        const long long i = N - 1;
         const double yp = A.y_in[i];
         double jy;
         if (fd) jy = (eps == 0.0) ? 0.0 : (A.fw[i] - A.fu[i]) * ieps;
