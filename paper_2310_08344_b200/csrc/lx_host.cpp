@@ -103,6 +103,8 @@ struct lx_ctx {
     int* tb2_segrow = nullptr;            // guided segment-row table (device) for tb2_key
     long long tb2_key = -1;               // (nrb, nb, grid) the table was built for
     int tb2_nsrow = 0;
+    int k3d = 0;                          // 3D single-GPU Leja kernel: 0/1 smem marching when n1 % 16 == 0 and
+                                          // n2 % 64 == 0 (else warp tiles), 2 warp tiles (LX_3D_KERNEL=tile)
     int tb2_sched = 0;                    // LX_TB2_SCHED: 0 fixed 32-row segments, 1 balanced, 2 guided
     bool coef_table = false;              // LX_COEF=table: prebuilt coefficient table instead of in-kernel
     double* cg_dev = nullptr;             // device (c, gamma, bound) of lx_integrate
@@ -463,6 +465,23 @@ static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u,
         }
         return LX_OK;
     }
+    if (P.ndim == 3 && ctx->k3d != 2 && P.n1 % 16 == 0 && P.n2 % 64 == 0) {
+        // 3D marching kernel with shared-memory plane tiles: Newton coefficients from a prebuilt table
+        if (P.coef_gen) {
+            CoefJobs jobs;
+            std::memset(&jobs, 0, sizeof jobs);
+            for (int k = 0; k < K; k++) jobs.j[jobs.n++] = CoefJob{P.table, coeffs[k], l, K, k};
+            CUDA_TRY(launch_coef_tables(ctx->xi_dev, ctx->rcp_dev, ctx->max_nodes, jobs, dt, c, gamma, ctx->cg_active,
+                                        &ctx->rec_dev[rec].status, ctx->stream));
+            ctx->launches++;
+            P.coef_gen = 0;
+        }
+        const int ncu = (P.n1 / 16) * (P.n2 / 64) * ((P.n_loc + 63) / 64);
+        P.grid = leja3d_smem_grid_size(ctx->device, K, diag, ncu);
+        CUDA_TRY(launch_leja3d_smem(P, ctx->stream, diag));
+        ctx->launches++;
+        return LX_OK;
+    }
     P.grid = leja_grid_size(ctx->device, K, diag, P.ndim, P.nunits);
     CUDA_TRY(launch_leja_persistent(P, ctx->stream, diag));
     ctx->launches++;
@@ -620,6 +639,8 @@ lx_status lx_ctx_create(const lx_problem* pb, int max_nodes, int device, void* c
     if (const char* ev = std::getenv("LX_LEJA_KERNEL")) ctx->variant = (std::strcmp(ev, "tma") == 0) ? 1 : 0;
     if (const char* ev = std::getenv("LX_TBLOCK")) ctx->tblock = std::atoi(ev) == 1 ? 1 : (std::atoi(ev) == 2 ? 2 : 0);
     if (const char* ev = std::getenv("LX_TB2_ORDER")) ctx->tb2_order = std::atoi(ev) != 0;
+    if (const char* ev = std::getenv("LX_3D_KERNEL"))
+        ctx->k3d = std::strcmp(ev, "smem") == 0 ? 1 : (std::strcmp(ev, "tile") == 0 ? 2 : 0);
     if (const char* ev = std::getenv("LX_TB2_SCHED"))
         ctx->tb2_sched = std::strcmp(ev, "balanced") == 0 ? 1 : (std::strcmp(ev, "guided") == 0 ? 2 : 0);
     if (std::getenv("LX_TB2_GUIDED")) ctx->tb2_sched = 2;

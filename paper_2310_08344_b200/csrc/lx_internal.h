@@ -145,6 +145,10 @@ struct LejaParams {
 cudaError_t launch_leja_persistent(const LejaParams& P, cudaStream_t s, bool diag);
 cudaError_t launch_power_persistent(const LejaParams& P, cudaStream_t s, bool diag);
 int leja_grid_size(int device, int K, bool diag, int ndim, int nunits);
+// 3D marching kernel with shared-memory plane tiles (single GPU, n1 % 8 == 0, n2 % 64 == 0, prebuilt
+// coefficient table); ncu = CTA units (8 j-rows x 64 k x 64 planes)
+int leja3d_smem_grid_size(int device, int K, bool diag, int ncu);
+cudaError_t launch_leja3d_smem(const LejaParams& P, cudaStream_t s, bool diag);
 // temporally blocked 2D kernel: two Leja iterations per HBM pass (single GPU, constant coefficients + diag)
 int leja_tb2_grid_size(int device, int K, bool diag, int nunits);
 cudaError_t launch_leja_tb2(const LejaParams& P, cudaStream_t s, bool diag);

@@ -547,3 +547,29 @@ def test_tblock_auto_policy(monkeypatch):
         assert ctx.iterations_per_pass == 2
     with lx.Context(_pair((8, 8, 64))[0]) as ctx:
         assert ctx.iterations_per_pass == 1        # 3D: one pass per iteration
+
+
+@pytest.mark.parametrize("shape,K,react", [((20, 32, 64), 1, 0.0), ((70, 16, 128), 2, 1.0), ((130, 48, 64), 3, 0.0)])
+def test_3d_smem_kernel_bitwise_equals_tiles(xi300, monkeypatch, shape, K, react):
+    # the shared-memory marching 3D kernel (plane runs of 64, ragged last run) evaluates every point with the
+    # warp-tile kernel's operation order: identical iterations and bitwise-equal outputs; oracle parity
+    diff, nu = (1e-3, 0.0) if react else (1.0, 10.0)
+    pb, ob = _pair(shape, diff=diff, nu=nu, react=react)
+    u = W.ic_random(shape, seed=31, amp=0.5) if react else None
+    v = W.ic_random(shape, seed=32, amp=0.2)
+    dt = 0.01 if react else 5 * min(W.dt_cfl(n, 10.0, 3) for n in shape)
+    coeffs = (0.5, 2 / 3, 1.0)[-K:]
+    res = {}
+    for kern in ("tile", "smem"):
+        monkeypatch.setenv("LX_3D_KERNEL", kern)
+        with lx.Context(pb) as ctx:
+            ud = _dev(u) if react else None
+            c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx, ud))
+            outs = [torch.empty(shape, dtype=torch.float64, device="cuda") for _ in range(K)]
+            it = lx.lx_real_leja_phi_vertical(ctx, _dev(v), outs, coeffs, dt, c, g, 1, TOL, TOL, u_lin=ud)
+            res[kern] = (it, [o.cpu().numpy() for o in outs])
+    r = O.real_leja_phi(ob, v, dt, c, g, 1, TOL, TOL, xi300, coeffs=coeffs, u_lin=u)
+    assert res["smem"][0] == res["tile"][0] == r.iters
+    for a, b, ref in zip(res["smem"][1], res["tile"][1], r.outs):
+        np.testing.assert_array_equal(a, b)
+        assert np.linalg.norm(a - ref) <= TOL * np.linalg.norm(ref)
