@@ -476,7 +476,7 @@ static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u,
             ctx->launches++;
             P.coef_gen = 0;
         }
-        const int ncu = (P.n1 / 16) * (P.n2 / 64) * ((P.n_loc + 63) / 64);
+        const int ncu = leja3d_smem_units(P.n_loc, P.n1, P.n2);
         P.grid = leja3d_smem_grid_size(ctx->device, K, diag, ncu);
         CUDA_TRY(launch_leja3d_smem(P, ctx->stream, diag));
         ctx->launches++;

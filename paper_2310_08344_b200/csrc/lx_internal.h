@@ -148,6 +148,7 @@ int leja_grid_size(int device, int K, bool diag, int ndim, int nunits);
 // 3D marching kernel with shared-memory plane tiles (single GPU, n1 % 8 == 0, n2 % 64 == 0, prebuilt
 // coefficient table); ncu = CTA units (8 j-rows x 64 k x 64 planes)
 int leja3d_smem_grid_size(int device, int K, bool diag, int ncu);
+int leja3d_smem_units(int n0, int n1, int n2);
 cudaError_t launch_leja3d_smem(const LejaParams& P, cudaStream_t s, bool diag);
 // temporally blocked 2D kernel: two Leja iterations per HBM pass (single GPU, constant coefficients + diag)
 int leja_tb2_grid_size(int device, int K, bool diag, int nunits);

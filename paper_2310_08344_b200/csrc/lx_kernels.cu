@@ -1926,7 +1926,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d_tb2(const __grid_constan
 // equal results).  Newton coefficients come from the prebuilt table (k_coef_tables); the grid
 // barrier and the P:155 decision are those of k_leja2d.
 // ---------------------------------------------------------------------------
-constexpr int kTI3 = 64;                 // planes per run
+#ifndef LX_TI3
+#define LX_TI3 64
+#endif
+constexpr int kTI3 = LX_TI3;             // planes per run
 constexpr int kS3Cols = 68;              // k0-2 .. k0+65
 constexpr int kS3J = 16;                 // output j-rows per CTA tile (2 per warp)
 constexpr int kS3Rows = kS3J + 3;        // j0-1 .. j0+kS3J+1
@@ -2209,6 +2212,8 @@ static void* leja3d_smem_ptr(int K, bool diag) {
     }
     return nullptr;
 }
+
+int leja3d_smem_units(int n0, int n1, int n2) { return (n1 / kS3J) * (n2 / 64) * ((n0 + kTI3 - 1) / kTI3); }
 
 int leja3d_smem_grid_size(int device, int K, bool diag, int ncu) {
     void* kern = leja3d_smem_ptr(K, diag);
