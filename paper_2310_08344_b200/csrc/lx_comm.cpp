@@ -19,6 +19,7 @@
 #include "lx_comm.h"
 
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -48,6 +49,12 @@ struct Transport {
     virtual int exchange_rows(const double* base, double* ghost, int n_loc, long long row, cudaStream_t s) = 0;
     virtual int allgather(const double* send, double* recv, int count, cudaStream_t s) = 0;
     virtual int allreduce_max_u64(unsigned long long* buf, cudaStream_t s) = 0;
+    // the per-iteration exchange: halo rows of y_m and the allgather of the per-rank partials
+    virtual int exchange_and_gather(const double* base, double* ghost, int n_loc, long long row, const double* send,
+                                    double* recv, int count, cudaStream_t s) {
+        if (exchange_rows(base, ghost, n_loc, row, s)) return 1;
+        return allgather(send, recv, count, s);
+    }
 };
 
 // ------------------------------------------------------------------ NCCL
@@ -83,6 +90,23 @@ struct NcclTransport : Transport {
         NC(ncclAllReduce(buf, buf, 1, ncclUint64, ncclMax, comm, s));
         return 0;
     }
+    // ONE NCCL group per Leja iteration: the 1+2-row halo send/recv and the partials allgather are
+    // aggregated into a single launch (halves the per-iteration NCCL launches of the slab protocol)
+    int exchange_and_gather(const double* base, double* ghost, int n_loc, long long row, const double* send,
+                            double* recv, int count, cudaStream_t s) override {
+        if (fused < 0) fused = std::getenv("LX_COMM_UNFUSED") ? 0 : 1;
+        if (!fused) return Transport::exchange_and_gather(base, ghost, n_loc, row, send, recv, count, s);
+        const int up = (rank - 1 + nranks) % nranks, down = (rank + 1) % nranks;
+        NC(ncclGroupStart());
+        NC(ncclSend(base, 2 * row, ncclDouble, up, comm, s));
+        NC(ncclRecv(ghost + row, 2 * row, ncclDouble, down, comm, s));
+        NC(ncclSend(base + (long long)(n_loc - 1) * row, row, ncclDouble, down, comm, s));
+        NC(ncclRecv(ghost, row, ncclDouble, up, comm, s));
+        NC(ncclAllGather(send, recv, count, ncclDouble, comm, s));
+        NC(ncclGroupEnd());
+        return 0;
+    }
+    int fused = -1;
 };
 #endif
 
@@ -340,9 +364,13 @@ lx_status comm_leja(Comm* c, LejaParams& P, bool diag, cudaStream_t s, int64_t* 
     auto launch = [&](int m) -> int {
         if (launch_leja_step(P, m, s, diag) != cudaSuccess) return cerr("step kernel launch failed");
         (*launches)++;
-        if (m < M) {
-            if (comm_exchange(c, c->Y[m & 1], c->Yg[m & 1], s)) return 1;
-            if (c->tr->allgather(c->rank_part, c->gathered, kSlot, s)) return 1;
+        // diagnostics (LX_COMM_SKIP, one rank): no halo, the gather replaced by a D2D copy -> the step kernels alone
+        static const bool skip = std::getenv("LX_COMM_SKIP") != nullptr;
+        if (m < M && skip) {
+            CU(cudaMemcpyAsync(c->gathered, c->rank_part, kSlot * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        } else if (m < M && c->tr->exchange_and_gather(c->Y[m & 1], c->Yg[m & 1], c->n_loc, c->row, c->rank_part,
+                                                       c->gathered, kSlot, s)) {
+            return 1;
         }
         return 0;
     };

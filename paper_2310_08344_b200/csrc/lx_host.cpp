@@ -754,7 +754,9 @@ lx_status lx_ctx_set_comm(lx_ctx* ctx, const void* uid, int rank, int nranks) {
     LX_TRY(check_slabs(ctx, rank, nranks));
     cudaStreamSynchronize(ctx->stream);
     Comm* c = nullptr;
-    if (nranks > 1 && comm_create(uid, rank, nranks, ctx->device, ctx->row, ctx->nsm * 8, &c))
+    // nranks == 1 also builds a (self-)communicator: the slab protocol with NCCL halos to itself, used to
+    // check the NCCL transport on one GPU (tools/nccl_selfcheck.py)
+    if (comm_create(uid, rank, nranks, ctx->device, ctx->row, ctx->nsm * 8, &c))
         return fail(LX_ERR_NCCL, "NCCL communicator: %s", comm_error());
     return attach_comm(ctx, c, rank, nranks);
 }

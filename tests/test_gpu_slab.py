@@ -148,3 +148,17 @@ def test_slab_3d_epirk(xi300, P):
     assert {r[0] for r in res} == {ref.iters}
     hi = np.concatenate([r[1] for r in res])
     assert np.linalg.norm(hi - ref.u_high) <= TOL * np.linalg.norm(ref.u_high)
+
+
+def test_nccl_transport_world_size_one():
+    # the real NCCL transport (not the in-process one) on one GPU: a communicator of size 1 exchanges halos
+    # with itself; results must match the single-domain path (tools/nccl_selfcheck.py, own process)
+    import json
+    import subprocess
+    import sys
+    root = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+    r = subprocess.run([sys.executable, root + "/tools/nccl_selfcheck.py"], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert res["ok"], res

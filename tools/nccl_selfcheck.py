@@ -1,0 +1,81 @@
+#!/usr/bin/env python
+"""Exercise the NCCL slab transport on ONE GPU: a world of size 1 over torch.distributed/NCCL, the library's
+own communicator (halo send/recv to itself as both neighbours, allgather of the per-rank partials).
+Compares a Leja call, an EXPRB43 step and the Gershgorin bound with the single-domain path: identical
+iteration counts, fields equal to 1e-13 (only the norm summation order differs).  Prints one JSON line."""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2310_08344_b200 as lx  # noqa: E402
+import paper_2310_08344_b200.dist as lxd  # noqa: E402
+import workloads as W  # noqa: E402
+
+
+def main():
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29631")
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    out = {}
+    n = 256
+    pb = lx.Problem((n, n), (2 / n, 2 / n), 1e-4, 0.0, 1.0)
+    u = torch.from_numpy(W.ic_allen_cahn_2d(n)).cuda()
+    v = torch.from_numpy(W.ic_random((n, n), seed=3, amp=0.2)).cuda()
+    res = {}
+    for mode in ("single", "nccl"):
+        ctx = lx.Context(pb)
+        if mode == "nccl":
+            lxd.attach(ctx)
+        bound = lx.lx_spectrum_bound(ctx, u)
+        c, g = lx.lx_shift_scale(bound)
+        o = torch.empty_like(u)
+        it = lx.lx_real_leja_phi(ctx, v, o, 0.01, c, g, 1, 1e-10, 1e-10, u_lin=u)
+        lo, hi = torch.empty_like(u), torch.empty_like(u)
+        its, err = lx.lx_step(ctx, "exprb43", u, lo, hi, 0.01, c, g, 1e-10, 1e-10)
+        res[mode] = (bound, it, o.cpu().numpy(), its, err, hi.cpu().numpy())
+        ctx.close()
+    a, b = res["single"], res["nccl"]
+    out["bound_equal"] = a[0] == b[0]
+    out["leja_iters"] = [a[1], b[1]]
+    out["leja_maxrel"] = float(np.abs(a[2] - b[2]).max() / np.abs(a[2]).max())
+    out["step_iters"] = [a[3], b[3]]
+    out["step_err"] = [a[4], b[4]]
+    out["step_maxrel"] = float(np.abs(a[5] - b[5]).max() / np.abs(a[5]).max())
+    out["ok"] = bool(out["bound_equal"] and a[1] == b[1] and a[3] == b[3] and out["leja_maxrel"] <= 1e-13
+                     and out["step_maxrel"] <= 1e-13)
+    if "--time" in sys.argv:
+        # per-iteration cost of the slab protocol (step kernels + NCCL halo/allgather, here to itself) vs the
+        # single-domain persistent kernel, 4096^2 phi_0 (config 1 shape)
+        wl = W.config(1)
+        pb = lx.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
+        u0 = torch.from_numpy(W.ic_problem1_2d(4096)).cuda()
+        for mode in ("single", "nccl"):
+            ctx = lx.Context(pb)
+            if mode == "nccl":
+                lxd.attach(ctx)
+            c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+            o = torch.empty_like(u0)
+            it = lx.lx_real_leja_phi(ctx, u0, o, wl.dt, c, g, 0, wl.rtol, wl.atol)
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            s0.record()
+            for _ in range(5):
+                lx.lx_real_leja_phi(ctx, u0, o, wl.dt, c, g, 0, wl.rtol, wl.atol)
+            s1.record()
+            torch.cuda.synchronize()
+            out["t_" + mode] = {"iters": it, "us_per_iter": s0.elapsed_time(s1) * 1e3 / (5 * it),
+                                "kernel": "two-step persistent" if mode == "single" else "step kernels + NCCL"}
+            ctx.close()
+    print(json.dumps(out), flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
