@@ -334,6 +334,8 @@ int comm_exchange(Comm* c, const double* base, double* ghost, cudaStream_t s) {
 // Enqueue iterations 1..last in chunks; poll `done` once per chunk (one chunk behind).
 template <typename Launch>
 static lx_status run_chunked(Comm* c, Ctrl* ctrl, int last, Launch launch, cudaStream_t s) {
+    static const int env_chunk = std::getenv("LX_COMM_CHUNK") ? std::atoi(std::getenv("LX_COMM_CHUNK")) : 0;
+    if (env_chunk > 0) c->chunk = env_chunk;   // experiments: iterations enqueued per host poll
     int chunk = 0;
     for (int m = 1; m <= last; m++) {
         if (launch(m)) return LX_ERR_NCCL;
