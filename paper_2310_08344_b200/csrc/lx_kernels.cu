@@ -1973,14 +1973,15 @@ __device__ __forceinline__ void s3_unit(const LejaParams& P, const double* __res
         cp_async_commit();
     }
     const int kc = k0 + 2 * lane;
-    // p / u of the next plane prefetched into registers one plane ahead (their latency off the barrier path)
-    double2 pv[RW][KK], uu[RW], pvn[RW][KK], uun[RW];
-    auto fetch = [&](int i, double2 (&pq)[RW][KK], double2 (&uq)[RW]) {
+    // p / u of the next plane prefetched into registers one plane ahead (their latency off the barrier path);
+    // K >= 3 keeps only u prefetched (the p registers would spill)
+    constexpr bool PREF = K <= 2;
+    constexpr int KP = PREF ? KK : 1;
+    double2 pv[RW][KK], uu[RW], pvn[RW][KP], uun[RW];
+    auto fetch_p = [&](int i, auto& pq) {
 #pragma unroll
         for (int r = 0; r < RW; r++) {
             const long long off = ((long long)i * n1 + (j0 + warp + r * kWarps)) * n2 + kc;
-            uq[r] = make_double2(0.0, 0.0);
-            if (DIAG && i < i1) uq[r] = ldg2(P.u + off);
 #pragma unroll
             for (int k = 0; k < KK; k++) {
                 pq[r][k] = make_double2(0.0, 0.0);
@@ -1988,12 +1989,23 @@ __device__ __forceinline__ void s3_unit(const LejaParams& P, const double* __res
             }
         }
     };
-    fetch(i0, pv, uu);
+    auto fetch_u = [&](int i, double2 (&uq)[RW]) {
+#pragma unroll
+        for (int r = 0; r < RW; r++) {
+            const long long off = ((long long)i * n1 + (j0 + warp + r * kWarps)) * n2 + kc;
+            uq[r] = make_double2(0.0, 0.0);
+            if (DIAG && i < i1) uq[r] = ldg2(P.u + off);
+        }
+    };
+    if constexpr (PREF) fetch_p(i0, pv);
+    fetch_u(i0, uu);
     for (int i = i0; i < i1; i++) {
         const int rel = i - i0 + 1;
         if (i + 3 <= i1 + 1) s3_issue(src, ring, i + 3, (rel + 3) % kS3Depth, j0, k0, n0, n1, n2);
-        cp_async_commit();
-        fetch(i + 1, pvn, uun);
+        cp_async_commit();   // (possibly empty group: keeps the wait_group accounting uniform)
+        if constexpr (PREF) fetch_p(i + 1, pvn);
+        fetch_u(i + 1, uun);
+        if constexpr (!PREF) fetch_p(i, pv);
         cp_async_wait<1>();
         __syncthreads();
         const uint32_t base = smem_u32(ring);
@@ -2066,8 +2078,10 @@ __device__ __forceinline__ void s3_unit(const LejaParams& P, const double* __res
 #pragma unroll
         for (int r = 0; r < RW; r++) {
             uu[r] = uun[r];
+            if constexpr (PREF) {
 #pragma unroll
-            for (int k = 0; k < KK; k++) pv[r][k] = pvn[r][k];
+                for (int k = 0; k < KP; k++) pv[r][k] = pvn[r][k];
+            }
         }
     }
     cp_async_wait<0>();
