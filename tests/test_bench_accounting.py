@@ -1,0 +1,46 @@
+"""Host-side accounting used by bench.py's roofline (CPU, no GPU).
+
+The algorithmic bytes of a Leja call are checked against an explicit pass-by-pass model of
+what each kernel reads and writes (one N-vector = 8 B/pt): the one-pass kernel does one pass per
+iteration; the two-step kernel does one pass per pair of iterations plus a rollback pass when the call
+stops on the first iteration of a pair.
+"""
+import pytest
+
+import bench
+
+
+def _passes_one_step(m):
+    traffic = 0
+    for it in range(1, m + 1):
+        if it == 1:
+            traffic += 8 * (1 + 2)          # read v; write y_1, p_1
+        else:
+            traffic += 8 * (2 + 2)          # read y, p; write y, p
+    return traffic
+
+
+def _passes_two_step(m):
+    traffic = 0
+    npass = (m + 1) // 2
+    for q in range(npass):
+        traffic += 8 * (1 + 2) if q == 0 else 8 * (2 + 2)
+    if m % 2 == 1:                           # stopped on the first iteration of the last pass: rollback
+        traffic += 8 * (2 + 1)               # read y, p; write p
+    return traffic
+
+
+@pytest.mark.parametrize("m", list(range(1, 41)))
+def test_leja_bytes_per_point_matches_pass_model(m):
+    assert bench.leja_bytes_per_point(m, False) == _passes_one_step(m)
+    assert bench.leja_bytes_per_point(m, True) == _passes_two_step(m)
+
+
+def test_config1_bytes_per_step():
+    # config 1 (4096^2, phi_0..phi_3 at 10 dt_CFL): 16/16/14/10 iterations (SURVEY 8(c) spectral simulation)
+    iters = (16, 16, 14, 10)
+    one = sum(bench.leja_bytes_per_point(m, False) for m in iters)
+    two = sum(bench.leja_bytes_per_point(m, True) for m in iters)
+    assert one == 8 * (3 + 4 * 15) + 8 * (3 + 4 * 15) + 8 * (3 + 4 * 13) + 8 * (3 + 4 * 9)
+    assert two == 8 * (3 + 4 * 7) * 2 + 8 * (3 + 4 * 6) + 8 * (3 + 4 * 4)
+    assert 2.0 < one / two < 2.1        # two iterations per pass (and the first pass reads v only)
