@@ -129,7 +129,10 @@ lx_status lx_ctx_destroy(lx_ctx *ctx);
  * per GPU).  nccl_unique_id: 128 bytes from lx_nccl_unique_id on rank 0,
  * broadcast by the caller (e.g. torch.distributed).  After this call every
  * vector argument is the caller's local slab (lx_slab_range).  Collective:
- * every rank must call it.  Errors: LX_ERR_NCCL, LX_ERR_DIM (slab < 2 rows). */
+ * every rank must call it.  nranks == 1 builds a real one-rank NCCL communicator
+ * (halo exchange and allgather with itself): the slab protocol on one GPU.
+ * Per Leja iteration: one step kernel + one NCCL group (1+2 halo rows, allgather
+ * of the 1+K per-rank partials).  Errors: LX_ERR_NCCL, LX_ERR_DIM (slab < 2 rows). */
 lx_status lx_nccl_unique_id(void *out128);
 lx_status lx_ctx_set_comm(lx_ctx *ctx, const void *nccl_unique_id, int rank, int nranks);
 
