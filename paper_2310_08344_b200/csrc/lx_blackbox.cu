@@ -102,10 +102,10 @@ __global__ void __launch_bounds__(kThreads) k_bb_perturb(BbArgs A, int m) {
     const long long npair = N >> 1;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < npair; i += (long long)gridDim.x * blockDim.x) {
         const double2 u = ld2g(A.u + 2 * i), y = ld2g(A.y_in + 2 * i);
-        st2g(A.w + 2 * i, make_double2(u.x + eps * y.x, u.y + eps * y.y));
+        st2g(A.w + 2 * i, make_double2(__dadd_rn(u.x, __dmul_rn(eps, y.x)), __dadd_rn(u.y, __dmul_rn(eps, y.y))));
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        if (N & 1) A.w[N - 1] = A.u[N - 1] + eps * A.y_in[N - 1];
+        if (N & 1) A.w[N - 1] = __dadd_rn(A.u[N - 1], __dmul_rn(eps, A.y_in[N - 1]));
         c->maxbits[m & 1] = 0ull;
     }
 }
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kThreads) k_bb_fdpiece(BbLin L, int op) {
     const double eps = ym == 0.0 ? 0.0 : kFdEps0 * (1.0 + u64_as_double(L.ctrl->umaxbits)) / ym;
     const long long N = L.N;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
-        if (op == 0) L.y0[i] = L.u[i] + eps * L.x0[i];
+        if (op == 0) L.y0[i] = __dadd_rn(L.u[i], __dmul_rn(eps, L.x0[i]));
         else L.y0[i] = L.x0[i] - (eps == 0.0 ? 0.0 : (L.x1[i] - L.fu[i]) / eps);
     }
 }
@@ -322,6 +322,55 @@ __global__ void __launch_bounds__(kThreads) k_bb_norm(BbLin L) {
     }
 }
 
+// f(u) of the built-in problems for the black-box path (lx_builtin_rhs), evaluated literally in the
+// order of the formulas (readings R10, R16, R24) with every operation explicitly
+// rounded (no FMA contraction, divisions by h^2 and 6h):
+//   lap_d = ((u_{+1} - 2 u_0) + u_{-1}) / (h h),   D_d(w) = ((((-w_{+2}) + 6 w_{+1}) - 3 w_0) - 2 w_{-1}) / (6 h)
+//   f = (diff sum_d lap_d) + (nu sum_d D_d(u)) [+ (beta 1/2) sum_d D_d(u u)] [+ react (u - (u u) u)] [+ S]
+// (sums over d in dimension order starting from 0).  The FD Jacobian (f(u + eps y) - f(u))/eps divides
+// every rounding difference of f by eps ~ 1.5e-8 (R25); a deterministic, contraction-free f makes the
+// black-box path reproducible bit for bit wherever its inputs are (SURVEY 8(f) f-1 "FMA-off").
+__device__ __forceinline__ long long lit_wrap(long long i, long long n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
+
+__device__ __forceinline__ double lit_at(const RhsLit& R, long long i0, long long i1, long long i2, int d, int o,
+                                         bool sq) {
+    if (d == 0) i0 = lit_wrap(i0 + o, R.n[0]);
+    else if (d == 1) i1 = lit_wrap(i1 + o, R.n[1]);
+    else i2 = lit_wrap(i2 + o, R.n[2]);
+    const double v = R.in[(i0 * R.n[1] + i1) * R.n[2] + i2];
+    return sq ? __dmul_rn(v, v) : v;
+}
+
+__device__ __forceinline__ double lit_upwind(double wm1, double w0, double w1, double w2, double h) {
+    return __ddiv_rn(__dsub_rn(__dsub_rn(__dadd_rn(-w2, __dmul_rn(6.0, w1)), __dmul_rn(3.0, w0)), __dmul_rn(2.0, wm1)),
+                     __dmul_rn(6.0, h));
+}
+
+__global__ void __launch_bounds__(kThreads) k_rhs_literal(RhsLit R) {
+    const long long N = R.n[0] * R.n[1] * R.n[2];
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+        const long long i2 = i % R.n[2], t = i / R.n[2];
+        const long long i1 = t % R.n[1], i0 = t / R.n[1];
+        double lap = 0.0, adv = 0.0, flx = 0.0;
+        for (int d = 0; d < R.ndim; d++) {
+            const double h = R.dx[d];
+            const double um1 = lit_at(R, i0, i1, i2, d, -1, false), u0 = lit_at(R, i0, i1, i2, d, 0, false);
+            const double up1 = lit_at(R, i0, i1, i2, d, 1, false), up2 = lit_at(R, i0, i1, i2, d, 2, false);
+            lap = __dadd_rn(lap, __ddiv_rn(__dadd_rn(__dsub_rn(up1, __dmul_rn(2.0, u0)), um1), __dmul_rn(h, h)));
+            adv = __dadd_rn(adv, lit_upwind(um1, u0, up1, up2, h));
+            if (R.flux != 0.0)
+                flx = __dadd_rn(flx, lit_upwind(lit_at(R, i0, i1, i2, d, -1, true), lit_at(R, i0, i1, i2, d, 0, true),
+                                                lit_at(R, i0, i1, i2, d, 1, true), lit_at(R, i0, i1, i2, d, 2, true), h));
+        }
+        double f = __dadd_rn(__dmul_rn(R.diff, lap), __dmul_rn(R.nu, adv));
+        if (R.flux != 0.0) f = __dadd_rn(f, __dmul_rn(__dmul_rn(R.flux, 0.5), flx));
+        const double u = R.in[i];
+        if (R.react != 0.0) f = __dadd_rn(f, __dmul_rn(R.react, __dsub_rn(u, __dmul_rn(__dmul_rn(u, u), u))));
+        if (R.src) f = __dadd_rn(f, R.src[i]);
+        R.out[i] = f;
+    }
+}
+
 }  // namespace
 
 int bb_grid(int nsm) { return nsm * 2; }
@@ -354,6 +403,10 @@ cudaError_t launch_bb_fdpiece(const BbLin& L, int op, cudaStream_t s) {
 }
 cudaError_t launch_bb_lincomb(const BbLin& L, cudaStream_t s) {
     k_bb_lincomb<<<L.grid, kThreads, 0, s>>>(L);
+    return cudaGetLastError();
+}
+cudaError_t launch_rhs_literal(const RhsLit& R, int grid, cudaStream_t s) {
+    k_rhs_literal<<<grid, kThreads, 0, s>>>(R);
     return cudaGetLastError();
 }
 cudaError_t launch_bb_norm(const BbLin& L, cudaStream_t s) {

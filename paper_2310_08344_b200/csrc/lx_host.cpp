@@ -1676,7 +1676,25 @@ void lx_builtin_rhs(const double* in, double* out, void* user, void* cuda_stream
     (void)cuda_stream;
     const lx_builtin_rhs_user* b = (const lx_builtin_rhs_user*)user;
     if (!b || !b->ctx || !b->pb) return;
-    rhs_device(b->ctx, b->pb, in, 1.0, out);
+    lx_ctx* ctx = b->ctx;
+    if (ctx->comm) {   // slab contexts: the fused stencil with halos
+        rhs_device(ctx, b->pb, in, 1.0, out);
+        return;
+    }
+    RhsLit R;
+    R.ndim = ctx->ndim;
+    for (int d = 0; d < 3; d++) {
+        R.n[d] = d < ctx->ndim ? ctx->n[d] : 1;
+        R.dx[d] = b->pb->dx[d];
+    }
+    R.diff = b->pb->diff;
+    R.nu = b->pb->nu;
+    R.react = b->pb->react;
+    R.flux = b->pb->flux;
+    R.src = b->pb->source;
+    R.in = in;
+    R.out = out;
+    if (launch_rhs_literal(R, ctx->nsm * 4, ctx->stream) == cudaSuccess) ctx->launches++;
 }
 
 lx_status lx_real_leja_phi_cb(lx_ctx* ctx, lx_rhs_fn f, void* user, const double* u, const double* v,

@@ -266,6 +266,17 @@ struct BbLin {
     BbCtrl* ctrl;
     Record* rec;
 };
+// literal, contraction-free f(u) of the built-in problems (lx_builtin_rhs; single domain)
+struct RhsLit {
+    int ndim;
+    long long n[3];                    // points per dimension (n[2] = 1 in 2D)
+    double dx[3];
+    double diff, nu, react, flux;
+    const double* src;                 // optional source S
+    const double* in;
+    double* out;
+};
+cudaError_t launch_rhs_literal(const RhsLit& R, int grid, cudaStream_t s);
 int bb_grid(int nsm);
 cudaError_t launch_bb_init(const BbArgs& A, cudaStream_t s);
 cudaError_t launch_bb_perturb(const BbArgs& A, int m, cudaStream_t s);

@@ -23,13 +23,15 @@ import paper_2310_08344_b200 as lx  # noqa: E402
 
 TOL = 1e-10
 FD_TOL = 1e-8
-# Integrator steps: the FD remainders F(x) = f(x) - J_FD(u) x carry the quotient noise
-# eps_mach sum|stencil terms| |u| / eps_x ~ 1.5e-8 |u| sum|coefficients|, times dt and the tableau
-# weights (up to 144).  Allen-Cahn at 64^2 (sum|coeff| ~ 3): ~1e-10 of |u| -> bar 1e-9 (measured
-# <= 3e-10; a wrong tableau weight moves u by ~|D| ~ 1e-7 and fails it).  Burgers at 48^2
-# (sum|coeff| ~ 5e3, dt ~ 2e-3): ~1e-8 -> bar 1e-7 (measured <= 1.7e-8).
+# Integrator steps.  The built-in black-box f (lx_builtin_rhs) evaluates the stencil formulas literally
+# with explicitly rounded operations (no FMA contraction; the order of P:549 / R10 / R24) and the FD
+# perturbation w = u + eps y is unfused, so the device's f(w) and f(u) equal the oracle's bit for bit;
+# the 1/eps amplification of rounding differences (~1e-8 per Jacobian application) is then gone and the
+# remaining differences are ordinary fp64 rounding in the Newton updates.  The steps are held to the f-1
+# bar of SURVEY 8(f), 1e-8 relative L2 (AC: 1e-9), with iteration counts equal.  A wrong tableau weight
+# moves u by ~|D| ~ 1e-7 and fails it.
 STEP_TOL_AC = 1e-9
-STEP_TOL_BURGERS = 1e-7
+STEP_TOL_BURGERS = 1e-8
 
 
 @pytest.fixture(scope="module", autouse=True)

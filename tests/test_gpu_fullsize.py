@@ -105,3 +105,27 @@ def test_config5_512cubed_tiled_epirk4s3a(xi300):
         for b in range(T):
             for d in range(T):
                 assert _rel(got[a, :, b, :, d, :], r.u_high) <= TOL, (a, b, d)
+
+
+def test_config2_allen_cahn_2048_steps_99_100(xi300):
+    # the END of config 2's 100-step run: lx_integrate runs steps 1..98 on the device (spectrum on the
+    # device every step); steps 99 and 100 are then compared one by one against the oracle started
+    # from the device state u_98 (same per-step iteration counts, relative L2 <= 1e-10, same err)
+    wl = W.config(2)
+    n = wl.shape[0]
+    assert wl.extra["steps"] == 100
+    pb = lx.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
+    ob = O.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
+    with lx.Context(pb) as ctx:
+        u = torch.from_numpy(W.ic_allen_cahn_2d(n)).cuda()
+        lx.lx_integrate(ctx, "exprb43", u, wl.dt, 98, wl.rtol, wl.atol)
+        ref = u.cpu().numpy()
+        for step in (99, 100):
+            it, err = lx.lx_integrate(ctx, "exprb43", u, wl.dt, 1, wl.rtol, wl.atol)
+            c, g = O.shift_scale(O.spectrum_bound(ob, ref))
+            r = O.step(ob, "exprb43", ref, wl.dt, c, g, wl.rtol, wl.atol, xi300)
+            assert r.status == O.OK
+            assert it == r.iters, (step, it, r.iters)
+            assert _rel(u.cpu().numpy(), r.u_high) <= TOL, step
+            assert err == pytest.approx(r.err, rel=1e-8), step
+            ref = u.cpu().numpy()   # continue from the device state (the comparison is per step)

