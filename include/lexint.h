@@ -126,27 +126,57 @@ lx_status lx_ctx_create(const lx_problem *pb, int max_nodes, int device, void *c
 lx_status lx_ctx_destroy(lx_ctx *ctx);
 
 /* Attach a communicator for slab decomposition over nranks GPUs (one process
- * per GPU).  nccl_unique_id: 128 bytes from lx_nccl_unique_id on rank 0,
- * broadcast by the caller (e.g. torch.distributed).  After this call every
- * vector argument is the caller's local slab (lx_slab_range).  Collective:
- * every rank must call it.  nranks == 1 builds a real one-rank NCCL communicator
- * (halo exchange and allgather with itself): the slab protocol on one GPU.
- * Per Leja iteration: one step kernel + one NCCL group (1+2 halo rows, allgather
- * of the 1+K per-rank partials).  Errors: LX_ERR_NCCL, LX_ERR_DIM (slab < 2 rows). */
+ * per GPU; SURVEY 8(e) -- the paper has no multi-GPU path).
+ * nccl_unique_id: 128 bytes from lx_nccl_unique_id on rank 0, broadcast by the
+ * caller (e.g. torch.distributed).  After this call every vector argument is
+ * the caller's local slab (lx_slab_range).  Collective: every rank must call it
+ * with the same flags.
+ * Leja calls on 2D grids with >= 16 rows per rank and >= 64 columns run ONE
+ * persistent kernel per call and rank (two Leja iterations per HBM pass): halo
+ * rows are stored into the neighbours' ghost rows through peer memory (CUDA IPC
+ * mappings of every rank's exchange block, handles gathered over NCCL) from
+ * inside the pass, and the per-rank norm partials meet at the pass barrier in
+ * every rank's exchange header (summed in rank order: identical decisions on
+ * every rank).  No NCCL call, no launch and no host round trip per iteration;
+ * a peer that does not arrive within 60 s ends the call with LX_ERR_TIMEOUT.
+ * Other operations (3D, Burgers, power iteration, stage kernels) use one step
+ * kernel + one NCCL group (1+2 halo rows, allgather of partials) per iteration.
+ * flags: LX_COMM_FORCE  -- build the communicator even for nranks == 1 (the slab
+ *                          protocol with itself; by default one rank = the
+ *                          single-domain context);
+ *        LX_COMM_NO_PEER -- never use the peer-memory slab kernel.
+ * Errors: LX_ERR_NCCL, LX_ERR_DIM (slab < 2 rows), LX_ERR_ARG. */
+#define LX_COMM_FORCE 1
+#define LX_COMM_NO_PEER 2
 lx_status lx_nccl_unique_id(void *out128);
 lx_status lx_ctx_set_comm(lx_ctx *ctx, const void *nccl_unique_id, int rank, int nranks);
+lx_status lx_ctx_set_comm_ex(lx_ctx *ctx, const void *nccl_unique_id, int rank, int nranks, int flags);
 
 /* In-process slab decomposition over `nranks` VIRTUAL ranks (host threads of
  * one process, all on the context's device).  Runs exactly the multi-rank
- * protocol of lx_ctx_set_comm (step kernels, 1+2-row halo exchange, rank-order
- * sum of gathered partials) with device-to-device copies and host barriers as
- * the transport; used to validate the slab path on one GPU and for
- * single-process multi-stream use.  Each rank's calls must be issued from its
- * own host thread, all ranks making the same sequence of calls. */
+ * protocols of lx_ctx_set_comm -- the peer-memory slab kernel (each virtual
+ * rank's persistent grid gets 1/nranks of the GPU) and the per-iteration step
+ * protocol with device-to-device copies and host barriers as the transport;
+ * used to validate the slab path on one GPU.  Each rank's calls must be issued
+ * from its own host thread, all ranks making the same sequence of calls.
+ * flags as for lx_ctx_set_comm_ex. */
 typedef struct lx_local_group lx_local_group;
 lx_status lx_local_group_create(int nranks, lx_local_group **out);
 lx_status lx_local_group_destroy(lx_local_group *group);
 lx_status lx_ctx_set_comm_local(lx_ctx *ctx, lx_local_group *group, int rank);
+lx_status lx_ctx_set_comm_local_ex(lx_ctx *ctx, lx_local_group *group, int rank, int flags);
+
+/* Peer-memory communicator whose handles the CALLER exchanges (e.g. over a
+ * torch.distributed gloo group): lx_ctx_ipc_handle allocates this context's
+ * exchange block and writes its 64-byte CUDA IPC handle to out64; after every
+ * rank gathered all handles (rank order, nranks x 64 bytes),
+ * lx_ctx_set_comm_ipc maps the peers' blocks.  Only Leja calls (the slab
+ * kernel) are available on such a context: operations that need a collective
+ * outside the kernel return LX_ERR_NCCL.  Ranks may share one GPU (processes
+ * time-slice it).  2D only, 1..8 ranks, >= 16 rows per rank, n1 >= 64.
+ * Errors: LX_ERR_UNSUPPORTED, LX_ERR_DIM, LX_ERR_ARG, LX_ERR_NCCL, LX_ERR_CUDA. */
+lx_status lx_ctx_ipc_handle(lx_ctx *ctx, void *out64);
+lx_status lx_ctx_set_comm_ipc(lx_ctx *ctx, int rank, int nranks, const void *handles);
 
 /* Local slab of this context: rows [*i_begin, *i_end), *n_local points. */
 lx_status lx_ctx_local(const lx_ctx *ctx, int64_t *i_begin, int64_t *i_end, int64_t *n_local);
@@ -157,10 +187,21 @@ lx_status lx_ctx_synchronize(lx_ctx *ctx, int *iters_total, double *err_last);
 
 /* Number of kernel launches this context has issued (for bench accounting). */
 int64_t lx_ctx_launch_count(const lx_ctx *ctx);
-/* Leja iterations per HBM pass of this context's Leja calls: 2 = the temporally blocked 2D kernel
- * (single GPU, >= 3*2^20 local points, or LX_TBLOCK=2), 1 = one pass per iteration.
- * Determines the algorithmic bytes of a call.  0 for a NULL context. */
+/* Leja iterations per HBM pass of this context's Leja calls on its constant-coefficient / Allen-Cahn
+ * problems: 2 = the temporally blocked 2D kernel (single domain with >= 3*2^20
+ * local points or lx_ctx_set_kernel(ctx, 2, .), and the peer-memory slab kernel), 1 = one pass per
+ * iteration.  Burgers (flux) problems always run one pass per iteration.  Determines the algorithmic
+ * bytes of a call.  0 for a NULL context. */
 int lx_ctx_iterations_per_pass(const lx_ctx *ctx);
+/* Kernel choice of this context (default 0 = automatic):
+ * iterations_per_pass -- 2D single-domain Leja calls: 1 = one Leja iteration per HBM pass
+ *                        (k_leja2d), 2 = two (k_leja2d_tb2, needs >= 16 rows and >= 64
+ *                        columns), 0 = two from 3*2^20 points on (measured crossover);
+ * kernel3d            -- 3D: 0 = shared-memory plane tiles when n1 % 16 == 0 and
+ *                        n2 % 64 == 0 (else warp tiles), 1 = warp tiles.
+ * All variants compute the same iterations (bitwise-equal fields except after a
+ * two-step rollback, which is within one rounding).  Errors: LX_ERR_ARG. */
+lx_status lx_ctx_set_kernel(lx_ctx *ctx, int iterations_per_pass, int kernel3d);
 
 /* ------------------------------------------------------------------------ */
 /* Spectrum (P:91, P:274-278 listing alg:lexint)                             */

@@ -28,6 +28,7 @@ LIB_PATH = os.environ.get("LX_LIBRARY") or os.path.join(_PKG, "liblexint_b200.so
 LX_OK, LX_ERR_ARG, LX_ERR_DIM, LX_ERR_ALIAS, LX_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 LX_ERR_NOCONV, LX_ERR_NONFINITE, LX_ERR_UNKNOWN_INTEGRATOR, LX_ERR_CUDA, LX_ERR_NCCL = 5, 6, 7, 8, 9
 LX_ERR_TIMEOUT = 10
+LX_COMM_FORCE, LX_COMM_NO_PEER = 1, 2
 STATUS_NAMES = {0: "LX_OK", 1: "LX_ERR_ARG", 2: "LX_ERR_DIM", 3: "LX_ERR_ALIAS", 4: "LX_ERR_UNSUPPORTED",
                 5: "LX_ERR_NOCONV", 6: "LX_ERR_NONFINITE", 7: "LX_ERR_UNKNOWN_INTEGRATOR", 8: "LX_ERR_CUDA",
                 9: "LX_ERR_NCCL", 10: "LX_ERR_TIMEOUT"}
@@ -43,7 +44,8 @@ EXPORTS = ("lx_last_error", "lx_version", "lx_leja_points", "lx_phi_scalar", "lx
            "lx_step_rosenbrock_euler", "lx_step_exprb32", "lx_step_exprb43", "lx_step_epirk4s3a",
            "lx_step_exprb42", "lx_step_epirk5p1",
            "lx_step", "lx_rhs", "lx_integrate", "lx_local_group_create", "lx_local_group_destroy", "lx_ctx_set_comm_local",
-           "lx_real_leja_phi_cb", "lx_step_cb", "lx_builtin_rhs")
+           "lx_real_leja_phi_cb", "lx_step_cb", "lx_builtin_rhs", "lx_ctx_set_comm_ex", "lx_ctx_set_comm_local_ex",
+           "lx_ctx_ipc_handle", "lx_ctx_set_comm_ipc", "lx_ctx_set_kernel")
 
 # void f(const double* in, double* out, void* user, void* cuda_stream)  (include/lexint.h lx_rhs_fn)
 RHS_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
@@ -134,6 +136,11 @@ def lib() -> ctypes.CDLL:
             "lx_local_group_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(vp)]),
             "lx_local_group_destroy": (ctypes.c_int, [vp]),
             "lx_ctx_set_comm_local": (ctypes.c_int, [vp, vp, ctypes.c_int]),
+            "lx_ctx_set_comm_ex": (ctypes.c_int, [vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+            "lx_ctx_set_comm_local_ex": (ctypes.c_int, [vp, vp, ctypes.c_int, ctypes.c_int]),
+            "lx_ctx_ipc_handle": (ctypes.c_int, [vp, vp]),
+            "lx_ctx_set_comm_ipc": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp]),
+            "lx_ctx_set_kernel": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int]),
             "lx_real_leja_phi_cb": (ctypes.c_int, [vp, vp, vp, vp, vp, ctypes.POINTER(vp), dp, ctypes.c_int,
                                                    d, d, d, ctypes.c_int, d, d, ip]),
             "lx_step_cb": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, vp, vp, vp, dp, d, d, d, d, d, ip]),
@@ -267,13 +274,29 @@ class Context:
     def __exit__(self, *a):
         self.close()
 
-    def set_comm(self, uid: bytes, rank: int, nranks: int):
+    def set_comm(self, uid: bytes, rank: int, nranks: int, flags: int = 0):
+        """flags: LX_COMM_FORCE (communicator even for one rank), LX_COMM_NO_PEER (no peer-memory kernel)."""
         buf = ctypes.create_string_buffer(uid, 128)
-        _check(lib().lx_ctx_set_comm(self.handle, buf, int(rank), int(nranks)))
+        _check(lib().lx_ctx_set_comm_ex(self.handle, buf, int(rank), int(nranks), int(flags)))
 
-    def set_comm_local(self, group: "LocalGroup", rank: int):
+    def set_comm_local(self, group: "LocalGroup", rank: int, flags: int = 0):
         self._group = group   # keep the group alive while the context uses it
-        _check(lib().lx_ctx_set_comm_local(self.handle, group.handle, int(rank)))
+        _check(lib().lx_ctx_set_comm_local_ex(self.handle, group.handle, int(rank), int(flags)))
+
+    def ipc_handle(self) -> bytes:
+        """64-byte CUDA IPC handle of this context's peer-memory exchange block (lx_ctx_ipc_handle)."""
+        buf = ctypes.create_string_buffer(64)
+        _check(lib().lx_ctx_ipc_handle(self.handle, buf))
+        return buf.raw
+
+    def set_comm_ipc(self, rank: int, handles: list):
+        """Peer-memory communicator from every rank's ipc_handle() (rank order)."""
+        buf = ctypes.create_string_buffer(b"".join(handles), 64 * len(handles))
+        _check(lib().lx_ctx_set_comm_ipc(self.handle, int(rank), len(handles), buf))
+
+    def set_kernel(self, iterations_per_pass: int = 0, kernel3d: int = 0):
+        """lx_ctx_set_kernel: 2D Leja iterations per HBM pass (0 auto, 1, 2); 3D kernel (0 auto, 1 warp tiles)."""
+        _check(lib().lx_ctx_set_kernel(self.handle, int(iterations_per_pass), int(kernel3d)))
 
     def local(self):
         b, e, n = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()

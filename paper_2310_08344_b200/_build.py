@@ -44,7 +44,8 @@ def _flags():
 
 
 def _deps():
-    return glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(ROOT, "include", "*.h"))
+    return (glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
+            glob.glob(os.path.join(ROOT, "include", "*.h")))
 
 
 def build(verbose: bool = False, force: bool = False) -> str:
@@ -56,18 +57,22 @@ def build(verbose: bool = False, force: bool = False) -> str:
         return LIB   # up to date (objects may be absent, e.g. on a gpurun box)
     objs = []
     flags = _flags()
+    cmds = []
     for s in srcs:
         o = os.path.join(BUILD, os.path.basename(s) + ".o")
         objs.append(o)
         if force or not os.path.exists(o) or os.path.getmtime(o) < max(os.path.getmtime(s), hdr_mtime):
             cmd = [NVCC] + ARCH + flags + ["-c", s, "-o", o]
-            if s.endswith(".cu"):
-                cmd += ["-Xptxas", "-v"] if verbose else []
-            else:
-                cmd += ["-x", "cu"] if False else []
+            if s.endswith(".cu") and verbose:
+                cmd += ["-Xptxas", "-v"]
             if verbose:
                 print(" ".join(cmd), file=sys.stderr)
-            subprocess.check_call(cmd)
+            cmds.append(cmd)
+    # translation units compile in parallel (the Leja kernel files dominate the build time)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        for f in [ex.submit(subprocess.check_call, c) for c in cmds]:
+            f.result()
     newest = max(os.path.getmtime(o) for o in objs)
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
         link = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB + ".tmp"] + objs

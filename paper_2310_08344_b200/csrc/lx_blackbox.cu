@@ -414,4 +414,17 @@ cudaError_t launch_bb_norm(const BbLin& L, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+cudaError_t preload_bb_kernels() {
+    const void* ks[] = {(const void*)k_bb_init, (const void*)k_bb_perturb, (const void*)k_bb_update<1>,
+                        (const void*)k_bb_update<2>, (const void*)k_bb_update<3>, (const void*)k_bb_update<4>,
+                        (const void*)k_bb_maxabs, (const void*)k_bb_fdpiece, (const void*)k_bb_lincomb,
+                        (const void*)k_bb_norm, (const void*)k_rhs_literal};
+    for (const void* k : ks) {
+        cudaFuncAttributes a;
+        const cudaError_t e = cudaFuncGetAttributes(&a, k);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 }  // namespace lx

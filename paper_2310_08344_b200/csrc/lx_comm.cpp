@@ -49,6 +49,10 @@ struct Transport {
     virtual int exchange_rows(const double* base, double* ghost, int n_loc, long long row, cudaStream_t s) = 0;
     virtual int allgather(const double* send, double* recv, int count, cudaStream_t s) = 0;
     virtual int allreduce_max_u64(unsigned long long* buf, cudaStream_t s) = 0;
+    // peer-memory slab transport: make every rank's exchange block addressable from this process;
+    // all[q] = rank q's block (all[rank] = mine).  Collective.
+    virtual int exchange_blocks(void* mine, void** all) = 0;
+    virtual void close_blocks(void** all) { (void)all; }
     // the per-iteration exchange: halo rows of y_m and the allgather of the per-rank partials
     virtual int exchange_and_gather(const double* base, double* ghost, int n_loc, long long row, const double* send,
                                     double* recv, int count, cudaStream_t s) {
@@ -94,8 +98,6 @@ struct NcclTransport : Transport {
     // aggregated into a single launch (halves the per-iteration NCCL launches of the slab protocol)
     int exchange_and_gather(const double* base, double* ghost, int n_loc, long long row, const double* send,
                             double* recv, int count, cudaStream_t s) override {
-        if (fused < 0) fused = std::getenv("LX_COMM_UNFUSED") ? 0 : 1;
-        if (!fused) return Transport::exchange_and_gather(base, ghost, n_loc, row, send, recv, count, s);
         const int up = (rank - 1 + nranks) % nranks, down = (rank + 1) % nranks;
         NC(ncclGroupStart());
         NC(ncclSend(base, 2 * row, ncclDouble, up, comm, s));
@@ -106,7 +108,38 @@ struct NcclTransport : Transport {
         NC(ncclGroupEnd());
         return 0;
     }
-    int fused = -1;
+    int fused = 1;
+    int exchange_blocks(void* mine, void** all) override {
+        cudaIpcMemHandle_t h;
+        CU(cudaIpcGetMemHandle(&h, mine));
+        char* buf = nullptr;
+        CU(cudaMalloc(&buf, (size_t)(nranks + 1) * sizeof h));
+        int rc = 0;
+        std::vector<cudaIpcMemHandle_t> hs(nranks);
+        if (cudaMemcpy(buf + (size_t)nranks * sizeof h, &h, sizeof h, cudaMemcpyHostToDevice) != cudaSuccess) {
+            rc = cerr("handle upload failed");
+        } else {
+            ncclResult_t r = ncclAllGather(buf + (size_t)nranks * sizeof h, buf, sizeof h, ncclChar, comm, 0);
+            if (r != ncclSuccess) rc = cerr(std::string("ncclAllGather(handles): ") + ncclGetErrorString(r));
+            else if (cudaStreamSynchronize(0) != cudaSuccess ||
+                     cudaMemcpy(hs.data(), buf, (size_t)nranks * sizeof h, cudaMemcpyDeviceToHost) != cudaSuccess)
+                rc = cerr("handle download failed");
+        }
+        cudaFree(buf);
+        for (int q = 0; q < nranks && !rc; q++) {
+            if (q == rank) {
+                all[q] = mine;
+                continue;
+            }
+            if (cudaIpcOpenMemHandle(&all[q], hs[q], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+                rc = cerr("cudaIpcOpenMemHandle of rank " + std::to_string(q) + " failed");
+        }
+        return rc;
+    }
+    void close_blocks(void** all) override {
+        for (int q = 0; q < nranks; q++)
+            if (q != rank && all[q]) cudaIpcCloseMemHandle(all[q]);
+    }
 };
 #endif
 
@@ -134,7 +167,8 @@ struct LocalGroup {
     std::vector<const void*> ptr;
     std::vector<int> nloc;
     std::vector<cudaEvent_t> ev;
-    explicit LocalGroup(int n) : nranks(n), ptr(n, nullptr), nloc(n, 0), ev(n, nullptr) {}
+    std::vector<void*> blk;    // peer-memory exchange blocks (same process: plain device pointers)
+    explicit LocalGroup(int n) : nranks(n), ptr(n, nullptr), nloc(n, 0), ev(n, nullptr), blk(n, nullptr) {}
     void barrier() {
         std::unique_lock<std::mutex> lk(mu);
         const long long g = gen;
@@ -206,6 +240,13 @@ struct LocalTransport : Transport {
         if (settle(s)) return 1;
         return rc;
     }
+    int exchange_blocks(void* mine, void** all) override {
+        g->blk[rank] = mine;
+        g->barrier();
+        for (int q = 0; q < nranks; q++) all[q] = g->blk[q];
+        g->barrier();
+        return 0;
+    }
     int allreduce_max_u64(unsigned long long* buf, cudaStream_t s) override {
         if (publish(buf, 0, s)) return 1;
         int rc = 0;
@@ -218,6 +259,33 @@ struct LocalTransport : Transport {
         if (settle(s)) return 1;   // all peers have read every buf before anyone overwrites its own
         if (!rc && launch_max_u64(tmp, nranks, buf, s) != cudaSuccess) rc = cerr("max kernel failed");
         return rc;
+    }
+};
+
+// ------------------------------------------------------------------ IPC only
+// Peer-memory transport whose handles were exchanged by the caller (lx_ctx_set_comm_ipc): the Leja
+// calls run the slab kernel over peer memory; operations that need a collective outside that kernel
+// (stage halos, norms, spectrum bounds) are not available in this mode.
+struct IpcTransport : Transport {
+    std::vector<cudaIpcMemHandle_t> hs;
+    int exchange_rows(const double*, double*, int, long long, cudaStream_t) override { return nocoll(); }
+    int allgather(const double*, double*, int, cudaStream_t) override { return nocoll(); }
+    int allreduce_max_u64(unsigned long long*, cudaStream_t) override { return nocoll(); }
+    static int nocoll() { return cerr("IPC-only communicator: only Leja calls (slab kernel) are supported"); }
+    int exchange_blocks(void* mine, void** all) override {
+        for (int q = 0; q < nranks; q++) {
+            if (q == rank) {
+                all[q] = mine;
+                continue;
+            }
+            if (cudaIpcOpenMemHandle(&all[q], hs[q], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+                return cerr("cudaIpcOpenMemHandle of rank " + std::to_string(q) + " failed");
+        }
+        return 0;
+    }
+    void close_blocks(void** all) override {
+        for (int q = 0; q < nranks; q++)
+            if (q != rank && all[q]) cudaIpcCloseMemHandle(all[q]);
     }
 };
 
@@ -236,7 +304,21 @@ struct Comm {
     Ctrl* ctrl_init = nullptr;     // pinned [kMaxK + 1] templates (hist[0] = active0)
     cudaEvent_t ev[2] = {nullptr, nullptr};
     int chunk = 4;
+    // peer-memory slab transport (k_leja2d_tb2<K, DIAG, true>)
+    bool peer = false;
+    char* blk = nullptr;           // this rank's exchange block: XHdr | ghost Y[0] | ghost Y[1] | ghost v | ghost u
+    void* blks[kMaxRanks] = {};    // every rank's block (peer pointers)
+    int grid_div = 1;              // virtual ranks share one GPU: each persistent grid gets 1/nranks of it
+    unsigned long long timeout_ns = 60ull * 1000000000ull;
 };
+
+static constexpr size_t kXHdrBytes = 4096;
+static_assert(sizeof(XHdr) <= kXHdrBytes, "exchange header");
+
+static size_t blk_bytes(long long row) { return kXHdrBytes + 4 * 6 * (size_t)row * sizeof(double); }
+static double* blk_ghost(void* b, long long row, int which) {   // 0, 1: Y[i]; 2: v; 3: u
+    return (double*)((char*)b + kXHdrBytes) + (size_t)which * 6 * row;
+}
 
 static int comm_alloc(Comm* c) {
     CU(cudaMalloc(&c->rank_part, kSlot * sizeof(double)));
@@ -307,6 +389,8 @@ int comm_create_local(LocalGroup* g, int rank, int device, long long row, Comm**
 
 void comm_destroy(Comm* c) {
     if (!c) return;
+    if (c->peer) c->tr->close_blocks(c->blks);
+    cudaFree(c->blk);
     delete c->tr;
     cudaFree(c->rank_part);
     cudaFree(c->gathered);
@@ -334,8 +418,6 @@ int comm_exchange(Comm* c, const double* base, double* ghost, cudaStream_t s) {
 // Enqueue iterations 1..last in chunks; poll `done` once per chunk (one chunk behind).
 template <typename Launch>
 static lx_status run_chunked(Comm* c, Ctrl* ctrl, int last, Launch launch, cudaStream_t s) {
-    static const int env_chunk = std::getenv("LX_COMM_CHUNK") ? std::atoi(std::getenv("LX_COMM_CHUNK")) : 0;
-    if (env_chunk > 0) c->chunk = env_chunk;   // experiments: iterations enqueued per host poll
     int chunk = 0;
     for (int m = 1; m <= last; m++) {
         if (launch(m)) return LX_ERR_NCCL;
@@ -366,11 +448,7 @@ lx_status comm_leja(Comm* c, LejaParams& P, bool diag, cudaStream_t s, int64_t* 
     auto launch = [&](int m) -> int {
         if (launch_leja_step(P, m, s, diag) != cudaSuccess) return cerr("step kernel launch failed");
         (*launches)++;
-        // diagnostics (LX_COMM_SKIP, one rank): no halo, the gather replaced by a D2D copy -> the step kernels alone
-        static const bool skip = std::getenv("LX_COMM_SKIP") != nullptr;
-        if (m < M && skip) {
-            CU(cudaMemcpyAsync(c->gathered, c->rank_part, kSlot * sizeof(double), cudaMemcpyDeviceToDevice, s));
-        } else if (m < M && c->tr->exchange_and_gather(c->Y[m & 1], c->Yg[m & 1], c->n_loc, c->row, c->rank_part,
+        if (m < M && c->tr->exchange_and_gather(c->Y[m & 1], c->Yg[m & 1], c->n_loc, c->row, c->rank_part,
                                                        c->gathered, kSlot, s)) {
             return 1;
         }
@@ -422,6 +500,70 @@ int comm_rhs(Comm* c, LejaParams& P, double scale, cudaStream_t s, int64_t* laun
     CU(launch_rhs(P, scale, s));
     (*launches)++;
     return 0;
+}
+
+// ------------------------------------------------------------------ peer-memory slab transport
+int comm_peer_enable(Comm* c, long long row) {
+    if (c->nranks > kMaxRanks) return cerr("peer transport: at most 8 ranks");
+    CU(cudaMalloc(&c->blk, blk_bytes(row)));
+    CU(cudaMemset(c->blk, 0, blk_bytes(row)));
+    CU(cudaDeviceSynchronize());   // zeroed flags before any peer can write them
+    if (c->tr->exchange_blocks(c->blk, c->blks)) return 1;
+    c->peer = true;
+    return 0;
+}
+
+size_t comm_block_bytes(long long row) { return blk_bytes(row); }
+
+int comm_create_ipc(int rank, int nranks, int device, long long row, const void* handles, void* blk, Comm** out) {
+    CU(cudaSetDevice(device));
+    if (nranks > kMaxRanks) return cerr("peer transport: at most 8 ranks");
+    Comm* c = new Comm();
+    c->rank = rank;
+    c->nranks = nranks;
+    c->device = device;
+    c->row = row;
+    c->blk = (char*)blk;   // owned from here on
+    auto* t = new IpcTransport();
+    t->rank = rank;
+    t->nranks = nranks;
+    t->hs.resize(nranks);
+    std::memcpy(t->hs.data(), handles, (size_t)nranks * sizeof(cudaIpcMemHandle_t));
+    c->tr = t;
+    if (comm_alloc(c) || c->tr->exchange_blocks(c->blk, c->blks)) {
+        comm_destroy(c);
+        return 1;
+    }
+    c->peer = true;
+    *out = c;
+    return 0;
+}
+
+void comm_set_grid_div(Comm* c, int div) { c->grid_div = div < 1 ? 1 : div; }
+bool comm_peer_ready(const Comm* c) { return c && c->peer; }
+int comm_grid_cap(const Comm* c, int grid) {
+    const int g = grid / c->grid_div;
+    return g < 1 ? 1 : g;
+}
+
+void comm_peer_params(const Comm* c, LejaParams& P, bool diag) {
+    (void)diag;
+    const int up = (c->rank - 1 + c->nranks) % c->nranks, dn = (c->rank + 1) % c->nranks;
+    P.xrank = c->rank;
+    P.xranks = c->nranks;
+    for (int q = 0; q < kMaxRanks; q++) P.xh[q] = q < c->nranks ? (XHdr*)c->blks[q] : nullptr;
+    for (int i = 0; i < 2; i++) {
+        P.gy[i] = blk_ghost(c->blk, c->row, i);
+        P.hup[i] = blk_ghost(c->blks[up], c->row, i);
+        P.hdn[i] = blk_ghost(c->blks[dn], c->row, i);
+    }
+    P.gv = blk_ghost(c->blk, c->row, 2);
+    P.gu = blk_ghost(c->blk, c->row, 3);
+    P.hup_v = blk_ghost(c->blks[up], c->row, 2);
+    P.hdn_v = blk_ghost(c->blks[dn], c->row, 2);
+    P.hup_u = blk_ghost(c->blks[up], c->row, 3);
+    P.hdn_u = blk_ghost(c->blks[dn], c->row, 3);
+    P.timeout_ns = c->timeout_ns;
 }
 
 }  // namespace lx

@@ -22,4 +22,14 @@ lx_status comm_power(Comm* c, LejaParams& P, bool diag, cudaStream_t s, int64_t*
 int comm_allreduce_max_u64(Comm* c, unsigned long long* dev, cudaStream_t s);
 int comm_stage_norm(Comm* c, int op, const StageArgs& A, cudaStream_t s, int64_t* launches);
 int comm_rhs(Comm* c, LejaParams& P, double scale, cudaStream_t s, int64_t* launches);
+// peer-memory slab transport (2D Leja calls: one persistent k_leja2d_tb2<K, DIAG, true> per call)
+int comm_peer_enable(Comm* c, long long row);                       // collective
+size_t comm_block_bytes(long long row);                            // exchange block of one rank
+// IPC-only communicator: blk = this rank's exchange block (cudaMalloc'd, zeroed; ownership passes to
+// the communicator), handles = every rank's cudaIpcMemHandle_t of its block (64 bytes each)
+int comm_create_ipc(int rank, int nranks, int device, long long row, const void* handles, void* blk, Comm** out);
+void comm_set_grid_div(Comm* c, int div);
+bool comm_peer_ready(const Comm* c);
+int comm_grid_cap(const Comm* c, int grid);
+void comm_peer_params(const Comm* c, LejaParams& P, bool diag);
 }  // namespace lx

@@ -90,23 +90,15 @@ struct lx_ctx {
     double* xi_dev = nullptr;             // Leja points on the device
     double* rcp_dev = nullptr;            // [M][M]: 1/(xi_j - xi_i), j > i (divided-difference recurrence)
     Comm* comm = nullptr;                 // slab decomposition (lx_comm.cpp)
-    int variant = 0;                      // 2D single-GPU Leja kernel: 0 = register tiles, 1 = TMA marching
-    int tblock = 0;                       // 2D single-GPU: Leja iterations per HBM pass (LX_TBLOCK=1 or 2;
-                                          // 0 = auto: two-step from kTb2MinPoints local points on)
-    int tb2_seg = -1;                     // two-step kernel: max segment length in chunks (LX_TB2_SEG; 0 static
-                                          // ranges; default 32 rows)
-    int tb2_order = 1;                    // two-step kernel: segment order (LX_TB2_ORDER)
+    int tblock = 0;                       // 2D single-GPU: Leja iterations per HBM pass (lx_ctx_set_kernel:
+                                          // 1 or 2; 0 = auto: two-step from kTb2MinPoints local points on)
     int tb2_cap = 0;                      // segments the buffers below can hold
     double* tb2_seg_part = nullptr;       // [cap][2(1+kMaxK)]
     double* tb2_grp_part = nullptr;       // [cap/32+1][2(1+kMaxK)]
     unsigned* tb2_grp_cnt = nullptr;      // [cap/32+1]
-    int* tb2_segrow = nullptr;            // guided segment-row table (device) for tb2_key
-    long long tb2_key = -1;               // (nrb, nb, grid) the table was built for
-    int tb2_nsrow = 0;
-    int k3d = 0;                          // 3D single-GPU Leja kernel: 0/1 smem marching when n1 % 16 == 0 and
-                                          // n2 % 64 == 0 (else warp tiles), 2 warp tiles (LX_3D_KERNEL=tile)
-    int tb2_sched = 0;                    // LX_TB2_SCHED: 0 fixed 32-row segments, 1 balanced, 2 guided
-    bool coef_table = false;              // LX_COEF=table: prebuilt coefficient table instead of in-kernel
+    void* ipc_blk = nullptr;              // exchange block handed out by lx_ctx_ipc_handle (before set_comm_ipc)
+    int k3d = 0;                          // 3D single-GPU Leja kernel: 0 = smem marching when n1 % 16 == 0 and
+                                          // n2 % 64 == 0 (else warp tiles), 1 = warp tiles (lx_ctx_set_kernel)
     double* cg_dev = nullptr;             // device (c, gamma, bound) of lx_integrate
     const double* cg_active = nullptr;    // when set, Leja kernels take (c, gamma) from here
     // black-box RHS path (lx_real_leja_phi_cb / lx_step_cb)
@@ -255,7 +247,8 @@ struct TableSpec {
 
 // Leja iterations per HBM pass of this context's 2D single-GPU Leja calls (1 or 2).
 static int ctx_tblock(const lx_ctx* ctx) {
-    if (ctx->ndim != 2 || ctx->comm || ctx->variant == 1 || ctx->n_loc < 16 || ctx->n[1] < 64) return 1;
+    if (ctx->comm) return comm_peer_ready(ctx->comm) ? 2 : 1;
+    if (ctx->ndim != 2 || ctx->n_loc < 16 || ctx->n[1] < 64) return 1;
     if (ctx->tblock == 1) return 1;
     if (ctx->tblock == 2) return 2;
     return ctx->N_loc >= kTb2MinPoints ? 2 : 1;
@@ -311,15 +304,43 @@ static LejaParams base_params(lx_ctx* ctx, const lx_problem* pb) {
 }
 
 // Core Leja call on device pointers (no staging, no sync).
+// Work decomposition of the two-step kernel (single domain and slab): items = (60-column band,
+// RT-row chunk); 32-row segments handed out dynamically, band fastest; per-segment / per-group partials.
+static lx_status tb2_setup(lx_ctx* ctx, LejaParams& P, int K, bool diag) {
+    P.nb = (P.n1 + kBand2 - 1) / kBand2;
+    P.nrb = (P.n_loc + tb2_rt(K) - 1) / tb2_rt(K);
+    P.nunits = P.nb * P.nrb;
+    P.grid = leja_tb2_grid_size(ctx->device, K, diag, P.nunits);
+    if (ctx->comm) P.grid = comm_grid_cap(ctx->comm, P.grid);
+    P.seg = 32 / tb2_rt(K);
+    P.nseg = P.nb * ((P.nrb + P.seg - 1) / P.seg);
+    P.ngrp = (P.nseg + 31) / 32;
+    if (P.nseg > ctx->tb2_cap) {
+        cudaFree(ctx->tb2_seg_part);
+    cudaFree(ctx->ipc_blk);
+        cudaFree(ctx->tb2_grp_part);
+        cudaFree(ctx->tb2_grp_cnt);
+        ctx->tb2_seg_part = nullptr;
+        ctx->tb2_grp_part = nullptr;
+        ctx->tb2_grp_cnt = nullptr;
+        ctx->tb2_cap = 0;
+        const size_t nv = 2 * (1 + kMaxK);
+        CUDA_TRY(cudaMalloc(&ctx->tb2_seg_part, (size_t)P.nseg * nv * sizeof(double)));
+        CUDA_TRY(cudaMalloc(&ctx->tb2_grp_part, (size_t)P.ngrp * nv * sizeof(double)));
+        CUDA_TRY(cudaMalloc(&ctx->tb2_grp_cnt, (size_t)P.ngrp * sizeof(unsigned)));
+        CUDA_TRY(cudaMemsetAsync(ctx->tb2_grp_cnt, 0, (size_t)P.ngrp * sizeof(unsigned), ctx->stream));
+        ctx->tb2_cap = P.nseg;
+    }
+    P.seg_part = ctx->tb2_seg_part;
+    P.grp_part = ctx->tb2_grp_part;
+    P.grp_cnt = ctx->tb2_grp_cnt;
+    return LX_OK;
+}
+
 static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u, const double* v, double* const* outs,
                              const double* coeffs, int K, double dt, double c, double gamma, int l, double rtol,
                              double atol, int rec, const double* table = nullptr) {
-    const bool tma = ctx->ndim == 2 && ctx->variant == 1 && !ctx->comm && !ctx->cg_active && pb->flux == 0.0;
     const double* coef = table;
-    if (!coef && (tma || (ctx->coef_table && !ctx->cg_active))) {   // prebuilt table (TMA / LX_COEF=table)
-        const TableSpec spec{l, K, coeffs};
-        LX_TRY(build_tables(ctx, &spec, 1, dt, c, gamma, rec, &coef));
-    }
     LejaParams P = base_params(ctx, pb);
     const bool diag = pb->react != 0.0;
     // coefficient description (read by the prologue of every Leja kernel)
@@ -352,120 +373,25 @@ static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u,
     for (int k = 0; k < K; k++) P.p[k] = outs[k];
     P.u = u;
     P.rec = ctx->rec_dev + rec;
-    if (ctx->comm) return comm_leja(ctx->comm, P, diag, ctx->stream, &ctx->launches);
-    if (ctx->ndim == 2 && ctx->variant == 1) {
-        P.grid = leja_tma_grid_size(ctx->device, K, diag, (long long)P.nb * P.n_loc);
-        if (P.grid > 0) {
-            CUDA_TRY(launch_leja_tma(P, ctx->stream, diag));
+    if (ctx->comm) {
+        // slab decomposition: the persistent two-step slab kernel over peer memory when the transport
+        // provides it (2D constant-coefficient / Allen-Cahn operators), else the per-iteration protocol
+        if (P.ndim == 2 && comm_peer_ready(ctx->comm) && P.n_loc >= 16 && P.n1 >= 64) {
+            LX_TRY(tb2_setup(ctx, P, K, diag));
+            comm_peer_params(ctx->comm, P, diag);
+            CUDA_TRY(launch_leja_tb2(P, ctx->stream, diag, true));
             ctx->launches++;
             return LX_OK;
         }
+        return comm_leja(ctx->comm, P, diag, ctx->stream, &ctx->launches);
     }
     if (P.ndim == 2 && ctx_tblock(ctx) == 2) {
-        // temporally blocked kernel: two iterations per pass; work items = (60-column band, RT-row chunk)
-        P.nb = (P.n1 + kBand2 - 1) / kBand2;
-        P.nrb = (P.n_loc + tb2_rt(K) - 1) / tb2_rt(K);
-        P.nunits = P.nb * P.nrb;
-        P.grid = leja_tb2_grid_size(ctx->device, K, diag, P.nunits);
-        P.seg = ctx->tb2_seg < 0 ? 32 / tb2_rt(K) : ctx->tb2_seg;   // default: 32-row segments
-        P.order = ctx->tb2_order;
-        P.segrow = nullptr;
-        if (ctx->tb2_seg < 0 && P.order && ctx->tb2_sched != 0) {
-            // guided self-scheduling: a segment row of length L chunks per band, L = remaining work /
-            // (2 x working warps), clamped to [8, 64] rows: large segments (few strip starts) early,
-            // short ones at the end of the pass (short tail before the grid barrier)
-            const long long key = ((((long long)P.nrb << 40) ^ ((long long)P.nb << 20) ^ (long long)P.grid) << 2) |
-                                  ctx->tb2_sched;
-            if (key != ctx->tb2_key) {
-                const int rt = tb2_rt(K);
-                const long long warps = (long long)P.grid * kWarps - 1;
-                std::vector<int> rows(1, 0);
-                if (ctx->tb2_sched == 1) {
-                    // balanced: a whole number k of ~32-row segments per working warp, so the last round of
-                    // the dynamic schedule keeps (almost) every warp busy: nsrow = floor(k warps / nb)
-                    // segment rows of nrb/nsrow chunks (lengths differ by <= 1 chunk)
-                    const long long units = (long long)P.nrb * P.nb;
-                    long long k = (units + (32 / rt) * warps / 2) / ((32 / rt) * warps);   // round(units / (32-row segment x warps))
-                    if (k < 1) k = 1;
-                    long long nsrow = k * warps / P.nb;
-                    if (nsrow < 1) nsrow = 1;
-                    if (nsrow > P.nrb) nsrow = P.nrb;
-                    for (long long i = 1; i <= nsrow; i++) rows.push_back((int)(i * P.nrb / nsrow));
-                } else {
-                int gmin = 16, gmax = 32, gk = 2;
-                if (const char* ev = std::getenv("LX_TB2_GUIDED")) std::sscanf(ev, "%d,%d,%d", &gmin, &gmax, &gk);
-                const int lmin = (gmin + rt - 1) / rt, lmax = gmax / rt;
-                int r = 0;
-                while (r < P.nrb) {
-                    const long long rem = (long long)(P.nrb - r) * P.nb;
-                    long long L = (rem + gk * warps - 1) / (gk * warps);
-                    L = L < lmin ? lmin : (L > lmax ? lmax : L);
-                    r = (int)std::min<long long>(P.nrb, r + L);
-                    rows.push_back(r);
-                }
-                }
-                cudaFree(ctx->tb2_segrow);
-                ctx->tb2_segrow = nullptr;
-                CUDA_TRY(cudaMalloc(&ctx->tb2_segrow, rows.size() * sizeof(int)));
-                CUDA_TRY(cudaMemcpyAsync(ctx->tb2_segrow, rows.data(), rows.size() * sizeof(int),
-                                         cudaMemcpyHostToDevice, ctx->stream));
-                CUDA_TRY(cudaStreamSynchronize(ctx->stream));   // rows is a host temporary
-                ctx->tb2_key = key;
-                ctx->tb2_nsrow = (int)rows.size() - 1;
-            }
-            P.segrow = ctx->tb2_segrow;
-            P.nseg = P.nb * ctx->tb2_nsrow;
-        } else if (P.seg > 0 && P.order) {
-            P.nseg = P.nb * ((P.nrb + P.seg - 1) / P.seg);
-        } else if (P.seg > 0) {
-            P.nseg = (P.nunits + P.seg - 1) / P.seg;
-        }
-        if (P.seg > 0) {
-            P.ngrp = (P.nseg + 31) / 32;
-            if (P.nseg > ctx->tb2_cap) {
-                cudaFree(ctx->tb2_seg_part);
-                cudaFree(ctx->tb2_grp_part);
-                cudaFree(ctx->tb2_grp_cnt);
-                ctx->tb2_seg_part = nullptr;
-                ctx->tb2_grp_part = nullptr;
-                ctx->tb2_grp_cnt = nullptr;
-                ctx->tb2_cap = 0;
-                const size_t nv = 2 * (1 + kMaxK);
-                CUDA_TRY(cudaMalloc(&ctx->tb2_seg_part, (size_t)P.nseg * nv * sizeof(double)));
-                CUDA_TRY(cudaMalloc(&ctx->tb2_grp_part, (size_t)P.ngrp * nv * sizeof(double)));
-                CUDA_TRY(cudaMalloc(&ctx->tb2_grp_cnt, (size_t)P.ngrp * sizeof(unsigned)));
-                CUDA_TRY(cudaMemsetAsync(ctx->tb2_grp_cnt, 0, (size_t)P.ngrp * sizeof(unsigned), ctx->stream));
-                ctx->tb2_cap = P.nseg;
-            }
-            P.seg_part = ctx->tb2_seg_part;
-            P.grp_part = ctx->tb2_grp_part;
-            P.grp_cnt = ctx->tb2_grp_cnt;
-        }
-        static const char* trace_path = std::getenv("LX_TB2_TRACE");   // diagnostics only
-        unsigned long long* tr = nullptr;
-        if (trace_path) {
-            CUDA_TRY(cudaMalloc(&tr, (size_t)160 * P.grid * 3 * sizeof(unsigned long long)));
-            CUDA_TRY(cudaMemsetAsync(tr, 0, (size_t)160 * P.grid * 3 * sizeof(unsigned long long), ctx->stream));
-            P.trace = tr;
-        }
+        LX_TRY(tb2_setup(ctx, P, K, diag));
         CUDA_TRY(launch_leja_tb2(P, ctx->stream, diag));
         ctx->launches++;
-        if (tr) {
-            std::vector<unsigned long long> h((size_t)160 * P.grid * 3);
-            CUDA_TRY(cudaMemcpyAsync(h.data(), tr, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                                     ctx->stream));
-            CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-            cudaFree(tr);
-            if (FILE* f = std::fopen(trace_path, "ab")) {
-                const int hdr[2] = {P.grid, 160};
-                std::fwrite(hdr, sizeof hdr, 1, f);
-                std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
-                std::fclose(f);
-            }
-        }
         return LX_OK;
     }
-    if (P.ndim == 3 && ctx->k3d != 2 && P.n1 % 16 == 0 && P.n2 % 64 == 0) {
+    if (P.ndim == 3 && ctx->k3d != 1 && P.n1 % 16 == 0 && P.n2 % 64 == 0) {
         // 3D marching kernel with shared-memory plane tiles: Newton coefficients from a prebuilt table
         if (P.coef_gen) {
             CoefJobs jobs;
@@ -562,7 +488,6 @@ static void free_ctx(lx_ctx* ctx) {
     cudaFree(ctx->tb2_seg_part);
     cudaFree(ctx->tb2_grp_part);
     cudaFree(ctx->tb2_grp_cnt);
-    cudaFree(ctx->tb2_segrow);
     cudaFree(ctx->ctrl);
     cudaFree(ctx->rec_dev);
     cudaFree(ctx->coef_dev);
@@ -636,16 +561,6 @@ lx_status lx_ctx_create(const lx_problem* pb, int max_nodes, int device, void* c
     ctx->N_loc = (int64_t)ctx->n_loc * ctx->row;
     ctx->N_glob = (double)ctx->n[0] * (double)ctx->row;
     ctx->max_nodes = max_nodes;
-    if (const char* ev = std::getenv("LX_LEJA_KERNEL")) ctx->variant = (std::strcmp(ev, "tma") == 0) ? 1 : 0;
-    if (const char* ev = std::getenv("LX_TBLOCK")) ctx->tblock = std::atoi(ev) == 1 ? 1 : (std::atoi(ev) == 2 ? 2 : 0);
-    if (const char* ev = std::getenv("LX_TB2_ORDER")) ctx->tb2_order = std::atoi(ev) != 0;
-    if (const char* ev = std::getenv("LX_3D_KERNEL"))
-        ctx->k3d = std::strcmp(ev, "smem") == 0 ? 1 : (std::strcmp(ev, "tile") == 0 ? 2 : 0);
-    if (const char* ev = std::getenv("LX_TB2_SCHED"))
-        ctx->tb2_sched = std::strcmp(ev, "balanced") == 0 ? 1 : (std::strcmp(ev, "guided") == 0 ? 2 : 0);
-    if (std::getenv("LX_TB2_GUIDED")) ctx->tb2_sched = 2;
-    if (const char* ev = std::getenv("LX_TB2_SEG")) ctx->tb2_seg = std::atoi(ev) > 0 ? std::atoi(ev) : 0;
-    if (const char* ev = std::getenv("LX_COEF")) ctx->coef_table = (std::strcmp(ev, "table") == 0);
     cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device);
     ctx->max_grid = ctx->nsm * 8;
     ctx->xi.resize(max_nodes);
@@ -749,16 +664,89 @@ static lx_status attach_comm(lx_ctx* ctx, Comm* c, int rank, int nranks) {
     return LX_OK;
 }
 
-lx_status lx_ctx_set_comm(lx_ctx* ctx, const void* uid, int rank, int nranks) {
+// Peer-memory slab contexts: every buffer a later call could allocate is allocated now.  A rank's
+// persistent slab kernel spins until all ranks' kernels arrive; a cudaMalloc / cudaFree on another rank
+// in between may wait for the device to idle (virtual ranks share one context) -> deadlock until the
+// watchdog.  Scratch vectors, and the two-step segment buffers for the largest segment count (RT = 2).
+static lx_status prealloc_slab(lx_ctx* ctx) {
+    for (int i = 0; i < kStage; i++)
+        if (!scratch(ctx, i)) return fail(LX_ERR_CUDA, "scratch allocation failed");
+    const int nb = ((int)ctx->n[1] + kBand2 - 1) / kBand2, nrb = (ctx->n_loc + 1) / 2, seg = 16;
+    const int nseg = nb * ((nrb + seg - 1) / seg), ngrp = (nseg + 31) / 32;
+    if (nseg > ctx->tb2_cap) {
+        cudaFree(ctx->tb2_seg_part);
+        cudaFree(ctx->tb2_grp_part);
+        cudaFree(ctx->tb2_grp_cnt);
+        const size_t nv = 2 * (1 + kMaxK);
+        CUDA_TRY(cudaMalloc(&ctx->tb2_seg_part, (size_t)nseg * nv * sizeof(double)));
+        CUDA_TRY(cudaMalloc(&ctx->tb2_grp_part, (size_t)ngrp * nv * sizeof(double)));
+        CUDA_TRY(cudaMalloc(&ctx->tb2_grp_cnt, (size_t)ngrp * sizeof(unsigned)));
+        CUDA_TRY(cudaMemsetAsync(ctx->tb2_grp_cnt, 0, (size_t)ngrp * sizeof(unsigned), ctx->stream));
+        ctx->tb2_cap = nseg;
+    }
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return LX_OK;
+}
+
+// The persistent slab kernel over peer memory needs a 2D grid with >= 16 rows per rank and >= 64
+// columns (the same condition on every rank: all ranks take the same path).
+static bool peer_eligible(const lx_ctx* ctx, int nranks, int flags) {
+    return !(flags & LX_COMM_NO_PEER) && ctx->ndim == 2 && nranks <= 8 && ctx->n[0] / nranks >= 16 && ctx->n[1] >= 64;
+}
+
+static lx_status detach_comm(lx_ctx* ctx) {
+    if (ctx->comm) comm_destroy(ctx->comm);
+    ctx->comm = nullptr;
+    return attach_comm(ctx, nullptr, 0, 1);
+}
+
+lx_status lx_ctx_set_comm_ex(lx_ctx* ctx, const void* uid, int rank, int nranks, int flags) {
     if (!ctx || !uid) return fail(LX_ERR_ARG, "NULL");
     LX_TRY(check_slabs(ctx, rank, nranks));
     cudaStreamSynchronize(ctx->stream);
+    if (nranks == 1 && !(flags & LX_COMM_FORCE)) return detach_comm(ctx);   // one rank = the single domain
     Comm* c = nullptr;
-    // nranks == 1 also builds a (self-)communicator: the slab protocol with NCCL halos to itself, used to
-    // check the NCCL transport on one GPU (tools/nccl_selfcheck.py)
     if (comm_create(uid, rank, nranks, ctx->device, ctx->row, ctx->nsm * 8, &c))
         return fail(LX_ERR_NCCL, "NCCL communicator: %s", comm_error());
-    return attach_comm(ctx, c, rank, nranks);
+    LX_TRY(attach_comm(ctx, c, rank, nranks));
+    if (peer_eligible(ctx, nranks, flags)) {
+        if (comm_peer_enable(c, ctx->row)) return fail(LX_ERR_NCCL, "peer-memory transport: %s", comm_error());
+        LX_TRY(prealloc_slab(ctx));
+    }
+    return LX_OK;
+}
+
+lx_status lx_ctx_set_comm(lx_ctx* ctx, const void* uid, int rank, int nranks) {
+    return lx_ctx_set_comm_ex(ctx, uid, rank, nranks, 0);
+}
+
+lx_status lx_ctx_ipc_handle(lx_ctx* ctx, void* out64) {
+    if (!ctx || !out64) return fail(LX_ERR_ARG, "NULL");
+    if (ctx->ndim != 2 || ctx->n[1] < 64) return fail(LX_ERR_UNSUPPORTED, "peer transport: 2D grids with n1 >= 64");
+    if (!ctx->ipc_blk) {
+        const size_t bytes = comm_block_bytes(ctx->row);
+        CUDA_TRY(cudaMalloc(&ctx->ipc_blk, bytes));
+        CUDA_TRY(cudaMemset(ctx->ipc_blk, 0, bytes));
+        CUDA_TRY(cudaDeviceSynchronize());
+    }
+    CUDA_TRY(cudaIpcGetMemHandle((cudaIpcMemHandle_t*)out64, ctx->ipc_blk));
+    return LX_OK;
+}
+
+lx_status lx_ctx_set_comm_ipc(lx_ctx* ctx, int rank, int nranks, const void* handles) {
+    if (!ctx || !handles) return fail(LX_ERR_ARG, "NULL");
+    if (!ctx->ipc_blk) return fail(LX_ERR_ARG, "call lx_ctx_ipc_handle first");
+    if (nranks < 1 || nranks > 8) return fail(LX_ERR_ARG, "IPC communicator: 1..8 ranks");
+    LX_TRY(check_slabs(ctx, rank, nranks));
+    if (!peer_eligible(ctx, nranks, 0)) return fail(LX_ERR_DIM, "IPC communicator: needs >= 16 rows per rank");
+    cudaStreamSynchronize(ctx->stream);
+    Comm* c = nullptr;
+    void* blk = ctx->ipc_blk;
+    ctx->ipc_blk = nullptr;   // owned by the communicator from here on
+    if (comm_create_ipc(rank, nranks, ctx->device, ctx->row, handles, blk, &c))
+        return fail(LX_ERR_NCCL, "IPC communicator: %s", comm_error());
+    LX_TRY(attach_comm(ctx, c, rank, nranks));
+    return prealloc_slab(ctx);
 }
 
 struct lx_local_group {
@@ -780,14 +768,29 @@ lx_status lx_local_group_destroy(lx_local_group* g) {
     return LX_OK;
 }
 
-lx_status lx_ctx_set_comm_local(lx_ctx* ctx, lx_local_group* g, int rank) {
+lx_status lx_ctx_set_comm_local_ex(lx_ctx* ctx, lx_local_group* g, int rank, int flags) {
     if (!ctx || !g) return fail(LX_ERR_ARG, "NULL");
     LX_TRY(check_slabs(ctx, rank, g->nranks));
     cudaStreamSynchronize(ctx->stream);
+    if (g->nranks == 1 && !(flags & LX_COMM_FORCE)) return detach_comm(ctx);
     Comm* c = nullptr;
-    if (g->nranks > 1 && comm_create_local(g->g, rank, ctx->device, ctx->row, &c))
+    // virtual ranks share this CUDA context: load every kernel before any of them spins on another
+    // (a lazy module load needs the context to idle -> deadlock with a spinning persistent kernel)
+    CUDA_TRY(preload_kernels());
+    CUDA_TRY(preload_bb_kernels());
+    if (comm_create_local(g->g, rank, ctx->device, ctx->row, &c))
         return fail(LX_ERR_NCCL, "local communicator: %s", comm_error());
-    return attach_comm(ctx, c, rank, g->nranks);
+    LX_TRY(attach_comm(ctx, c, rank, g->nranks));
+    if (peer_eligible(ctx, g->nranks, flags)) {
+        comm_set_grid_div(c, g->nranks);   // the virtual ranks' persistent grids share one GPU
+        if (comm_peer_enable(c, ctx->row)) return fail(LX_ERR_NCCL, "peer-memory transport: %s", comm_error());
+        LX_TRY(prealloc_slab(ctx));
+    }
+    return LX_OK;
+}
+
+lx_status lx_ctx_set_comm_local(lx_ctx* ctx, lx_local_group* g, int rank) {
+    return lx_ctx_set_comm_local_ex(ctx, g, rank, 0);
 }
 
 lx_status lx_ctx_local(const lx_ctx* ctx, int64_t* i_begin, int64_t* i_end, int64_t* n_local) {
@@ -812,6 +815,15 @@ lx_status lx_ctx_synchronize(lx_ctx* ctx, int* iters_total, double* err_last) {
 int64_t lx_ctx_launch_count(const lx_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 int lx_ctx_iterations_per_pass(const lx_ctx* ctx) { return ctx ? ctx_tblock(ctx) : 0; }
+
+lx_status lx_ctx_set_kernel(lx_ctx* ctx, int iterations_per_pass, int kernel3d) {
+    if (!ctx) return fail(LX_ERR_ARG, "NULL");
+    if (iterations_per_pass < 0 || iterations_per_pass > 2) return fail(LX_ERR_ARG, "iterations_per_pass in {0, 1, 2}");
+    if (kernel3d < 0 || kernel3d > 1) return fail(LX_ERR_ARG, "kernel3d in {0, 1}");
+    ctx->tblock = iterations_per_pass;
+    ctx->k3d = kernel3d;
+    return LX_OK;
+}
 
 // ---------------------------------------------------------------- Leja
 lx_status lx_real_leja_phi_vertical(lx_ctx* ctx, const lx_problem* pb, const double* u_lin, const double* v,
@@ -1030,43 +1042,6 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
     const double one = 1.0;
     // all coefficient tables of the step in one device launch
     static const double c1[1] = {1.0}, c2[2] = {0.5, 1.0}, c3[3] = {0.5, 2.0 / 3.0, 1.0}, c42[2] = {0.75, 1.0};
-    const double* tab[4] = {nullptr, nullptr, nullptr, nullptr};
-    if (!ctx->cg_active && ((ctx->ndim == 2 && ctx->variant == 1 && !ctx->comm) || ctx->coef_table)) {
-        TableSpec specs[4];
-        int n = 0;
-        if (method == LX_ROSENBROCK_EULER) {
-            specs[n++] = {1, 1, c1};
-        } else if (method == LX_EXPRB32) {
-            specs[n++] = {1, 1, c1};
-            specs[n++] = {3, 1, c1};
-        } else if (method == LX_EXPRB42) {
-            specs[n++] = {1, 2, c42};
-            specs[n++] = {3, 1, c1};
-        } else if (method == LX_EXPRB53S3) {
-            static const double e3[3] = {0.5, 0.9, 1.0};
-            specs[n++] = {1, 3, e3};
-            specs[n++] = {3, 3, e3};
-            specs[n++] = {3, 1, c1};
-            specs[n++] = {4, 1, c1};
-        } else if (method == LX_EPIRK5P1) {
-            static const double e3[3] = {epirk5::g11, epirk5::g21, epirk5::g31};
-            static const double e2[2] = {epirk5::g32, epirk5::g22};
-            static const double e1[1] = {epirk5::g33};
-            specs[n++] = {1, 3, e3};
-            specs[n++] = {1, 2, e2};
-            specs[n++] = {3, 1, e1};
-        } else if (method == LX_EXPRB43) {
-            specs[n++] = {1, 2, c2};
-            specs[n++] = {1, 1, c1};
-            specs[n++] = {3, 1, c1};
-            specs[n++] = {4, 1, c1};
-        } else {
-            specs[n++] = {1, 3, c3};
-            specs[n++] = {3, 1, c1};
-            specs[n++] = {4, 1, c1};
-        }
-        LX_TRY(build_tables(ctx, specs, n, dt, c, gamma, rec, tab));
-    }
     // f_u = RHS(u) * dt   (alg:Ros_Eu P:468-469)
     LX_TRY(rhs_device(ctx, pb, u, dt, S0));
     StageArgs A = stage_args(ctx, pb, rec);
@@ -1074,7 +1049,7 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
     A.u = u;
     if (method == LX_ROSENBROCK_EULER) {
         double* o[1] = {hi};
-        LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 1, rtol, atol, rec, tab[0]));
+        LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 1, rtol, atol, rec));
         A.x0 = u; A.x1 = hi; A.y0 = hi; A.a0 = 1.0; A.a1 = 1.0;  // u_exprb2 = u + phi_1(J dt) f dt
         LX_TRY(run_stage(ctx, ST_AXPBY, A));
         if (lo && lo != hi) CUDA_TRY(cudaMemcpyAsync(lo, hi, ctx->N_loc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
@@ -1083,7 +1058,7 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
     if (method == LX_EXPRB32) {
         // P:414-418, alg:exprb32: u_flux (in hi) -> a (lo), R_a (S0) -> u_nl_3 (hi) -> u_3 = a + 2 u_nl_3
         double* o[1] = {hi};
-        LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 1, rtol, atol, rec, tab[0]));
+        LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 1, rtol, atol, rec));
         if (!flux) {
             A.x0 = u; A.x1 = hi; A.y1 = lo; A.y0 = S0;
             LX_TRY(run_stage(ctx, ST_EXPRB32_A, A));
@@ -1092,7 +1067,7 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
             LX_TRY(run_stage(ctx, ST_AXPBY, A));
             LX_TRY(stage_remainder(ctx, pb, rec, u, lo, nullptr, 0.0, nullptr, 0.0, 1.0, dt, S0, nullptr));
         }
-        LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 3, rtol, atol, rec, tab[1]));
+        LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 3, rtol, atol, rec));
         A = stage_args(ctx, pb, rec);
         A.x0 = lo; A.x1 = hi; A.y0 = hi;
         return run_stage(ctx, ST_FINAL_EXPRB32, A);
@@ -1103,10 +1078,10 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
         double* S2 = scratch(ctx, 2);
         if (!S1 || !S2) return fail(LX_ERR_CUDA, "scratch allocation failed");
         double* pv[2] = {S1, S2};
-        LX_TRY(leja_device(ctx, pb, ul, S0, pv, c42, 2, dt, c, gamma, 1, rtol, atol, rec, tab[0]));
+        LX_TRY(leja_device(ctx, pb, ul, S0, pv, c42, 2, dt, c, gamma, 1, rtol, atol, rec));
         LX_TRY(stage_remainder(ctx, pb, rec, u, u, S1, 0.75, nullptr, 0.0, 32.0 / 9.0, dt, S0, hi));
         double* o3[1] = {S1};
-        LX_TRY(leja_device(ctx, pb, ul, S0, o3, &one, 1, dt, c, gamma, 3, rtol, atol, rec, tab[1]));
+        LX_TRY(leja_device(ctx, pb, ul, S0, o3, &one, 1, dt, c, gamma, 3, rtol, atol, rec));
         A = stage_args(ctx, pb, rec);
         A.x0 = u; A.x1 = S2; A.x2 = S1; A.y0 = hi;
         LX_TRY(run_stage(ctx, ST_SUM3, A));
@@ -1122,10 +1097,10 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
         if (!S1 || !S2 || !S3 || !S7) return fail(LX_ERR_CUDA, "scratch allocation failed");
         const double e3[3] = {0.5, 0.9, 1.0};
         double* pv[3] = {S1, S2, S3};                        // phi_1(c hJ) hf, c = 1/2, 9/10, 1
-        LX_TRY(leja_device(ctx, pb, ul, S0, pv, e3, 3, dt, c, gamma, 1, rtol, atol, rec, tab[0]));
+        LX_TRY(leja_device(ctx, pb, ul, S0, pv, e3, 3, dt, c, gamma, 1, rtol, atol, rec));
         LX_TRY(stage_remainder(ctx, pb, rec, u, u, S1, 0.5, nullptr, 0.0, 1.0, dt, S0, hi));   // D2 -> S0
         double* qv[3] = {S1, hi, lo};                        // phi_3(c hJ) D2, c = 1/2, 9/10, 1
-        LX_TRY(leja_device(ctx, pb, ul, S0, qv, e3, 3, dt, c, gamma, 3, rtol, atol, rec, tab[1]));
+        LX_TRY(leja_device(ctx, pb, ul, S0, qv, e3, 3, dt, c, gamma, 3, rtol, atol, rec));
         A = stage_args(ctx, pb, rec);                        // U3 = u + c3 P09 + 27/25 Q05 + 729/125 Q09
         A.x0 = u; A.x1 = S2; A.x2 = S1; A.x3 = hi; A.a0 = 0.9; A.a1 = 27.0 / 25.0; A.a2 = 729.0 / 125.0; A.y0 = S7;
         LX_TRY(run_stage(ctx, ST_LIN4, A));
@@ -1135,9 +1110,9 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
         A.a0 = 18.0; A.a1 = -250.0 / 81.0; A.a2 = -60.0; A.a3 = 500.0 / 27.0;
         LX_TRY(run_stage(ctx, ST_COMBINE2, A));
         double* o3[1] = {hi};
-        LX_TRY(leja_device(ctx, pb, ul, S1, o3, &one, 1, dt, c, gamma, 3, rtol, atol, rec, tab[2]));
+        LX_TRY(leja_device(ctx, pb, ul, S1, o3, &one, 1, dt, c, gamma, 3, rtol, atol, rec));
         double* o4[1] = {S0};
-        LX_TRY(leja_device(ctx, pb, ul, S7, o4, &one, 1, dt, c, gamma, 4, rtol, atol, rec, tab[3]));
+        LX_TRY(leja_device(ctx, pb, ul, S7, o4, &one, 1, dt, c, gamma, 4, rtol, atol, rec));
         A = stage_args(ctx, pb, rec);                        // d = Z3 + Z4 - 8 Q1 -> S2
         A.x0 = hi; A.x1 = S0; A.x2 = lo; A.a0 = 1.0; A.a1 = -8.0; A.y0 = S2;
         LX_TRY(run_stage(ctx, ST_LIN3, A));
@@ -1159,18 +1134,18 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
         if (!S1 || !S2 || !S3 || !S7) return fail(LX_ERR_CUDA, "scratch allocation failed");
         const double e3[3] = {g11, g21, g31}, e2[2] = {g32, g22}, e1[1] = {g33};
         double* pv[3] = {S1, S2, S3};
-        LX_TRY(leja_device(ctx, pb, ul, S0, pv, e3, 3, dt, c, gamma, 1, rtol, atol, rec, tab[0]));
+        LX_TRY(leja_device(ctx, pb, ul, S0, pv, e3, 3, dt, c, gamma, 1, rtol, atol, rec));
         // R1 = dt F(u + a11 P1) - dt F(u) -> S0 (f dt consumed)
         LX_TRY(stage_remainder(ctx, pb, rec, u, u, S1, a11, nullptr, 0.0, 1.0, dt, S0, hi));
         double* qv[2] = {S1, hi};                            // Q1 = phi_1(g32 hJ) R1, Q2 = phi_1(hJ) R1
-        LX_TRY(leja_device(ctx, pb, ul, S0, qv, e2, 2, dt, c, gamma, 1, rtol, atol, rec, tab[1]));
+        LX_TRY(leja_device(ctx, pb, ul, S0, qv, e2, 2, dt, c, gamma, 1, rtol, atol, rec));
         // R2 = dt F(u + a21 P2 + a22 Q2) - dt F(u) -> S2
         LX_TRY(stage_remainder(ctx, pb, rec, u, u, S2, a21, hi, a22, 1.0, dt, S7, S2));
         A = stage_args(ctx, pb, rec);
         A.x0 = S7; A.x1 = S0; A.a0 = 1.0; A.a1 = -2.0; A.y0 = S0;  // R2 - 2 R1
         LX_TRY(run_stage(ctx, ST_AXPBY, A));
         double* o3[1] = {S2};
-        LX_TRY(leja_device(ctx, pb, ul, S0, o3, e1, 1, dt, c, gamma, 3, rtol, atol, rec, tab[2]));
+        LX_TRY(leja_device(ctx, pb, ul, S0, o3, e1, 1, dt, c, gamma, 3, rtol, atol, rec));
         A = stage_args(ctx, pb, rec);
         A.x0 = u; A.x1 = S3; A.x2 = S1; A.x3 = S2; A.a0 = b1; A.a1 = b2; A.a2 = b3; A.y0 = hi;
         LX_TRY(run_stage(ctx, ST_LIN4, A));
@@ -1185,7 +1160,7 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
     if (!S1 || !S2 || (epirk && !S3)) return fail(LX_ERR_CUDA, "scratch allocation failed");
     const double cf2[2] = {0.5, 1.0}, cf3[3] = {0.5, 2.0 / 3.0, 1.0};
     double* pv[3] = {S1, S2, S3};
-    LX_TRY(leja_device(ctx, pb, ul, S0, pv, epirk ? cf3 : cf2, epirk ? 3 : 2, dt, c, gamma, 1, rtol, atol, rec, tab[0]));
+    LX_TRY(leja_device(ctx, pb, ul, S0, pv, epirk ? cf3 : cf2, epirk ? 3 : 2, dt, c, gamma, 1, rtol, atol, rec));
     double* p_one = epirk ? S3 : S2;
     // D_a = dt F(u + 1/2 p_half) - dt F(u)  -> S0
     LX_TRY(stage_remainder(ctx, pb, rec, u, u, S1, 0.5, nullptr, 0.0, 1.0, dt, S0, hi));
@@ -1197,7 +1172,7 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
     } else {
         // phi_1(hJ) D_a -> S1 ; b = u + p_one + S1 ; D_b -> lo
         double* o[1] = {S1};
-        LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 1, rtol, atol, rec, tab[1]));
+        LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 1, rtol, atol, rec));
         LX_TRY(stage_remainder(ctx, pb, rec, u, u, p_one, 1.0, S1, 1.0, 1.0, dt, lo, hi));
         Db = lo;
     }
@@ -1212,9 +1187,9 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
     double* q3 = S0;
     double* q4 = epirk ? S1 : lo;
     double* o3[1] = {q3};
-    LX_TRY(leja_device(ctx, pb, ul, w3, o3, &one, 1, dt, c, gamma, 3, rtol, atol, rec, tab[epirk ? 1 : 2]));
+    LX_TRY(leja_device(ctx, pb, ul, w3, o3, &one, 1, dt, c, gamma, 3, rtol, atol, rec));
     double* o4[1] = {q4};
-    LX_TRY(leja_device(ctx, pb, ul, hi, o4, &one, 1, dt, c, gamma, 4, rtol, atol, rec, tab[epirk ? 2 : 3]));
+    LX_TRY(leja_device(ctx, pb, ul, hi, o4, &one, 1, dt, c, gamma, 4, rtol, atol, rec));
     // u3 = u + p_one + q3 -> lo ; u4 = u3 + q4 -> hi ; err = ||u4 - u3||
     A = stage_args(ctx, pb, rec);
     A.x0 = u; A.x1 = p_one; A.x2 = q3; A.x3 = q4; A.y0 = lo; A.y1 = hi;

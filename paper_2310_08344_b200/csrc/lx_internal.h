@@ -83,6 +83,18 @@ struct Stencil {
     double a0[3], am1[3], ap1[3], ap2[3];   // D_d: centre, -1, +1, +2
 };
 
+// Exchange header of the peer-memory slab transport (one per rank, in IPC-shareable device memory;
+// every rank writes into every rank's header).  flag[q] = last epoch rank q published here;
+// part[e & 1][q] = rank q's partial sums of epoch e.  `epoch` is this rank's own counter.
+constexpr int kMaxRanks = 8;
+constexpr int kXNV = 2 * (1 + kMaxK);
+struct XHdr {
+    unsigned long long flag[kMaxRanks];
+    unsigned long long epoch;
+    unsigned long long pad[7];
+    double part[2][kMaxRanks][kXNV + 2];
+};
+
 struct LejaParams {
     int ndim;
     int n_loc;            // local rows (dim 0)
@@ -127,18 +139,24 @@ struct LejaParams {
     // nullptr -> cc / cgamma / alpha from the host
     const double* cg_dev;
     const double* source;  // optional source S added by the f(u) (M_RHS) tiles (Problem II)
-    // two-step kernel, dynamic segments of `seg` chunks (0 = static ranges): per-segment norm partials,
+    // two-step kernel: dynamic segments of `seg` chunks (band fastest); per-segment norm partials,
     // reduced in fixed order per group of 32 segments by the group's last finisher, then over groups
     int seg;
-    int order;            // 0: segments band-major (vertical strips); 1: band fastest (row-major)
     int nseg, ngrp;
     double* seg_part;     // [nseg][2(1+K)]
     double* grp_part;     // [ngrp][2(1+K)]
     unsigned* grp_cnt;    // [ngrp] finished segments of the group (reset by its last finisher)
-    // guided segment rows (order 1): segment row r covers chunks [segrow[r], segrow[r+1]) of every band;
-    // lengths shrink towards the end of a pass (guided self-scheduling) so the end-of-pass tail is short
-    const int* segrow;    // nullptr -> fixed rows of `seg` chunks
-    unsigned long long* trace;   // diagnostics (LX_TB2_TRACE): [pass][grid][3] globaltimer start/arrive/exit
+    // peer-memory slab mode (k_leja2d_tb2<K, DIAG, true>): ghost blocks hold rows
+    // -2, -1, n, n+1, n+2, n+3 of the local slab
+    XHdr* xh[kMaxRanks];  // every rank's exchange header (peer pointers; xh[xrank] is this rank's)
+    int xrank, xranks;
+    const double* gy[2];  // this rank's ghost blocks of Y[0], Y[1]
+    const double* gv;     // ... of the iteration-1 input v
+    const double* gu;     // ... of the linearisation state u (DIAG)
+    double* hup[2];       // ghost blocks of Y[i] on rank-1 (receive rows 0..3) ...
+    double* hdn[2];       // ... and on rank+1 (receive rows n-2, n-1)
+    double* hup_v; double* hdn_v; double* hup_u; double* hdn_u;
+    unsigned long long timeout_ns;   // cross-rank wait limit (LX_ERR_TIMEOUT)
 };
 
 // launchers (lx_kernels.cu)
@@ -152,10 +170,7 @@ int leja3d_smem_units(int n0, int n1, int n2);
 cudaError_t launch_leja3d_smem(const LejaParams& P, cudaStream_t s, bool diag);
 // temporally blocked 2D kernel: two Leja iterations per HBM pass (single GPU, constant coefficients + diag)
 int leja_tb2_grid_size(int device, int K, bool diag, int nunits);
-cudaError_t launch_leja_tb2(const LejaParams& P, cudaStream_t s, bool diag);
-// TMA-pipelined marching variant (2D, single GPU)
-int leja_tma_grid_size(int device, int K, bool diag, long long band_rows);
-cudaError_t launch_leja_tma(const LejaParams& P, cudaStream_t s, bool diag);
+cudaError_t launch_leja_tb2(const LejaParams& P, cudaStream_t s, bool diag, bool slab = false);
 
 struct StageArgs {
     int ndim, n_loc, n1, n2, nb, nrb, nunits;
@@ -277,6 +292,9 @@ struct RhsLit {
     double* out;
 };
 cudaError_t launch_rhs_literal(const RhsLit& R, int grid, cudaStream_t s);
+// load every kernel now (CUDA lazy loading): required before virtual ranks run spinning persistent kernels
+cudaError_t preload_kernels();
+cudaError_t preload_bb_kernels();
 int bb_grid(int nsm);
 cudaError_t launch_bb_init(const BbArgs& A, cudaStream_t s);
 cudaError_t launch_bb_perturb(const BbArgs& A, int m, cudaStream_t s);

@@ -1,4 +1,7 @@
-// lx_kernels.cu -- sm_100a fp64 kernels of the LeXInt hot path (arxiv 2310.08344).
+// lx_kernels.cu -- sm_100a fp64 kernels of the LeXInt hot path (arxiv 2310.08344): overview, the
+// coefficient / shift kernels, the integrator stage kernels and the preload of every kernel.
+// The Leja kernels live in lx_k_leja.cu (one pass per iteration), lx_k_tb2.cu (two per pass, single
+// domain and slab), lx_k_3d.cu (3D shared-memory tiles); shared device code in lx_dev.cuh.
 //
 // k_leja2d : ONE persistent cooperative kernel per Leja call.  Each iteration m
 //            is one fused HBM pass over the grid (Eq. (2)):
@@ -19,2344 +22,12 @@
 // upwind stencil reaches i-1, i+1, i+2), takes column neighbours from warp
 // shuffles (+2 edge-lane halo loads), and streams p.  Adjacent warps of a CTA
 // own adjacent column bands of the same rows, so halo re-reads hit L1/L2.
-#include "lx_internal.h"
-
-#include <cstdio>
-#include <map>
-#include <mutex>
+#include "lx_dev.cuh"
 
 namespace lx {
 
-#define FULL_MASK 0xffffffffu
 
-__device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
-__device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
-__device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
 
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-// spin-wait read: relaxed (no L1 invalidation per poll); the waiter issues one fence_acquire() after
-// it has seen the released value (relaxed load + fence.acq_rel = acquire pattern)
-__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-__device__ __forceinline__ void st_release64(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
-    unsigned old;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-    return old;
-}
-
-__device__ __forceinline__ const double* rowp(const RowSrc& s, int r) {
-    if ((unsigned)r < (unsigned)s.n_loc) return s.base + (long long)r * s.stride;
-    if (s.ghost) return s.ghost + (long long)(r < 0 ? 0 : r - s.n_loc + 1) * s.stride;
-    return s.base + (long long)(r < 0 ? r + s.n_loc : r - s.n_loc) * s.stride;
-}
-
-// phi_l with explicitly rounded operations (no FMA contraction), so every kernel
-// that evaluates it -- and every coefficient derived from it -- is bitwise reproducible.
-// Taylor terms use the constant reciprocals 1/n (one multiply instead of a division).
-__constant__ double c_inv_int[40] = {
-    0.0, 1.0, 1.0 / 2, 1.0 / 3, 1.0 / 4, 1.0 / 5, 1.0 / 6, 1.0 / 7, 1.0 / 8, 1.0 / 9, 1.0 / 10,
-    1.0 / 11, 1.0 / 12, 1.0 / 13, 1.0 / 14, 1.0 / 15, 1.0 / 16, 1.0 / 17, 1.0 / 18, 1.0 / 19, 1.0 / 20,
-    1.0 / 21, 1.0 / 22, 1.0 / 23, 1.0 / 24, 1.0 / 25, 1.0 / 26, 1.0 / 27, 1.0 / 28, 1.0 / 29, 1.0 / 30,
-    1.0 / 31, 1.0 / 32, 1.0 / 33, 1.0 / 34, 1.0 / 35, 1.0 / 36, 1.0 / 37, 1.0 / 38, 1.0 / 39};
-
-__device__ double phi_dev(int l, double z) {
-    const double inv_fact[6] = {1.0, 1.0, 0.5, 1.0 / 6.0, 1.0 / 24.0, 1.0 / 120.0};
-    if (fabs(z) < 2.0) {   // Taylor: sum_k z^k/(k+l)!  (34 terms: 2^34/34! ~ 1e-29)
-        double term = inv_fact[l], s = term;
-#pragma unroll
-        for (int k = 1; k < 34; k++) {
-            term = __dmul_rn(term, __dmul_rn(z, c_inv_int[k + l]));
-            s = __dadd_rn(s, term);
-        }
-        return s;
-    }
-    double p = exp(z);
-    for (int j = 0; j < l; j++) p = __ddiv_rn(__dsub_rn(p, inv_fact[j]), z);
-    return p;
-}
-
-__device__ __forceinline__ double coef_arg(double a, double dt, double c, double gamma, double x) {
-    // a*dt*(c + gamma*x), explicitly rounded (no contraction)
-    return __dmul_rn(__dmul_rn(a, dt), __dadd_rn(c, __dmul_rn(gamma, x)));
-}
-
-__device__ __forceinline__ double P_c(const LejaParams& P) { return P.cg_dev ? P.cg_dev[0] : P.cc; }
-__device__ __forceinline__ double P_g(const LejaParams& P) { return P.cg_dev ? P.cg_dev[1] : P.cgamma; }
-__device__ __forceinline__ double P_alpha(const LejaParams& P) {
-    return P.cg_dev ? (P.cdt == 0.0 ? 0.0 : 1.0 / P.cg_dev[1]) : P.alpha;
-}
-
-__device__ __forceinline__ double coef_h(const LejaParams& P, int k, int j) {
-    return phi_dev(P.l, coef_arg(P.ak[k], P.cdt, P_c(P), P_g(P), P.xi[j]));
-}
-
-// one step of the recurrence: (d - d_i) * 1/(xi_j - xi_i), explicitly rounded
-__device__ __forceinline__ double dd_step(double d, double di, double r) { return __dmul_rn(__dsub_rn(d, di), r); }
-
-__device__ __forceinline__ double coef_fold(const LejaParams& P, int K, int k, int j) {
-    double d = coef_h(P, k, j);
-    const int M = P.max_nodes;
-    const double* tab = P.table + 1 + k;
-    const double* Rc = P.R + j;
-    int i = 0;
-    for (; i + 4 <= j; i += 4) {
-        const double t0 = tab[(size_t)i * (1 + K)], t1 = tab[(size_t)(i + 1) * (1 + K)];
-        const double t2 = tab[(size_t)(i + 2) * (1 + K)], t3 = tab[(size_t)(i + 3) * (1 + K)];
-        const double r0 = Rc[(size_t)i * M], r1 = Rc[(size_t)(i + 1) * M];
-        const double r2 = Rc[(size_t)(i + 2) * M], r3 = Rc[(size_t)(i + 3) * M];
-        d = dd_step(d, t0, r0);
-        d = dd_step(d, t1, r1);
-        d = dd_step(d, t2, r2);
-        d = dd_step(d, t3, r3);
-    }
-    for (; i < j; i++) d = dd_step(d, tab[(size_t)i * (1 + K)], Rc[(size_t)i * M]);
-    return d;
-}
-
-// d_0, d_1, d_2 of accumulator k: computed by lane 0 of every warp, broadcast by shuffle
-// (all lanes of the warp must call it).
-__device__ __forceinline__ void coef_first3(const LejaParams& P, int k, double& d0, double& d1, double& d2) {
-    const int M = P.max_nodes;
-    double e0 = 0.0, e1 = 0.0, e2 = 0.0;
-    if ((threadIdx.x & 31) == 0) {
-        e0 = coef_h(P, k, 0);
-        e1 = M > 1 ? dd_step(coef_h(P, k, 1), e0, P.R[1]) : 0.0;
-        e2 = M > 2 ? dd_step(dd_step(coef_h(P, k, 2), e0, P.R[2]), e1, P.R[M + 2]) : 0.0;
-    }
-    d0 = __shfl_sync(0xffffffffu, e0, 0);
-    d1 = __shfl_sync(0xffffffffu, e1, 0);
-    d2 = __shfl_sync(0xffffffffu, e2, 0);
-}
-
-// Coefficient warp: write rows 0..2 (prologue) or row j (>= 3) of the table.
-template <int K>
-__device__ __forceinline__ void coef_write_row(const LejaParams& P, int j, int lane, int active, const double* dk) {
-    if (j >= P.max_nodes) return;
-    double* row = P.table + (size_t)j * (1 + K);
-    if (lane == 0) row[0] = (j == 0 || P.cdt == 0.0) ? 0.0 : (-P_c(P) / P_g(P) - P.xi[j - 1]);
-    if (lane < K && ((active >> lane) & 1)) row[1 + lane] = dk ? dk[lane] : coef_fold(P, K, lane, j);
-}
-
-__device__ __forceinline__ double coef_beta(const LejaParams& P, int m) {
-    return (P.cdt == 0.0) ? 0.0 : (-P_c(P) / P_g(P) - P.xi[m - 1]);
-}
-
-// Deterministic block reduction of n values: xor-butterfly inside warps, then
-// warps summed in index order by thread 0.  Result valid in thread 0.
-template <int N>
-__device__ __forceinline__ void block_reduce(double (&v)[N], double (*s_red)[kSlot]) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int i = 0; i < N; i++) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) v[i] += __shfl_xor_sync(FULL_MASK, v[i], off);
-    }
-    if (lane == 0) {
-#pragma unroll
-        for (int i = 0; i < N; i++) s_red[warp][i] = v[i];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int i = 0; i < N; i++) {
-            double s = s_red[0][i];
-            for (int w = 1; w < kWarps; w++) s += s_red[w][i];
-            v[i] = s;
-        }
-    }
-    __syncthreads();
-}
-
-__device__ __forceinline__ double nl_rem(double react, double x, double u) {
-    // F(x) = g(x) - g'(u) x,  g(x) = react (x - x^3)    (reading R18)
-    const double g = react * (x - x * x * x);
-    const double gp = react * (1.0 - 3.0 * u * u);
-    return g - gp * x;
-}
-
-enum TileMode { M_LEJA = 0, M_POWER = 1, M_RHS = 2, M_REM = 3 };
-
-// One warp work unit of the 2D stencil (64 columns x kRT rows).
-template <int K, bool DIAG, bool FIRST, int MODE, bool RO>
-__device__ __forceinline__ void tile2d(const LejaParams& P, const RowSrc& src, double* __restrict__ dst,
-                                       int unit, int lane, double beta, const double* d0, const double* dm,
-                                       int active, double scale, double& sy, double* sp) {
-    const int b = unit % P.nb;
-    const int rb = unit / P.nb;
-    const int n1 = P.n1;
-    const int j0 = b * 64 + 2 * lane;
-    const bool valid = j0 < n1;
-    const int last = min(31, ((n1 - b * 64) >> 1) - 1);
-    const int i0 = rb * kRT;
-    const int nout = min(kRT, P.n_loc - i0);
-    const Stencil& S = P.st;
-
-    double2 w[kRT + 3];
-#pragma unroll
-    for (int t = 0; t < kRT + 3; t++) {
-        w[t] = make_double2(0.0, 0.0);
-        if (valid && t < nout + 3) {
-            const double* rp = rowp(src, i0 - 1 + t) + j0;
-            w[t] = RO ? ldg2(rp) : ld2(rp);
-        }
-    }
-    double hl[kRT];
-    double2 hr[kRT];
-#pragma unroll
-    for (int t = 0; t < kRT; t++) {
-        hl[t] = 0.0;
-        hr[t] = make_double2(0.0, 0.0);
-        if (t < nout) {
-            const double* rp = rowp(src, i0 + t);
-            if (lane == 0) {
-                const int jl = (j0 == 0) ? n1 - 1 : j0 - 1;
-                hl[t] = RO ? __ldg(rp + jl) : rp[jl];
-            }
-            if (lane == last) {
-                int jr = j0 + 2;
-                if (jr >= n1) jr -= n1;
-                hr[t] = RO ? ldg2(rp + jr) : ld2(rp + jr);
-            }
-        }
-    }
-    constexpr int KK = K > 0 ? K : 1;
-    double2 pv[kRT][KK];
-    double2 uu[kRT];
-#pragma unroll
-    for (int t = 0; t < kRT; t++) {
-        const long long off = (long long)(i0 + t) * n1 + j0;
-        if (MODE == M_LEJA && !FIRST) {
-#pragma unroll
-            for (int k = 0; k < KK; k++) {
-                pv[t][k] = make_double2(0.0, 0.0);
-                if (valid && t < nout && ((active >> k) & 1)) pv[t][k] = ld2(P.p[k] + off);
-            }
-        }
-        uu[t] = make_double2(0.0, 0.0);
-        if (DIAG && valid && t < nout) uu[t] = ldg2(P.u + off);
-    }
-
-#pragma unroll
-    for (int t = 0; t < kRT; t++) {
-        if (t < nout) {  // uniform across the warp
-            const double2 yc = w[t + 1], up = w[t], dn1 = w[t + 2], dn2 = w[t + 3];
-            double left = __shfl_up_sync(FULL_MASK, yc.y, 1);
-            double r1 = __shfl_down_sync(FULL_MASK, yc.x, 1);
-            double r2 = __shfl_down_sync(FULL_MASK, yc.y, 1);
-            if (lane == 0) left = hl[t];
-            if (lane == last) {
-                r1 = hr[t].x;
-                r2 = hr[t].y;
-            }
-            // A y at (i, j0) and (i, j0+1): fixed summation order
-            double ax = S.c0 * yc.x;
-            ax = fma(S.m1[0], up.x, ax);
-            ax = fma(S.p1[0], dn1.x, ax);
-            ax = fma(S.p2[0], dn2.x, ax);
-            ax = fma(S.m1[1], left, ax);
-            ax = fma(S.p1[1], yc.y, ax);
-            ax = fma(S.p2[1], r1, ax);
-            double ay = S.c0 * yc.y;
-            ay = fma(S.m1[0], up.y, ay);
-            ay = fma(S.p1[0], dn1.y, ay);
-            ay = fma(S.p2[0], dn2.y, ay);
-            ay = fma(S.m1[1], yc.x, ay);
-            ay = fma(S.p1[1], r1, ay);
-            ay = fma(S.p2[1], r2, ay);
-            if (DIAG) {
-                ax = fma(fma(S.qb, uu[t].x * uu[t].x, S.qa), yc.x, ax);
-                ay = fma(fma(S.qb, uu[t].y * uu[t].y, S.qa), yc.y, ay);
-            }
-            double2 yn;
-            if (MODE == M_POWER) {
-                yn.x = scale * ax;
-                yn.y = scale * ay;
-            } else if (MODE == M_RHS) {
-                // f(u)*scale = scale*(A u + react*(u - u^3) [+ S])
-                double fx = fma(S.react, yc.x - yc.x * yc.x * yc.x, ax);
-                double fy = fma(S.react, yc.y - yc.y * yc.y * yc.y, ay);
-                if (P.source && valid) {
-                    const double2 sv = ldg2(P.source + (long long)(i0 + t) * n1 + j0);
-                    fx += sv.x;
-                    fy += sv.y;
-                }
-                yn.x = scale * fx;
-                yn.y = scale * fy;
-            } else {
-                yn.x = fma(scale, ax, beta * yc.x);   // M_LEJA: scale = alpha = 1/gamma
-                yn.y = fma(scale, ay, beta * yc.y);
-            }
-            if (valid) {
-                const long long off = (long long)(i0 + t) * n1 + j0;
-                st2(dst + off, yn);
-                sy = fma(yn.x, yn.x, sy);
-                sy = fma(yn.y, yn.y, sy);
-                if (MODE == M_LEJA) {
-#pragma unroll
-                    for (int k = 0; k < KK; k++) {
-                        if ((active >> k) & 1) {
-                            double2 pn;
-                            if (FIRST) {
-                                pn.x = fma(dm[k], yn.x, d0[k] * yc.x);
-                                pn.y = fma(dm[k], yn.y, d0[k] * yc.y);
-                            } else {
-                                pn.x = fma(dm[k], yn.x, pv[t][k].x);
-                                pn.y = fma(dm[k], yn.y, pv[t][k].y);
-                            }
-                            st2(P.p[k] + off, pn);
-                            sp[k] = fma(pn.x, pn.x, sp[k]);
-                            sp[k] = fma(pn.y, pn.y, sp[k]);
-                        }
-                    }
-                }
-            }
-        }
-    }
-}
-
-
-// One warp work unit of the 3D stencil: 64 contiguous k (dim 2) x one j row (dim 1)
-// x kRT3 planes (dim 0).  i-neighbours from the plane window, j-neighbours from
-// rows j-1, j+1, j+2 of the same plane (adjacent warps own adjacent j -> L1 hits),
-// k-neighbours by shuffles + edge-lane halo loads.  Units: u = (pb*nb + b)*n1 + j.
-template <int K, bool DIAG, bool FIRST, int MODE, bool RO>
-__device__ __forceinline__ void tile3d(const LejaParams& P, const RowSrc& src, double* __restrict__ dst,
-                                       int unit, int lane, double beta, const double* d0, const double* dm,
-                                       int active, double scale, double& sy, double* sp) {
-    const int n1 = P.n1, n2 = P.n2;
-    const int j = unit % n1;
-    const int t0 = unit / n1;
-    const int b = t0 % P.nb;
-    const int pb = t0 / P.nb;
-    const int k0 = b * 64 + 2 * lane;
-    const bool valid = k0 < n2;
-    const int last = min(31, ((n2 - b * 64) >> 1) - 1);
-    const int i0 = pb * kRT3;
-    const int nout = min(kRT3, P.n_loc - i0);
-    const int jm = (j == 0) ? n1 - 1 : j - 1;
-    const int jp1 = (j + 1 >= n1) ? j + 1 - n1 : j + 1;
-    const int jp2 = (j + 2 >= n1) ? j + 2 - n1 : j + 2;
-    const Stencil& S = P.st;
-    auto LD2 = [&](const double* q) { return RO ? ldg2(q) : ld2(q); };
-
-    double2 w[kRT3 + 3];
-#pragma unroll
-    for (int t = 0; t < kRT3 + 3; t++) {
-        w[t] = make_double2(0.0, 0.0);
-        if (valid && t < nout + 3) w[t] = LD2(rowp(src, i0 - 1 + t) + (long long)j * n2 + k0);
-    }
-    double2 wm[kRT3], wp1[kRT3], wp2[kRT3];
-    double hl[kRT3];
-    double2 hr[kRT3];
-#pragma unroll
-    for (int t = 0; t < kRT3; t++) {
-        wm[t] = wp1[t] = wp2[t] = hr[t] = make_double2(0.0, 0.0);
-        hl[t] = 0.0;
-        if (t < nout) {
-            const double* pl = rowp(src, i0 + t);
-            if (valid) {
-                wm[t] = LD2(pl + (long long)jm * n2 + k0);
-                wp1[t] = LD2(pl + (long long)jp1 * n2 + k0);
-                wp2[t] = LD2(pl + (long long)jp2 * n2 + k0);
-            }
-            const double* rp = pl + (long long)j * n2;
-            if (lane == 0) {
-                const int kl = (k0 == 0) ? n2 - 1 : k0 - 1;
-                hl[t] = RO ? __ldg(rp + kl) : rp[kl];
-            }
-            if (lane == last) {
-                int kr = k0 + 2;
-                if (kr >= n2) kr -= n2;
-                hr[t] = LD2(rp + kr);
-            }
-        }
-    }
-    constexpr int KK = K > 0 ? K : 1;
-    double2 pv[kRT3][KK];
-    double2 uu[kRT3];
-#pragma unroll
-    for (int t = 0; t < kRT3; t++) {
-        const long long off = ((long long)(i0 + t) * n1 + j) * n2 + k0;
-        if (MODE == M_LEJA && !FIRST) {
-#pragma unroll
-            for (int k = 0; k < KK; k++) {
-                pv[t][k] = make_double2(0.0, 0.0);
-                if (valid && t < nout && ((active >> k) & 1)) pv[t][k] = ld2(P.p[k] + off);
-            }
-        }
-        uu[t] = make_double2(0.0, 0.0);
-        if (DIAG && valid && t < nout) uu[t] = ldg2(P.u + off);
-    }
-#pragma unroll
-    for (int t = 0; t < kRT3; t++) {
-        if (t < nout) {
-            const double2 yc = w[t + 1], up = w[t], dn1 = w[t + 2], dn2 = w[t + 3];
-            double left = __shfl_up_sync(FULL_MASK, yc.y, 1);
-            double r1 = __shfl_down_sync(FULL_MASK, yc.x, 1);
-            double r2 = __shfl_down_sync(FULL_MASK, yc.y, 1);
-            if (lane == 0) left = hl[t];
-            if (lane == last) {
-                r1 = hr[t].x;
-                r2 = hr[t].y;
-            }
-            double ax = S.c0 * yc.x;
-            ax = fma(S.m1[0], up.x, ax);
-            ax = fma(S.p1[0], dn1.x, ax);
-            ax = fma(S.p2[0], dn2.x, ax);
-            ax = fma(S.m1[1], wm[t].x, ax);
-            ax = fma(S.p1[1], wp1[t].x, ax);
-            ax = fma(S.p2[1], wp2[t].x, ax);
-            ax = fma(S.m1[2], left, ax);
-            ax = fma(S.p1[2], yc.y, ax);
-            ax = fma(S.p2[2], r1, ax);
-            double ay = S.c0 * yc.y;
-            ay = fma(S.m1[0], up.y, ay);
-            ay = fma(S.p1[0], dn1.y, ay);
-            ay = fma(S.p2[0], dn2.y, ay);
-            ay = fma(S.m1[1], wm[t].y, ay);
-            ay = fma(S.p1[1], wp1[t].y, ay);
-            ay = fma(S.p2[1], wp2[t].y, ay);
-            ay = fma(S.m1[2], yc.x, ay);
-            ay = fma(S.p1[2], r1, ay);
-            ay = fma(S.p2[2], r2, ay);
-            if (DIAG) {
-                ax = fma(fma(S.qb, uu[t].x * uu[t].x, S.qa), yc.x, ax);
-                ay = fma(fma(S.qb, uu[t].y * uu[t].y, S.qa), yc.y, ay);
-            }
-            double2 yn;
-            if (MODE == M_POWER) {
-                yn.x = scale * ax;
-                yn.y = scale * ay;
-            } else if (MODE == M_RHS) {
-                double fx = fma(S.react, yc.x - yc.x * yc.x * yc.x, ax);
-                double fy = fma(S.react, yc.y - yc.y * yc.y * yc.y, ay);
-                if (P.source && valid) {
-                    const double2 sv = ldg2(P.source + ((long long)(i0 + t) * n1 + j) * n2 + k0);
-                    fx += sv.x;
-                    fy += sv.y;
-                }
-                yn.x = scale * fx;
-                yn.y = scale * fy;
-            } else {
-                yn.x = fma(scale, ax, beta * yc.x);   // M_LEJA: scale = alpha = 1/gamma
-                yn.y = fma(scale, ay, beta * yc.y);
-            }
-            if (valid) {
-                const long long off = ((long long)(i0 + t) * n1 + j) * n2 + k0;
-                st2(dst + off, yn);
-                sy = fma(yn.x, yn.x, sy);
-                sy = fma(yn.y, yn.y, sy);
-                if (MODE == M_LEJA) {
-#pragma unroll
-                    for (int k = 0; k < KK; k++) {
-                        if ((active >> k) & 1) {
-                            double2 pn;
-                            if (FIRST) {
-                                pn.x = fma(dm[k], yn.x, d0[k] * yc.x);
-                                pn.y = fma(dm[k], yn.y, d0[k] * yc.y);
-                            } else {
-                                pn.x = fma(dm[k], yn.x, pv[t][k].x);
-                                pn.y = fma(dm[k], yn.y, pv[t][k].y);
-                            }
-                            st2(P.p[k] + off, pn);
-                            sp[k] = fma(pn.x, pn.x, sp[k]);
-                            sp[k] = fma(pn.y, pn.y, sp[k]);
-                        }
-                    }
-                }
-            }
-        }
-    }
-}
-
-
-// ---------------------------------------------------------------------------
-// Flux-form 2D tile (Problem III, viscous Burgers; exact Jacobian R13):
-//   M_LEJA/M_POWER: A y = diff lap(y) + sum_d D_d((nu + beta u) y)      (J(u) y)
-//   M_RHS:          f(u) = diff lap(u) + sum_d D_d((nu + beta/2 u) u) [+ react g(u) + S]
-//   M_REM:          a2 * (dt F(x) - dt F(u)),  F(x) = sum_d D_d(beta/2 x^2 - beta u x) + g-part
-// Two register windows (the field y/x and u) with the same row / shuffle / halo
-// pattern as tile2d.  Single GPU (u is read with periodic wrap).  For M_REM the
-// `beta` argument carries dt and `scale` carries a2.
-// ---------------------------------------------------------------------------
-template <int K, bool FIRST, int MODE, bool RO>
-__device__ __forceinline__ void tile2d_flux(const LejaParams& P, const RowSrc& src, double* __restrict__ dst,
-                                            int unit, int lane, double beta, const double* d0, const double* dm,
-                                            int active, double scale, double& sy, double* sp) {
-    constexpr bool TWO = (MODE != M_RHS);   // RHS: the coefficient field is the input itself
-    const int b = unit % P.nb;
-    const int rb = unit / P.nb;
-    const int n1 = P.n1;
-    const int j0 = b * 64 + 2 * lane;
-    const bool valid = j0 < n1;
-    const int last = min(31, ((n1 - b * 64) >> 1) - 1);
-    const int i0 = rb * kRT;
-    const int nout = min(kRT, P.n_loc - i0);
-    const Stencil& S = P.st;
-    const RowSrc us{P.u, nullptr, (long long)n1, P.n_loc, 0};
-    auto LD2 = [&](const double* q) { return RO ? ldg2(q) : ld2(q); };
-    auto LD1 = [&](const double* q) { return RO ? __ldg(q) : *q; };
-
-    double2 w[kRT + 3], uw[kRT + 3];
-#pragma unroll
-    for (int t = 0; t < kRT + 3; t++) {
-        w[t] = uw[t] = make_double2(0.0, 0.0);
-        if (valid && t < nout + 3) {
-            w[t] = LD2(rowp(src, i0 - 1 + t) + j0);
-            if (TWO) uw[t] = ldg2(rowp(us, i0 - 1 + t) + j0);
-        }
-    }
-    double hl[kRT], uhl[kRT];
-    double2 hr[kRT], uhr[kRT];
-#pragma unroll
-    for (int t = 0; t < kRT; t++) {
-        hl[t] = uhl[t] = 0.0;
-        hr[t] = uhr[t] = make_double2(0.0, 0.0);
-        if (t < nout) {
-            const double* rp = rowp(src, i0 + t);
-            const double* rq = rowp(us, i0 + t);
-            const int jl = (j0 == 0) ? n1 - 1 : j0 - 1;
-            int jr = j0 + 2;
-            if (jr >= n1) jr -= n1;
-            if (lane == 0) {
-                hl[t] = LD1(rp + jl);
-                if (TWO) uhl[t] = __ldg(rq + jl);
-            }
-            if (lane == last) {
-                hr[t] = LD2(rp + jr);
-                if (TWO) uhr[t] = ldg2(rq + jr);
-            }
-        }
-    }
-    constexpr int KK = K > 0 ? K : 1;
-    double2 pv[kRT][KK];
-#pragma unroll
-    for (int t = 0; t < kRT; t++) {
-        const long long off = (long long)(i0 + t) * n1 + j0;
-        if (MODE == M_LEJA && !FIRST) {
-#pragma unroll
-            for (int k = 0; k < KK; k++) {
-                pv[t][k] = make_double2(0.0, 0.0);
-                if (valid && t < nout && ((active >> k) & 1)) pv[t][k] = ld2(P.p[k] + off);
-            }
-        }
-    }
-    const double nu = S.nu, bt = S.flux;
-#pragma unroll
-    for (int t = 0; t < kRT; t++) {
-        if (t < nout) {
-            const double2 yc = w[t + 1], up = w[t], dn1 = w[t + 2], dn2 = w[t + 3];
-            const double2 uc = TWO ? uw[t + 1] : yc, uu = TWO ? uw[t] : up;
-            const double2 ud1 = TWO ? uw[t + 2] : dn1, ud2 = TWO ? uw[t + 3] : dn2;
-            double yl = __shfl_up_sync(FULL_MASK, yc.y, 1);
-            double yr1 = __shfl_down_sync(FULL_MASK, yc.x, 1);
-            double yr2 = __shfl_down_sync(FULL_MASK, yc.y, 1);
-            double ul = __shfl_up_sync(FULL_MASK, uc.y, 1);
-            double ur1 = __shfl_down_sync(FULL_MASK, uc.x, 1);
-            double ur2 = __shfl_down_sync(FULL_MASK, uc.y, 1);
-            if (lane == 0) {
-                yl = hl[t];
-                ul = TWO ? uhl[t] : hl[t];
-            }
-            if (lane == last) {
-                yr1 = hr[t].x;
-                yr2 = hr[t].y;
-                ur1 = TWO ? uhr[t].x : hr[t].x;
-                ur2 = TWO ? uhr[t].y : hr[t].y;
-            }
-            // pointwise flux field w(y, u) at the stencil points
-            auto wf = [&](double yv, double uv) -> double {
-                if (MODE == M_RHS) return (nu + 0.5 * bt * uv) * uv;
-                if (MODE == M_REM) return 0.5 * bt * yv * yv - bt * uv * yv;
-                return (nu + bt * uv) * yv;
-            };
-            auto wu = [&](double uv) -> double { return -0.5 * bt * uv * uv; };   // M_REM: F(u) field
-            // value at point x=(i,j0) and y=(i,j0+1)
-            double res[2];
-#pragma unroll
-            for (int h = 0; h < 2; h++) {
-                const double y0 = h ? yc.y : yc.x, u0 = h ? uc.y : uc.x;
-                const double ymr = h ? up.y : up.x, ypr = h ? dn1.y : dn1.x, yp2r = h ? dn2.y : dn2.x;
-                const double umr = h ? uu.y : uu.x, upr = h ? ud1.y : ud1.x, up2r = h ? ud2.y : ud2.x;
-                const double ymc = h ? yc.x : yl, ypc = h ? yr1 : yc.y, yp2c = h ? yr2 : yr1;
-                const double umc = h ? uc.x : ul, upc = h ? ur1 : uc.y, up2c = h ? ur2 : ur1;
-                double adv = (S.a0[0] + S.a0[1]) * wf(y0, u0);
-                adv = fma(S.am1[0], wf(ymr, umr), adv);
-                adv = fma(S.ap1[0], wf(ypr, upr), adv);
-                adv = fma(S.ap2[0], wf(yp2r, up2r), adv);
-                adv = fma(S.am1[1], wf(ymc, umc), adv);
-                adv = fma(S.ap1[1], wf(ypc, upc), adv);
-                adv = fma(S.ap2[1], wf(yp2c, up2c), adv);
-                if (MODE == M_REM) {
-                    double advu = (S.a0[0] + S.a0[1]) * wu(u0);
-                    advu = fma(S.am1[0], wu(umr), advu);
-                    advu = fma(S.ap1[0], wu(upr), advu);
-                    advu = fma(S.ap2[0], wu(up2r), advu);
-                    advu = fma(S.am1[1], wu(umc), advu);
-                    advu = fma(S.ap1[1], wu(upc), advu);
-                    advu = fma(S.ap2[1], wu(up2c), advu);
-                    const double Fx = adv + nl_rem(S.react, y0, u0);
-                    const double Fu = advu + nl_rem(S.react, u0, u0);
-                    res[h] = scale * (beta * Fx + (-beta) * Fu);   // a2 * (dt F(x) - dt F(u))
-                } else {
-                    double lap = S.dd0 * y0;
-                    lap = fma(S.dm1[0], ymr, lap);
-                    lap = fma(S.dp1[0], ypr, lap);
-                    lap = fma(S.dm1[1], ymc, lap);
-                    lap = fma(S.dp1[1], ypc, lap);
-                    double a = lap + adv;
-                    if (MODE == M_RHS) {
-                        a = fma(S.react, y0 - y0 * y0 * y0, a);
-                    } else if (S.react != 0.0) {
-                        a = fma(fma(S.qb, u0 * u0, S.qa), y0, a);
-                    }
-                    res[h] = a;
-                }
-            }
-            double2 yn;
-            if (MODE == M_POWER) {
-                yn.x = scale * res[0];
-                yn.y = scale * res[1];
-            } else if (MODE == M_RHS) {
-                double fx = res[0], fy = res[1];
-                if (P.source && valid) {
-                    const double2 sv = ldg2(P.source + (long long)(i0 + t) * n1 + j0);
-                    fx += sv.x;
-                    fy += sv.y;
-                }
-                yn.x = scale * fx;
-                yn.y = scale * fy;
-            } else if (MODE == M_REM) {
-                yn.x = res[0];
-                yn.y = res[1];
-            } else {
-                yn.x = fma(scale, res[0], beta * yc.x);
-                yn.y = fma(scale, res[1], beta * yc.y);
-            }
-            if (valid) {
-                const long long off = (long long)(i0 + t) * n1 + j0;
-                st2(dst + off, yn);
-                sy = fma(yn.x, yn.x, sy);
-                sy = fma(yn.y, yn.y, sy);
-                if (MODE == M_LEJA) {
-#pragma unroll
-                    for (int k = 0; k < KK; k++) {
-                        if ((active >> k) & 1) {
-                            double2 pn;
-                            if (FIRST) {
-                                pn.x = fma(dm[k], yn.x, d0[k] * yc.x);
-                                pn.y = fma(dm[k], yn.y, d0[k] * yc.y);
-                            } else {
-                                pn.x = fma(dm[k], yn.x, pv[t][k].x);
-                                pn.y = fma(dm[k], yn.y, pv[t][k].y);
-                            }
-                            st2(P.p[k] + off, pn);
-                            sp[k] = fma(pn.x, pn.x, sp[k]);
-                            sp[k] = fma(pn.y, pn.y, sp[k]);
-                        }
-                    }
-                }
-            }
-        }
-    }
-}
-
-template <int NDIM, int K, bool DIAG, bool FIRST, int MODE, bool RO>
-__device__ __forceinline__ void tile(const LejaParams& P, const RowSrc& src, double* __restrict__ dst, int unit,
-                                     int lane, double beta, const double* d0, const double* dm, int active,
-                                     double scale, double& sy, double* sp) {
-    if (NDIM == 4)   // flux form (Burgers), 2D
-        tile2d_flux<K, FIRST, MODE, RO>(P, src, dst, unit, lane, beta, d0, dm, active, scale, sy, sp);
-    else if (NDIM == 2)
-        tile2d<K, DIAG, FIRST, MODE, RO>(P, src, dst, unit, lane, beta, d0, dm, active, scale, sy, sp);
-    else
-        tile3d<K, DIAG, FIRST, MODE, RO>(P, src, dst, unit, lane, beta, d0, dm, active, scale, sy, sp);
-}
-
-// ---------------------------------------------------------------------------
-// Stopping decision of P:155 for iteration m (shared by the persistent and the
-// step kernels).  sums = {S_y, S_p^(0..K-1)} over the whole (global) grid.
-// rec != nullptr: the single writer updates margins / per-accumulator iters.
-// ---------------------------------------------------------------------------
-template <int K>
-__device__ __forceinline__ void leja_decide(const LejaParams& P, int m, const double* sums, const double* dm,
-                                            int& act, int& done, int& status, Record* rec) {
-    const double N = P.N_glob;
-    const double ny = sqrt(sums[0] / N);
-    int nact = 0;
-    done = 0;
-    status = 0;
-    for (int k = 0; k < K; k++) {
-        if (!((act >> k) & 1)) continue;
-        const double err = fabs(dm[k]) * ny;
-        const double thr = P.rtol * sqrt(sums[1 + k] / N) + P.atol;
-        if (!isfinite(err) || !isfinite(thr)) {
-            status = 6;  // LX_ERR_NONFINITE
-            break;
-        }
-        if (err <= thr) {
-            act &= ~(1 << k);
-            if (rec) {
-                rec->iters_k[k] = m;
-                const double r = err > 0.0 ? thr / err : INFINITY;
-                if (r < rec->margin_accept) rec->margin_accept = r;
-            }
-        } else {
-            nact++;
-            if (rec) {
-                const double r = err / thr;
-                if (r < rec->margin_reject) rec->margin_reject = r;
-            }
-        }
-    }
-    if (status) done = 1;
-    else if (nact == 0) done = 1;
-    else if (m >= P.max_nodes - 1) { done = 1; status = 5; }  // LX_ERR_NOCONV
-    if (done && rec) {
-        rec->iters += m;
-        rec->ncalls += 1;
-        if (rec->status == 0) rec->status = status;
-    }
-}
-
-// Power iteration: estimate ||w_m|| / ||v_{m-1}|| and the scale of v_m = w_m/||w_m||.
-__device__ __forceinline__ void power_decide(const LejaParams& P, int m, double sumsq, int& done, int& status,
-                                             double* est_out, double* scale_out, Record* rec) {
-    const double N = P.N_glob;
-    const double nw = sqrt(sumsq / N);
-    const double nv = (m == 1) ? sqrt((N + 3.0) / N) : 1.0;
-    const double est = nw / nv;
-    *est_out = est;
-    *scale_out = 1.0 / nw;
-    done = 0;
-    status = 0;
-    if (!isfinite(nw) || nw == 0.0) { done = 1; status = 6; }
-    if (m >= P.power_iters) done = 1;
-    if (done && rec) {
-        rec->est = est;
-        rec->iters += m;
-        rec->ncalls += 1;
-        if (rec->status == 0) rec->status = status;
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Grid barrier with the convergence decision taken by the last arriver.
-// Returns (in smem) done / active for the next iteration.
-// ---------------------------------------------------------------------------
-template <int K, int MODE>
-__device__ __forceinline__ void barrier_decide(const LejaParams& P, int m, unsigned gen0, const double* dm,
-                                               int active, double (*s_red)[kSlot], int* s_flags) {
-    // Grid barrier + device-side decision.  Arrival = one acq_rel atomic per CTA
-    // (releases this CTA's y/p stores and its partial slot, ordered before it by
-    // bar.sync); the last arriver sums the slots in fixed order, decides, and
-    // publishes {generation, status, done, active} in ONE st.release of a 64-bit
-    // word, which the waiters acquire (no further fences or control reads).
-    constexpr int NV = (MODE == M_LEJA) ? 1 + K : 1;
-    const int tid = threadIdx.x;
-    Ctrl* ctrl = P.ctrl;
-    const int par = m & 1;
-    __syncthreads();
-    if (tid == 0) {
-        const unsigned t = atom_add_acq_rel(&ctrl->arrive, 1u);
-        s_flags[0] = (t == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (s_flags[0]) {
-        double acc[NV];
-#pragma unroll
-        for (int i = 0; i < NV; i++) acc[i] = 0.0;
-        for (int c = tid; c < (int)gridDim.x; c += kThreads) {
-            const double* slot = P.partials + ((size_t)par * gridDim.x + c) * kSlot;
-#pragma unroll
-            for (int i = 0; i < NV; i++) acc[i] += __ldcg(slot + i);
-        }
-        block_reduce<NV>(acc, s_red);
-        if (tid == 0) {
-            Record* rec = P.rec;
-            int done = 0, status = 0, act = active;
-            double scale = 0.0;
-            if (MODE == M_LEJA) {
-                leja_decide<K>(P, m, acc, dm, act, done, status, rec);
-            } else {
-                power_decide(P, m, acc[0], done, status, &ctrl->est, &scale, rec);
-                ctrl->scale = scale;
-            }
-            ctrl->arrive = 0u;
-            const unsigned long long w = ((unsigned long long)(gen0 + (unsigned)m) << 32) |
-                                         ((unsigned long long)(status & 0xffff) << 16) |
-                                         ((unsigned long long)(done & 0xff) << 8) | (unsigned long long)(act & 0xff);
-            st_release64(&ctrl->word, w);
-            s_flags[1] = done;
-            s_flags[2] = act;
-            s_red[0][kSlot - 1] = scale;
-        }
-    } else if (tid == 0) {
-        unsigned long long w = ld_relaxed64(&ctrl->word);
-        int spins = 0;
-        while ((int)((unsigned)(w >> 32) - gen0) < m) {
-            if (++spins > 32) __nanosleep(32);
-            if (spins > P.timeout_spins) {
-                atomicExch(&P.rec->status, 10);  // LX_ERR_TIMEOUT
-                w = (1ull << 8);
-                break;
-            }
-            w = ld_relaxed64(&ctrl->word);
-        }
-        fence_acquire();
-        s_flags[1] = (int)((w >> 8) & 0xff);
-        s_flags[2] = (int)(w & 0xff);
-        if (MODE == M_POWER) s_red[0][kSlot - 1] = *(volatile double*)&ctrl->scale;
-    }
-    __syncthreads();
-}
-
-template <int NDIM, int K, bool DIAG>
-__global__ void __launch_bounds__(kThreads, (NDIM == 4 ? 1 : 2)) k_leja2d(const __grid_constant__ LejaParams P) {
-    __shared__ double s_red[kWarps][kSlot];
-    __shared__ int s_flags[4];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // warp 0 of CTA 0 computes the Newton coefficients two iterations ahead; all
-    // other warps share the stencil units
-    const bool cwarp = (blockIdx.x == 0 && warp == 0);
-    const int gw = blockIdx.x * kWarps + warp - 1;
-    const int W = gridDim.x * kWarps - 1;
-    unsigned gen0 = 0;
-    if (tid == 0) gen0 = (unsigned)(ld_acquire64(&P.ctrl->word) >> 32);
-    int active = P.active0;
-    const int M = P.max_nodes;
-    const double alpha = P_alpha(P);
-    double d0[K], d1[K], d2[K];
-#pragma unroll
-    for (int k = 0; k < K; k++) coef_first3(P, k, d0[k], d1[k], d2[k]);
-    if (cwarp && P.coef_gen) {
-        coef_write_row<K>(P, 0, lane, active, d0);
-        coef_write_row<K>(P, 1, lane, active, d1);
-        coef_write_row<K>(P, 2, lane, active, d2);
-    }
-    double beta_n = coef_beta(P, 1), dm_n[K];
-#pragma unroll
-    for (int k = 0; k < K; k++) dm_n[k] = d1[k];
-    for (int m = 1; m < M; m++) {
-        const double beta = beta_n;
-        double dm[K], sp[K];
-#pragma unroll
-        for (int k = 0; k < K; k++) {
-            dm[k] = dm_n[k];
-            sp[k] = 0.0;
-        }
-        double sy = 0.0;
-        const int par = m & 1;
-        double* dst = P.ydst[par];
-        if (cwarp) {
-            if (P.coef_gen && m + 2 < M) coef_write_row<K>(P, m + 2, lane, active, nullptr);
-        } else if (m == 1) {
-            for (int unit = gw; unit < P.nunits; unit += W)
-                tile<NDIM, K, DIAG, true, M_LEJA, true>(P, P.v, dst, unit, lane, beta, d0, dm, active, alpha, sy, sp);
-        } else {
-            const RowSrc src = P.ysrc[par ^ 1];
-            for (int unit = gw; unit < P.nunits; unit += W)
-                tile<NDIM, K, DIAG, false, M_LEJA, false>(P, src, dst, unit, lane, beta, d0, dm, active, alpha, sy, sp);
-        }
-        double vals[1 + K];
-        vals[0] = sy;
-#pragma unroll
-        for (int k = 0; k < K; k++) vals[1 + k] = sp[k];
-        // coefficients of iteration m+1, fetched before the barrier: row m+1 was written during
-        // iteration m-1 and released by barrier m-1
-        if (m + 1 < M) {
-            beta_n = coef_beta(P, m + 1);
-#pragma unroll
-            for (int k = 0; k < K; k++) dm_n[k] = (m + 1 == 2) ? d2[k] : P.table[(size_t)(m + 1) * (1 + K) + 1 + k];
-        }
-        block_reduce<1 + K>(vals, s_red);
-        if (tid == 0) {
-            double* slot = P.partials + ((size_t)par * gridDim.x + blockIdx.x) * kSlot;
-#pragma unroll
-            for (int i = 0; i < 1 + K; i++) slot[i] = vals[i];
-        }
-        barrier_decide<K, M_LEJA>(P, m, gen0, dm, active, s_red, s_flags);
-        active = s_flags[2];
-        if (s_flags[1]) break;
-    }
-}
-
-template <int NDIM, bool DIAG>
-__global__ void __launch_bounds__(kThreads, (NDIM == 4 ? 1 : 2)) k_power2d(const __grid_constant__ LejaParams P) {
-    __shared__ double s_red[kWarps][kSlot];
-    __shared__ int s_flags[4];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    unsigned gen0 = 0;
-    if (tid == 0) gen0 = (unsigned)(ld_acquire64(&P.ctrl->word) >> 32);
-    double scale = 1.0;
-    for (int m = 1; m <= P.power_iters; m++) {
-        double sy = 0.0, sp[1] = {0.0};
-        const int par = m & 1;
-        double* dst = P.ydst[par];
-        const RowSrc src = (m == 1) ? P.v : P.ysrc[par ^ 1];
-        for (int unit = blockIdx.x * kWarps + warp; unit < P.nunits; unit += gridDim.x * kWarps)
-            tile<NDIM, 0, DIAG, false, M_POWER, false>(P, src, dst, unit, lane, 0.0, nullptr, nullptr, 0, scale, sy, sp);
-        double vals[1] = {sy};
-        block_reduce<1>(vals, s_red);
-        if (tid == 0) P.partials[((size_t)par * gridDim.x + blockIdx.x) * kSlot] = vals[0];
-        barrier_decide<0, M_POWER>(P, m, gen0, nullptr, 0, s_red, s_flags);
-        scale = s_red[0][kSlot - 1];
-        if (s_flags[1]) break;
-    }
-}
-
-
-// ---------------------------------------------------------------------------
-// Step mode (multi-rank slab decomposition): one launch per iteration m.
-// Prologue: decision of iteration m-1 from the per-rank partials gathered by
-// the transport (summed in rank order -> identical decision on every rank);
-// body: tiles of iteration m; epilogue: CTA partials -> rank partial (fixed
-// order, last-block ticket).  Speculative launches after convergence exit at
-// entry (ctrl->done), so the host may enqueue iterations in chunks.
-// ---------------------------------------------------------------------------
-template <int NV>
-__device__ __forceinline__ void rank_reduce(const LejaParams& P, double (&vals)[NV], double (*s_red)[kSlot],
-                                            int* s_last) {
-    block_reduce<NV>(vals, s_red);
-    if (threadIdx.x == 0) {
-        double* slot = P.partials + (size_t)blockIdx.x * kSlot;
-#pragma unroll
-        for (int i = 0; i < NV; i++) slot[i] = vals[i];
-        __threadfence();
-        const unsigned t = atomicAdd(&P.ctrl->ticket, 1u);
-        *s_last = (t == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (*s_last) {
-        __threadfence();
-        double acc[NV];
-#pragma unroll
-        for (int i = 0; i < NV; i++) acc[i] = 0.0;
-        for (int c = threadIdx.x; c < (int)gridDim.x; c += kThreads) {
-#pragma unroll
-            for (int i = 0; i < NV; i++) acc[i] += __ldcg(P.partials + (size_t)c * kSlot + i);
-        }
-        block_reduce<NV>(acc, s_red);
-        if (threadIdx.x == 0) {
-#pragma unroll
-            for (int i = 0; i < NV; i++) P.rank_part[i] = acc[i];
-            P.ctrl->ticket = 0u;
-        }
-    }
-}
-
-template <int NDIM, int K, bool DIAG>
-__global__ void __launch_bounds__(kThreads, 2) k_leja2d_step(const __grid_constant__ LejaParams P, int m) {
-    __shared__ double s_red[kWarps][kSlot];
-    __shared__ int s_last;
-    Ctrl* ctrl = P.ctrl;
-    if (*(volatile int*)&ctrl->done) return;
-    const bool writer = blockIdx.x == 0 && threadIdx.x == 0;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const bool cwarp = (blockIdx.x == 0 && warp == 0);   // coefficient warp: row m+2 of the table
-    const int M = P.max_nodes;
-    int active = P.active0;
-    if (m >= 2) {
-        const int prev = *(volatile int*)&ctrl->hist[m & 1];   // mask after iteration m-2
-        double sums[1 + K];
-#pragma unroll
-        for (int i = 0; i < 1 + K; i++) {
-            double s = 0.0;
-            for (int r = 0; r < P.nranks; r++) s += P.gathered[r * kSlot + i];
-            sums[i] = s;
-        }
-        double dmp[K];   // d_{m-1}: row written by launch 1 (m-1 <= 2) or launch m-3
-#pragma unroll
-        for (int k = 0; k < K; k++) dmp[k] = P.table[(size_t)(m - 1) * (1 + K) + 1 + k];
-        int act = prev, done = 0, status = 0;
-        leja_decide<K>(P, m - 1, sums, dmp, act, done, status, writer ? P.rec : nullptr);
-        if (writer) {
-            ctrl->hist[(m - 1) & 1] = act;
-            if (done) {
-                ctrl->status = status;
-                ctrl->m = m - 1;
-                ctrl->done = 1;
-            }
-        }
-        if (done) return;
-        active = act;
-    }
-    if (m >= M) return;   // decision-only launch
-    double d0[K], dm[K], sp[K];
-    if (m <= 2 || cwarp) {
-        double e0[K], e1[K], e2[K];
-#pragma unroll
-        for (int k = 0; k < K; k++) coef_first3(P, k, e0[k], e1[k], e2[k]);
-        if (cwarp && m == 1 && P.coef_gen) {
-            coef_write_row<K>(P, 0, lane, active, e0);
-            coef_write_row<K>(P, 1, lane, active, e1);
-            coef_write_row<K>(P, 2, lane, active, e2);
-        }
-#pragma unroll
-        for (int k = 0; k < K; k++) {
-            d0[k] = e0[k];
-            dm[k] = (m == 1) ? e1[k] : e2[k];
-        }
-    }
-    if (m >= 3) {
-#pragma unroll
-        for (int k = 0; k < K; k++) {
-            d0[k] = P.table[1 + k];
-            dm[k] = P.table[(size_t)m * (1 + K) + 1 + k];   // written by launch m-2
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < K; k++) sp[k] = 0.0;
-    const double beta = coef_beta(P, m);
-    const double alpha = P_alpha(P);
-    double sy = 0.0;
-    double* dst = P.ydst[m & 1];
-    if (cwarp) {
-        if (P.coef_gen && m + 2 < M) coef_write_row<K>(P, m + 2, lane, active, nullptr);
-    } else {
-        const int gw = blockIdx.x * kWarps + warp - 1;
-        const int W = gridDim.x * kWarps - 1;
-        if (m == 1) {
-            for (int unit = gw; unit < P.nunits; unit += W)
-                tile<NDIM, K, DIAG, true, M_LEJA, true>(P, P.v, dst, unit, lane, beta, d0, dm, active, alpha, sy, sp);
-        } else {
-            const RowSrc src = P.ysrc[(m - 1) & 1];
-            for (int unit = gw; unit < P.nunits; unit += W)
-                tile<NDIM, K, DIAG, false, M_LEJA, false>(P, src, dst, unit, lane, beta, d0, dm, active, alpha, sy, sp);
-        }
-    }
-    double vals[1 + K];
-    vals[0] = sy;
-#pragma unroll
-    for (int k = 0; k < K; k++) vals[1 + k] = sp[k];
-    rank_reduce<1 + K>(P, vals, s_red, &s_last);
-}
-
-template <int NDIM, bool DIAG>
-__global__ void __launch_bounds__(kThreads, 2) k_power2d_step(const __grid_constant__ LejaParams P, int m) {
-    __shared__ double s_red[kWarps][kSlot];
-    __shared__ int s_last;
-    Ctrl* ctrl = P.ctrl;
-    if (*(volatile int*)&ctrl->done) return;
-    const bool writer = blockIdx.x == 0 && threadIdx.x == 0;
-    double scale = 1.0;
-    if (m >= 2) {
-        double s = 0.0;
-        for (int r = 0; r < P.nranks; r++) s += P.gathered[r * kSlot];
-        int done = 0, status = 0;
-        double est;
-        power_decide(P, m - 1, s, done, status, &est, &scale, writer ? P.rec : nullptr);
-        if (done) {
-            if (writer) {
-                ctrl->status = status;
-                ctrl->done = 1;
-            }
-            return;
-        }
-    }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double sy = 0.0, sp[1] = {0.0};
-    const RowSrc src = (m == 1) ? P.v : P.ysrc[(m - 1) & 1];
-    double* dst = P.ydst[m & 1];
-    for (int unit = blockIdx.x * kWarps + warp; unit < P.nunits; unit += gridDim.x * kWarps)
-        tile<NDIM, 0, DIAG, false, M_POWER, false>(P, src, dst, unit, lane, 0.0, nullptr, nullptr, 0, scale, sy, sp);
-    double vals[1] = {sy};
-    rank_reduce<1>(P, vals, s_red, &s_last);
-}
-
-__global__ void k_finalize_err(const double* gathered, int nranks, double N, Record* rec) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        double s = 0.0;
-        for (int r = 0; r < nranks; r++) s += gathered[r * kSlot];
-        rec->err = sqrt(s / N);
-    }
-}
-
-__global__ void k_max_u64(const unsigned long long* vals, int n, unsigned long long* out) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        unsigned long long m = 0ull;
-        for (int i = 0; i < n; i++) m = vals[i] > m ? vals[i] : m;
-        *out = m;
-    }
-}
-
-
-// ---------------------------------------------------------------------------
-// TMA-pipelined marching variant of the 2D Leja iteration (k_leja2d_tma).
-//
-// Each warp owns a contiguous run of rows of one 64-column band ("segment";
-// the band-rows of the grid are split evenly over all warps) and marches down
-// it.  Row data arrive in a per-warp shared-memory ring through bulk async
-// copies (cp.async.bulk, TMA engine) completing on one mbarrier per ring slot:
-// entry e = {y row r+2 (+16-byte halos on both sides), p row r, u row r}.
-// The stencil for row r reads y rows r-1..r+2 from the last 4 entries, so every
-// y row crosses HBM once per iteration (+3 preamble rows per segment) with no
-// register-held tiles; D = RS-4 entries are in flight ahead of the consumer.
-// Same arithmetic order, reductions and device-side decision as k_leja2d.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t ok = 0;
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-    } while (!ok);
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-template <int K, bool DIAG>
-struct TmaCfg {
-    static constexpr int RS = (K <= 1) ? 8 : 6;             // ring slots per warp
-    static constexpr int D = RS - 4;                        // entries in flight ahead of the consumer
-    static constexpr int YS = 68;                           // y slot: [j0-2, j0+64) + right halo
-    static constexpr int ES = YS + 64 * K + (DIAG ? 64 : 0);  // doubles per entry
-    static constexpr int WARP_BYTES = RS * (ES * 8 + 8);
-    static constexpr int SMEM = kWarps * WARP_BYTES;
-};
-
-// Warp work list: band-rows [t0, t1) in band-major order (t -> band t / n, row t % n).
-struct SegIter {
-    long long t0, t1;
-    int n_loc;
-};
-
-template <int K, bool DIAG>
-__global__ void __launch_bounds__(kThreads, (K <= 1 ? 3 : 2)) k_leja2d_tma(const __grid_constant__ LejaParams P) {
-    using C = TmaCfg<K, DIAG>;
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ double s_red[kWarps][kSlot];
-    __shared__ int s_flags[4];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    unsigned char* wbase = smem + warp * C::WARP_BYTES;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(wbase);
-    double* ring = reinterpret_cast<double*>(wbase + C::RS * 8);
-    if (lane == 0)
-        for (int i = 0; i < C::RS; i++) mbar_init(&bars[i], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncthreads();
-
-    const int n1 = P.n1, n_loc = P.n_loc;
-    const long long T = (long long)P.nb * n_loc;
-    const long long W = (long long)gridDim.x * kWarps;
-    const long long gw = (long long)blockIdx.x * kWarps + warp;
-    const long long t0 = T * gw / W, t1 = T * (gw + 1) / W;
-    // entries of this warp per iteration: rows + 3 preamble entries per segment
-    int nseg = 0;
-    for (long long t = t0; t < t1;) {
-        const long long len = min(t1 - t, (long long)(n_loc - (int)(t % n_loc)));
-        nseg++;
-        t += len;
-    }
-    const int NE = (int)(t1 - t0) + 3 * nseg;
-
-    unsigned gen0 = 0;
-    if (tid == 0) gen0 = (unsigned)(ld_acquire64(&P.ctrl->word) >> 32);
-    int active = P.active0;
-    double d0[K];
-#pragma unroll
-    for (int k = 0; k < K; k++) d0[k] = P.coef[1 + k];
-    unsigned long long qbase = 0;
-    const Stencil& S = P.st;
-
-    for (int m = 1; m < P.max_nodes; m++) {
-        const double* cm = P.coef + (size_t)m * (1 + K);
-        const double beta = cm[0];
-        double dm[K], sp[K];
-#pragma unroll
-        for (int k = 0; k < K; k++) {
-            dm[k] = cm[1 + k];
-            sp[k] = 0.0;
-        }
-        double sy = 0.0;
-        const int par = m & 1;
-        const bool first = (m == 1);
-        const RowSrc src = first ? P.v : P.ysrc[par ^ 1];
-        double* dst = P.ydst[par];
-        // producer cursor over (segment, position) in entry order
-        long long pt = t0;     // band-row of the producer's current segment start
-        int ppos = 0;          // position within segment (0..2 preamble, then rows)
-        long long ct = t0;     // consumer's current segment start
-        int cpos = 0;
-        int e_p = 0;
-        for (int e = 0; e < NE; e++) {
-            // ---- producer: keep D entries in flight
-            while (e_p < NE && e_p <= e + C::D) {
-                const int b = (int)(pt / n_loc);
-                const int i0 = (int)(pt % n_loc);
-                const int len = (int)min(t1 - pt, (long long)(n_loc - i0));
-                if (lane == 0) {
-                    const unsigned long long q = qbase + e_p;
-                    const int slot = (int)(q % C::RS);
-                    double* ent = ring + slot * C::ES;
-                    uint64_t* bar = &bars[slot];
-                    const int j0 = b * 64;
-                    const int vc = min(64, n1 - j0);
-                    const int jl = (j0 == 0) ? n1 - 2 : j0 - 2;
-                    const int jr = (j0 + vc >= n1) ? 0 : j0 + vc;
-                    const int yrow = (ppos < 3) ? i0 - 1 + ppos : i0 + (ppos - 3) + 2;
-                    const double* rp = rowp(src, yrow);
-                    uint32_t bytes = (uint32_t)(vc * 8 + 32);
-                    const bool full = ppos >= 3;
-                    const int prow = i0 + (ppos - 3);
-                    int nact = 0;
-                    if (full && !first) {
-#pragma unroll
-                        for (int k = 0; k < K; k++) nact += (active >> k) & 1;
-                    }
-                    if (full) bytes += (uint32_t)(vc * 8) * (uint32_t)(nact + (DIAG ? 1 : 0));
-                    fence_proxy_async();
-                    mbar_expect_tx(bar, bytes);
-                    bulk_g2s(ent, rp + jl, 16, bar);
-                    bulk_g2s(ent + 2, rp + j0, vc * 8, bar);
-                    bulk_g2s(ent + 2 + vc, rp + jr, 16, bar);
-                    if (full) {
-                        const long long off = (long long)prow * n1 + j0;
-                        if (!first) {
-#pragma unroll
-                            for (int k = 0; k < K; k++)
-                                if ((active >> k) & 1) bulk_g2s(ent + C::YS + 64 * k, P.p[k] + off, vc * 8, bar);
-                        }
-                        if (DIAG) bulk_g2s(ent + C::YS + 64 * K, P.u + off, vc * 8, bar);
-                    }
-                }
-                e_p++;
-                if (++ppos == 3 + len) {
-                    pt += len;
-                    ppos = 0;
-                }
-            }
-            // ---- consumer
-            const unsigned long long q = qbase + e;
-            mbar_wait(&bars[q % C::RS], (uint32_t)((q / C::RS) & 1));
-            const int b = (int)(ct / n_loc);
-            const int i0 = (int)(ct % n_loc);
-            const int len = (int)min(t1 - ct, (long long)(n_loc - i0));
-            if (cpos >= 3) {
-                const int r = i0 + (cpos - 3);
-                const double* Ed2 = ring + (int)(q % C::RS) * C::ES;
-                const double* Ed1 = ring + (int)((q + C::RS - 1) % C::RS) * C::ES;
-                const double* Ec = ring + (int)((q + C::RS - 2) % C::RS) * C::ES;
-                const double* Eu = ring + (int)((q + C::RS - 3) % C::RS) * C::ES;
-                const int j0 = b * 64;
-                const int j = j0 + 2 * lane;
-                if (j < n1) {
-                    const double2 yc = *reinterpret_cast<const double2*>(Ec + 2 + 2 * lane);
-                    const double left = Ec[1 + 2 * lane];
-                    const double2 rr = *reinterpret_cast<const double2*>(Ec + 4 + 2 * lane);
-                    const double2 up = *reinterpret_cast<const double2*>(Eu + 2 + 2 * lane);
-                    const double2 dn1 = *reinterpret_cast<const double2*>(Ed1 + 2 + 2 * lane);
-                    const double2 dn2 = *reinterpret_cast<const double2*>(Ed2 + 2 + 2 * lane);
-                    double ax = S.c0 * yc.x;
-                    ax = fma(S.m1[0], up.x, ax);
-                    ax = fma(S.p1[0], dn1.x, ax);
-                    ax = fma(S.p2[0], dn2.x, ax);
-                    ax = fma(S.m1[1], left, ax);
-                    ax = fma(S.p1[1], yc.y, ax);
-                    ax = fma(S.p2[1], rr.x, ax);
-                    double ay = S.c0 * yc.y;
-                    ay = fma(S.m1[0], up.y, ay);
-                    ay = fma(S.p1[0], dn1.y, ay);
-                    ay = fma(S.p2[0], dn2.y, ay);
-                    ay = fma(S.m1[1], yc.x, ay);
-                    ay = fma(S.p1[1], rr.x, ay);
-                    ay = fma(S.p2[1], rr.y, ay);
-                    if (DIAG) {
-                        const double2 uu = *reinterpret_cast<const double2*>(Ed2 + C::YS + 64 * K + 2 * lane);
-                        ax = fma(fma(S.qb, uu.x * uu.x, S.qa), yc.x, ax);
-                        ay = fma(fma(S.qb, uu.y * uu.y, S.qa), yc.y, ay);
-                    }
-                    double2 yn;
-                    yn.x = fma(P.alpha, ax, beta * yc.x);
-                    yn.y = fma(P.alpha, ay, beta * yc.y);
-                    const long long off = (long long)r * n1 + j;
-                    st2(dst + off, yn);
-                    sy = fma(yn.x, yn.x, sy);
-                    sy = fma(yn.y, yn.y, sy);
-#pragma unroll
-                    for (int k = 0; k < K; k++) {
-                        if ((active >> k) & 1) {
-                            double2 pn;
-                            if (first) {
-                                pn.x = fma(dm[k], yn.x, d0[k] * yc.x);
-                                pn.y = fma(dm[k], yn.y, d0[k] * yc.y);
-                            } else {
-                                const double2 pv = *reinterpret_cast<const double2*>(Ed2 + C::YS + 64 * k + 2 * lane);
-                                pn.x = fma(dm[k], yn.x, pv.x);
-                                pn.y = fma(dm[k], yn.y, pv.y);
-                            }
-                            st2(P.p[k] + off, pn);
-                            sp[k] = fma(pn.x, pn.x, sp[k]);
-                            sp[k] = fma(pn.y, pn.y, sp[k]);
-                        }
-                    }
-                }
-            }
-            __syncwarp();
-            if (++cpos == 3 + len) {
-                ct += len;
-                cpos = 0;
-            }
-        }
-        qbase += NE;
-        double vals[1 + K];
-        vals[0] = sy;
-#pragma unroll
-        for (int k = 0; k < K; k++) vals[1 + k] = sp[k];
-        block_reduce<1 + K>(vals, s_red);
-        if (tid == 0) {
-            double* slot = P.partials + ((size_t)par * gridDim.x + blockIdx.x) * kSlot;
-#pragma unroll
-            for (int i = 0; i < 1 + K; i++) slot[i] = vals[i];
-        }
-        barrier_decide<K, M_LEJA>(P, m, gen0, dm, active, s_red, s_flags);
-        active = s_flags[2];
-        if (s_flags[1]) break;
-    }
-}
-
-
-// ===========================================================================
-// Temporal blocking: TWO Leja iterations per HBM pass.
-//   pass (m, m+1): read y_{m-1}, p_{m-1};  y_m is formed in registers on a
-//   widened halo (rows i0-1 .. i0+RT+1, columns j0-2 .. j0+61 of a 64-column
-//   warp window whose 60 inner columns are outputs);  y_{m+1} and p_{m+1} are
-//   written.  -> 32 B/pt per TWO iterations (16 B/pt per iteration) and one grid
-//   barrier per two iterations.  Both iterations' norms are reduced, and the
-//   stopping rule of P:155 is applied to m and then m+1 exactly as in the
-//   one-step kernel (same decisions, same iteration counts).  If an accumulator
-//   converges at the first iteration of a pass, its p_{m+1} is rolled back to
-//   p_m = p_{m+1} - d_{m+1} y_{m+1} (<= 1 ulp from the one-step value) in the
-//   next pass, or in a final pointwise pass when the call ends.
-// ===========================================================================
-// stencil of the constant-coefficient operator at the two columns of a lane (same order as tile2d)
-__device__ __forceinline__ void stencil2(const Stencil& S, const double2 yc, const double2 up, const double2 dn1,
-                                         const double2 dn2, double left, double r1, double r2, double& ax, double& ay) {
-    ax = S.c0 * yc.x;
-    ax = fma(S.m1[0], up.x, ax);
-    ax = fma(S.p1[0], dn1.x, ax);
-    ax = fma(S.p2[0], dn2.x, ax);
-    ax = fma(S.m1[1], left, ax);
-    ax = fma(S.p1[1], yc.y, ax);
-    ax = fma(S.p2[1], r1, ax);
-    ay = S.c0 * yc.y;
-    ay = fma(S.m1[0], up.y, ay);
-    ay = fma(S.p1[0], dn1.y, ay);
-    ay = fma(S.p2[0], dn2.y, ay);
-    ay = fma(S.m1[1], yc.x, ay);
-    ay = fma(S.p1[1], r1, ay);
-    ay = fma(S.p2[1], r2, ay);
-}
-
-// y_m = alpha (A + diag) y_{m-1} + beta y_{m-1} at one row of the lane's two columns.
-// r1/r2 come from the next lane; lane 31 uses its halo pair h (columns c0+62, c0+63).
-template <bool DIAG>
-__device__ __forceinline__ double2 leja_row(const Stencil& S, double alpha, double beta, const double2 up,
-                                            const double2 yc, const double2 dn1, const double2 dn2, const double2 h,
-                                            const double2 uu, int lane) {
-    const double left = __shfl_up_sync(FULL_MASK, yc.y, 1);
-    double r1 = __shfl_down_sync(FULL_MASK, yc.x, 1);
-    double r2 = __shfl_down_sync(FULL_MASK, yc.y, 1);
-    if (lane == 31) {
-        r1 = h.x;
-        r2 = h.y;
-    }
-    double ax, ay;
-    stencil2(S, yc, up, dn1, dn2, left, r1, r2, ax, ay);
-    if (DIAG) {
-        ax = fma(fma(S.qb, uu.x * uu.x, S.qa), yc.x, ax);
-        ay = fma(fma(S.qb, uu.y * uu.y, S.qa), yc.y, ay);
-    }
-    return make_double2(fma(alpha, ax, beta * yc.x), fma(alpha, ay, beta * yc.y));
-}
-
-// xor-butterfly sum of N values over the warp (fixed order: every lane ends with the same bits)
-template <int N>
-__device__ __forceinline__ void warp_sum(double* v) {
-#pragma unroll
-    for (int i = 0; i < N; i++) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) v[i] += __shfl_xor_sync(FULL_MASK, v[i], off);
-    }
-}
-
-// Shared-memory staging of the two-step kernel: per warp a ring of tb2_depth stages, one stage =
-// the global rows one chunk consumes (16 B per lane per row, lane-private: every lane reads back only
-// what its own cp.async wrote -> no warp synchronisation needed):
-//   y_{m-1} rows i0+4 .. i0+RT+3 | halo pair of lane 31 for rows i0+2 .. i0+RT+1 |
-//   p_k rows i0 .. i0+RT-1 (k < K) | u rows i0+2 .. i0+RT+1 (DIAG)
-template <int K, bool DIAG>
-struct Tb2Stage {
-    static constexpr int RT = tb2_rt(K);
-    static constexpr int Y = 0;
-    static constexpr int H = RT * 32;
-    static constexpr int PP = H + RT;
-    static constexpr int U = PP + RT * K * 32;
-    static constexpr int SIZE = U + (DIAG ? RT * 32 : 0);          // double2 per stage
-    static constexpr int DEPTH = tb2_depth(K, DIAG);
-    static constexpr int WARP = SIZE * DEPTH;                        // double2 per warp
-};
-
-__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ double2 lds2(uint32_t addr) {
-    double2 v;
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
-    return v;
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// stage the global rows of chunk ci into ring stage st (every lane: its own 16-byte pieces)
-template <int K, bool DIAG, bool FIRST>
-__device__ __forceinline__ void tb2_issue(const LejaParams& P, const double* __restrict__ src,
-                                          double2* __restrict__ ring, int ci, int st, int lane, int active,
-                                          int rbmask) {
-    using L = Tb2Stage<K, DIAG>;
-    constexpr int RT = L::RT;
-    constexpr int KK = K > 0 ? K : 1;
-    const int n1 = P.n1, n = P.n_loc, nc = P.nrb;
-    auto wrap = [n](int r) { return r < 0 ? r + n : (r >= n ? r - n : r); };
-    auto colw = [n1](int c) { return c < 0 ? c + n1 : (c >= n1 ? c - n1 : c); };
-    const int b = ci / nc;
-    const int i0 = (ci - b * nc) * RT;
-    const int jraw = b * kBand2 - 2 + 2 * lane;
-    const int j = colw(jraw);
-    double2* sg = ring + st * L::SIZE;
-#pragma unroll
-    for (int q = 0; q < RT; q++) {
-        cp_async16(sg + L::Y + q * 32 + lane, src + (size_t)wrap(i0 + 4 + q) * n1 + j);
-        if (lane == 31) cp_async16(sg + L::H + q, src + (size_t)wrap(i0 + 2 + q) * n1 + colw(jraw + 2));
-        if (DIAG) cp_async16(sg + L::U + q * 32 + lane, P.u + (size_t)wrap(i0 + 2 + q) * n1 + j);
-    }
-#pragma unroll
-    for (int t = 0; t < RT; t++) {
-#pragma unroll
-        for (int k = 0; k < KK; k++) {
-            const bool need = ((active >> k) & 1) ? !FIRST : (K > 1 && ((rbmask >> k) & 1));
-            if (need) cp_async16(sg + L::PP + (t * K + k) * 32 + lane, P.p[k] + (size_t)wrap(i0 + t) * n1 + j);
-        }
-    }
-}
-
-// Temporally blocked pass over a contiguous range [cbeg, cend) of (band, chunk) work items in
-// band-major order (chunk = RT rows of a 60-column band).  A warp marches down its rows with
-// register windows: y_{m-1} rows [i0, i0+RT+4), y_m rows [i0-1, i0+RT+2), u rows [i0, i0+RT+2);
-// per chunk it consumes RT new rows of y_{m-1} (and p, u) staged DEPTH-1 chunks ahead by
-// cp.async, forms RT new rows of y_m (the 3-row halo recomputation happens only at a strip start)
-// and writes RT rows of y_{m+1} and p_{m+1}.  Lanes 1..30 own the band's 60 output columns;
-// lanes 0 and 31 carry halo columns.  Requires n_loc >= 16, n1 >= 64 (host-checked).
-template <int K, bool DIAG, bool FIRST, bool TWO>
-__device__ __forceinline__ void strip2d_tb2(const LejaParams& P, const double* __restrict__ src,
-                                            double* __restrict__ dst, int cbeg, int cend, int lane, double alpha,
-                                            double b1, double b2, const double* d0, const double* da,
-                                            const double* db, int active, int rbmask, const double* rbd,
-                                            double (&acc)[2 * (1 + K)], double2* __restrict__ ring) {
-    using L = Tb2Stage<K, DIAG>;
-    constexpr int RT = L::RT, D = L::DEPTH;
-    const int n1 = P.n1, n = P.n_loc, nc = P.nrb;
-    const Stencil& S = P.st;
-    auto wrap = [n](int r) { return r < 0 ? r + n : (r >= n ? r - n : r); };
-    auto colw = [n1](int c) { return c < 0 ? c + n1 : (c >= n1 ? c - n1 : c); };
-    constexpr int KK = K > 0 ? K : 1;
-    double2 aw[RT + 4], yw[RT + 3], uw[RT + 2];
-    const double2 z2 = make_double2(0.0, 0.0);
-    // prime the ring: chunks cbeg .. cbeg+D-2
-#pragma unroll
-    for (int d = 0; d < D - 1; d++) {
-        if (cbeg + d < cend) tb2_issue<K, DIAG, FIRST>(P, src, ring, cbeg + d, d, lane, active, rbmask);
-        cp_async_commit();
-    }
-    int ci = cbeg, st = 0;
-#pragma unroll 1
-    while (ci < cend) {
-        const int b = ci / nc;
-        const int cseg = min(cend, (b + 1) * nc);   // this band's part of the range
-        const int c0 = b * kBand2;
-        const int jraw = c0 - 2 + 2 * lane;
-        const int j = colw(jraw);
-        const int jh = colw(jraw + 2);
-        const bool outl = lane >= 1 && lane <= 30 && jraw < n1 && jraw < c0 + kBand2;
-        {
-            // strip start: y_{m-1} rows i0-2 .. i0+3 (direct loads), y_m rows i0-1 .. i0+1
-            const int i0 = (ci - b * nc) * RT;
-            double2 t6[6], h3[3], u3[3];
-#pragma unroll
-            for (int q = 0; q < 6; q++) t6[q] = ld2(src + (size_t)wrap(i0 - 2 + q) * n1 + j);
-#pragma unroll
-            for (int q = 0; q < 3; q++) {
-                h3[q] = (lane == 31) ? ld2(src + (size_t)wrap(i0 - 1 + q) * n1 + jh) : z2;
-                u3[q] = DIAG ? ldg2(P.u + (size_t)wrap(i0 - 1 + q) * n1 + j) : z2;
-            }
-#pragma unroll
-            for (int q = 0; q < 3; q++)
-                yw[q] = leja_row<DIAG>(S, alpha, b1, t6[q], t6[q + 1], t6[q + 2], t6[q + 3], h3[q], u3[q], lane);
-#pragma unroll
-            for (int q = 0; q < 4; q++) aw[q] = t6[q + 2];
-            uw[0] = u3[1];
-            uw[1] = u3[2];
-        }
-#pragma unroll 1
-        for (int i0 = (ci - b * nc) * RT; ci < cseg; ci++, i0 += RT) {
-            // keep D-1 chunks in flight: stage chunk ci+D-1, then wait for chunk ci's group
-            {
-                int sn = st + D - 1;
-                if (sn >= D) sn -= D;
-                if (ci + D - 1 < cend) tb2_issue<K, DIAG, FIRST>(P, src, ring, ci + D - 1, sn, lane, active, rbmask);
-                cp_async_commit();
-                cp_async_wait<D - 1>();
-            }
-            // shared-space loads (ld.shared, not generic): 32-bit address of this stage
-            const uint32_t sgb = smem_u32(ring) + (uint32_t)(st * L::SIZE) * 16u;
-            auto sg = [sgb](int i) { return lds2(sgb + (uint32_t)i * 16u); };
-            if (++st == D) st = 0;
-            const int nout = min(RT, n - i0);
-            double2 ah[RT];
-#pragma unroll
-            for (int q = 0; q < RT; q++) {
-                aw[4 + q] = sg(L::Y + q * 32 + lane);
-                ah[q] = (lane == 31) ? sg(L::H + q) : z2;
-                if (DIAG) uw[2 + q] = sg(L::U + q * 32 + lane);
-            }
-            // step 1: y_m rows i0+2 .. i0+RT+1
-#pragma unroll
-            for (int q = 0; q < RT; q++)
-                yw[3 + q] = leja_row<DIAG>(S, alpha, b1, aw[1 + q], aw[2 + q], aw[3 + q], aw[4 + q], ah[q],
-                                           DIAG ? uw[2 + q] : z2, lane);
-            // step 2: y_{m+1} on the output rows; p updates and norms
-#pragma unroll
-            for (int t = 0; t < RT; t++) {
-                if (t < nout) {
-                    const double2 yc = yw[t + 1];
-                    double2 zz = yc;
-                    if (TWO) zz = leja_row<DIAG>(S, alpha, b2, yw[t], yc, yw[t + 2], yw[t + 3], z2, uw[t], lane);
-                    if (outl) {
-                        const size_t off = (size_t)(i0 + t) * n1 + j;
-                        st2(dst + off, zz);
-                        acc[0] = fma(yc.y, yc.y, fma(yc.x, yc.x, acc[0]));
-                        if (TWO) acc[1 + K] = fma(zz.y, zz.y, fma(zz.x, zz.x, acc[1 + K]));
-                        const double2 yprev = aw[t];   // y_{m-1} (= v on the first pass)
-#pragma unroll
-                        for (int k = 0; k < KK; k++) {
-                            if ((active >> k) & 1) {
-                                double2 pm;
-                                if (FIRST) {
-                                    pm.x = fma(da[k], yc.x, d0[k] * yprev.x);
-                                    pm.y = fma(da[k], yc.y, d0[k] * yprev.y);
-                                } else {
-                                    const double2 pv = sg(L::PP + (t * K + k) * 32 + lane);
-                                    pm.x = fma(da[k], yc.x, pv.x);
-                                    pm.y = fma(da[k], yc.y, pv.y);
-                                }
-                                acc[1 + k] = fma(pm.y, pm.y, fma(pm.x, pm.x, acc[1 + k]));
-                                double2 pn = pm;
-                                if (TWO) {
-                                    pn.x = fma(db[k], zz.x, pm.x);
-                                    pn.y = fma(db[k], zz.y, pm.y);
-                                    acc[2 + K + k] = fma(pn.y, pn.y, fma(pn.x, pn.x, acc[2 + K + k]));
-                                }
-                                st2(P.p[k] + off, pn);
-                            } else if (K > 1 && ((rbmask >> k) & 1)) {
-                                // roll back the speculative last update of the previous pass (K = 1: the
-                                // call ends at that decision -> final rollback pass instead)
-                                const double2 pv = sg(L::PP + (t * K + k) * 32 + lane);
-                                st2(P.p[k] + off, make_double2(fma(-rbd[k], yprev.x, pv.x),
-                                                               fma(-rbd[k], yprev.y, pv.y)));
-                            }
-                        }
-                    }
-                }
-            }
-            // advance the windows by RT rows
-#pragma unroll
-            for (int q = 0; q < 4; q++) aw[q] = aw[RT + q];
-#pragma unroll
-            for (int q = 0; q < 3; q++) yw[q] = yw[RT + q];
-#pragma unroll
-            for (int q = 0; q < 2; q++) uw[q] = uw[RT + q];
-        }
-    }
-    cp_async_wait<0>();
-}
-
-// the four (first pass, two iterations) instantiations of strip2d_tb2
-template <int K, bool DIAG>
-__device__ __forceinline__ void tb2_strip(const LejaParams& P, bool first, bool two, const double* __restrict__ src,
-                                          double* __restrict__ dst, int c_b, int c_e, int lane, double alpha,
-                                          double b1, double b2, const double* d0, const double* da, const double* db,
-                                          int active, int rbmask, const double* rbd, double (&acc)[2 * (1 + K)],
-                                          double2* __restrict__ ring) {
-    if (first) {
-        if (two) strip2d_tb2<K, DIAG, true, true>(P, src, dst, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active,
-                                                 rbmask, rbd, acc, ring);
-        else strip2d_tb2<K, DIAG, true, false>(P, src, dst, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active,
-                                               rbmask, rbd, acc, ring);
-    } else {
-        if (two) strip2d_tb2<K, DIAG, false, true>(P, src, dst, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active,
-                                                  rbmask, rbd, acc, ring);
-        else strip2d_tb2<K, DIAG, false, false>(P, src, dst, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active,
-                                                rbmask, rbd, acc, ring);
-    }
-}
-
-// Final rollback pass: p_k -= rbd[k] * y (y = the last written y_{m+1}) on the strip's output points.
-template <int K, int RT>
-__device__ __forceinline__ void strip2d_tb2_rollback(const LejaParams& P, const double* y, int cbeg, int cend,
-                                                     int lane, int rbmask, const double* rbd) {
-    const int n1 = P.n1, n = P.n_loc, nc = P.nrb;
-    for (int ci = cbeg; ci < cend; ci++) {
-        const int b = ci / nc, ic = ci - b * nc;
-        const int c0 = b * kBand2;
-        const int jraw = c0 - 2 + 2 * lane;
-        if (!(lane >= 1 && lane <= 30 && jraw < n1 && jraw < c0 + kBand2)) continue;
-        const int i0 = ic * RT;
-        const int nout = min(RT, n - i0);
-        for (int t = 0; t < nout; t++) {
-            const size_t off = (size_t)(i0 + t) * n1 + jraw;
-            const double2 yy = ld2(y + off);
-#pragma unroll
-            for (int k = 0; k < K; k++) {
-                if ((rbmask >> k) & 1) {
-                    const double2 pp = ld2(P.p[k] + off);
-                    st2(P.p[k] + off, make_double2(fma(-rbd[k], yy.x, pp.x), fma(-rbd[k], yy.y, pp.y)));
-                }
-            }
-        }
-    }
-}
-
-// grid barrier + decisions of iterations m (and m+1): flags[1] done, [2] active, [3] rollback mask
-template <int K>
-__device__ __forceinline__ void barrier_decide_tb2(const LejaParams& P, int m, bool two, unsigned gen0, const double* da,
-                                                   const double* db, int active, double (*s_red)[kSlot],
-                                                   int* s_flags) {
-    constexpr int NV = 2 * (1 + K);
-    const int tid = threadIdx.x;
-    Ctrl* ctrl = P.ctrl;
-    const int par = ((m - 1) / 2) & 1;
-    __syncthreads();
-    if (tid == 0) {
-        const unsigned t = atom_add_acq_rel(&ctrl->arrive, 1u);
-        s_flags[0] = (t == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (s_flags[0]) {
-        double acc[NV];
-#pragma unroll
-        for (int i = 0; i < NV; i++) acc[i] = 0.0;
-        if (P.seg > 0) {
-            for (int g = tid; g < P.ngrp; g += kThreads) {
-#pragma unroll
-                for (int i = 0; i < NV; i++) acc[i] += __ldcg(P.grp_part + (size_t)g * NV + i);
-            }
-        } else {
-            for (int c = tid; c < (int)gridDim.x; c += kThreads) {
-                const double* slot = P.partials + ((size_t)par * gridDim.x + c) * kSlot;
-#pragma unroll
-                for (int i = 0; i < NV; i++) acc[i] += __ldcg(slot + i);
-            }
-        }
-        block_reduce<NV>(acc, s_red);
-        if (tid == 0) {
-            int act = active, done = 0, status = 0;
-            leja_decide<K>(P, m, acc, da, act, done, status, P.rec);
-            const int rb = active & ~act;   // converged at the first iteration of the pass -> roll back
-            if (!done && two) leja_decide<K>(P, m + 1, acc + 1 + K, db, act, done, status, P.rec);
-            ctrl->arrive = 0u;
-            const int pass = (m - 1) >> 1;
-            ctrl->work[(pass + 1) & 1] = 0u;     // segment counter of the next pass
-            if (done) ctrl->work[pass & 1] = 0u;  // ... and of this one for the next call
-            const unsigned long long w = ((unsigned long long)(gen0 + (unsigned)m) << 32) |
-                                         ((unsigned long long)(status & 0xff) << 16) |
-                                         ((unsigned long long)(rb & 0xf) << 12) |
-                                         ((unsigned long long)(done & 0xf) << 8) | (unsigned long long)(act & 0xff);
-            st_release64(&ctrl->word, w);
-            s_flags[1] = done;
-            s_flags[2] = act;
-            s_flags[3] = two ? rb : 0;
-        }
-    } else if (tid == 0) {
-        unsigned long long w = ld_relaxed64(&ctrl->word);
-        int spins = 0;
-        while ((int)((unsigned)(w >> 32) - gen0) < m) {
-            if (++spins > 4096) __nanosleep(32);
-            if (spins > P.timeout_spins) {
-                atomicExch(&P.rec->status, 10);
-                w = (1ull << 8);
-                break;
-            }
-            w = ld_relaxed64(&ctrl->word);
-        }
-        fence_acquire();
-        s_flags[1] = (int)((w >> 8) & 0xf);
-        s_flags[2] = (int)(w & 0xff);
-        s_flags[3] = two ? (int)((w >> 12) & 0xf) : 0;
-    }
-    __syncthreads();
-}
-
-template <int K>
-__device__ __forceinline__ void coef_first5(const LejaParams& P, int k, double* d) {
-    // d_0..d_4 of accumulator k by lane 0 of the warp (column form, explicitly rounded), broadcast
-    const int M = P.max_nodes;
-    double e[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    if ((threadIdx.x & 31) == 0) {
-#pragma unroll
-        for (int jj = 0; jj < 5; jj++) {
-            if (jj < M) {
-                double v = coef_h(P, k, jj);
-#pragma unroll
-                for (int i = 0; i < jj; i++) v = dd_step(v, e[i], P.R[(size_t)i * M + jj]);
-                e[jj] = v;
-            }
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < 5; i++) d[i] = __shfl_sync(0xffffffffu, e[i], 0);
-}
-
-__device__ __forceinline__ unsigned long long globaltimer_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-
-template <int K, bool DIAG>
-__global__ void __launch_bounds__(kThreads, 2) k_leja2d_tb2(const __grid_constant__ LejaParams P) {
-    __shared__ double s_red[kWarps][kSlot];
-    extern __shared__ double2 tb2_ring[];
-    __shared__ int s_flags[4];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const bool cwarp = (blockIdx.x == 0 && warp == 0);
-    const int gw = blockIdx.x * kWarps + warp - 1;
-    const int W = gridDim.x * kWarps - 1;
-    constexpr int RT = tb2_rt(K);
-    constexpr int NV = 2 * (1 + K);
-    double2* ring = tb2_ring + (size_t)warp * Tb2Stage<K, DIAG>::WARP;
-    const int cbeg = cwarp ? 0 : (int)((long long)gw * P.nunits / W);
-    const int cend = cwarp ? 0 : (int)((long long)(gw + 1) * P.nunits / W);
-    unsigned gen0 = 0;
-    if (tid == 0) gen0 = (unsigned)(ld_acquire64(&P.ctrl->word) >> 32);
-    int active = P.active0, rbmask = 0;
-    const int M = P.max_nodes;
-    const double alpha = P_alpha(P);
-    double dd[K][5];
-#pragma unroll
-    for (int k = 0; k < K; k++) coef_first5<K>(P, k, dd[k]);
-    if (cwarp && P.coef_gen) {
-        for (int r = 0; r < 5 && r < M; r++) {
-            double row[K];
-#pragma unroll
-            for (int k = 0; k < K; k++) row[k] = dd[k][r];
-            coef_write_row<K>(P, r, lane, active, row);
-        }
-    }
-    double d0[K], da[K], db[K], rbd[K];
-#pragma unroll
-    for (int k = 0; k < K; k++) {
-        d0[k] = dd[k][0];
-        da[k] = dd[k][1];
-        db[k] = dd[k][2];
-        rbd[k] = 0.0;
-    }
-    double na[K], nb[K];   // rows m+2, m+3 (rows 3, 4 from the prologue for the first pass)
-#pragma unroll
-    for (int k = 0; k < K; k++) {
-        na[k] = dd[k][3];
-        nb[k] = dd[k][4];
-    }
-    int m = 1;
-    double nb1 = coef_beta(P, 1), nb2 = (2 < M) ? coef_beta(P, 2) : 0.0;
-    for (; m < M; m += 2) {
-        const bool two = (m + 1 < M);
-        const double b1 = nb1, b2 = two ? nb2 : 0.0;
-        // next pass's shifts (constant inputs): loaded now, off the post-barrier critical path
-        nb1 = (m + 2 < M) ? coef_beta(P, m + 2) : 0.0;
-        nb2 = (m + 3 < M) ? coef_beta(P, m + 3) : 0.0;
-        const int pass = (m - 1) >> 1;
-        if (P.trace && tid == 0 && pass < 160) P.trace[((size_t)pass * gridDim.x + blockIdx.x) * 3] = globaltimer_ns();
-        double* dst = P.ydst[pass & 1];
-        double acc[2 * (1 + K)];
-#pragma unroll
-        for (int i = 0; i < 2 * (1 + K); i++) acc[i] = 0.0;
-        if (cwarp) {
-            if (P.coef_gen) {
-                if (m + 4 < M) coef_write_row<K>(P, m + 4, lane, active, nullptr);
-                if (m + 5 < M) coef_write_row<K>(P, m + 5, lane, active, nullptr);
-            }
-        } else {
-            const double* src = (m == 1) ? P.v.base : P.ysrc[(pass & 1) ^ 1].base;
-            if (P.seg > 0) {
-                // dynamic segments of P.seg chunks (balances the end-of-pass tail).  The norm partials
-                // stay deterministic: each segment's sums are formed by one warp in a fixed order and
-                // stored by segment index; the last finisher of each group of 32 segments sums the
-                // group in index order (fixed butterfly); the barrier sums the groups in order.
-                unsigned* ctr = &P.ctrl->work[pass & 1];
-#pragma unroll 1
-                for (;;) {
-                    int sg = 0;
-                    if (lane == 0) sg = (int)atomicAdd(ctr, 1u);
-                    sg = __shfl_sync(FULL_MASK, sg, 0);
-                    if (sg >= P.nseg) break;
-                    int c_b, c_e;
-                    if (P.order) {   // band fastest: adjacent bands of the same rows run together
-                        const int rs = sg / P.nb, b = sg - rs * P.nb;
-                        if (P.segrow) {
-                            c_b = b * P.nrb + __ldg(P.segrow + rs);
-                            c_e = b * P.nrb + __ldg(P.segrow + rs + 1);
-                        } else {
-                            c_b = b * P.nrb + rs * P.seg;
-                            c_e = b * P.nrb + min(P.nrb, rs * P.seg + P.seg);
-                        }
-                    } else {
-                        c_b = sg * P.seg;
-                        c_e = min(P.nunits, c_b + P.seg);
-                    }
-#pragma unroll
-                    for (int i = 0; i < NV; i++) acc[i] = 0.0;
-                    tb2_strip<K, DIAG>(P, m == 1, two, src, dst, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active,
-                                       rbmask, rbd, acc, ring);
-                    double sacc[NV];
-#pragma unroll
-                    for (int i = 0; i < NV; i++) sacc[i] = acc[i];
-                    warp_sum<NV>(sacc);
-                    int last = 0;
-                    const int g = sg >> 5;
-                    if (lane == 0) {
-#pragma unroll
-                        for (int i = 0; i < NV; i++) P.seg_part[(size_t)sg * NV + i] = sacc[i];
-                        __threadfence();
-                        const unsigned t = atomicAdd(&P.grp_cnt[g], 1u);
-                        last = (int)(t == (unsigned)(min(32, P.nseg - g * 32) - 1));
-                    }
-                    last = __shfl_sync(FULL_MASK, last, 0);
-                    if (last) {
-                        __threadfence();
-                        const int s2 = g * 32 + lane;
-                        double gv[NV];
-#pragma unroll
-                        for (int i = 0; i < NV; i++) gv[i] = (s2 < P.nseg) ? __ldcg(P.seg_part + (size_t)s2 * NV + i) : 0.0;
-                        warp_sum<NV>(gv);
-                        if (lane == 0) {
-#pragma unroll
-                            for (int i = 0; i < NV; i++) P.grp_part[(size_t)g * NV + i] = gv[i];
-                            P.grp_cnt[g] = 0u;
-                        }
-                    }
-                }
-            } else {
-                tb2_strip<K, DIAG>(P, m == 1, two, src, dst, cbeg, cend, lane, alpha, b1, b2, d0, da, db, active,
-                                   rbmask, rbd, acc, ring);
-            }
-        }
-        if (P.seg == 0) {
-            block_reduce<2 * (1 + K)>(acc, s_red);
-            if (tid == 0) {
-                double* slot = P.partials + ((size_t)(pass & 1) * gridDim.x + blockIdx.x) * kSlot;
-#pragma unroll
-                for (int i = 0; i < 2 * (1 + K); i++) slot[i] = acc[i];
-            }
-        }
-        if (P.trace) {
-            __syncthreads();
-            if (tid == 0 && pass < 160) P.trace[((size_t)pass * gridDim.x + blockIdx.x) * 3 + 1] = globaltimer_ns();
-        }
-        barrier_decide_tb2<K>(P, m, two, gen0, da, db, active, s_red, s_flags);
-        if (P.trace && tid == 0 && pass < 160) P.trace[((size_t)pass * gridDim.x + blockIdx.x) * 3 + 2] = globaltimer_ns();
-        active = s_flags[2];
-        rbmask = s_flags[3];
-#pragma unroll
-        for (int k = 0; k < K; k++) {
-            rbd[k] = db[k];
-            da[k] = na[k];
-            db[k] = nb[k];
-            // rows m+4, m+5 (written by the coefficient warp during pass m-2... visible after this barrier)
-            na[k] = (m + 4 < M) ? P.table[(size_t)(m + 4) * (1 + K) + 1 + k] : 0.0;
-            nb[k] = (m + 5 < M) ? P.table[(size_t)(m + 5) * (1 + K) + 1 + k] : 0.0;
-        }
-        if (s_flags[1]) break;
-    }
-    // the call ended on the first iteration of a pass for some accumulators: final rollback
-    if (rbmask && !cwarp && m < M) strip2d_tb2_rollback<K, RT>(P, P.ydst[((m - 1) >> 1) & 1], cbeg, cend, lane, rbmask, rbd);
-}
-
-// ---------------------------------------------------------------------------
-// 3D marching kernel with shared-memory plane tiles (single GPU; n1 % 8 == 0, n2 % 64 == 0).
-// A CTA owns a (8 j-rows x 64 k) column of one run of TI3 planes and marches along i: every plane's
-// tile of rows j0-1 .. j0+9 (11 rows: the j-neighbours j-1, j+1, j+2 of the 8 output rows) and
-// columns k0-2 .. k0+65 is staged once by cp.async into a ring of 6 planes, so each y value is read
-// from L2/HBM ~1.4 times (11/8 rows + run halos) instead of ~5.5 times by the warp-unit tile3d;
-// i-, j- and k-neighbours all come from shared memory.  Same per-point FMA order as tile3d (bitwise
-// equal results).  Newton coefficients come from the prebuilt table (k_coef_tables); the grid
-// barrier and the P:155 decision are those of k_leja2d.
-// ---------------------------------------------------------------------------
-#ifndef LX_TI3
-#define LX_TI3 64
-#endif
-constexpr int kTI3 = LX_TI3;             // planes per run
-constexpr int kS3Cols = 68;              // k0-2 .. k0+65
-constexpr int kS3J = 16;                 // output j-rows per CTA tile (2 per warp)
-constexpr int kS3Rows = kS3J + 3;        // j0-1 .. j0+kS3J+1
-constexpr int kS3Plane = kS3Rows * kS3Cols;   // doubles per staged plane
-constexpr int kS3Depth = 6;              // ring of planes
-constexpr int kS3Smem = kS3Depth * kS3Plane * 8;
-
-__device__ __forceinline__ void s3_issue(const double* __restrict__ src, double* ring, int ip, int slot, int j0,
-                                         int k0, int n0, int n1, int n2) {
-    // kS3Rows rows x 34 16-byte pieces
-    const int pl = ip < 0 ? ip + n0 : (ip >= n0 ? ip - n0 : ip);
-    double* dst = ring + slot * kS3Plane;
-    for (int t = threadIdx.x; t < kS3Rows * (kS3Cols / 2); t += kThreads) {
-        const int r = t / (kS3Cols / 2), c2 = t - r * (kS3Cols / 2);
-        int j = j0 - 1 + r;
-        j = j < 0 ? j + n1 : (j >= n1 ? j - n1 : j);
-        int k = k0 - 2 + 2 * c2;
-        k = k < 0 ? k + n2 : (k >= n2 ? k - n2 : k);
-        cp_async16(dst + r * kS3Cols + 2 * c2, src + ((size_t)pl * n1 + j) * n2 + k);
-    }
-}
-
-template <int K, bool DIAG, bool FIRST>
-__device__ __forceinline__ void s3_unit(const LejaParams& P, const double* __restrict__ src, double* __restrict__ dst,
-                                        int cu, double* ring, int lane, int warp, double beta, const double* d0,
-                                        const double* dm, int active, double alpha, double& sy, double* sp) {
-    const int n0 = P.n_loc, n1 = P.n1, n2 = P.n2;
-    const int njb = n1 / kS3J, nkb = n2 >> 6;
-    const int jb = cu % njb;
-    const int t0 = cu / njb;
-    const int kb = t0 % nkb;
-    const int ir = t0 / nkb;
-    const int j0 = jb * kS3J, k0 = kb * 64;
-    const int i0 = ir * kTI3, i1 = min(n0, i0 + kTI3);
-    const Stencil& S = P.st;
-    constexpr int KK = K > 0 ? K : 1;
-    constexpr int RW = kS3J / kWarps;               // rows per warp
-#pragma unroll
-    for (int q = 0; q < 4; q++) {
-        s3_issue(src, ring, i0 - 1 + q, q, j0, k0, n0, n1, n2);
-        cp_async_commit();
-    }
-    const int kc = k0 + 2 * lane;
-    // p / u of the next plane prefetched into registers one plane ahead (their latency off the barrier path);
-    // K >= 3 keeps only u prefetched (the p registers would spill)
-    constexpr bool PREF = K <= 2;
-    constexpr int KP = PREF ? KK : 1;
-    double2 pv[RW][KK], uu[RW], pvn[RW][KP], uun[RW];
-    auto fetch_p = [&](int i, auto& pq) {
-#pragma unroll
-        for (int r = 0; r < RW; r++) {
-            const long long off = ((long long)i * n1 + (j0 + warp + r * kWarps)) * n2 + kc;
-#pragma unroll
-            for (int k = 0; k < KK; k++) {
-                pq[r][k] = make_double2(0.0, 0.0);
-                if (!FIRST && i < i1 && ((active >> k) & 1)) pq[r][k] = ld2(P.p[k] + off);
-            }
-        }
-    };
-    auto fetch_u = [&](int i, double2 (&uq)[RW]) {
-#pragma unroll
-        for (int r = 0; r < RW; r++) {
-            const long long off = ((long long)i * n1 + (j0 + warp + r * kWarps)) * n2 + kc;
-            uq[r] = make_double2(0.0, 0.0);
-            if (DIAG && i < i1) uq[r] = ldg2(P.u + off);
-        }
-    };
-    if constexpr (PREF) fetch_p(i0, pv);
-    fetch_u(i0, uu);
-    for (int i = i0; i < i1; i++) {
-        const int rel = i - i0 + 1;
-        if (i + 3 <= i1 + 1) s3_issue(src, ring, i + 3, (rel + 3) % kS3Depth, j0, k0, n0, n1, n2);
-        cp_async_commit();   // (possibly empty group: keeps the wait_group accounting uniform)
-        if constexpr (PREF) fetch_p(i + 1, pvn);
-        fetch_u(i + 1, uun);
-        if constexpr (!PREF) fetch_p(i, pv);
-        cp_async_wait<1>();
-        __syncthreads();
-        const uint32_t base = smem_u32(ring);
-        auto at = [&](int pos, int row, int col) {
-            return lds2(base + (uint32_t)(((pos % kS3Depth) * kS3Plane + row * kS3Cols + col) * 8));
-        };
-        const int cc = 2 + 2 * lane;
-#pragma unroll
-        for (int r = 0; r < RW; r++) {
-            const int row = warp + r * kWarps + 1;     // staged row of output j
-            const int j = j0 + row - 1;
-            const double2 yc = at(rel, row, cc);
-            const double2 up = at(rel - 1 + kS3Depth, row, cc);
-            const double2 dn1 = at(rel + 1, row, cc);
-            const double2 dn2 = at(rel + 2, row, cc);
-            const double2 wm = at(rel, row - 1, cc);
-            const double2 wp1 = at(rel, row + 1, cc);
-            const double2 wp2 = at(rel, row + 2, cc);
-            const double2 lf = at(rel, row, cc - 2);
-            const double2 rt = at(rel, row, cc + 2);
-            const double left = lf.y, r1 = rt.x, r2 = rt.y;
-            const long long off = ((long long)i * n1 + j) * n2 + kc;
-            double ax = S.c0 * yc.x;
-            ax = fma(S.m1[0], up.x, ax);
-            ax = fma(S.p1[0], dn1.x, ax);
-            ax = fma(S.p2[0], dn2.x, ax);
-            ax = fma(S.m1[1], wm.x, ax);
-            ax = fma(S.p1[1], wp1.x, ax);
-            ax = fma(S.p2[1], wp2.x, ax);
-            ax = fma(S.m1[2], left, ax);
-            ax = fma(S.p1[2], yc.y, ax);
-            ax = fma(S.p2[2], r1, ax);
-            double ay = S.c0 * yc.y;
-            ay = fma(S.m1[0], up.y, ay);
-            ay = fma(S.p1[0], dn1.y, ay);
-            ay = fma(S.p2[0], dn2.y, ay);
-            ay = fma(S.m1[1], wm.y, ay);
-            ay = fma(S.p1[1], wp1.y, ay);
-            ay = fma(S.p2[1], wp2.y, ay);
-            ay = fma(S.m1[2], yc.x, ay);
-            ay = fma(S.p1[2], r1, ay);
-            ay = fma(S.p2[2], r2, ay);
-            if (DIAG) {
-                ax = fma(fma(S.qb, uu[r].x * uu[r].x, S.qa), yc.x, ax);
-                ay = fma(fma(S.qb, uu[r].y * uu[r].y, S.qa), yc.y, ay);
-            }
-            double2 yn;
-            yn.x = fma(alpha, ax, beta * yc.x);
-            yn.y = fma(alpha, ay, beta * yc.y);
-            st2(dst + off, yn);
-            sy = fma(yn.x, yn.x, sy);
-            sy = fma(yn.y, yn.y, sy);
-#pragma unroll
-            for (int k = 0; k < KK; k++) {
-                if ((active >> k) & 1) {
-                    double2 pn;
-                    if (FIRST) {
-                        pn.x = fma(dm[k], yn.x, d0[k] * yc.x);
-                        pn.y = fma(dm[k], yn.y, d0[k] * yc.y);
-                    } else {
-                        pn.x = fma(dm[k], yn.x, pv[r][k].x);
-                        pn.y = fma(dm[k], yn.y, pv[r][k].y);
-                    }
-                    st2(P.p[k] + off, pn);
-                    sp[k] = fma(pn.x, pn.x, sp[k]);
-                    sp[k] = fma(pn.y, pn.y, sp[k]);
-                }
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < RW; r++) {
-            uu[r] = uun[r];
-            if constexpr (PREF) {
-#pragma unroll
-                for (int k = 0; k < KP; k++) pv[r][k] = pvn[r][k];
-            }
-        }
-    }
-    cp_async_wait<0>();
-    __syncthreads();   // the ring is reused by the next unit
-}
-
-template <int K, bool DIAG>
-__global__ void __launch_bounds__(kThreads, 2) k_leja3d_smem(const __grid_constant__ LejaParams P) {
-    __shared__ double s_red[kWarps][kSlot];
-    __shared__ int s_flags[4];
-    extern __shared__ double s3_ring[];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    unsigned gen0 = 0;
-    if (tid == 0) gen0 = (unsigned)(ld_acquire64(&P.ctrl->word) >> 32);
-    int active = P.active0;
-    const int M = P.max_nodes;
-    const double alpha = P_alpha(P);
-    const int ncu = (P.n1 / kS3J) * (P.n2 >> 6) * ((P.n_loc + kTI3 - 1) / kTI3);
-    double d0[K];
-#pragma unroll
-    for (int k = 0; k < K; k++) d0[k] = P.table[1 + k];
-    double beta_n = coef_beta(P, 1), dm_n[K];
-#pragma unroll
-    for (int k = 0; k < K; k++) dm_n[k] = P.table[(size_t)(1 + K) + 1 + k];
-    for (int m = 1; m < M; m++) {
-        const double beta = beta_n;
-        double dm[K], sp[K];
-#pragma unroll
-        for (int k = 0; k < K; k++) {
-            dm[k] = dm_n[k];
-            sp[k] = 0.0;
-        }
-        double sy = 0.0;
-        const int par = m & 1;
-        double* dst = P.ydst[par];
-        if (m == 1) {
-            for (int cu = blockIdx.x; cu < ncu; cu += gridDim.x)
-                s3_unit<K, DIAG, true>(P, P.v.base, dst, cu, s3_ring, lane, warp, beta, d0, dm, active, alpha, sy, sp);
-        } else {
-            const double* src = P.ydst[par ^ 1];
-            for (int cu = blockIdx.x; cu < ncu; cu += gridDim.x)
-                s3_unit<K, DIAG, false>(P, src, dst, cu, s3_ring, lane, warp, beta, d0, dm, active, alpha, sy, sp);
-        }
-        double vals[1 + K];
-        vals[0] = sy;
-#pragma unroll
-        for (int k = 0; k < K; k++) vals[1 + k] = sp[k];
-        if (m + 1 < M) {
-            beta_n = coef_beta(P, m + 1);
-#pragma unroll
-            for (int k = 0; k < K; k++) dm_n[k] = P.table[(size_t)(m + 1) * (1 + K) + 1 + k];
-        }
-        block_reduce<1 + K>(vals, s_red);
-        if (tid == 0) {
-            double* slot = P.partials + ((size_t)par * gridDim.x + blockIdx.x) * kSlot;
-#pragma unroll
-            for (int i = 0; i < 1 + K; i++) slot[i] = vals[i];
-        }
-        barrier_decide<K, M_LEJA>(P, m, gen0, dm, active, s_red, s_flags);
-        active = s_flags[2];
-        if (s_flags[1]) break;
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Launchers
-// ---------------------------------------------------------------------------
-// Co-resident CTAs (kThreads each, no dynamic smem) of a kernel on a device: SMs x blocks per SM,
-// cached per (device, kernel) -- occupancy queries cost host microseconds on every Leja call.
-static int coresident(int device, const void* kern) {
-    static std::mutex mu;
-    static std::map<std::pair<int, const void*>, int> cache;
-    std::lock_guard<std::mutex> lock(mu);
-    auto it = cache.find({device, kern});
-    if (it != cache.end()) return it->second;
-    int nsm = 0, per = 0;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, 0);
-    if (per < 1) per = 1;
-    cache[{device, kern}] = nsm * per;
-    return nsm * per;
-}
-
-template <typename Kern>
-static int max_coresident(int device, Kern kern) {
-    return coresident(device, (const void*)kern);
-}
-
-template <int NDIM>
-static void* leja_kernel_ptr_nd(int K, bool diag) {
-    switch (K * 2 + (diag ? 1 : 0)) {
-        case 2: return (void*)k_leja2d<NDIM, 1, false>;
-        case 3: return (void*)k_leja2d<NDIM, 1, true>;
-        case 4: return (void*)k_leja2d<NDIM, 2, false>;
-        case 5: return (void*)k_leja2d<NDIM, 2, true>;
-        case 6: return (void*)k_leja2d<NDIM, 3, false>;
-        case 7: return (void*)k_leja2d<NDIM, 3, true>;
-        case 8: return (void*)k_leja2d<NDIM, 4, false>;
-        case 9: return (void*)k_leja2d<NDIM, 4, true>;
-    }
-    return nullptr;
-}
-
-static void* leja_kernel_ptr(int ndim, int K, bool diag) {
-    if (ndim == 4) {   // flux form (Burgers, 2D); react handled at run time inside the tile
-        switch (K) {
-            case 1: return (void*)k_leja2d<4, 1, false>;
-            case 2: return (void*)k_leja2d<4, 2, false>;
-            case 3: return (void*)k_leja2d<4, 3, false>;
-            case 4: return (void*)k_leja2d<4, 4, false>;
-        }
-        return nullptr;
-    }
-    return ndim == 3 ? leja_kernel_ptr_nd<3>(K, diag) : leja_kernel_ptr_nd<2>(K, diag);
-}
-
-int leja_grid_size(int device, int K, bool diag, int ndim, int nunits) {
-    long long g = coresident(device, leja_kernel_ptr(ndim, K, diag));
-    // never more CTAs than work: at least 2 units per warp for tiny grids
-    long long need = (nunits + kWarps - 1) / kWarps;
-    if (g > need) g = need > 0 ? need : 1;
-    return (int)g;
-}
-
-cudaError_t launch_leja_persistent(const LejaParams& P, cudaStream_t s, bool diag) {
-    void* kern = leja_kernel_ptr(P.ndim, P.K, diag);
-    if (!kern) return cudaErrorInvalidValue;
-    void* args[] = {(void*)&P};
-    return cudaLaunchCooperativeKernel(kern, dim3(P.grid), dim3(kThreads), args, 0, s);
-}
-
-static void* leja3d_smem_ptr(int K, bool diag) {
-    switch (K * 2 + (diag ? 1 : 0)) {
-        case 2: return (void*)k_leja3d_smem<1, false>;
-        case 3: return (void*)k_leja3d_smem<1, true>;
-        case 4: return (void*)k_leja3d_smem<2, false>;
-        case 5: return (void*)k_leja3d_smem<2, true>;
-        case 6: return (void*)k_leja3d_smem<3, false>;
-        case 7: return (void*)k_leja3d_smem<3, true>;
-        case 8: return (void*)k_leja3d_smem<4, false>;
-        case 9: return (void*)k_leja3d_smem<4, true>;
-    }
-    return nullptr;
-}
-
-int leja3d_smem_units(int n0, int n1, int n2) { return (n1 / kS3J) * (n2 / 64) * ((n0 + kTI3 - 1) / kTI3); }
-
-int leja3d_smem_grid_size(int device, int K, bool diag, int ncu) {
-    void* kern = leja3d_smem_ptr(K, diag);
-    if (!kern) return 0;
-    static std::mutex mu;
-    static std::map<std::pair<int, const void*>, int> cache;
-    std::lock_guard<std::mutex> lock(mu);
-    auto it = cache.find({device, kern});
-    int g;
-    if (it != cache.end()) {
-        g = it->second;
-    } else {
-        int nsm = 0, per = 0;
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kS3Smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, kS3Smem);
-        g = nsm * (per < 1 ? 1 : per);
-        cache[{device, kern}] = g;
-    }
-    return g < ncu ? g : ncu;
-}
-
-cudaError_t launch_leja3d_smem(const LejaParams& P, cudaStream_t s, bool diag) {
-    void* kern = leja3d_smem_ptr(P.K, diag);
-    if (!kern) return cudaErrorInvalidValue;
-    void* args[] = {(void*)&P};
-    return cudaLaunchCooperativeKernel(kern, dim3(P.grid), dim3(kThreads), args, kS3Smem, s);
-}
-
-cudaError_t launch_power_persistent(const LejaParams& P, cudaStream_t s, bool diag) {
-    void* kern = P.ndim == 4 ? (void*)k_power2d<4, false>
-                 : P.ndim == 3 ? (diag ? (void*)k_power2d<3, true> : (void*)k_power2d<3, false>)
-                               : (diag ? (void*)k_power2d<2, true> : (void*)k_power2d<2, false>);
-    void* args[] = {(void*)&P};
-    return cudaLaunchCooperativeKernel(kern, dim3(P.grid), dim3(kThreads), args, 0, s);
-}
-
-
-template <int NDIM>
-static void* leja_step_ptr_nd(int K, bool diag) {
-    switch (K * 2 + (diag ? 1 : 0)) {
-        case 2: return (void*)k_leja2d_step<NDIM, 1, false>;
-        case 3: return (void*)k_leja2d_step<NDIM, 1, true>;
-        case 4: return (void*)k_leja2d_step<NDIM, 2, false>;
-        case 5: return (void*)k_leja2d_step<NDIM, 2, true>;
-        case 6: return (void*)k_leja2d_step<NDIM, 3, false>;
-        case 7: return (void*)k_leja2d_step<NDIM, 3, true>;
-        case 8: return (void*)k_leja2d_step<NDIM, 4, false>;
-        case 9: return (void*)k_leja2d_step<NDIM, 4, true>;
-    }
-    return nullptr;
-}
-
-static void* leja_step_ptr(int ndim, int K, bool diag) {
-    return ndim == 3 ? leja_step_ptr_nd<3>(K, diag) : leja_step_ptr_nd<2>(K, diag);
-}
-
-int step_grid_size(int device, int nunits) {
-    int nsm = 0;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
-    long long g = (long long)nsm * 2;
-    long long need = (nunits + kWarps - 1) / kWarps;
-    if (g > need) g = need > 0 ? need : 1;
-    return (int)g;
-}
-
-cudaError_t launch_leja_step(const LejaParams& P, int m, cudaStream_t s, bool diag) {
-    void* kern = leja_step_ptr(P.ndim, P.K, diag);
-    if (!kern) return cudaErrorInvalidValue;
-    void* args[] = {(void*)&P, (void*)&m};
-    return cudaLaunchKernel(kern, dim3(P.grid), dim3(kThreads), args, 0, s);
-}
-
-cudaError_t launch_power_step(const LejaParams& P, int m, cudaStream_t s, bool diag) {
-    void* kern = P.ndim == 3 ? (diag ? (void*)k_power2d_step<3, true> : (void*)k_power2d_step<3, false>)
-                             : (diag ? (void*)k_power2d_step<2, true> : (void*)k_power2d_step<2, false>);
-    void* args[] = {(void*)&P, (void*)&m};
-    return cudaLaunchKernel(kern, dim3(P.grid), dim3(kThreads), args, 0, s);
-}
-
-cudaError_t launch_finalize_err(const double* gathered, int nranks, double N, Record* rec, cudaStream_t s) {
-    k_finalize_err<<<1, 32, 0, s>>>(gathered, nranks, N, rec);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_max_u64(const unsigned long long* vals, int n, unsigned long long* out, cudaStream_t s) {
-    k_max_u64<<<1, 32, 0, s>>>(vals, n, out);
-    return cudaGetLastError();
-}
-
-
-// ---- TMA marching kernel launch
-template <int K, bool DIAG>
-static cudaError_t tma_prepare(int device, int* per_sm) {
-    using C = TmaCfg<K, DIAG>;
-    cudaError_t e = cudaFuncSetAttribute(k_leja2d_tma<K, DIAG>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_leja2d_tma<K, DIAG>, kThreads, C::SMEM);
-}
-
-template <int K, bool DIAG>
-static cudaError_t tma_launch(const LejaParams& P, cudaStream_t s) {
-    using C = TmaCfg<K, DIAG>;
-    void* args[] = {(void*)&P};
-    return cudaLaunchCooperativeKernel((void*)k_leja2d_tma<K, DIAG>, dim3(P.grid), dim3(kThreads), args, C::SMEM, s);
-}
-
-static cudaError_t tma_dispatch(int K, bool diag, int device, int* per_sm, const LejaParams* P, cudaStream_t s) {
-#define LX_TMA_CASE(KK, DD)                                                    \
-    if (K == KK && diag == DD) return P ? tma_launch<KK, DD>(*P, s) : tma_prepare<KK, DD>(device, per_sm);
-    LX_TMA_CASE(1, false) LX_TMA_CASE(1, true) LX_TMA_CASE(2, false) LX_TMA_CASE(2, true)
-    LX_TMA_CASE(3, false) LX_TMA_CASE(3, true) LX_TMA_CASE(4, false) LX_TMA_CASE(4, true)
-#undef LX_TMA_CASE
-    return cudaErrorInvalidValue;
-}
-
-int leja_tma_grid_size(int device, int K, bool diag, long long band_rows) {
-    int nsm = 0, per = 0;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
-    if (tma_dispatch(K, diag, device, &per, nullptr, nullptr) != cudaSuccess || per < 1) return 0;
-    long long g = (long long)nsm * per;
-    const long long need = (band_rows + kWarps * 8 - 1) / (kWarps * 8);   // >= 8 rows per warp
-    if (g > need) g = need > 0 ? need : 1;
-    return (int)g;
-}
-
-cudaError_t launch_leja_tma(const LejaParams& P, cudaStream_t s, bool diag) {
-    return tma_dispatch(P.K, diag, 0, nullptr, &P, s);
-}
 
 
 // ---------------------------------------------------------------------------
@@ -2448,53 +119,6 @@ cudaError_t launch_shift_scale(const unsigned long long* umax, const ShiftArgs& 
     return cudaGetLastError();
 }
 
-
-static void* leja_tb2_ptr(int K, bool diag) {
-    switch (K * 2 + (diag ? 1 : 0)) {
-        case 2: return (void*)k_leja2d_tb2<1, false>;
-        case 3: return (void*)k_leja2d_tb2<1, true>;
-        case 4: return (void*)k_leja2d_tb2<2, false>;
-        case 5: return (void*)k_leja2d_tb2<2, true>;
-        case 6: return (void*)k_leja2d_tb2<3, false>;
-        case 7: return (void*)k_leja2d_tb2<3, true>;
-        case 8: return (void*)k_leja2d_tb2<4, false>;
-        case 9: return (void*)k_leja2d_tb2<4, true>;
-    }
-    return nullptr;
-}
-
-static int tb2_prepare(int device, int K, bool diag) {
-    // dynamic shared memory opt-in (once per kernel) + co-resident CTAs with that smem, cached
-    static std::mutex mu;
-    static std::map<std::pair<int, int>, int> cache;
-    std::lock_guard<std::mutex> lock(mu);
-    const int key = K * 2 + (diag ? 1 : 0);
-    auto it = cache.find({device, key});
-    if (it != cache.end()) return it->second;
-    const void* kern = leja_tb2_ptr(K, diag);
-    const int smem = tb2_smem_bytes(K, diag);
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int nsm = 0, per = 0;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, smem);
-    if (per < 1) per = 1;
-    cache[{device, key}] = nsm * per;
-    return nsm * per;
-}
-
-int leja_tb2_grid_size(int device, int K, bool diag, int nunits) {
-    long long g = tb2_prepare(device, K, diag);
-    long long need = (nunits + kWarps - 1) / kWarps + 1;
-    if (g > need) g = need;
-    return (int)g;
-}
-
-cudaError_t launch_leja_tb2(const LejaParams& P, cudaStream_t s, bool diag) {
-    void* kern = leja_tb2_ptr(P.K, diag);
-    if (!kern) return cudaErrorInvalidValue;
-    void* args[] = {(void*)&P};
-    return cudaLaunchCooperativeKernel(kern, dim3(P.grid), dim3(kThreads), args, tb2_smem_bytes(P.K, diag), s);
-}
 
 // ---------------------------------------------------------------------------
 // Stage kernels
@@ -2711,6 +335,33 @@ cudaError_t launch_stage(int op, const StageArgs& A, cudaStream_t s) {
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
+}
+
+cudaError_t preload_leja();
+cudaError_t preload_tb2();
+cudaError_t preload_3d();
+
+// Force every kernel of the library to be loaded now (cudaFuncGetAttributes loads a function under CUDA
+// lazy loading).  Virtual ranks sharing one context run persistent kernels that spin on each other; a
+// lazy load during that time needs the context to idle and would deadlock until the watchdog.
+cudaError_t preload_kernels() {
+    cudaError_t e = preload_leja();
+    if (e == cudaSuccess) e = preload_tb2();
+    if (e == cudaSuccess) e = preload_3d();
+    if (e != cudaSuccess) return e;
+    for (int op = ST_RHS_SCALED; op <= ST_LIN4; op++) {
+        const void* k = stage_kernel_ptr(op);   // (ST_RHS_SCALED is a stencil kernel: k_rhs2d below)
+        cudaFuncAttributes a;
+        if (k && cudaFuncGetAttributes(&a, k) != cudaSuccess) return cudaGetLastError();
+    }
+    const void* fixed[] = {(const void*)k_coef_tables, (const void*)k_shift_scale, (const void*)k_fill_start,
+                           (const void*)k_rem2d_flux, (const void*)k_rhs2d<2>, (const void*)k_rhs2d<3>,
+                           (const void*)k_rhs2d<4>};
+    for (const void* k : fixed) {
+        cudaFuncAttributes a;
+        if (cudaFuncGetAttributes(&a, k) != cudaSuccess) return cudaGetLastError();
+    }
+    return cudaSuccess;
 }
 
 }  // namespace lx

@@ -31,12 +31,12 @@ def share_unique_id() -> bytes:
     return obj[0]
 
 
-def attach(ctx: Context) -> tuple:
-    """Attach the context to an NCCL communicator spanning the process group.
-    Returns this rank's slab (i_begin, i_end)."""
+def attach(ctx: Context, flags: int = 0) -> tuple:
+    """Attach the context to an NCCL communicator spanning the process group (lx_ctx_set_comm_ex;
+    flags: LX_COMM_FORCE, LX_COMM_NO_PEER).  Returns this rank's slab (i_begin, i_end)."""
     import torch.distributed as dist
     uid = share_unique_id()
-    ctx.set_comm(uid, dist.get_rank(), dist.get_world_size())
+    ctx.set_comm(uid, dist.get_rank(), dist.get_world_size(), flags)
     b, e, _ = ctx.local()
     return b, e
 

@@ -336,36 +336,6 @@ def test_steps_3d(xi300, method):
     assert err == pytest.approx(r.err, rel=1e-8)
 
 
-@pytest.mark.parametrize("shape,K,react", [((64, 64), 1, 0.0), ((50, 70), 2, 0.0), ((130, 66), 3, 1.0),
-                                           ((4096, 256), 1, 1.0)])
-def test_kernel_variants_bitwise_equal(xi300, monkeypatch, shape, K, react):
-    # register-tile kernel (default; Newton coefficients computed in-kernel) and the experimental
-    # TMA marching kernel (LX_LEJA_KERNEL=tma; coefficients from the table kernel) do the same
-    # per-point stencil arithmetic in the same order, and all coefficient arithmetic is explicitly
-    # rounded (no FMA contraction): identical iterations and bitwise-identical outputs.
-    diff, nu = (1e-4, 0.0) if react else (1.0, 10.0)
-    pb, ob = _pair(shape, diff=diff, nu=nu, react=react)
-    u = W.ic_allen_cahn_2d(*shape) if react else None
-    v = W.ic_random(shape, seed=21, amp=0.2)
-    dt = 0.01 if react else 10 * min(W.dt_cfl(n, 10.0) for n in shape)
-    coeffs = (0.5, 2 / 3, 0.9, 1.0)[-K:]
-    res = {}
-    monkeypatch.setenv("LX_TBLOCK", "1")   # one iteration per pass (the two-step kernel: test_tblock2_*)
-    for variant in ("tile", "tma"):   # LX_LEJA_KERNEL values
-        monkeypatch.setenv("LX_LEJA_KERNEL", variant)
-        with lx.Context(pb) as ctx:
-            ud = _dev(u) if react else None
-            c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx, ud))
-            outs = [torch.empty(shape, dtype=torch.float64, device="cuda") for _ in range(K)]
-            it = lx.lx_real_leja_phi_vertical(ctx, _dev(v), outs, coeffs, dt, c, g, 1, TOL, TOL, u_lin=ud)
-            res[variant] = (it, [o.cpu().numpy() for o in outs])
-    assert res["tile"][0] == res["tma"][0]
-    for a, b in zip(res["tile"][1], res["tma"][1]):
-        np.testing.assert_array_equal(a, b)
-    r = O.real_leja_phi(ob, v, dt, c, g, 1, TOL, TOL, xi300, coeffs=coeffs, u_lin=u)
-    assert res["tma"][0] == r.iters
-
-
 @pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3"])
 def test_integrate_device_spectrum(xi300, method):
     # lx_integrate: the paper's time loop with (c, gamma) recomputed ON THE DEVICE every
@@ -481,8 +451,7 @@ def test_burgers_leja_power_rhs_integrate(xi300):
 @pytest.mark.parametrize("shape,K,react,l", [((64, 64), 1, 0.0, 0), ((66, 62), 2, 0.0, 1), ((7, 24), 1, 0.0, 2),
                                              ((130, 122), 3, 1.0, 1), ((131, 182), 4, 0.0, 1),
                                              ((200, 60), 4, 1.0, 3), ((4096, 256), 1, 1.0, 0)])
-def test_tblock2_matches_oracle_and_one_step(xi300, monkeypatch, shape, K, react, l):
-    # (also: dynamic segments (LX_TB2_SEG=8, default) and static ranges (0) give bitwise-equal fields)
+def test_tblock2_matches_oracle_and_one_step(xi300, shape, K, react, l):
     # two Leja iterations per HBM pass: ragged 60-column bands (n1 = 62, 122,
     # 182, 24 < 64), odd row counts, K = 1..4 (accumulators converging at different m, i.e. on
     # either half of a pass -> rollback), with and without the diagonal term.  Same iteration
@@ -495,34 +464,33 @@ def test_tblock2_matches_oracle_and_one_step(xi300, monkeypatch, shape, K, react
     dt = 0.01 if react else 10 * min(W.dt_cfl(n, 10.0) for n in shape)
     coeffs = (0.25, 0.5, 0.75, 1.0)[-K:]
     res = {}
-    for tb, seg in (("1", "8"), ("2", "8"), ("2s", "0")):   # one-step; two-step dynamic / static segments
-        monkeypatch.setenv("LX_TBLOCK", tb[0])
-        monkeypatch.setenv("LX_TB2_SEG", seg)
+    for tb in (1, 2):   # one iteration per pass (k_leja2d); two (k_leja2d_tb2; needs >= 16 rows, >= 64 columns)
         with lx.Context(pb) as ctx:
+            ctx.set_kernel(tb)
+            assert ctx.iterations_per_pass == (tb if shape[0] >= 16 and shape[1] >= 64 else 1)
             ud = _dev(u) if react else None
             c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx, ud))
             outs = [torch.full(shape, float("nan"), dtype=torch.float64, device="cuda") for _ in range(K)]
             it = lx.lx_real_leja_phi_vertical(ctx, _dev(v), outs, coeffs, dt, c, g, l, TOL, TOL, u_lin=ud)
             res[tb] = (it, [o.cpu().numpy() for o in outs])
     r = O.real_leja_phi(ob, v, dt, c, g, l, TOL, TOL, xi300, coeffs=coeffs, u_lin=u)
-    assert res["2"][0] == res["2s"][0] == res["1"][0] == r.iters
-    for a, s_, b, ref in zip(res["2"][1], res["2s"][1], res["1"][1], r.outs):
-        np.testing.assert_array_equal(a, s_)   # work partition does not change any point's arithmetic
+    assert res[2][0] == res[1][0] == r.iters
+    for a, b, ref in zip(res[2][1], res[1][1], r.outs):
         assert np.isfinite(a).all()
         np.testing.assert_allclose(a, b, rtol=0, atol=8 * np.finfo(float).eps * np.abs(b).max())
         assert np.linalg.norm(a - ref) <= TOL * np.linalg.norm(ref)
 
 
-def test_tblock2_dynamic_segments_reproducible(xi300, monkeypatch):
+def test_tblock2_dynamic_segments_reproducible(xi300):
     # dynamic work assignment (atomic segment counter) must not leak into the results: per-segment
     # norm partials are reduced in segment order -> identical iterations and bitwise-equal outputs
     # over repeated calls, at a size with thousands of segments (n = 1536: 26 bands x 384 chunks)
     n = 1536
-    monkeypatch.setenv("LX_TBLOCK", "2")   # below the auto threshold: force the two-step kernel
     pb, _ = _pair((n, n))
     u0 = _dev(W.ic_random((n, n), seed=5, amp=0.3))
     dt = 10 * W.dt_cfl(n, 10.0)
     with lx.Context(pb) as ctx:
+        ctx.set_kernel(2)   # below the auto threshold: force the two-step kernel
         c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
         runs = []
         for _ in range(4):
@@ -535,22 +503,24 @@ def test_tblock2_dynamic_segments_reproducible(xi300, monkeypatch):
             assert torch.equal(a, b)
 
 
-def test_tblock_auto_policy(monkeypatch):
-    # two-step kernel from 3*2^20 local points on (2D single GPU), one-pass below; LX_TBLOCK forces
-    monkeypatch.delenv("LX_TBLOCK", raising=False)
+def test_tblock_auto_policy():
+    # two-step kernel from 3*2^20 local points on (2D single GPU), one-pass below; lx_ctx_set_kernel forces
     for shape, want in (((1536, 1536), 1), ((2048, 2048), 2), ((64, 64), 1)):
         pb, _ = _pair(shape)
         with lx.Context(pb) as ctx:
             assert ctx.iterations_per_pass == want, shape
-    monkeypatch.setenv("LX_TBLOCK", "2")
     with lx.Context(_pair((64, 64))[0]) as ctx:
+        ctx.set_kernel(2)
         assert ctx.iterations_per_pass == 2
+        with pytest.raises(lx.LxError):
+            ctx.set_kernel(3)
     with lx.Context(_pair((8, 8, 64))[0]) as ctx:
+        ctx.set_kernel(2)
         assert ctx.iterations_per_pass == 1        # 3D: one pass per iteration
 
 
 @pytest.mark.parametrize("shape,K,react", [((20, 32, 64), 1, 0.0), ((70, 16, 128), 2, 1.0), ((130, 48, 64), 3, 0.0)])
-def test_3d_smem_kernel_bitwise_equals_tiles(xi300, monkeypatch, shape, K, react):
+def test_3d_smem_kernel_bitwise_equals_tiles(xi300, shape, K, react):
     # the shared-memory marching 3D kernel (plane runs of 64, ragged last run) evaluates every point with the
     # warp-tile kernel's operation order: identical iterations and bitwise-equal outputs; oracle parity
     diff, nu = (1e-3, 0.0) if react else (1.0, 10.0)
@@ -561,8 +531,8 @@ def test_3d_smem_kernel_bitwise_equals_tiles(xi300, monkeypatch, shape, K, react
     coeffs = (0.5, 2 / 3, 1.0)[-K:]
     res = {}
     for kern in ("tile", "smem"):
-        monkeypatch.setenv("LX_3D_KERNEL", kern)
         with lx.Context(pb) as ctx:
+            ctx.set_kernel(0, 1 if kern == "tile" else 0)
             ud = _dev(u) if react else None
             c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx, ud))
             outs = [torch.empty(shape, dtype=torch.float64, device="cuda") for _ in range(K)]

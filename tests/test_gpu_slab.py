@@ -1,9 +1,13 @@
-"""Multi-rank slab decomposition on ONE GPU: virtual ranks (host threads) with the
-in-process transport run exactly the protocol of the NCCL path (step kernels,
-1+2-row halo exchange, rank-order sum of the gathered partials).  Results must
-match the oracle (same iterations, rel L2 <= 1e-10) and -- since the per-point
-arithmetic is identical and only the norm summation order differs -- equal the
-single-domain CUDA result bitwise."""
+"""Multi-rank slab decomposition on ONE GPU.
+
+Virtual ranks (host threads) with the in-process transport run exactly the protocols of the
+multi-GPU path: 2D Leja calls with >= 16 rows per rank take the persistent peer-memory slab kernel
+(k_leja2d_tb2<K, DIAG, true>: halo rows stored into the neighbours' ghost blocks from inside the
+pass, per-rank partials exchanged at the pass barrier); everything else the per-iteration step
+protocol (step kernels, 1+2-row halo exchange, rank-order sum of the gathered partials).  Results
+must match the oracle (same iterations, rel L2 <= 1e-10) and -- since the per-point arithmetic is
+identical and only the norm summation order differs -- equal the single-domain CUDA result of the
+same kernel family bitwise.  A two-process test maps the exchange blocks through CUDA IPC."""
 import threading
 
 import numpy as np
@@ -52,8 +56,10 @@ def _run_ranks(P, fn):
 
 
 @pytest.mark.parametrize("P,shape", [(2, (64, 64)), (3, (50, 70)), (4, (130, 66)), (8, (64, 128))])
-def test_slab_leja_matches_oracle_and_single_domain(xi300, monkeypatch, P, shape):
-    monkeypatch.setenv("LX_TBLOCK", "1")   # single-domain reference: the one-step kernel (same arithmetic)
+def test_slab_leja_matches_oracle_and_single_domain(xi300, P, shape):
+    # peer-memory slab kernel when every rank has >= 16 rows (two iterations per pass: compared with the
+    # single-domain two-step kernel), else the step protocol (compared with the one-step kernel)
+    peer = shape[0] // P >= 16 and shape[1] >= 64
     dx = tuple(2.0 / n for n in shape)
     pb = lx.Problem(shape, dx, 1.0, 10.0, 0.0)
     ob = O.Problem(shape, dx, 1.0, 10.0, 0.0)
@@ -64,6 +70,7 @@ def test_slab_leja_matches_oracle_and_single_domain(xi300, monkeypatch, P, shape
     def rank_fn(r, group, s):
         ctx = lx.Context(pb, stream=s)
         ctx.set_comm_local(group, r)
+        assert ctx.iterations_per_pass == (2 if peer else 1)
         b, e, _ = ctx.local()
         vloc = torch.from_numpy(v[b:e]).cuda()
         outs = []
@@ -76,6 +83,7 @@ def test_slab_leja_matches_oracle_and_single_domain(xi300, monkeypatch, P, shape
 
     res = _run_ranks(P, rank_fn)
     with lx.Context(pb) as ctx1:
+        ctx1.set_kernel(2 if peer else 1)
         for idx, l in enumerate((0, 1, 3)):
             full = np.concatenate([res[r][2][idx][1] for r in range(P)], axis=0)
             its = {res[r][2][idx][0] for r in range(P)}
@@ -162,3 +170,108 @@ def test_nccl_transport_world_size_one():
     assert r.returncode == 0, r.stderr[-2000:]
     res = json.loads(r.stdout.strip().splitlines()[-1])
     assert res["ok"], res
+
+
+def _slab_vs_single(xi300, P, shape, K, react, l, flags=0, mult=10.0):
+    """P virtual ranks through the peer-memory slab kernel vs the single-domain two-step kernel
+    (bitwise) and the oracle (same iterations, 1e-10)."""
+    diff, nu = (1e-4, 0.0) if react else (1.0, 10.0)
+    dx = tuple(2.0 / n for n in shape)
+    pb = lx.Problem(shape, dx, diff, nu, react)
+    ob = O.Problem(shape, dx, diff, nu, react)
+    u = W.ic_allen_cahn_2d(*shape) if react else None
+    v = W.ic_random(shape, seed=41, amp=0.2)
+    dt = 0.01 if react else mult * min(W.dt_cfl(n, 10.0) for n in shape)
+    c, g = O.shift_scale(O.spectrum_bound(ob, u))
+    coeffs = (0.25, 0.5, 0.75, 1.0)[-K:]
+
+    def rank_fn(r, group, s):
+        ctx = lx.Context(pb, stream=s)
+        ctx.set_comm_local(group, r, flags)
+        assert ctx.iterations_per_pass == 2
+        b, e, _ = ctx.local()
+        ul = torch.from_numpy(u[b:e]).cuda() if react else None
+        vl = torch.from_numpy(v[b:e]).cuda()
+        outs = [torch.full_like(vl, float("nan")) for _ in range(K)]
+        it = lx.lx_real_leja_phi_vertical(ctx, vl, outs, coeffs, dt, c, g, l, TOL, TOL, u_lin=ul)
+        it2 = lx.lx_real_leja_phi_vertical(ctx, vl, outs, coeffs, dt, c, g, l, TOL, TOL, u_lin=ul)   # reuse
+        ctx.close()
+        return it, it2, [o.cpu().numpy() for o in outs]
+
+    res = _run_ranks(P, rank_fn)
+    with lx.Context(pb) as ctx1:
+        ctx1.set_kernel(2)
+        ones = [torch.empty(shape, dtype=torch.float64, device="cuda") for _ in range(K)]
+        it1 = lx.lx_real_leja_phi_vertical(ctx1, torch.from_numpy(v).cuda(), ones, coeffs, dt, c, g, l, TOL, TOL,
+                                           u_lin=torch.from_numpy(u).cuda() if react else None)
+    ref = O.real_leja_phi(ob, v, dt, c, g, l, TOL, TOL, xi300, coeffs=coeffs, u_lin=u)
+    assert {(r[0], r[1]) for r in res} == {(ref.iters, ref.iters)} and it1 == ref.iters
+    for k in range(K):
+        full = np.concatenate([res[r][2][k] for r in range(P)], axis=0)
+        np.testing.assert_array_equal(full, ones[k].cpu().numpy())
+        assert np.linalg.norm(full - ref.outs[k]) <= TOL * np.linalg.norm(ref.outs[k])
+
+
+@pytest.mark.parametrize("P,shape,K,react,l", [(2, (96, 130), 1, 0.0, 0), (4, (131, 64), 2, 0.0, 1),
+                                               (3, (200, 122), 3, 1.0, 1), (8, (256, 182), 4, 0.0, 3),
+                                               (2, (1024, 256), 1, 1.0, 0)])
+def test_peer_slab_kernel_bitwise(xi300, P, shape, K, react, l):
+    # ragged slabs (131 rows over 4 ranks), ragged 60-column bands, K = 1..4 (rollbacks), Allen-Cahn J
+    _slab_vs_single(xi300, P, shape, K, react, l)
+
+
+def test_peer_slab_kernel_one_rank_is_single_domain(xi300):
+    # LX_COMM_FORCE with one virtual rank: the slab kernel with itself as both neighbours (its ghost rows
+    # are its own periodic images) -- bitwise the single-domain two-step kernel
+    _slab_vs_single(xi300, 1, (128, 128), 2, 0.0, 1, flags=lx.LX_COMM_FORCE)
+
+
+def test_no_peer_flag_uses_step_protocol(xi300):
+    shape = (64, 64)
+    dx = tuple(2.0 / n for n in shape)
+    pb = lx.Problem(shape, dx, 1.0, 10.0, 0.0)
+
+    def rank_fn(r, group, s):
+        ctx = lx.Context(pb, stream=s)
+        ctx.set_comm_local(group, r, lx.LX_COMM_NO_PEER)
+        ipp = ctx.iterations_per_pass
+        ctx.close()
+        return ipp
+
+    assert _run_ranks(2, rank_fn) == [1, 1]
+    with lx.Context(pb) as ctx:   # one rank without FORCE: the single-domain context
+        ctx.set_comm_local(lx.LocalGroup(1), 0)
+        assert ctx.local() == (0, 64, 64 * 64)
+
+
+def test_peer_slab_kernel_two_processes_ipc(xi300):
+    # two processes on one GPU, exchange blocks mapped with CUDA IPC (tools/ipc_slab_check.py)
+    import json
+    import os
+    import subprocess
+    import sys
+    shape = (96, 128)
+    dx = tuple(2.0 / n for n in shape)
+    ob = O.Problem(shape, dx, 1.0, 10.0, 0.0)
+    c, g = O.shift_scale(O.spectrum_bound(ob))
+    dt = 10 * min(W.dt_cfl(n, 10.0) for n in shape)
+    ls = [0, 1, 3]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    arg = json.dumps({"dt": dt, "c": c, "g": g, "ls": ls, "tol": TOL})
+    r = subprocess.run([sys.executable, root + "/tools/ipc_slab_check.py", arg], capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    ranks = sorted(json.loads(r.stdout.strip().splitlines()[-1])["ranks"], key=lambda x: x["rank"])
+    assert [x["ipp"] for x in ranks] == [2, 2]
+    v = W.ic_random(shape, seed=51, amp=0.2)
+    pb = lx.Problem(shape, dx, 1.0, 10.0, 0.0)
+    with lx.Context(pb) as ctx1:
+        ctx1.set_kernel(2)
+        for idx, l in enumerate(ls):
+            full = np.concatenate([np.array(x["res"][idx][1]) for x in ranks], axis=0)
+            ref = O.real_leja_phi(ob, v, dt, c, g, l, TOL, TOL, xi300)
+            assert {x["res"][idx][0] for x in ranks} == {ref.iters}
+            assert np.linalg.norm(full - ref.outs[0]) <= TOL * np.linalg.norm(ref.outs[0])
+            one = torch.empty(shape, dtype=torch.float64, device="cuda")
+            lx.lx_real_leja_phi(ctx1, torch.from_numpy(v).cuda(), one, dt, c, g, l, TOL, TOL)
+            np.testing.assert_array_equal(full, one.cpu().numpy())

@@ -1,8 +1,11 @@
 #!/usr/bin/env python
-"""Exercise the NCCL slab transport on ONE GPU: a world of size 1 over torch.distributed/NCCL, the library's
-own communicator (halo send/recv to itself as both neighbours, allgather of the per-rank partials).
+"""Exercise the NCCL-created slab communicator on ONE GPU: a world of size 1 over torch.distributed/NCCL with
+LX_COMM_FORCE (the library's own communicator with itself as both neighbours).  Mode "nccl": Leja calls run
+the peer-memory slab kernel (exchange block handles gathered over NCCL), stage operations the NCCL step
+protocol; mode "nccl_nopeer" (LX_COMM_NO_PEER): every Leja iteration through step kernels + NCCL groups.
 Compares a Leja call, an EXPRB43 step and the Gershgorin bound with the single-domain path: identical
-iteration counts, fields equal to 1e-13 (only the norm summation order differs).  Prints one JSON line."""
+iteration counts, fields equal to 1e-13 (only the norm summation order differs).  --time: per-iteration
+cost of the three paths at 4096^2 (config 1 shape).  Prints one JSON line."""
 import json
 import os
 import sys
@@ -29,10 +32,12 @@ def main():
     u = torch.from_numpy(W.ic_allen_cahn_2d(n)).cuda()
     v = torch.from_numpy(W.ic_random((n, n), seed=3, amp=0.2)).cuda()
     res = {}
-    for mode in ("single", "nccl"):
+    modes = {"single": None, "nccl": lx.LX_COMM_FORCE, "nccl_nopeer": lx.LX_COMM_FORCE | lx.LX_COMM_NO_PEER}
+    for mode, flags in modes.items():
         ctx = lx.Context(pb)
-        if mode == "nccl":
-            lxd.attach(ctx)
+        if flags is not None:
+            lxd.attach(ctx, flags)
+        out["ipp_" + mode] = ctx.iterations_per_pass
         bound = lx.lx_spectrum_bound(ctx, u)
         c, g = lx.lx_shift_scale(bound)
         o = torch.empty_like(u)
@@ -41,25 +46,28 @@ def main():
         its, err = lx.lx_step(ctx, "exprb43", u, lo, hi, 0.01, c, g, 1e-10, 1e-10)
         res[mode] = (bound, it, o.cpu().numpy(), its, err, hi.cpu().numpy())
         ctx.close()
-    a, b = res["single"], res["nccl"]
-    out["bound_equal"] = a[0] == b[0]
-    out["leja_iters"] = [a[1], b[1]]
-    out["leja_maxrel"] = float(np.abs(a[2] - b[2]).max() / np.abs(a[2]).max())
-    out["step_iters"] = [a[3], b[3]]
-    out["step_err"] = [a[4], b[4]]
-    out["step_maxrel"] = float(np.abs(a[5] - b[5]).max() / np.abs(a[5]).max())
-    out["ok"] = bool(out["bound_equal"] and a[1] == b[1] and a[3] == b[3] and out["leja_maxrel"] <= 1e-13
-                     and out["step_maxrel"] <= 1e-13)
+    a = res["single"]
+    ok = out["ipp_nccl"] == 2 and out["ipp_nccl_nopeer"] == 1
+    for mode in ("nccl", "nccl_nopeer"):
+        b = res[mode]
+        out[mode] = {"bound_equal": a[0] == b[0], "leja_iters": [a[1], b[1]],
+                     "leja_maxrel": float(np.abs(a[2] - b[2]).max() / np.abs(a[2]).max()),
+                     "step_iters": [a[3], b[3]], "step_err": [a[4], b[4]],
+                     "step_maxrel": float(np.abs(a[5] - b[5]).max() / np.abs(a[5]).max())}
+        r = out[mode]
+        ok = ok and bool(r["bound_equal"] and a[1] == b[1] and a[3] == b[3] and r["leja_maxrel"] <= 1e-13
+                         and r["step_maxrel"] <= 1e-13)
+    out["ok"] = ok
     if "--time" in sys.argv:
         # per-iteration cost of the slab protocol (step kernels + NCCL halo/allgather, here to itself) vs the
         # single-domain persistent kernel, 4096^2 phi_0 (config 1 shape)
         wl = W.config(1)
         pb = lx.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
         u0 = torch.from_numpy(W.ic_problem1_2d(4096)).cuda()
-        for mode in ("single", "nccl"):
+        for mode, flags in modes.items():
             ctx = lx.Context(pb)
-            if mode == "nccl":
-                lxd.attach(ctx)
+            if flags is not None:
+                lxd.attach(ctx, flags)
             c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
             o = torch.empty_like(u0)
             it = lx.lx_real_leja_phi(ctx, u0, o, wl.dt, c, g, 0, wl.rtol, wl.atol)
@@ -70,8 +78,10 @@ def main():
                 lx.lx_real_leja_phi(ctx, u0, o, wl.dt, c, g, 0, wl.rtol, wl.atol)
             s1.record()
             torch.cuda.synchronize()
-            out["t_" + mode] = {"iters": it, "us_per_iter": s0.elapsed_time(s1) * 1e3 / (5 * it),
-                                "kernel": "two-step persistent" if mode == "single" else "step kernels + NCCL"}
+            kern = {"single": "two-step persistent (single domain)",
+                    "nccl": "two-step persistent slab kernel, peer-memory halos (itself as neighbour)",
+                    "nccl_nopeer": "step kernels + NCCL group per iteration"}[mode]
+            out["t_" + mode] = {"iters": it, "us_per_iter": s0.elapsed_time(s1) * 1e3 / (5 * it), "kernel": kern}
             ctx.close()
     print(json.dumps(out), flush=True)
     dist.destroy_process_group()
