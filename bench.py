@@ -1,24 +1,27 @@
 #!/usr/bin/env python
 """Benchmark of the B200-native LeXInt hot path (BASELINE.json metric).
 
-Workload at N=1 (BASELINE.json configs[1]): 2D linear advection-diffusion on a
-4096^2 periodic grid (nu = 10, Problem-I Gaussian IC), fp64;
-phi_0..phi_3(dt A) u_0 by real Leja interpolation at dt = 10 dt_CFL with
-rtol = atol = 1e-10.  One bench STEP = the whole hot path over that input:
-spectrum bound -> (c, gamma) -> for l in 0..3: divided differences (host) +
-one persistent fused Leja kernel (device-side stopping decision).
+Workloads (`--config`, BASELINE.json configs, 1-based here as in BASELINE.md):
+  1 (default)  2D linear advection-diffusion, 4096^2 periodic grid (nu = 10, Problem-I Gaussian IC,
+               P:562), fp64; one STEP = spectrum bound -> (c, gamma) -> phi_0..phi_3(dt A) u_0 by real
+               Leja interpolation at dt = 10 dt_CFL, rtol = atol = 1e-10 (4 persistent Leja kernels).
+               N>1 (torchrun): WEAK scaling -- each rank owns a 4096-row slab of a (4096 N) x 4096 grid;
+               Leja calls run the persistent slab kernel over peer memory (lexint.h lx_ctx_set_comm).
+  4            2D advection-diffusion, n x n grid (default n = 16384; --n 8192), phi_0 at 10 dt_CFL;
+               N>1: STRONG scaling -- the same grid split into N slabs (slab kernel over peer memory).
+  5            3D advection-diffusion, 512^3, one EPIRK4s3A step per STEP (spectrum bound, vertical
+               phi_1 {1/2, 2/3, 1}, remainders, phi_3, phi_4); N>1: slabs of planes (step protocol).
 
-value   = Leja iterations / s (device-timed, inputs resident in HBM)
-e2e     = same metric through the C-ABI with HOST (pinned) buffers, copies inside
-roofline: dominant kernel k_leja2d_tb2<1,false> (two Leja iterations per HBM pass),
-          algorithmic bytes N*(24 + 32*(ceil(m/2)-1) [+24 if m odd]) per launch
-          (leja_bytes_per_point; one-step schedule: N*(24 + 32*(m-1)))
-          / CUDA-event duration.
-cpu_baseline / --impl reference: the oracle (oracle/) on the host cores.
-
-N>1 (torchrun): weak scaling -- each rank owns a 4096-row slab of a
-(4096*N) x 4096 grid (slab decomposition, NCCL halos + norm allgather); value
-counts 4096^2-equivalent Leja iterations of all ranks.
+value   = the config's metric (Leja it/s, or EPIRK steps/s for config 5), device-timed with CUDA events
+          on the context stream, inputs resident in HBM; N>1: all ranks' work / max-over-ranks time.
+e2e     = the same metric through the C ABI with pinned HOST buffers (lx_real_leja_phi / lx_step on host
+          pointers; the library stages the copies itself: pipelined H2D / kernels / D2H for Leja calls),
+          wall clock, host<->device copies inside the timed region.
+roofline: the dominant kernel (one persistent launch per Leja call): algorithmic bytes per launch
+          (leja_bytes_per_point x points) / its CUDA-event duration vs MEASURED_PEAKS.json.
+cpu_baseline / --impl reference: the oracle (oracle/, plain C) on the host cores -- single-threaded and
+          all cores (OpenMP build, bit-identical) -- on a bounded sample: the per-iteration cost is the
+          difference of a k-iteration and a 1-iteration call (allocation and first-touch cancel).
 """
 from __future__ import annotations
 
@@ -111,52 +114,106 @@ def _dist():
     return ws, rank, local
 
 
-def cpu_baseline(n: int, iters: int = 2, reps: int = 1):
-    """Oracle (as it stands, single-threaded C) on a bounded sample of the workload."""
+def _host_info():
+    info = {"nproc": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core", "NUMA node(s)"):
+                info[k.strip()] = v.strip()
+    except Exception:
+        pass
+    return info
+
+
+# ---------------------------------------------------------------------------------------- oracle samples
+def oracle_iteration_rate(shape, dt, l=0, k_iters=4, coeffs=(1.0,), threads="all"):
+    """Oracle Leja iterations/s on `shape` (Problem-I Gaussian for 2D, 3D Gaussian for 3D), from the
+    difference of a k-iteration call and a 1-iteration call (node caps k+1 and 2): the allocation and
+    first touch of the oracle's work vectors cancel.  threads: 1 (serial build) or "all" (OpenMP build)."""
     import oracle as O
-    wl = W.config(1, n=n)
-    ob = O.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
-    u0 = W.ic_problem1_2d(n)
-    xi = O.leja_points(300)
-    c, g = O.shift_scale(O.spectrum_bound(ob))
-    tot_it, t = 0, 0.0
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        r = O.real_leja_phi(ob, u0, wl.dt, c, g, 0, wl.rtol, wl.atol, xi, max_nodes=iters + 1)
-        t += time.perf_counter() - t0
-        tot_it += r.iters
-    return {"value": tot_it / t, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": "oracle real_leja_phi phi_0 on the full %dx%d grid, first %d Leja iterations "
-                      "(node cap %d) x %d, single-threaded plain C" % (n, n, iters, iters + 1, reps)}
+    O.use_openmp(threads != 1)
+    try:
+        if threads != 1:
+            os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
+        dx = tuple(2.0 / n for n in shape)
+        ob = O.Problem(shape, dx, 1.0, 10.0, 0.0)
+        v = W.ic_problem1_2d(shape[0]) if len(shape) == 2 else W.ic_gaussian_3d(shape[0])
+        xi = O.leja_points(300)
+        c, g = O.shift_scale(O.spectrum_bound(ob))
+        ts = {}
+        for cap in (2, k_iters + 1):
+            t0 = time.perf_counter()
+            r = O.real_leja_phi(ob, v, dt, c, g, l, 1e-10, 1e-10, xi, coeffs=coeffs, max_nodes=cap)
+            ts[cap] = (time.perf_counter() - t0, r.iters)
+        it = ts[k_iters + 1][1] - ts[2][1]
+        t = ts[k_iters + 1][0] - ts[2][0]
+        return it / t, t
+    finally:
+        O.use_openmp(False)
+
+
+def cpu_baseline(cfg_id, wl, scale_points=1.0, unit=UNIT, per_step_iters=None):
+    """cpu_baseline object: oracle on all host cores (primary) and on one core."""
+    sample_shape = wl.shape if cfg_id == 1 else ((4096, 4096) if cfg_id == 4 else (128, 128, 128))
+    ncores = os.cpu_count() or 1
+    k = 4 if cfg_id == 1 else 2
+    res = {}
+    for threads in ("all", 1):
+        rate, secs = oracle_iteration_rate(sample_shape, wl.dt, k_iters=k, threads=threads)
+        npts = float(np.prod(sample_shape))
+        rate_cfg = rate * npts / float(np.prod(wl.shape))    # per-point cost x the config's points
+        if per_step_iters:                                   # config 5: EPIRK steps/s estimate
+            rate_cfg = rate_cfg / per_step_iters
+        res[threads] = (rate_cfg, secs)
+    sample = ("oracle real_leja_phi phi_0 on a %s grid (spacing of the config), per-iteration cost = (t[%d "
+              "iterations] - t[1 iteration]) / %d" % ("x".join(map(str, sample_shape)), k + 1, k))
+    if sample_shape != tuple(wl.shape):
+        sample += ", scaled by points to the %s grid" % "x".join(map(str, wl.shape))
+    if per_step_iters:
+        sample += ", divided by the %d Leja iterations of one step (K = 1 equivalent; stage kernels ignored)" % \
+                  per_step_iters
+    return {"value": res["all"][0], "unit": unit, "cores": ncores, "kind": "oracle",
+            "sample": sample + "; OpenMP build (bit-identical to the serial oracle), %d threads" % ncores,
+            "single_core": {"value": res[1][0], "unit": unit, "cores": 1, "kind": "oracle",
+                            "sample": sample + "; serial build"},
+            "host": _host_info()}
 
 
 def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
         return
-    n = args.n or 4096
-    per_step = args.ref_iters
-    cfg = {"workload": W.config(1, n=n).name, "grid": [n, n], "ls": [0, 1, 2, 3], "dt_cfl_mult": 10.0,
-           "tol": 1e-10, "inputs": "synthetic Problem-I Gaussian IC (P:562)"}
+    cfg_id, wl = _workload(args)
+    unit = "steps/s" if cfg_id == 5 else UNIT
+    per_step = 60 if cfg_id == 5 else None
+    shape = wl.shape if cfg_id == 1 else ((4096, 4096) if cfg_id == 4 else (128, 128, 128))
+    scale = float(np.prod(shape)) / float(np.prod(wl.shape))
     for _ in range(args.warmup):
-        cpu_baseline(n, per_step)
+        oracle_iteration_rate(shape, wl.dt, k_iters=2)
     t0 = time.perf_counter()
-    tot = 0
+    t_iter = 0.0
     for _ in range(args.steps):
-        r = cpu_baseline(n, per_step)
-        tot += per_step
-    dt = time.perf_counter() - t0
-    val = tot / dt
-    out = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
-           "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": r["sample"]},
-           "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        rate, secs = oracle_iteration_rate(shape, wl.dt, k_iters=2)
+        t_iter += secs                     # one iteration per sample (3-iteration call - 1-iteration call)
+    wall = time.perf_counter() - t0
+    val = args.steps / t_iter * scale / (per_step or 1)
+    cpu = cpu_baseline(cfg_id, wl, unit=unit, per_step_iters=per_step) if not args.no_cpu else None
+    out = {"impl": "reference", "metric": METRIC, "value": val, "unit": unit, "n_gpus": ws, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
+           "scaling": "weak" if cfg_id == 1 else "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": {"workload": wl.name, "grid": list(wl.shape)},
+           "cpu_baseline": dict(cpu or {}, value=val),
+           "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "note": "each step: oracle (OpenMP build, all host cores) per-iteration cost from a 2- and a "
+                   "1-iteration call on the sample grid, scaled to the config (see cpu_baseline.sample)"}
     print(json.dumps(out), flush=True)
 
 
+# ---------------------------------------------------------------------------------------- accounting
 def leja_bytes_per_point(m, tb2):
-    """Algorithmic HBM bytes per grid point of one Leja call with m iterations (roofline).
+    """Algorithmic HBM bytes per grid point of one K = 1 Leja call with m iterations.
 
     one-step kernel: iteration 1 reads v, writes y, p (24 B); every later one reads y, p and writes
     y, p (32 B).  two-step kernel (temporal blocking): pass 1 = iterations 1, 2 reads v, writes y, p
@@ -168,216 +225,352 @@ def leja_bytes_per_point(m, tb2):
     return 24 + 32 * (passes - 1) + (24 if m % 2 == 1 else 0)
 
 
+def leja_bytes_per_point_vertical(m_k):
+    """One-pass kernel with K accumulators frozen at iterations m_k (3D): iteration 1 reads v, writes y and
+    the K accumulators (16 + 8K B); iteration m >= 2 reads and writes y (16 B) and every accumulator still
+    active at m (16 B each)."""
+    M = max(m_k)
+    b = 16 + 8 * len(m_k)
+    for m in range(2, M + 1):
+        b += 16 + 16 * sum(1 for mk in m_k if mk >= m)
+    return b
+
+
 def _traffic_from_profiles():
     p = os.path.join(ROOT, "profiles", "leja_traffic.json")
     if os.path.exists(p):
         try:
-            d = json.load(open(p))
-            return d
+            return json.load(open(p))
         except Exception:
             return None
     return None
 
 
-def exprb43_steps(lx, torch, stream, n=2048, warm=2, steps=20):
-    """EXPRB steps/s: Allen-Cahn 2048^2 (config 2 shape), EXPRB43, spectrum (Gershgorin) and
-    (c, gamma) recomputed on the device every step -- lx_integrate, the paper's time loop."""
-    wl = W.config(2, n=n)
+def exprb43_steps(lx, torch, stream):
+    """EXPRB steps/s: Allen-Cahn 2048^2, EXPRB43 over the config's full 100 steps (BASELINE configs[2]),
+    spectrum (Gershgorin) and (c, gamma) recomputed on the device every step -- lx_integrate, the paper's
+    time loop, one asynchronous call; device-timed."""
+    wl = W.config(2)
+    n = wl.shape[0]
+    nsteps = wl.extra["steps"]
     pb = lx.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
     ctx = lx.Context(pb, stream=stream)
-    u = torch.from_numpy(W.ic_allen_cahn_2d(n)).cuda()
-    it_w, _ = lx.lx_integrate(ctx, "exprb43", u, wl.dt, warm, wl.rtol, wl.atol)
+    u0 = torch.from_numpy(W.ic_allen_cahn_2d(n)).cuda()
+    u = u0.clone()
+    lx.lx_integrate(ctx, "exprb43", u, wl.dt, 3, wl.rtol, wl.atol)   # warm-up (3 steps)
+    u.copy_(u0)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     l0 = ctx.launch_count
     a.record(stream)
-    lx.lx_integrate(ctx, "exprb43", u, wl.dt, steps, wl.rtol, wl.atol, sync=False)
+    lx.lx_integrate(ctx, "exprb43", u, wl.dt, nsteps, wl.rtol, wl.atol, sync=False)
     b.record(stream)
     torch.cuda.synchronize()
     its, err = ctx.synchronize()
     ms = a.elapsed_time(b)
     launches = ctx.launch_count - l0
     ctx.close()
-    return {"metric": "EXPRB43 steps/s", "value": steps / (ms * 1e-3), "unit": "steps/s",
-            "workload": wl.name, "grid": [n, n], "steps_timed": steps, "after_steps": warm,
-            "ms_per_step": ms / steps, "leja_iters_timed": its, "leja_iters_per_step": its / steps,
+    return {"metric": "EXPRB43 steps/s", "value": nsteps / (ms * 1e-3), "unit": "steps/s",
+            "workload": wl.name, "grid": [n, n], "steps_timed": nsteps, "from_step": 0,
+            "ms_per_step": ms / nsteps, "leja_iters_timed": its, "leja_iters_per_step": its / nsteps,
             "last_err": err, "gpu_launches": launches,
-            "note": "lx_integrate (one async call): Gershgorin bound + (c, gamma) on the device every step, "
-                    "no host round trips; device-timed"}
+            "note": "the whole 100-step run from u_0 (T = 1): lx_integrate (one async call), Gershgorin bound "
+                    "+ (c, gamma) on the device every step, no host round trips; device-timed"}
 
 
-def run_ours(args):
-    import torch
+def _workload(args):
+    cfg_id = args.config
+    if cfg_id == 1:
+        return 1, W.config(1, n=args.n or None)
+    if cfg_id == 4:
+        return 4, W.config(3, n=args.n or None)
+    if cfg_id == 5:
+        return 5, W.config(4, n=args.n or None)
+    raise SystemExit("--config must be 1, 4 or 5")
 
-    import paper_2310_08344_b200 as lx
 
-    ws, rank, local = _dist()
-    if not torch.cuda.is_available():
-        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
-    torch.cuda.set_device(local)
-    n = args.n or 4096
-    wl = W.config(1, n=n)
-    if ws > 1:
-        import torch.distributed as dist
-        from paper_2310_08344_b200 import dist as lxd
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        # weak scaling: a (n*ws) x n grid at the SAME spacing, Problem-I IC replicated per
-        # slab (x-periodic images) -> every rank does exactly the N=1 work + halos/gathers
+# ---------------------------------------------------------------------------------------- our arm
+class Job:
+    """Distributed setup shared by the configs."""
+
+    def __init__(self, args):
+        import torch
+
+        import paper_2310_08344_b200 as lx
+        self.lx, self.torch = lx, torch
+        self.ws, self.rank, self.local = _dist()
+        if not torch.cuda.is_available():
+            raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+        torch.cuda.set_device(self.local)
+        if self.ws > 1:
+            import torch.distributed as dist
+            from paper_2310_08344_b200 import dist as lxd
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.lxd = lxd
+        self.stream = torch.cuda.Stream()
+        torch.cuda.set_stream(self.stream)
+
+    def context(self, pb):
+        ctx = self.lx.Context(pb, stream=self.stream)
+        if self.ws > 1:
+            self.lxd.attach(ctx)
+        return ctx
+
+    def barrier(self):
+        self.torch.cuda.synchronize()
+        if self.ws > 1:
+            self.torch.distributed.barrier()
+            self.torch.cuda.synchronize()
+
+    def max_ms(self, ms):
+        return self.lxd.max_over_ranks(ms, device=self.torch.device("cuda", self.local)) if self.ws > 1 else ms
+
+    def close(self):
+        if self.ws > 1:
+            self.torch.distributed.barrier()
+            self.torch.distributed.destroy_process_group()
+
+
+def _roofline(kernel, bytes_per_launch, launch_ms, extra=None):
+    peak, peak_kind = _peaks()
+    achieved = float(np.sum(bytes_per_launch) / (np.sum(launch_ms) * 1e-3) / 1e9)
+    tr = _traffic_from_profiles()
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": (tr or {}).get("traffic_bytes_per_launch"), "kernel": kernel,
+            "algorithmic_bytes_per_launch": [float(b) for b in bytes_per_launch],
+            "launch_ms": [float(x) for x in launch_ms],
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (%s)" % peak_kind, "frac_of_8TBs_spec": achieved / 8000.0}
+    roof.update(extra or {})
+    return roof
+
+
+def bench_leja_2d(job, args, cfg_id, wl):
+    """Configs 1 and 4: Leja calls on a 2D grid (config 1: phi_0..phi_3 per step, weak scaling;
+    config 4: phi_0 per step on a fixed grid, strong scaling)."""
+    lx, torch, stream = job.lx, job.torch, job.stream
+    ws = job.ws
+    n = wl.shape[0]
+    ls = [0, 1, 2, 3] if cfg_id == 1 else [0]
+    if cfg_id == 1 and ws > 1:
+        # weak scaling: a (n*ws) x n grid at the SAME spacing, Problem-I IC replicated per slab
+        # (x-periodic images) -> every rank does exactly the N=1 work + the slab protocol
         pb = lx.Problem((n * ws, n), wl.dx, wl.diff, wl.nu, wl.react)
     else:
         pb = lx.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
-    stream = torch.cuda.Stream()
-    torch.cuda.set_stream(stream)
-    ctx = lx.Context(pb, stream=stream)
-    if ws > 1:
-        b, e = lxd.attach(ctx)
-        assert e - b == n, (b, e)
-    u0_h = W.ic_problem1_2d(n)
+    ctx = job.context(pb)
+    b, e, _ = ctx.local()
+    u0_full = W.ic_problem1_2d(n)
+    u0_h = u0_full if cfg_id == 1 else np.ascontiguousarray(u0_full[b:e])
     u0 = torch.from_numpy(u0_h).cuda()
-    outs = [torch.empty_like(u0) for _ in range(4)]
+    outs = [torch.empty_like(u0) for _ in ls]
     N = u0.numel()
+    c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+    iters = [lx.lx_real_leja_phi(ctx, u0, outs[i], wl.dt, c, g, l, wl.rtol, wl.atol) for i, l in enumerate(ls)]
 
     def step(ev=None):
-        bound = lx.lx_spectrum_bound(ctx)
-        c, g = lx.lx_shift_scale(bound)
-        for l in range(4):
+        c2, g2 = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+        for i, l in enumerate(ls):
             if ev is not None:
-                ev[l][0].record(stream)
-            lx.lx_real_leja_phi(ctx, u0, outs[l], wl.dt, c, g, l, wl.rtol, wl.atol, sync=False)
+                ev[i][0].record(stream)
+            lx.lx_real_leja_phi(ctx, u0, outs[i], wl.dt, c2, g2, l, wl.rtol, wl.atol, sync=False)
             if ev is not None:
-                ev[l][1].record(stream)
+                ev[i][1].record(stream)
 
-    # iteration counts per call (untimed, sync)
-    c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
-    iters = [lx.lx_real_leja_phi(ctx, u0, outs[l], wl.dt, c, g, l, wl.rtol, wl.atol) for l in range(4)]
     for _ in range(args.warmup):
         step()
     ctx.synchronize()
-    torch.cuda.synchronize()
-    if ws > 1:
-        torch.distributed.barrier()
-        torch.cuda.synchronize()
-
-    evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in range(4)]
+    job.barrier()
+    evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in ls]
            for _ in range(args.steps)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = ctx.launch_count
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        if ws > 1:
-            torch.distributed.barrier()
-            torch.cuda.synchronize()
+    with ClockSampler(job.local) as clk:
+        job.barrier()
         start.record(stream)
         for s in range(args.steps):
             step(evs[s])
         stop.record(stream)
-        torch.cuda.synchronize()
-        if ws > 1:
-            torch.distributed.barrier()
+        job.barrier()
     launches = ctx.launch_count - launches0
     total_iters, _ = ctx.synchronize()
-    ms = start.elapsed_time(stop)
-    if ws > 1:
-        ms = lxd.max_over_ranks(ms, device=u0.device)
+    ms = job.max_ms(start.elapsed_time(stop))
     assert total_iters == args.steps * sum(iters), (total_iters, iters)
-    value = ws * total_iters / (ms * 1e-3)   # 4096^2-equivalent Leja iterations of all ranks
+    # config 1: 4096^2-equivalent Leja iterations of all ranks; config 4: iterations of the global grid
+    value = (ws if cfg_id == 1 else 1) * total_iters / (ms * 1e-3)
 
-    # roofline of the dominant kernel (persistent Leja kernel, one launch per call)
-    durs = np.array([[evs[s][l][0].elapsed_time(evs[s][l][1]) for l in range(4)] for s in range(args.steps)])
-    tb2 = ctx.iterations_per_pass == 2   # the library's kernel choice for this context (lexint.h)
-    bytes_per_call = np.array([N * leja_bytes_per_point(m, tb2) for m in iters], dtype=np.float64)
+    tb2 = ctx.iterations_per_pass == 2
+    durs = np.array([[evs[s][i][0].elapsed_time(evs[s][i][1]) for i in range(len(ls))] for s in range(args.steps)])
     per_call_ms = durs.mean(axis=0)
-    achieved = float(bytes_per_call.sum() / (per_call_ms.sum() * 1e-3) / 1e9)
-    peak, peak_kind = _peaks()
-    tr = _traffic_from_profiles()
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": (tr or {}).get("traffic_bytes_per_launch"),
-            "kernel": ("k_leja2d_tb2<1,false> (persistent, 2 Leja iterations per HBM pass, 1 launch per call)"
-                       if tb2 else "k_leja2d<1,false> (persistent, 1 launch per Leja call)"),
-            "one_step_equivalent_frac": float(N * sum(leja_bytes_per_point(m, False) for m in iters)
-                                              / (per_call_ms.sum() * 1e-3) / 1e9 / peak),
-            "algorithmic_bytes_per_launch": [float(b) for b in bytes_per_call],
-            "launch_ms": [float(x) for x in per_call_ms],
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs (%s)" % peak_kind,
-            "frac_of_8TBs_spec": achieved / 8000.0,
-            "kernel_share_of_step": float(per_call_ms.sum() / (ms / args.steps))}
+    bytes_per_call = np.array([N * leja_bytes_per_point(m, tb2) for m in iters], dtype=np.float64)
+    kname = ("k_leja2d_tb2<1,false,%s> (persistent, 2 Leja iterations per HBM pass, 1 launch per call%s)"
+             % ("true" if ws > 1 else "false", "; slab kernel over peer memory, per rank" if ws > 1 else "")
+             if tb2 else "k_leja2d<1,false> (persistent, 1 launch per Leja call)")
+    roof = _roofline(kname, bytes_per_call, per_call_ms, {
+        "one_step_equivalent_frac": float(N * sum(leja_bytes_per_point(m, False) for m in iters)
+                                          / (per_call_ms.sum() * 1e-3) / 1e9 / _peaks()[0]),
+        "kernel_share_of_step": float(per_call_ms.sum() / (start.elapsed_time(stop) / args.steps)),
+        "points_per_launch": N})
 
-    # e2e through the public API with the step's input in pinned HOST memory and its results read back to
-    # pinned host memory inside the timed region: per step one H2D of u0 (copy stream), the 4
-    # lx_real_leja_phi calls on the context stream, and a D2H of each phi_l output on a second copy stream
-    # as soon as its call ends (overlapping the next calls; H2D and D2H run full duplex)
-    uh = torch.from_numpy(u0_h).pin_memory()
-    oh = [torch.empty(wl.shape, dtype=torch.float64).pin_memory() for _ in range(4)]
-    ud = torch.empty_like(u0)
-    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-    ev_in = torch.cuda.Event()
-    ev_call = [torch.cuda.Event() for _ in range(4)]
-    ev_read = [torch.cuda.Event() for _ in range(4)]
-    for e in ev_read:
-        e.record(s_out)
+    # e2e through the public API on pinned HOST buffers: every call stages its own H2D (v) and D2H (out)
+    # inside the library (lx_real_leja_phi on host pointers: pipelined copy-in / kernel / copy-out streams)
+    # a stream of inputs: two pinned host input buffers used alternately, so every step's input is a new
+    # host buffer the library must upload (H2D per step), while the D2H of step k's outputs overlaps the
+    # H2D of step k+1 (separate copy engines); one lx_ctx_synchronize at the end
+    uh = [torch.from_numpy(u0_h).pin_memory() for _ in range(2)]
+    oh = [torch.empty(u0_h.shape, dtype=torch.float64).pin_memory() for _ in ls]
     e2e_steps = max(2, min(args.steps, 6))
 
-    def step_e2e():
-        with torch.cuda.stream(s_in):
-            s_in.wait_event(ev_call[3])               # the previous step's last call has read ud
-            ud.copy_(uh, non_blocking=True)
-            ev_in.record(s_in)
-        stream.wait_event(ev_in)
+    def step_host(k):
         c2, g2 = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
-        for l in range(4):
-            stream.wait_event(ev_read[l])             # outs[l] of the previous step has been read back
-            lx.lx_real_leja_phi(ctx, ud, outs[l], wl.dt, c2, g2, l, wl.rtol, wl.atol, sync=False)
-            ev_call[l].record(stream)
-            with torch.cuda.stream(s_out):
-                s_out.wait_event(ev_call[l])
-                oh[l].copy_(outs[l], non_blocking=True)
-                ev_read[l].record(s_out)
+        for i, l in enumerate(ls):
+            lx.lx_real_leja_phi(ctx, uh[k & 1], oh[i], wl.dt, c2, g2, l, wl.rtol, wl.atol, sync=False)
 
-    step_e2e()
+    step_host(0)
+    ctx.synchronize()
+    job.barrier()
+    t0 = time.perf_counter()
+    for k in range(e2e_steps):
+        step_host(k + 1)
+    e_it, _ = ctx.synchronize()   # kernels done and every output's D2H landed
+    e_t = time.perf_counter() - t0
+    assert e_it == e2e_steps * sum(iters), (e_it, iters)
+    for i in range(len(ls)):      # the host buffers hold the step's results
+        assert torch.equal(oh[i], outs[i].cpu())
+    e_t = job.max_ms(e_t * 1e3) * 1e-3
+    e2e = {"value": (ws if cfg_id == 1 else 1) * e_it / e_t, "unit": UNIT,
+           "h2d_bytes_per_step": N * 8, "d2h_bytes_per_step": len(ls) * N * 8, "steps": e2e_steps,
+           "note": "per step and rank: %d asynchronous lx_real_leja_phi calls on a pinned host input (a new "
+                   "buffer every step: two alternate) and pinned host outputs; the library uploads the step's "
+                   "input once (H2D; async calls may not modify it before lx_ctx_synchronize, so the later "
+                   "calls reuse the staged copy) and reads every output back (D2H on a copy-out stream, "
+                   "overlapping the next calls and the next step's H2D); one lx_ctx_synchronize at the end; "
+                   "wall clock" % len(ls)}
+    cfg = {"workload": wl.name, "grid": list(pb.shape), "per_rank_grid": [e - b, n], "ls": ls, "dt_cfl_mult": 10.0,
+           "dt": wl.dt, "tol": 1e-10, "leja_iters_per_call": iters, "leja_iters_per_step": sum(iters),
+           "l2_policy": "inputs larger than L2 (each fp64 vector %.0f MB > 126 MB L2)" % (N * 8 / 1e6)
+           if N * 8 > 126e6 else "per-rank vectors %.0f MB (below the 126 MB L2)" % (N * 8 / 1e6),
+           "inputs": "synthetic Problem-I Gaussian IC (P:562), nu=10" + (" replicated per slab" if cfg_id == 1 and ws > 1 else ""),
+           "parallelism": ("slab%d: persistent slab kernel, halos and norm partials over peer memory" % ws)
+           if ws > 1 else "single GPU"}
+    out = {"value": value, "ms_per_step": ms / args.steps, "scaling": "weak" if cfg_id == 1 else "strong",
+           "config": cfg, "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary()}
+    ctx.close()
+    return out
+
+
+def bench_epirk_3d(job, args, wl):
+    """Config 5: 512^3 3D advection-diffusion, one EPIRK4s3A step per STEP."""
+    lx, torch, stream = job.lx, job.torch, job.stream
+    ws = job.ws
+    n = wl.shape[0]
+    pb = lx.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
+    ctx = job.context(pb)
+    b, e, _ = ctx.local()
+    u_h = np.ascontiguousarray(W.ic_gaussian_3d(n)[b:e])
+    u = torch.from_numpy(u_h).cuda()
+    lo, hi = torch.empty_like(u), torch.empty_like(u)
+    N = u.numel()
+    c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+    it_step, _ = lx.lx_step(ctx, "epirk4s3a", u, lo, hi, wl.dt, c, g, wl.rtol, wl.atol)
+
+    def step():
+        c2, g2 = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+        lx.lx_step(ctx, "epirk4s3a", u, lo, hi, wl.dt, c2, g2, wl.rtol, wl.atol, sync=False)
+
+    for _ in range(args.warmup):
+        step()
+    ctx.synchronize()
+    job.barrier()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.launch_count
+    with ClockSampler(job.local) as clk:
+        job.barrier()
+        start.record(stream)
+        for _ in range(args.steps):
+            step()
+        stop.record(stream)
+        job.barrier()
+    launches = ctx.launch_count - launches0
+    total_iters, _ = ctx.synchronize()
+    ms = job.max_ms(start.elapsed_time(stop))
+    assert total_iters == args.steps * it_step, (total_iters, it_step)
+    value = args.steps / (ms * 1e-3)
+
+    # dominant kernel: the step's vertical phi_1 {1/2, 2/3, 1} call (K = 3) on f(u) dt, timed alone
+    fdt = torch.empty_like(u)
+    lx.lx_rhs(ctx, u, fdt, wl.dt)
+    coeffs = (0.5, 2.0 / 3.0, 1.0)
+    vouts = [torch.empty_like(u) for _ in coeffs]
+    m_k = [lx.lx_real_leja_phi(ctx, fdt, vouts[0], wl.dt * a, c, g, 1, wl.rtol, wl.atol) for a in coeffs]
+    m_v = lx.lx_real_leja_phi_vertical(ctx, fdt, vouts, coeffs, wl.dt, c, g, 1, wl.rtol, wl.atol)
+    assert m_v == max(m_k), (m_v, m_k)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(3)]
+    for ea, eb in evs:
+        ea.record(stream)
+        lx.lx_real_leja_phi_vertical(ctx, fdt, vouts, coeffs, wl.dt, c, g, 1, wl.rtol, wl.atol, sync=False)
+        eb.record(stream)
     torch.cuda.synchronize()
     ctx.synchronize()
-    if ws > 1:
-        torch.distributed.barrier()
+    kms = float(np.mean([ea.elapsed_time(eb) for ea, eb in evs]))
+    kbytes = N * leja_bytes_per_point_vertical(m_k)
+    kname = ("k_leja3d_smem<3,false> (shared-memory plane tiles, 1 launch per Leja call)" if ws == 1 else
+             "k_leja2d_step<3,3,false> (step protocol, one launch per iteration; rank 0)")
+    roof = _roofline(kname, [kbytes], [kms], {"accumulator_iters": m_k,
+                                              "kernel_share_of_step_estimate": kms / (ms / args.steps)})
+
+    # e2e: lx_step on pinned host u / u_low / u_high (the library stages H2D / D2H inside the call)
+    uh = torch.from_numpy(u_h).pin_memory()
+    loh, hih = torch.empty_like(uh).pin_memory(), torch.empty_like(uh).pin_memory()
+    e2e_steps = 2
+    lx.lx_step(ctx, "epirk4s3a", uh, loh, hih, wl.dt, c, g, wl.rtol, wl.atol)
+    job.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        step_e2e()
-    torch.cuda.synchronize()
-    e_t = time.perf_counter() - t0
-    e_it, _ = ctx.synchronize()
-    assert e_it == e2e_steps * sum(iters), (e_it, iters)
-    for l in range(4):   # the read-back results are the step's outputs
-        assert torch.equal(oh[l], outs[l].cpu())
-    if ws > 1:
-        e_t = lxd.max_over_ranks(e_t, device=u0.device)
-    e2e = {"value": ws * e_it / e_t, "unit": UNIT, "h2d_bytes_per_step": N * 8, "d2h_bytes_per_step": 4 * N * 8,
-           "steps": e2e_steps, "note": "per step: H2D of u0 from pinned host memory, 4 lx_real_leja_phi calls, "
-           "D2H of each phi_l output to pinned host memory overlapped with the next call (wall clock)"}
-
-    # secondary metric of BASELINE.json: EXPRB steps/s (config 2 shape: Allen-Cahn 2048^2, EXPRB43,
-    # Gershgorin (c, gamma) recomputed every step).  Single-GPU only.
-    exprb = None
-    if ws == 1 and not args.no_exprb:
-        exprb = exprb43_steps(lx, torch, stream)
-
-    cpu = None
-    if rank == 0 and not args.no_cpu:
-        cpu = cpu_baseline(n, args.ref_iters)
-    cfg = {"workload": wl.name, "grid": list(pb.shape), "per_rank_grid": [n, n], "ls": [0, 1, 2, 3], "dt_cfl_mult": 10.0, "dt": wl.dt,
-           "tol": 1e-10, "leja_iters_per_call": iters, "leja_iters_per_step": sum(iters),
+        c2, g2 = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+        lx.lx_step(ctx, "epirk4s3a", uh, loh, hih, wl.dt, c2, g2, wl.rtol, wl.atol)
+    e_t = job.max_ms((time.perf_counter() - t0) * 1e3) * 1e-3
+    assert torch.equal(hih, hi.cpu())
+    e2e = {"value": e2e_steps / e_t, "unit": "steps/s", "h2d_bytes_per_step": N * 8,
+           "d2h_bytes_per_step": 2 * N * 8, "steps": e2e_steps,
+           "note": "lx_step on pinned host u, u_low, u_high (library staging inside the call), wall clock"}
+    cfg = {"workload": wl.name, "grid": list(wl.shape), "per_rank_grid": [e - b, n, n], "method": "epirk4s3a",
+           "dt": wl.dt, "dt_cfl_mult": 10.0, "tol": 1e-10, "leja_iters_per_step": it_step,
            "l2_policy": "inputs larger than L2 (each fp64 vector %.0f MB > 126 MB L2)" % (N * 8 / 1e6),
-           "inputs": "synthetic Problem-I Gaussian IC (P:562), nu=10" + (" replicated per slab" if ws > 1 else ""),
-           "parallelism": ("slab%d (NCCL halos + partial allgather per Leja iteration)" % ws) if ws > 1 else "single GPU"}
-    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-           "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg, "roofline": roof,
-           "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
-           "exprb43": exprb}
-    if rank == 0:
-        print(json.dumps(out), flush=True)
+           "inputs": "synthetic 3D Gaussian IC, nu=10",
+           "parallelism": ("slab%d (step protocol: NCCL halo + partial allgather per Leja iteration)" % ws)
+           if ws > 1 else "single GPU"}
+    out = {"value": value, "ms_per_step": ms / args.steps, "scaling": "strong", "config": cfg, "roofline": roof,
+           "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(), "unit": "steps/s"}
     ctx.close()
-    if ws > 1:
-        torch.distributed.barrier()
-        torch.distributed.destroy_process_group()
+    return out
+
+
+def run_ours(args):
+    job = Job(args)
+    cfg_id, wl = _workload(args)
+    if cfg_id in (1, 4):
+        res = bench_leja_2d(job, args, cfg_id, wl)
+        unit = UNIT
+    else:
+        res = bench_epirk_3d(job, args, wl)
+        unit = "steps/s"
+    exprb = None
+    if cfg_id == 1 and job.ws == 1 and not args.no_exprb:
+        exprb = exprb43_steps(job.lx, job.torch, job.stream)
+    cpu = None
+    if job.rank == 0 and not args.no_cpu and job.ws == 1:
+        cpu = cpu_baseline(cfg_id, wl, unit=unit, per_step_iters=res["config"].get("leja_iters_per_step")
+                           if cfg_id == 5 else None)
+    out = {"metric": METRIC, "value": res["value"], "unit": unit, "n_gpus": job.ws, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
+           "scaling": res["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": res["config"], "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res["e2e"],
+           "gpu_launches": res["gpu_launches"], "clocks": res["clocks"]}
+    if exprb:
+        out["exprb43"] = exprb
+    if job.rank == 0:
+        print(json.dumps(out), flush=True)
+    job.close()
 
 
 def main():
@@ -386,8 +579,10 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=0, help="grid side override (default 4096)")
-    ap.add_argument("--ref-iters", type=int, default=2, help="oracle Leja iterations per cpu sample")
+    ap.add_argument("--config", type=int, default=1, choices=[1, 4, 5],
+                    help="BASELINE config: 1 = 4096^2 phi_0..3 (default), 4 = 16384^2 phi_0 strong scaling, "
+                         "5 = 512^3 EPIRK4s3A")
+    ap.add_argument("--n", type=int, default=0, help="grid side override")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-exprb", action="store_true")
     args = ap.parse_args()

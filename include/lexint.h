@@ -13,9 +13,16 @@
  *    have to lie contiguous in memory".
  *  - Pointers may be DEVICE pointers (cudaMalloc / torch CUDA tensors, on the
  *    context's device, 16-byte aligned) or HOST pointers (pageable or pinned).
- *    Host data is staged through context-owned device buffers with the copies
- *    on the context stream (the host<->device copies are part of the call).
- *    Mixing host and device pointers in one call is allowed.
+ *    Host data is staged through context-owned device buffers (the
+ *    host<->device copies are part of the call).  Mixing host and device
+ *    pointers in one call is allowed.  Leja calls (lx_real_leja_phi*) whose
+ *    host vectors are all PINNED (cudaHostAlloc / cudaHostRegister / torch
+ *    pin_memory) and whose u_lin is on the device are PIPELINED: H2D on a
+ *    copy-in stream, the kernels on the context stream, D2H on a copy-out
+ *    stream, two staging slots, so consecutive calls overlap their copies
+ *    with each other's kernels; such calls may also be asynchronous (all
+ *    out-pointers NULL) -- the host outputs are valid after
+ *    lx_ctx_synchronize.  Other host-pointer calls are synchronous.
  *  - Ownership: the caller allocates and owns every input and output vector
  *    ("the user has to assign the required amount of memory for
  *    the output vector").  The context owns all scratch (P:307, P:359-407:

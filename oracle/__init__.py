@@ -22,6 +22,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "lxoracle.c")
 _LIB = os.path.join(_HERE, "liblxoracle.so")
+_LIB_OMP = os.path.join(_HERE, "liblxoracle_omp.so")   # same source with -fopenmp (bench cpu_baseline only)
 
 OK, ERR_ARG, ERR_UNSUPPORTED, ERR_NOCONV, ERR_NONFINITE = 0, 1, 4, 5, 6
 METHODS = {"rosenbrock_euler": 0, "exprb32": 1, "exprb43": 2, "epirk4s3a": 3, "exprb42": 4, "epirk5p1": 5, "exprb53s3": 6}
@@ -29,23 +30,35 @@ JAC = {"exact": 0, "fd": 1, "linear_f": 2}     # lxoracle.c OC_JAC_* (black-box 
 
 
 def ensure_built(force: bool = False) -> str:
-    """Compile lxoracle.c -> liblxoracle.so (plain -O2, no FMA contraction)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + ".tmp%d" % os.getpid()
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fPIC", "-shared",
-                               "-o", tmp, _SRC, "-lm"])
-        os.replace(tmp, _LIB)
+    """Compile lxoracle.c -> liblxoracle.so (plain -O2, no FMA contraction) and the OpenMP build
+    liblxoracle_omp.so (same source and flags + -fopenmp; bit-identical results)."""
+    for lib_path, extra in ((_LIB, []), (_LIB_OMP, ["-fopenmp"])):
+        if force or not os.path.exists(lib_path) or os.path.getmtime(lib_path) < os.path.getmtime(_SRC):
+            tmp = lib_path + ".tmp%d" % os.getpid()
+            subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fPIC", "-shared"] + extra +
+                                  ["-o", tmp, _SRC, "-lm"])
+            os.replace(tmp, lib_path)
     return _LIB
 
 
 _lib = None
+_use_omp = False
+
+
+def use_openmp(on: bool = True):
+    """Switch this process to the OpenMP build (bench.py's all-core cpu_baseline / reference arm);
+    results are bit-identical to the serial build."""
+    global _lib, _use_omp
+    if on != _use_omp:
+        _use_omp = on
+        _lib = None
 
 
 def lib():
     global _lib
     if _lib is None:
         ensure_built()
-        L = ctypes.CDLL(_LIB)
+        L = ctypes.CDLL(_LIB_OMP if _use_omp else _LIB)
         dp = ctypes.POINTER(ctypes.c_double)
         L.oc_l2norm_scaled.restype = ctypes.c_double
         L.oc_l2norm_scaled.argtypes = [dp, ctypes.c_long]

@@ -22,6 +22,16 @@
 #include <string.h>
 #include <float.h>
 
+/* Parallel build (bench.py's all-core cpu_baseline only; -fopenmp): the element-wise loops below are
+ * split over threads with `OC_PARFOR` and the pairwise norm evaluates the top 6 levels of its
+ * recursion tree in parallel -- the same tree, so every result is bit-identical to the serial build
+ * (tests/test_oracle_scalar.py checks it).  Without -fopenmp the pragmas vanish. */
+#ifdef _OPENMP
+#define OC_PARFOR _Pragma("omp parallel for schedule(static)")
+#else
+#define OC_PARFOR
+#endif
+
 #define OC_OK 0
 #define OC_ERR_ARG 1
 #define OC_ERR_UNSUPPORTED 4
@@ -44,10 +54,40 @@ static double sumsq_pairwise(const double *x, long lo, long hi)
     return sumsq_pairwise(x, lo, mid) + sumsq_pairwise(x, mid, hi);
 }
 
+#ifdef _OPENMP
+/* leaves of the pairwise recursion at depth 6 (same midpoints as sumsq_pairwise) */
+static void oc_leaves(long lo, long hi, int depth, long *los, long *his, int *k)
+{
+    if (depth == 6) { los[*k] = lo; his[*k] = hi; (*k)++; return; }
+    long mid = lo + (hi - lo) / 2;
+    oc_leaves(lo, mid, depth + 1, los, his, k);
+    oc_leaves(mid, hi, depth + 1, los, his, k);
+}
+static double oc_combine(int depth, const double *leaf, int *k)
+{
+    if (depth == 6) return leaf[(*k)++];
+    double a = oc_combine(depth + 1, leaf, k);
+    double b = oc_combine(depth + 1, leaf, k);
+    return a + b;
+}
+#endif
+
 /* ||x||_2 / sqrt(N): "l2 norm normalised to sqrt(N)" (§2.2). */
 double oc_l2norm_scaled(const double *x, long n)
 {
     if (n <= 0) return 0.0;
+#ifdef _OPENMP
+    if (n >= 4096) {   /* every range above depth 6 has > 8 points: the serial recursion splits there too */
+        long los[64], his[64];
+        double leaf[64];
+        int k = 0;
+        oc_leaves(0, n, 0, los, his, &k);
+        _Pragma("omp parallel for schedule(dynamic)")
+        for (int i = 0; i < 64; i++) leaf[i] = sumsq_pairwise(x, los[i], his[i]);
+        k = 0;
+        return sqrt(oc_combine(0, leaf, &k) / (double)n);
+    }
+#endif
     return sqrt(sumsq_pairwise(x, 0, n) / (double)n);
 }
 
@@ -225,6 +265,7 @@ static double at(const oc_problem *pb, const double *y, long i0, long i1, long i
 static void apply_linear(const oc_problem *pb, const double *y, double *w)
 {
     long n0 = pb->n[0], n1 = pb->n[1], n2 = pb->ndim == 3 ? pb->n[2] : 1;
+    OC_PARFOR
     for (long i0 = 0; i0 < n0; i0++)
         for (long i1 = 0; i1 < n1; i1++)
             for (long i2 = 0; i2 < n2; i2++) {
@@ -278,6 +319,7 @@ void oc_jac_apply_slab(const oc_problem *pb, long n_loc, const double *u, const 
 static void apply_upwind_sum(const oc_problem *pb, const double *w, double *out)
 {
     long n0 = pb->n[0], n1 = pb->n[1], n2 = pb->ndim == 3 ? pb->n[2] : 1;
+    OC_PARFOR
     for (long i0 = 0; i0 < n0; i0++)
         for (long i1 = 0; i1 < n1; i1++)
             for (long i2 = 0; i2 < n2; i2++) {
@@ -327,6 +369,7 @@ void oc_jac_apply(const oc_problem *pb, const double *u, const double *y, double
     apply_linear(pb, y, w);
     if (pb->flux != 0.0) add_flux(pb, u, y, 1.0, w);     /* beta sum_d D_d(u y) */
     if (pb->react != 0.0)
+        OC_PARFOR
         for (long i = 0; i < N; i++) w[i] += pb->react * (1.0 - 3.0 * u[i] * u[i]) * y[i];
 }
 
@@ -535,15 +578,18 @@ int oc_real_leja_phi_ex(const oc_problem *pb, int jac_mode, const double *u_lin,
     }
 
     int active[4] = {0, 0, 0, 0};
+    OC_PARFOR
     for (long i = 0; i < N; i++) y[i] = v[i];
     for (int k = 0; k < K; k++) {
         active[k] = 1;
+        OC_PARFOR
         for (long i = 0; i < N; i++) outs[k][i] = d[(size_t)k * max_nodes + 0] * v[i];
     }
 
     status = OC_ERR_NOCONV;
     for (int m = 1; m < max_nodes; m++) {
         jac_mode_apply(pb, jac_mode, u_lin, f_u, y, w);      /* w = J y */
+        OC_PARFOR
         for (long i = 0; i < N; i++)                         /* Eq. (2) */
             y[i] = (w[i] - c * y[i]) / gamma - xi[m - 1] * y[i];
         double ny = oc_l2norm_scaled(y, N);
@@ -551,6 +597,7 @@ int oc_real_leja_phi_ex(const oc_problem *pb, int jac_mode, const double *u_lin,
         for (int k = 0; k < K; k++) {
             if (!active[k]) continue;
             double dm = d[(size_t)k * max_nodes + m];
+            OC_PARFOR
             for (long i = 0; i < N; i++) outs[k][i] = outs[k][i] + dm * y[i];
             double np = oc_l2norm_scaled(outs[k], N);
             double err = fabs(dm) * ny;

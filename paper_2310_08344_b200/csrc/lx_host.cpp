@@ -97,6 +97,14 @@ struct lx_ctx {
     double* tb2_grp_part = nullptr;       // [cap/32+1][2(1+kMaxK)]
     unsigned* tb2_grp_cnt = nullptr;      // [cap/32+1]
     void* ipc_blk = nullptr;              // exchange block handed out by lx_ctx_ipc_handle (before set_comm_ipc)
+    // pipelined host-buffer staging of Leja calls (pinned host memory): two slots, copy-in / copy-out streams
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    double* pin_in[2] = {};
+    double* pin_out[2][kMaxK] = {};
+    cudaEvent_t ev_in[2] = {}, ev_comp[2] = {}, ev_out[2] = {};
+    int pipe_next = 0;
+    const void* pin_key = nullptr;        // host input staged in pin_in[pin_key_slot], valid until the next
+    int pin_key_slot = 0;                 // synchronisation point (the caller may not modify it before)
     int k3d = 0;                          // 3D single-GPU Leja kernel: 0 = smem marching when n1 % 16 == 0 and
                                           // n2 % 64 == 0 (else warp tiles), 1 = warp tiles (lx_ctx_set_kernel)
     double* cg_dev = nullptr;             // device (c, gamma, bound) of lx_integrate
@@ -118,6 +126,16 @@ static bool is_device_ptr(const void* p) {
         return false;
     }
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static bool is_pinned_host_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
 }
 
 static Stencil make_stencil(const lx_problem* pb) {
@@ -484,6 +502,14 @@ static void free_ctx(lx_ctx* ctx) {
     cudaFree(ctx->vg);
     for (double* p : ctx->S) cudaFree(p);
     for (double* p : ctx->H) cudaFree(p);
+    for (int i = 0; i < 2; i++) {
+        cudaFree(ctx->pin_in[i]);
+        for (double* p : ctx->pin_out[i]) cudaFree(p);
+        for (cudaEvent_t e : {ctx->ev_in[i], ctx->ev_comp[i], ctx->ev_out[i]})
+            if (e) cudaEventDestroy(e);
+    }
+    if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
+    if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
     cudaFree(ctx->partials);
     cudaFree(ctx->tb2_seg_part);
     cudaFree(ctx->tb2_grp_part);
@@ -807,6 +833,8 @@ lx_status lx_ctx_synchronize(lx_ctx* ctx, int* iters_total, double* err_last) {
     LX_TRY(read_record(ctx, 1, &r));
     LX_TRY(reset_record(ctx, 1));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (ctx->s_out) CUDA_TRY(cudaStreamSynchronize(ctx->s_out));   // pipelined host outputs landed
+    ctx->pin_key = nullptr;                                         // host inputs may change from here on
     if (iters_total) *iters_total = r.iters;
     if (err_last) *err_last = r.err;
     return status_of(r);
@@ -826,6 +854,80 @@ lx_status lx_ctx_set_kernel(lx_ctx* ctx, int iterations_per_pass, int kernel3d) 
 }
 
 // ---------------------------------------------------------------- Leja
+// Pipelined host staging of Leja calls (pinned host buffers): slot i & 1 of a two-slot ring.
+//   copy-in stream : wait "kernel of call i-2 done with slot" -> H2D v -> event in[slot]
+//   context stream : wait in[slot], wait "D2H of call i-2 done" -> Leja kernel(s) -> event comp[slot]
+//   copy-out stream: wait comp[slot] -> D2H outputs -> event out[slot]
+// so consecutive calls overlap their copies with each other's kernels (H2D and D2H use separate copy
+// engines).  A call with iters_out waits for its own outputs; an asynchronous call (iters_out NULL)
+// returns at once -- the caller must not touch its host buffers before lx_ctx_synchronize.
+static lx_status leja_pipelined(lx_ctx* ctx, const lx_problem* pb, const double* ud, const double* v,
+                                double* const* outs, const double* coeffs, int K, double dt, double c, double gamma,
+                                int l, double rtol, double atol, int* iters_out) {
+    const size_t bytes = ctx->N_loc * sizeof(double);
+    if (!ctx->s_in) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&ctx->s_in, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&ctx->s_out, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; i++) {
+            CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_in[i], cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_comp[i], cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_out[i], cudaEventDisableTiming));
+            CUDA_TRY(cudaEventRecord(ctx->ev_comp[i], ctx->stream));
+            CUDA_TRY(cudaEventRecord(ctx->ev_out[i], ctx->s_out));
+        }
+    }
+    const int sl = ctx->pipe_next;
+    ctx->pipe_next ^= 1;
+    const bool vhost = !is_device_ptr(v);
+    const double* vd = v;
+    if (vhost && ctx->pin_key == v) {
+        // the same host input as an earlier asynchronous call since the last synchronisation point: the
+        // caller may not modify it before lx_ctx_synchronize (lexint.h), so its staged copy is reused
+        const int ks = ctx->pin_key_slot;
+        CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_in[ks], 0));
+        vd = ctx->pin_in[ks];
+    } else if (vhost) {
+        int is = sl;
+        if (ctx->pin_key && ctx->pin_key_slot == is) is ^= 1;   // keep a cached input in place
+        if (!ctx->pin_in[is]) CUDA_TRY(cudaMalloc(&ctx->pin_in[is], bytes));
+        CUDA_TRY(cudaStreamWaitEvent(ctx->s_in, ctx->ev_comp[is], 0));
+        CUDA_TRY(cudaMemcpyAsync(ctx->pin_in[is], v, bytes, cudaMemcpyHostToDevice, ctx->s_in));
+        CUDA_TRY(cudaEventRecord(ctx->ev_in[is], ctx->s_in));
+        CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_in[is], 0));
+        vd = ctx->pin_in[is];
+        ctx->pin_key = v;
+        ctx->pin_key_slot = is;
+    }
+    double* od[kMaxK];
+    bool ohost[kMaxK];
+    for (int k = 0; k < K; k++) {
+        ohost[k] = !is_device_ptr(outs[k]);
+        od[k] = outs[k];
+        if (ohost[k]) {
+            if (!ctx->pin_out[sl][k]) CUDA_TRY(cudaMalloc(&ctx->pin_out[sl][k], bytes));
+            od[k] = ctx->pin_out[sl][k];
+        }
+    }
+    CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_out[sl], 0));
+    const bool sync = iters_out != nullptr;
+    const int rec = sync ? 0 : 1;
+    if (sync) LX_TRY(reset_record(ctx, 0));
+    LX_TRY(leja_device(ctx, pb, ud, vd, od, coeffs, K, dt, c, gamma, l, rtol, atol, rec));
+    CUDA_TRY(cudaEventRecord(ctx->ev_comp[sl], ctx->stream));
+    if (vhost) CUDA_TRY(cudaEventRecord(ctx->ev_comp[ctx->pin_key_slot], ctx->stream));   // input slot in use
+    CUDA_TRY(cudaStreamWaitEvent(ctx->s_out, ctx->ev_comp[sl], 0));
+    for (int k = 0; k < K; k++)
+        if (ohost[k]) CUDA_TRY(cudaMemcpyAsync(outs[k], od[k], bytes, cudaMemcpyDeviceToHost, ctx->s_out));
+    CUDA_TRY(cudaEventRecord(ctx->ev_out[sl], ctx->s_out));
+    if (!sync) return LX_OK;
+    ctx->pin_key = nullptr;   // synchronous call: the caller may modify its buffers after it returns
+    CUDA_TRY(cudaEventSynchronize(ctx->ev_out[sl]));
+    Record r;
+    LX_TRY(read_record(ctx, 0, &r));
+    *iters_out = r.iters;
+    return status_of(r);
+}
+
 lx_status lx_real_leja_phi_vertical(lx_ctx* ctx, const lx_problem* pb, const double* u_lin, const double* v,
                                     double* const* outs, const double* coeffs, int K, double dt, double c,
                                     double gamma, int l, double rtol, double atol, int* iters_out) {
@@ -833,6 +935,18 @@ lx_status lx_real_leja_phi_vertical(lx_ctx* ctx, const lx_problem* pb, const dou
     LX_TRY(check_problem(ctx, pb));
     LX_TRY(validate_leja(pb, u_lin, v, outs, coeffs, K, dt, gamma, l));
     if (pb->react == 0.0 && pb->flux == 0.0) u_lin = nullptr;
+    {
+        // host buffers in PINNED memory (v and/or outputs; u_lin on the device): pipelined staging --
+        // the H2D of this call, the kernels of the previous one and the D2H of the one before overlap
+        bool host = !is_device_ptr(v), pinned = !host || is_pinned_host_ptr(v);
+        for (int k = 0; k < K; k++) {
+            const bool h = !is_device_ptr(outs[k]);
+            host = host || h;
+            pinned = pinned && (!h || is_pinned_host_ptr(outs[k]));
+        }
+        if (host && pinned && (!u_lin || is_device_ptr(u_lin)))
+            return leja_pipelined(ctx, pb, u_lin, v, outs, coeffs, K, dt, c, gamma, l, rtol, atol, iters_out);
+    }
     Staging sg(ctx);
     const double *vd, *ud;
     double* od[kMaxK];

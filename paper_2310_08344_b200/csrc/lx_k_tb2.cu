@@ -106,7 +106,6 @@ __device__ __forceinline__ void strip2d_tb2(const LejaParams& P, const Tb2Pass& 
     constexpr int KK = K > 0 ? K : 1;
     double2 aw[RT + 4], yw[RT + 3], uw[RT + 2];
     const double2 z2 = make_double2(0.0, 0.0);
-    bool halo = false;
     // prime the ring: chunks cbeg .. cbeg+D-2
 #pragma unroll
     for (int d = 0; d < D - 1; d++) {
@@ -179,16 +178,6 @@ __device__ __forceinline__ void strip2d_tb2(const LejaParams& P, const Tb2Pass& 
                     if (outl) {
                         const size_t off = (size_t)(i0 + t) * n1 + j;
                         st2(T.dst + off, zz);
-                        if (SLAB) {
-                            const int r = i0 + t;
-                            if (r < 4) {
-                                st2(T.hup + (size_t)(2 + r) * n1 + j, zz);
-                                halo = true;
-                            } else if (r >= n - 2) {
-                                st2(T.hdn + (size_t)(r - n + 2) * n1 + j, zz);
-                                halo = true;
-                            }
-                        }
                         acc[0] = fma(yc.y, yc.y, fma(yc.x, yc.x, acc[0]));
                         if (TWO) acc[1 + K] = fma(zz.y, zz.y, fma(zz.x, zz.x, acc[1 + K]));
                         const double2 yprev = aw[t];   // y_{m-1} (= v on the first pass)
@@ -233,7 +222,28 @@ __device__ __forceinline__ void strip2d_tb2(const LejaParams& P, const Tb2Pass& 
         }
     }
     cp_async_wait<0>();
-    if (SLAB && halo) __threadfence_system();   // peer ghost rows visible before this CTA's barrier arrival
+    if (SLAB) {
+        // boundary rows 0..3 / n-2, n-1 of y_{m+1} this strip wrote -> the neighbours' ghost blocks (peer
+        // stores of rows this warp just stored itself: L2 hits), then a system-scope fence so they are
+        // visible before this CTA's barrier arrival (outside the streaming loop: no per-row branches there)
+        const int b = cbeg / nc;
+        const int r0 = (cbeg - b * nc) * RT, r1 = min(n, (cend - b * nc) * RT);
+        const int jraw = b * kBand2 - 2 + 2 * lane;
+        const bool outl = lane >= 1 && lane <= 30 && jraw < n1 && jraw < b * kBand2 + kBand2;
+        bool halo = false;
+        for (int r = r0; r < r1; r++) {
+            if (r >= 4 && r < n - 2) {
+                r = n - 3;   // skip to the last two rows
+                continue;
+            }
+            if (outl) {
+                const double2 v = ld2(T.dst + (size_t)r * n1 + jraw);
+                st2((r < 4 ? T.hup + (size_t)(2 + r) * n1 : T.hdn + (size_t)(r - n + 2) * n1) + jraw, v);
+            }
+            halo = true;
+        }
+        if (halo) __threadfence_system();
+    }
 }
 
 // the four (first pass, two iterations) instantiations of strip2d_tb2

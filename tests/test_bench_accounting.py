@@ -44,3 +44,20 @@ def test_config1_bytes_per_step():
     assert one == 8 * (3 + 4 * 15) + 8 * (3 + 4 * 15) + 8 * (3 + 4 * 13) + 8 * (3 + 4 * 9)
     assert two == 8 * (3 + 4 * 7) * 2 + 8 * (3 + 4 * 6) + 8 * (3 + 4 * 4)
     assert 2.0 < one / two < 2.1        # two iterations per pass (and the first pass reads v only)
+
+
+def _passes_vertical(m_k):
+    # one pass per iteration; iteration 1 reads v and writes y and every accumulator; iteration m >= 2
+    # reads/writes y and every accumulator still active at m (converged at m_k >= m)
+    traffic = 0
+    for m in range(1, max(m_k) + 1):
+        if m == 1:
+            traffic += 8 * (1 + 1 + len(m_k))
+        else:
+            traffic += 8 * 2 + 16 * sum(1 for mk in m_k if mk >= m)
+    return traffic
+
+
+@pytest.mark.parametrize("m_k", [(1,), (5, 7, 9), (13, 14, 16), (3, 3)])
+def test_vertical_bytes_match_pass_model(m_k):
+    assert bench.leja_bytes_per_point_vertical(list(m_k)) == _passes_vertical(m_k)

@@ -614,3 +614,33 @@ def test_3d_real_leja_limit_noconv(xi300):
         out = torch.empty(shape, dtype=torch.float64, device="cuda")
         it = _expect_status(lambda: lx.lx_real_leja_phi(ctx, _dev(v), out, dt, c, g, 0, TOL, TOL), lx.LX_ERR_NOCONV)
     assert (r.status, r.iters) == (O.ERR_NOCONV, it) == (O.ERR_NOCONV, 299)
+
+
+def test_pinned_host_pipelined_leja_calls(xi300):
+    # lexint.h: Leja calls on PINNED host buffers are pipelined (copy-in / kernel / copy-out streams); async
+    # calls reuse a staged input until lx_ctx_synchronize; outputs equal the device-pointer results bitwise
+    n = 256
+    pb, ob = _pair((n, n))
+    dt = 10 * W.dt_cfl(n, 10.0)
+    v = torch.from_numpy(W.ic_random((n, n), seed=61, amp=0.3)).pin_memory()
+    outs = [torch.full((n, n), float("nan"), dtype=torch.float64).pin_memory() for _ in range(4)]
+    with lx.Context(pb) as ctx:
+        c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+        ref = []
+        for l in range(4):
+            o = torch.empty((n, n), dtype=torch.float64, device="cuda")
+            ref.append((lx.lx_real_leja_phi(ctx, v.cuda(), o, dt, c, g, l, TOL, TOL), o.cpu()))
+        for rnd in range(2):
+            for l in range(4):
+                lx.lx_real_leja_phi(ctx, v, outs[l], dt, c, g, l, TOL, TOL, sync=False)
+            its, _ = ctx.synchronize()
+            assert its == sum(r[0] for r in ref)
+            for l in range(4):
+                assert torch.equal(outs[l], ref[l][1]), (rnd, l)
+        v.mul_(0.5)                       # after the synchronize the caller may change v: no stale copy
+        it = lx.lx_real_leja_phi(ctx, v, outs[0], dt, c, g, 0, TOL, TOL)
+        o = torch.empty((n, n), dtype=torch.float64, device="cuda")
+        it2 = lx.lx_real_leja_phi(ctx, v.cuda(), o, dt, c, g, 0, TOL, TOL)
+        assert it == it2 and torch.equal(outs[0], o.cpu())
+    r = O.real_leja_phi(ob, v.numpy(), dt, c, g, 0, TOL, TOL, xi300)
+    assert r.iters == it and _rel(outs[0], r.outs[0]) <= TOL

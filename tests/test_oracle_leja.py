@@ -442,3 +442,24 @@ def test_leja_3d_real_leja_limit(xi300):
     m_exact, _ = refs.spectral_leja_iters(sym, v, dt, c, g, 0, 1e-10, 1e-10, xi300, d=d_mp, max_nodes=300)
     m_fp64, _ = refs.spectral_leja_iters(sym, v, dt, c, g, 0, 1e-10, 1e-10, xi300, d=d_64, max_nodes=300)
     assert m_exact == 38 and m_fp64 is None
+
+
+def test_openmp_oracle_build_is_bit_identical(xi300):
+    # bench.py's all-core cpu_baseline times liblxoracle_omp.so: the same source with -fopenmp (element-wise
+    # loops split over threads, the pairwise norm's top recursion levels in parallel over the SAME tree) --
+    # it must compute exactly what the serial oracle computes
+    n = 128
+    pb = _advdiff(n)
+    c, g = _cg(pb)
+    v = W.ic_random((n, n), seed=8, amp=0.3)
+    res = []
+    try:
+        for omp in (False, True):
+            O.use_openmp(omp)
+            r = O.real_leja_phi(pb, v, 10 * W.dt_cfl(n, 10.0), c, g, 1, 1e-10, 1e-10, xi300, coeffs=(0.5, 1.0))
+            res.append((r.iters, r.outs, O.l2norm_scaled(v)))
+    finally:
+        O.use_openmp(False)
+    assert res[0][0] == res[1][0] and res[0][2] == res[1][2]
+    for a, b in zip(res[0][1], res[1][1]):
+        np.testing.assert_array_equal(a, b)
