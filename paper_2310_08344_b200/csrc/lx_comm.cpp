@@ -315,9 +315,16 @@ struct Comm {
 static constexpr size_t kXHdrBytes = 4096;
 static_assert(sizeof(XHdr) <= kXHdrBytes, "exchange header");
 
-static size_t blk_bytes(long long row) { return kXHdrBytes + 4 * 6 * (size_t)row * sizeof(double); }
+// exchange block: XHdr | ghost blocks (6 rows each) of Y[0], Y[1], v, u | band flags fl_up[nbmax], fl_dn[nbmax]
+static size_t blk_nbmax(long long row) { return (size_t)(row / kBand2 + 2); }
+static size_t blk_bytes(long long row) {
+    return kXHdrBytes + 4 * 6 * (size_t)row * sizeof(double) + 2 * blk_nbmax(row) * sizeof(unsigned);
+}
 static double* blk_ghost(void* b, long long row, int which) {   // 0, 1: Y[i]; 2: v; 3: u
     return (double*)((char*)b + kXHdrBytes) + (size_t)which * 6 * row;
+}
+static unsigned* blk_flags(void* b, long long row, int dir) {   // 0: fl_up, 1: fl_dn
+    return (unsigned*)((char*)b + kXHdrBytes + 4 * 6 * (size_t)row * sizeof(double)) + (size_t)dir * blk_nbmax(row);
 }
 
 static int comm_alloc(Comm* c) {
@@ -563,6 +570,10 @@ void comm_peer_params(const Comm* c, LejaParams& P, bool diag) {
     P.hdn_v = blk_ghost(c->blks[dn], c->row, 2);
     P.hup_u = blk_ghost(c->blks[up], c->row, 3);
     P.hdn_u = blk_ghost(c->blks[dn], c->row, 3);
+    P.fl_up = blk_flags(c->blk, c->row, 0);
+    P.fl_dn = blk_flags(c->blk, c->row, 1);
+    P.fl_up_dn = blk_flags(c->blks[dn], c->row, 0);
+    P.fl_dn_up = blk_flags(c->blks[up], c->row, 1);
     P.timeout_ns = c->timeout_ns;
 }
 

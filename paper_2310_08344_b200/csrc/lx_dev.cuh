@@ -819,20 +819,16 @@ __device__ __forceinline__ void barrier_decide(const LejaParams& P, int m, unsig
 // stencil of the constant-coefficient operator at the two columns of a lane (same order as tile2d)
 __device__ __forceinline__ void stencil2(const Stencil& S, const double2 yc, const double2 up, const double2 dn1,
                                          const double2 dn2, double left, double r1, double r2, double& ax, double& ay) {
-    ax = S.c0 * yc.x;
-    ax = fma(S.m1[0], up.x, ax);
-    ax = fma(S.p1[0], dn1.x, ax);
-    ax = fma(S.p2[0], dn2.x, ax);
-    ax = fma(S.m1[1], left, ax);
-    ax = fma(S.p1[1], yc.y, ax);
-    ax = fma(S.p2[1], r1, ax);
-    ay = S.c0 * yc.y;
-    ay = fma(S.m1[0], up.y, ay);
-    ay = fma(S.p1[0], dn1.y, ay);
-    ay = fma(S.p2[0], dn2.y, ay);
-    ay = fma(S.m1[1], yc.x, ay);
-    ay = fma(S.p1[1], r1, ay);
-    ay = fma(S.p2[1], r2, ay);
+    // the 7 stencil terms summed as a short tree (dependent FMA chain 4 deep instead of 7: the two-step
+    // kernel is latency-bound on this chain), the same order in every kernel that uses it
+    const double ax0 = fma(S.m1[0], up.x, S.c0 * yc.x);
+    const double ax1 = fma(S.p2[0], dn2.x, S.p1[0] * dn1.x);
+    const double ax2 = fma(S.p1[1], yc.y, S.m1[1] * left);
+    ax = (ax0 + ax1) + fma(S.p2[1], r1, ax2);
+    const double ay0 = fma(S.m1[0], up.y, S.c0 * yc.y);
+    const double ay1 = fma(S.p2[0], dn2.y, S.p1[0] * dn1.y);
+    const double ay2 = fma(S.p1[1], r1, S.m1[1] * yc.x);
+    ay = (ay0 + ay1) + fma(S.p2[1], r2, ay2);
 }
 
 // y_m = alpha (A + diag) y_{m-1} + beta y_{m-1} at one row of the lane's two columns.
@@ -887,6 +883,17 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 }
 __device__ __forceinline__ void st_release_sys64(unsigned long long* p, unsigned long long v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed32(unsigned* p, unsigned v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_sys32(unsigned* p, unsigned v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_sys32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
 }
 __device__ __forceinline__ unsigned long long ld_acquire_sys64(const unsigned long long* p) {
     unsigned long long v;

@@ -93,9 +93,12 @@ struct lx_ctx {
     int tblock = 0;                       // 2D single-GPU: Leja iterations per HBM pass (lx_ctx_set_kernel:
                                           // 1 or 2; 0 = auto: two-step from kTb2MinPoints local points on)
     int tb2_cap = 0;                      // segments the buffers below can hold
-    double* tb2_seg_part = nullptr;       // [cap][2(1+kMaxK)]
-    double* tb2_grp_part = nullptr;       // [cap/32+1][2(1+kMaxK)]
-    unsigned* tb2_grp_cnt = nullptr;      // [cap/32+1]
+    Tb2Ctl* tb2_ctl = nullptr;            // pipelined two-step kernel control block (pbase starts at 1)
+    unsigned* tb2_scnt = nullptr;         // [cap] per-segment completion tags
+    double* tb2_pscr[kMaxK] = {};         // p ping-pong scratch halves (one N-vector per accumulator)
+    double* tb2_seg_part = nullptr;       // [2 pass parities][cap][2(1+kMaxK)]
+    double* tb2_grp_part = nullptr;       // [2][cap/32+1][2(1+kMaxK)]
+    unsigned* tb2_grp_cnt = nullptr;      // [2][cap/32+1]
     void* ipc_blk = nullptr;              // exchange block handed out by lx_ctx_ipc_handle (before set_comm_ipc)
     // pipelined host-buffer staging of Leja calls (pinned host memory): two slots, copy-in / copy-out streams
     cudaStream_t s_in = nullptr, s_out = nullptr;
@@ -324,34 +327,65 @@ static LejaParams base_params(lx_ctx* ctx, const lx_problem* pb) {
 // Core Leja call on device pointers (no staging, no sync).
 // Work decomposition of the two-step kernel (single domain and slab): items = (60-column band,
 // RT-row chunk); 32-row segments handed out dynamically, band fastest; per-segment / per-group partials.
+static lx_status tb2_buffers(lx_ctx* ctx, int nseg, int K) {
+    if (!ctx->tb2_ctl) {
+        CUDA_TRY(cudaMalloc(&ctx->tb2_ctl, sizeof(Tb2Ctl)));
+        Tb2Ctl init;
+        std::memset(&init, 0, sizeof init);
+        init.pbase = 1u;   // tags >= 1: the zeroed counters, flags and decision words never match
+        CUDA_TRY(cudaMemcpy(ctx->tb2_ctl, &init, sizeof init, cudaMemcpyHostToDevice));
+    }
+    if (nseg > ctx->tb2_cap) {
+        cudaFree(ctx->tb2_seg_part);
+        cudaFree(ctx->tb2_grp_part);
+        cudaFree(ctx->tb2_grp_cnt);
+        cudaFree(ctx->tb2_scnt);
+        ctx->tb2_seg_part = nullptr;
+        ctx->tb2_grp_part = nullptr;
+        ctx->tb2_grp_cnt = nullptr;
+        ctx->tb2_scnt = nullptr;
+        ctx->tb2_cap = 0;
+        const size_t nv = 2 * (1 + kMaxK), ngrp = (size_t)(nseg + 31) / 32;
+        CUDA_TRY(cudaMalloc(&ctx->tb2_seg_part, 2 * (size_t)nseg * nv * sizeof(double)));
+        CUDA_TRY(cudaMalloc(&ctx->tb2_grp_part, 2 * ngrp * nv * sizeof(double)));
+        CUDA_TRY(cudaMalloc(&ctx->tb2_grp_cnt, 2 * ngrp * sizeof(unsigned)));
+        CUDA_TRY(cudaMalloc(&ctx->tb2_scnt, (size_t)nseg * sizeof(unsigned)));
+        CUDA_TRY(cudaMemsetAsync(ctx->tb2_grp_cnt, 0, 2 * ngrp * sizeof(unsigned), ctx->stream));
+        CUDA_TRY(cudaMemsetAsync(ctx->tb2_scnt, 0, (size_t)nseg * sizeof(unsigned), ctx->stream));
+        ctx->tb2_cap = nseg;
+    }
+    for (int k = 0; k < K; k++)
+        if (!ctx->tb2_pscr[k]) CUDA_TRY(cudaMalloc(&ctx->tb2_pscr[k], ctx->N_loc * sizeof(double)));
+    return LX_OK;
+}
+
+// Work decomposition of the two-step kernel (single domain and slab): items = (60-column band,
+// RT-row chunk); 32-row segments handed out in (pass, segment) order, band fastest; per-segment /
+// per-group partials by pass parity; p ping-pong between the caller's output and context scratch.
 static lx_status tb2_setup(lx_ctx* ctx, LejaParams& P, int K, bool diag) {
     P.nb = (P.n1 + kBand2 - 1) / kBand2;
     P.nrb = (P.n_loc + tb2_rt(K) - 1) / tb2_rt(K);
     P.nunits = P.nb * P.nrb;
     P.grid = leja_tb2_grid_size(ctx->device, K, diag, P.nunits);
     if (ctx->comm) P.grid = comm_grid_cap(ctx->comm, P.grid);
-    P.seg = 32 / tb2_rt(K);
-    P.nseg = P.nb * ((P.nrb + P.seg - 1) / P.seg);
+    P.seg = 32 / tb2_rt(K);   // 32-row segments (measured: 64 rows are 5% slower at 4096^2)
+    // segment rows of 32 rows; a short remainder (< 4 rows) joins the last full one, so that every
+    // segment row has >= 4 rows (the kernel's dependency sets assume it)
+    int nsr = (P.nrb + P.seg - 1) / P.seg;
+    if (nsr > 1 && P.n_loc - (nsr - 1) * P.seg * tb2_rt(K) < 4) nsr--;
+    P.nseg = P.nb * nsr;
     P.ngrp = (P.nseg + 31) / 32;
-    if (P.nseg > ctx->tb2_cap) {
-        cudaFree(ctx->tb2_seg_part);
-    cudaFree(ctx->ipc_blk);
-        cudaFree(ctx->tb2_grp_part);
-        cudaFree(ctx->tb2_grp_cnt);
-        ctx->tb2_seg_part = nullptr;
-        ctx->tb2_grp_part = nullptr;
-        ctx->tb2_grp_cnt = nullptr;
-        ctx->tb2_cap = 0;
-        const size_t nv = 2 * (1 + kMaxK);
-        CUDA_TRY(cudaMalloc(&ctx->tb2_seg_part, (size_t)P.nseg * nv * sizeof(double)));
-        CUDA_TRY(cudaMalloc(&ctx->tb2_grp_part, (size_t)P.ngrp * nv * sizeof(double)));
-        CUDA_TRY(cudaMalloc(&ctx->tb2_grp_cnt, (size_t)P.ngrp * sizeof(unsigned)));
-        CUDA_TRY(cudaMemsetAsync(ctx->tb2_grp_cnt, 0, (size_t)P.ngrp * sizeof(unsigned), ctx->stream));
-        ctx->tb2_cap = P.nseg;
-    }
+    LX_TRY(tb2_buffers(ctx, P.nseg, K));
     P.seg_part = ctx->tb2_seg_part;
     P.grp_part = ctx->tb2_grp_part;
     P.grp_cnt = ctx->tb2_grp_cnt;
+    P.tc = ctx->tb2_ctl;
+    P.scnt = ctx->tb2_scnt;
+    for (int k = 0; k < kMaxK; k++) {
+        P.pp[k][0] = k < K ? P.p[k] : nullptr;
+        P.pp[k][1] = k < K ? ctx->tb2_pscr[k] : nullptr;
+    }
+    if (!P.timeout_ns) P.timeout_ns = 60ull * 1000000000ull;
     return LX_OK;
 }
 
@@ -698,18 +732,7 @@ static lx_status prealloc_slab(lx_ctx* ctx) {
     for (int i = 0; i < kStage; i++)
         if (!scratch(ctx, i)) return fail(LX_ERR_CUDA, "scratch allocation failed");
     const int nb = ((int)ctx->n[1] + kBand2 - 1) / kBand2, nrb = (ctx->n_loc + 1) / 2, seg = 16;
-    const int nseg = nb * ((nrb + seg - 1) / seg), ngrp = (nseg + 31) / 32;
-    if (nseg > ctx->tb2_cap) {
-        cudaFree(ctx->tb2_seg_part);
-        cudaFree(ctx->tb2_grp_part);
-        cudaFree(ctx->tb2_grp_cnt);
-        const size_t nv = 2 * (1 + kMaxK);
-        CUDA_TRY(cudaMalloc(&ctx->tb2_seg_part, (size_t)nseg * nv * sizeof(double)));
-        CUDA_TRY(cudaMalloc(&ctx->tb2_grp_part, (size_t)ngrp * nv * sizeof(double)));
-        CUDA_TRY(cudaMalloc(&ctx->tb2_grp_cnt, (size_t)ngrp * sizeof(unsigned)));
-        CUDA_TRY(cudaMemsetAsync(ctx->tb2_grp_cnt, 0, (size_t)ngrp * sizeof(unsigned), ctx->stream));
-        ctx->tb2_cap = nseg;
-    }
+    LX_TRY(tb2_buffers(ctx, nb * ((nrb + seg - 1) / seg), kMaxK));   // the largest segment count (RT = 2)
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     return LX_OK;
 }

@@ -95,6 +95,28 @@ struct XHdr {
     double part[2][kMaxRanks][kXNV + 2];
 };
 
+// Per-context state of the pipelined two-step kernel (k_leja2d_tb2).  Pass tags are pbase + pass and
+// grow across calls (the leader of each call advances pbase past every tag it used), so no per-call
+// reset of completion counters, flags or decision words is needed.
+struct Tb2Ctl {
+    unsigned ticket;              // next (pass, segment) work item of this call
+    unsigned pbase;               // pass-tag base of the current call (starts at 1)
+    unsigned gdone[2];            // segment groups finished, by pass parity
+    unsigned long long dec[2];    // decision words of the last two passes (tag, status, rb, done, active)
+    unsigned crow;                // Newton-coefficient rows ready (rows < crow)
+    unsigned abort;               // a watchdog fired in this call
+    unsigned arrive, release;     // end-of-call grid barrier
+    unsigned final_tag;           // pbase + the pass whose decision ended the call
+    unsigned snap_final, snap_abort;   // the leader's snapshot for the fix-up
+    unsigned frtag[kMaxK];        // pbase + the pass in which accumulator k froze
+    unsigned frrb[kMaxK];         // ... on the first iteration of that pass (rollback pending)
+    double frd[kMaxK];            // its rollback coefficient d_{m+1}
+    unsigned long long pkey[8];   // ping-pong parity prediction: parameter keys of recent calls ...
+    unsigned pfin[8];             // ... and their final passes
+    unsigned pnext;
+};
+constexpr int kTb2Pred = 8;
+
 struct LejaParams {
     int ndim;
     int n_loc;            // local rows (dim 0)
@@ -156,7 +178,18 @@ struct LejaParams {
     double* hup[2];       // ghost blocks of Y[i] on rank-1 (receive rows 0..3) ...
     double* hdn[2];       // ... and on rank+1 (receive rows n-2, n-1)
     double* hup_v; double* hdn_v; double* hup_u; double* hdn_u;
-    unsigned long long timeout_ns;   // cross-rank wait limit (LX_ERR_TIMEOUT)
+    unsigned long long timeout_ns;   // wait limit of the persistent kernels' watchdogs (LX_ERR_TIMEOUT)
+    // pipelined two-step kernel: control block, per-segment completion tags, p ping-pong halves
+    // (pp[k][0] = the caller's output, pp[k][1] = context scratch), slab band flags (pbase + pass after
+    // the halo rows of that pass landed): fl_up / fl_dn this rank's (deliveries from rank-1 / rank+1),
+    // fl_up_dn = rank+1's fl_up, fl_dn_up = rank-1's fl_dn (this rank signals into them)
+    Tb2Ctl* tc;
+    unsigned* scnt;
+    double* pp[kMaxK][2];
+    unsigned* fl_up;
+    unsigned* fl_dn;
+    unsigned* fl_up_dn;
+    unsigned* fl_dn_up;
 };
 
 // launchers (lx_kernels.cu)

@@ -6,16 +6,29 @@ namespace lx {
 
 // ===========================================================================
 // Temporal blocking: TWO Leja iterations per HBM pass.
-//   pass (m, m+1): read y_{m-1}, p_{m-1};  y_m is formed in registers on a
-//   widened halo (rows i0-1 .. i0+RT+1, columns j0-2 .. j0+61 of a 64-column
-//   warp window whose 60 inner columns are outputs);  y_{m+1} and p_{m+1} are
-//   written.  -> 32 B/pt per TWO iterations (16 B/pt per iteration) and one grid
-//   barrier per two iterations.  Both iterations' norms are reduced, and the
-//   stopping rule of P:155 is applied to m and then m+1 exactly as in the
-//   one-step kernel (same decisions, same iteration counts).  If an accumulator
-//   converges at the first iteration of a pass, its p_{m+1} is rolled back to
-//   p_m = p_{m+1} - d_{m+1} y_{m+1} (<= 1 ulp from the one-step value) in the
-//   next pass, or in a final pointwise pass when the call ends.
+//   pass q = iterations (m, m+1) = (2q+1, 2q+2): read y_{m-1}, p_{m-1}; y_m is formed
+//   in registers on a widened halo (rows i0-1 .. i0+RT+1, columns j0-2 .. j0+61 of a
+//   64-column warp window whose 60 inner columns are outputs); y_{m+1} and p_{m+1}
+//   are written -> 32 B/pt per TWO iterations.  Both iterations' norms are reduced
+//   and the stopping rule of P:155 is applied to m and then m+1 exactly as in the
+//   one-step kernel (same decisions, same iteration counts).
+//
+// Pipelined passes (no grid barrier between passes).  Work = (pass, 32-row x 60-column
+// segment) tickets taken in order from one counter.  A segment of pass q starts when
+//   * pass q-1 has finished on its 3 x 3 neighbour segments (per-segment completion
+//     counters; in a slab, the neighbouring rank's boundary segments signal through
+//     per-band flags in this rank's exchange block after storing their halo rows into
+//     its ghost block), and
+//   * the stopping decision of pass q-2 is known (the decision is LAGGED by one pass:
+//     pass q+1 runs speculatively while pass q is decided; if pass q ends the call,
+//     pass q+1 is discarded -- p ping-pongs between the caller's output and a
+//     scratch vector, so the accepted p_q is never overwritten).
+// The last finisher of a pass sums its per-segment partials in fixed order (and, in a
+// slab, exchanges the per-rank sums through every rank's exchange header) and publishes
+// the decision.  An accumulator that converges on the FIRST iteration of its pass is
+// rolled back, p_m = p_{m+1} - d_{m+1} y_{m+1} (<= 1 ulp from the one-step value),
+// by the pass two later (before it overwrites y_{m+1}) or by the end-of-call fix-up,
+// which also copies results that ended in the scratch half of the ping-pong.
 // ===========================================================================
 // Shared-memory staging of the two-step kernel: per warp a ring of tb2_depth stages, one stage =
 // the global rows one chunk consumes (16 B per lane per row, lane-private: every lane reads back only
@@ -45,18 +58,18 @@ __device__ __forceinline__ const double* tb2_row(const double* base, const doubl
 
 // Per-pass sources / destinations of the two-step kernel
 struct Tb2Pass {
-    const double* src;    // y_{m-1} (v on the first pass)
-    const double* gsrc;   // its ghost block (SLAB)
-    const double* gu;     // ghost block of u (SLAB, DIAG)
-    double* dst;          // y_{m+1}
-    double* hup;          // SLAB: ghost block of rank-1 receiving rows 0..3 of y_{m+1} (its rows n..n+3)
-    double* hdn;          // SLAB: ghost block of rank+1 receiving rows n-2, n-1 (its rows -2, -1)
+    const double* src;            // y_{m-1} (v on the first pass)
+    const double* gsrc;           // its ghost block (SLAB)
+    const double* gu;             // ghost block of u (SLAB, DIAG)
+    double* dst;                  // y_{m+1}
+    const double* pin[kMaxK];     // p_{m-1}^(k) (ping-pong half (q-1) & 1)
+    double* pout[kMaxK];          // p_{m+1}^(k) (half q & 1)
 };
 
 // stage the global rows of chunk ci into ring stage st (every lane: its own 16-byte pieces)
 template <int K, bool DIAG, bool FIRST, bool SLAB>
 __device__ __forceinline__ void tb2_issue(const LejaParams& P, const Tb2Pass& T, double2* __restrict__ ring, int ci,
-                                          int st, int lane, int active, int rbmask) {
+                                          int st, int lane, int active) {
     using L = Tb2Stage<K, DIAG>;
     constexpr int RT = L::RT;
     constexpr int KK = K > 0 ? K : 1;
@@ -74,30 +87,29 @@ __device__ __forceinline__ void tb2_issue(const LejaParams& P, const Tb2Pass& T,
         if (lane == 31) cp_async16(sg + L::H + q, tb2_row<SLAB>(T.src, T.gsrc, i0 + 2 + q, n, n1) + colw(jraw + 2));
         if (DIAG) cp_async16(sg + L::U + q * 32 + lane, tb2_row<SLAB>(P.u, T.gu, i0 + 2 + q, n, n1) + j);
     }
+    if (!FIRST) {
 #pragma unroll
-    for (int t = 0; t < RT; t++) {
+        for (int t = 0; t < RT; t++) {
 #pragma unroll
-        for (int k = 0; k < KK; k++) {
-            const bool need = ((active >> k) & 1) ? !FIRST : (K > 1 && ((rbmask >> k) & 1));
-            if (need) cp_async16(sg + L::PP + (t * K + k) * 32 + lane, P.p[k] + (size_t)wrap(i0 + t) * n1 + j);
+            for (int k = 0; k < KK; k++)
+                if ((active >> k) & 1)
+                    cp_async16(sg + L::PP + (t * K + k) * 32 + lane, T.pin[k] + (size_t)wrap(i0 + t) * n1 + j);
         }
     }
 }
 
-// Temporally blocked pass over a contiguous range [cbeg, cend) of (band, chunk) work items in
-// band-major order (chunk = RT rows of a 60-column band).  A warp marches down its rows with
-// register windows: y_{m-1} rows [i0, i0+RT+4), y_m rows [i0-1, i0+RT+2), u rows [i0, i0+RT+2);
-// per chunk it consumes RT new rows of y_{m-1} (and p, u) staged DEPTH-1 chunks ahead by
-// cp.async, forms RT new rows of y_m (the 3-row halo recomputation happens only at a strip start)
-// and writes RT rows of y_{m+1} and p_{m+1}.  Lanes 1..30 own the band's 60 output columns;
-// lanes 0 and 31 carry halo columns.  Requires n_loc >= 16, n1 >= 64 (host-checked).
-// SLAB: rows 0..3 and n-2, n-1 of y_{m+1} are also stored into the neighbours' ghost blocks (peer
-// memory: the halo exchange overlaps the rest of the pass), followed by a system-scope fence.
+// Temporally blocked pass over a contiguous range [cbeg, cend) of (band, chunk) work items of ONE band
+// (chunk = RT rows of a 60-column band).  A warp marches down its rows with register windows:
+// y_{m-1} rows [i0, i0+RT+4), y_m rows [i0-1, i0+RT+2), u rows [i0, i0+RT+2); per chunk it consumes RT
+// new rows of y_{m-1} (and p, u) staged DEPTH-1 chunks ahead by cp.async, forms RT new rows of y_m
+// (the 3-row halo recomputation happens only at a strip start) and writes RT rows of y_{m+1} and
+// p_{m+1}.  Lanes 1..30 own the band's 60 output columns; lanes 0 and 31 carry halo columns.
+// Requires n_loc >= 16, n1 >= 64 (host-checked).
 template <int K, bool DIAG, bool FIRST, bool TWO, bool SLAB>
 __device__ __forceinline__ void strip2d_tb2(const LejaParams& P, const Tb2Pass& T, int cbeg, int cend, int lane,
                                             double alpha, double b1, double b2, const double* d0, const double* da,
-                                            const double* db, int active, int rbmask, const double* rbd,
-                                            double (&acc)[2 * (1 + K)], double2* __restrict__ ring) {
+                                            const double* db, int active, double (&acc)[2 * (1 + K)],
+                                            double2* __restrict__ ring) {
     using L = Tb2Stage<K, DIAG>;
     constexpr int RT = L::RT, D = L::DEPTH;
     const int n1 = P.n1, n = P.n_loc, nc = P.nrb;
@@ -109,186 +121,146 @@ __device__ __forceinline__ void strip2d_tb2(const LejaParams& P, const Tb2Pass& 
     // prime the ring: chunks cbeg .. cbeg+D-2
 #pragma unroll
     for (int d = 0; d < D - 1; d++) {
-        if (cbeg + d < cend) tb2_issue<K, DIAG, FIRST, SLAB>(P, T, ring, cbeg + d, d, lane, active, rbmask);
+        if (cbeg + d < cend) tb2_issue<K, DIAG, FIRST, SLAB>(P, T, ring, cbeg + d, d, lane, active);
         cp_async_commit();
     }
     int ci = cbeg, st = 0;
-#pragma unroll 1
-    while (ci < cend) {
-        const int b = ci / nc;
-        const int cseg = min(cend, (b + 1) * nc);   // this band's part of the range
-        const int c0 = b * kBand2;
-        const int jraw = c0 - 2 + 2 * lane;
-        const int j = colw(jraw);
-        const int jh = colw(jraw + 2);
-        const bool outl = lane >= 1 && lane <= 30 && jraw < n1 && jraw < c0 + kBand2;
-        {
-            // strip start: y_{m-1} rows i0-2 .. i0+3 (direct loads), y_m rows i0-1 .. i0+1
-            const int i0 = (ci - b * nc) * RT;
-            double2 t6[6], h3[3], u3[3];
+    const int b = ci / nc;
+    const int c0 = b * kBand2;
+    const int jraw = c0 - 2 + 2 * lane;
+    const int j = colw(jraw);
+    const int jh = colw(jraw + 2);
+    const bool outl = lane >= 1 && lane <= 30 && jraw < n1 && jraw < c0 + kBand2;
+    {
+        // strip start: y_{m-1} rows i0-2 .. i0+3 (direct loads), y_m rows i0-1 .. i0+1
+        const int i0 = (ci - b * nc) * RT;
+        double2 t6[6], h3[3], u3[3];
 #pragma unroll
-            for (int q = 0; q < 6; q++) t6[q] = ld2(tb2_row<SLAB>(T.src, T.gsrc, i0 - 2 + q, n, n1) + j);
+        for (int q = 0; q < 6; q++) t6[q] = ld2(tb2_row<SLAB>(T.src, T.gsrc, i0 - 2 + q, n, n1) + j);
 #pragma unroll
-            for (int q = 0; q < 3; q++) {
-                h3[q] = (lane == 31) ? ld2(tb2_row<SLAB>(T.src, T.gsrc, i0 - 1 + q, n, n1) + jh) : z2;
-                u3[q] = DIAG ? ldg2(tb2_row<SLAB>(P.u, T.gu, i0 - 1 + q, n, n1) + j) : z2;
-            }
-#pragma unroll
-            for (int q = 0; q < 3; q++)
-                yw[q] = leja_row<DIAG>(S, alpha, b1, t6[q], t6[q + 1], t6[q + 2], t6[q + 3], h3[q], u3[q], lane);
-#pragma unroll
-            for (int q = 0; q < 4; q++) aw[q] = t6[q + 2];
-            uw[0] = u3[1];
-            uw[1] = u3[2];
+        for (int q = 0; q < 3; q++) {
+            h3[q] = (lane == 31) ? ld2(tb2_row<SLAB>(T.src, T.gsrc, i0 - 1 + q, n, n1) + jh) : z2;
+            u3[q] = DIAG ? ldg2(tb2_row<SLAB>(P.u, T.gu, i0 - 1 + q, n, n1) + j) : z2;
         }
+#pragma unroll
+        for (int q = 0; q < 3; q++)
+            yw[q] = leja_row<DIAG>(S, alpha, b1, t6[q], t6[q + 1], t6[q + 2], t6[q + 3], h3[q], u3[q], lane);
+#pragma unroll
+        for (int q = 0; q < 4; q++) aw[q] = t6[q + 2];
+        uw[0] = u3[1];
+        uw[1] = u3[2];
+    }
 #pragma unroll 1
-        for (int i0 = (ci - b * nc) * RT; ci < cseg; ci++, i0 += RT) {
-            // keep D-1 chunks in flight: stage chunk ci+D-1, then wait for chunk ci's group
-            {
-                int sn = st + D - 1;
-                if (sn >= D) sn -= D;
-                if (ci + D - 1 < cend) tb2_issue<K, DIAG, FIRST, SLAB>(P, T, ring, ci + D - 1, sn, lane, active, rbmask);
-                cp_async_commit();
-                cp_async_wait<D - 1>();
-            }
-            // shared-space loads (ld.shared, not generic): 32-bit address of this stage
-            const uint32_t sgb = smem_u32(ring) + (uint32_t)(st * L::SIZE) * 16u;
-            auto sg = [sgb](int i) { return lds2(sgb + (uint32_t)i * 16u); };
-            if (++st == D) st = 0;
-            const int nout = min(RT, n - i0);
-            double2 ah[RT];
+    for (int i0 = (ci - b * nc) * RT; ci < cend; ci++, i0 += RT) {
+        // keep D-1 chunks in flight: stage chunk ci+D-1, then wait for chunk ci's group
+        {
+            int sn = st + D - 1;
+            if (sn >= D) sn -= D;
+            if (ci + D - 1 < cend) tb2_issue<K, DIAG, FIRST, SLAB>(P, T, ring, ci + D - 1, sn, lane, active);
+            cp_async_commit();
+            cp_async_wait<D - 1>();
+        }
+        // shared-space loads (ld.shared, not generic): 32-bit address of this stage
+        const uint32_t sgb = smem_u32(ring) + (uint32_t)(st * L::SIZE) * 16u;
+        auto sg = [sgb](int i) { return lds2(sgb + (uint32_t)i * 16u); };
+        if (++st == D) st = 0;
+        const int nout = min(RT, n - i0);
+        double2 ah[RT];
 #pragma unroll
-            for (int q = 0; q < RT; q++) {
-                aw[4 + q] = sg(L::Y + q * 32 + lane);
-                ah[q] = (lane == 31) ? sg(L::H + q) : z2;
-                if (DIAG) uw[2 + q] = sg(L::U + q * 32 + lane);
-            }
-            // step 1: y_m rows i0+2 .. i0+RT+1
+        for (int q = 0; q < RT; q++) {
+            aw[4 + q] = sg(L::Y + q * 32 + lane);
+            ah[q] = (lane == 31) ? sg(L::H + q) : z2;
+            if (DIAG) uw[2 + q] = sg(L::U + q * 32 + lane);
+        }
+        // step 1: y_m rows i0+2 .. i0+RT+1
 #pragma unroll
-            for (int q = 0; q < RT; q++)
-                yw[3 + q] = leja_row<DIAG>(S, alpha, b1, aw[1 + q], aw[2 + q], aw[3 + q], aw[4 + q], ah[q],
-                                           DIAG ? uw[2 + q] : z2, lane);
-            // step 2: y_{m+1} on the output rows; p updates and norms
+        for (int q = 0; q < RT; q++)
+            yw[3 + q] = leja_row<DIAG>(S, alpha, b1, aw[1 + q], aw[2 + q], aw[3 + q], aw[4 + q], ah[q],
+                                       DIAG ? uw[2 + q] : z2, lane);
+        // step 2: y_{m+1} on the output rows; p updates and norms
 #pragma unroll
-            for (int t = 0; t < RT; t++) {
-                if (t < nout) {
-                    const double2 yc = yw[t + 1];
-                    double2 zz = yc;
-                    if (TWO) zz = leja_row<DIAG>(S, alpha, b2, yw[t], yc, yw[t + 2], yw[t + 3], z2, uw[t], lane);
-                    if (outl) {
-                        const size_t off = (size_t)(i0 + t) * n1 + j;
-                        st2(T.dst + off, zz);
-                        acc[0] = fma(yc.y, yc.y, fma(yc.x, yc.x, acc[0]));
-                        if (TWO) acc[1 + K] = fma(zz.y, zz.y, fma(zz.x, zz.x, acc[1 + K]));
-                        const double2 yprev = aw[t];   // y_{m-1} (= v on the first pass)
+        for (int t = 0; t < RT; t++) {
+            if (t < nout) {
+                const double2 yc = yw[t + 1];
+                double2 zz = yc;
+                if (TWO) zz = leja_row<DIAG>(S, alpha, b2, yw[t], yc, yw[t + 2], yw[t + 3], z2, uw[t], lane);
+                if (outl) {
+                    const size_t off = (size_t)(i0 + t) * n1 + j;
+                    st2(T.dst + off, zz);
+                    acc[0] = fma(yc.y, yc.y, fma(yc.x, yc.x, acc[0]));
+                    if (TWO) acc[1 + K] = fma(zz.y, zz.y, fma(zz.x, zz.x, acc[1 + K]));
+                    const double2 yprev = aw[t];   // y_{m-1} (= v on the first pass)
 #pragma unroll
-                        for (int k = 0; k < KK; k++) {
-                            if ((active >> k) & 1) {
-                                double2 pm;
-                                if (FIRST) {
-                                    pm.x = fma(da[k], yc.x, d0[k] * yprev.x);
-                                    pm.y = fma(da[k], yc.y, d0[k] * yprev.y);
-                                } else {
-                                    const double2 pv = sg(L::PP + (t * K + k) * 32 + lane);
-                                    pm.x = fma(da[k], yc.x, pv.x);
-                                    pm.y = fma(da[k], yc.y, pv.y);
-                                }
-                                acc[1 + k] = fma(pm.y, pm.y, fma(pm.x, pm.x, acc[1 + k]));
-                                double2 pn = pm;
-                                if (TWO) {
-                                    pn.x = fma(db[k], zz.x, pm.x);
-                                    pn.y = fma(db[k], zz.y, pm.y);
-                                    acc[2 + K + k] = fma(pn.y, pn.y, fma(pn.x, pn.x, acc[2 + K + k]));
-                                }
-                                st2(P.p[k] + off, pn);
-                            } else if (K > 1 && ((rbmask >> k) & 1)) {
-                                // roll back the speculative last update of the previous pass (K = 1: the
-                                // call ends at that decision -> final rollback pass instead)
+                    for (int k = 0; k < KK; k++) {
+                        if ((active >> k) & 1) {
+                            double2 pm;
+                            if (FIRST) {
+                                pm.x = fma(da[k], yc.x, d0[k] * yprev.x);
+                                pm.y = fma(da[k], yc.y, d0[k] * yprev.y);
+                            } else {
                                 const double2 pv = sg(L::PP + (t * K + k) * 32 + lane);
-                                st2(P.p[k] + off, make_double2(fma(-rbd[k], yprev.x, pv.x),
-                                                               fma(-rbd[k], yprev.y, pv.y)));
+                                pm.x = fma(da[k], yc.x, pv.x);
+                                pm.y = fma(da[k], yc.y, pv.y);
                             }
+                            acc[1 + k] = fma(pm.y, pm.y, fma(pm.x, pm.x, acc[1 + k]));
+                            double2 pn = pm;
+                            if (TWO) {
+                                pn.x = fma(db[k], zz.x, pm.x);
+                                pn.y = fma(db[k], zz.y, pm.y);
+                                acc[2 + K + k] = fma(pn.y, pn.y, fma(pn.x, pn.x, acc[2 + K + k]));
+                            }
+                            st2(T.pout[k] + off, pn);
                         }
                     }
                 }
             }
-            // advance the windows by RT rows
-#pragma unroll
-            for (int q = 0; q < 4; q++) aw[q] = aw[RT + q];
-#pragma unroll
-            for (int q = 0; q < 3; q++) yw[q] = yw[RT + q];
-#pragma unroll
-            for (int q = 0; q < 2; q++) uw[q] = uw[RT + q];
         }
+        // advance the windows by RT rows
+#pragma unroll
+        for (int q = 0; q < 4; q++) aw[q] = aw[RT + q];
+#pragma unroll
+        for (int q = 0; q < 3; q++) yw[q] = yw[RT + q];
+#pragma unroll
+        for (int q = 0; q < 2; q++) uw[q] = uw[RT + q];
     }
     cp_async_wait<0>();
-    if (SLAB) {
-        // boundary rows 0..3 / n-2, n-1 of y_{m+1} this strip wrote -> the neighbours' ghost blocks (peer
-        // stores of rows this warp just stored itself: L2 hits), then a system-scope fence so they are
-        // visible before this CTA's barrier arrival (outside the streaming loop: no per-row branches there)
-        const int b = cbeg / nc;
-        const int r0 = (cbeg - b * nc) * RT, r1 = min(n, (cend - b * nc) * RT);
-        const int jraw = b * kBand2 - 2 + 2 * lane;
-        const bool outl = lane >= 1 && lane <= 30 && jraw < n1 && jraw < b * kBand2 + kBand2;
-        bool halo = false;
-        for (int r = r0; r < r1; r++) {
-            if (r >= 4 && r < n - 2) {
-                r = n - 3;   // skip to the last two rows
-                continue;
-            }
-            if (outl) {
-                const double2 v = ld2(T.dst + (size_t)r * n1 + jraw);
-                st2((r < 4 ? T.hup + (size_t)(2 + r) * n1 : T.hdn + (size_t)(r - n + 2) * n1) + jraw, v);
-            }
-            halo = true;
-        }
-        if (halo) __threadfence_system();
-    }
 }
 
 // the four (first pass, two iterations) instantiations of strip2d_tb2
 template <int K, bool DIAG, bool SLAB>
 __device__ __forceinline__ void tb2_strip(const LejaParams& P, bool first, bool two, const Tb2Pass& T, int c_b,
                                           int c_e, int lane, double alpha, double b1, double b2, const double* d0,
-                                          const double* da, const double* db, int active, int rbmask,
-                                          const double* rbd, double (&acc)[2 * (1 + K)], double2* __restrict__ ring) {
+                                          const double* da, const double* db, int active,
+                                          double (&acc)[2 * (1 + K)], double2* __restrict__ ring) {
     if (first) {
-        if (two) strip2d_tb2<K, DIAG, true, true, SLAB>(P, T, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active,
-                                                       rbmask, rbd, acc, ring);
-        else strip2d_tb2<K, DIAG, true, false, SLAB>(P, T, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active,
-                                                     rbmask, rbd, acc, ring);
+        if (two) strip2d_tb2<K, DIAG, true, true, SLAB>(P, T, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active, acc, ring);
+        else strip2d_tb2<K, DIAG, true, false, SLAB>(P, T, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active, acc, ring);
     } else {
-        if (two) strip2d_tb2<K, DIAG, false, true, SLAB>(P, T, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active,
-                                                        rbmask, rbd, acc, ring);
-        else strip2d_tb2<K, DIAG, false, false, SLAB>(P, T, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active,
-                                                      rbmask, rbd, acc, ring);
+        if (two) strip2d_tb2<K, DIAG, false, true, SLAB>(P, T, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active, acc, ring);
+        else strip2d_tb2<K, DIAG, false, false, SLAB>(P, T, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active, acc, ring);
     }
 }
 
-// Final rollback pass: p_k -= rbd[k] * y (y = the last written y_{m+1}) on the strip's output points.
-template <int K, int RT>
-__device__ __forceinline__ void strip2d_tb2_rollback(const LejaParams& P, const double* y, int cbeg, int cend,
-                                                     int lane, int rbmask, const double* rbd) {
-    const int n1 = P.n1, n = P.n_loc, nc = P.nrb;
-    for (int ci = cbeg; ci < cend; ci++) {
-        const int b = ci / nc, ic = ci - b * nc;
-        const int c0 = b * kBand2;
-        const int jraw = c0 - 2 + 2 * lane;
-        if (!(lane >= 1 && lane <= 30 && jraw < n1 && jraw < c0 + kBand2)) continue;
-        const int i0 = ic * RT;
-        const int nout = min(RT, n - i0);
-        for (int t = 0; t < nout; t++) {
-            const size_t off = (size_t)(i0 + t) * n1 + jraw;
-            const double2 yy = ld2(y + off);
-#pragma unroll
-            for (int k = 0; k < K; k++) {
-                if ((rbmask >> k) & 1) {
-                    const double2 pp = ld2(P.p[k] + off);
-                    st2(P.p[k] + off, make_double2(fma(-rbd[k], yy.x, pp.x), fma(-rbd[k], yy.y, pp.y)));
-                }
-            }
+// Output columns of band b owned by this lane (lanes 1..30, two columns each), or -1.
+__device__ __forceinline__ int tb2_col(int b, int lane, int n1) {
+    const int jraw = b * kBand2 - 2 + 2 * lane;
+    return (lane >= 1 && lane <= 30 && jraw < n1 && jraw < b * kBand2 + kBand2) ? jraw : -1;
+}
+
+// SLAB halo delivery: rows [r0, r0 + nr) of x, band b -> ghost rows [g0, g0 + nr) of a neighbour's ghost
+// block, then (all lanes) a system-scope fence and (lane 0) the release of the neighbour's band flag.
+__device__ __forceinline__ void tb2_deliver(const double* x, int r0, int nr, double* g, int g0, int b, int lane,
+                                            int n1, unsigned* flag, unsigned value, const double* x2, double* g2) {
+    const int j = tb2_col(b, lane, n1);
+    if (j >= 0) {
+        for (int r = 0; r < nr; r++) {
+            st2(g + (size_t)(g0 + r) * n1 + j, ld2(x + (size_t)(r0 + r) * n1 + j));
+            if (x2) st2(g2 + (size_t)(g0 + r) * n1 + j, ldg2(x2 + (size_t)(r0 + r) * n1 + j));
         }
     }
+    __threadfence_system();
+    __syncwarp();
+    if (lane == 0) st_release_sys32(flag, value);
 }
 
 // Cross-rank step of the slab kernel's barrier (ONE thread: the last arriver of this rank's grid
@@ -327,86 +299,120 @@ __device__ __forceinline__ int xrank_sum(const LejaParams& P, double* acc) {
     return 0;
 }
 
-// grid barrier + decisions of iterations m (and m+1): flags[1] done, [2] active, [3] rollback mask.
-// g = generation offset of this barrier within the call (waiters release at gen0 + g).
+
+// Decision word of pass q: [63:32] tag (pbase + q), [31:24] status, [19:16] rollback mask (accumulators
+// that converged on the first iteration of the pass), [15:8] done, [7:0] active mask after the pass.
+__device__ __forceinline__ unsigned dec_tag(unsigned long long w) { return (unsigned)(w >> 32); }
+__device__ __forceinline__ int dec_done(unsigned long long w) { return (int)((w >> 8) & 0xff); }
+__device__ __forceinline__ int dec_act(unsigned long long w) { return (int)(w & 0xff); }
+__device__ __forceinline__ int dec_rb(unsigned long long w) { return (int)((w >> 16) & 0xf); }
+__device__ __forceinline__ int dec_status(unsigned long long w) { return (int)((w >> 24) & 0xff); }
+
+// wrap-safe "counter has reached target" for 32-bit tags
+__device__ __forceinline__ bool tag_ge(unsigned a, unsigned b) { return (int)(a - b) >= 0; }
+
+// The call has ended at a pass < q (its final decision is published or about to be): pass q is
+// beyond the speculative pass and its decision will never come.
+__device__ __forceinline__ bool tb2_ended_before(const LejaParams& P, unsigned pbase, int q) {
+    const unsigned ft = ld_acquire(&P.tc->final_tag);
+    return tag_ge(ft, pbase) && (int)(ft - pbase) < q;
+}
+
+constexpr unsigned long long kDecStop = 1ull;   // tb2_wait_dec: the call ended earlier (tag 0: never a real word)
+
+// Spin (one thread) until the decision of pass q is published.  Returns the word, kDecStop if the call
+// ended before pass q, 0 on watchdog / abort.
+__device__ __forceinline__ unsigned long long tb2_wait_dec(const LejaParams& P, unsigned pbase, int q) {
+    Tb2Ctl* tc = P.tc;
+    const unsigned tag = pbase + (unsigned)q;
+    unsigned long long w = ld_acquire64(&tc->dec[q & 1]);
+    if (dec_tag(w) == tag) return w;
+    const unsigned long long t0 = globaltimer_ns();
+    for (int spins = 0;; spins++) {
+        __nanosleep(64);
+        w = ld_acquire64(&tc->dec[q & 1]);
+        if (dec_tag(w) == tag) return w;
+        if ((spins & 15) == 15 && tb2_ended_before(P, pbase, q)) return kDecStop;
+        if ((spins & 255) == 255 && (ld_acquire(&tc->abort) || globaltimer_ns() - t0 > P.timeout_ns)) {
+            atomicExch(&tc->abort, 1u);
+            atomicExch(&P.rec->status, 10);
+            return 0ull;
+        }
+    }
+}
+
+// Spin (one thread) until *c >= target.  Returns 1; 2 if `q >= 0` and the call ended before pass q
+// (a speculative pass stops quietly); 0 on watchdog / abort.
+__device__ __forceinline__ int tb2_wait_ge(const LejaParams& P, const unsigned* c, unsigned target, bool sys,
+                                           unsigned pbase, int q) {
+    if (tag_ge(sys ? ld_acquire_sys32(c) : ld_acquire(c), target)) return 1;
+    const unsigned long long t0 = globaltimer_ns();
+    for (int spins = 0;; spins++) {
+        __nanosleep(32);
+        if (tag_ge(sys ? ld_acquire_sys32(c) : ld_acquire(c), target)) return 1;
+        if (q >= 0 && (spins & 15) == 15 && tb2_ended_before(P, pbase, q)) return 2;
+        if ((spins & 255) == 255 && (ld_acquire(&P.tc->abort) || globaltimer_ns() - t0 > P.timeout_ns)) {
+            atomicExch(&P.tc->abort, 1u);
+            atomicExch(&P.rec->status, 10);
+            return 0;
+        }
+    }
+}
+
+// Decision of pass q (lane 0 of the warp that finished its last segment group): wait for the decision of
+// pass q-1; if that ended the call, pass q was speculative -> published as done without a decision
+// (and without a cross-rank exchange: every rank decides the same passes).  Else the fixed-order group
+// sums (and in a slab the rank-ordered cross-rank sums) enter the P:155 test for iterations 2q+1 and 2q+2.
 template <int K, bool SLAB>
-__device__ __forceinline__ void barrier_decide_tb2(const LejaParams& P, int m, int g, bool two, unsigned gen0,
-                                                   const double* da, const double* db, int active,
-                                                   double (*s_red)[kSlot], int* s_flags) {
+__device__ __forceinline__ void tb2_decide(const LejaParams& P, unsigned pbase, int q, bool two, const double* sums_in,
+                                           const double* da, const double* db) {
     constexpr int NV = 2 * (1 + K);
-    const int tid = threadIdx.x;
-    Ctrl* ctrl = P.ctrl;
-    __syncthreads();
-    if (tid == 0) {
-        const unsigned t = atom_add_acq_rel(&ctrl->arrive, 1u);
-        s_flags[0] = (t == gridDim.x - 1);
+    Tb2Ctl* tc = P.tc;
+    int act = P.active0, status = 0;
+    if (q >= 1) {
+        const unsigned long long wp = tb2_wait_dec(P, pbase, q - 1);
+        if (wp <= kDecStop) return;
+        if (dec_done(wp)) {
+            const unsigned long long w = ((unsigned long long)(pbase + (unsigned)q) << 32) |
+                                         ((unsigned long long)(dec_status(wp) & 0xff) << 24) | (1ull << 8) |
+                                         (unsigned long long)(dec_act(wp) & 0xff);
+            tc->gdone[q & 1] = 0u;
+            st_release64(&tc->dec[q & 1], w);
+            return;
+        }
+        act = dec_act(wp);
     }
-    __syncthreads();
-    if (s_flags[0]) {
-        double acc[NV];
+    double acc[NV];
 #pragma unroll
-        for (int i = 0; i < NV; i++) acc[i] = 0.0;
-        for (int gi = tid; gi < P.ngrp; gi += kThreads) {
-#pragma unroll
-            for (int i = 0; i < NV; i++) acc[i] += __ldcg(P.grp_part + (size_t)gi * NV + i);
+    for (int i = 0; i < NV; i++) acc[i] = sums_in[i];
+    if (SLAB) {
+        status = xrank_sum<NV>(P, acc);
+        if (status) {
+            atomicExch(&tc->abort, 1u);
+            atomicExch(&P.rec->status, 10);
+            return;
         }
-        block_reduce<NV>(acc, s_red);
-        if (tid == 0) {
-            int act = active, done = 0, status = 0;
-            if (SLAB && m == 0) {   // the call's first barrier: ghost rows of v (and u) are in place
-                status = xrank_sum<0>(P, acc);
-                done = status != 0;
-            } else {
-                if (SLAB) status = xrank_sum<NV>(P, acc);
-                if (status) {
-                    done = 1;
-                } else {
-                    leja_decide<K>(P, m, acc, da, act, done, status, P.rec);
-                }
-            }
-            if (status == 10) atomicExch(&P.rec->status, 10);
-            const int rb = (m > 0) ? (active & ~act) : 0;   // converged at the first iteration of a pass -> roll back
-            if (m > 0 && !done && two) leja_decide<K>(P, m + 1, acc + 1 + K, db, act, done, status, P.rec);
-            ctrl->arrive = 0u;
-            if (m > 0) {
-                const int pass = (m - 1) >> 1;
-                ctrl->work[(pass + 1) & 1] = 0u;     // segment counter of the next pass
-                if (done) ctrl->work[pass & 1] = 0u;  // ... and of this one for the next call
-            } else if (done) {
-                ctrl->work[0] = 0u;
-            }
-            const unsigned long long w = ((unsigned long long)(gen0 + (unsigned)g) << 32) |
-                                         ((unsigned long long)(status & 0xff) << 16) |
-                                         ((unsigned long long)(rb & 0xf) << 12) |
-                                         ((unsigned long long)(done & 0xf) << 8) | (unsigned long long)(act & 0xff);
-            st_release64(&ctrl->word, w);
-            s_flags[1] = done;
-            s_flags[2] = act;
-            s_flags[3] = two ? rb : 0;
-        }
-    } else if (tid == 0) {
-        // waiters: time-based watchdog, longer than the last arriver's cross-rank limit (SLAB)
-        const unsigned long long limit = (SLAB ? P.timeout_ns : 0ull) + 10000000000ull;
-        const unsigned long long t0 = globaltimer_ns();
-        unsigned long long w = ld_relaxed64(&ctrl->word);
-        int spins = 0;
-        while ((int)((unsigned)(w >> 32) - gen0) < g) {
-            if (++spins > 4096) {
-                __nanosleep(32);
-                if ((spins & 1023) == 0 && globaltimer_ns() - t0 > limit) {
-                    atomicExch(&P.rec->status, 10);
-                    w = (1ull << 8);
-                    break;
-                }
-            }
-            w = ld_relaxed64(&ctrl->word);
-        }
-        fence_acquire();
-        s_flags[1] = (int)((w >> 8) & 0xf);
-        s_flags[2] = (int)(w & 0xff);
-        s_flags[3] = two ? (int)((w >> 12) & 0xf) : 0;
     }
-    __syncthreads();
+    const int act0 = act;
+    int done = 0;
+    leja_decide<K>(P, 2 * q + 1, acc, da, act, done, status, P.rec);
+    const int rb = two ? (act0 & ~act) : 0;     // converged on the first iteration: p_{m+1} holds one term too many
+    const int act1 = act;
+    if (!done && two) leja_decide<K>(P, 2 * q + 2, acc + 1 + K, db, act, done, status, P.rec);
+    for (int k = 0; k < K; k++) {
+        if (((act0 >> k) & 1) && !((act >> k) & 1)) {   // frozen in this pass
+            tc->frtag[k] = pbase + (unsigned)q;
+            tc->frrb[k] = (rb >> k) & 1;
+            tc->frd[k] = db[k];
+        }
+    }
+    (void)act1;
+    if (done) tc->final_tag = pbase + (unsigned)q;
+    tc->gdone[q & 1] = 0u;                          // reused by pass q+2 (which starts after this decision)
+    const unsigned long long w = ((unsigned long long)(pbase + (unsigned)q) << 32) |
+                                 ((unsigned long long)(status & 0xff) << 24) | ((unsigned long long)(rb & 0xf) << 16) |
+                                 ((unsigned long long)(done & 0xff) << 8) | (unsigned long long)(act & 0xff);
+    st_release64(&tc->dec[q & 1], w);
 }
 
 template <int K>
@@ -429,161 +435,348 @@ __device__ __forceinline__ void coef_first5(const LejaParams& P, int k, double* 
     for (int i = 0; i < 5; i++) d[i] = __shfl_sync(0xffffffffu, e[i], 0);
 }
 
-// Two Leja iterations per HBM pass.  SLAB = the slab-decomposed variant:
-// one persistent kernel per Leja call and rank; the halo rows travel through peer memory from inside
-// the pass (tb2 strip), the norm partials through the exchange headers at the grid barrier
-// (xrank_sum); no host round trip, no NCCL call and no extra launch per iteration.
+
+// Key of a Leja call's parameters (node count, phi index, dt, shift / scale, vertical coefficients,
+// tolerances) for the ping-pong parity prediction.
+template <int K>
+__device__ __forceinline__ unsigned long long tb2_call_key(const LejaParams& P) {
+    unsigned long long h = 1469598103934665603ull;
+    auto mix = [&h](unsigned long long x) {
+        h ^= x;
+        h *= 1099511628211ull;
+    };
+    mix((unsigned long long)P.l | ((unsigned long long)K << 8) | ((unsigned long long)P.max_nodes << 16) |
+        ((unsigned long long)P.active0 << 40));
+    mix((unsigned long long)__double_as_longlong(P.cdt));
+    mix((unsigned long long)__double_as_longlong(P_c(P)));
+    mix((unsigned long long)__double_as_longlong(P_g(P)));
+    mix((unsigned long long)__double_as_longlong(P.rtol));
+    mix((unsigned long long)__double_as_longlong(P.atol));
+#pragma unroll
+    for (int k = 0; k < K; k++) mix((unsigned long long)__double_as_longlong(P.ak[k]));
+    return h | 1ull;
+}
+
+// Two Leja iterations per HBM pass, passes pipelined (see the header comment).  SLAB = the
+// slab-decomposed variant: one persistent kernel per Leja call and rank; halo rows and
+// norm partials travel through peer memory from inside the kernel; no host round trip, no NCCL call and
+// no extra launch per iteration.
 template <int K, bool DIAG, bool SLAB>
 __global__ void __launch_bounds__(kThreads, 2) k_leja2d_tb2(const __grid_constant__ LejaParams P) {
-    __shared__ double s_red[kWarps][kSlot];
     extern __shared__ double2 tb2_ring[];
-    __shared__ int s_flags[4];
+    __shared__ int s_flag;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool cwarp = (blockIdx.x == 0 && warp == 0);
-    const int gw = blockIdx.x * kWarps + warp - 1;
-    const int W = gridDim.x * kWarps - 1;
-    constexpr int RT = tb2_rt(K);
     constexpr int NV = 2 * (1 + K);
+    constexpr int RT = tb2_rt(K);
     double2* ring = tb2_ring + (size_t)warp * Tb2Stage<K, DIAG>::WARP;
-    const int cbeg = cwarp ? 0 : (int)((long long)gw * P.nunits / W);
-    const int cend = cwarp ? 0 : (int)((long long)(gw + 1) * P.nunits / W);
-    unsigned gen0 = 0;
-    if (tid == 0) gen0 = (unsigned)(ld_acquire64(&P.ctrl->word) >> 32);
-    int active = P.active0, rbmask = 0;
-    const int M = P.max_nodes;
-    const double alpha = P_alpha(P);
-    const int n = P.n_loc, n1 = P.n1;
-    if (SLAB) {
-        // halo rows of v (and u) into the neighbours' ghost blocks, then the call's first cross-rank barrier
-        const long long tot = 6LL * n1;
-        for (long long x = (long long)blockIdx.x * kThreads + tid; x < tot; x += (long long)gridDim.x * kThreads) {
-            const int r = (int)(x / n1), j = (int)(x - (long long)r * n1);
-            const int sr = r < 4 ? r : n - 6 + r;                // rows 0..3 -> rank-1, rows n-2, n-1 -> rank+1
-            double* gv = r < 4 ? P.hup_v + (size_t)(2 + r) * n1 : P.hdn_v + (size_t)(r - 4) * n1;
-            gv[j] = P.v.base[(size_t)sr * n1 + j];
-            if (DIAG) {
-                double* gu = r < 4 ? P.hup_u + (size_t)(2 + r) * n1 : P.hdn_u + (size_t)(r - 4) * n1;
-                gu[j] = P.u[(size_t)sr * n1 + j];
-            }
+    Tb2Ctl* tc = P.tc;
+    const unsigned pbase = tc->pbase;             // written by the previous call's leader (kernel boundary)
+    // p ping-pong parity: pass q writes half (q + poff) & 1 (half 0 = the caller's output).  poff is the
+    // final-pass parity of the last call with the same parameters (a small table written by each call's
+    // leader): repeated calls then end in the caller's buffer and the fix-up copies nothing
+    const unsigned long long key = tb2_call_key<K>(P);
+    int poff = 0, pslot = -1;
+    for (int i = 0; i < kTb2Pred; i++)
+        if (tc->pkey[i] == key) {
+            poff = (int)(tc->pfin[i] & 1u);
+            pslot = i;
         }
-        __threadfence_system();
-        barrier_decide_tb2<K, true>(P, 0, 1, false, gen0, nullptr, nullptr, active, s_red, s_flags);
-        if (s_flags[1]) return;   // peer timeout
-    }
+    unsigned rel0 = 0;
+    if (tid == 0) rel0 = ld_acquire(&tc->release);
+    const int M = P.max_nodes;
+    const int qmax = (M - 2) / 2;                 // last pass: first iteration 2q+1 <= M-1
+    const int nb = P.nb, nseg = P.nseg, nsr = nseg / nb, n = P.n_loc, n1 = P.n1;
+    const double alpha = P_alpha(P);
     double dd[K][5];
 #pragma unroll
     for (int k = 0; k < K; k++) coef_first5<K>(P, k, dd[k]);
-    if (cwarp && P.coef_gen) {
-        for (int r = 0; r < 5 && r < M; r++) {
-            double row[K];
+    if (cwarp) {
+        // coefficient warp: rows 0..4 now, then d_j (lane k = accumulator k) ahead of the issued passes
+        if (!P.coef_gen && lane == 0) st_release(&tc->crow, (unsigned)M);   // prebuilt table
+        if (P.coef_gen) {
+            for (int r = 0; r < 5 && r < M; r++) {
+                double row[K];
 #pragma unroll
-            for (int k = 0; k < K; k++) row[k] = dd[k][r];
-            coef_write_row<K>(P, r, lane, active, row);
-        }
-    }
-    double d0[K], da[K], db[K], rbd[K];
-#pragma unroll
-    for (int k = 0; k < K; k++) {
-        d0[k] = dd[k][0];
-        da[k] = dd[k][1];
-        db[k] = dd[k][2];
-        rbd[k] = 0.0;
-    }
-    double na[K], nb[K];   // rows m+2, m+3 (rows 3, 4 from the prologue for the first pass)
-#pragma unroll
-    for (int k = 0; k < K; k++) {
-        na[k] = dd[k][3];
-        nb[k] = dd[k][4];
-    }
-    int m = 1;
-    double nb1 = coef_beta(P, 1), nb2 = (2 < M) ? coef_beta(P, 2) : 0.0;
-    for (; m < M; m += 2) {
-        const bool two = (m + 1 < M);
-        const double b1 = nb1, b2 = two ? nb2 : 0.0;
-        // next pass's shifts (constant inputs): loaded now, off the post-barrier critical path
-        nb1 = (m + 2 < M) ? coef_beta(P, m + 2) : 0.0;
-        nb2 = (m + 3 < M) ? coef_beta(P, m + 3) : 0.0;
-        const int pass = (m - 1) >> 1;
-        double acc[NV];
-#pragma unroll
-        for (int i = 0; i < NV; i++) acc[i] = 0.0;
-        if (cwarp) {
-            if (P.coef_gen) {
-                if (m + 4 < M) coef_write_row<K>(P, m + 4, lane, active, nullptr);
-                if (m + 5 < M) coef_write_row<K>(P, m + 5, lane, active, nullptr);
+                for (int k = 0; k < K; k++) row[k] = dd[k][r];
+                coef_write_row<K>(P, r, lane, P.active0, row);
             }
-        } else {
+            __syncwarp();
+            __threadfence();
+            if (lane == 0) st_release(&tc->crow, 5u);
+            int j = 5;
+            while (j < M) {
+                unsigned t = 0, stop = 0;
+                if (lane == 0) {
+                    t = ld_acquire(&tc->ticket);
+                    stop = ld_acquire(&tc->abort) || tag_ge(ld_acquire(&tc->final_tag), pbase);
+                }
+                t = __shfl_sync(FULL_MASK, t, 0);
+                if (__shfl_sync(FULL_MASK, stop, 0)) break;
+                const int want = min(M - 1, 2 * (int)(t / (unsigned)nseg) + 8);
+                if (j > want) {
+                    __nanosleep(256);
+                    continue;
+                }
+                coef_write_row<K>(P, j, lane, (1 << K) - 1, nullptr);
+                __syncwarp();
+                __threadfence();
+                if (lane == 0) st_release(&tc->crow, (unsigned)(j + 1));
+                j++;
+            }
+        }
+    } else {
+        for (;;) {
+            unsigned tk = 0;
+            if (lane == 0) tk = atomicAdd(&tc->ticket, 1u);
+            tk = __shfl_sync(FULL_MASK, tk, 0);
+            const int q = (int)(tk / (unsigned)nseg);
+            if (q > qmax) break;
+            // pass q visits the segment rows starting at row q mod nsr (band fastest): its first segments
+            // depend on the rows pass q-1 visited FIRST, so consecutive passes overlap instead of pass q
+            // waiting for the previous pass's last (periodically adjacent) rows
+            const int ti = (int)(tk - (unsigned)q * (unsigned)nseg);
+            const int rsi = ti / nb;
+            const int s = ((rsi + q) % nsr) * nb + (ti - rsi * nb);
+            // lagged decision: pass q needs the decision of pass q-2
+            int act = P.active0, rbm = 0, stop = 0;
+            if (lane == 0) {
+                if (q >= 2) {
+                    const unsigned long long w = tb2_wait_dec(P, pbase, q - 2);
+                    if (w <= kDecStop || dec_done(w)) stop = 1;
+                    else {
+                        act = dec_act(w);
+                        rbm = dec_rb(w);
+                    }
+                }
+                if (!stop && q >= 1) {   // pass q-1 already known to end the call: nothing left to do
+                    const unsigned long long w1 = ld_acquire64(&tc->dec[(q - 1) & 1]);
+                    if (dec_tag(w1) == pbase + (unsigned)(q - 1) && dec_done(w1)) stop = 1;
+                }
+            }
+            if (__shfl_sync(FULL_MASK, stop, 0)) break;
+            act = __shfl_sync(FULL_MASK, act, 0);
+            rbm = __shfl_sync(FULL_MASK, rbm, 0);
+            const bool two = (2 * q + 2 < M);
+            // Newton coefficients of iterations 2q+1, 2q+2 (rows 0..4 from the prologue)
+            double d0[K], da[K], db[K];
+            if (q >= 2) {
+                if (lane == 0 && tb2_wait_ge(P, &tc->crow, (unsigned)min(2 * q + 3, M), false, pbase, q) != 1) stop = 1;
+                if (__shfl_sync(FULL_MASK, stop, 0)) break;
+                __syncwarp();
+            }
+#pragma unroll
+            for (int k = 0; k < K; k++) {
+                d0[k] = dd[k][0];
+                da[k] = q == 0 ? dd[k][1] : (q == 1 ? dd[k][3] : __ldcg(P.table + (size_t)(2 * q + 1) * (1 + K) + 1 + k));
+                db[k] = !two ? 0.0 : (q == 0 ? dd[k][2] : (q == 1 ? dd[k][4] : __ldcg(P.table + (size_t)(2 * q + 2) * (1 + K) + 1 + k)));
+            }
+            const double b1 = coef_beta(P, 2 * q + 1), b2 = two ? coef_beta(P, 2 * q + 2) : 0.0;
+            const int rs = s / nb, b = s - rs * nb;
+            const bool top = SLAB && rs == 0, bot = SLAB && rs == nsr - 1;
+            // SLAB, first pass: this rank's boundary rows of v (and u) into the neighbours' ghost blocks
+            if (SLAB && q == 0) {
+                if (top) tb2_deliver(P.v.base, 0, 4, P.hup_v, 2, b, lane, n1, P.fl_dn_up + b, pbase,
+                                     DIAG ? P.u : nullptr, P.hup_u);
+                if (bot) tb2_deliver(P.v.base, n - 2, 2, P.hdn_v, 0, b, lane, n1, P.fl_up_dn + b, pbase,
+                                     DIAG ? P.u : nullptr, P.hdn_u);
+            }
+            // dependencies: pass q-1 done on the 3 x 3 neighbour segments (slab edges: the neighbour
+            // rank's boundary segments, signalled by band flags after their halo rows landed here)
+            if (lane < 9) {
+                const int dr = lane / 3 - 1, dbn = lane % 3 - 1;
+                const int bb = (b + dbn + nb) % nb;
+                const int rr = rs + dr;
+                if (SLAB && rr < 0) stop = tb2_wait_ge(P, P.fl_up + bb, pbase + (unsigned)q, true, pbase, q) != 1;
+                else if (SLAB && rr >= nsr) stop = tb2_wait_ge(P, P.fl_dn + bb, pbase + (unsigned)q, true, pbase, q) != 1;
+                else if (q >= 1)
+                    stop = tb2_wait_ge(P, P.scnt + ((rr + nsr) % nsr) * nb + bb, pbase + (unsigned)q, false, pbase, q) != 1;
+            }
+            if (__any_sync(FULL_MASK, stop)) break;
+            __syncwarp();
+            // segment rows of P.seg chunks; the last one also takes the remainder (>= 4 rows: a segment's
+            // stencil halo, rows -2 .. +3, then reaches only the adjacent segment rows / ghost rows)
+            const int c_b = b * P.nrb + rs * P.seg;
+            const int c_e = b * P.nrb + (rs == nsr - 1 ? P.nrb : rs * P.seg + P.seg);
+            const int r0 = rs * P.seg * RT, r1 = (rs == nsr - 1) ? n : (rs * P.seg + P.seg) * RT;
+            // accumulators that converged on the first iteration of pass q-2: p_m = p_{m+1} - d_{m+1} y_{m+1},
+            // in place in their final ping-pong half, before this pass overwrites y_{m+1}
+            if (rbm) {
+                const int j = tb2_col(b, lane, n1);
+                const double* y = P.ydst[q & 1];
+#pragma unroll
+                for (int k = 0; k < K; k++) {
+                    if (!((rbm >> k) & 1) || j < 0) continue;
+                    double* pk = P.pp[k][(q + poff) & 1];
+                    const double dk = __ldcg(&tc->frd[k]);
+                    for (int r = r0; r < r1; r++) {
+                        const size_t off = (size_t)r * n1 + j;
+                        const double2 yy = ld2(y + off), pv = ld2(pk + off);
+                        st2(pk + off, make_double2(fma(-dk, yy.x, pv.x), fma(-dk, yy.y, pv.y)));
+                    }
+                }
+            }
             Tb2Pass T;
-            T.src = (m == 1) ? P.v.base : P.ydst[(pass & 1) ^ 1];
-            T.gsrc = (m == 1) ? P.gv : P.gy[(pass & 1) ^ 1];
+            T.src = (q == 0) ? P.v.base : P.ydst[(q - 1) & 1];
+            T.gsrc = (q == 0) ? P.gv : P.gy[(q - 1) & 1];
             T.gu = P.gu;
-            T.dst = P.ydst[pass & 1];
-            T.hup = P.hup[pass & 1];
-            T.hdn = P.hdn[pass & 1];
-            // dynamic segments of P.seg chunks, band fastest (adjacent bands of the same rows run together;
-            // the dynamic schedule balances the end-of-pass tail).  The norm partials stay deterministic:
-            // each segment's sums are formed by one warp in a fixed order and stored by segment index; the
-            // last finisher of each group of 32 segments sums the group in index order (fixed butterfly);
-            // the barrier sums the groups in order.
-            unsigned* ctr = &P.ctrl->work[pass & 1];
-#pragma unroll 1
-            for (;;) {
-                int sg = 0;
-                if (lane == 0) sg = (int)atomicAdd(ctr, 1u);
-                sg = __shfl_sync(FULL_MASK, sg, 0);
-                if (sg >= P.nseg) break;
-                const int rs = sg / P.nb, b = sg - rs * P.nb;
-                const int c_b = b * P.nrb + rs * P.seg;
-                const int c_e = b * P.nrb + min(P.nrb, rs * P.seg + P.seg);
+            T.dst = P.ydst[q & 1];
 #pragma unroll
-                for (int i = 0; i < NV; i++) acc[i] = 0.0;
-                tb2_strip<K, DIAG, SLAB>(P, m == 1, two, T, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active, rbmask,
-                                         rbd, acc, ring);
-                double sacc[NV];
+            for (int k = 0; k < kMaxK; k++) {
+                T.pin[k] = P.pp[k][(q - 1 + poff) & 1];
+                T.pout[k] = P.pp[k][(q + poff) & 1];
+            }
+            double acc[NV];
 #pragma unroll
-                for (int i = 0; i < NV; i++) sacc[i] = acc[i];
-                warp_sum<NV>(sacc);
-                int last = 0;
-                const int g = sg >> 5;
+            for (int i = 0; i < NV; i++) acc[i] = 0.0;
+            tb2_strip<K, DIAG, SLAB>(P, q == 0, two, T, c_b, c_e, lane, alpha, b1, b2, d0, da, db, act, acc, ring);
+            // SLAB: this pass's boundary rows of y into the neighbours' ghost blocks (+ their band flags)
+            if (top) tb2_deliver(T.dst, 0, 4, P.hup[q & 1], 2, b, lane, n1, P.fl_dn_up + b, pbase + (unsigned)q + 1,
+                                 nullptr, nullptr);
+            if (bot) tb2_deliver(T.dst, n - 2, 2, P.hdn[q & 1], 0, b, lane, n1, P.fl_up_dn + b,
+                                 pbase + (unsigned)q + 1, nullptr, nullptr);
+            // the segment is done with pass q: its norm partials, then ONE fence (ordering this warp's y / p
+            // stores and the partials) before the completion tag and the group counter
+            warp_sum<NV>(acc);
+            double* segp = P.seg_part + ((size_t)(q & 1) * P.nseg + s) * NV;
+            const int g = s >> 5;
+            int last = 0;
+            if (lane == 0) {
+#pragma unroll
+                for (int i = 0; i < NV; i++) segp[i] = acc[i];
+            }
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence();
+                st_relaxed32(P.scnt + s, pbase + (unsigned)q + 1);
+                const unsigned t = atomicAdd(&P.grp_cnt[(q & 1) * P.ngrp + g], 1u);
+                last = (int)(t == (unsigned)(min(32, nseg - g * 32) - 1));
+            }
+            last = __shfl_sync(FULL_MASK, last, 0);
+            if (last) {
+                __threadfence();
+                const int s2 = g * 32 + lane;
+                double gv[NV];
+#pragma unroll
+                for (int i = 0; i < NV; i++)
+                    gv[i] = (s2 < nseg) ? __ldcg(P.seg_part + ((size_t)(q & 1) * P.nseg + s2) * NV + i) : 0.0;
+                warp_sum<NV>(gv);
+                int lastg = 0;
                 if (lane == 0) {
 #pragma unroll
-                    for (int i = 0; i < NV; i++) P.seg_part[(size_t)sg * NV + i] = sacc[i];
+                    for (int i = 0; i < NV; i++) P.grp_part[((size_t)(q & 1) * P.ngrp + g) * NV + i] = gv[i];
+                    P.grp_cnt[(q & 1) * P.ngrp + g] = 0u;
                     __threadfence();
-                    const unsigned t = atomicAdd(&P.grp_cnt[g], 1u);
-                    last = (int)(t == (unsigned)(min(32, P.nseg - g * 32) - 1));
+                    lastg = (int)(atomicAdd(&tc->gdone[q & 1], 1u) == (unsigned)(P.ngrp - 1));
                 }
-                last = __shfl_sync(FULL_MASK, last, 0);
-                if (last) {
+                lastg = __shfl_sync(FULL_MASK, lastg, 0);
+                if (lastg) {
+                    // the pass is complete: fixed-order sum over its groups (lane-strided, then butterfly)
                     __threadfence();
-                    const int s2 = g * 32 + lane;
-                    double gv[NV];
+                    double sv[NV];
 #pragma unroll
-                    for (int i = 0; i < NV; i++) gv[i] = (s2 < P.nseg) ? __ldcg(P.seg_part + (size_t)s2 * NV + i) : 0.0;
-                    warp_sum<NV>(gv);
-                    if (lane == 0) {
+                    for (int i = 0; i < NV; i++) sv[i] = 0.0;
+                    for (int g2 = lane; g2 < P.ngrp; g2 += 32) {
 #pragma unroll
-                        for (int i = 0; i < NV; i++) P.grp_part[(size_t)g * NV + i] = gv[i];
-                        P.grp_cnt[g] = 0u;
+                        for (int i = 0; i < NV; i++) sv[i] += __ldcg(P.grp_part + ((size_t)(q & 1) * P.ngrp + g2) * NV + i);
+                    }
+                    warp_sum<NV>(sv);
+                    if (lane == 0) tb2_decide<K, SLAB>(P, pbase, q, two, sv, da, db);
+                    __syncwarp();
+                }
+            }
+        }
+    }
+    // ---- end of the call: every warp has stopped (one grid barrier per call), then the fix-up
+    __syncthreads();
+    if (tid == 0) {
+        const unsigned t = atom_add_acq_rel(&tc->arrive, 1u);
+        s_flag = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (s_flag) {
+        if (tid == 0) {
+            // leader: snapshot the call's outcome for the fix-up, reset the per-call counters (nobody uses
+            // them after this barrier), advance the pass tags above every tag of this call (speculative
+            // pass f + 1 included), then release
+            const unsigned ft = ld_acquire(&tc->final_tag);
+            const unsigned ab = ld_acquire(&tc->abort);
+            const unsigned fl = tag_ge(ft, pbase) ? ft - pbase : 0u;
+            tc->snap_final = fl;
+            tc->snap_abort = ab;
+            if (!ab) {   // remember this call's final pass for the next call with the same parameters
+                const int slot = pslot >= 0 ? pslot : (int)(tc->pnext++ % (unsigned)kTb2Pred);
+                tc->pkey[slot] = key;
+                tc->pfin[slot] = fl;
+            }
+            tc->ticket = 0u;
+            tc->crow = 0u;
+            tc->abort = 0u;
+            tc->pbase = pbase + fl + 3u + (ab ? (unsigned)qmax + 3u : 0u);
+            tc->arrive = 0u;
+            st_release(&tc->release, rel0 + 1u);
+        }
+    } else if (tid == 0) {
+        const unsigned long long t0 = globaltimer_ns();
+        while (ld_acquire(&tc->release) == rel0) {
+            __nanosleep(64);
+            if (globaltimer_ns() - t0 > P.timeout_ns + 10000000000ull) {
+                atomicExch(&P.rec->status, 10);
+                break;
+            }
+        }
+    }
+    __syncthreads();
+    const bool aborted = __ldcg(&tc->snap_abort) != 0u;
+    const int f = (int)__ldcg(&tc->snap_final);
+    // fix-up: each accumulator's final value is p of its freeze pass f_k (ping-pong half f_k & 1), minus
+    // d y_{m+1} if it converged on the first iteration of that pass and pass f_k + 2 (which rolls back in
+    // place) did not run on the segment; results in the scratch half are copied to the caller's output
+    if (!aborted) {
+        int fk[K], rbk[K];
+        double dk[K];
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            const unsigned tg = __ldcg(&tc->frtag[k]);
+            const bool frozen = tag_ge(tg, pbase) && ((P.active0 >> k) & 1);
+            fk[k] = frozen ? (int)(tg - pbase) : f;
+            rbk[k] = frozen ? (int)__ldcg(&tc->frrb[k]) : 0;
+            dk[k] = __ldcg(&tc->frd[k]);
+            any = any || rbk[k] || ((fk[k] + poff) & 1);
+        }
+        if (any) {
+            const int gw = blockIdx.x * kWarps + warp, W = gridDim.x * kWarps;
+            for (int s = gw; s < nseg; s += W) {
+                const int rs = s / nb, b = s - rs * nb;
+                const int j = tb2_col(b, lane, n1);
+                if (j < 0) continue;
+                const int r0 = rs * P.seg * RT, r1 = (rs == nsr - 1) ? n : (rs * P.seg + P.seg) * RT;
+                const unsigned done_s = ld_acquire(P.scnt + s);
+#pragma unroll
+                for (int k = 0; k < K; k++) {
+                    const bool pend = rbk[k] && !tag_ge(done_s, pbase + (unsigned)fk[k] + 3u);
+                    if (!pend && !((fk[k] + poff) & 1)) continue;
+                    const double* src = P.pp[k][(fk[k] + poff) & 1];
+                    const double* y = P.ydst[fk[k] & 1];
+                    double* out = P.pp[k][0];
+                    for (int r = r0; r < r1; r++) {
+                        const size_t off = (size_t)r * n1 + j;
+                        double2 pv = ld2(src + off);
+                        if (pend) {
+                            const double2 yy = ld2(y + off);
+                            pv = make_double2(fma(-dk[k], yy.x, pv.x), fma(-dk[k], yy.y, pv.y));
+                        }
+                        st2(out + off, pv);
                     }
                 }
             }
         }
-        barrier_decide_tb2<K, SLAB>(P, m, SLAB ? m + 1 : m, two, gen0, da, db, active, s_red, s_flags);
-        active = s_flags[2];
-        rbmask = s_flags[3];
-#pragma unroll
-        for (int k = 0; k < K; k++) {
-            rbd[k] = db[k];
-            da[k] = na[k];
-            db[k] = nb[k];
-            // rows m+4, m+5 (written by the coefficient warp during pass m-2... visible after this barrier)
-            na[k] = (m + 4 < M) ? P.table[(size_t)(m + 4) * (1 + K) + 1 + k] : 0.0;
-            nb[k] = (m + 5 < M) ? P.table[(size_t)(m + 5) * (1 + K) + 1 + k] : 0.0;
-        }
-        if (s_flags[1]) break;
     }
-    // the call ended on the first iteration of a pass for some accumulators: final rollback
-    if (rbmask && !cwarp && m < M) strip2d_tb2_rollback<K, RT>(P, P.ydst[((m - 1) >> 1) & 1], cbeg, cend, lane, rbmask, rbd);
+    // the speculative pass (and an aborted call) may leave group counters partly counted: clear them for the
+    // next call (nobody counts after the barrier)
+    for (int i = blockIdx.x * kThreads + tid; i < 2 * P.ngrp; i += gridDim.x * kThreads) P.grp_cnt[i] = 0u;
+    if (blockIdx.x == 0 && tid < 2) tc->gdone[tid] = 0u;
 }
 
 static void* leja_tb2_ptr(int K, bool diag, bool slab) {
