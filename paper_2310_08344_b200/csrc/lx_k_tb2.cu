@@ -50,8 +50,10 @@ struct Tb2Stage {
 // Row pointer of the two-step kernel: rows [0, n) of a local array; rows -2, -1, n .. n+3 by periodic
 // wrap (single domain) or, in the slab kernel (SLAB), from the 6-row ghost block g (rows -2, -1, n,
 // n+1, n+2, n+3), which the neighbouring ranks fill through peer memory.
-template <bool SLAB>
+// EDGE = false: a segment row away from the slab / periodic boundary (rows always in [0, n)).
+template <bool SLAB, bool EDGE = true>
 __device__ __forceinline__ const double* tb2_row(const double* base, const double* g, int r, int n, int n1) {
+    if (!EDGE) return base + (size_t)r * n1;
     if (SLAB && (unsigned)r >= (unsigned)n) return g + (size_t)(r < 0 ? r + 2 : r - n + 2) * n1;
     return base + (size_t)(r < 0 ? r + n : (r >= n ? r - n : r)) * n1;
 }
@@ -67,7 +69,7 @@ struct Tb2Pass {
 };
 
 // stage the global rows of chunk ci into ring stage st (every lane: its own 16-byte pieces)
-template <int K, bool DIAG, bool FIRST, bool SLAB>
+template <int K, bool DIAG, bool FIRST, bool SLAB, bool EDGE>
 __device__ __forceinline__ void tb2_issue(const LejaParams& P, const Tb2Pass& T, double2* __restrict__ ring, int ci,
                                           int st, int lane, int active) {
     using L = Tb2Stage<K, DIAG>;
@@ -83,9 +85,10 @@ __device__ __forceinline__ void tb2_issue(const LejaParams& P, const Tb2Pass& T,
     double2* sg = ring + st * L::SIZE;
 #pragma unroll
     for (int q = 0; q < RT; q++) {
-        cp_async16(sg + L::Y + q * 32 + lane, tb2_row<SLAB>(T.src, T.gsrc, i0 + 4 + q, n, n1) + j);
-        if (lane == 31) cp_async16(sg + L::H + q, tb2_row<SLAB>(T.src, T.gsrc, i0 + 2 + q, n, n1) + colw(jraw + 2));
-        if (DIAG) cp_async16(sg + L::U + q * 32 + lane, tb2_row<SLAB>(P.u, T.gu, i0 + 2 + q, n, n1) + j);
+        cp_async16(sg + L::Y + q * 32 + lane, tb2_row<SLAB, EDGE>(T.src, T.gsrc, i0 + 4 + q, n, n1) + j);
+        if (lane == 31)
+            cp_async16(sg + L::H + q, tb2_row<SLAB, EDGE>(T.src, T.gsrc, i0 + 2 + q, n, n1) + colw(jraw + 2));
+        if (DIAG) cp_async16(sg + L::U + q * 32 + lane, tb2_row<SLAB, EDGE>(P.u, T.gu, i0 + 2 + q, n, n1) + j);
     }
     if (!FIRST) {
 #pragma unroll
@@ -93,7 +96,8 @@ __device__ __forceinline__ void tb2_issue(const LejaParams& P, const Tb2Pass& T,
 #pragma unroll
             for (int k = 0; k < KK; k++)
                 if ((active >> k) & 1)
-                    cp_async16(sg + L::PP + (t * K + k) * 32 + lane, T.pin[k] + (size_t)wrap(i0 + t) * n1 + j);
+                    cp_async16(sg + L::PP + (t * K + k) * 32 + lane,
+                               T.pin[k] + (size_t)(EDGE ? wrap(i0 + t) : i0 + t) * n1 + j);
         }
     }
 }
@@ -105,7 +109,7 @@ __device__ __forceinline__ void tb2_issue(const LejaParams& P, const Tb2Pass& T,
 // (the 3-row halo recomputation happens only at a strip start) and writes RT rows of y_{m+1} and
 // p_{m+1}.  Lanes 1..30 own the band's 60 output columns; lanes 0 and 31 carry halo columns.
 // Requires n_loc >= 16, n1 >= 64 (host-checked).
-template <int K, bool DIAG, bool FIRST, bool TWO, bool SLAB>
+template <int K, bool DIAG, bool FIRST, bool TWO, bool SLAB, bool EDGE>
 __device__ __forceinline__ void strip2d_tb2(const LejaParams& P, const Tb2Pass& T, int cbeg, int cend, int lane,
                                             double alpha, double b1, double b2, const double* d0, const double* da,
                                             const double* db, int active, double (&acc)[2 * (1 + K)],
@@ -121,7 +125,7 @@ __device__ __forceinline__ void strip2d_tb2(const LejaParams& P, const Tb2Pass& 
     // prime the ring: chunks cbeg .. cbeg+D-2
 #pragma unroll
     for (int d = 0; d < D - 1; d++) {
-        if (cbeg + d < cend) tb2_issue<K, DIAG, FIRST, SLAB>(P, T, ring, cbeg + d, d, lane, active);
+        if (cbeg + d < cend) tb2_issue<K, DIAG, FIRST, SLAB, EDGE>(P, T, ring, cbeg + d, d, lane, active);
         cp_async_commit();
     }
     int ci = cbeg, st = 0;
@@ -136,11 +140,11 @@ __device__ __forceinline__ void strip2d_tb2(const LejaParams& P, const Tb2Pass& 
         const int i0 = (ci - b * nc) * RT;
         double2 t6[6], h3[3], u3[3];
 #pragma unroll
-        for (int q = 0; q < 6; q++) t6[q] = ld2(tb2_row<SLAB>(T.src, T.gsrc, i0 - 2 + q, n, n1) + j);
+        for (int q = 0; q < 6; q++) t6[q] = ld2(tb2_row<SLAB, EDGE>(T.src, T.gsrc, i0 - 2 + q, n, n1) + j);
 #pragma unroll
         for (int q = 0; q < 3; q++) {
-            h3[q] = (lane == 31) ? ld2(tb2_row<SLAB>(T.src, T.gsrc, i0 - 1 + q, n, n1) + jh) : z2;
-            u3[q] = DIAG ? ldg2(tb2_row<SLAB>(P.u, T.gu, i0 - 1 + q, n, n1) + j) : z2;
+            h3[q] = (lane == 31) ? ld2(tb2_row<SLAB, EDGE>(T.src, T.gsrc, i0 - 1 + q, n, n1) + jh) : z2;
+            u3[q] = DIAG ? ldg2(tb2_row<SLAB, EDGE>(P.u, T.gu, i0 - 1 + q, n, n1) + j) : z2;
         }
 #pragma unroll
         for (int q = 0; q < 3; q++)
@@ -156,7 +160,7 @@ __device__ __forceinline__ void strip2d_tb2(const LejaParams& P, const Tb2Pass& 
         {
             int sn = st + D - 1;
             if (sn >= D) sn -= D;
-            if (ci + D - 1 < cend) tb2_issue<K, DIAG, FIRST, SLAB>(P, T, ring, ci + D - 1, sn, lane, active);
+            if (ci + D - 1 < cend) tb2_issue<K, DIAG, FIRST, SLAB, EDGE>(P, T, ring, ci + D - 1, sn, lane, active);
             cp_async_commit();
             cp_async_wait<D - 1>();
         }
@@ -226,18 +230,26 @@ __device__ __forceinline__ void strip2d_tb2(const LejaParams& P, const Tb2Pass& 
     cp_async_wait<0>();
 }
 
-// the four (first pass, two iterations) instantiations of strip2d_tb2
+// the eight (first pass, two iterations, boundary segment row) instantiations of strip2d_tb2
+template <int K, bool DIAG, bool SLAB, bool FIRST, bool TWO>
+__device__ __forceinline__ void tb2_strip_e(const LejaParams& P, bool edge, const Tb2Pass& T, int c_b, int c_e,
+                                            int lane, double alpha, double b1, double b2, const double* d0,
+                                            const double* da, const double* db, int active,
+                                            double (&acc)[2 * (1 + K)], double2* __restrict__ ring) {
+    if (edge) strip2d_tb2<K, DIAG, FIRST, TWO, SLAB, true>(P, T, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active, acc, ring);
+    else strip2d_tb2<K, DIAG, FIRST, TWO, SLAB, false>(P, T, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active, acc, ring);
+}
 template <int K, bool DIAG, bool SLAB>
-__device__ __forceinline__ void tb2_strip(const LejaParams& P, bool first, bool two, const Tb2Pass& T, int c_b,
-                                          int c_e, int lane, double alpha, double b1, double b2, const double* d0,
-                                          const double* da, const double* db, int active,
+__device__ __forceinline__ void tb2_strip(const LejaParams& P, bool first, bool two, bool edge, const Tb2Pass& T,
+                                          int c_b, int c_e, int lane, double alpha, double b1, double b2,
+                                          const double* d0, const double* da, const double* db, int active,
                                           double (&acc)[2 * (1 + K)], double2* __restrict__ ring) {
     if (first) {
-        if (two) strip2d_tb2<K, DIAG, true, true, SLAB>(P, T, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active, acc, ring);
-        else strip2d_tb2<K, DIAG, true, false, SLAB>(P, T, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active, acc, ring);
+        if (two) tb2_strip_e<K, DIAG, SLAB, true, true>(P, edge, T, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active, acc, ring);
+        else tb2_strip_e<K, DIAG, SLAB, true, false>(P, edge, T, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active, acc, ring);
     } else {
-        if (two) strip2d_tb2<K, DIAG, false, true, SLAB>(P, T, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active, acc, ring);
-        else strip2d_tb2<K, DIAG, false, false, SLAB>(P, T, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active, acc, ring);
+        if (two) tb2_strip_e<K, DIAG, SLAB, false, true>(P, edge, T, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active, acc, ring);
+        else tb2_strip_e<K, DIAG, SLAB, false, false>(P, edge, T, c_b, c_e, lane, alpha, b1, b2, d0, da, db, active, acc, ring);
     }
 }
 
@@ -488,6 +500,32 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d_tb2(const __grid_constan
     const int qmax = (M - 2) / 2;                 // last pass: first iteration 2q+1 <= M-1
     const int nb = P.nb, nseg = P.nseg, nsr = nseg / nb, n = P.n_loc, n1 = P.n1;
     const double alpha = P_alpha(P);
+    if (SLAB) {
+        // this rank's boundary rows of v (and u) into the neighbours' ghost blocks, one band per CTA (rows
+        // 0..3 -> rank-1's rows n..n+3, rows n-2, n-1 -> rank+1's rows -2, -1), then the band flags (tag
+        // pbase: "pass -1 delivered"); done first so that no pass-0 segment waits for a late delivery
+        for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+            const int pr = tid / 30, lp = tid - pr * 30;   // 6 rows x 30 column pairs
+            if (pr < 6) {
+                const int j = b * kBand2 + 2 * lp;
+                if (j < n1) {
+                    const int src = pr < 4 ? pr : n - 6 + pr;
+                    double* gv = pr < 4 ? P.hup_v + (size_t)(2 + pr) * n1 : P.hdn_v + (size_t)(pr - 4) * n1;
+                    st2(gv + j, ld2(P.v.base + (size_t)src * n1 + j));
+                    if (DIAG) {
+                        double* gu = pr < 4 ? P.hup_u + (size_t)(2 + pr) * n1 : P.hdn_u + (size_t)(pr - 4) * n1;
+                        st2(gu + j, ldg2(P.u + (size_t)src * n1 + j));
+                    }
+                }
+            }
+            __threadfence_system();
+            __syncthreads();
+            if (tid == 0) {
+                st_release_sys32(P.fl_dn_up + b, pbase);
+                st_release_sys32(P.fl_up_dn + b, pbase);
+            }
+        }
+    }
     double dd[K][5];
 #pragma unroll
     for (int k = 0; k < K; k++) coef_first5<K>(P, k, dd[k]);
@@ -574,13 +612,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d_tb2(const __grid_constan
             const double b1 = coef_beta(P, 2 * q + 1), b2 = two ? coef_beta(P, 2 * q + 2) : 0.0;
             const int rs = s / nb, b = s - rs * nb;
             const bool top = SLAB && rs == 0, bot = SLAB && rs == nsr - 1;
-            // SLAB, first pass: this rank's boundary rows of v (and u) into the neighbours' ghost blocks
-            if (SLAB && q == 0) {
-                if (top) tb2_deliver(P.v.base, 0, 4, P.hup_v, 2, b, lane, n1, P.fl_dn_up + b, pbase,
-                                     DIAG ? P.u : nullptr, P.hup_u);
-                if (bot) tb2_deliver(P.v.base, n - 2, 2, P.hdn_v, 0, b, lane, n1, P.fl_up_dn + b, pbase,
-                                     DIAG ? P.u : nullptr, P.hdn_u);
-            }
             // dependencies: pass q-1 done on the 3 x 3 neighbour segments (slab edges: the neighbour
             // rank's boundary segments, signalled by band flags after their halo rows landed here)
             if (lane < 9) {
@@ -629,7 +660,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d_tb2(const __grid_constan
             double acc[NV];
 #pragma unroll
             for (int i = 0; i < NV; i++) acc[i] = 0.0;
-            tb2_strip<K, DIAG, SLAB>(P, q == 0, two, T, c_b, c_e, lane, alpha, b1, b2, d0, da, db, act, acc, ring);
+            // boundary segment rows (the first and the last: their stencil halo reaches the periodic image or
+            // the ghost rows) take the checked row addressing, all others the direct one
+            tb2_strip<K, DIAG, SLAB>(P, q == 0, two, rs == 0 || rs == nsr - 1, T, c_b, c_e, lane, alpha, b1, b2, d0,
+                                     da, db, act, acc, ring);
             // SLAB: this pass's boundary rows of y into the neighbours' ghost blocks (+ their band flags)
             if (top) tb2_deliver(T.dst, 0, 4, P.hup[q & 1], 2, b, lane, n1, P.fl_dn_up + b, pbase + (unsigned)q + 1,
                                  nullptr, nullptr);
