@@ -488,10 +488,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d_tb2(const __grid_constan
     // final-pass parity of the last call with the same parameters (a small table written by each call's
     // leader): repeated calls then end in the caller's buffer and the fix-up copies nothing
     const unsigned long long key = tb2_call_key<K>(P);
-    int poff = 0, pslot = -1;
+    int poff = 0, pslot = -1, fpred = -2;
     for (int i = 0; i < kTb2Pred; i++)
         if (tc->pkey[i] == key) {
             poff = (int)(tc->pfin[i] & 1u);
+            fpred = (int)tc->pfin[i];
             pslot = i;
         }
     unsigned rel0 = 0;
@@ -590,6 +591,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d_tb2(const __grid_constan
                 if (!stop && q >= 1) {   // pass q-1 already known to end the call: nothing left to do
                     const unsigned long long w1 = ld_acquire64(&tc->dec[(q - 1) & 1]);
                     if (dec_tag(w1) == pbase + (unsigned)(q - 1) && dec_done(w1)) stop = 1;
+                }
+                if (!stop && q == fpred + 1) {
+                    // the last call with these parameters ended at pass q-1: rather than running pass q
+                    // speculatively (a pass of wasted HBM traffic when the prediction holds), wait for the
+                    // decision of pass q-1
+                    const unsigned long long w1 = tb2_wait_dec(P, pbase, q - 1);
+                    if (w1 <= kDecStop || dec_done(w1)) stop = 1;
                 }
             }
             if (__shfl_sync(FULL_MASK, stop, 0)) break;
