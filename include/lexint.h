@@ -92,6 +92,18 @@ lx_status lx_divided_differences(int l, const double *xi, int m, double dt, doub
 /* Rows [i_begin, i_end) of dimension 0 owned by `rank` of `nranks` slabs. */
 lx_status lx_slab_range(int64_t n0, int rank, int nranks, int64_t *i_begin, int64_t *i_end);
 
+/* Halo exchange plan of one rank (host only, no device): the +x-biased upwind stencil reaches rows i-1,
+ * i+1, i+2 (reading R10).  Writes up to max_ops ops of 5 ints {kind (0 = send, 1 = recv), peer,
+ * first local row (send; 0 for recv), row count, first ghost slot (at the peer for a send, at this rank for
+ * a recv)} in issue order and returns their number (-1 on bad arguments; max_ops >= 4).
+ *   mode 0: the step protocol, one Leja iteration per exchange: rows 0, 1 -> rank-1 (its rows n, n+1), row
+ *           n-1 -> rank+1 (its row -1); 3-row ghost block, slot 0 = row -1, slots 1, 2 = rows n, n+1.
+ *   mode 1: the two-step slab kernel, two iterations per exchange: rows 0..3 -> rank-1 (its rows n..n+3),
+ *           rows n-2, n-1 -> rank+1 (its rows -2, -1); 6-row ghost block, slots 0, 1 = rows -2, -1, slots
+ *           2..5 = rows n..n+3.
+ * The NCCL step protocol issues exactly these ops; the slab kernel's peer stores follow mode 1. */
+int lx_slab_halo_plan(int rank, int nranks, int64_t n_loc, int mode, int *ops, int max_ops);
+
 /* ------------------------------------------------------------------------ */
 /* Problem: du/dt = f(u) = A u + g(u)   (Eq. (1))                   */
 /*   A u  = diff * lap(u) + nu * sum_d D_d u                                */

@@ -45,7 +45,7 @@ EXPORTS = ("lx_last_error", "lx_version", "lx_leja_points", "lx_phi_scalar", "lx
            "lx_step_exprb42", "lx_step_epirk5p1",
            "lx_step", "lx_rhs", "lx_integrate", "lx_local_group_create", "lx_local_group_destroy", "lx_ctx_set_comm_local",
            "lx_real_leja_phi_cb", "lx_step_cb", "lx_builtin_rhs", "lx_ctx_set_comm_ex", "lx_ctx_set_comm_local_ex",
-           "lx_ctx_ipc_handle", "lx_ctx_set_comm_ipc", "lx_ctx_set_kernel")
+           "lx_ctx_ipc_handle", "lx_ctx_set_comm_ipc", "lx_ctx_set_kernel", "lx_slab_halo_plan")
 
 # void f(const double* in, double* out, void* user, void* cuda_stream)  (include/lexint.h lx_rhs_fn)
 RHS_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
@@ -141,6 +141,8 @@ def lib() -> ctypes.CDLL:
             "lx_ctx_ipc_handle": (ctypes.c_int, [vp, vp]),
             "lx_ctx_set_comm_ipc": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp]),
             "lx_ctx_set_kernel": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int]),
+            "lx_slab_halo_plan": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int,
+                                                 ctypes.POINTER(ctypes.c_int), ctypes.c_int]),
             "lx_real_leja_phi_cb": (ctypes.c_int, [vp, vp, vp, vp, vp, ctypes.POINTER(vp), dp, ctypes.c_int,
                                                    d, d, d, ctypes.c_int, d, d, ip]),
             "lx_step_cb": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, vp, vp, vp, dp, d, d, d, d, d, ip]),
@@ -191,6 +193,15 @@ def lx_divided_differences(l, xi, m, dt, c, gamma, a=1.0) -> np.ndarray:
     _check(lib().lx_divided_differences(int(l), xi.ctypes.data_as(dp), int(m), float(dt), float(c), float(gamma),
                                         float(a), d.ctypes.data_as(dp)))
     return d
+
+
+def lx_slab_halo_plan(rank: int, nranks: int, n_loc: int, mode: int) -> list:
+    """The library's halo exchange plan (lexint.h): [(kind, peer, first_row, nrows, ghost_slot)]."""
+    ops = (ctypes.c_int * 40)()
+    n = lib().lx_slab_halo_plan(int(rank), int(nranks), int(n_loc), int(mode), ops, 8)
+    if n < 0:
+        raise LxError(LX_ERR_ARG, "lx_slab_halo_plan: bad arguments")
+    return [("send" if ops[5 * i] == 0 else "recv",) + tuple(ops[5 * i + 1:5 * i + 5]) for i in range(n)]
 
 
 def lx_slab_range(n0: int, rank: int, nranks: int):

@@ -330,14 +330,14 @@ __global__ void __launch_bounds__(kThreads) k_bb_norm(BbLin L) {
 // (sums over d in dimension order starting from 0).  The FD Jacobian (f(u + eps y) - f(u))/eps divides
 // every rounding difference of f by eps ~ 1.5e-8 (R25); a deterministic, contraction-free f makes the
 // black-box path reproducible bit for bit wherever its inputs are (SURVEY 8(f) f-1 "FMA-off").
-__device__ __forceinline__ long long lit_wrap(long long i, long long n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
+__device__ __forceinline__ int lit_wrap(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
 
-__device__ __forceinline__ double lit_at(const RhsLit& R, long long i0, long long i1, long long i2, int d, int o,
-                                         bool sq) {
-    if (d == 0) i0 = lit_wrap(i0 + o, R.n[0]);
-    else if (d == 1) i1 = lit_wrap(i1 + o, R.n[1]);
-    else i2 = lit_wrap(i2 + o, R.n[2]);
-    const double v = R.in[(i0 * R.n[1] + i1) * R.n[2] + i2];
+// value of the input at offset o along dimension d from (i0, i1, i2); squared for the Burgers flux field
+__device__ __forceinline__ double lit_at(const RhsLit& R, int i0, int i1, int i2, int d, int o, bool sq) {
+    if (d == 0) i0 = lit_wrap(i0 + o, (int)R.n[0]);
+    else if (d == 1) i1 = lit_wrap(i1 + o, (int)R.n[1]);
+    else i2 = lit_wrap(i2 + o, (int)R.n[2]);
+    const double v = R.in[((size_t)i0 * R.n[1] + i1) * R.n[2] + i2];
     return sq ? __dmul_rn(v, v) : v;
 }
 
@@ -346,28 +346,35 @@ __device__ __forceinline__ double lit_upwind(double wm1, double w0, double w1, d
                      __dmul_rn(6.0, h));
 }
 
+// grid: x over the contiguous dimension, y over the rows (i0, i1) -- no 64-bit index division
 __global__ void __launch_bounds__(kThreads) k_rhs_literal(RhsLit R) {
-    const long long N = R.n[0] * R.n[1] * R.n[2];
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
-        const long long i2 = i % R.n[2], t = i / R.n[2];
-        const long long i1 = t % R.n[1], i0 = t / R.n[1];
-        double lap = 0.0, adv = 0.0, flx = 0.0;
-        for (int d = 0; d < R.ndim; d++) {
-            const double h = R.dx[d];
-            const double um1 = lit_at(R, i0, i1, i2, d, -1, false), u0 = lit_at(R, i0, i1, i2, d, 0, false);
-            const double up1 = lit_at(R, i0, i1, i2, d, 1, false), up2 = lit_at(R, i0, i1, i2, d, 2, false);
-            lap = __dadd_rn(lap, __ddiv_rn(__dadd_rn(__dsub_rn(up1, __dmul_rn(2.0, u0)), um1), __dmul_rn(h, h)));
-            adv = __dadd_rn(adv, lit_upwind(um1, u0, up1, up2, h));
-            if (R.flux != 0.0)
-                flx = __dadd_rn(flx, lit_upwind(lit_at(R, i0, i1, i2, d, -1, true), lit_at(R, i0, i1, i2, d, 0, true),
-                                                lit_at(R, i0, i1, i2, d, 1, true), lit_at(R, i0, i1, i2, d, 2, true), h));
+    // rows = all but the contiguous dimension (2D: dim 0; 3D: dims 0, 1)
+    const bool d3 = R.ndim == 3;
+    const int nrow = d3 ? (int)(R.n[0] * R.n[1]) : (int)R.n[0];
+    const int ninner = d3 ? (int)R.n[2] : (int)R.n[1];
+    for (int row = blockIdx.y; row < nrow; row += gridDim.y) {
+        const int r0 = d3 ? row / (int)R.n[1] : row, r1 = d3 ? row - r0 * (int)R.n[1] : 0;
+        for (int in = blockIdx.x * kThreads + threadIdx.x; in < ninner; in += gridDim.x * kThreads) {
+            const int i0 = r0, i1 = d3 ? r1 : in, i2 = d3 ? in : 0;
+            double lap = 0.0, adv = 0.0, flx = 0.0;
+            for (int d = 0; d < R.ndim; d++) {
+                const double h = R.dx[d];
+                const double um1 = lit_at(R, i0, i1, i2, d, -1, false), u0 = lit_at(R, i0, i1, i2, d, 0, false);
+                const double up1 = lit_at(R, i0, i1, i2, d, 1, false), up2 = lit_at(R, i0, i1, i2, d, 2, false);
+                lap = __dadd_rn(lap, __ddiv_rn(__dadd_rn(__dsub_rn(up1, __dmul_rn(2.0, u0)), um1), __dmul_rn(h, h)));
+                adv = __dadd_rn(adv, lit_upwind(um1, u0, up1, up2, h));
+                if (R.flux != 0.0)
+                    flx = __dadd_rn(flx, lit_upwind(lit_at(R, i0, i1, i2, d, -1, true), lit_at(R, i0, i1, i2, d, 0, true),
+                                                    lit_at(R, i0, i1, i2, d, 1, true), lit_at(R, i0, i1, i2, d, 2, true), h));
+            }
+            const size_t idx = (size_t)row * ninner + in;
+            double f = __dadd_rn(__dmul_rn(R.diff, lap), __dmul_rn(R.nu, adv));
+            if (R.flux != 0.0) f = __dadd_rn(f, __dmul_rn(__dmul_rn(R.flux, 0.5), flx));
+            const double u = R.in[idx];
+            if (R.react != 0.0) f = __dadd_rn(f, __dmul_rn(R.react, __dsub_rn(u, __dmul_rn(__dmul_rn(u, u), u))));
+            if (R.src) f = __dadd_rn(f, R.src[idx]);
+            R.out[idx] = f;
         }
-        double f = __dadd_rn(__dmul_rn(R.diff, lap), __dmul_rn(R.nu, adv));
-        if (R.flux != 0.0) f = __dadd_rn(f, __dmul_rn(__dmul_rn(R.flux, 0.5), flx));
-        const double u = R.in[i];
-        if (R.react != 0.0) f = __dadd_rn(f, __dmul_rn(R.react, __dsub_rn(u, __dmul_rn(__dmul_rn(u, u), u))));
-        if (R.src) f = __dadd_rn(f, R.src[i]);
-        R.out[i] = f;
     }
 }
 
@@ -406,7 +413,12 @@ cudaError_t launch_bb_lincomb(const BbLin& L, cudaStream_t s) {
     return cudaGetLastError();
 }
 cudaError_t launch_rhs_literal(const RhsLit& R, int grid, cudaStream_t s) {
-    k_rhs_literal<<<grid, kThreads, 0, s>>>(R);
+    const long long nrow = R.ndim == 3 ? R.n[0] * R.n[1] : R.n[0];
+    const long long ninner = R.ndim == 3 ? R.n[2] : R.n[1];
+    const int gx = (int)((ninner + kThreads - 1) / kThreads);
+    const int gy = (int)(nrow < 65535 ? nrow : 65535);
+    (void)grid;
+    k_rhs_literal<<<dim3(gx, gy), kThreads, 0, s>>>(R);
     return cudaGetLastError();
 }
 cudaError_t launch_bb_norm(const BbLin& L, cudaStream_t s) {

@@ -43,6 +43,26 @@ static int cerr(const std::string& m) {
         if (e_ != cudaSuccess) return cerr(std::string(#x ": ") + cudaGetErrorString(e_));  \
     } while (0)
 
+// The halo exchange plan of one rank: ops of 5 ints {kind (0 send, 1 recv), peer, first local row
+// (send) / 0, row count, first ghost slot (at the peer for a send, here for a recv)}, in the order the
+// transport issues them ("up" then "down", so that with two ranks -- both neighbours the same peer -- the
+// messages still match one to one).  mode 0: the step protocol (3-row ghost block: slot 0 = row -1, slots 1, 2
+// = rows n, n+1); mode 1: the two-step slab kernel's deliveries (6-row ghost block: slots 0, 1 = rows -2, -1,
+// slots 2..5 = rows n..n+3).
+int comm_halo_plan(int rank, int nranks, int n_loc, int mode, int* ops, int max_ops) {
+    if (nranks < 1 || rank < 0 || rank >= nranks || max_ops < 4 || (mode != 0 && mode != 1)) return -1;
+    const int up = (rank - 1 + nranks) % nranks, dn = (rank + 1) % nranks;
+    const int nu = mode ? kTb2UpRows : kStepUpRows, nd = mode ? kTb2DnRows : kStepDnRows;
+    const int gup = mode ? 2 : 1, gdn = 0;   // ghost slot of the first row received from below / above
+    const int o[4][5] = {{0, up, 0, nu, gup},            // my first rows -> rank-1's rows n..
+                         {1, dn, 0, nu, gup},            // rank+1's first rows -> my rows n..
+                         {0, dn, n_loc - nd, nd, gdn},   // my last rows -> rank+1's rows -nd..-1
+                         {1, up, 0, nd, gdn}};           // rank-1's last rows -> my rows -nd..-1
+    for (int i = 0; i < 4; i++)
+        for (int j = 0; j < 5; j++) ops[5 * i + j] = o[i][j];
+    return 4;
+}
+
 struct Transport {
     int rank = 0, nranks = 1;
     virtual ~Transport() {}
@@ -74,15 +94,20 @@ struct NcclTransport : Transport {
     ~NcclTransport() override {
         if (comm) ncclCommDestroy(comm);
     }
+    // the step protocol's halo (comm_halo_plan mode 0) as one NCCL group
+    int issue_halo(const double* base, double* ghost, int n_loc, long long row, cudaStream_t s) {
+        int ops[20];
+        const int nop = comm_halo_plan(rank, nranks, n_loc, 0, ops, 4);
+        for (int i = 0; i < nop; i++) {
+            const int* o = ops + 5 * i;
+            if (o[0] == 0) NC(ncclSend(base + (long long)o[2] * row, (size_t)o[3] * row, ncclDouble, o[1], comm, s));
+            else NC(ncclRecv(ghost + (long long)o[4] * row, (size_t)o[3] * row, ncclDouble, o[1], comm, s));
+        }
+        return 0;
+    }
     int exchange_rows(const double* base, double* ghost, int n_loc, long long row, cudaStream_t s) override {
-        const int up = (rank - 1 + nranks) % nranks, down = (rank + 1) % nranks;
         NC(ncclGroupStart());
-        // direction "up": my rows 0,1 -> ghost rows n, n+1 of rank r-1; I receive rank r+1's rows 0,1
-        NC(ncclSend(base, 2 * row, ncclDouble, up, comm, s));
-        NC(ncclRecv(ghost + row, 2 * row, ncclDouble, down, comm, s));
-        // direction "down": my last row -> ghost row -1 of rank r+1; I receive rank r-1's last row
-        NC(ncclSend(base + (long long)(n_loc - 1) * row, row, ncclDouble, down, comm, s));
-        NC(ncclRecv(ghost, row, ncclDouble, up, comm, s));
+        if (issue_halo(base, ghost, n_loc, row, s)) return 1;
         NC(ncclGroupEnd());
         return 0;
     }
@@ -98,12 +123,8 @@ struct NcclTransport : Transport {
     // aggregated into a single launch (halves the per-iteration NCCL launches of the slab protocol)
     int exchange_and_gather(const double* base, double* ghost, int n_loc, long long row, const double* send,
                             double* recv, int count, cudaStream_t s) override {
-        const int up = (rank - 1 + nranks) % nranks, down = (rank + 1) % nranks;
         NC(ncclGroupStart());
-        NC(ncclSend(base, 2 * row, ncclDouble, up, comm, s));
-        NC(ncclRecv(ghost + row, 2 * row, ncclDouble, down, comm, s));
-        NC(ncclSend(base + (long long)(n_loc - 1) * row, row, ncclDouble, down, comm, s));
-        NC(ncclRecv(ghost, row, ncclDouble, up, comm, s));
+        if (issue_halo(base, ghost, n_loc, row, s)) return 1;
         NC(ncclAllGather(send, recv, count, ncclDouble, comm, s));
         NC(ncclGroupEnd());
         return 0;

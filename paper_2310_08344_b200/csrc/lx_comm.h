@@ -10,6 +10,7 @@ namespace lx {
 struct Comm;
 const char* comm_error();
 int comm_unique_id(void* out128);
+int comm_halo_plan(int rank, int nranks, int n_loc, int mode, int* ops, int max_ops);
 int comm_create(const void* uid, int rank, int nranks, int device, long long row, int max_grid, Comm** out);
 struct LocalGroup;
 LocalGroup* local_group_create(int nranks);

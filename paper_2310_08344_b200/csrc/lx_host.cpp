@@ -100,6 +100,7 @@ struct lx_ctx {
     double* tb2_grp_part = nullptr;       // [2][cap/32+1][2(1+kMaxK)]
     unsigned* tb2_grp_cnt = nullptr;      // [2][cap/32+1]
     void* ipc_blk = nullptr;              // exchange block handed out by lx_ctx_ipc_handle (before set_comm_ipc)
+    bool bb_literal = true;               // lx_builtin_rhs: literal formula order (FD mode) or fused stencil
     // pipelined host-buffer staging of Leja calls (pinned host memory): two slots, copy-in / copy-out streams
     cudaStream_t s_in = nullptr, s_out = nullptr;
     double* pin_in[2] = {};
@@ -510,6 +511,11 @@ lx_status lx_divided_differences(int l, const double* xi, int m, double dt, doub
     if (s == 4) return fail(LX_ERR_UNSUPPORTED, "phi_%d not supported", l);
     if (s == 6) return fail(LX_ERR_NONFINITE, "divided differences overflow");
     return LX_OK;
+}
+
+int lx_slab_halo_plan(int rank, int nranks, int64_t n_loc, int mode, int* ops, int max_ops) {
+    if (!ops) return -1;
+    return comm_halo_plan(rank, nranks, (int)n_loc, mode, ops, max_ops);
 }
 
 lx_status lx_slab_range(int64_t n0, int rank, int nranks, int64_t* i_begin, int64_t* i_end) {
@@ -1624,6 +1630,9 @@ static lx_status bb_setup(lx_ctx* ctx, BbRun& R, lx_rhs_fn f, void* user, const 
     R.u = u;
     R.fu = nullptr;
     R.rec = 0;
+    // FD Jacobians (u given) divide f's rounding differences by eps: the built-in f then runs in the literal,
+    // contraction-free formula order (R30); a linear black-box operator uses the fused stencil
+    ctx->bb_literal = u != nullptr;
     CUDA_TRY(cudaMemsetAsync(ctx->bb, 0, sizeof(BbCtrl), ctx->stream));
     if (u) {
         double* fu = bb_vec(ctx, BB_FU);
@@ -1789,7 +1798,7 @@ void lx_builtin_rhs(const double* in, double* out, void* user, void* cuda_stream
     const lx_builtin_rhs_user* b = (const lx_builtin_rhs_user*)user;
     if (!b || !b->ctx || !b->pb) return;
     lx_ctx* ctx = b->ctx;
-    if (ctx->comm) {   // slab contexts: the fused stencil with halos
+    if (ctx->comm || !ctx->bb_literal) {   // slab contexts / a linear black-box operator: the fused stencil
         rhs_device(ctx, b->pb, in, 1.0, out);
         return;
     }

@@ -23,6 +23,12 @@ __host__ __device__ constexpr int tb2_depth(int K, bool diag) { return tb2_stage
 __host__ __device__ constexpr int tb2_smem_bytes(int K, bool diag) { return 8 * tb2_depth(K, diag) * tb2_stage_bytes(K, diag); }
 constexpr int kBand2 = 60;        // output columns per warp band of the two-step kernel (64 loaded)
 constexpr int kMaxK = 4;          // vertical accumulators
+// Slab halos (the +x-biased upwind stencil reaches rows i-1, i+1, i+2, reading R10):
+//   step protocol (one iteration per exchange): rows 0, 1 -> rank-1 (its rows n, n+1), row n-1 -> rank+1 (its row -1)
+//   two-step slab kernel (two iterations per exchange): rows 0..3 -> rank-1 (its rows n..n+3), rows n-2, n-1 ->
+//   rank+1 (its rows -2, -1); ghost blocks of 3 and 6 rows respectively (comm_halo_plan, lx_slab_halo_plan)
+constexpr int kStepUpRows = 2, kStepDnRows = 1;
+constexpr int kTb2UpRows = 4, kTb2DnRows = 2;
 constexpr int kSlot = 12;         // doubles per CTA partial slot (2 (1 + K) <= 10 for two-step passes)
 
 // Per-call record, written on the device, read by the host once per call/step.

@@ -673,9 +673,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_leja2d_tb2(const __grid_constan
             tb2_strip<K, DIAG, SLAB>(P, q == 0, two, rs == 0 || rs == nsr - 1, T, c_b, c_e, lane, alpha, b1, b2, d0,
                                      da, db, act, acc, ring);
             // SLAB: this pass's boundary rows of y into the neighbours' ghost blocks (+ their band flags)
-            if (top) tb2_deliver(T.dst, 0, 4, P.hup[q & 1], 2, b, lane, n1, P.fl_dn_up + b, pbase + (unsigned)q + 1,
-                                 nullptr, nullptr);
-            if (bot) tb2_deliver(T.dst, n - 2, 2, P.hdn[q & 1], 0, b, lane, n1, P.fl_up_dn + b,
+            // (the rows / ghost slots of lx_slab_halo_plan mode 1)
+            if (top) tb2_deliver(T.dst, 0, kTb2UpRows, P.hup[q & 1], 2, b, lane, n1, P.fl_dn_up + b,
+                                 pbase + (unsigned)q + 1, nullptr, nullptr);
+            if (bot) tb2_deliver(T.dst, n - kTb2DnRows, kTb2DnRows, P.hdn[q & 1], 0, b, lane, n1, P.fl_up_dn + b,
                                  pbase + (unsigned)q + 1, nullptr, nullptr);
             // the segment is done with pass q: its norm partials, then ONE fence (ordering this warp's y / p
             // stores and the partials) before the completion tag and the group counter

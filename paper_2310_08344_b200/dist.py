@@ -5,15 +5,12 @@ the library's own communicator is broadcast with ``broadcast_object_list``,
 timings are reduced with MAX.  The per-iteration halo exchange and the partial
 gather run inside liblexint_b200.so (csrc/lx_comm.cpp) on the context stream.
 
-``halo_plan`` states the exchange protocol of csrc/lx_comm.cpp in host terms
-(which rows go to which peer, in which order); the CPU gloo tests drive an
-oracle-based emulation of the slab path with it.
+The exchange plan itself is the library's (``lx_slab_halo_plan``); the CPU gloo
+tests drive an oracle-based emulation of both slab protocols with it.
 """
 from __future__ import annotations
 
 import os
-from dataclasses import dataclass
-
 from . import Context, lx_nccl_unique_id, lx_slab_range
 
 
@@ -49,22 +46,6 @@ def max_over_ranks(x: float, device=None) -> float:
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
-
-
-@dataclass(frozen=True)
-class HaloOp:
-    kind: str        # "send" | "recv"
-    peer: int
-    rows: tuple      # local rows (send) or ghost slots (recv): ghost slot 0 = row -1, 1..2 = rows n, n+1
-
-
-def halo_plan(rank: int, world: int, n_loc: int) -> list:
-    """Ordered point-to-point operations of one halo exchange (csrc/lx_comm.cpp):
-    the +x-biased upwind stencil (reading R10) reaches rows i-1, i+1, i+2, so a
-    slab needs 1 ghost row from rank r-1 and 2 from rank r+1 (periodic in rank)."""
-    up, down = (rank - 1) % world, (rank + 1) % world
-    return [HaloOp("send", up, (0, 1)), HaloOp("recv", down, (1, 2)),
-            HaloOp("send", down, (n_loc - 1,)), HaloOp("recv", up, (0,))]
 
 
 def slabs(n0: int, world: int) -> list:

@@ -2,10 +2,12 @@
 
 * the NCCL unique id bootstrap through torch.distributed (same 128 bytes on all ranks);
 * slab ranges, max-over-ranks timing reduction;
-* an oracle-based emulation of the slab Leja iteration that follows the product's
-  exchange protocol (dist.halo_plan, executed with gloo send/recv) and the
-  rank-order sum of gathered partials: the fields must equal the single-domain
-  oracle BITWISE and stop at the same iteration.
+* oracle-based emulations of the two slab protocols that follow the LIBRARY's exchange plan
+  (lx_slab_halo_plan from liblexint_b200.so, host-only, executed with gloo send/recv) and the
+  rank-order sum of the per-rank partials: mode 0, the step protocol (one Leja iteration per
+  exchange, 3 ghost rows); mode 1, the two-step slab kernel (two iterations per exchange, 6 ghost
+  rows, the first iteration recomputed on the halo-extended slab).  The fields must equal the
+  single-domain oracle BITWISE and stop at the same iteration.
 """
 import os
 import socket
@@ -27,24 +29,26 @@ def _free_port():
     return p
 
 
-def _exchange(slab_gh, n_loc, rank, world):
-    """Fill ghost rows of slab_gh (rows -1..n_loc+1 stored at 0..n_loc+2) per halo_plan."""
-    from paper_2310_08344_b200.dist import halo_plan
+def _exchange(gh, n_loc, rank, world, mode):
+    """Fill the ghost rows of gh (local rows stored from index G, G = 1 (mode 0) or 2 (mode 1); ghost slot
+    0.. = rows -G..-1, then rows n_loc.. ) per the library's plan."""
+    from paper_2310_08344_b200 import lx_slab_halo_plan
+    G = 1 if mode == 0 else 2
     reqs = []
-    for op in halo_plan(rank, world, n_loc):
-        if op.kind == "send":
-            buf = torch.from_numpy(np.ascontiguousarray(slab_gh[[r + 1 for r in op.rows]]))
-            reqs.append(dist.isend(buf, op.peer))
+    for kind, peer, first, nrows, slot in lx_slab_halo_plan(rank, world, n_loc, mode):
+        if kind == "send":
+            buf = torch.from_numpy(np.ascontiguousarray(gh[G + first:G + first + nrows]))
+            reqs.append(dist.isend(buf, peer))
         else:
-            buf = torch.empty((len(op.rows),) + slab_gh.shape[1:], dtype=torch.float64)
-            dist.recv(buf, op.peer)
-            slots = [0] if op.rows == (0,) else [n_loc + 1, n_loc + 2]
-            slab_gh[slots] = buf.numpy()
+            buf = torch.empty((nrows,) + gh.shape[1:], dtype=torch.float64)
+            dist.recv(buf, peer)
+            rows = [slot + i if slot + i < G else n_loc + slot + i for i in range(nrows)]   # slot -> gh index
+            gh[rows] = buf.numpy()
     for r in reqs:
         r.wait()
 
 
-def _worker(rank, world, port, result_dir):
+def _worker(rank, world, port, result_dir, mode):
     import sys
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -63,7 +67,7 @@ def _worker(rank, world, port, result_dir):
     sl = lxd.slabs(n0, world)
     b, e = sl[rank]
     assert lxd.max_over_ranks(float(rank) + 0.5) == world - 0.5
-    # 3. emulated slab Leja iteration (oracle arithmetic, product protocol)
+    # 3. emulated slab Leja iterations (oracle arithmetic, the library's exchange plan)
     shape = (n0, n1)
     dx = (2.0 / n0, 2.0 / n1)
     pb = O.Problem(shape, dx, 1.0, 10.0, 0.0)
@@ -73,40 +77,64 @@ def _worker(rank, world, port, result_dir):
     c, g = O.shift_scale(O.spectrum_bound(pb))
     d = O.divided_differences(1, xi, 300, dt, c, g)
     n_loc = e - b
-    y = np.zeros((n_loc + 3, n1))
-    y[1:n_loc + 1] = v[b:e]
-    p = d[0] * v[b:e]
     N = n0 * n1
-    iters = None
-    for m in range(1, 300):
-        _exchange(y, n_loc, rank, world)
-        w = O.jac_apply_slab(pb, n_loc, None, y)
-        yin = y[1:n_loc + 1]
-        ynew = (w - c * yin) / g - xi[m - 1] * yin
-        p = p + d[m] * ynew
-        y[1:n_loc + 1] = ynew
-        part = torch.tensor([np.sum(ynew * ynew), np.sum(p * p)], dtype=torch.float64)
+    G = 1 if mode == 0 else 2
+    y = np.zeros((n_loc + G + (2 if mode == 0 else 4), n1))   # ghost rows -G..-1, local rows, ghost rows n..
+    y[G:G + n_loc] = v[b:e]
+    p = d[0] * v[b:e]
+
+    def step(ygh_ext, n_ext, m):
+        # one Leja iteration (Eq. (2)) on n_ext rows whose ghosted input ygh_ext has 1 row before, 2 after
+        w = O.jac_apply_slab(pb, n_ext, None, ygh_ext)
+        yin = ygh_ext[1:n_ext + 1]
+        return (w - c * yin) / g - xi[m - 1] * yin
+
+    def converged(m, ynew, pnew):
+        part = torch.tensor([np.sum(ynew * ynew), np.sum(pnew * pnew)], dtype=torch.float64)
         allp = [torch.zeros(2, dtype=torch.float64) for _ in range(world)]
         dist.all_gather(allp, part)
-        sy = 0.0
-        sp = 0.0
+        sy = sp = 0.0
         for t in allp:            # rank order
             sy += float(t[0])
             sp += float(t[1])
-        if abs(d[m]) * np.sqrt(sy / N) <= 1e-10 * np.sqrt(sp / N) + 1e-10:
-            iters = m
-            break
+        return abs(d[m]) * np.sqrt(sy / N) <= 1e-10 * np.sqrt(sp / N) + 1e-10
+
+    iters = None
+    m = 1
+    while m < 300 and iters is None:
+        _exchange(y, n_loc, rank, world, mode)
+        if mode == 0:
+            ynew = step(y, n_loc, m)
+            p = p + d[m] * ynew
+            y[1:n_loc + 1] = ynew
+            if converged(m, ynew, p):
+                iters = m
+            m += 1
+        else:
+            # two iterations per exchange: y_m on rows -1 .. n+1 from y_{m-1} rows -2 .. n+3, then y_{m+1}
+            ym_ext = step(y, n_loc + 3, m)                 # rows -1 .. n+1
+            ym = ym_ext[1:n_loc + 1]
+            p = p + d[m] * ym
+            if converged(m, ym, p):
+                iters = m
+                break
+            ym1 = step(ym_ext, n_loc, m + 1)
+            p = p + d[m + 1] * ym1
+            y[2:n_loc + 2] = ym1
+            if converged(m + 1, ym1, p):
+                iters = m + 1
+            m += 2
     np.save(os.path.join(result_dir, "p%d.npy" % rank), p)
     np.save(os.path.join(result_dir, "it%d.npy" % rank), np.array([iters, b, e]))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_gloo_slab_protocol(tmp_path, world):
+@pytest.mark.parametrize("world,mode", [(2, 0), (3, 0), (2, 1), (3, 1)])
+def test_gloo_slab_protocol(tmp_path, world, mode):
     import oracle as O
     import workloads as W
-    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path), mode), nprocs=world, join=True,
                        start_method="spawn")
     n0, n1 = 40, 24
     pb = O.Problem((n0, n1), (2.0 / n0, 2.0 / n1), 1.0, 10.0, 0.0)
@@ -123,3 +151,22 @@ def test_gloo_slab_protocol(tmp_path, world):
     # the recurrence's field values are bitwise those of the single-domain oracle
     # (only the norm summation order differs); literal (w - c y)/gamma form as the oracle
     np.testing.assert_array_equal(np.concatenate(parts), ref.outs[0])
+
+
+def test_halo_plan_shapes():
+    # the plan's rows reach what the +x-biased stencil needs (i-1, i+1, i+2 per iteration; twice that for
+    # the two-step kernel), sends and receives pair up across ranks, and two ranks still match in order
+    from paper_2310_08344_b200 import lx_slab_halo_plan
+    for world in (1, 2, 3, 8):
+        for mode, (nu, nd) in ((0, (2, 1)), (1, (4, 2))):
+            plans = [lx_slab_halo_plan(r, world, 16, mode) for r in range(world)]
+            for r, plan in enumerate(plans):
+                assert [op[0] for op in plan] == ["send", "recv", "send", "recv"]
+                assert plan[0][1] == (r - 1) % world and plan[0][2:4] == (0, nu)
+                assert plan[2][1] == (r + 1) % world and plan[2][2:4] == (16 - nd, nd)
+                # my i-th send is received by its peer as that peer's op with the same direction
+                for i in (0, 2):
+                    peer = plan[i][1]
+                    recv = plans[peer][i + 1]
+                    assert recv[0] == "recv" and recv[1] == r and recv[3] == plan[i][3]
+                    assert recv[4] == plan[i][4]
