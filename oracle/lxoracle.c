@@ -626,7 +626,7 @@ done:
 /* Exponential integrators (listings alg:Ros_Eu, alg:exprb32;      */
 /* EXPRB43 and EPIRK4s3A tableaux from P:83's citations, R17).                */
 /*   method 0 Rosenbrock-Euler, 1 EXPRB32, 2 EXPRB43, 3 EPIRK4s3A, 4 EXPRB42,    */
-/*   5 EPIRK5P1, 6 EXPRB53s3.                                                  */
+/*   5 EPIRK5P1, 6 EXPRB53s3, 7 EXPRB54s4.                                      */
 /* u_low may be NULL for Rosenbrock-Euler (non-embedded, err = 0).            */
 /* ------------------------------------------------------------------------- */
 static void axpby(double a, const double *x, double b, const double *y, double *z, long N)
@@ -651,7 +651,7 @@ int oc_step_ex(const oc_problem *pb, int jac_mode, int method, const double *u, 
     int it = 0, total = 0, s = OC_OK;
     if (err) *err = 0.0;
     if (iters) *iters = 0;
-    if (method < 0 || method > 6) return OC_ERR_ARG;
+    if (method < 0 || method > 7) return OC_ERR_ARG;
     if (jac_mode != OC_JAC_EXACT && jac_mode != OC_JAC_FD) return OC_ERR_ARG;
     size_t bytes = sizeof(double) * (size_t)N;
     double *fu_raw = NULL;
@@ -800,6 +800,77 @@ int oc_step_ex(const oc_problem *pb, int jac_mode, int method, const double *u, 
         if (s) goto out;
         for (long i = 0; i < N; i++) u_high[i] = u[i] + t3[i] + t4[i] + t5[i];   /* u5 */
         for (long i = 0; i < N; i++) u_low[i] = u[i] + t3[i] + 8.0 * t7[i];      /* u3 */
+        for (long i = 0; i < N; i++) t1[i] = u_high[i] - u_low[i];
+        if (err) *err = oc_l2norm_scaled(t1, N);
+    } else if (method == 7) {
+        /* EXPRB54s4 (Luan & Ostermann 2014, cited at P:83; reading R31), D_x = h (F(x) - F(u)),
+         * nodes c2 = 1/4, c3 = 1/2, c4 = 9/10:
+         *   U2 = u + c2 h phi_1(c2 hJ) f
+         *   U3 = u + c3 h phi_1(c3 hJ) f + 4 phi_3(c3 hJ) D2
+         *   U4 = u + c4 h phi_1(c4 hJ) f + phi_3(c4 hJ)(5832/125 D2 - 729/125 D3)
+         *                                 + phi_4(c4 hJ)(-157464/625 D2 + 39366/625 D3)
+         *   u5 = u + h phi_1(hJ) f + phi_3(hJ)(18 D3 - 250/81 D4) + phi_4(hJ)(-60 D3 + 500/27 D4)
+         *   u4 = u + h phi_1(hJ) f + phi_3(hJ)(64 D2 - 8 D3) + phi_4(hJ)(-384 D2 + 96 D3)   (embedded, order 4)
+         *   err = ||u5 - u4|| */
+        double cf4[4] = {0.25, 0.5, 0.9, 1.0};
+        double *pv[4] = {t1, t2, t3, t7};                    /* phi_1(c hJ) hf, c = 1/4, 1/2, 9/10, 1 */
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, f_u, pv, cf4, 4, dt, c, gamma, 1, rtol, atol, xi,
+                                max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        remainder_mode(pb, jac_mode, u, fu_raw, u, t4);      /* NL_u */
+        axpby(1.0, u, 0.25, t1, t5, N);                      /* U2 */
+        remainder_mode(pb, jac_mode, u, fu_raw, t5, t6);
+        axpby(dt, t6, -dt, t4, t5, N);                       /* D2 */
+        double half = 0.5, c4 = 0.9, one = 1.0;
+        double *o1[1] = {t1};
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, t5, o1, &half, 1, dt, c, gamma, 3, rtol, atol, xi,
+                                max_nodes, &it, NULL);                               /* phi_3(hJ/2) D2 */
+        total += it;
+        if (s) goto out;
+        for (long i = 0; i < N; i++) t6[i] = u[i] + 0.5 * t2[i] + 4.0 * t1[i];     /* U3 */
+        remainder_mode(pb, jac_mode, u, fu_raw, t6, u_low);
+        axpby(dt, u_low, -dt, t4, t6, N);                    /* D3 */
+        axpby(5832.0 / 125.0, t5, -729.0 / 125.0, t6, t1, N);
+        axpby(-157464.0 / 625.0, t5, 39366.0 / 625.0, t6, t2, N);
+        double *o2[1] = {u_low};
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, t1, o2, &c4, 1, dt, c, gamma, 3, rtol, atol, xi,
+                                max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        double *o3[1] = {u_high};
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, t2, o3, &c4, 1, dt, c, gamma, 4, rtol, atol, xi,
+                                max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        for (long i = 0; i < N; i++) t1[i] = u[i] + 0.9 * t3[i] + u_low[i] + u_high[i];   /* U4 */
+        remainder_mode(pb, jac_mode, u, fu_raw, t1, t2);
+        axpby(dt, t2, -dt, t4, t3, N);                       /* D4 */
+        axpby(64.0, t5, -8.0, t6, t1, N);                    /* embedded: 64 D2 - 8 D3, -384 D2 + 96 D3 */
+        axpby(-384.0, t5, 96.0, t6, t2, N);
+        double *o4[1] = {t4};
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, t1, o4, &one, 1, dt, c, gamma, 3, rtol, atol, xi,
+                                max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        double *o5[1] = {u_low};
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, t2, o5, &one, 1, dt, c, gamma, 4, rtol, atol, xi,
+                                max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        for (long i = 0; i < N; i++) u_low[i] = u[i] + t7[i] + t4[i] + u_low[i];  /* u4 */
+        axpby(18.0, t6, -250.0 / 81.0, t3, t1, N);           /* 18 D3 - 250/81 D4 */
+        axpby(-60.0, t6, 500.0 / 27.0, t3, t2, N);           /* -60 D3 + 500/27 D4 */
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, t1, o4, &one, 1, dt, c, gamma, 3, rtol, atol, xi,
+                                max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        double *o6[1] = {t5};
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, t2, o6, &one, 1, dt, c, gamma, 4, rtol, atol, xi,
+                                max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        for (long i = 0; i < N; i++) u_high[i] = u[i] + t7[i] + t4[i] + t5[i];   /* u5 */
         for (long i = 0; i < N; i++) t1[i] = u_high[i] - u_low[i];
         if (err) *err = oc_l2norm_scaled(t1, N);
     } else {

@@ -155,7 +155,8 @@ def test_leja_noconv_and_errors(xi300):
 
 
 # ---------------------------------------------------------------- integrators
-@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3"])
+@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3",
+                                    "exprb54s4"])
 def test_integrator_linear_exactness(xi300, method):
     # every exponential integrator is exact on linear homogeneous problems
     n = 64
@@ -463,3 +464,34 @@ def test_openmp_oracle_build_is_bit_identical(xi300):
     assert res[0][0] == res[1][0] and res[0][2] == res[1][2]
     for a, b in zip(res[0][1], res[1][1]):
         np.testing.assert_array_equal(a, b)
+
+
+def test_exprb54s4_orders(xi300):
+    # EXPRB54s4 (reading R31): fifth-order solution and fourth-order embedded solution on Allen-Cahn.  Its
+    # fourth stage carries D2 AND D3 (both stiff stage conditions psi_3 = psi_4 = 0 at c4 = 9/10), which makes
+    # its error constant far smaller than EXPRB53s3's (a D3-only fourth stage is an ordinary order-5 method
+    # with EXPRB53s3-sized errors) -- pinned as a ratio, together with the orders
+    n = 16
+    pb = O.Problem((n, n), (2 / n, 2 / n), 2e-3, 0.0, 1.0)
+    u0 = W.ic_allen_cahn_2d(n)
+    T = 0.5
+    uref = _allen_cahn_reference(pb, u0, T)
+    res = {}
+    for method, attr in (("exprb54s4", "u_high"), ("exprb54s4", "u_low"), ("exprb53s3", "u_high")):
+        errs = []
+        for nsteps in (8, 16, 32):
+            u = u0.copy()
+            for _ in range(nsteps):
+                c, g = _cg(pb, u)
+                r = O.step(pb, method, u, T / nsteps, c, g, 1e-14, 1e-14, xi300)
+                assert r.status == O.OK
+                assert r.err == pytest.approx(O.l2norm_scaled(r.u_high - r.u_low), rel=1e-12)
+                u = getattr(r, attr)
+            errs.append(np.linalg.norm(u - uref) / np.linalg.norm(uref))
+        res[(method, attr)] = (errs, np.log2(np.array(errs[:-1]) / np.array(errs[1:])))
+    e5, o5 = res[("exprb54s4", "u_high")]
+    e4, o4 = res[("exprb54s4", "u_low")]
+    e53, _ = res[("exprb53s3", "u_high")]
+    assert abs(o5[-1] - 5.0) < 0.35, res
+    assert np.all(np.abs(o4 - 4.0) < 0.3), res
+    assert e5[-1] < 0.3 * e53[-1], res
