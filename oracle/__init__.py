@@ -95,6 +95,11 @@ def lib():
         L.oc_step_ex.argtypes = [pp, ctypes.c_int, ctypes.c_int, dp, dp, dp, dp, ctypes.c_double,
                                  ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, dp,
                                  ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+        L.oc_integrate_adaptive.restype = ctypes.c_int
+        L.oc_integrate_adaptive.argtypes = [pp, ctypes.c_int, dp, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                            ctypes.c_double, ctypes.c_double, dp, ctypes.c_int, ctypes.c_int,
+                                            ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), dp, dp,
+                                            ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
         L.oc_step.restype = ctypes.c_int
         L.oc_step.argtypes = [pp, ctypes.c_int, dp, dp, dp, dp, ctypes.c_double, ctypes.c_double,
                               ctypes.c_double, ctypes.c_double, ctypes.c_double, dp, ctypes.c_int,
@@ -300,3 +305,32 @@ def step(pb: Problem, method: str, u, dt, c, gamma, rtol, atol, xi, max_nodes=No
                       float(dt), float(c), float(gamma), float(rtol), float(atol), _dp(xi),
                       int(max_nodes), ctypes.byref(it))
     return StepResult(lo, hi, float(err[0]), it.value, s)
+
+
+@dataclass
+class AdaptiveResult:
+    u: np.ndarray
+    accepted: int
+    rejected: int
+    dts: np.ndarray        # every attempted step size, in order
+    errs: np.ndarray       # its embedded error estimate
+    acc: np.ndarray        # accepted?
+    iters: int
+    status: int
+
+
+def integrate_adaptive(pb: Problem, method: str, u0, t_end, dt0, tol, rtol, atol, xi, max_nodes=None,
+                       max_steps: int = 1000) -> AdaptiveResult:
+    """Embedded-error step-size control (reading R32): see oc_integrate_adaptive."""
+    u = _vec(u0, pb).copy()
+    xi = _vec(xi)
+    max_nodes = len(xi) if max_nodes is None else max_nodes
+    dts, errs = np.zeros(max_steps), np.zeros(max_steps)
+    acc = np.zeros(max_steps, dtype=np.int32)
+    na, nr, it = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0)
+    s = lib().oc_integrate_adaptive(ctypes.byref(pb.c_struct()), METHODS[method], _dp(u), float(t_end), float(dt0),
+                                    float(tol), float(rtol), float(atol), _dp(xi), int(max_nodes), int(max_steps),
+                                    ctypes.byref(na), ctypes.byref(nr), _dp(dts), _dp(errs),
+                                    acc.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), ctypes.byref(it))
+    k = na.value + nr.value
+    return AdaptiveResult(u, na.value, nr.value, dts[:k], errs[:k], acc[:k].astype(bool), it.value, s)

@@ -943,3 +943,75 @@ int oc_step(const oc_problem *pb, int method, const double *u, double *u_low, do
     return oc_step_ex(pb, OC_JAC_EXACT, method, u, u_low, u_high, err, dt, c, gamma, rtol, atol, xi, max_nodes,
                       iters);
 }
+
+/* ------------------------------------------------------------------------- */
+/* Step-size control by the embedded error ("may be used to control the */
+/* step sizes"; reading R32): the elementary controller                        */
+/*   accept iff err <= tol;  h_new = h min(5, max(0.2, 0.9 (tol/err)^(1/(q+1)))) */
+/* (err = 0 -> 5), q = order of the embedded (lower-order) solution; the last  */
+/* step is clipped to land on t_end; a step whose Leja calls fail (NOCONV,     */
+/* NONFINITE) counts as rejected with err = inf (factor 0.2).                  */
+/* (c, gamma) from the Gershgorin / closed-                                    */
+/* form bound of the current state.  u is overwritten with u(t_end).*/
+/* log_dt / log_err / log_acc (max_steps entries each) record every attempt.   */
+/* ------------------------------------------------------------------------- */
+static int oc_embedded_order(int method)
+{
+    switch (method) {
+    case 1: return 2;   /* EXPRB32: a */
+    case 2: return 3;   /* EXPRB43: u_3 */
+    case 3: return 3;   /* EPIRK4s3A: u_3 */
+    case 6: return 3;   /* EXPRB53s3: u_3 */
+    case 7: return 4;   /* EXPRB54s4: u_4 */
+    default: return 0;  /* non-embedded */
+    }
+}
+
+int oc_integrate_adaptive(const oc_problem *pb, int method, double *u, double t_end, double dt0, double tol,
+                          double rtol, double atol, const double *xi, int max_nodes, int max_steps, int *accepted,
+                          int *rejected, double *log_dt, double *log_err, int *log_acc, int *iters)
+{
+    int q = oc_embedded_order(method);
+    if (q == 0 || !(dt0 > 0.0) || !(tol > 0.0) || !(t_end > 0.0)) return OC_ERR_ARG;
+    long N = oc_npoints(pb);
+    double *lo = (double *)malloc(sizeof(double) * (size_t)N), *hi = (double *)malloc(sizeof(double) * (size_t)N);
+    if (!lo || !hi) { free(lo); free(hi); return OC_ERR_ARG; }
+    double t = 0.0, h = dt0;
+    int acc = 0, rej = 0, total = 0, s = OC_OK;
+    for (int k = 0; k < max_steps && t < t_end; k++) {
+        if (h > t_end - t) h = t_end - t;
+        double bound = oc_spectrum_bound(pb, u);
+        double eig = -1.05 * bound, c = eig / 2.0, gamma = -eig / 4.0;
+        double err = 0.0;
+        int it = 0;
+        s = oc_step_ex(pb, OC_JAC_EXACT, method, u, lo, hi, &err, h, c, gamma, rtol, atol, xi, max_nodes, &it);
+        total += it;
+        if (s == OC_ERR_NOCONV || s == OC_ERR_NONFINITE) {   /* a failed step is a rejected one */
+            err = INFINITY;
+            s = OC_OK;
+        }
+        if (s) break;
+        int ok = err <= tol;
+        if (log_dt) log_dt[k] = h;
+        if (log_err) log_err[k] = err;
+        if (log_acc) log_acc[k] = ok;
+        double fac = err > 0.0 ? 0.9 * pow(tol / err, 1.0 / (q + 1)) : 5.0;
+        if (fac > 5.0) fac = 5.0;
+        if (fac < 0.2) fac = 0.2;
+        if (ok) {
+            memcpy(u, hi, sizeof(double) * (size_t)N);
+            t = (h == t_end - t) ? t_end : t + h;
+            acc++;
+        } else {
+            rej++;
+        }
+        h = h * fac;
+    }
+    if (!s && t < t_end) s = OC_ERR_NOCONV;   /* step budget exhausted */
+    if (accepted) *accepted = acc;
+    if (rejected) *rejected = rej;
+    if (iters) *iters = total;
+    free(lo);
+    free(hi);
+    return s;
+}

@@ -495,3 +495,61 @@ def test_exprb54s4_orders(xi300):
     assert abs(o5[-1] - 5.0) < 0.35, res
     assert np.all(np.abs(o4 - 4.0) < 0.3), res
     assert e5[-1] < 0.3 * e53[-1], res
+
+
+def _replay_controller(res, t_end, dt0, tol, q):
+    # the controller of reading R32 replayed from the logged errors: accept iff err <= tol, next step
+    # h min(5, max(0.2, 0.9 (tol/err)^(1/(q+1)))), the last step clipped to t_end
+    t, h = 0.0, dt0
+    for k in range(len(res.dts)):
+        h = min(h, t_end - t)
+        assert res.dts[k] == pytest.approx(h, rel=1e-14, abs=0.0), k
+        ok = res.errs[k] <= tol
+        assert bool(res.acc[k]) == ok, k
+        fac = 5.0 if res.errs[k] == 0.0 else min(5.0, max(0.2, 0.9 * (tol / res.errs[k]) ** (1.0 / (q + 1))))
+        if not np.isfinite(res.errs[k]):     # a failed step (NOCONV / NONFINITE) is a rejection with factor 0.2
+            fac = 0.2
+        if ok:
+            t = t_end if h == t_end - t else t + h
+        h = h * fac
+    assert t == t_end
+
+
+def test_adaptive_linear_problem_grows_steps(xi300):
+    # Problem I is linear: every remainder vanishes (R18), so the embedded error is exactly 0, every step is
+    # accepted and the step grows by the maximal factor 5 until the last one lands on t_end; the result is the
+    # FFT-exact exp(t_end A) u0 (pure diffusion: a real spectrum, so the large late steps stay within real
+    # Leja's reach, R28)
+    n = 32
+    pb = _advdiff(n, nu=0.0)
+    u0 = W.ic_problem1_2d(n)
+    dt0 = W.dt_cfl(n, 10.0)
+    t_end = 200 * dt0
+    res = O.integrate_adaptive(pb, "exprb43", u0, t_end, dt0, 1e-6, 1e-12, 1e-12, xi300)
+    assert res.status == O.OK and res.rejected == 0
+    assert np.all(res.errs == 0.0)
+    np.testing.assert_allclose(res.dts[:-1], dt0 * 5.0 ** np.arange(len(res.dts) - 1), rtol=1e-14)
+    assert len(res.dts) == 5      # dt0 (1 + 5 + 25 + 125) = 156 dt0 < 200 dt0 <= 781 dt0
+    sym = refs.impulse_symbol(lambda x: O.jac_apply(pb, None, x), (n, n))
+    ex = refs.fft_apply_phi(sym, u0, t_end, 0)
+    assert np.linalg.norm(res.u - ex) <= 1e-9 * np.linalg.norm(ex)
+
+
+@pytest.mark.parametrize("method,q", [("exprb32", 2), ("exprb43", 3), ("epirk4s3a", 3), ("exprb54s4", 4)])
+def test_adaptive_controller_allen_cahn(xi300, method, q):
+    # Allen-Cahn: the accept / reject decisions and the step sequence follow R32 exactly (replayed from the
+    # logs), a too-large first step is rejected, and the global error at t_end shrinks with the tolerance
+    n = 16
+    pb = O.Problem((n, n), (2 / n, 2 / n), 2e-3, 0.0, 1.0)
+    u0 = W.ic_allen_cahn_2d(n)
+    t_end = 0.5
+    uref = _allen_cahn_reference(pb, u0, t_end)
+    errs = []
+    for tol in (1e-5, 1e-7, 1e-9):
+        res = O.integrate_adaptive(pb, method, u0, t_end, 0.5, tol, 1e-12, 1e-12, xi300)
+        assert res.status == O.OK
+        assert res.rejected >= 1 and not res.acc[0]
+        _replay_controller(res, t_end, 0.5, tol, q)
+        errs.append(np.linalg.norm(res.u - uref) / np.linalg.norm(uref))
+    assert errs[0] > errs[1] > errs[2], errs
+    assert errs[1] < 1e-5, errs
