@@ -283,7 +283,8 @@ typedef enum {
     LX_EPIRK4S3A = 3,
     LX_EXPRB42 = 4,       /* Luan 2017 (cited at P:83), 4th order, non-embedded (err = 0) */
     LX_EPIRK5P1 = 5,      /* Tokman et al. 2012 (cited at P:83, Table 2), 5th order, non-embedded (R26) */
-    LX_EXPRB53S3 = 6      /* Luan & Ostermann 2014 (cited at P:83), 5th order, embedded 3rd (R27)      */
+    LX_EXPRB53S3 = 6,     /* Luan & Ostermann 2014 (cited at P:83), 5th order, embedded 3rd (R27)      */
+    LX_EXPRB54S4 = 7      /* Luan & Ostermann 2014 (cited at P:83), 5th order, embedded 4th (R31)      */
 } lx_method;
 
 /* Rosenbrock-Euler: u_out = u + phi_1(dt J(u)) f(u) dt (alg:Ros_Eu). */
@@ -310,6 +311,19 @@ lx_status lx_step_epirk5p1(lx_ctx *ctx, const lx_problem *pb, const double *u, d
 lx_status lx_step(lx_ctx *ctx, lx_method method, const lx_problem *pb, const double *u,
                   double *u_low, double *u_high, double *err_out, double dt, double c,
                   double gamma, double rtol, double atol, int *iters_out);
+
+/* Embedded-error step-size control (the embedded error "may be used to control the step sizes";
+ * reading R32).  Integrates u (device pointer, in place) from 0 to t_end with an embedded method
+ * (EXPRB32, EXPRB43, EPIRK4s3A, EXPRB53S3, EXPRB54S4): per attempted step the spectrum bound of the
+ * current state gives (c, gamma), the step gives err = ||u_high - u_low|| / sqrt(N); accept
+ * iff err <= tol; next step h * min(5, max(0.2, 0.9 (tol/err)^(1/(q+1)))) with q the embedded order
+ * (2, 3, 3, 3, 4); the last step is clipped to land on t_end; a step whose Leja calls fail (NOCONV /
+ * NONFINITE) is rejected with factor 0.2.  Optional logs (max_steps entries): every attempted step size
+ * and its error.  One host round trip per attempted step.  Errors: LX_ERR_ARG (non-embedded method, bad
+ * t_end / dt0 / tol, host u), LX_ERR_NOCONV (max_steps attempts did not reach t_end), device errors. */
+lx_status lx_integrate_adaptive(lx_ctx *ctx, lx_method method, const lx_problem *pb, double *u, double t_end,
+                                double dt0, double tol, double rtol, double atol, int max_steps, int *accepted,
+                                int *rejected, double *log_dt, double *log_err, int *iters_out);
 
 /* The paper's time loop (listing alg:lexint) run on the device: nsteps steps of
  * `method` from the state in u (overwritten with u^{n+nsteps}).  Before every step the spectrum

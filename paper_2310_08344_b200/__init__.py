@@ -32,9 +32,9 @@ LX_COMM_FORCE, LX_COMM_NO_PEER = 1, 2
 STATUS_NAMES = {0: "LX_OK", 1: "LX_ERR_ARG", 2: "LX_ERR_DIM", 3: "LX_ERR_ALIAS", 4: "LX_ERR_UNSUPPORTED",
                 5: "LX_ERR_NOCONV", 6: "LX_ERR_NONFINITE", 7: "LX_ERR_UNKNOWN_INTEGRATOR", 8: "LX_ERR_CUDA",
                 9: "LX_ERR_NCCL", 10: "LX_ERR_TIMEOUT"}
-LX_ROSENBROCK_EULER, LX_EXPRB32, LX_EXPRB43, LX_EPIRK4S3A, LX_EXPRB42, LX_EPIRK5P1, LX_EXPRB53S3 = range(7)
+LX_ROSENBROCK_EULER, LX_EXPRB32, LX_EXPRB43, LX_EPIRK4S3A, LX_EXPRB42, LX_EPIRK5P1, LX_EXPRB53S3, LX_EXPRB54S4 = range(8)
 METHODS = {"rosenbrock_euler": 0, "exprb32": 1, "exprb43": 2, "epirk4s3a": 3, "exprb42": 4, "epirk5p1": 5,
-           "exprb53s3": 6}
+           "exprb53s3": 6, "exprb54s4": 7}
 
 # Every symbol include/lexint.h declares (checked by tests/test_abi.py).
 EXPORTS = ("lx_last_error", "lx_version", "lx_leja_points", "lx_phi_scalar", "lx_divided_differences",
@@ -45,7 +45,7 @@ EXPORTS = ("lx_last_error", "lx_version", "lx_leja_points", "lx_phi_scalar", "lx
            "lx_step_exprb42", "lx_step_epirk5p1",
            "lx_step", "lx_rhs", "lx_integrate", "lx_local_group_create", "lx_local_group_destroy", "lx_ctx_set_comm_local",
            "lx_real_leja_phi_cb", "lx_step_cb", "lx_builtin_rhs", "lx_ctx_set_comm_ex", "lx_ctx_set_comm_local_ex",
-           "lx_ctx_ipc_handle", "lx_ctx_set_comm_ipc", "lx_ctx_set_kernel", "lx_slab_halo_plan")
+           "lx_ctx_ipc_handle", "lx_ctx_set_comm_ipc", "lx_ctx_set_kernel", "lx_slab_halo_plan", "lx_integrate_adaptive")
 
 # void f(const double* in, double* out, void* user, void* cuda_stream)  (include/lexint.h lx_rhs_fn)
 RHS_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
@@ -141,6 +141,8 @@ def lib() -> ctypes.CDLL:
             "lx_ctx_ipc_handle": (ctypes.c_int, [vp, vp]),
             "lx_ctx_set_comm_ipc": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp]),
             "lx_ctx_set_kernel": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int]),
+            "lx_integrate_adaptive": (ctypes.c_int, [vp, ctypes.c_int, pbp, vp, d, d, d, d, d, ctypes.c_int, ip, ip,
+                                                     dp, dp, ip]),
             "lx_slab_halo_plan": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int,
                                                  ctypes.POINTER(ctypes.c_int), ctypes.c_int]),
             "lx_real_leja_phi_cb": (ctypes.c_int, [vp, vp, vp, vp, vp, ctypes.POINTER(vp), dp, ctypes.c_int,
@@ -258,10 +260,14 @@ class Context:
             try:
                 import torch
                 if torch.cuda.is_available():
-                    stream = torch.cuda.current_stream()
+                    # the current stream OF THE CONTEXT'S DEVICE (not of whatever device is current)
+                    stream = torch.cuda.current_stream(device if device >= 0 else None)
             except ImportError:
                 pass
         if stream is not None:
+            dev = getattr(stream, "device", None)
+            if device >= 0 and dev is not None and getattr(dev, "index", device) not in (None, device):
+                raise LxError(LX_ERR_ARG, "stream belongs to device %s, context to device %d" % (dev, device))
             sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
             if sp == 0:
                 sp = 1   # the legacy default stream (cudaStreamLegacy); NULL would mean "own stream"
@@ -415,6 +421,23 @@ def lx_integrate(ctx: Context, method, u, dt, nsteps, rtol, atol, problem: Probl
                             float(atol), ctypes.byref(it) if sync else None, ctypes.byref(err) if sync else None)
     _check(st, it.value)
     return (it.value, err.value) if sync else (None, None)
+
+
+def lx_integrate_adaptive(ctx: Context, method, u, t_end, dt0, tol, rtol, atol, max_steps: int = 1000,
+                          problem: Problem | None = None):
+    """Embedded-error step-size control (lexint.h; reading R32) in place on device u.
+    Returns (accepted, rejected, step sizes tried, their errors, Leja iterations)."""
+    m = METHODS[method] if isinstance(method, str) else int(method)
+    na, nr, it = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0)
+    dts = np.zeros(max_steps)
+    errs = np.zeros(max_steps)
+    dp = ctypes.POINTER(ctypes.c_double)
+    st = lib().lx_integrate_adaptive(ctx.handle, m, _pb(ctx, problem), _ptr(u), float(t_end), float(dt0), float(tol),
+                                     float(rtol), float(atol), int(max_steps), ctypes.byref(na), ctypes.byref(nr),
+                                     dts.ctypes.data_as(dp), errs.ctypes.data_as(dp), ctypes.byref(it))
+    _check(st, it.value)
+    k = na.value + nr.value
+    return na.value, nr.value, dts[:k], errs[:k], it.value
 
 
 def lx_rhs(ctx: Context, u, f_out, scale: float = 1.0, problem: Problem | None = None):

@@ -18,7 +18,9 @@
 // validated on a single B200 against the single-domain result.
 #include "lx_comm.h"
 
+#include <chrono>
 #include <condition_variable>
+#include <thread>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -66,6 +68,16 @@ int comm_halo_plan(int rank, int nranks, int n_loc, int mode, int* ops, int max_
 struct Transport {
     int rank = 0, nranks = 1;
     virtual ~Transport() {}
+    // make this rank's later writes safe against peers' still-pending reads of its buffers (the in-process
+    // transport's D2D pulls run on the peers' streams); NCCL orders send/recv itself
+    virtual int settle(cudaStream_t s) {
+        (void)s;
+        return 0;
+    }
+    // asynchronous transport error (NCCL: ncclCommGetAsyncError); abort() tears the communicator down so
+    // that no rank blocks forever on a peer that failed
+    virtual int async_error() { return 0; }
+    virtual void abort() {}
     virtual int exchange_rows(const double* base, double* ghost, int n_loc, long long row, cudaStream_t s) = 0;
     virtual int allgather(const double* send, double* recv, int count, cudaStream_t s) = 0;
     virtual int allreduce_max_u64(unsigned long long* buf, cudaStream_t s) = 0;
@@ -130,6 +142,16 @@ struct NcclTransport : Transport {
         return 0;
     }
     int fused = 1;
+    int async_error() override {
+        ncclResult_t st = ncclSuccess;
+        if (ncclCommGetAsyncError(comm, &st) != ncclSuccess || (st != ncclSuccess && st != ncclInProgress))
+            return cerr(std::string("NCCL async error: ") + ncclGetErrorString(st));
+        return 0;
+    }
+    void abort() override {
+        if (comm) ncclCommAbort(comm);
+        comm = nullptr;
+    }
     int exchange_blocks(void* mine, void** all) override {
         cudaIpcMemHandle_t h;
         CU(cudaIpcGetMemHandle(&h, mine));
@@ -240,7 +262,7 @@ struct LocalTransport : Transport {
     }
     // Make every rank's stream wait until all peers finished the copies they just
     // enqueued (so a rank cannot overwrite a buffer a peer has not read yet).
-    int settle(cudaStream_t s) {
+    int settle(cudaStream_t s) override {
         if (publish(nullptr, 0, s)) return 1;
         int rc = 0;
         for (int r = 0; r < nranks; r++)
@@ -454,7 +476,21 @@ static lx_status run_chunked(Comm* c, Ctrl* ctrl, int last, Launch launch, cudaS
                 cudaEventRecord(c->ev[chunk & 1], s) != cudaSuccess)
                 return LX_ERR_CUDA;
             if (chunk >= 1) {
-                if (cudaEventSynchronize(c->ev[(chunk - 1) & 1]) != cudaSuccess) return LX_ERR_CUDA;
+                // poll instead of blocking: a failed peer (NCCL async error) or a stall beyond the watchdog
+                // aborts the communicator rather than hanging this rank forever
+                const auto t0 = std::chrono::steady_clock::now();
+                for (;;) {
+                    const cudaError_t q = cudaEventQuery(c->ev[(chunk - 1) & 1]);
+                    if (q == cudaSuccess) break;
+                    if (q != cudaErrorNotReady) return LX_ERR_CUDA;
+                    if (c->tr->async_error() ||
+                        std::chrono::steady_clock::now() - t0 > std::chrono::seconds(c->timeout_ns / 1000000000ull)) {
+                        if (!c->tr->async_error()) cerr("slab protocol: no progress within the watchdog limit");
+                        c->tr->abort();
+                        return LX_ERR_NCCL;
+                    }
+                    std::this_thread::sleep_for(std::chrono::microseconds(20));
+                }
                 if (c->done_host[(chunk - 1) & 1]) break;
             }
             chunk++;
@@ -471,7 +507,7 @@ lx_status comm_leja(Comm* c, LejaParams& P, bool diag, cudaStream_t s, int64_t* 
     P.v.ghost = c->vg;
     if (cudaMemcpyAsync(P.ctrl, &c->ctrl_init[P.K], sizeof(Ctrl), cudaMemcpyHostToDevice, s) != cudaSuccess)
         return LX_ERR_CUDA;
-    if (comm_exchange(c, P.v.base, c->vg, s)) return LX_ERR_NCCL;
+    if (comm_exchange(c, P.v.base, c->vg, s) || c->tr->settle(s)) return LX_ERR_NCCL;
     const int M = P.max_nodes;
     auto launch = [&](int m) -> int {
         if (launch_leja_step(P, m, s, diag) != cudaSuccess) return cerr("step kernel launch failed");
@@ -523,6 +559,7 @@ int comm_stage_norm(Comm* c, int op, const StageArgs& A0, cudaStream_t s, int64_
 
 int comm_rhs(Comm* c, LejaParams& P, double scale, cudaStream_t s, int64_t* launches) {
     if (comm_exchange(c, P.v.base, c->vg, s)) return 1;
+    if (c->tr->settle(s)) return 1;   // peers' pulls of this rank's rows done before the caller may overwrite u
     P.v.ghost = c->vg;
     P.grid = step_grid_size(c->device, P.nunits);
     CU(launch_rhs(P, scale, s));

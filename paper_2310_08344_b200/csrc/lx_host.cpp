@@ -8,6 +8,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -47,7 +48,8 @@ static lx_status fail(lx_status s, const char* fmt, ...) {
     } while (0)
 
 static constexpr int kCoefSlots = 32;
-static constexpr int kStage = 8;   // integrator scratch vectors (4 stages + 3 states for lx_integrate + 1 EPIRK5P1)
+static constexpr int kStage = 10;  // integrator scratch vectors (4 stages + 3 states for lx_integrate + 1 EPIRK5P1
+                                   // + 2 EXPRB54s4)
 static constexpr int kHost = 6;    // host-pointer staging vectors
 static constexpr int kBb = 11;     // black-box path vectors
 // Auto policy of the two-step kernel (measured round 1): its per-pass latency chain (~27 us)
@@ -1231,6 +1233,58 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
         if (lo && lo != hi) CUDA_TRY(cudaMemcpyAsync(lo, hi, ctx->N_loc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
         return LX_OK;
     }
+    if (method == LX_EXPRB54S4) {
+        // reading R31: c2 = 1/4, c3 = 1/2, c4 = 9/10, D_x = dt (F(x) - F(u)); 8 Leja calls
+        double* S1 = scratch(ctx, 1);
+        double* S2 = scratch(ctx, 2);
+        double* S3 = scratch(ctx, 3);
+        double* S4 = scratch(ctx, 8);    // (scratch 4..6 hold lx_integrate's states)
+        double* S5 = scratch(ctx, 9);
+        if (!S1 || !S2 || !S3 || !S4 || !S5) return fail(LX_ERR_CUDA, "scratch allocation failed");
+        const double e4[4] = {0.25, 0.5, 0.9, 1.0}, half = 0.5, c4 = 0.9;
+        double* pv[4] = {S1, S2, S3, S4};                    // phi_1(c hJ) hf, c = 1/4, 1/2, 9/10, 1
+        LX_TRY(leja_device(ctx, pb, ul, S0, pv, e4, 4, dt, c, gamma, 1, rtol, atol, rec));
+        LX_TRY(stage_remainder(ctx, pb, rec, u, u, S1, 0.25, nullptr, 0.0, 1.0, dt, S0, hi));   // D2 -> S0
+        double* q1[1] = {S1};
+        LX_TRY(leja_device(ctx, pb, ul, S0, q1, &half, 1, dt, c, gamma, 3, rtol, atol, rec));    // phi_3(hJ/2) D2
+        A = stage_args(ctx, pb, rec);                        // U3 = u + 1/2 P05 + 4 Q -> S5
+        A.x0 = u; A.x1 = S2; A.x2 = S1; A.a0 = 0.5; A.a1 = 4.0; A.y0 = S5;
+        LX_TRY(run_stage(ctx, ST_LIN3, A));
+        LX_TRY(stage_remainder(ctx, pb, rec, u, S5, nullptr, 0.0, nullptr, 0.0, 1.0, dt, S2, nullptr));  // D3 -> S2
+        A = stage_args(ctx, pb, rec);                        // U4 stage combinations of D2, D3 -> S1, S5
+        A.x0 = S0; A.x1 = S2; A.y0 = S1; A.y1 = S5;
+        A.a0 = 5832.0 / 125.0; A.a1 = -729.0 / 125.0; A.a2 = -157464.0 / 625.0; A.a3 = 39366.0 / 625.0;
+        LX_TRY(run_stage(ctx, ST_COMBINE2, A));
+        double* o3a[1] = {lo};
+        LX_TRY(leja_device(ctx, pb, ul, S1, o3a, &c4, 1, dt, c, gamma, 3, rtol, atol, rec));
+        double* o4a[1] = {hi};
+        LX_TRY(leja_device(ctx, pb, ul, S5, o4a, &c4, 1, dt, c, gamma, 4, rtol, atol, rec));
+        A = stage_args(ctx, pb, rec);                        // U4 = u + 9/10 P09 + lo + hi -> S1
+        A.x0 = u; A.x1 = S3; A.x2 = lo; A.x3 = hi; A.a0 = 0.9; A.a1 = 1.0; A.a2 = 1.0; A.y0 = S1;
+        LX_TRY(run_stage(ctx, ST_LIN4, A));
+        LX_TRY(stage_remainder(ctx, pb, rec, u, S1, nullptr, 0.0, nullptr, 0.0, 1.0, dt, S3, nullptr));  // D4 -> S3
+        A = stage_args(ctx, pb, rec);                        // embedded: 64 D2 - 8 D3 -> S1, -384 D2 + 96 D3 -> S5
+        A.x0 = S0; A.x1 = S2; A.y0 = S1; A.y1 = S5;
+        A.a0 = 64.0; A.a1 = -8.0; A.a2 = -384.0; A.a3 = 96.0;
+        LX_TRY(run_stage(ctx, ST_COMBINE2, A));
+        LX_TRY(leja_device(ctx, pb, ul, S1, o3a, &one, 1, dt, c, gamma, 3, rtol, atol, rec));
+        LX_TRY(leja_device(ctx, pb, ul, S5, o4a, &one, 1, dt, c, gamma, 4, rtol, atol, rec));
+        A = stage_args(ctx, pb, rec);                        // E = lo + hi -> S0
+        A.x0 = lo; A.x1 = hi; A.a0 = 1.0; A.a1 = 1.0; A.y0 = S0;
+        LX_TRY(run_stage(ctx, ST_AXPBY, A));
+        A = stage_args(ctx, pb, rec);                        // 18 D3 - 250/81 D4 -> S1, -60 D3 + 500/27 D4 -> S5
+        A.x0 = S2; A.x1 = S3; A.y0 = S1; A.y1 = S5;
+        A.a0 = 18.0; A.a1 = -250.0 / 81.0; A.a2 = -60.0; A.a3 = 500.0 / 27.0;
+        LX_TRY(run_stage(ctx, ST_COMBINE2, A));
+        LX_TRY(leja_device(ctx, pb, ul, S1, o3a, &one, 1, dt, c, gamma, 3, rtol, atol, rec));
+        LX_TRY(leja_device(ctx, pb, ul, S5, o4a, &one, 1, dt, c, gamma, 4, rtol, atol, rec));
+        A = stage_args(ctx, pb, rec);                        // d = lo + hi - E -> S2
+        A.x0 = lo; A.x1 = hi; A.x2 = S0; A.a0 = 1.0; A.a1 = -1.0; A.y0 = S2;
+        LX_TRY(run_stage(ctx, ST_LIN3, A));
+        A = stage_args(ctx, pb, rec);                        // u4 = u + P1 + E ; u5 = u4 + d ; err = ||d||
+        A.x0 = u; A.x1 = S4; A.x2 = S0; A.x3 = S2; A.y0 = lo; A.y1 = hi;
+        return run_stage(ctx, ST_FINAL4, A);
+    }
     if (method == LX_EXPRB53S3) {
         // reading R27: c2 = 1/2, c3 = 9/10, D_x = dt (F(x) - F(u))
         double* S1 = scratch(ctx, 1);
@@ -1346,7 +1400,7 @@ lx_status lx_step(lx_ctx* ctx, lx_method method, const lx_problem* pb0, const do
     const lx_problem* pb = &pbs;
     if (!ctx) return fail(LX_ERR_ARG, "ctx is NULL");
     LX_TRY(check_problem(ctx, pb));
-    if ((int)method < 0 || (int)method > 6) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
+    if ((int)method < 0 || (int)method > 7) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
     if (!u || !u_high) return fail(LX_ERR_ARG, "NULL argument");
     if (!nonembedded(method) && !u_low)
         return fail(LX_ERR_ARG, "u_low required for embedded methods");
@@ -1373,6 +1427,79 @@ lx_status lx_step(lx_ctx* ctx, lx_method method, const lx_problem* pb0, const do
     return status_of(r);
 }
 
+// Embedded-error step-size control ("may be used to control the step sizes"; reading R32): accept iff
+// err <= tol; next step h min(5, max(0.2, 0.9 (tol/err)^(1/(q+1)))) (err = 0 -> 5), q = order of the embedded
+// solution; the last step clipped to land on t_end; a step whose Leja calls fail (NOCONV / NONFINITE) is a
+// rejection with factor 0.2.  (c, gamma) from the spectrum bound of the current state.  One host
+// round trip per attempted step (the decision needs err).
+static int embedded_order(lx_method m) {
+    switch (m) {
+        case LX_EXPRB32: return 2;
+        case LX_EXPRB43: return 3;
+        case LX_EPIRK4S3A: return 3;
+        case LX_EXPRB53S3: return 3;
+        case LX_EXPRB54S4: return 4;
+        default: return 0;
+    }
+}
+
+lx_status lx_integrate_adaptive(lx_ctx* ctx, lx_method method, const lx_problem* pb0, double* u, double t_end,
+                                double dt0, double tol, double rtol, double atol, int max_steps, int* accepted,
+                                int* rejected, double* log_dt, double* log_err, int* iters_out) {
+    if (!ctx || !u || !pb0) return fail(LX_ERR_ARG, "NULL argument");
+    LX_TRY(check_problem(ctx, pb0));
+    const int q = embedded_order(method);
+    if (q == 0) return fail(LX_ERR_ARG, "step-size control needs an embedded method (EXPRB32/43/53s3/54s4, EPIRK4s3A)");
+    if (!(dt0 > 0.0) || !(tol > 0.0) || !(t_end > 0.0) || max_steps < 1) return fail(LX_ERR_ARG, "bad t_end / dt0 / tol");
+    if (!is_device_ptr(u)) return fail(LX_ERR_ARG, "u must be a device pointer");
+    lx_problem pbs = *pb0;
+    const lx_problem* pb = &pbs;
+    Staging sg(ctx);
+    LX_TRY(sg.in(pb0->source, &pbs.source));
+    double* lo = scratch(ctx, 6);   // (scratch 6 is lx_integrate's discarded lower-order solution)
+    double* hi = scratch(ctx, 4);
+    if (!lo || !hi) return fail(LX_ERR_CUDA, "scratch allocation failed");
+    double t = 0.0, h = dt0;
+    int acc = 0, rej = 0, total = 0;
+    lx_status st = LX_OK;
+    for (int k = 0; k < max_steps && t < t_end; k++) {
+        if (h > t_end - t) h = t_end - t;
+        double bound = 0.0, c = 0.0, gamma = 0.0;
+        LX_TRY(lx_spectrum_bound(ctx, pb, u, &bound));
+        LX_TRY(lx_shift_scale(bound, &c, &gamma));
+        LX_TRY(reset_record(ctx, 0));
+        LX_TRY(step_device(ctx, method, pb, u, lo, hi, h, c, gamma, rtol, atol, 0));
+        Record r;
+        LX_TRY(read_record(ctx, 0, &r));
+        total += r.iters;
+        double err = r.err;
+        if (r.status == 5 || r.status == 6) err = INFINITY;   // failed step: rejected
+        else if (r.status != 0) {
+            st = status_of(r);
+            break;
+        }
+        const bool ok = err <= tol;
+        if (log_dt) log_dt[k] = h;
+        if (log_err) log_err[k] = err;
+        double fac = err > 0.0 ? 0.9 * std::pow(tol / err, 1.0 / (q + 1)) : 5.0;
+        fac = std::min(5.0, std::max(0.2, fac));
+        if (ok) {
+            CUDA_TRY(cudaMemcpyAsync(u, hi, ctx->N_loc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+            t = (h == t_end - t) ? t_end : t + h;
+            acc++;
+        } else {
+            rej++;
+        }
+        h = h * fac;
+    }
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (accepted) *accepted = acc;
+    if (rejected) *rejected = rej;
+    if (iters_out) *iters_out = total;
+    if (st == LX_OK && t < t_end) return fail(LX_ERR_NOCONV, "step budget exhausted at t = %g of %g", t, t_end);
+    return st;
+}
+
 // The paper's time loop (listing alg:lexint) on the device: every step recomputes the
 // spectrum bound (Gershgorin / closed form, x1.05, c = eig/2, gamma = -eig/4) with a
 // device max-reduction + k_shift_scale, so the whole run is enqueued without host round trips.
@@ -1382,7 +1509,7 @@ lx_status lx_integrate(lx_ctx* ctx, lx_method method, const lx_problem* pb0, dou
     lx_problem pbs = *pb0;
     const lx_problem* pb = &pbs;
     LX_TRY(check_problem(ctx, pb));
-    if ((int)method < 0 || (int)method > 6) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
+    if ((int)method < 0 || (int)method > 7) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
     if (nsteps < 0) return fail(LX_ERR_ARG, "nsteps < 0");
     if (!std::isfinite(dt)) return fail(LX_ERR_ARG, "dt not finite");
     Staging sg(ctx);
@@ -1699,6 +1826,50 @@ static lx_status bb_step(BbRun& R, lx_method method, const double* u, double* lo
         if (lo && lo != hi) LX_TRY(R.comb(lo, 1.0, hi));
         return LX_OK;
     }
+    if (method == LX_EXPRB54S4) {                      // reading R31
+        const double e4[4] = {0.25, 0.5, 0.9, 1.0}, half = 0.5, c4 = 0.9;
+        double* pv[4] = {t[1], t[2], t[3], t[7]};
+        LX_TRY(R.leja(f_u, pv, e4, 4, dt, c, gamma, 1, rtol, atol));
+        LX_TRY(R.remainder(u, t[4]));                 // NL_u
+        LX_TRY(R.comb(t[5], 1.0, u, 0.25, t[1]));     // U2
+        LX_TRY(R.remainder(t[5], t[6]));
+        LX_TRY(R.comb(t[5], dt, t[6], -dt, t[4]));    // D2
+        double* q1[1] = {t[1]};
+        LX_TRY(R.leja(t[5], q1, &half, 1, dt, c, gamma, 3, rtol, atol));
+        LX_TRY(R.comb(t[6], 1.0, u, 0.5, t[2], 4.0, t[1]));   // U3
+        LX_TRY(R.remainder(t[6], lo));
+        LX_TRY(R.comb(t[6], dt, lo, -dt, t[4]));      // D3
+        LX_TRY(R.comb(t[1], 5832.0 / 125.0, t[5], -729.0 / 125.0, t[6]));
+        LX_TRY(R.comb(t[2], -157464.0 / 625.0, t[5], 39366.0 / 625.0, t[6]));
+        double* ol[1] = {lo};
+        double* oh[1] = {hi};
+        LX_TRY(R.leja(t[1], ol, &c4, 1, dt, c, gamma, 3, rtol, atol));
+        LX_TRY(R.leja(t[2], oh, &c4, 1, dt, c, gamma, 4, rtol, atol));
+        LX_TRY(R.comb(t[1], 1.0, u, 0.9, t[3], 1.0, lo, 1.0, hi));   // U4
+        LX_TRY(R.remainder(t[1], t[2]));
+        LX_TRY(R.comb(t[3], dt, t[2], -dt, t[4]));    // D4
+        LX_TRY(R.comb(t[1], 64.0, t[5], -8.0, t[6]));
+        LX_TRY(R.comb(t[2], -384.0, t[5], 96.0, t[6]));
+        double* o4[1] = {t[4]};
+        LX_TRY(R.leja(t[1], o4, &one, 1, dt, c, gamma, 3, rtol, atol));
+        double* o5[1] = {lo};
+        LX_TRY(R.leja(t[2], o5, &one, 1, dt, c, gamma, 4, rtol, atol));
+        LX_TRY(R.comb(lo, 1.0, u, 1.0, t[7], 1.0, t[4], 1.0, lo));   // u4
+        LX_TRY(R.comb(t[1], 18.0, t[6], -250.0 / 81.0, t[3]));
+        LX_TRY(R.comb(t[2], -60.0, t[6], 500.0 / 27.0, t[3]));
+        LX_TRY(R.leja(t[1], o4, &one, 1, dt, c, gamma, 3, rtol, atol));
+        double* o6[1] = {t[5]};
+        LX_TRY(R.leja(t[2], o6, &one, 1, dt, c, gamma, 4, rtol, atol));
+        LX_TRY(R.comb(hi, 1.0, u, 1.0, t[7], 1.0, t[4], 1.0, t[5]));  // u5
+        BbLin L = R.lin();
+        L.x0 = hi;
+        L.a0 = 1.0;
+        L.x1 = lo;
+        L.a1 = -1.0;
+        CUDA_TRY(launch_bb_norm(L, ctx->stream));
+        ctx->launches++;
+        return LX_OK;
+    }
     if (method == LX_EXPRB53S3) {                      // reading R27
         const double e3[3] = {0.5, 0.9, 1.0};
         double* pv[3] = {t[1], t[2], t[3]};
@@ -1846,7 +2017,7 @@ lx_status lx_step_cb(lx_ctx* ctx, lx_method method, lx_rhs_fn f, void* user, con
                      double* u_high, double* err_out, double dt, double c, double gamma, double rtol, double atol,
                      int* iters_out) {
     if (!ctx || !f || !u || !u_high) return fail(LX_ERR_ARG, "NULL argument");
-    if ((int)method < 0 || (int)method > 6) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
+    if ((int)method < 0 || (int)method > 7) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
     if (!nonembedded(method) && !u_low)
         return fail(LX_ERR_ARG, "u_low required for embedded methods");
     if (u_low == u || u_high == u) return fail(LX_ERR_ALIAS, "outputs must not alias u");

@@ -644,3 +644,25 @@ def test_pinned_host_pipelined_leja_calls(xi300):
         assert it == it2 and torch.equal(outs[0], o.cpu())
     r = O.real_leja_phi(ob, v.numpy(), dt, c, g, 0, TOL, TOL, xi300)
     assert r.iters == it and _rel(outs[0], r.outs[0]) <= TOL
+
+
+@pytest.mark.parametrize("method", ["exprb32", "exprb43", "epirk4s3a", "exprb53s3", "exprb54s4"])
+def test_adaptive_step_size_control(xi300, method):
+    # lx_integrate_adaptive vs the oracle's controller (reading R32): the same accept / reject sequence, the
+    # same step sizes (they depend on err^(1/(q+1)); err agrees to rounding), the same final state
+    n = 32
+    pb, ob = _pair((n, n), diff=2e-3, nu=0.0, react=1.0)
+    u0 = W.ic_allen_cahn_2d(n)
+    t_end, dt0, tol = 0.5, 0.5, 1e-7
+    ref = O.integrate_adaptive(ob, method, u0, t_end, dt0, tol, 1e-12, 1e-12, xi300)
+    assert ref.status == O.OK and ref.rejected >= 1
+    with lx.Context(pb) as ctx:
+        u = _dev(u0)
+        acc, rej, dts, errs, its = lx.lx_integrate_adaptive(ctx, method, u, t_end, dt0, tol, 1e-12, 1e-12)
+    assert (acc, rej) == (ref.accepted, ref.rejected)
+    np.testing.assert_allclose(dts, ref.dts, rtol=1e-8)
+    fin = np.isfinite(ref.errs)
+    assert np.array_equal(np.isfinite(errs), fin)
+    np.testing.assert_allclose(errs[fin], ref.errs[fin], rtol=1e-6, atol=1e-15)
+    assert its == ref.iters
+    assert _rel(u, ref.u) <= 1e-9
