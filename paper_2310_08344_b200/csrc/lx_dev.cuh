@@ -63,8 +63,10 @@ static __constant__ double c_inv_int[40] = {
     1.0 / 21, 1.0 / 22, 1.0 / 23, 1.0 / 24, 1.0 / 25, 1.0 / 26, 1.0 / 27, 1.0 / 28, 1.0 / 29, 1.0 / 30,
     1.0 / 31, 1.0 / 32, 1.0 / 33, 1.0 / 34, 1.0 / 35, 1.0 / 36, 1.0 / 37, 1.0 / 38, 1.0 / 39};
 
+static __constant__ double c_inv_fact[6] = {1.0, 1.0, 0.5, 1.0 / 6.0, 1.0 / 24.0, 1.0 / 120.0};
+
 static __device__ double phi_dev(int l, double z) {
-    const double inv_fact[6] = {1.0, 1.0, 0.5, 1.0 / 6.0, 1.0 / 24.0, 1.0 / 120.0};
+    const double* inv_fact = c_inv_fact;   // constant bank (a local array indexed by l would live in local memory)
     if (fabs(z) < 2.0) {   // Taylor: sum_k z^k/(k+l)!  (34 terms: 2^34/34! ~ 1e-29)
         double term = inv_fact[l], s = term;
 #pragma unroll
@@ -138,7 +140,17 @@ __device__ __forceinline__ void coef_write_row(const LejaParams& P, int j, int l
     if (j >= P.max_nodes) return;
     double* row = P.table + (size_t)j * (1 + K);
     if (lane == 0) row[0] = (j == 0 || P.cdt == 0.0) ? 0.0 : (-P_c(P) / P_g(P) - P.xi[j - 1]);
-    if (lane < K && ((active >> lane) & 1)) row[1 + lane] = dk ? dk[lane] : coef_fold(P, K, lane, j);
+    if (lane < K && ((active >> lane) & 1)) {
+        double v = 0.0;
+        if (dk) {   // select by unrolled compare: an array indexed by the lane would live in local memory
+#pragma unroll
+            for (int k = 0; k < K; k++)
+                if (lane == k) v = dk[k];
+        } else {
+            v = coef_fold(P, K, lane, j);
+        }
+        row[1 + lane] = v;
+    }
 }
 
 __device__ __forceinline__ double coef_beta(const LejaParams& P, int m) {
