@@ -55,6 +55,7 @@ static constexpr int kBb = 11;     // black-box path vectors
 // Auto policy of the two-step kernel (measured round 1): its per-pass latency chain (~27 us)
 // loses to the one-pass kernel below ~1700^2 points (Leja calls and Allen-Cahn EXPRB43 alike).
 static constexpr int64_t kTb2MinPoints = 3 << 20;
+static constexpr int64_t kTb3MinPoints = 1 << 20;   // 3D two-step kernel from this many points on
 
 struct lx_ctx {
     int device = 0;
@@ -270,8 +271,16 @@ struct TableSpec {
 };
 
 // Leja iterations per HBM pass of this context's 2D single-GPU Leja calls (1 or 2).
+static bool tb3_shape(const lx_ctx* ctx) {
+    return ctx->ndim == 3 && ctx->k3d != 1 && ctx->n[1] % 16 == 0 && ctx->n[2] % 64 == 0;
+}
+
 static int ctx_tblock(const lx_ctx* ctx) {
-    if (ctx->comm) return comm_peer_ready(ctx->comm) ? 2 : 1;
+    if (ctx->comm) return (ctx->ndim == 2 && comm_peer_ready(ctx->comm)) ? 2 : 1;
+    if (ctx->ndim == 3) {
+        if (!tb3_shape(ctx) || ctx->tblock == 1) return 1;
+        return (ctx->tblock == 2 || ctx->N_loc >= kTb3MinPoints) ? 2 : 1;
+    }
     if (ctx->ndim != 2 || ctx->n_loc < 16 || ctx->n[1] < 64) return 1;
     if (ctx->tblock == 1) return 1;
     if (ctx->tblock == 2) return 2;
@@ -458,6 +467,13 @@ static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u,
             P.coef_gen = 0;
         }
         const int ncu = leja3d_smem_units(P.n_loc, P.n1, P.n2);
+        if (!diag && ctx_tblock(ctx) == 2) {
+            // two Leja iterations per HBM pass (2.5D temporal blocking)
+            P.grid = leja3d_tb2_grid_size(ctx->device, K, ncu);
+            CUDA_TRY(launch_leja3d_tb2(P, ctx->stream));
+            ctx->launches++;
+            return LX_OK;
+        }
         P.grid = leja3d_smem_grid_size(ctx->device, K, diag, ncu);
         CUDA_TRY(launch_leja3d_smem(P, ctx->stream, diag));
         ctx->launches++;

@@ -277,12 +277,625 @@ cudaError_t launch_leja3d_smem(const LejaParams& P, cudaStream_t s, bool diag) {
     return cudaLaunchCooperativeKernel(kern, dim3(P.grid), dim3(kThreads), args, kS3Smem, s);
 }
 
-cudaError_t preload_3d() {
-    for (int K = 1; K <= kMaxK; K++)
-        for (int d = 0; d < 2; d++) {
-            cudaFuncAttributes a;
-            if (cudaFuncGetAttributes(&a, leja3d_smem_ptr(K, d != 0)) != cudaSuccess) return cudaGetLastError();
+// ---------------------------------------------------------------------------
+// 3D two-step kernel (2.5D temporal blocking, SURVEY 8(f) f-3 in 3D; constant-coefficient operators).
+// One pass over the grid performs Leja iterations m = 2q+1 and m+1 (Eq. (2) twice).  A CTA owns a
+// (16 j-rows x 64 k) column of a run of kTI3 planes and marches along i; its 16 warps have two roles,
+// one barrier per plane step t:
+//   stage A (warps 0..7): y_m on plane t over the halo-extended tile (rows j0-1 .. j0+17, columns
+//            k0-2 .. k0+65: the j/k neighbours j-1, j+1, j+2 stage B needs) from the staged y_{m-1}
+//            tiles (rows j0-2 .. j0+19, columns k0-4 .. k0+67; a cp.async ring of 5 planes that these
+//            warps fill, plane t+4 into the slot of plane t-1) into a shared-memory ring of 5 y_m planes;
+//            each thread keeps its own column's y_{m-1} at planes t-1, t, t+1 in registers and shares
+//            the j-neighbours of its 3 consecutive rows; y_m never goes to HBM;
+//   stage B (warps 8..15): y_{m+1} on plane t-3 over the 16 x 64 interior from the y_m planes t-4 .. t-1
+//            finished in earlier steps (two rows per warp sharing their j-neighbours),
+//            p_m = p_{m-1} + d_m y_m, p_{m+1} = p_m + d_{m+1} y_{m+1}, the norms of y_m, p_m, y_{m+1},
+//            p_{m+1}; writes y_{m+1} and p.
+// HBM per pass: read y_{m-1}, p; write y_{m+1}, p (32 B/pt for K = 1, +16 per further accumulator): half
+// the bytes of two one-pass iterations.  Same per-point FMA order as k_leja3d_smem, so y and p are bitwise
+// those of the one-pass kernel; only the norm summation order differs.  One grid barrier per pass; the
+// last arriver decides m, then m+1.  An accumulator that converges at m got one term too many:
+// it is rolled back, p_m = p_{m+1} - d_{m+1} y_{m+1} (within one rounding of the one-step value, as in
+// the 2D two-step kernel), by the next pass's stage B or by the end-of-call fix-up.  Coefficients from
+// the prebuilt table (k_coef_tables), as k_leja3d_smem.  n1 % 16 == 0, n2 % 64 == 0; no Allen-Cahn term.
+// ---------------------------------------------------------------------------
+constexpr int kB3J = 16;                        // output j-rows per tile
+constexpr int kB3R1R = kB3J + 6, kB3R1C = 72;   // staged y_{m-1}: rows j0-2 .. j0+19, columns k0-4 .. k0+67
+constexpr int kB3R1P = kB3R1R * kB3R1C;
+constexpr int kB3R2R = kB3J + 3, kB3R2C = 68;   // y_m: rows j0-1 .. j0+17, columns k0-2 .. k0+65
+constexpr int kB3R2P = kB3R2R * kB3R2C;
+constexpr int kB3D = 5;                         // ring depth of both rings (planes)
+constexpr int kB3Threads = 512, kB3Warps = kB3Threads / 32;   // 8 stage-A warps + 8 stage-B warps
+constexpr int kB3Pieces = kB3R1R * (kB3R1C / 2);             // 16-B pieces of a staged plane (792)
+constexpr int kB3PPT = (kB3Pieces + 255) / 256;              // pieces per stage-A thread (4)
+static_assert(kB3J == 16 && kB3R2R == 19, "stage roles assume 16 output rows (19 y_m rows)");
+constexpr int kB3SmemRings = kB3D * (kB3R1P + kB3R2P) * 8;
+// + stage-B private staging of p_k / v / y_{m-1} (two rows x (K + 1) 16-B pieces per thread, two planes)
+__host__ __device__ constexpr int b3_np(int K) { return 2 * (K + 1); }
+__host__ __device__ constexpr int b3_smem(int K) { return kB3SmemRings + 2 * b3_np(K) * 16 * 256; }
+
+__device__ __forceinline__ int b3_inc(int x, int n) { return x + 1 == n ? 0 : x + 1; }
+
+// mbarrier helpers (CTA scope): the y_m ring's full / empty handshake between the two roles
+__device__ __forceinline__ void mbar_init(uint32_t bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "LX_MBW_%=:\n"
+        " mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra LX_MBW_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+// named barrier of the 256 stage-A threads (the y_{m-1} ring is theirs alone)
+__device__ __forceinline__ void bar_a() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+// A y (before the alpha / beta scaling) at the two columns of a pair, k_leja3d_smem's FMA order
+__device__ __forceinline__ double2 b3_apply(const Stencil& S, double2 yc, double2 up, double2 dn1, double2 dn2,
+                                            double2 wm, double2 wp1, double2 wp2, double left, double2 rt) {
+    double ax = S.c0 * yc.x;
+    ax = fma(S.m1[0], up.x, ax);
+    ax = fma(S.p1[0], dn1.x, ax);
+    ax = fma(S.p2[0], dn2.x, ax);
+    ax = fma(S.m1[1], wm.x, ax);
+    ax = fma(S.p1[1], wp1.x, ax);
+    ax = fma(S.p2[1], wp2.x, ax);
+    ax = fma(S.m1[2], left, ax);
+    ax = fma(S.p1[2], yc.y, ax);
+    ax = fma(S.p2[2], rt.x, ax);
+    double ay = S.c0 * yc.y;
+    ay = fma(S.m1[0], up.y, ay);
+    ay = fma(S.p1[0], dn1.y, ay);
+    ay = fma(S.p2[0], dn2.y, ay);
+    ay = fma(S.m1[1], wm.y, ay);
+    ay = fma(S.p1[1], wp1.y, ay);
+    ay = fma(S.p2[1], wp2.y, ay);
+    ay = fma(S.m1[2], yc.x, ay);
+    ay = fma(S.p1[2], rt.x, ay);
+    ay = fma(S.p2[2], rt.y, ay);
+    return make_double2(ax, ay);
+}
+
+// Per-pass coefficients (shared memory): d_m, d_{m+1}, d_0 (first pass), d_{m-1} (rollback)
+template <int K>
+struct B3Coef {
+    double ba, bb, alpha;
+    double da[K], db[K], d0[K], dr[K];
+};
+
+// Stage A, main warps: R consecutive y_m rows a0 .. a0+R-1 of the pair column `lane` (R2 columns 2 lane,
+// 2 lane + 1).  The own column's y_{m-1} at planes t-1, t, t+1 is kept in a register window (wu, wc, wd),
+// so a row costs its k-neighbours and plane t+2; the j-neighbours of the R rows are the R centres plus
+// three loads (R1 rows a0, a0+R+1, a0+R+2).
+template <int R>
+__device__ __forceinline__ void b3_stage_a(const Stencil& S, double alpha, double beta, uint32_t pc, uint32_t pd2,
+                                           uint32_t pw, int a0, int lane, double2 (&wu)[3], double2 (&wc)[3],
+                                           double2 (&wd)[3]) {
+    constexpr uint32_t RB = kB3R1C * 8;
+    const uint32_t cb = (uint32_t)a0 * RB + (uint32_t)((2 * lane + 2) * 8);   // R1 row a0 (= wm of row a0)
+    double2 col[R + 3];
+    col[0] = lds2(pc + cb);
+#pragma unroll
+    for (int r = 0; r < R; r++) col[1 + r] = wc[r];
+    col[R + 1] = lds2(pc + cb + (R + 1) * RB);
+    col[R + 2] = lds2(pc + cb + (R + 2) * RB);
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        const uint32_t c = cb + (r + 1) * RB;
+        const double2 dn2 = lds2(pd2 + c);
+        const double2 lf = lds2(pc + c - 16);
+        const double2 rt = lds2(pc + c + 16);
+        const double2 yc = col[r + 1];
+        const double2 ax = b3_apply(S, yc, wu[r], wd[r], dn2, col[r], col[r + 2], col[r + 3], lf.y, rt);
+        const double yx = fma(alpha, ax.x, beta * yc.x), yy = fma(alpha, ax.y, beta * yc.y);
+        const uint32_t o = pw + (uint32_t)((((a0 + r) * kB3R2C) + 2 * lane) * 8);
+        asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(o), "d"(yx), "d"(yy) : "memory");
+        wu[r] = yc;
+        wc[r] = wd[r];
+        wd[r] = dn2;
+    }
+}
+
+// R1 byte offset of the centre of stage-A edge task e (warp 7): row e % 19, pair 32 + e / 19
+__device__ __forceinline__ uint32_t b3_edge_c(int e) {
+    const int a = e % kB3R2R, b = 32 + e / kB3R2R;
+    return (uint32_t)(((a + 1) * kB3R1C + 2 * b + 2) * 8);
+}
+
+// Stage A, warp 7: the right-halo pairs 32, 33 (columns k0+62 .. k0+65) of all 19 rows (38 tasks, two per
+// lane), own column's window as the main warps
+__device__ __forceinline__ void b3_stage_a_edge(const Stencil& S, double alpha, double beta, uint32_t pc,
+                                                uint32_t pd2, uint32_t pw, int lane, double2 (&wu)[3],
+                                                double2 (&wc)[3], double2 (&wd)[3]) {
+    constexpr uint32_t RB = kB3R1C * 8;
+#pragma unroll
+    for (int rnd = 0; rnd < 2; rnd++) {
+        const int e = lane + 32 * rnd;
+        if (e < 2 * kB3R2R) {
+            const uint32_t c = b3_edge_c(e);
+            const double2 yc = wc[rnd];
+            const double2 dn2 = lds2(pd2 + c);
+            const double2 wm = lds2(pc + c - RB);
+            const double2 wp1 = lds2(pc + c + RB);
+            const double2 wp2 = lds2(pc + c + 2 * RB);
+            const double2 lf = lds2(pc + c - 16);
+            const double2 rt = lds2(pc + c + 16);
+            const double2 ax = b3_apply(S, yc, wu[rnd], wd[rnd], dn2, wm, wp1, wp2, lf.y, rt);
+            const double yx = fma(alpha, ax.x, beta * yc.x), yy = fma(alpha, ax.y, beta * yc.y);
+            const int a = e % kB3R2R, b = 32 + e / kB3R2R;
+            const uint32_t o = pw + (uint32_t)((a * kB3R2C + 2 * b) * 8);
+            asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(o), "d"(yx), "d"(yy) : "memory");
+            wu[rnd] = yc;
+            wc[rnd] = wd[rnd];
+            wd[rnd] = dn2;
         }
+    }
+}
+
+// Stage B (warps 8 .. 15, wb = warp - 8): y_{m+1} on plane s, output rows 2 wb, 2 wb + 1 (R2 rows
+// 2 wb + 1, + 2); j-neighbours shared between the two rows; p_m, p_{m+1} and the four norms.
+template <int K, bool FIRST>
+__device__ __forceinline__ void b3_stage_b(const LejaParams& P, const B3Coef<K>& C, double* __restrict__ dst,
+                                           uint32_t pm1, uint32_t ps, uint32_t pn1, uint32_t pt, uint32_t cbB,
+                                           long long off0, long long rstride, int act, int rbm, bool two,
+                                           uint32_t pst, double* sums) {
+    constexpr uint32_t RB2 = kB3R2C * 8;
+    const Stencil& S = P.st;
+    const double alpha = C.alpha, bb = C.bb;
+    double2 col[5];
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+        if (r == 0) {
+#pragma unroll
+            for (int i = 0; i < 4; i++) col[i] = lds2(ps + cbB + i * RB2);
+        } else {
+            col[4] = lds2(ps + cbB + 4 * RB2);
+        }
+        const uint32_t c = cbB + (r + 1) * RB2;
+        const double2 up = lds2(pm1 + c);
+        const double2 dn1 = lds2(pn1 + c);
+        const double2 dn2 = lds2(pt + c);
+        const double2 lf = lds2(ps + c - 16);
+        const double2 rt = lds2(ps + c + 16);
+        const double2 yc = col[r + 1];
+        const double2 ax = b3_apply(S, yc, up, dn1, dn2, col[r], col[r + 2], col[r + 3], lf.y, rt);
+        double2 yn;
+        yn.x = fma(alpha, ax.x, bb * yc.x);
+        yn.y = fma(alpha, ax.y, bb * yc.y);
+        const long long off = off0 + r * rstride;
+        st2(dst + off, yn);
+        sums[0] = fma(yc.x, yc.x, sums[0]);
+        sums[0] = fma(yc.y, yc.y, sums[0]);
+        sums[1 + K] = fma(yn.x, yn.x, sums[1 + K]);
+        sums[1 + K] = fma(yn.y, yn.y, sums[1 + K]);
+        // staged inputs of this thread (piece i at pst + 4096 i): p_k (i = r (K+1) + k), v / y_{m-1} (i = r (K+1) + K)
+        double2 yo = make_double2(0.0, 0.0);
+        if (FIRST || rbm) yo = lds2(pst + (uint32_t)((r * (K + 1) + K) * 4096));
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            if ((act >> k) & 1) {
+                double2 pm, pn;
+                if (FIRST) {
+                    pm.x = fma(C.da[k], yc.x, C.d0[k] * yo.x);
+                    pm.y = fma(C.da[k], yc.y, C.d0[k] * yo.y);
+                } else {
+                    const double2 pin = lds2(pst + (uint32_t)((r * (K + 1) + k) * 4096));
+                    pm.x = fma(C.da[k], yc.x, pin.x);
+                    pm.y = fma(C.da[k], yc.y, pin.y);
+                }
+                sums[1 + k] = fma(pm.x, pm.x, sums[1 + k]);
+                sums[1 + k] = fma(pm.y, pm.y, sums[1 + k]);
+                pn = pm;
+                if (two) {
+                    pn.x = fma(C.db[k], yn.x, pm.x);
+                    pn.y = fma(C.db[k], yn.y, pm.y);
+                }
+                sums[2 + K + k] = fma(pn.x, pn.x, sums[2 + K + k]);
+                sums[2 + K + k] = fma(pn.y, pn.y, sums[2 + K + k]);
+                st2(P.p[k] + off, pn);
+            } else if (!FIRST && ((rbm >> k) & 1)) {
+                const double2 pin = lds2(pst + (uint32_t)((r * (K + 1) + k) * 4096));
+                double2 pr;
+                pr.x = fma(-C.dr[k], yo.x, pin.x);
+                pr.y = fma(-C.dr[k], yo.y, pin.y);
+                st2(P.p[k] + off, pr);
+            }
+        }
+    }
+}
+
+// One unit (16 j x 64 k column of a run of kTI3 planes).  Stage A computes y_m on planes t = i0-1 .. i1+1,
+// stage B y_{m+1} on planes s = i0 .. i1-1 from y_m planes s-1 .. s+2.  The roles are decoupled: y_m ring
+// slot (x - i0 + 2) % 5 of plane x has a "full" mbarrier (256 stage-A arrivals after its stores) and an
+// "empty" one (256 stage-B arrivals after its last read, at s = x+1), so stage A runs up to two planes
+// ahead of stage B and the stage-B warps run independently of each other; the stage-A warps keep one
+// named barrier per plane for their own y_{m-1} ring.  Phase parities are tracked per slot (fb, eb).
+template <int K, bool FIRST>
+__device__ __forceinline__ void b3_unit(const LejaParams& P, const double* __restrict__ src, double* __restrict__ dst,
+                                        int cu, double* r1, double* r2, uint32_t bars, unsigned& ph,
+                                        const B3Coef<K>& C, int act, int rbm, bool two, double* sums) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n0 = P.n_loc, n1 = P.n1, n2 = P.n2;
+    const int njb = n1 / kB3J, nkb = n2 >> 6;
+    const int jb = cu % njb;
+    const int t0 = cu / njb;
+    const int kb = t0 % nkb;
+    const int ir = t0 / nkb;
+    const int j0 = jb * kB3J, k0 = kb * 64;
+    const int i0 = ir * kTI3, i1 = min(n0, i0 + kTI3);
+    const long long plane = (long long)n1 * n2;
+    const uint32_t b1 = smem_u32(r1), b2 = smem_u32(r2);
+    const uint32_t fullb = bars, emptyb = bars + kB3D * 8;
+    constexpr uint32_t RB1 = kB3R1C * 8, RB2 = kB3R2C * 8;
+    constexpr uint32_t SL1 = kB3R1P * 8, SL2 = kB3R2P * 8;   // slot bytes
+    if (warp < 8) {
+        const Stencil& S = P.st;
+        // this thread's pieces of a staged plane (fixed per unit): global offset in the plane, smem offset
+        int goff[kB3PPT];
+        uint32_t soff[kB3PPT];
+#pragma unroll
+        for (int q = 0; q < kB3PPT; q++) {
+            const int pc = tid + 256 * q;
+            goff[q] = -1;
+            soff[q] = 0;
+            if (pc < kB3Pieces) {
+                const int r = pc / (kB3R1C / 2), c2 = pc - r * (kB3R1C / 2);
+                int j = j0 - 2 + r;
+                j = j < 0 ? j + n1 : (j >= n1 ? j - n1 : j);
+                int k = k0 - 4 + 2 * c2;
+                k = k < 0 ? k + n2 : (k >= n2 ? k - n2 : k);
+                goff[q] = j * n2 + k;
+                soff[q] = (uint32_t)((r * kB3R1C + 2 * c2) * 8);
+            }
+        }
+        int pl = (i0 - 2) % n0;
+        if (pl < 0) pl += n0;
+        auto issue = [&](int slot) {
+            const double* base = src + (long long)pl * plane;
+            const uint32_t sb = b1 + (uint32_t)slot * SL1;
+#pragma unroll
+            for (int q = 0; q < kB3PPT; q++)
+                if (goff[q] >= 0)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + soff[q]), "l"(base + goff[q])
+                                 : "memory");
+            pl = b3_inc(pl, n0);
+        };
+#pragma unroll 1
+        for (int q = 0; q < 5; q++) {   // planes i0-2 .. i0+2 -> slots 0..4
+            issue(q);
+            cp_async_commit();
+        }
+        cp_async_wait<2>();
+        bar_a();
+        // stage-A window: own column's y_{m-1} at planes t-1, t, t+1 (slots 0, 1, 2 for t = i0-1)
+        double2 au[3], ac[3], ad[3];
+        if (warp < 7) {
+            const int a0 = warp < 6 ? 3 * warp : 18;
+#pragma unroll
+            for (int r = 0; r < 3; r++) {
+                if (warp < 6 || r == 0) {
+                    const uint32_t c = (uint32_t)(a0 + r + 1) * RB1 + (uint32_t)((2 * lane + 2) * 8);
+                    au[r] = lds2(b1 + c);
+                    ac[r] = lds2(b1 + SL1 + c);
+                    ad[r] = lds2(b1 + 2 * SL1 + c);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < 2; r++) {
+                if (lane + 32 * r < 2 * kB3R2R) {
+                    const uint32_t c = b3_edge_c(lane + 32 * r);
+                    au[r] = lds2(b1 + c);
+                    ac[r] = lds2(b1 + SL1 + c);
+                    ad[r] = lds2(b1 + 2 * SL1 + c);
+                }
+            }
+        }
+        int sc = 1;   // slot of plane t (both rings)
+        for (int t = i0 - 1; t <= i1 + 1; t++) {
+            cp_async_wait<1>();   // plane t+2 has landed (t+3 may be in flight)
+            bar_a();
+            const int si = sc == 0 ? 4 : sc - 1;   // slot of plane t-1 <- plane t+4
+            if (t + 4 <= i1 + 3) issue(si);
+            cp_async_commit();
+            const int s2 = sc >= 3 ? sc - 3 : sc + 2;   // slot of plane t+2
+            const uint32_t pc = b1 + (uint32_t)sc * SL1, pd2 = b1 + (uint32_t)s2 * SL1;
+            const uint32_t pw = b2 + (uint32_t)sc * SL2;
+            mbar_wait(emptyb + sc * 8, ((ph >> (8 + sc)) & 1) ^ 1);   // stage B released the slot's previous plane
+            ph ^= 1u << (8 + sc);
+            if (warp < 6) b3_stage_a<3>(S, C.alpha, C.ba, pc, pd2, pw, 3 * warp, lane, au, ac, ad);
+            else if (warp == 6) b3_stage_a<1>(S, C.alpha, C.ba, pc, pd2, pw, 18, lane, au, ac, ad);
+            else b3_stage_a_edge(S, C.alpha, C.ba, pc, pd2, pw, lane, au, ac, ad);
+            mbar_arrive(fullb + sc * 8);
+            sc = b3_inc(sc, kB3D);
+        }
+        cp_async_wait<0>();
+        bar_a();   // the y_{m-1} ring is refilled by the next unit
+    } else {
+        const int wb = warp - 8;
+        const uint32_t cbB = (uint32_t)(2 * wb) * RB2 + (uint32_t)((2 * lane + 2) * 8);   // R2 row 2 wb, pair lane
+        const long long rstride = n2;
+        long long off0 = ((long long)i0 * n1 + (j0 + 2 * wb)) * n2 + k0 + 2 * lane;   // plane s
+        // planes i0-1, i0, i0+1 (slots 1, 2, 3): wait for them once here (each fill is waited exactly once)
+#pragma unroll
+        for (int q = 1; q <= 3; q++) {
+            mbar_wait(fullb + q * 8, (ph >> q) & 1);
+            ph ^= 1u << q;
+        }
+        // per-thread staging of the plane's p_{m-1} (or v) / rollback operand, one plane ahead (cp.async;
+        // each thread reads only its own pieces, so its own wait_group orders them)
+        const uint32_t pbase = b2 + (uint32_t)kB3D * SL2 + (uint32_t)(tid - 256) * 16;
+        constexpr uint32_t PSL = (uint32_t)b3_np(K) * 4096;   // staging slot bytes
+        auto stage_in = [&](long long off, uint32_t d) {
+#pragma unroll
+            for (int r = 0; r < 2; r++) {
+                const long long o = off + r * rstride;
+                if (FIRST || rbm)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + (uint32_t)((r * (K + 1) + K) * 4096)),
+                                 "l"(src + o)
+                                 : "memory");
+#pragma unroll
+                for (int k = 0; k < K; k++)
+                    if (!FIRST && (((act | rbm) >> k) & 1))
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + (uint32_t)((r * (K + 1) + k) * 4096)),
+                                     "l"(P.p[k] + o)
+                                     : "memory");
+            }
+        };
+        stage_in(off0, pbase);
+        cp_async_commit();
+        uint32_t pslot = 0;
+        int sb = 1;   // slot of plane s-1
+        for (int s = i0; s < i1; s++) {
+            const int s0 = b3_inc(sb, kB3D), s1 = b3_inc(s0, kB3D), s2 = b3_inc(s1, kB3D);
+            if (s + 1 < i1) stage_in(off0 + plane, pbase + (pslot ^ PSL));
+            cp_async_commit();
+            cp_async_wait<1>();   // this plane's pieces have landed
+            mbar_wait(fullb + s2 * 8, (ph >> s2) & 1);   // y_m plane s+2 (and, in order, s-1 .. s+1)
+            ph ^= 1u << s2;
+            b3_stage_b<K, FIRST>(P, C, dst, b2 + (uint32_t)sb * SL2, b2 + (uint32_t)s0 * SL2, b2 + (uint32_t)s1 * SL2,
+                                 b2 + (uint32_t)s2 * SL2, cbB, off0, rstride, act, rbm, two, pbase + pslot, sums);
+            mbar_arrive(emptyb + sb * 8);   // plane s-1: last read
+            sb = s0;
+            off0 += plane;
+            pslot ^= PSL;
+        }
+        cp_async_wait<0>();
+        // planes i1-1, i1, i1+1 are not read again
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+            mbar_arrive(emptyb + sb * 8);
+            sb = b3_inc(sb, kB3D);
+        }
+    }
+}
+
+// Deterministic reduction over the 16 warps of a k_leja3d_tb2 CTA (result in thread 0)
+template <int N>
+__device__ __forceinline__ void b3_block_reduce(double (&v)[N], double (*s_red)[kSlot]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 0; i < N; i++) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v[i] += __shfl_xor_sync(FULL_MASK, v[i], off);
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < N; i++) s_red[warp][i] = v[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < N; i++) {
+            double x = s_red[0][i];
+            for (int w = 1; w < kB3Warps; w++) x += s_red[w][i];
+            v[i] = x;
+        }
+    }
+    __syncthreads();
+}
+
+// Grid barrier + the decisions of iterations m and m+1 (last arriver); word [63:32] gen0 + q + 1,
+// [31:24] status, [23:16] rollback mask, [15:8] done, [7:0] active.
+template <int K>
+__device__ __forceinline__ void b3_barrier_decide(const LejaParams& P, int q, int m, bool two, unsigned gen0,
+                                                  const B3Coef<K>& C, int active, double (*s_red)[kSlot], int* s_flags) {
+    constexpr int NV = 2 * (1 + K);
+    const int tid = threadIdx.x;
+    Ctrl* ctrl = P.ctrl;
+    const int par = q & 1;
+    __syncthreads();
+    if (tid == 0) {
+        const unsigned t = atom_add_acq_rel(&ctrl->arrive, 1u);
+        s_flags[0] = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (s_flags[0]) {
+        double acc[NV];
+#pragma unroll
+        for (int i = 0; i < NV; i++) acc[i] = 0.0;
+        for (int c = tid; c < (int)gridDim.x; c += kB3Threads) {
+            const double* slot = P.partials + ((size_t)par * gridDim.x + c) * kSlot;
+#pragma unroll
+            for (int i = 0; i < NV; i++) acc[i] += __ldcg(slot + i);
+        }
+        b3_block_reduce<NV>(acc, s_red);
+        if (tid == 0) {
+            Record* rec = P.rec;
+            int done = 0, status = 0, act = active;
+            leja_decide<K>(P, m, acc, C.da, act, done, status, rec);
+            const int rb = (two && status != 6) ? (active & ~act) : 0;
+            if (!done) {
+                if (two) leja_decide<K>(P, m + 1, acc + 1 + K, C.db, act, done, status, rec);
+                else { done = 1; status = 5; }   // unreachable: m < M - 1 implies two
+            }
+            ctrl->arrive = 0u;
+            const unsigned long long w = ((unsigned long long)(gen0 + (unsigned)q + 1u) << 32) |
+                                         ((unsigned long long)(status & 0xff) << 24) |
+                                         ((unsigned long long)(rb & 0xff) << 16) |
+                                         ((unsigned long long)(done & 0xff) << 8) | (unsigned long long)(act & 0xff);
+            st_release64(&ctrl->word, w);
+            s_flags[1] = done;
+            s_flags[2] = act;
+            s_flags[3] = rb;
+        }
+    } else if (tid == 0) {
+        unsigned long long w = ld_relaxed64(&ctrl->word);
+        int spins = 0;
+        while ((int)((unsigned)(w >> 32) - gen0) < q + 1) {
+            if (++spins > 32) __nanosleep(32);
+            if (spins > P.timeout_spins) {
+                atomicExch(&P.rec->status, 10);  // LX_ERR_TIMEOUT
+                w = (1ull << 8);
+                break;
+            }
+            w = ld_relaxed64(&ctrl->word);
+        }
+        fence_acquire();
+        s_flags[1] = (int)((w >> 8) & 0xff);
+        s_flags[2] = (int)(w & 0xff);
+        s_flags[3] = (int)((w >> 16) & 0xff);
+    }
+    __syncthreads();
+}
+
+template <int K>
+__global__ void __launch_bounds__(kB3Threads, 1) k_leja3d_tb2(const __grid_constant__ LejaParams P) {
+    __shared__ double s_red[kB3Warps][kSlot];
+    __shared__ int s_flags[4];
+    extern __shared__ double b3_ring[];
+    __shared__ __align__(8) unsigned long long s_bar[2 * kB3D];   // y_m ring: full[5], empty[5]
+    double* r1 = b3_ring;
+    double* r2 = b3_ring + kB3D * kB3R1P;
+    const int tid = threadIdx.x;
+    const uint32_t bars = smem_u32(s_bar);
+    unsigned ph = 0;   // bits 0..4: full-barrier parities (stage B), 8..12: empty-barrier parities (stage A)
+    if (tid == 0) {
+        for (int q = 0; q < 2 * kB3D; q++) mbar_init(bars + q * 8, 256);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    unsigned gen0 = 0;
+    if (tid == 0) gen0 = (unsigned)(ld_acquire64(&P.ctrl->word) >> 32);
+    int active = P.active0, rbm = 0;
+    const int M = P.max_nodes;
+    const int ncu = (P.n1 / kB3J) * (P.n2 >> 6) * ((P.n_loc + kTI3 - 1) / kTI3);
+    // per-pass coefficients in shared memory (broadcast reads; registers are the scarce resource)
+    __shared__ B3Coef<K> C;
+    if (tid == 0) {
+        C.alpha = P_alpha(P);
+        for (int k = 0; k < K; k++) {
+            C.d0[k] = P.table[1 + k];
+            C.dr[k] = 0.0;
+        }
+    }
+    for (int q = 0;; q++) {
+        const int m = 2 * q + 1;
+        const bool two = m + 1 < M;
+        if (tid == 0) {
+            C.ba = coef_beta(P, m);
+            C.bb = two ? coef_beta(P, m + 1) : 0.0;
+            for (int k = 0; k < K; k++) {
+                C.dr[k] = q ? C.db[k] : 0.0;
+                C.da[k] = P.table[(size_t)m * (1 + K) + 1 + k];
+                C.db[k] = two ? P.table[(size_t)(m + 1) * (1 + K) + 1 + k] : 0.0;
+            }
+        }
+        __syncthreads();
+        double sums[2 * (1 + K)];
+#pragma unroll
+        for (int i = 0; i < 2 * (1 + K); i++) sums[i] = 0.0;
+        double* dst = P.ydst[q & 1];
+        if (q == 0) {
+            for (int cu = blockIdx.x; cu < ncu; cu += gridDim.x)
+                b3_unit<K, true>(P, P.v.base, dst, cu, r1, r2, bars, ph, C, active, 0, two, sums);
+        } else {
+            const double* src = P.ydst[(q - 1) & 1];
+            for (int cu = blockIdx.x; cu < ncu; cu += gridDim.x)
+                b3_unit<K, false>(P, src, dst, cu, r1, r2, bars, ph, C, active, rbm, two, sums);
+        }
+        b3_block_reduce<2 * (1 + K)>(sums, s_red);
+        if (tid == 0) {
+            double* slot = P.partials + ((size_t)(q & 1) * gridDim.x + blockIdx.x) * kSlot;
+#pragma unroll
+            for (int i = 0; i < 2 * (1 + K); i++) slot[i] = sums[i];
+        }
+        b3_barrier_decide<K>(P, q, m, two, gen0, C, active, s_red, s_flags);
+        active = s_flags[2];
+        rbm = s_flags[3];
+        if (s_flags[1]) {
+            // end of the call: roll back accumulators that converged at m (p holds one term too many)
+            if (rbm) {
+                const size_t npair = (size_t)P.n_loc * P.n1 * P.n2 / 2;
+                for (size_t i = (size_t)blockIdx.x * kB3Threads + tid; i < npair; i += (size_t)gridDim.x * kB3Threads) {
+                    const double2 y = ld2(dst + 2 * i);
+#pragma unroll
+                    for (int k = 0; k < K; k++) {
+                        if ((rbm >> k) & 1) {
+                            double2 p = ld2(P.p[k] + 2 * i);
+                            p.x = fma(-C.db[k], y.x, p.x);
+                            p.y = fma(-C.db[k], y.y, p.y);
+                            st2(P.p[k] + 2 * i, p);
+                        }
+                    }
+                }
+            }
+            break;
+        }
+    }
+}
+
+static void* leja3d_tb2_ptr(int K) {
+    switch (K) {
+        case 1: return (void*)k_leja3d_tb2<1>;
+        case 2: return (void*)k_leja3d_tb2<2>;
+        case 3: return (void*)k_leja3d_tb2<3>;
+        case 4: return (void*)k_leja3d_tb2<4>;
+    }
+    return nullptr;
+}
+
+int leja3d_tb2_grid_size(int device, int K, int ncu) {
+    void* kern = leja3d_tb2_ptr(K);
+    if (!kern) return 0;
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, int> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find({device, kern});
+    int g;
+    if (it != cache.end()) {
+        g = it->second;
+    } else {
+        int nsm = 0, per = 0;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, b3_smem(K));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kB3Threads, b3_smem(K));
+        g = nsm * (per < 1 ? 1 : per);
+        cache[{device, kern}] = g;
+    }
+    return g < ncu ? g : ncu;
+}
+
+cudaError_t launch_leja3d_tb2(const LejaParams& P, cudaStream_t s) {
+    void* kern = leja3d_tb2_ptr(P.K);
+    if (!kern) return cudaErrorInvalidValue;
+    void* args[] = {(void*)&P};
+    return cudaLaunchCooperativeKernel(kern, dim3(P.grid), dim3(kB3Threads), args, b3_smem(P.K), s);
+}
+
+cudaError_t preload_3d() {
+    for (int K = 1; K <= kMaxK; K++) {
+        cudaFuncAttributes a;
+        if (cudaFuncGetAttributes(&a, leja3d_tb2_ptr(K)) != cudaSuccess) return cudaGetLastError();
+        for (int d = 0; d < 2; d++)
+            if (cudaFuncGetAttributes(&a, leja3d_smem_ptr(K, d != 0)) != cudaSuccess) return cudaGetLastError();
+    }
     return cudaSuccess;
 }
 

@@ -545,6 +545,57 @@ def test_3d_smem_kernel_bitwise_equals_tiles(xi300, shape, K, react):
         assert np.linalg.norm(a - ref) <= TOL * np.linalg.norm(ref)
 
 
+@pytest.mark.parametrize("shape,K,l", [((20, 32, 64), 1, 0), ((70, 16, 128), 2, 1), ((130, 48, 64), 3, 1),
+                                       ((7, 16, 64), 4, 2), ((4, 32, 192), 1, 3), ((66, 16, 64), 3, 4)])
+def test_3d_tblock2_vs_one_pass(xi300, shape, K, l):
+    # 3D two-step kernel (2.5D temporal blocking: two Leja iterations per plane sweep; plane runs of 64 with
+    # a ragged last run, runs shorter than the 6-plane halo, accumulators converging on either half of a
+    # pass -> rollback) against the one-pass shared-memory kernel and the oracle: same iteration counts;
+    # y and p bitwise those of the one-pass kernel except after a rollback (a few ulp)
+    pb, ob = _pair(shape)
+    v = W.ic_random(shape, seed=41 + K, amp=0.2)
+    dt = 5 * min(W.dt_cfl(n, 10.0, 3) for n in shape)
+    coeffs = (0.25, 0.5, 2 / 3, 1.0)[-K:]
+    res = {}
+    for tb in (1, 2):
+        with lx.Context(pb) as ctx:
+            ctx.set_kernel(tb)
+            assert ctx.iterations_per_pass == tb
+            c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+            outs = [torch.full(shape, float("nan"), dtype=torch.float64, device="cuda") for _ in range(K)]
+            it = lx.lx_real_leja_phi_vertical(ctx, _dev(v), outs, coeffs, dt, c, g, l, TOL, TOL)
+            res[tb] = (it, [o.cpu().numpy() for o in outs])
+    r = O.real_leja_phi(ob, v, dt, c, g, l, TOL, TOL, xi300, coeffs=coeffs)
+    assert res[2][0] == res[1][0] == r.iters
+    for a, b, ref in zip(res[2][1], res[1][1], r.outs):
+        assert np.isfinite(a).all()
+        np.testing.assert_allclose(a, b, rtol=0, atol=8 * np.finfo(float).eps * np.abs(b).max())
+        assert np.linalg.norm(a - ref) <= TOL * np.linalg.norm(ref)
+
+
+def test_3d_tblock2_auto_and_limits(xi300):
+    # auto policy: two-step from 2^20 points on (n1 % 16 == 0, n2 % 64 == 0), one pass below / for other
+    # shapes; the NOCONV limit (R28) and a NONFINITE run end with the same status and m as the oracle
+    for shape, want in (((64, 64, 256), 2), ((32, 64, 256), 1), ((64, 72, 256), 1), ((256, 64, 96), 1)):
+        with lx.Context(_pair(shape)[0]) as ctx:
+            assert ctx.iterations_per_pass == want, shape
+    n = 16
+    shape = (n, n, 4 * n)
+    pb, ob = _pair(shape)
+    v = W.ic_random(shape, seed=4, amp=0.5)
+    c, g = O.shift_scale(O.spectrum_bound(ob))
+    for dt, fac, status in ((20.0 * W.dt_cfl(n, 10.0, 3), 1.0, lx.LX_ERR_NOCONV),   # m = 299: first half, cap
+                            (W.dt_cfl(n, 10.0, 3), 1e-4, lx.LX_ERR_NONFINITE)):
+        r = O.real_leja_phi(ob, v, dt, c * fac, g * fac, 0, TOL, TOL, xi300)
+        assert r.status == {lx.LX_ERR_NOCONV: O.ERR_NOCONV, lx.LX_ERR_NONFINITE: O.ERR_NONFINITE}[status]
+        with lx.Context(pb) as ctx:
+            ctx.set_kernel(2)
+            out = torch.empty(shape, dtype=torch.float64, device="cuda")
+            it = _expect_status(lambda: lx.lx_real_leja_phi(ctx, _dev(v), out, dt, c * fac, g * fac, 0, TOL, TOL),
+                                status)
+        assert it == r.iters
+
+
 # ---------------------------------------------------------------- non-finite and divergent runs
 def _expect_status(fn, status):
     with pytest.raises(lx.LxError) as e:
