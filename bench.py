@@ -236,6 +236,25 @@ def leja_bytes_per_point_vertical(m_k):
     return b
 
 
+def leja_bytes_per_point_vertical_tb2(m_k):
+    """3D two-step kernel (k_leja3d_tb2, two iterations per plane sweep) with K accumulators frozen at m_k.
+    Pass q performs iterations 2q+1, 2q+2.  Pass 0 reads v and writes y and every accumulator (16 + 8K B);
+    pass q >= 1 reads and writes y (16 B) and every accumulator still active at 2q+1 (16 B each), plus, in
+    place, every accumulator that converged on the first iteration of pass q-1 (rollback: read p, write p;
+    its operand y_{2q-1} is the pass's own input).  An accumulator that converged on the first iteration of
+    the LAST pass is rolled back by the end-of-call fix-up (read y; read, write p)."""
+    M = max(m_k)
+    Q = (M + 1) // 2
+    b = 16 + 8 * len(m_k)
+    for q in range(1, Q):
+        m = 2 * q + 1
+        b += 16 + 16 * sum(1 for mk in m_k if mk >= m or mk == m - 2)
+    rb = sum(1 for mk in m_k if mk == 2 * Q - 1)
+    if rb:
+        b += 8 + 16 * rb
+    return b
+
+
 def _traffic_from_profiles():
     p = os.path.join(ROOT, "profiles", "leja_traffic.json")
     if os.path.exists(p):
@@ -512,9 +531,14 @@ def bench_epirk_3d(job, args, wl):
     torch.cuda.synchronize()
     ctx.synchronize()
     kms = float(np.mean([ea.elapsed_time(eb) for ea, eb in evs]))
-    kbytes = N * leja_bytes_per_point_vertical(m_k)
-    kname = ("k_leja3d_smem<3,false> (shared-memory plane tiles, 1 launch per Leja call)" if ws == 1 else
-             "k_leja2d_step<3,3,false> (step protocol, one launch per iteration; rank 0)")
+    tb3 = ctx.iterations_per_pass == 2
+    kbytes = N * (leja_bytes_per_point_vertical_tb2(m_k) if tb3 else leja_bytes_per_point_vertical(m_k))
+    if ws > 1:
+        kname = "k_leja2d_step<3,3,false> (step protocol, one launch per iteration; rank 0)"
+    elif tb3:
+        kname = "k_leja3d_tb2<3> (2.5D temporal blocking: two Leja iterations per plane sweep, 1 launch per call)"
+    else:
+        kname = "k_leja3d_smem<3,false> (shared-memory plane tiles, 1 launch per Leja call)"
     roof = _roofline(kname, [kbytes], [kms], {"accumulator_iters": m_k,
                                               "kernel_share_of_step_estimate": kms / (ms / args.steps)})
 

@@ -61,3 +61,32 @@ def _passes_vertical(m_k):
 @pytest.mark.parametrize("m_k", [(1,), (5, 7, 9), (13, 14, 16), (3, 3)])
 def test_vertical_bytes_match_pass_model(m_k):
     assert bench.leja_bytes_per_point_vertical(list(m_k)) == _passes_vertical(m_k)
+
+
+def _passes_vertical_tb2(m_k):
+    # 3D two-step kernel: pass q performs iterations 2q+1, 2q+2 and touches y plus the accumulators it
+    # updates or rolls back; simulated iteration by iteration
+    M = max(m_k)
+    traffic = 0
+    pending = set()                          # accumulators whose p holds one term too many
+    for q in range((M + 1) // 2):
+        m = 2 * q + 1
+        if q == 0:
+            traffic += 8 * (1 + 1 + len(m_k))    # read v; write y_2 and every p
+        else:
+            touched = {k for k, mk in enumerate(m_k) if mk >= m} | pending
+            traffic += 8 * 2 + 16 * len(touched)
+        pending = {k for k, mk in enumerate(m_k) if mk == m}   # stopped on the first iteration of pass q
+    if pending:                              # end-of-call fix-up
+        traffic += 8 + 16 * len(pending)
+    return traffic
+
+
+@pytest.mark.parametrize("m_k", [(1,), (2,), (5, 7, 9), (13, 14, 16), (3, 3), (4, 5, 6), (9, 11, 12), (7, 8, 8, 9)])
+def test_vertical_tb2_bytes_match_pass_model(m_k):
+    assert bench.leja_bytes_per_point_vertical_tb2(list(m_k)) == _passes_vertical_tb2(m_k)
+
+
+@pytest.mark.parametrize("m", list(range(1, 30)))
+def test_vertical_tb2_single_accumulator_is_two_step(m):
+    assert bench.leja_bytes_per_point_vertical_tb2([m]) == bench.leja_bytes_per_point(m, True)
