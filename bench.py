@@ -255,8 +255,8 @@ def leja_bytes_per_point_vertical_tb2(m_k):
     return b
 
 
-def _traffic_from_profiles():
-    p = os.path.join(ROOT, "profiles", "leja_traffic.json")
+def _traffic_from_profiles(name="leja_traffic.json"):
+    p = os.path.join(ROOT, "profiles", name)
     if os.path.exists(p):
         try:
             return json.load(open(p))
@@ -350,10 +350,10 @@ class Job:
             self.torch.distributed.destroy_process_group()
 
 
-def _roofline(kernel, bytes_per_launch, launch_ms, extra=None):
+def _roofline(kernel, bytes_per_launch, launch_ms, extra=None, traffic_file="leja_traffic.json"):
     peak, peak_kind = _peaks()
     achieved = float(np.sum(bytes_per_launch) / (np.sum(launch_ms) * 1e-3) / 1e9)
-    tr = _traffic_from_profiles()
+    tr = _traffic_from_profiles(traffic_file)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": (tr or {}).get("traffic_bytes_per_launch"), "kernel": kernel,
             "algorithmic_bytes_per_launch": [float(b) for b in bytes_per_launch],
@@ -533,14 +533,18 @@ def bench_epirk_3d(job, args, wl):
     kms = float(np.mean([ea.elapsed_time(eb) for ea, eb in evs]))
     tb3 = ctx.iterations_per_pass == 2
     kbytes = N * (leja_bytes_per_point_vertical_tb2(m_k) if tb3 else leja_bytes_per_point_vertical(m_k))
-    if ws > 1:
+    if ws > 1 and tb3:
+        kname = ("k_leja3d_tb2<3,true> (peer-memory slab kernel: two Leja iterations per plane sweep, ghost "
+                 "planes stored into the neighbours' exchange blocks, 1 launch per call; rank 0)")
+    elif ws > 1:
         kname = "k_leja2d_step<3,3,false> (step protocol, one launch per iteration; rank 0)"
     elif tb3:
         kname = "k_leja3d_tb2<3> (2.5D temporal blocking: two Leja iterations per plane sweep, 1 launch per call)"
     else:
         kname = "k_leja3d_smem<3,false> (shared-memory plane tiles, 1 launch per Leja call)"
     roof = _roofline(kname, [kbytes], [kms], {"accumulator_iters": m_k,
-                                              "kernel_share_of_step_estimate": kms / (ms / args.steps)})
+                                              "kernel_share_of_step_estimate": kms / (ms / args.steps)},
+                     traffic_file="leja3d_traffic.json" if (tb3 and ws == 1) else "none")
 
     # e2e: lx_step on pinned host u / u_low / u_high (the library stages H2D / D2H inside the call)
     uh = torch.from_numpy(u_h).pin_memory()
@@ -561,8 +565,8 @@ def bench_epirk_3d(job, args, wl):
            "dt": wl.dt, "dt_cfl_mult": 10.0, "tol": 1e-10, "leja_iters_per_step": it_step,
            "l2_policy": "inputs larger than L2 (each fp64 vector %.0f MB > 126 MB L2)" % (N * 8 / 1e6),
            "inputs": "synthetic 3D Gaussian IC, nu=10",
-           "parallelism": ("slab%d (step protocol: NCCL halo + partial allgather per Leja iteration)" % ws)
-           if ws > 1 else "single GPU"}
+           "parallelism": ("slab%d (Leja calls: persistent peer-memory slab kernel; stage kernels: NCCL halo "
+                           "per stage)" % ws) if ws > 1 else "single GPU"}
     out = {"value": value, "ms_per_step": ms / args.steps, "scaling": "strong", "config": cfg, "roofline": roof,
            "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(), "unit": "steps/s"}
     ctx.close()

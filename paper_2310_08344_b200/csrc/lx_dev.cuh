@@ -936,4 +936,41 @@ inline int max_coresident(int device, Kern kern) {
 }
 
 
+// Cross-rank step of the slab kernel's barrier (ONE thread: the last arriver of this rank's grid
+// barrier).  The rank's NV partial sums go to slot [epoch & 1][rank] of EVERY rank's exchange header
+// (peer stores), then a system-scope release of flag[rank] = epoch on every rank; once all ranks'
+// flags reached the epoch, the NV sums are replaced by the rank-ordered totals (identical on every
+// rank -> identical decisions; with one rank, 0 + x = x: bitwise the single-domain sums).  A rank can
+// be at most one epoch ahead of another (it waits for everybody each epoch), so two parities suffice.
+// Returns 0, or 10 (LX_ERR_TIMEOUT) if a peer did not arrive within P.timeout_ns.
+template <int NV>
+__device__ __forceinline__ int xrank_sum(const LejaParams& P, double* acc) {
+    XHdr* me = P.xh[P.xrank];
+    const unsigned long long e = me->epoch + 1;
+    me->epoch = e;
+    const int par = (int)(e & 1);
+    for (int q = 0; q < P.xranks; q++) {
+        double* slot = &P.xh[q]->part[par][P.xrank][0];
+#pragma unroll
+        for (int i = 0; i < NV; i++) slot[i] = acc[i];
+    }
+    __threadfence_system();
+    for (int q = 0; q < P.xranks; q++) st_release_sys64(&P.xh[q]->flag[P.xrank], e);
+    const unsigned long long t0 = globaltimer_ns();
+    for (int q = 0; q < P.xranks; q++) {
+        while (ld_acquire_sys64(&me->flag[q]) < e) {
+            if (globaltimer_ns() - t0 > P.timeout_ns) return 10;
+            __nanosleep(32);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < NV; i++) {
+        double s = 0.0;
+        for (int q = 0; q < P.xranks; q++) s += __ldcv(&me->part[par][q][i]);
+        acc[i] = s;
+    }
+    return 0;
+}
+
+
 }  // namespace lx

@@ -276,7 +276,7 @@ static bool tb3_shape(const lx_ctx* ctx) {
 }
 
 static int ctx_tblock(const lx_ctx* ctx) {
-    if (ctx->comm) return (ctx->ndim == 2 && comm_peer_ready(ctx->comm)) ? 2 : 1;
+    if (ctx->comm) return ((ctx->ndim == 2 || tb3_shape(ctx)) && comm_peer_ready(ctx->comm)) ? 2 : 1;
     if (ctx->ndim == 3) {
         if (!tb3_shape(ctx) || ctx->tblock == 1) return 1;
         return (ctx->tblock == 2 || ctx->N_loc >= kTb3MinPoints) ? 2 : 1;
@@ -401,6 +401,20 @@ static lx_status tb2_setup(lx_ctx* ctx, LejaParams& P, int K, bool diag) {
     return LX_OK;
 }
 
+// The 3D kernels read the Newton coefficients from a table built by one k_coef_tables launch.
+static lx_status leja3d_table(lx_ctx* ctx, LejaParams& P, int K, int l, const double* coeffs, double dt, double c,
+                              double gamma, int rec) {
+    if (!P.coef_gen) return LX_OK;
+    CoefJobs jobs;
+    std::memset(&jobs, 0, sizeof jobs);
+    for (int k = 0; k < K; k++) jobs.j[jobs.n++] = CoefJob{P.table, coeffs[k], l, K, k};
+    CUDA_TRY(launch_coef_tables(ctx->xi_dev, ctx->rcp_dev, ctx->max_nodes, jobs, dt, c, gamma, ctx->cg_active,
+                                &ctx->rec_dev[rec].status, ctx->stream));
+    ctx->launches++;
+    P.coef_gen = 0;
+    return LX_OK;
+}
+
 static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u, const double* v, double* const* outs,
                              const double* coeffs, int K, double dt, double c, double gamma, int l, double rtol,
                              double atol, int rec, const double* table = nullptr) {
@@ -447,6 +461,15 @@ static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u,
             ctx->launches++;
             return LX_OK;
         }
+        if (P.ndim == 3 && !diag && comm_peer_ready(ctx->comm) && tb3_shape(ctx)) {
+            // 3D: the two-step plane-sweep kernel over peer memory (ghost planes, global barrier per pass)
+            LX_TRY(leja3d_table(ctx, P, K, l, coeffs, dt, c, gamma, rec));
+            P.grid = comm_grid_cap(ctx->comm, leja3d_tb2_grid_size(ctx->device, K, leja3d_smem_units(P.n_loc, P.n1, P.n2), true));
+            comm_peer_params(ctx->comm, P, diag);
+            CUDA_TRY(launch_leja3d_tb2(P, ctx->stream, true));
+            ctx->launches++;
+            return LX_OK;
+        }
         return comm_leja(ctx->comm, P, diag, ctx->stream, &ctx->launches);
     }
     if (P.ndim == 2 && ctx_tblock(ctx) == 2) {
@@ -457,15 +480,7 @@ static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u,
     }
     if (P.ndim == 3 && ctx->k3d != 1 && P.n1 % 16 == 0 && P.n2 % 64 == 0) {
         // 3D marching kernel with shared-memory plane tiles: Newton coefficients from a prebuilt table
-        if (P.coef_gen) {
-            CoefJobs jobs;
-            std::memset(&jobs, 0, sizeof jobs);
-            for (int k = 0; k < K; k++) jobs.j[jobs.n++] = CoefJob{P.table, coeffs[k], l, K, k};
-            CUDA_TRY(launch_coef_tables(ctx->xi_dev, ctx->rcp_dev, ctx->max_nodes, jobs, dt, c, gamma, ctx->cg_active,
-                                        &ctx->rec_dev[rec].status, ctx->stream));
-            ctx->launches++;
-            P.coef_gen = 0;
-        }
+        LX_TRY(leja3d_table(ctx, P, K, l, coeffs, dt, c, gamma, rec));
         const int ncu = leja3d_smem_units(P.n_loc, P.n1, P.n2);
         if (!diag && ctx_tblock(ctx) == 2) {
             // two Leja iterations per HBM pass (2.5D temporal blocking)
@@ -761,10 +776,13 @@ static lx_status prealloc_slab(lx_ctx* ctx) {
     return LX_OK;
 }
 
-// The persistent slab kernel over peer memory needs a 2D grid with >= 16 rows per rank and >= 64
-// columns (the same condition on every rank: all ranks take the same path).
+// The persistent slab kernels over peer memory need a 2D grid with >= 16 rows per rank and >= 64
+// columns, or a 3D grid of the two-step kernel's shape (n1 % 16 == 0, n2 % 64 == 0) with >= 4 planes per
+// rank (the same condition on every rank: all ranks take the same path).
 static bool peer_eligible(const lx_ctx* ctx, int nranks, int flags) {
-    return !(flags & LX_COMM_NO_PEER) && ctx->ndim == 2 && nranks <= 8 && ctx->n[0] / nranks >= 16 && ctx->n[1] >= 64;
+    if ((flags & LX_COMM_NO_PEER) || nranks > 8) return false;
+    if (ctx->ndim == 3) return ctx->n[1] % 16 == 0 && ctx->n[2] % 64 == 0 && ctx->n[0] / nranks >= 4;
+    return ctx->ndim == 2 && ctx->n[0] / nranks >= 16 && ctx->n[1] >= 64;
 }
 
 static lx_status detach_comm(lx_ctx* ctx) {

@@ -207,8 +207,10 @@ int leja_grid_size(int device, int K, bool diag, int ndim, int nunits);
 int leja3d_smem_grid_size(int device, int K, bool diag, int ncu);
 int leja3d_smem_units(int n0, int n1, int n2);
 cudaError_t launch_leja3d_smem(const LejaParams& P, cudaStream_t s, bool diag);
-int leja3d_tb2_grid_size(int device, int K, int ncu);
-cudaError_t launch_leja3d_tb2(const LejaParams& P, cudaStream_t s);
+// 3D two-step kernel (2.5D temporal blocking); slab = the peer-memory slab instantiation (ghost planes
+// -2, -1, n .. n+3 in the exchange block, norm partials exchanged at each pass barrier)
+int leja3d_tb2_grid_size(int device, int K, int ncu, bool slab = false);
+cudaError_t launch_leja3d_tb2(const LejaParams& P, cudaStream_t s, bool slab = false);
 // temporally blocked 2D kernel: two Leja iterations per HBM pass (single GPU, constant coefficients + diag)
 int leja_tb2_grid_size(int device, int K, bool diag, int nunits);
 cudaError_t launch_leja_tb2(const LejaParams& P, cudaStream_t s, bool diag, bool slab = false);

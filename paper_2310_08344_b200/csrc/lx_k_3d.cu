@@ -440,11 +440,11 @@ __device__ __forceinline__ void b3_stage_a_edge(const Stencil& S, double alpha, 
 
 // Stage B (warps 8 .. 15, wb = warp - 8): y_{m+1} on plane s, output rows 2 wb, 2 wb + 1 (R2 rows
 // 2 wb + 1, + 2); j-neighbours shared between the two rows; p_m, p_{m+1} and the four norms.
-template <int K, bool FIRST>
+template <int K, bool FIRST, bool SLAB>
 __device__ __forceinline__ void b3_stage_b(const LejaParams& P, const B3Coef<K>& C, double* __restrict__ dst,
                                            uint32_t pm1, uint32_t ps, uint32_t pn1, uint32_t pt, uint32_t cbB,
                                            long long off0, long long rstride, int act, int rbm, bool two,
-                                           uint32_t pst, double* sums) {
+                                           uint32_t pst, double* sums, double* x1, double* x2) {
     constexpr uint32_t RB2 = kB3R2C * 8;
     const Stencil& S = P.st;
     const double alpha = C.alpha, bb = C.bb;
@@ -470,6 +470,10 @@ __device__ __forceinline__ void b3_stage_b(const LejaParams& P, const B3Coef<K>&
         yn.y = fma(alpha, ax.y, bb * yc.y);
         const long long off = off0 + r * rstride;
         st2(dst + off, yn);
+        if (SLAB) {   // a boundary plane of y_{m+1}: also into the neighbour's ghost block (peer memory)
+            if (x1) st2(x1 + off, yn);
+            if (x2) st2(x2 + off, yn);
+        }
         sums[0] = fma(yc.x, yc.x, sums[0]);
         sums[0] = fma(yc.y, yc.y, sums[0]);
         sums[1 + K] = fma(yn.x, yn.x, sums[1 + K]);
@@ -516,10 +520,11 @@ __device__ __forceinline__ void b3_stage_b(const LejaParams& P, const B3Coef<K>&
 // "empty" one (256 stage-B arrivals after its last read, at s = x+1), so stage A runs up to two planes
 // ahead of stage B and the stage-B warps run independently of each other; the stage-A warps keep one
 // named barrier per plane for their own y_{m-1} ring.  Phase parities are tracked per slot (fb, eb).
-template <int K, bool FIRST>
+template <int K, bool FIRST, bool SLAB>
 __device__ __forceinline__ void b3_unit(const LejaParams& P, const double* __restrict__ src, double* __restrict__ dst,
                                         int cu, double* r1, double* r2, uint32_t bars, unsigned& ph,
-                                        const B3Coef<K>& C, int act, int rbm, bool two, double* sums) {
+                                        const B3Coef<K>& C, int act, int rbm, bool two, double* sums,
+                                        const double* gsrc, double* xup, double* xdn, bool& peer) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n0 = P.n_loc, n1 = P.n1, n2 = P.n2;
     const int njb = n1 / kB3J, nkb = n2 >> 6;
@@ -554,17 +559,24 @@ __device__ __forceinline__ void b3_unit(const LejaParams& P, const double* __res
                 soff[q] = (uint32_t)((r * kB3R1C + 2 * c2) * 8);
             }
         }
-        int pl = (i0 - 2) % n0;
-        if (pl < 0) pl += n0;
+        // plane pl of y_{m-1}: periodic wrap (single domain) or, in the slab kernel, planes -2, -1, n .. n+3
+        // from this rank's ghost block gsrc (slots 0, 1 = planes -2, -1; 2 .. 5 = planes n .. n+3)
+        int pl = i0 - 2;
+        if (!SLAB) {
+            pl %= n0;
+            if (pl < 0) pl += n0;
+        }
         auto issue = [&](int slot) {
-            const double* base = src + (long long)pl * plane;
+            const double* base;
+            if (SLAB && (unsigned)pl >= (unsigned)n0) base = gsrc + (long long)(pl < 0 ? pl + 2 : pl - n0 + 2) * plane;
+            else base = src + (long long)pl * plane;
             const uint32_t sb = b1 + (uint32_t)slot * SL1;
 #pragma unroll
             for (int q = 0; q < kB3PPT; q++)
                 if (goff[q] >= 0)
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + soff[q]), "l"(base + goff[q])
                                  : "memory");
-            pl = b3_inc(pl, n0);
+            pl = SLAB ? pl + 1 : b3_inc(pl, n0);
         };
 #pragma unroll 1
         for (int q = 0; q < 5; q++) {   // planes i0-2 .. i0+2 -> slots 0..4
@@ -659,8 +671,18 @@ __device__ __forceinline__ void b3_unit(const LejaParams& P, const double* __res
             cp_async_wait<1>();   // this plane's pieces have landed
             mbar_wait(fullb + s2 * 8, (ph >> s2) & 1);   // y_m plane s+2 (and, in order, s-1 .. s+1)
             ph ^= 1u << s2;
-            b3_stage_b<K, FIRST>(P, C, dst, b2 + (uint32_t)sb * SL2, b2 + (uint32_t)s0 * SL2, b2 + (uint32_t)s1 * SL2,
-                                 b2 + (uint32_t)s2 * SL2, cbB, off0, rstride, act, rbm, two, pbase + pslot, sums);
+            // slab: planes 0 .. 3 go to rank-1's ghost planes n .. n+3 (slots 2 .. 5), planes n-2, n-1 to
+            // rank+1's ghost planes -2, -1 (slots 0, 1); x + off addresses the ghost copy of dst + off
+            double* x1 = nullptr;
+            double* x2 = nullptr;
+            if (SLAB) {
+                if (s < 4) x1 = xup + 2 * plane;
+                if (s >= n0 - 2) x2 = xdn + (2 - (long long)n0) * plane;
+                peer |= (x1 != nullptr) | (x2 != nullptr);
+            }
+            b3_stage_b<K, FIRST, SLAB>(P, C, dst, b2 + (uint32_t)sb * SL2, b2 + (uint32_t)s0 * SL2,
+                                       b2 + (uint32_t)s1 * SL2, b2 + (uint32_t)s2 * SL2, cbB, off0, rstride, act,
+                                       rbm, two, pbase + pslot, sums, x1, x2);
             mbar_arrive(emptyb + sb * 8);   // plane s-1: last read
             sb = s0;
             off0 += plane;
@@ -703,13 +725,19 @@ __device__ __forceinline__ void b3_block_reduce(double (&v)[N], double (*s_red)[
 
 // Grid barrier + the decisions of iterations m and m+1 (last arriver); word [63:32] gen0 + q + 1,
 // [31:24] status, [23:16] rollback mask, [15:8] done, [7:0] active.
-template <int K>
+// SLAB: every thread that stored ghost planes into a neighbour fences them system-wide before the CTA
+// arrives; the last arriver exchanges the rank's partial sums with every rank (xrank_sum), which also
+// makes the barrier global: no rank starts pass q+1 (which overwrites the ghost planes its neighbours
+// read in pass q-1 ... and reads the ones they wrote in pass q) before every rank finished pass q.
+template <int K, bool SLAB>
 __device__ __forceinline__ void b3_barrier_decide(const LejaParams& P, int q, int m, bool two, unsigned gen0,
-                                                  const B3Coef<K>& C, int active, double (*s_red)[kSlot], int* s_flags) {
+                                                  const B3Coef<K>& C, int active, double (*s_red)[kSlot], int* s_flags,
+                                                  bool peer) {
     constexpr int NV = 2 * (1 + K);
     const int tid = threadIdx.x;
     Ctrl* ctrl = P.ctrl;
     const int par = q & 1;
+    if (SLAB && peer) __threadfence_system();
     __syncthreads();
     if (tid == 0) {
         const unsigned t = atom_add_acq_rel(&ctrl->arrive, 1u);
@@ -729,8 +757,13 @@ __device__ __forceinline__ void b3_barrier_decide(const LejaParams& P, int q, in
         if (tid == 0) {
             Record* rec = P.rec;
             int done = 0, status = 0, act = active;
-            leja_decide<K>(P, m, acc, C.da, act, done, status, rec);
-            const int rb = (two && status != 6) ? (active & ~act) : 0;
+            if (SLAB && xrank_sum<NV>(P, acc)) {   // a peer did not arrive: LX_ERR_TIMEOUT on this rank
+                atomicExch(&rec->status, 10);
+                done = 1;
+                status = 10;
+            }
+            if (!done) leja_decide<K>(P, m, acc, C.da, act, done, status, rec);
+            const int rb = (two && status != 6 && status != 10) ? (active & ~act) : 0;
             if (!done) {
                 if (two) leja_decide<K>(P, m + 1, acc + 1 + K, C.db, act, done, status, rec);
                 else { done = 1; status = 5; }   // unreachable: m < M - 1 implies two
@@ -765,7 +798,52 @@ __device__ __forceinline__ void b3_barrier_decide(const LejaParams& P, int q, in
     __syncthreads();
 }
 
-template <int K>
+// Prologue of the slab kernel: this rank's boundary planes of v into the neighbours' ghost blocks (planes
+// 0 .. 3 -> rank-1's planes n .. n+3, planes n-2, n-1 -> rank+1's planes -2, -1), then a global barrier
+// (grid barrier + an empty cross-rank exchange) so that pass 0 reads complete ghosts.  Generation gen0+1.
+__device__ __forceinline__ void b3_slab_prologue(const LejaParams& P, unsigned gen0, int* s_flags) {
+    const long long plane = (long long)P.n1 * P.n2, half = plane / 2;
+    const int n = P.n_loc;
+    for (long long t = (long long)blockIdx.x * kB3Threads + threadIdx.x; t < 6 * half;
+         t += (long long)gridDim.x * kB3Threads) {
+        const int pr = (int)(t / half);
+        const long long o = 2 * (t - pr * half);
+        const int src = pr < 4 ? pr : n - 6 + pr;
+        double* g = pr < 4 ? P.hup_v + (2 + pr) * plane : P.hdn_v + (pr - 4) * plane;
+        st2(g + o, ld2(P.v.base + src * plane + o));
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Ctrl* ctrl = P.ctrl;
+        const unsigned t = atom_add_acq_rel(&ctrl->arrive, 1u);
+        if (t == gridDim.x - 1) {
+            double none[1] = {0.0};
+            const int st = xrank_sum<0>(P, none);
+            if (st) atomicExch(&P.rec->status, 10);
+            ctrl->arrive = 0u;
+            st_release64(&ctrl->word, ((unsigned long long)(gen0 + 1u) << 32) | (st ? (1ull << 8) : 0ull));
+            s_flags[1] = st != 0;
+        } else {
+            unsigned long long w = ld_relaxed64(&ctrl->word);
+            const unsigned long long t0 = globaltimer_ns();
+            while ((int)((unsigned)(w >> 32) - gen0) < 1) {
+                __nanosleep(32);
+                if (globaltimer_ns() - t0 > P.timeout_ns + 1000000000ull) {
+                    atomicExch(&P.rec->status, 10);
+                    w = (1ull << 8);
+                    break;
+                }
+                w = ld_relaxed64(&ctrl->word);
+            }
+            fence_acquire();
+            s_flags[1] = (int)((w >> 8) & 0xff);
+        }
+    }
+    __syncthreads();
+}
+
+template <int K, bool SLAB>
 __global__ void __launch_bounds__(kB3Threads, 1) k_leja3d_tb2(const __grid_constant__ LejaParams P) {
     __shared__ double s_red[kB3Warps][kSlot];
     __shared__ int s_flags[4];
@@ -783,6 +861,11 @@ __global__ void __launch_bounds__(kB3Threads, 1) k_leja3d_tb2(const __grid_const
     __syncthreads();
     unsigned gen0 = 0;
     if (tid == 0) gen0 = (unsigned)(ld_acquire64(&P.ctrl->word) >> 32);
+    if (SLAB) {
+        b3_slab_prologue(P, gen0, s_flags);
+        if (s_flags[1]) return;   // a peer never arrived (LX_ERR_TIMEOUT recorded)
+        gen0 += 1u;
+    }
     int active = P.active0, rbm = 0;
     const int M = P.max_nodes;
     const int ncu = (P.n1 / kB3J) * (P.n2 >> 6) * ((P.n_loc + kTI3 - 1) / kTI3);
@@ -812,13 +895,20 @@ __global__ void __launch_bounds__(kB3Threads, 1) k_leja3d_tb2(const __grid_const
 #pragma unroll
         for (int i = 0; i < 2 * (1 + K); i++) sums[i] = 0.0;
         double* dst = P.ydst[q & 1];
+        bool peer = false;
+        // slab: y_{m-1}'s ghost planes (this rank's block) and the neighbours' ghost blocks of y_{m+1}
+        const double* gsrc = SLAB ? (q == 0 ? P.gv : P.gy[(q - 1) & 1]) : nullptr;
+        double* xup = SLAB ? P.hup[q & 1] : nullptr;
+        double* xdn = SLAB ? P.hdn[q & 1] : nullptr;
         if (q == 0) {
             for (int cu = blockIdx.x; cu < ncu; cu += gridDim.x)
-                b3_unit<K, true>(P, P.v.base, dst, cu, r1, r2, bars, ph, C, active, 0, two, sums);
+                b3_unit<K, true, SLAB>(P, P.v.base, dst, cu, r1, r2, bars, ph, C, active, 0, two, sums, gsrc, xup,
+                                       xdn, peer);
         } else {
             const double* src = P.ydst[(q - 1) & 1];
             for (int cu = blockIdx.x; cu < ncu; cu += gridDim.x)
-                b3_unit<K, false>(P, src, dst, cu, r1, r2, bars, ph, C, active, rbm, two, sums);
+                b3_unit<K, false, SLAB>(P, src, dst, cu, r1, r2, bars, ph, C, active, rbm, two, sums, gsrc, xup,
+                                        xdn, peer);
         }
         b3_block_reduce<2 * (1 + K)>(sums, s_red);
         if (tid == 0) {
@@ -826,7 +916,7 @@ __global__ void __launch_bounds__(kB3Threads, 1) k_leja3d_tb2(const __grid_const
 #pragma unroll
             for (int i = 0; i < 2 * (1 + K); i++) slot[i] = sums[i];
         }
-        b3_barrier_decide<K>(P, q, m, two, gen0, C, active, s_red, s_flags);
+        b3_barrier_decide<K, SLAB>(P, q, m, two, gen0, C, active, s_red, s_flags, peer);
         active = s_flags[2];
         rbm = s_flags[3];
         if (s_flags[1]) {
@@ -851,18 +941,27 @@ __global__ void __launch_bounds__(kB3Threads, 1) k_leja3d_tb2(const __grid_const
     }
 }
 
-static void* leja3d_tb2_ptr(int K) {
+static void* leja3d_tb2_ptr(int K, bool slab) {
+    if (slab) {
+        switch (K) {
+            case 1: return (void*)k_leja3d_tb2<1, true>;
+            case 2: return (void*)k_leja3d_tb2<2, true>;
+            case 3: return (void*)k_leja3d_tb2<3, true>;
+            case 4: return (void*)k_leja3d_tb2<4, true>;
+        }
+        return nullptr;
+    }
     switch (K) {
-        case 1: return (void*)k_leja3d_tb2<1>;
-        case 2: return (void*)k_leja3d_tb2<2>;
-        case 3: return (void*)k_leja3d_tb2<3>;
-        case 4: return (void*)k_leja3d_tb2<4>;
+        case 1: return (void*)k_leja3d_tb2<1, false>;
+        case 2: return (void*)k_leja3d_tb2<2, false>;
+        case 3: return (void*)k_leja3d_tb2<3, false>;
+        case 4: return (void*)k_leja3d_tb2<4, false>;
     }
     return nullptr;
 }
 
-int leja3d_tb2_grid_size(int device, int K, int ncu) {
-    void* kern = leja3d_tb2_ptr(K);
+int leja3d_tb2_grid_size(int device, int K, int ncu, bool slab) {
+    void* kern = leja3d_tb2_ptr(K, slab);
     if (!kern) return 0;
     static std::mutex mu;
     static std::map<std::pair<int, const void*>, int> cache;
@@ -882,8 +981,8 @@ int leja3d_tb2_grid_size(int device, int K, int ncu) {
     return g < ncu ? g : ncu;
 }
 
-cudaError_t launch_leja3d_tb2(const LejaParams& P, cudaStream_t s) {
-    void* kern = leja3d_tb2_ptr(P.K);
+cudaError_t launch_leja3d_tb2(const LejaParams& P, cudaStream_t s, bool slab) {
+    void* kern = leja3d_tb2_ptr(P.K, slab);
     if (!kern) return cudaErrorInvalidValue;
     void* args[] = {(void*)&P};
     return cudaLaunchCooperativeKernel(kern, dim3(P.grid), dim3(kB3Threads), args, b3_smem(P.K), s);
@@ -892,7 +991,8 @@ cudaError_t launch_leja3d_tb2(const LejaParams& P, cudaStream_t s) {
 cudaError_t preload_3d() {
     for (int K = 1; K <= kMaxK; K++) {
         cudaFuncAttributes a;
-        if (cudaFuncGetAttributes(&a, leja3d_tb2_ptr(K)) != cudaSuccess) return cudaGetLastError();
+        for (int sl = 0; sl < 2; sl++)
+            if (cudaFuncGetAttributes(&a, leja3d_tb2_ptr(K, sl != 0)) != cudaSuccess) return cudaGetLastError();
         for (int d = 0; d < 2; d++)
             if (cudaFuncGetAttributes(&a, leja3d_smem_ptr(K, d != 0)) != cudaSuccess) return cudaGetLastError();
     }

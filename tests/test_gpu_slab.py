@@ -275,3 +275,85 @@ def test_peer_slab_kernel_two_processes_ipc(xi300):
             one = torch.empty(shape, dtype=torch.float64, device="cuda")
             lx.lx_real_leja_phi(ctx1, torch.from_numpy(v).cuda(), one, dt, c, g, l, TOL, TOL)
             np.testing.assert_array_equal(full, one.cpu().numpy())
+
+
+def _slab3d_vs_single(xi300, P, shape, K, l, flags=0, mult=5.0):
+    """3D: P virtual ranks through the peer-memory two-step plane-sweep kernel (k_leja3d_tb2<K, true>:
+    ghost planes stored into the neighbours' exchange blocks by stage B, norm partials exchanged at every
+    pass barrier) vs the single-domain k_leja3d_tb2 (bitwise) and the oracle (same iterations, 1e-10)."""
+    dx = tuple(2.0 / n for n in shape)
+    pb = lx.Problem(shape, dx, 1.0, 10.0, 0.0)
+    ob = O.Problem(shape, dx, 1.0, 10.0, 0.0)
+    v = W.ic_random(shape, seed=43, amp=0.2)
+    dt = mult * min(W.dt_cfl(n, 10.0, 3) for n in shape)
+    c, g = O.shift_scale(O.spectrum_bound(ob))
+    coeffs = (0.25, 0.5, 0.75, 1.0)[-K:]
+
+    def rank_fn(r, group, s):
+        ctx = lx.Context(pb, stream=s)
+        ctx.set_comm_local(group, r, flags)
+        assert ctx.iterations_per_pass == 2
+        b, e, _ = ctx.local()
+        vl = torch.from_numpy(v[b:e]).cuda()
+        outs = [torch.full_like(vl, float("nan")) for _ in range(K)]
+        it = lx.lx_real_leja_phi_vertical(ctx, vl, outs, coeffs, dt, c, g, l, TOL, TOL)
+        it2 = lx.lx_real_leja_phi_vertical(ctx, vl, outs, coeffs, dt, c, g, l, TOL, TOL)   # reuse
+        ctx.close()
+        return it, it2, [o.cpu().numpy() for o in outs]
+
+    res = _run_ranks(P, rank_fn)
+    with lx.Context(pb) as ctx1:
+        ctx1.set_kernel(2)
+        assert ctx1.iterations_per_pass == 2
+        ones = [torch.empty(shape, dtype=torch.float64, device="cuda") for _ in range(K)]
+        it1 = lx.lx_real_leja_phi_vertical(ctx1, torch.from_numpy(v).cuda(), ones, coeffs, dt, c, g, l, TOL, TOL)
+    ref = O.real_leja_phi(ob, v, dt, c, g, l, TOL, TOL, xi300, coeffs=coeffs)
+    assert {(r[0], r[1]) for r in res} == {(ref.iters, ref.iters)} and it1 == ref.iters
+    for k in range(K):
+        full = np.concatenate([res[r][2][k] for r in range(P)], axis=0)
+        np.testing.assert_array_equal(full, ones[k].cpu().numpy())
+        assert np.linalg.norm(full - ref.outs[k]) <= TOL * np.linalg.norm(ref.outs[k])
+
+
+@pytest.mark.parametrize("P,shape,K,l", [(2, (24, 16, 64), 1, 0), (4, (37, 32, 64), 2, 1), (4, (16, 16, 128), 3, 0),
+                                         (8, (64, 16, 64), 4, 3), (3, (40, 16, 64), 1, 2)])
+def test_peer_slab_3d_kernel_bitwise(xi300, P, shape, K, l):
+    # ragged slabs (37 planes over 4 ranks), the minimum of 4 planes per rank (16 / 4: every plane is a
+    # boundary plane of one or both neighbours), K = 1..4 (rollbacks), phi_0..phi_3
+    _slab3d_vs_single(xi300, P, shape, K, l)
+
+
+def test_peer_slab_3d_one_rank_is_single_domain(xi300):
+    # one virtual rank with LX_COMM_FORCE: its ghost planes are its own periodic images
+    _slab3d_vs_single(xi300, 1, (20, 16, 64), 2, 1, flags=lx.LX_COMM_FORCE)
+
+
+def test_peer_slab_3d_epirk_step(xi300):
+    # a whole EPIRK4s3A step (config 5's integrator) with the 3D Leja calls on the peer-memory kernel and
+    # the stage kernels on the step protocol
+    P, shape = 2, (32, 16, 64)
+    dx = tuple(2.0 / n for n in shape)
+    pb = lx.Problem(shape, dx, 1.0, 10.0, 0.0)
+    ob = O.Problem(shape, dx, 1.0, 10.0, 0.0)
+    u = W.ic_random(shape, seed=17, amp=0.3)
+    dt = 5 * min(W.dt_cfl(n, 10.0, 3) for n in shape)
+    c, g = O.shift_scale(O.spectrum_bound(ob))
+
+    def rank_fn(r, group, s):
+        ctx = lx.Context(pb, stream=s)
+        ctx.set_comm_local(group, r)
+        assert ctx.iterations_per_pass == 2
+        b, e, _ = ctx.local()
+        ul = torch.from_numpy(u[b:e]).cuda()
+        lo, hi = torch.empty_like(ul), torch.empty_like(ul)
+        it, err = lx.lx_step(ctx, "epirk4s3a", ul, lo, hi, dt, c, g, TOL, TOL)
+        ctx.close()
+        return it, err, lo.cpu().numpy(), hi.cpu().numpy()
+
+    res = _run_ranks(P, rank_fn)
+    ref = O.step(ob, "epirk4s3a", u, dt, c, g, TOL, TOL, xi300)
+    assert {r[0] for r in res} == {ref.iters}
+    hi = np.concatenate([r[3] for r in res])
+    lo = np.concatenate([r[2] for r in res])
+    assert np.linalg.norm(hi - ref.u_high) <= TOL * np.linalg.norm(ref.u_high)
+    assert np.linalg.norm(lo - ref.u_low) <= TOL * np.linalg.norm(ref.u_low)

@@ -2,6 +2,7 @@
 """Summarise an `ncu --set full` capture of the Leja kernel into profiles/leja_traffic.json.
 
   python tools/ncu_traffic.py gpurun_out/leja_tb2_full.ncu-rep 16,16,14,10 4096 tb2 "capture description"
+  python tools/ncu_traffic.py gpurun_out/vert3d.ncu-rep 10:13:16 512 vert3d "..."   # 3D K=3 call, n^3 points
 
 per launch: dram read/write bytes (traffic), gpu time, the algorithmic bytes of that launch
 (bench.leja_bytes_per_point x N) and their ratio (traffic well above 1 = wasted re-reads)."""
@@ -14,7 +15,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-from bench import leja_bytes_per_point  # noqa: E402
+from bench import leja_bytes_per_point, leja_bytes_per_point_vertical_tb2  # noqa: E402
 
 MET = ("dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,launch__grid_size,"
        "launch__registers_per_thread,sm__warps_active.avg.pct_of_peak_sustained_active,"
@@ -24,8 +25,9 @@ SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "us": 1e-3, "ms"
 
 
 def main():
-    rep, iters, n, kind, desc = sys.argv[1], [int(x) for x in sys.argv[2].split(",")], int(sys.argv[3]), \
-        sys.argv[4], sys.argv[5]
+    rep, n, kind, desc = sys.argv[1], int(sys.argv[3]), sys.argv[4], sys.argv[5]
+    # per launch: an iteration count, or (vert3d) the accumulators' iteration counts joined by ':'
+    iters = [[int(y) for y in x.split(":")] for x in sys.argv[2].split(",")]
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", MET],
                          capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
@@ -36,10 +38,11 @@ def main():
         return float(r[col[name]].replace(",", "")) * SCALE.get(units[col[name]], 1.0)
 
     launches = []
-    N = n * n
-    for r, m in zip(data, iters):
+    N = n ** 3 if kind == "vert3d" else n * n
+    for r, mk in zip(data, iters):
         rd, wr = val(r, "dram__bytes_read.sum"), val(r, "dram__bytes_write.sum")
-        alg = N * leja_bytes_per_point(m, kind == "tb2")
+        m = mk if kind == "vert3d" else mk[0]
+        alg = N * (leja_bytes_per_point_vertical_tb2(mk) if kind == "vert3d" else leja_bytes_per_point(m, kind == "tb2"))
         launches.append({"iters": m, "gpu_time_ms": val(r, "gpu__time_duration.sum"), "dram_read_bytes": rd,
                          "dram_write_bytes": wr, "traffic_bytes": rd + wr, "algorithmic_bytes": alg,
                          "traffic_over_algorithmic": (rd + wr) / alg})

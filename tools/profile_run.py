@@ -3,6 +3,7 @@
 
   python tools/profile_run.py leja2d 4096 0      # phi_0 Leja call, 2D
   python tools/profile_run.py leja3d 512 0       # phi_0 Leja call, 3D
+  python tools/profile_run.py vert3d 512 1       # config 5's dominant call: vertical phi_1 {1/2, 2/3, 1} on f(u) dt
   python tools/profile_run.py ac 2048 2          # Allen-Cahn EXPRB43, 2 steps
   python tools/profile_run.py step 4096 0        # bench step (phi_0..phi_3), warm-up + 1
   python tools/profile_run.py aci 2048 2         # the same through lx_integrate
@@ -42,6 +43,20 @@ def main():
         for _ in range(reps):
             it = lx.lx_real_leja_phi(ctx, u, out, wl.dt, c, g, arg, wl.rtol, wl.atol)
         print("iters", it)
+    elif what == "vert3d":   # bench config 5's dominant kernel (the EPIRK4s3A step's K = 3 call)
+        wl = W.config(4, n=n)
+        pb = lx.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
+        ctx = lx.Context(pb)
+        u = torch.from_numpy(W.ic_gaussian_3d(n)).cuda()
+        c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+        fdt = torch.empty_like(u)
+        lx.lx_rhs(ctx, u, fdt, wl.dt)
+        coeffs = (0.5, 2.0 / 3.0, 1.0)
+        outs = [torch.empty_like(u) for _ in coeffs]
+        m_k = [lx.lx_real_leja_phi(ctx, fdt, outs[0], wl.dt * a, c, g, arg, wl.rtol, wl.atol) for a in coeffs]
+        for _ in range(reps):
+            it = lx.lx_real_leja_phi_vertical(ctx, fdt, outs, coeffs, wl.dt, c, g, arg, wl.rtol, wl.atol)
+        print("iters", it, "accumulators", ":".join(str(m) for m in m_k))
     elif what == "ac":
         wl = W.config(2, n=n)
         pb = lx.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)

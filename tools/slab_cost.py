@@ -6,7 +6,9 @@
   each rank's grid capped to 1/P of the GPU -- the same bytes as "single" on the same GPU, so the ratio
   t_peer / t_single isolates the slab protocol's overhead (ghost-row stores, cross-rank barrier);
 * step P: the same with LX_COMM_NO_PEER (step kernel + D2D halo copies + host barriers per iteration).
-Grid: n0 x n1 = (rows per rank x P) x n1, phi_0 of the Problem-I Gaussian at 10 x CFL.  Prints JSON lines.
+Grid: n0 x n1 = (rows per rank x P) x n1, phi_0 of the Problem-I Gaussian at 10 x CFL; with a third argument
+n2, the 3D grid (planes per rank x P) x n1 x n2 (random input, 5 x CFL; the 3D two-step kernel and its
+peer-memory slab instantiation).  Prints JSON lines.
 """
 import json
 import os
@@ -23,8 +25,8 @@ import workloads as W  # noqa: E402
 
 def run(shape, P, flags, reps=5):
     pb = lx.Problem(shape, tuple(2.0 / s for s in shape), 1.0, 10.0, 0.0)
-    u0 = W.ic_problem1_2d(*shape) if shape[0] == shape[1] else W.ic_random(shape, seed=3, amp=0.2)
-    dt = 10 * W.dt_cfl(max(shape), 10.0)
+    u0 = W.ic_problem1_2d(*shape) if len(shape) == 2 and shape[0] == shape[1] else W.ic_random(shape, seed=3, amp=0.2)
+    dt = (10 if len(shape) == 2 else 5) * W.dt_cfl(max(shape), 10.0, len(shape))
     c, g = lx.lx_shift_scale(sum(4.0 / (h * h) + 40.0 / (3.0 * h) for h in (2.0 / s for s in shape)))   # R9
     out = [None] * P
     errs = []
@@ -72,8 +74,9 @@ def run(shape, P, flags, reps=5):
 def main():
     rows = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
     n1 = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
-    for P in (1, 2, 4):
-        shape = (rows * max(P, 1), n1)
+    rest = (int(sys.argv[3]),) if len(sys.argv) > 3 else ()
+    for P in ((1, 2, 4, 8) if rest else (1, 2, 4)):
+        shape = (rows * max(P, 1), n1) + rest
         base = run(shape, 0, 0)
         print(json.dumps(dict(base, mode="single")), flush=True)
         for mode, flags in (("peer", lx.LX_COMM_FORCE), ("step", lx.LX_COMM_FORCE | lx.LX_COMM_NO_PEER)):
