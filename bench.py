@@ -236,13 +236,15 @@ def leja_bytes_per_point_vertical(m_k):
     return b
 
 
-def leja_bytes_per_point_vertical_tb2(m_k):
+def leja_bytes_per_point_vertical_tb2(m_k, predicted=False):
     """3D two-step kernel (k_leja3d_tb2, two iterations per plane sweep) with K accumulators frozen at m_k.
     Pass q performs iterations 2q+1, 2q+2.  Pass 0 reads v and writes y and every accumulator (16 + 8K B);
     pass q >= 1 reads and writes y (16 B) and every accumulator still active at 2q+1 (16 B each), plus, in
     place, every accumulator that converged on the first iteration of pass q-1 (rollback: read p, write p;
     its operand y_{2q-1} is the pass's own input).  An accumulator that converged on the first iteration of
-    the LAST pass is rolled back by the end-of-call fix-up (read y; read, write p)."""
+    the LAST pass is rolled back by the end-of-call fix-up (read y; read, write p) -- unless the final
+    iteration was predicted (a repeated call): then the last pass performs that one iteration
+    only and nothing is rolled back at the end (same bytes for the pass itself)."""
     M = max(m_k)
     Q = (M + 1) // 2
     b = 16 + 8 * len(m_k)
@@ -250,7 +252,7 @@ def leja_bytes_per_point_vertical_tb2(m_k):
         m = 2 * q + 1
         b += 16 + 16 * sum(1 for mk in m_k if mk >= m or mk == m - 2)
     rb = sum(1 for mk in m_k if mk == 2 * Q - 1)
-    if rb:
+    if rb and not (predicted and M % 2 == 1):
         b += 8 + 16 * rb
     return b
 
@@ -532,7 +534,7 @@ def bench_epirk_3d(job, args, wl):
     ctx.synchronize()
     kms = float(np.mean([ea.elapsed_time(eb) for ea, eb in evs]))
     tb3 = ctx.iterations_per_pass == 2
-    kbytes = N * (leja_bytes_per_point_vertical_tb2(m_k) if tb3 else leja_bytes_per_point_vertical(m_k))
+    kbytes = N * (leja_bytes_per_point_vertical_tb2(m_k, predicted=True) if tb3 else leja_bytes_per_point_vertical(m_k))
     if ws > 1 and tb3:
         kname = ("k_leja3d_tb2<3,true> (peer-memory slab kernel: two Leja iterations per plane sweep, ghost "
                  "planes stored into the neighbours' exchange blocks, 1 launch per call; rank 0)")

@@ -339,7 +339,9 @@ static LejaParams base_params(lx_ctx* ctx, const lx_problem* pb) {
 // Core Leja call on device pointers (no staging, no sync).
 // Work decomposition of the two-step kernel (single domain and slab): items = (60-column band,
 // RT-row chunk); 32-row segments handed out dynamically, band fastest; per-segment / per-group partials.
-static lx_status tb2_buffers(lx_ctx* ctx, int nseg, int K) {
+// Control block of the two-step kernels (2D: pipelined-pass state + prediction table; 3D: the table of
+// final iterations of recent calls).
+static lx_status tb2_ctl_alloc(lx_ctx* ctx) {
     if (!ctx->tb2_ctl) {
         CUDA_TRY(cudaMalloc(&ctx->tb2_ctl, sizeof(Tb2Ctl)));
         Tb2Ctl init;
@@ -347,6 +349,11 @@ static lx_status tb2_buffers(lx_ctx* ctx, int nseg, int K) {
         init.pbase = 1u;   // tags >= 1: the zeroed counters, flags and decision words never match
         CUDA_TRY(cudaMemcpy(ctx->tb2_ctl, &init, sizeof init, cudaMemcpyHostToDevice));
     }
+    return LX_OK;
+}
+
+static lx_status tb2_buffers(lx_ctx* ctx, int nseg, int K) {
+    LX_TRY(tb2_ctl_alloc(ctx));
     if (nseg > ctx->tb2_cap) {
         cudaFree(ctx->tb2_seg_part);
         cudaFree(ctx->tb2_grp_part);
@@ -464,6 +471,8 @@ static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u,
         if (P.ndim == 3 && !diag && comm_peer_ready(ctx->comm) && tb3_shape(ctx)) {
             // 3D: the two-step plane-sweep kernel over peer memory (ghost planes, global barrier per pass)
             LX_TRY(leja3d_table(ctx, P, K, l, coeffs, dt, c, gamma, rec));
+            LX_TRY(tb2_ctl_alloc(ctx));
+            P.tc = ctx->tb2_ctl;
             P.grid = comm_grid_cap(ctx->comm, leja3d_tb2_grid_size(ctx->device, K, leja3d_smem_units(P.n_loc, P.n1, P.n2), true));
             comm_peer_params(ctx->comm, P, diag);
             CUDA_TRY(launch_leja3d_tb2(P, ctx->stream, true));
@@ -484,6 +493,8 @@ static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u,
         const int ncu = leja3d_smem_units(P.n_loc, P.n1, P.n2);
         if (!diag && ctx_tblock(ctx) == 2) {
             // two Leja iterations per HBM pass (2.5D temporal blocking)
+            LX_TRY(tb2_ctl_alloc(ctx));
+            P.tc = ctx->tb2_ctl;
             P.grid = leja3d_tb2_grid_size(ctx->device, K, ncu);
             CUDA_TRY(launch_leja3d_tb2(P, ctx->stream));
             ctx->launches++;
@@ -768,6 +779,7 @@ static lx_status attach_comm(lx_ctx* ctx, Comm* c, int rank, int nranks) {
 // in between may wait for the device to idle (virtual ranks share one context) -> deadlock until the
 // watchdog.  Scratch vectors, and the two-step segment buffers for the largest segment count (RT = 2).
 static lx_status prealloc_slab(lx_ctx* ctx) {
+    LX_TRY(tb2_ctl_alloc(ctx));
     for (int i = 0; i < kStage; i++)
         if (!scratch(ctx, i)) return fail(LX_ERR_CUDA, "scratch allocation failed");
     const int nb = ((int)ctx->n[1] + kBand2 - 1) / kBand2, nrb = (ctx->n_loc + 1) / 2, seg = 16;

@@ -469,6 +469,7 @@ __device__ __forceinline__ void b3_stage_b(const LejaParams& P, const B3Coef<K>&
         yn.x = fma(alpha, ax.x, bb * yc.x);
         yn.y = fma(alpha, ax.y, bb * yc.y);
         const long long off = off0 + r * rstride;
+        if (!two) yn = yc;   // one-iteration pass: y_m is the next pass's input
         st2(dst + off, yn);
         if (SLAB) {   // a boundary plane of y_{m+1}: also into the neighbour's ghost block (peer memory)
             if (x1) st2(x1 + off, yn);
@@ -732,7 +733,7 @@ __device__ __forceinline__ void b3_block_reduce(double (&v)[N], double (*s_red)[
 template <int K, bool SLAB>
 __device__ __forceinline__ void b3_barrier_decide(const LejaParams& P, int q, int m, bool two, unsigned gen0,
                                                   const B3Coef<K>& C, int active, double (*s_red)[kSlot], int* s_flags,
-                                                  bool peer) {
+                                                  bool peer, unsigned long long key, int pslot) {
     constexpr int NV = 2 * (1 + K);
     const int tid = threadIdx.x;
     Ctrl* ctrl = P.ctrl;
@@ -764,9 +765,17 @@ __device__ __forceinline__ void b3_barrier_decide(const LejaParams& P, int q, in
             }
             if (!done) leja_decide<K>(P, m, acc, C.da, act, done, status, rec);
             const int rb = (two && status != 6 && status != 10) ? (active & ~act) : 0;
+            int fm = m;
             if (!done) {
+                // a one-iteration pass (predicted final iteration) that did not end the call simply continues
                 if (two) leja_decide<K>(P, m + 1, acc + 1 + K, C.db, act, done, status, rec);
-                else { done = 1; status = 5; }   // unreachable: m < M - 1 implies two
+                fm = m + 1;
+            }
+            if (done && status != 10) {   // remember the final iteration for the next call with these parameters
+                Tb2Ctl* tc = P.tc;
+                const int slot = pslot >= 0 ? pslot : (int)(tc->pnext++ % (unsigned)kTb2Pred);
+                tc->pkey[slot] = key;
+                tc->pfin[slot] = (unsigned)fm;
             }
             ctrl->arrive = 0u;
             const unsigned long long w = ((unsigned long long)(gen0 + (unsigned)q + 1u) << 32) |
@@ -861,11 +870,29 @@ __global__ void __launch_bounds__(kB3Threads, 1) k_leja3d_tb2(const __grid_const
     __syncthreads();
     unsigned gen0 = 0;
     if (tid == 0) gen0 = (unsigned)(ld_acquire64(&P.ctrl->word) >> 32);
+    // final iteration of the last call with the same parameters (Tb2Ctl prediction table): a pass whose
+    // FIRST iteration is predicted to end the call performs only that iteration (stage B then stores y_m,
+    // not y_{m+1}), so a correct prediction needs no rollback; a wrong one continues at m + 1 next pass
+    unsigned long long key = 0;
+    __shared__ int s_pred[2];
+    if (tid == 0) {
+        key = tb2_call_key<K>(P);
+        int fp = -1, ps = -1;
+        for (int i = 0; i < kTb2Pred; i++)
+            if (P.tc->pkey[i] == key) {
+                fp = (int)P.tc->pfin[i];
+                ps = i;
+            }
+        s_pred[0] = fp;
+        s_pred[1] = ps;
+    }
     if (SLAB) {
-        b3_slab_prologue(P, gen0, s_flags);
+        b3_slab_prologue(P, gen0, s_flags);   // (syncs the block: s_pred visible)
         if (s_flags[1]) return;   // a peer never arrived (LX_ERR_TIMEOUT recorded)
         gen0 += 1u;
     }
+    __syncthreads();
+    const int fpred = s_pred[0], pslot = s_pred[1];
     int active = P.active0, rbm = 0;
     const int M = P.max_nodes;
     const int ncu = (P.n1 / kB3J) * (P.n2 >> 6) * ((P.n_loc + kTI3 - 1) / kTI3);
@@ -878,9 +905,9 @@ __global__ void __launch_bounds__(kB3Threads, 1) k_leja3d_tb2(const __grid_const
             C.dr[k] = 0.0;
         }
     }
+    int m = 1;   // first iteration of pass q
     for (int q = 0;; q++) {
-        const int m = 2 * q + 1;
-        const bool two = m + 1 < M;
+        const bool two = m + 1 < M && m != fpred;
         if (tid == 0) {
             C.ba = coef_beta(P, m);
             C.bb = two ? coef_beta(P, m + 1) : 0.0;
@@ -916,7 +943,7 @@ __global__ void __launch_bounds__(kB3Threads, 1) k_leja3d_tb2(const __grid_const
 #pragma unroll
             for (int i = 0; i < 2 * (1 + K); i++) slot[i] = sums[i];
         }
-        b3_barrier_decide<K, SLAB>(P, q, m, two, gen0, C, active, s_red, s_flags, peer);
+        b3_barrier_decide<K, SLAB>(P, q, m, two, gen0, C, active, s_red, s_flags, peer, key, pslot);
         active = s_flags[2];
         rbm = s_flags[3];
         if (s_flags[1]) {
@@ -938,6 +965,7 @@ __global__ void __launch_bounds__(kB3Threads, 1) k_leja3d_tb2(const __grid_const
             }
             break;
         }
+        m += two ? 2 : 1;
     }
 }
 

@@ -411,27 +411,6 @@ __device__ __forceinline__ void coef_first5(const LejaParams& P, int k, double* 
 }
 
 
-// Key of a Leja call's parameters (node count, phi index, dt, shift / scale, vertical coefficients,
-// tolerances) for the ping-pong parity prediction.
-template <int K>
-__device__ __forceinline__ unsigned long long tb2_call_key(const LejaParams& P) {
-    unsigned long long h = 1469598103934665603ull;
-    auto mix = [&h](unsigned long long x) {
-        h ^= x;
-        h *= 1099511628211ull;
-    };
-    mix((unsigned long long)P.l | ((unsigned long long)K << 8) | ((unsigned long long)P.max_nodes << 16) |
-        ((unsigned long long)P.active0 << 40));
-    mix((unsigned long long)__double_as_longlong(P.cdt));
-    mix((unsigned long long)__double_as_longlong(P_c(P)));
-    mix((unsigned long long)__double_as_longlong(P_g(P)));
-    mix((unsigned long long)__double_as_longlong(P.rtol));
-    mix((unsigned long long)__double_as_longlong(P.atol));
-#pragma unroll
-    for (int k = 0; k < K; k++) mix((unsigned long long)__double_as_longlong(P.ak[k]));
-    return h | 1ull;
-}
-
 // Two Leja iterations per HBM pass, passes pipelined (see the header comment).  SLAB = the
 // slab-decomposed variant: one persistent kernel per Leja call and rank; halo rows and
 // norm partials travel through peer memory from inside the kernel; no host round trip, no NCCL call and

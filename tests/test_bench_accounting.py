@@ -90,3 +90,15 @@ def test_vertical_tb2_bytes_match_pass_model(m_k):
 @pytest.mark.parametrize("m", list(range(1, 30)))
 def test_vertical_tb2_single_accumulator_is_two_step(m):
     assert bench.leja_bytes_per_point_vertical_tb2([m]) == bench.leja_bytes_per_point(m, True)
+
+
+@pytest.mark.parametrize("m_k", [(1,), (5,), (3, 5, 7), (13, 14, 16), (9, 11, 11)])
+def test_vertical_tb2_predicted_final_iteration(m_k):
+    # a predicted odd final iteration M: the last pass performs only iteration M, no end-of-call rollback
+    full = bench.leja_bytes_per_point_vertical_tb2(list(m_k))
+    pred = bench.leja_bytes_per_point_vertical_tb2(list(m_k), predicted=True)
+    M = max(m_k)
+    if M % 2:
+        assert full - pred == 8 + 16 * sum(1 for mk in m_k if mk == M)
+    else:
+        assert pred == full

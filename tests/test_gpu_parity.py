@@ -573,6 +573,43 @@ def test_3d_tblock2_vs_one_pass(xi300, shape, K, l):
         assert np.linalg.norm(a - ref) <= TOL * np.linalg.norm(ref)
 
 
+@pytest.mark.parametrize("K", [1, 2])
+def test_3d_tblock2_predicted_final_iteration(xi300, K):
+    # repeated calls with the same parameters: the 3D two-step kernel predicts the final iteration from the
+    # previous call (Tb2Ctl table) and, when it is the FIRST iteration of a pass, performs that iteration
+    # alone (no rollback).  Sequence: zero input twice (m = 1: rollback, then predicted), a nonzero input
+    # with the stale prediction m = 1 (wrong: the call continues at m = 2 in the next pass), the same input
+    # again (right prediction).  Every call against the oracle (iterations, 1e-10) and the one-pass kernel.
+    shape = (40, 16, 64)
+    pb, ob = _pair(shape)
+    v = W.ic_random(shape, seed=77, amp=0.2)
+    dt = 5 * min(W.dt_cfl(n, 10.0, 3) for n in shape)
+    coeffs = (0.5, 1.0)[-K:]
+    zero = np.zeros(shape)
+    seq = [zero, zero, v, v, zero, v]
+    res = {}
+    for tb in (1, 2):
+        with lx.Context(pb) as ctx:
+            ctx.set_kernel(tb)
+            c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+            res[tb] = []
+            for x in seq:
+                outs = [torch.full(shape, float("nan"), dtype=torch.float64, device="cuda") for _ in range(K)]
+                it = lx.lx_real_leja_phi_vertical(ctx, _dev(x), outs, coeffs, dt, c, g, 1, TOL, TOL)
+                res[tb].append((it, [o.cpu().numpy() for o in outs]))
+    refs = {id(x): O.real_leja_phi(ob, x, dt, c, g, 1, TOL, TOL, xi300, coeffs=coeffs) for x in (zero, v)}
+    assert refs[id(zero)].iters == 1
+    for x, (it2, o2), (it1, o1) in zip(seq, res[2], res[1]):
+        r = refs[id(x)]
+        assert it2 == it1 == r.iters
+        for a, b, ref in zip(o2, o1, r.outs):
+            if x is zero:
+                assert not a.any() and not ref.any()
+                continue
+            np.testing.assert_allclose(a, b, rtol=0, atol=8 * np.finfo(float).eps * np.abs(b).max())
+            assert np.linalg.norm(a - ref) <= TOL * np.linalg.norm(ref)
+
+
 def test_3d_tblock2_auto_and_limits(xi300):
     # auto policy: two-step from 2^20 points on (n1 % 16 == 0, n2 % 64 == 0), one pass below / for other
     # shapes; the NOCONV limit (R28) and a NONFINITE run end with the same status and m as the oracle

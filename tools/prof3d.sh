@@ -7,7 +7,7 @@ mkdir -p gpurun_out
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     -c 300 --csv --log-file gpurun_out/launches_c5.csv \
     python bench.py --config 5 --steps 1 --warmup 3 --no-cpu > gpurun_out/c5_ncu.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_leja3d_tb2 -s 1 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"tb2<.int.3" -s 1 -c 1 \
     -o gpurun_out/vert3d_full python tools/profile_run.py vert3d 512 1 > gpurun_out/ncu_vert3d.log 2>&1
 ACC=$(grep -o "accumulators [0-9:]*" gpurun_out/ncu_vert3d.log | awk '{print $2}')
 python tools/ncu_traffic.py gpurun_out/vert3d_full.ncu-rep "$ACC" 512 vert3d \
