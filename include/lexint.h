@@ -158,8 +158,12 @@ lx_status lx_ctx_destroy(lx_ctx *ctx);
  * every rank's exchange header (summed in rank order: identical decisions on
  * every rank).  No NCCL call, no launch and no host round trip per iteration;
  * a peer that does not arrive within 60 s ends the call with LX_ERR_TIMEOUT.
- * Other operations (3D, Burgers, power iteration, stage kernels) use one step
- * kernel + one NCCL group (1+2 halo rows, allgather of partials) per iteration.
+ * Leja calls on 3D grids with n1 % 16 == 0, n2 % 64 == 0 and >= 4 planes per
+ * rank (constant-coefficient operators) do the same with ghost PLANES (the 3D
+ * two-step kernel: two iterations per plane sweep, one global barrier per pass).
+ * Other operations (3D Allen-Cahn, Burgers, power iteration, stage kernels) use
+ * one step kernel + one NCCL group (1+2 halo rows, allgather of partials) per
+ * iteration.
  * flags: LX_COMM_FORCE  -- build the communicator even for nranks == 1 (the slab
  *                          protocol with itself; by default one rank = the
  *                          single-domain context);
@@ -207,10 +211,11 @@ lx_status lx_ctx_synchronize(lx_ctx *ctx, int *iters_total, double *err_last);
 /* Number of kernel launches this context has issued (for bench accounting). */
 int64_t lx_ctx_launch_count(const lx_ctx *ctx);
 /* Leja iterations per HBM pass of this context's Leja calls on its constant-coefficient / Allen-Cahn
- * problems: 2 = the temporally blocked 2D kernel (single domain with >= 3*2^20
- * local points or lx_ctx_set_kernel(ctx, 2, .), and the peer-memory slab kernel), 1 = one pass per
- * iteration.  Burgers (flux) problems always run one pass per iteration.  Determines the algorithmic
- * bytes of a call.  0 for a NULL context. */
+ * problems: 2 = the temporally blocked kernels (2D single domain with >= 3*2^20
+ * local points, 3D (n1 % 16 == 0, n2 % 64 == 0) with >= 2^20, or lx_ctx_set_kernel(ctx, 2, .), and
+ * the peer-memory slab kernels), 1 = one pass per iteration.  Burgers (flux) problems, and Allen-Cahn
+ * problems in 3D, always run one pass per iteration.  Determines the algorithmic bytes of a call
+ * (DESIGN.md §5).  0 for a NULL context. */
 int lx_ctx_iterations_per_pass(const lx_ctx *ctx);
 /* Kernel choice of this context (default 0 = automatic):
  * iterations_per_pass -- 2D single-domain Leja calls: 1 = one Leja iteration per HBM pass
