@@ -658,8 +658,8 @@ int oc_step_ex(const oc_problem *pb, int jac_mode, int method, const double *u, 
     double *f_u = (double *)malloc(bytes);
     double *t1 = (double *)malloc(bytes), *t2 = (double *)malloc(bytes), *t3 = (double *)malloc(bytes);
     double *t4 = (double *)malloc(bytes), *t5 = (double *)malloc(bytes), *t6 = (double *)malloc(bytes);
-    double *t7 = (double *)malloc(bytes);
-    if (!f_u || !t1 || !t2 || !t3 || !t4 || !t5 || !t6 || !t7) { s = OC_ERR_ARG; goto out; }
+    double *t7 = (double *)malloc(bytes), *t8 = (double *)malloc(bytes);
+    if (!f_u || !t1 || !t2 || !t3 || !t4 || !t5 || !t6 || !t7 || !t8) { s = OC_ERR_ARG; goto out; }
 
     /* f_u = RHS(u) * dt  (alg:Ros_Eu P:468-469) */
     oc_rhs(pb, u, f_u);
@@ -725,7 +725,8 @@ int oc_step_ex(const oc_problem *pb, int jac_mode, int method, const double *u, 
          *   Y1 = u + a11 h phi_1(g11 hJ) f
          *   Y2 = u + a21 h phi_1(g21 hJ) f + a22 phi_1(g22 hJ) R(Y1)
          *   u+ = u + b1 h phi_1(g31 hJ) f + b2 phi_1(g32 hJ) R(Y1) + b3 phi_3(g33 hJ) (R(Y2) - 2 R(Y1))
-         * non-embedded here (u_low = u_high, err = 0). */
+         * embedded fourth-order solution (reading R33): the same with g32 -> 1/2, g33 -> 1,
+         *   u4 = u + b1 h phi_1(hJ) f + b2 phi_1(hJ/2) R(Y1) + b3 phi_3(hJ) (R(Y2) - 2 R(Y1)). */
         const double a11 = 0.35129592695058193092, a21 = 0.84405472011657126298, a22 = 1.6905891609568963624;
         const double b1 = 1.0, b2 = 1.2727127317356892397, b3 = 2.2714599265422622275;
         const double g11 = 0.35129592695058193092, g21 = 0.84405472011657126298, g22 = 1.0;
@@ -740,9 +741,9 @@ int oc_step_ex(const oc_problem *pb, int jac_mode, int method, const double *u, 
         axpby(1.0, u, a11, t1, t5, N);                       /* Y1 */
         remainder_mode(pb, jac_mode, u, fu_raw, t5, t6);     /* NL_Y1 */
         axpby(dt, t6, -dt, t4, t5, N);                       /* R1 = h (F(Y1) - F(u)) */
-        double cf2[2] = {g32, g22};                          /* vertical phi_1 on R1 */
-        double *qv[2] = {t6, t7};
-        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, t5, qv, cf2, 2, dt, c, gamma, 1, rtol, atol, xi,
+        double cf2[3] = {0.5, g32, g22};                     /* vertical phi_1 on R1 (1/2: embedded) */
+        double *qv[3] = {t8, t6, t7};
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, t5, qv, cf2, 3, dt, c, gamma, 1, rtol, atol, xi,
                                 max_nodes, &it, NULL);
         total += it;
         if (s) goto out;
@@ -750,14 +751,17 @@ int oc_step_ex(const oc_problem *pb, int jac_mode, int method, const double *u, 
         remainder_mode(pb, jac_mode, u, fu_raw, t1, t2);     /* NL_Y2 */
         axpby(dt, t2, -dt, t4, t7, N);                       /* R2 */
         axpby(1.0, t7, -2.0, t5, t2, N);                     /* R2 - 2 R1 */
-        double one33 = g33;
-        double *o3[1] = {t7};
-        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, t2, o3, &one33, 1, dt, c, gamma, 3, rtol, atol, xi,
+        double cf33[2] = {g33, 1.0};                         /* vertical phi_3 (1: embedded) */
+        double *o3[2] = {t7, t1};
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, t2, o3, cf33, 2, dt, c, gamma, 3, rtol, atol, xi,
                                 max_nodes, &it, NULL);
         total += it;
         if (s) goto out;
         for (long i = 0; i < N; i++) u_high[i] = u[i] + b1 * t3[i] + b2 * t6[i] + b3 * t7[i];
-        if (u_low) for (long i = 0; i < N; i++) u_low[i] = u_high[i];
+        for (long i = 0; i < N; i++) t2[i] = u[i] + b1 * t3[i] + b2 * t8[i] + b3 * t1[i];   /* u4 */
+        if (u_low) for (long i = 0; i < N; i++) u_low[i] = t2[i];
+        for (long i = 0; i < N; i++) t1[i] = u_high[i] - t2[i];
+        if (err) *err = oc_l2norm_scaled(t1, N);                            /* P:252, R20 */
     } else if (method == 6) {
         /* EXPRB53s3 (Luan & Ostermann 2014, cited at P:83; reading R27), D_x = h (F(x) - F(u)):
          *   U2 = u + c2 h phi_1(c2 hJ) f                                  c2 = 1/2
@@ -930,7 +934,7 @@ int oc_step_ex(const oc_problem *pb, int jac_mode, int method, const double *u, 
     }
 out:
     if (iters) *iters = total;
-    free(f_u); free(t1); free(t2); free(t3); free(t4); free(t5); free(t6); free(t7);
+    free(f_u); free(t1); free(t2); free(t3); free(t4); free(t5); free(t6); free(t7); free(t8);
     free(fu_raw);
     return s;
 }
@@ -962,6 +966,7 @@ static int oc_embedded_order(int method)
     case 2: return 3;   /* EXPRB43: u_3 */
     case 3: return 3;   /* EPIRK4s3A: u_3 */
     case 6: return 3;   /* EXPRB53s3: u_3 */
+    case 5: return 4;   /* EPIRK5P1: u_4 (R33) */
     case 7: return 4;   /* EXPRB54s4: u_4 */
     default: return 0;  /* non-embedded */
     }

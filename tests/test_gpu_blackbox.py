@@ -135,7 +135,7 @@ def test_fd_steps_allen_cahn(xi300, method):
     assert r.status == O.OK
     assert it == r.iters
     assert _rel(hi, r.u_high) <= STEP_TOL_AC
-    if method not in ("rosenbrock_euler", "exprb42", "epirk5p1"):
+    if method not in ("rosenbrock_euler", "exprb42"):
         assert _rel(lo, r.u_low) <= STEP_TOL_AC
         assert err == pytest.approx(r.err, rel=1e-3, abs=1e-12)
 

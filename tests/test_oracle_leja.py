@@ -169,7 +169,7 @@ def test_integrator_linear_exactness(xi300, method):
     sym = refs.impulse_symbol(lambda x: O.jac_apply(pb, None, x), (n, n))
     ex = refs.fft_apply_phi(sym, u0, dt, 0)
     assert np.linalg.norm(r.u_high - ex) <= 1e-11 * np.linalg.norm(ex)
-    if method not in ("rosenbrock_euler", "exprb42", "epirk5p1"):
+    if method not in ("rosenbrock_euler", "exprb42"):
         assert r.err == 0.0       # R18: F == 0 exactly for linear f
 
 
@@ -291,7 +291,7 @@ def test_epirk5p1_fifth_order(xi300):
         for _ in range(nsteps):
             c, g = _cg(pb, u)
             r = O.step(pb, "epirk5p1", u, h, c, g, 1e-14, 1e-14, xi300)
-            assert r.status == O.OK and r.err == 0.0
+            assert r.status == O.OK and r.err > 0.0   # embedded fourth-order estimate (R33)
             u = r.u_high
         errs.append(np.linalg.norm(u - uref) / np.linalg.norm(uref))
     orders = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
@@ -341,7 +341,7 @@ def test_exprb53s3_orders(xi300):
 
 
 # ---------------------------------------------------------------- round-2 pins (VERDICT r1 "What's weak" #1)
-@pytest.mark.parametrize("method,order", [("exprb32", 2), ("exprb43", 3), ("epirk4s3a", 3)])
+@pytest.mark.parametrize("method,order", [("exprb32", 2), ("exprb43", 3), ("epirk4s3a", 3), ("epirk5p1", 4)])
 def test_embedded_solution_order(xi300, method, order):
     # The embedded (lower-order) solutions u_low that the error estimate ||u_high - u_low|| (P:252,
     # reading R20) compares against: EXPRB32 -> a (order 2), EXPRB43 / EPIRK4s3A -> u_3
@@ -535,7 +535,8 @@ def test_adaptive_linear_problem_grows_steps(xi300):
     assert np.linalg.norm(res.u - ex) <= 1e-9 * np.linalg.norm(ex)
 
 
-@pytest.mark.parametrize("method,q", [("exprb32", 2), ("exprb43", 3), ("epirk4s3a", 3), ("exprb54s4", 4)])
+@pytest.mark.parametrize("method,q", [("exprb32", 2), ("exprb43", 3), ("epirk4s3a", 3), ("exprb54s4", 4),
+                                      ("epirk5p1", 4)])
 def test_adaptive_controller_allen_cahn(xi300, method, q):
     # Allen-Cahn: the accept / reject decisions and the step sequence follow R32 exactly (replayed from the
     # logs), a too-large first step is rejected, and the global error at t_end shrinks with the tolerance
@@ -553,3 +554,25 @@ def test_adaptive_controller_allen_cahn(xi300, method, q):
         errs.append(np.linalg.norm(res.u - uref) / np.linalg.norm(uref))
     assert errs[0] > errs[1] > errs[2], errs
     assert errs[1] < 1e-5, errs
+
+
+def test_epirk5p1_embedded_is_fourth_order_and_estimates_the_local_error(xi300):
+    # EPIRK5P1's embedded solution (reading R33: g32 -> 1/2, g33 -> 1): its local error is O(h^5) (global
+    # order 4, test_embedded_solution_order), so the estimate err = ||u5 - u4|| / sqrt(N) falls
+    # like h^5 and tracks the true local error of u4 within a small factor.  Any other (g32, g33) near
+    # these values gives local order 4 (checked while reconstructing the tableau; DESIGN R33).
+    n = 16
+    pb = O.Problem((n, n), (2 / n, 2 / n), 2e-3, 0.0, 1.0)
+    u0 = W.ic_allen_cahn_2d(n)
+    ests, trues = [], []
+    for h in (0.0625, 0.03125, 0.015625):
+        c, g = _cg(pb, u0)
+        r = O.step(pb, "epirk5p1", u0, h, c, g, 1e-14, 1e-14, xi300)
+        assert r.status == O.OK
+        ex = _allen_cahn_reference(pb, u0, h)
+        ests.append(r.err)
+        trues.append(np.linalg.norm(r.u_low - ex) / np.sqrt(ex.size))
+    orders = np.log2(np.array(ests[:-1]) / np.array(ests[1:]))
+    assert abs(orders[-1] - 5.0) < 0.3 and np.all(orders > 4.4), (ests, orders)
+    ratio = np.array(ests) / np.array(trues)
+    assert np.all((ratio > 0.5) & (ratio < 2.0)), ratio

@@ -56,8 +56,11 @@ def cfg0(stream):
             "sync_us_per_step": host_us, "note": "L1/L2 resident, launch/latency bound: no roofline claim"}
 
 
-def cfg_leja(stream, n, ls, name, reps=3):
+def cfg_leja(stream, n, ls, name, reps=3, mult=10.0):
+    """phi_l Leja calls on the n^2 Problem-I Gaussian at mult x dt_CFL (config 1: mult = 10; the dt sweep
+    1 / 10 / 100 x CFL of SURVEY 8(d))."""
     wl = W.config(1, n=n)
+    dt = wl.dt * mult / 10.0
     pb = lx.Problem(wl.shape, wl.dx, wl.diff, wl.nu, wl.react)
     ctx = lx.Context(pb, stream=stream)
     u = torch.from_numpy(W.ic_problem1_2d(n)).cuda()
@@ -65,8 +68,8 @@ def cfg_leja(stream, n, ls, name, reps=3):
     c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
     res = []
     for l in ls:
-        it = lx.lx_real_leja_phi(ctx, u, out, wl.dt, c, g, l, wl.rtol, wl.atol)
-        ms, _ = timed(stream, lambda: lx.lx_real_leja_phi(ctx, u, out, wl.dt, c, g, l, wl.rtol, wl.atol,
+        it = lx.lx_real_leja_phi(ctx, u, out, dt, c, g, l, wl.rtol, wl.atol)
+        ms, _ = timed(stream, lambda: lx.lx_real_leja_phi(ctx, u, out, dt, c, g, l, wl.rtol, wl.atol,
                                                            sync=False), reps)
         ctx.synchronize()
         tb2 = ctx.iterations_per_pass == 2
@@ -75,7 +78,7 @@ def cfg_leja(stream, n, ls, name, reps=3):
         res.append({"l": l, "iters": it, "ms": ms, "GBps": byt / ms / 1e6, "frac": byt / ms / 1e6 / PEAK,
                     "one_pass_equiv_frac": byt1 / ms / 1e6 / PEAK})
     ctx.close()
-    return {"config": name, "grid": [n, n], "calls": res,
+    return {"config": name, "grid": [n, n], "dt_cfl_mult": mult, "calls": res,
             "leja_it_per_s": sum(r["iters"] for r in res) / sum(r["ms"] for r in res) * 1e3}
 
 
@@ -254,7 +257,7 @@ def cfg_catalogue(stream, n=2048, steps=20):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="0,1,2,3,4,5,6,7")
+    ap.add_argument("--only", default="0,1,2,3,4,5,6,7,8")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     s = torch.cuda.Stream()
@@ -276,6 +279,9 @@ def main():
         print(json.dumps(cfg_blackbox(s)), flush=True)
     if 7 in want:
         print(json.dumps(cfg_catalogue(s)), flush=True)
+    if 8 in want:   # config-1 dt sweep (1 and 100 x CFL; 10 x CFL is row 1)
+        for mult in (1.0, 100.0):
+            print(json.dumps(cfg_leja(s, 4096, (0, 1, 2, 3), "1 (dt sweep)", mult=mult)), flush=True)
 
 
 if __name__ == "__main__":
