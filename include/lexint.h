@@ -287,7 +287,7 @@ typedef enum {
     LX_EXPRB43 = 2,
     LX_EPIRK4S3A = 3,
     LX_EXPRB42 = 4,       /* Luan 2017 (cited at P:83), 4th order, non-embedded (err = 0) */
-    LX_EPIRK5P1 = 5,      /* Tokman et al. 2012 (cited at P:83, Table 2), 5th order, non-embedded (R26) */
+    LX_EPIRK5P1 = 5,      /* Tokman et al. 2012 (cited at P:83, Table 2), 5th order, embedded 4th (R26, R33) */
     LX_EXPRB53S3 = 6,     /* Luan & Ostermann 2014 (cited at P:83), 5th order, embedded 3rd (R27)      */
     LX_EXPRB54S4 = 7      /* Luan & Ostermann 2014 (cited at P:83), 5th order, embedded 4th (R31)      */
 } lx_method;
@@ -309,7 +309,9 @@ lx_status lx_step_epirk4s3a(lx_ctx *ctx, const lx_problem *pb, const double *u, 
 lx_status lx_step_exprb42(lx_ctx *ctx, const lx_problem *pb, const double *u, double *u_out, double dt,
                           double c, double gamma, double rtol, double atol, int *iters_out);
 /* EPIRK5P1 (reading R26): Y1 = u + a11 hphi_1(g11 hJ) f; Y2 = u + a21 hphi_1(g21 hJ) f + a22 phi_1(hJ) R(Y1);
- * u_out = u + hphi_1(hJ) f + b2 phi_1(g32 hJ) R(Y1) + b3 phi_3(g33 hJ)(R(Y2) - 2R(Y1)), R(x) = h(F(x) - F(u)). */
+ * u_out = u + hphi_1(hJ) f + b2 phi_1(g32 hJ) R(Y1) + b3 phi_3(g33 hJ)(R(Y2) - 2R(Y1)), R(x) = h(F(x) - F(u)).
+ * lx_step(LX_EPIRK5P1, ...) also returns the embedded fourth-order solution u_low (g32 -> 1/2, g33 -> 1,
+ * reading R33; u_low may be NULL) and err = ||u_high - u_low|| / sqrt(N). */
 lx_status lx_step_epirk5p1(lx_ctx *ctx, const lx_problem *pb, const double *u, double *u_out, double dt,
                            double c, double gamma, double rtol, double atol, int *iters_out);
 /* Dispatch by method (the paper's exp_int / embed_exp_int). */

@@ -1145,7 +1145,7 @@ static lx_status run_stage(lx_ctx* ctx, int op, const StageArgs& A0) {
     StageArgs A = A0;
     A.grid = stage_grid_size(ctx->device, op);
     if (A.grid > ctx->max_grid) A.grid = ctx->max_grid;
-    if (ctx->comm && (op == ST_FINAL4 || op == ST_FINAL_EXPRB32))
+    if (ctx->comm && (op == ST_FINAL4 || op == ST_FINAL_EXPRB32 || op == ST_LIN4_ERR))
         return comm_stage_norm(ctx->comm, op, A, ctx->stream, &ctx->launches) ? fail(LX_ERR_NCCL, "stage norm: %s", comm_error()) : LX_OK;
     CUDA_TRY(launch_stage(op, A, ctx->stream));
     ctx->launches++;
@@ -1213,7 +1213,7 @@ static lx_status stage_remainder(lx_ctx* ctx, const lx_problem* pb, int rec, con
 }
 
 // Non-embedded methods: err = 0, u_low optional (a copy of u_high).
-static bool nonembedded(lx_method m) { return m == LX_ROSENBROCK_EULER || m == LX_EXPRB42 || m == LX_EPIRK5P1; }
+static bool nonembedded(lx_method m) { return m == LX_ROSENBROCK_EULER || m == LX_EXPRB42; }
 
 // EPIRK5P1 tableau (reading R26; Tokman, Loffeld & Tranquilli 2012, cited at P:83)
 namespace epirk5 {
@@ -1367,33 +1367,39 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
         return run_stage(ctx, ST_FINAL4, A);
     }
     if (method == LX_EPIRK5P1) {
-        // reading R26: R(x) = dt (F(x) - F(u)); vertical phi_1 {g11, g21, 1} on f dt, vertical phi_1 {g32, 1}
-        // on R(Y1), phi_3(g33 hJ) on R(Y2) - 2 R(Y1)
+        // reading R26: R(x) = dt (F(x) - F(u)); vertical phi_1 {g11, g21, 1} on f dt, vertical phi_1
+        // {1/2, g32, 1} on R(Y1), vertical phi_3 {g33, 1} on R(Y2) - 2 R(Y1); the 1/2 and the second phi_3
+        // accumulator make the embedded fourth-order solution (reading R33)
         using namespace epirk5;
         double* S1 = scratch(ctx, 1);
         double* S2 = scratch(ctx, 2);
         double* S3 = scratch(ctx, 3);
         double* S7 = scratch(ctx, 7);
-        if (!S1 || !S2 || !S3 || !S7) return fail(LX_ERR_CUDA, "scratch allocation failed");
-        const double e3[3] = {g11, g21, g31}, e2[2] = {g32, g22}, e1[1] = {g33};
+        double* S8 = scratch(ctx, 8);    // (scratch 4..6 hold lx_integrate's states; 8, 9 are free here)
+        double* S9 = scratch(ctx, 9);
+        double* u4 = lo ? lo : scratch(ctx, 6);
+        if (!S1 || !S2 || !S3 || !S7 || !S8 || !S9 || !u4) return fail(LX_ERR_CUDA, "scratch allocation failed");
+        const double e3[3] = {g11, g21, g31}, e2[3] = {0.5, g32, g22}, e1[2] = {g33, 1.0};
         double* pv[3] = {S1, S2, S3};
         LX_TRY(leja_device(ctx, pb, ul, S0, pv, e3, 3, dt, c, gamma, 1, rtol, atol, rec));
         // R1 = dt F(u + a11 P1) - dt F(u) -> S0 (f dt consumed)
         LX_TRY(stage_remainder(ctx, pb, rec, u, u, S1, a11, nullptr, 0.0, 1.0, dt, S0, hi));
-        double* qv[2] = {S1, hi};                            // Q1 = phi_1(g32 hJ) R1, Q2 = phi_1(hJ) R1
-        LX_TRY(leja_device(ctx, pb, ul, S0, qv, e2, 2, dt, c, gamma, 1, rtol, atol, rec));
+        // Qh = phi_1(hJ/2) R1 (embedded), Q1 = phi_1(g32 hJ) R1, Q2 = phi_1(hJ) R1
+        double* qv[3] = {S8, S1, hi};
+        LX_TRY(leja_device(ctx, pb, ul, S0, qv, e2, 3, dt, c, gamma, 1, rtol, atol, rec));
         // R2 = dt F(u + a21 P2 + a22 Q2) - dt F(u) -> S2
         LX_TRY(stage_remainder(ctx, pb, rec, u, u, S2, a21, hi, a22, 1.0, dt, S7, S2));
         A = stage_args(ctx, pb, rec);
         A.x0 = S7; A.x1 = S0; A.a0 = 1.0; A.a1 = -2.0; A.y0 = S0;  // R2 - 2 R1
         LX_TRY(run_stage(ctx, ST_AXPBY, A));
-        double* o3[1] = {S2};
-        LX_TRY(leja_device(ctx, pb, ul, S0, o3, e1, 1, dt, c, gamma, 3, rtol, atol, rec));
-        A = stage_args(ctx, pb, rec);
-        A.x0 = u; A.x1 = S3; A.x2 = S1; A.x3 = S2; A.a0 = b1; A.a1 = b2; A.a2 = b3; A.y0 = hi;
+        double* o3[2] = {S2, S9};                            // phi_3(g33 hJ), phi_3(hJ) (embedded)
+        LX_TRY(leja_device(ctx, pb, ul, S0, o3, e1, 2, dt, c, gamma, 3, rtol, atol, rec));
+        A = stage_args(ctx, pb, rec);                        // u4 (embedded)
+        A.x0 = u; A.x1 = S3; A.x2 = S8; A.x3 = S9; A.a0 = b1; A.a1 = b2; A.a2 = b3; A.y0 = u4;
         LX_TRY(run_stage(ctx, ST_LIN4, A));
-        if (lo && lo != hi) CUDA_TRY(cudaMemcpyAsync(lo, hi, ctx->N_loc * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
-        return LX_OK;
+        A = stage_args(ctx, pb, rec);                        // u5 ; err = ||u5 - u4||
+        A.x0 = u; A.x1 = S3; A.x2 = S1; A.x3 = S2; A.a0 = b1; A.a1 = b2; A.a2 = b3; A.y0 = hi; A.y1 = u4;
+        return run_stage(ctx, ST_LIN4_ERR, A);
     }
     // EXPRB43 / EPIRK4s3A (reading R17)
     const bool epirk = method == LX_EPIRK4S3A;
@@ -1448,7 +1454,7 @@ lx_status lx_step(lx_ctx* ctx, lx_method method, const lx_problem* pb0, const do
     LX_TRY(check_problem(ctx, pb));
     if ((int)method < 0 || (int)method > 7) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
     if (!u || !u_high) return fail(LX_ERR_ARG, "NULL argument");
-    if (!nonembedded(method) && !u_low)
+    if (!nonembedded(method) && method != LX_EPIRK5P1 && !u_low)   // EPIRK5P1: u_low optional (R33)
         return fail(LX_ERR_ARG, "u_low required for embedded methods");
     if (u_low == u || u_high == u) return fail(LX_ERR_ALIAS, "outputs must not alias u");
     if (u_low && u_low == u_high) return fail(LX_ERR_ALIAS, "u_low must differ from u_high");
@@ -1484,6 +1490,7 @@ static int embedded_order(lx_method m) {
         case LX_EXPRB43: return 3;
         case LX_EPIRK4S3A: return 3;
         case LX_EXPRB53S3: return 3;
+        case LX_EPIRK5P1: return 4;   // reading R33
         case LX_EXPRB54S4: return 4;
         default: return 0;
     }
@@ -1948,23 +1955,31 @@ static lx_status bb_step(BbRun& R, lx_method method, const double* u, double* lo
     }
     if (method == LX_EPIRK5P1) {                       // reading R26
         using namespace epirk5;
-        const double e3[3] = {g11, g21, g31}, e2[2] = {g32, g22}, e1[1] = {g33};
+        const double e3[3] = {g11, g21, g31}, e2[3] = {0.5, g32, g22}, e1[2] = {g33, 1.0};
         double* pv[3] = {t[1], t[2], t[3]};
         LX_TRY(R.leja(f_u, pv, e3, 3, dt, c, gamma, 1, rtol, atol));
         LX_TRY(R.remainder(u, t[4]));                 // NL_u
         LX_TRY(R.comb(t[5], 1.0, u, a11, t[1]));      // Y1
         LX_TRY(R.remainder(t[5], t[6]));
         LX_TRY(R.comb(t[5], dt, t[6], -dt, t[4]));    // R1
-        double* qv[2] = {t[6], t[7]};
-        LX_TRY(R.leja(t[5], qv, e2, 2, dt, c, gamma, 1, rtol, atol));
-        LX_TRY(R.comb(t[1], 1.0, u, a21, t[2], a22, t[7]));   // Y2
-        LX_TRY(R.remainder(t[1], t[2]));
-        LX_TRY(R.comb(t[7], dt, t[2], -dt, t[4]));    // R2
-        LX_TRY(R.comb(t[2], 1.0, t[7], -2.0, t[5]));  // R2 - 2 R1
-        double* o3[1] = {t[7]};
-        LX_TRY(R.leja(t[2], o3, e1, 1, dt, c, gamma, 3, rtol, atol));
-        LX_TRY(R.comb(hi, 1.0, u, b1, t[3], b2, t[6], b3, t[7]));
-        if (lo && lo != hi) LX_TRY(R.comb(lo, 1.0, hi));
+        double* qv[3] = {t[1], t[6], t[7]};           // phi_1 {1/2 (embedded, R33), g32, 1} on R1
+        LX_TRY(R.leja(t[5], qv, e2, 3, dt, c, gamma, 1, rtol, atol));
+        LX_TRY(R.comb(t[2], 1.0, u, a21, t[2], a22, t[7]));   // Y2 (in place)
+        LX_TRY(R.remainder(t[2], t[7]));
+        LX_TRY(R.comb(t[2], dt, t[7], -dt, t[4]));    // R2
+        LX_TRY(R.comb(t[2], 1.0, t[2], -2.0, t[5]));  // R2 - 2 R1
+        double* o3[2] = {t[7], t[5]};                 // phi_3 {g33, 1 (embedded)}
+        LX_TRY(R.leja(t[2], o3, e1, 2, dt, c, gamma, 3, rtol, atol));
+        LX_TRY(R.comb(hi, 1.0, u, b1, t[3], b2, t[6], b3, t[7]));   // u5
+        double* u4 = lo ? lo : t[4];
+        LX_TRY(R.comb(u4, 1.0, u, b1, t[3], b2, t[1], b3, t[5]));   // u4
+        BbLin L = R.lin();
+        L.x0 = hi;
+        L.a0 = 1.0;
+        L.x1 = u4;
+        L.a1 = -1.0;
+        CUDA_TRY(launch_bb_norm(L, ctx->stream));
+        ctx->launches++;
         return LX_OK;
     }
     // EXPRB43 / EPIRK4s3A (reading R17)
@@ -2064,7 +2079,7 @@ lx_status lx_step_cb(lx_ctx* ctx, lx_method method, lx_rhs_fn f, void* user, con
                      int* iters_out) {
     if (!ctx || !f || !u || !u_high) return fail(LX_ERR_ARG, "NULL argument");
     if ((int)method < 0 || (int)method > 7) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
-    if (!nonembedded(method) && !u_low)
+    if (!nonembedded(method) && method != LX_EPIRK5P1 && !u_low)   // EPIRK5P1: u_low optional (R33)
         return fail(LX_ERR_ARG, "u_low required for embedded methods");
     if (u_low == u || u_high == u) return fail(LX_ERR_ALIAS, "outputs must not alias u");
     if (u_low && u_low == u_high) return fail(LX_ERR_ALIAS, "u_low must differ from u_high");

@@ -245,6 +245,7 @@ enum StageOp {
     ST_SUM3,              // y0 = x0 + x1 + x2
     ST_LIN3,              // y0 = x0 + a0*x1 + a1*x2
     ST_LIN4,              // y0 = x0 + a0*x1 + a1*x2 + a2*x3
+    ST_LIN4_ERR,          // y0 = x0 + a0*x1 + a1*x2 + a2*x3 ; err = ||y0 - y1|| (y1 read: the embedded solution)
 };
 cudaError_t launch_stage(int op, const StageArgs& A, cudaStream_t s);
 cudaError_t launch_rhs(const LejaParams& P, double scale, cudaStream_t s);

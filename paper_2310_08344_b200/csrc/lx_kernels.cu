@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kThreads) k_stage_pointwise(const __grid_const
     // before any store (outputs may alias inputs element-wise, which blocks the compiler from
     // overlapping trips on its own), so every thread keeps UN x (inputs) 16-byte loads in flight.
     constexpr int UN = 4;
-    constexpr int NIN = (OP == ST_FINAL4 || OP == ST_LIN4) ? 4 : (OP == ST_STAGE_REMAINDER) ? 4
+    constexpr int NIN = (OP == ST_LIN4_ERR) ? 5 : (OP == ST_FINAL4 || OP == ST_LIN4) ? 4 : (OP == ST_STAGE_REMAINDER) ? 4
                         : (OP == ST_SUM3 || OP == ST_LIN3) ? 3 : (OP == ST_MAXSQ) ? 1 : 2;
     __shared__ double s_red[kWarps][kSlot];
     __shared__ int s_last;
@@ -164,11 +164,12 @@ __global__ void __launch_bounds__(kThreads) k_stage_pointwise(const __grid_const
     double acc = 0.0;
     unsigned long long umax = 0ull;
     const double dt = A.dt, react = A.st.react;
-    const double* in[4];
+    const double* in[5] = {};
     if (OP == ST_REMAINDER_DIFF) { in[0] = A.x0; in[1] = A.u; }
     else if (OP == ST_STAGE_REMAINDER) { in[0] = A.x0; in[1] = A.u; in[2] = A.x1; in[3] = A.x2; }
     else if (OP == ST_EXPRB32_A) { in[0] = A.x0; in[1] = A.x1; }
     else { in[0] = A.x0; in[1] = A.x1; in[2] = A.x2; in[3] = A.x3; }
+    if (OP == ST_LIN4_ERR) in[4] = A.y1;
     for (long long i0 = (long long)blockIdx.x * kThreads + threadIdx.x; i0 < npair; i0 += UN * stride) {
         double2 v[UN][NIN];
 #pragma unroll
@@ -232,6 +233,14 @@ __global__ void __launch_bounds__(kThreads) k_stage_pointwise(const __grid_const
                 const double2 x = v[q][0], y = v[q][1], z = v[q][2], w = v[q][3];
                 st2(A.y0 + o, make_double2(x.x + A.a0 * y.x + A.a1 * z.x + A.a2 * w.x,
                                            x.y + A.a0 * y.y + A.a1 * z.y + A.a2 * w.y));
+            } else if (OP == ST_LIN4_ERR) {
+                const double2 x = v[q][0], y = v[q][1], z = v[q][2], w = v[q][3], e = v[q][4];
+                const double2 r = make_double2(x.x + A.a0 * y.x + A.a1 * z.x + A.a2 * w.x,
+                                               x.y + A.a0 * y.y + A.a1 * z.y + A.a2 * w.y);
+                st2(A.y0 + o, r);
+                const double ex = r.x - e.x, ey = r.y - e.y;
+                acc = fma(ex, ex, acc);
+                acc = fma(ey, ey, acc);
             } else if (OP == ST_SUM3) {
                 const double2 x = v[q][0], y = v[q][1], z = v[q][2];
                 st2(A.y0 + o, make_double2(x.x + y.x + z.x, x.y + y.y + z.y));
@@ -243,7 +252,7 @@ __global__ void __launch_bounds__(kThreads) k_stage_pointwise(const __grid_const
             }
         }
     }
-    if (OP == ST_FINAL4 || OP == ST_FINAL_EXPRB32) stage_reduce_err(A, acc, s_red, &s_last);
+    if (OP == ST_FINAL4 || OP == ST_FINAL_EXPRB32 || OP == ST_LIN4_ERR) stage_reduce_err(A, acc, s_red, &s_last);
     if (OP == ST_MAXSQ) {
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
@@ -285,6 +294,7 @@ static void* stage_kernel_ptr(int op) {
         case ST_SUM3: return (void*)k_stage_pointwise<ST_SUM3>;
         case ST_LIN3: return (void*)k_stage_pointwise<ST_LIN3>;
         case ST_LIN4: return (void*)k_stage_pointwise<ST_LIN4>;
+        case ST_LIN4_ERR: return (void*)k_stage_pointwise<ST_LIN4_ERR>;
     }
     return nullptr;
 }
@@ -332,6 +342,7 @@ cudaError_t launch_stage(int op, const StageArgs& A, cudaStream_t s) {
         case ST_SUM3: k_stage_pointwise<ST_SUM3><<<g, b, 0, s>>>(A); break;
         case ST_LIN3: k_stage_pointwise<ST_LIN3><<<g, b, 0, s>>>(A); break;
         case ST_LIN4: k_stage_pointwise<ST_LIN4><<<g, b, 0, s>>>(A); break;
+        case ST_LIN4_ERR: k_stage_pointwise<ST_LIN4_ERR><<<g, b, 0, s>>>(A); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

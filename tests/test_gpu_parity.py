@@ -734,7 +734,7 @@ def test_pinned_host_pipelined_leja_calls(xi300):
     assert r.iters == it and _rel(outs[0], r.outs[0]) <= TOL
 
 
-@pytest.mark.parametrize("method", ["exprb32", "exprb43", "epirk4s3a", "exprb53s3", "exprb54s4"])
+@pytest.mark.parametrize("method", ["exprb32", "exprb43", "epirk4s3a", "exprb53s3", "exprb54s4", "epirk5p1"])
 def test_adaptive_step_size_control(xi300, method):
     # lx_integrate_adaptive vs the oracle's controller (reading R32): the same accept / reject sequence, the
     # same step sizes (they depend on err^(1/(q+1)); err agrees to rounding), the same final state
