@@ -196,7 +196,8 @@ lx_status lx_ctx_set_comm_local_ex(lx_ctx *ctx, lx_local_group *group, int rank,
  * lx_ctx_set_comm_ipc maps the peers' blocks.  Only Leja calls (the slab
  * kernel) are available on such a context: operations that need a collective
  * outside the kernel return LX_ERR_NCCL.  Ranks may share one GPU (processes
- * time-slice it).  2D only, 1..8 ranks, >= 16 rows per rank, n1 >= 64.
+ * time-slice it).  1..8 ranks; 2D: >= 16 rows per rank, n1 >= 64; 3D: >= 4 planes per rank,
+ * n1 % 16 == 0, n2 % 64 == 0.
  * Errors: LX_ERR_UNSUPPORTED, LX_ERR_DIM, LX_ERR_ARG, LX_ERR_NCCL, LX_ERR_CUDA. */
 lx_status lx_ctx_ipc_handle(lx_ctx *ctx, void *out64);
 lx_status lx_ctx_set_comm_ipc(lx_ctx *ctx, int rank, int nranks, const void *handles);

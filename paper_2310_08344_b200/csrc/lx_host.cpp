@@ -825,7 +825,8 @@ lx_status lx_ctx_set_comm(lx_ctx* ctx, const void* uid, int rank, int nranks) {
 
 lx_status lx_ctx_ipc_handle(lx_ctx* ctx, void* out64) {
     if (!ctx || !out64) return fail(LX_ERR_ARG, "NULL");
-    if (ctx->ndim != 2 || ctx->n[1] < 64) return fail(LX_ERR_UNSUPPORTED, "peer transport: 2D grids with n1 >= 64");
+    const bool ok = ctx->ndim == 2 ? ctx->n[1] >= 64 : (ctx->n[1] % 16 == 0 && ctx->n[2] % 64 == 0);
+    if (!ok) return fail(LX_ERR_UNSUPPORTED, "peer transport: 2D grids with n1 >= 64, 3D with n1 % 16 == 0, n2 % 64 == 0");
     if (!ctx->ipc_blk) {
         const size_t bytes = comm_block_bytes(ctx->row);
         CUDA_TRY(cudaMalloc(&ctx->ipc_blk, bytes));

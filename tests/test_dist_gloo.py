@@ -48,7 +48,24 @@ def _exchange(gh, n_loc, rank, world, mode):
         r.wait()
 
 
-def _worker(rank, world, port, result_dir, mode):
+def _case(shape):
+    """Input, dt and (c, gamma) of the emulated slab run: the Problem-I Gaussian (2D, 10 x CFL) or a
+    seeded random field (3D, 5 x CFL; the 3D slab kernel follows the mode-1 plan with planes)."""
+    import oracle as O
+    import workloads as W
+    dx = tuple(2.0 / n for n in shape)
+    pb = O.Problem(shape, dx, 1.0, 10.0, 0.0)
+    if len(shape) == 2:
+        v = W.ic_problem1_2d(*shape)
+        dt = 10 * W.dt_cfl(shape[0], 10.0)
+    else:
+        v = W.ic_random(shape, seed=29, amp=0.2)
+        dt = 5 * min(W.dt_cfl(n, 10.0, 3) for n in shape)
+    c, g = O.shift_scale(O.spectrum_bound(pb))
+    return pb, v, dt, c, g
+
+
+def _worker(rank, world, port, result_dir, mode, shape=(40, 24)):
     import sys
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -63,23 +80,18 @@ def _worker(rank, world, port, result_dir, mode):
     dist.all_gather_object(ids, uid)
     assert len(uid) == 128 and all(i == uid for i in ids)
     # 2. slabs and timing reduction
-    n0, n1 = 40, 24
+    n0 = shape[0]
     sl = lxd.slabs(n0, world)
     b, e = sl[rank]
     assert lxd.max_over_ranks(float(rank) + 0.5) == world - 0.5
     # 3. emulated slab Leja iterations (oracle arithmetic, the library's exchange plan)
-    shape = (n0, n1)
-    dx = (2.0 / n0, 2.0 / n1)
-    pb = O.Problem(shape, dx, 1.0, 10.0, 0.0)
-    v = W.ic_problem1_2d(n0, n1)
+    pb, v, dt, c, g = _case(shape)
     xi = O.leja_points(300)
-    dt = 10 * W.dt_cfl(n0, 10.0)
-    c, g = O.shift_scale(O.spectrum_bound(pb))
     d = O.divided_differences(1, xi, 300, dt, c, g)
     n_loc = e - b
-    N = n0 * n1
+    N = v.size
     G = 1 if mode == 0 else 2
-    y = np.zeros((n_loc + G + (2 if mode == 0 else 4), n1))   # ghost rows -G..-1, local rows, ghost rows n..
+    y = np.zeros((n_loc + G + (2 if mode == 0 else 4),) + tuple(shape[1:]))   # ghost rows -G..-1, local, n..
     y[G:G + n_loc] = v[b:e]
     p = d[0] * v[b:e]
 
@@ -130,18 +142,16 @@ def _worker(rank, world, port, result_dir, mode):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,mode", [(2, 0), (3, 0), (2, 1), (3, 1)])
-def test_gloo_slab_protocol(tmp_path, world, mode):
+@pytest.mark.parametrize("world,mode,shape", [(2, 0, (40, 24)), (3, 0, (40, 24)), (2, 1, (40, 24)), (3, 1, (40, 24)),
+                                              (2, 1, (24, 8, 8)), (3, 1, (20, 8, 6))])
+def test_gloo_slab_protocol(tmp_path, world, mode, shape):
+    # 3D rows: the 3D peer-memory slab kernel's ghost PLANES follow the same mode-1 plan (rows = planes;
+    # 20 planes over 3 ranks: ragged slabs of 7 / 7 / 6)
     import oracle as O
-    import workloads as W
-    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path), mode), nprocs=world, join=True,
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path), mode, shape), nprocs=world, join=True,
                        start_method="spawn")
-    n0, n1 = 40, 24
-    pb = O.Problem((n0, n1), (2.0 / n0, 2.0 / n1), 1.0, 10.0, 0.0)
-    v = W.ic_problem1_2d(n0, n1)
+    pb, v, dt, c, g = _case(shape)
     xi = O.leja_points(300)
-    dt = 10 * W.dt_cfl(n0, 10.0)
-    c, g = O.shift_scale(O.spectrum_bound(pb))
     ref = O.real_leja_phi(pb, v, dt, c, g, 1, 1e-10, 1e-10, xi)
     parts, its = [], set()
     for r in range(world):

@@ -357,3 +357,36 @@ def test_peer_slab_3d_epirk_step(xi300):
     lo = np.concatenate([r[2] for r in res])
     assert np.linalg.norm(hi - ref.u_high) <= TOL * np.linalg.norm(ref.u_high)
     assert np.linalg.norm(lo - ref.u_low) <= TOL * np.linalg.norm(ref.u_low)
+
+
+def test_peer_slab_3d_kernel_two_processes_ipc(xi300):
+    # two processes on one GPU, 3D ghost planes through CUDA IPC mappings of the exchange blocks
+    import json
+    import os
+    import subprocess
+    import sys
+    shape = (16, 16, 64)
+    dx = tuple(2.0 / n for n in shape)
+    ob = O.Problem(shape, dx, 1.0, 10.0, 0.0)
+    c, g = O.shift_scale(O.spectrum_bound(ob))
+    dt = 5 * min(W.dt_cfl(n, 10.0, 3) for n in shape)
+    ls = [0, 2]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    arg = json.dumps({"dt": dt, "c": c, "g": g, "ls": ls, "tol": TOL, "shape": list(shape)})
+    r = subprocess.run([sys.executable, root + "/tools/ipc_slab_check.py", arg], capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    ranks = sorted(json.loads(r.stdout.strip().splitlines()[-1])["ranks"], key=lambda x: x["rank"])
+    assert [x["ipp"] for x in ranks] == [2, 2]
+    v = W.ic_random(shape, seed=51, amp=0.2)
+    pb = lx.Problem(shape, dx, 1.0, 10.0, 0.0)
+    with lx.Context(pb) as ctx1:
+        ctx1.set_kernel(2)
+        for idx, l in enumerate(ls):
+            full = np.concatenate([np.array(x["res"][idx][1]) for x in ranks], axis=0)
+            ref = O.real_leja_phi(ob, v, dt, c, g, l, TOL, TOL, xi300)
+            assert {x["res"][idx][0] for x in ranks} == {ref.iters}
+            assert np.linalg.norm(full - ref.outs[0]) <= TOL * np.linalg.norm(ref.outs[0])
+            one = torch.empty(shape, dtype=torch.float64, device="cuda")
+            lx.lx_real_leja_phi(ctx1, torch.from_numpy(v).cuda(), one, dt, c, g, l, TOL, TOL)
+            np.testing.assert_array_equal(full, one.cpu().numpy())

@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Two PROCESSES, one GPU, the peer-memory slab kernel through real CUDA IPC mappings.
 
-Each process owns a context on cuda:0 and one slab of a 2D advection-diffusion grid; the 64-byte IPC
+Each process owns a context on cuda:0 and one slab of a 2D (or, with "shape" of length 3, 3D) advection-diffusion
+grid; the 64-byte IPC
 handles of the exchange blocks are gathered by the parent and handed back (lx_ctx_ipc_handle /
 lx_ctx_set_comm_ipc -- the caller-side handle exchange the ABI offers), then every process runs
 lx_real_leja_phi on its slab.  The processes time-slice the GPU, so each cross-rank barrier waits for
@@ -43,9 +44,9 @@ def child(rank, nranks, conn, shape, dt, c, g, ls, tol):
 
 
 def main():
-    shape = (96, 128)
-    nranks = 2
     args = json.loads(sys.argv[1]) if len(sys.argv) > 1 else {}
+    shape = tuple(args.get("shape", (96, 128)))
+    nranks = 2
     dt, c, g, ls, tol = args["dt"], args["c"], args["g"], args["ls"], args["tol"]
     ctx = mp.get_context("spawn")
     pipes = [ctx.Pipe() for _ in range(nranks)]
