@@ -3,8 +3,9 @@
 LX_COMM_FORCE (the library's own communicator with itself as both neighbours).  Mode "nccl": Leja calls run
 the peer-memory slab kernel (exchange block handles gathered over NCCL), stage operations the NCCL step
 protocol; mode "nccl_nopeer" (LX_COMM_NO_PEER): every Leja iteration through step kernels + NCCL groups.
-Compares a Leja call, an EXPRB43 step and the Gershgorin bound with the single-domain path: identical
-iteration counts, fields equal to 1e-13 (only the norm summation order differs).  --time: per-iteration
+Compares a Leja call, an EXPRB43 step and the Gershgorin bound with the single-domain path (and, on a 3D grid,
+a vertical Leja call and an EPIRK4s3A step through the 3D slab kernel): identical iteration counts, fields
+equal to 1e-13 (only the norm summation order differs).  --time: per-iteration
 cost of the three paths at 4096^2 (config 1 shape).  Prints one JSON line."""
 import json
 import os
@@ -57,6 +58,36 @@ def main():
         r = out[mode]
         ok = ok and bool(r["bound_equal"] and a[1] == b[1] and a[3] == b[3] and r["leja_maxrel"] <= 1e-13
                          and r["step_maxrel"] <= 1e-13)
+    # 3D (the 3D two-step peer-memory slab kernel with itself as neighbour: ghost planes through the
+    # NCCL-gathered exchange block) -- a vertical Leja call and an EPIRK4s3A step
+    shape = (32, 16, 64)
+    pb3 = lx.Problem(shape, tuple(2.0 / m for m in shape), 1.0, 10.0, 0.0)
+    v3 = torch.from_numpy(W.ic_random(shape, seed=5, amp=0.2)).cuda()
+    dt3 = 5 * min(W.dt_cfl(m, 10.0, 3) for m in shape)
+    res3 = {}
+    for mode, flags in modes.items():
+        ctx = lx.Context(pb3)
+        if flags is not None:
+            lxd.attach(ctx, flags)
+        else:
+            ctx.set_kernel(2)
+        out["ipp3_" + mode] = ctx.iterations_per_pass
+        c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+        outs = [torch.empty_like(v3) for _ in range(2)]
+        it = lx.lx_real_leja_phi_vertical(ctx, v3, outs, (0.5, 1.0), dt3, c, g, 1, 1e-10, 1e-10)
+        lo, hi = torch.empty_like(v3), torch.empty_like(v3)
+        its, err = lx.lx_step(ctx, "epirk4s3a", v3, lo, hi, dt3, c, g, 1e-10, 1e-10)
+        res3[mode] = (it, [o.cpu().numpy() for o in outs], its, hi.cpu().numpy())
+        ctx.close()
+    a = res3["single"]
+    ok = ok and out["ipp3_single"] == 2 and out["ipp3_nccl"] == 2 and out["ipp3_nccl_nopeer"] == 1
+    for mode in ("nccl", "nccl_nopeer"):
+        b = res3[mode]
+        r = {"leja_iters": [a[0], b[0]], "step_iters": [a[2], b[2]],
+             "leja_maxrel": max(float(np.abs(x - y).max() / np.abs(x).max()) for x, y in zip(a[1], b[1])),
+             "step_maxrel": float(np.abs(a[3] - b[3]).max() / np.abs(a[3]).max())}
+        out[mode + "_3d"] = r
+        ok = ok and a[0] == b[0] and a[2] == b[2] and r["leja_maxrel"] <= 1e-13 and r["step_maxrel"] <= 1e-13
     out["ok"] = ok
     if "--time" in sys.argv:
         # per-iteration cost of the slab protocol (step kernels + NCCL halo/allgather, here to itself) vs the
