@@ -430,7 +430,9 @@ def bench_leja_2d(job, args, cfg_id, wl):
         "one_step_equivalent_frac": float(N * sum(leja_bytes_per_point(m, False) for m in iters)
                                           / (per_call_ms.sum() * 1e-3) / 1e9 / _peaks()[0]),
         "kernel_share_of_step": float(per_call_ms.sum() / (start.elapsed_time(stop) / args.steps)),
-        "points_per_launch": N})
+        "points_per_launch": N},
+        # the committed ncu capture is of config 1's launches (4096^2, one GPU); other grids: no capture
+        traffic_file="leja_traffic.json" if (cfg_id == 1 and ws == 1) else "none")
 
     # e2e through the public API on pinned HOST buffers: every call stages its own H2D (v) and D2H (out)
     # inside the library (lx_real_leja_phi on host pointers: pipelined copy-in / kernel / copy-out streams)
