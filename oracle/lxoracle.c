@@ -626,7 +626,7 @@ done:
 /* Exponential integrators (listings alg:Ros_Eu, alg:exprb32;      */
 /* EXPRB43 and EPIRK4s3A tableaux from P:83's citations, R17).                */
 /*   method 0 Rosenbrock-Euler, 1 EXPRB32, 2 EXPRB43, 3 EPIRK4s3A, 4 EXPRB42,    */
-/*   5 EPIRK5P1, 6 EXPRB53s3, 7 EXPRB54s4.                                      */
+/*   5 EPIRK5P1, 6 EXPRB53s3, 7 EXPRB54s4, 8 EPIRK4s3B.                         */
 /* u_low may be NULL for Rosenbrock-Euler (non-embedded, err = 0).            */
 /* ------------------------------------------------------------------------- */
 static void axpby(double a, const double *x, double b, const double *y, double *z, long N)
@@ -651,7 +651,7 @@ int oc_step_ex(const oc_problem *pb, int jac_mode, int method, const double *u, 
     int it = 0, total = 0, s = OC_OK;
     if (err) *err = 0.0;
     if (iters) *iters = 0;
-    if (method < 0 || method > 7) return OC_ERR_ARG;
+    if (method < 0 || method > 8) return OC_ERR_ARG;
     if (jac_mode != OC_JAC_EXACT && jac_mode != OC_JAC_FD) return OC_ERR_ARG;
     size_t bytes = sizeof(double) * (size_t)N;
     double *fu_raw = NULL;
@@ -806,6 +806,48 @@ int oc_step_ex(const oc_problem *pb, int jac_mode, int method, const double *u, 
         for (long i = 0; i < N; i++) u_low[i] = u[i] + t3[i] + 8.0 * t7[i];      /* u3 */
         for (long i = 0; i < N; i++) t1[i] = u_high[i] - u_low[i];
         if (err) *err = oc_l2norm_scaled(t1, N);
+    } else if (method == 8) {
+        /* EPIRK4s3B (Rainwater & Tokman 2016, cited at P:83; reading R34), D_x = h (F(x) - F(u)):
+         *   a  = u + 2/3 h phi_2(hJ/2) f;   b = u + h phi_2(3hJ/4) f
+         *   u3 = u + h phi_1(hJ) f + phi_3(hJ) (54 D_a - 16 D_b)
+         *   u4 = u3 + phi_4(hJ) (-324 D_a + 144 D_b)
+         * vertical phi_2 {1/2, 3/4} on f_u, phi_1 on f_u; err = ||u4 - u3||. */
+        double cf2[2] = {0.5, 0.75};
+        double *qv[2] = {t1, t2};
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, f_u, qv, cf2, 2, dt, c, gamma, 2, rtol, atol, xi,
+                                max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        double one = 1.0;
+        double *o1[1] = {t3};
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, f_u, o1, &one, 1, dt, c, gamma, 1, rtol, atol, xi,
+                                max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        double *NLu = t4, *Da = t5, *Db = t6, *tmp = t7;
+        remainder_mode(pb, jac_mode, u, fu_raw, u, NLu);
+        axpby(1.0, u, 2.0 / 3.0, t1, u_low, N);               /* a */
+        remainder_mode(pb, jac_mode, u, fu_raw, u_low, tmp);
+        axpby(dt, tmp, -dt, NLu, Da, N);                      /* D_a */
+        axpby(1.0, u, 1.0, t2, u_low, N);                     /* b */
+        remainder_mode(pb, jac_mode, u, fu_raw, u_low, tmp);
+        axpby(dt, tmp, -dt, NLu, Db, N);                      /* D_b */
+        axpby(54.0, Da, -16.0, Db, tmp, N);                   /* w3 */
+        axpby(-324.0, Da, 144.0, Db, NLu, N);                 /* w4 */
+        double *o3[1] = {Da};
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, tmp, o3, &one, 1, dt, c, gamma, 3, rtol, atol, xi,
+                                max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        double *o4[1] = {Db};
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, NLu, o4, &one, 1, dt, c, gamma, 4, rtol, atol, xi,
+                                max_nodes, &it, NULL);
+        total += it;
+        if (s) goto out;
+        for (long i = 0; i < N; i++) u_low[i] = u[i] + t3[i] + Da[i];        /* u3 */
+        for (long i = 0; i < N; i++) u_high[i] = u_low[i] + Db[i];           /* u4 */
+        for (long i = 0; i < N; i++) tmp[i] = u_high[i] - u_low[i];
+        if (err) *err = oc_l2norm_scaled(tmp, N);
     } else if (method == 7) {
         /* EXPRB54s4 (Luan & Ostermann 2014, cited at P:83; reading R31), D_x = h (F(x) - F(u)),
          * nodes c2 = 1/4, c3 = 1/2, c4 = 9/10:
@@ -968,6 +1010,7 @@ static int oc_embedded_order(int method)
     case 6: return 3;   /* EXPRB53s3: u_3 */
     case 5: return 4;   /* EPIRK5P1: u_4 (R33) */
     case 7: return 4;   /* EXPRB54s4: u_4 */
+    case 8: return 3;   /* EPIRK4s3B: u_3 (R34) */
     default: return 0;  /* non-embedded */
     }
 }

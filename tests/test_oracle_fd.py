@@ -117,7 +117,8 @@ def test_blackbox_leja_vs_fft_exact(xi300, l, jac):
     assert rel <= (1e-11 if jac == "linear_f" else 1e-7), rel
 
 
-@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3", "exprb54s4"])
+@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3", "exprb54s4",
+                                    "epirk4s3b"])
 def test_fd_integrators_linear_exactness(xi300, method):
     n = 64
     pb = O.Problem((n, n), (2 / n, 2 / n), 1.0, 10.0, 0.0)
