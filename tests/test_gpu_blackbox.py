@@ -120,7 +120,8 @@ def test_fd_leja_torch_callback(xi300):
     assert _rel(out, r.outs[0]) <= FD_TOL
 
 
-@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3", "exprb54s4"])
+@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3", "exprb54s4",
+                                    "epirk4s3b"])
 def test_fd_steps_allen_cahn(xi300, method):
     n = 64
     pb, ob = _pair((n, n), diff=1e-4, nu=0.0, react=1.0)

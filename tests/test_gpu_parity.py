@@ -208,7 +208,8 @@ def test_power_iteration_and_rhs(xi300):
 
 
 # ---------------------------------------------------------------- integrators
-@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3", "exprb54s4"])
+@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3", "exprb54s4",
+                                    "epirk4s3b"])
 def test_steps_linear_advdiff(xi300, method):
     n = 64
     pb, ob = _pair((n, n))
@@ -226,7 +227,8 @@ def test_steps_linear_advdiff(xi300, method):
         assert err == r.err == 0.0
 
 
-@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3", "exprb54s4"])
+@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3", "exprb54s4",
+                                    "epirk4s3b"])
 def test_steps_allen_cahn(xi300, method):
     n = 128
     pb, ob = _pair((n, n), diff=1e-4, nu=0.0, react=1.0)
@@ -306,7 +308,7 @@ def test_leja_3d(xi300, shape):
         assert est == pytest.approx(O.power_iteration(ob, None, 20), rel=1e-10)
 
 
-@pytest.mark.parametrize("method", ["epirk4s3a", "exprb43"])
+@pytest.mark.parametrize("method", ["epirk4s3a", "exprb43", "epirk4s3b"])
 def test_steps_3d(xi300, method):
     n = 32
     shape = (n, n, n)
@@ -336,7 +338,8 @@ def test_steps_3d(xi300, method):
     assert err == pytest.approx(r.err, rel=1e-8)
 
 
-@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3", "exprb54s4"])
+@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3", "exprb54s4",
+                                    "epirk4s3b"])
 def test_integrate_device_spectrum(xi300, method):
     # lx_integrate: the paper's time loop with (c, gamma) recomputed ON THE DEVICE every
     # step; the oracle recomputes them from its own state with the same formula (R16).
@@ -395,7 +398,8 @@ def _burgers_pair(n, beta=10.0):
     return lx.Problem((n, n), dx, 1.0, 0.0, 0.0, None, beta), O.Problem((n, n), dx, 1.0, 0.0, 0.0, None, beta)
 
 
-@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3", "exprb54s4"])
+@pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3", "exprb54s4",
+                                    "epirk4s3b"])
 def test_burgers_steps(xi300, method):
     n = 128
     pb, ob = _burgers_pair(n)
@@ -734,7 +738,8 @@ def test_pinned_host_pipelined_leja_calls(xi300):
     assert r.iters == it and _rel(outs[0], r.outs[0]) <= TOL
 
 
-@pytest.mark.parametrize("method", ["exprb32", "exprb43", "epirk4s3a", "exprb53s3", "exprb54s4", "epirk5p1"])
+@pytest.mark.parametrize("method", ["exprb32", "exprb43", "epirk4s3a", "exprb53s3", "exprb54s4", "epirk5p1",
+                                    "epirk4s3b"])
 def test_adaptive_step_size_control(xi300, method):
     # lx_integrate_adaptive vs the oracle's controller (reading R32): the same accept / reject sequence, the
     # same step sizes (they depend on err^(1/(q+1)); err agrees to rounding), the same final state
