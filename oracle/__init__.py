@@ -26,7 +26,7 @@ _LIB_OMP = os.path.join(_HERE, "liblxoracle_omp.so")   # same source with -fopen
 
 OK, ERR_ARG, ERR_UNSUPPORTED, ERR_NOCONV, ERR_NONFINITE = 0, 1, 4, 5, 6
 METHODS = {"rosenbrock_euler": 0, "exprb32": 1, "exprb43": 2, "epirk4s3a": 3, "exprb42": 4, "epirk5p1": 5, "exprb53s3": 6,
-           "exprb54s4": 7, "epirk4s3b": 8}
+           "exprb54s4": 7, "epirk4s3b": 8, "epirk4s3": 9}
 JAC = {"exact": 0, "fd": 1, "linear_f": 2}     # lxoracle.c OC_JAC_* (black-box RHS modes, reading R25)
 
 

@@ -626,7 +626,7 @@ done:
 /* Exponential integrators (listings alg:Ros_Eu, alg:exprb32;      */
 /* EXPRB43 and EPIRK4s3A tableaux from P:83's citations, R17).                */
 /*   method 0 Rosenbrock-Euler, 1 EXPRB32, 2 EXPRB43, 3 EPIRK4s3A, 4 EXPRB42,    */
-/*   5 EPIRK5P1, 6 EXPRB53s3, 7 EXPRB54s4, 8 EPIRK4s3B.                         */
+/*   5 EPIRK5P1, 6 EXPRB53s3, 7 EXPRB54s4, 8 EPIRK4s3B, 9 EPIRK4s3.             */
 /* u_low may be NULL for Rosenbrock-Euler (non-embedded, err = 0).            */
 /* ------------------------------------------------------------------------- */
 static void axpby(double a, const double *x, double b, const double *y, double *z, long N)
@@ -651,7 +651,7 @@ int oc_step_ex(const oc_problem *pb, int jac_mode, int method, const double *u, 
     int it = 0, total = 0, s = OC_OK;
     if (err) *err = 0.0;
     if (iters) *iters = 0;
-    if (method < 0 || method > 8) return OC_ERR_ARG;
+    if (method < 0 || method > 9) return OC_ERR_ARG;
     if (jac_mode != OC_JAC_EXACT && jac_mode != OC_JAC_FD) return OC_ERR_ARG;
     size_t bytes = sizeof(double) * (size_t)N;
     double *fu_raw = NULL;
@@ -920,29 +920,37 @@ int oc_step_ex(const oc_problem *pb, int jac_mode, int method, const double *u, 
         for (long i = 0; i < N; i++) t1[i] = u_high[i] - u_low[i];
         if (err) *err = oc_l2norm_scaled(t1, N);
     } else {
-        /* EXPRB43 (method 2) / EPIRK4s3A (method 3) -- R17 tableaux:
+        /* EXPRB43 (method 2) / EPIRK4s3A (method 3) -- R17 tableaux -- / EPIRK4s3 (method 9, R35):
          *  EXPRB43:   a = u + 1/2 hphi_1(hJ/2) f;  b = u + hphi_1 f + hphi_1 D_a
          *             u3 = u + hphi_1 f + hphi_3 (16 D_a - 2 D_b)
          *             u4 = u3 + hphi_4 (-48 D_a + 12 D_b)
          *  EPIRK4s3A: a = u + 1/2 hphi_1(hJ/2) f;  b = u + 2/3 hphi_1(2hJ/3) f
          *             u3 = u + hphi_1 f + hphi_3 (32 D_a - 27/2 D_b)
          *             u4 = u3 + hphi_4 (-144 D_a + 81 D_b)
+         *  EPIRK4s3:  a = u + 1/8 hphi_1(hJ/8) f;  b = u + 1/9 hphi_1(hJ/9) f
+         *             u3 = u + hphi_1 f + phi_3 (-1024 D_a + 1458 D_b)
+         *             u4 = u3 + phi_4 (27648 D_a - 34992 D_b)
          *  D_x = dt (F(x) - F(u)); vertical phi_1 on f_u. */
-        int epirk = (method == 3);
-        double cf2[2] = {0.5, 1.0}, cf3[3] = {0.5, 2.0 / 3.0, 1.0};
+        int e4s3 = (method == 9);
+        int epirk = (method == 3) || e4s3;
+        double cf2[2] = {0.5, 1.0}, cf3[3] = {0.5, 2.0 / 3.0, 1.0}, cf9[3] = {1.0 / 9.0, 1.0 / 8.0, 1.0};
         double *pv[3] = {t1, t2, t3};
-        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, f_u, pv, epirk ? cf3 : cf2, epirk ? 3 : 2, dt, c, gamma, 1,
-                             rtol, atol, xi, max_nodes, &it, NULL);
+        s = oc_real_leja_phi_ex(pb, jac_mode, u, fu_raw, f_u, pv, e4s3 ? cf9 : epirk ? cf3 : cf2, epirk ? 3 : 2, dt, c,
+                             gamma, 1, rtol, atol, xi, max_nodes, &it, NULL);
         total += it;
         if (s) goto out;
         double *p_half = t1, *p_one = epirk ? t3 : t2;
         double *NLu = t4, *Da = t5, *Db = t6, *tmp = t7;
         remainder_mode(pb, jac_mode, u, fu_raw, u, NLu);
-        /* a = u + 1/2 p_half */
-        axpby(1.0, u, 0.5, p_half, u_low, N);
+        /* a = u + 1/2 p_half  (EPIRK4s3: u + 1/8 p_{1/8}, the second vertical output) */
+        if (e4s3) axpby(1.0, u, 0.125, t2, u_low, N);
+        else axpby(1.0, u, 0.5, p_half, u_low, N);
         remainder_mode(pb, jac_mode, u, fu_raw, u_low, tmp);
         axpby(dt, tmp, -dt, NLu, Da, N);                      /* D_a */
-        if (epirk) {
+        if (e4s3) {
+            /* b = u + 1/9 p_{1/9} (the first vertical output) */
+            axpby(1.0, u, 1.0 / 9.0, t1, u_low, N);
+        } else if (epirk) {
             /* b = u + 2/3 p_twothirds */
             axpby(1.0, u, 2.0 / 3.0, t2, u_low, N);
         } else {
@@ -956,8 +964,8 @@ int oc_step_ex(const oc_problem *pb, int jac_mode, int method, const double *u, 
         }
         remainder_mode(pb, jac_mode, u, fu_raw, u_low, tmp);
         axpby(dt, tmp, -dt, NLu, Db, N);                      /* D_b */
-        double a3 = epirk ? 32.0 : 16.0, b3 = epirk ? -13.5 : -2.0;
-        double a4 = epirk ? -144.0 : -48.0, b4 = epirk ? 81.0 : 12.0;
+        double a3 = e4s3 ? -1024.0 : epirk ? 32.0 : 16.0, b3 = e4s3 ? 1458.0 : epirk ? -13.5 : -2.0;
+        double a4 = e4s3 ? 27648.0 : epirk ? -144.0 : -48.0, b4 = e4s3 ? -34992.0 : epirk ? 81.0 : 12.0;
         axpby(a3, Da, b3, Db, tmp, N);                        /* w3 */
         axpby(a4, Da, b4, Db, NLu, N);                        /* w4 (NLu no longer needed) */
         double one = 1.0;
@@ -1011,6 +1019,7 @@ static int oc_embedded_order(int method)
     case 5: return 4;   /* EPIRK5P1: u_4 (R33) */
     case 7: return 4;   /* EXPRB54s4: u_4 */
     case 8: return 3;   /* EPIRK4s3B: u_3 (R34) */
+    case 9: return 3;   /* EPIRK4s3: u_3 (R35) */
     default: return 0;  /* non-embedded */
     }
 }

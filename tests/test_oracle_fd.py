@@ -118,7 +118,7 @@ def test_blackbox_leja_vs_fft_exact(xi300, l, jac):
 
 
 @pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3", "exprb54s4",
-                                    "epirk4s3b"])
+                                    "epirk4s3b", "epirk4s3"])
 def test_fd_integrators_linear_exactness(xi300, method):
     n = 64
     pb = O.Problem((n, n), (2 / n, 2 / n), 1.0, 10.0, 0.0)
@@ -130,9 +130,10 @@ def test_fd_integrators_linear_exactness(xi300, method):
     sym = refs.impulse_symbol(lambda x: O.jac_apply(pb, None, x), (n, n))
     ex = refs.fft_apply_phi(sym, u0, dt, 0)
     # F(x) - F(u) vanishes in exact arithmetic, but the literal FD remainder carries the quotient's
-    # roundoff eps_mach |A x| / eps ~ 1e-8 |u| (times the tableau weights, up to 144): not 1e-11 as with
-    # the analytic remainder (R18)
-    assert np.linalg.norm(r.u_high - ex) <= 3e-8 * np.linalg.norm(ex)
+    # roundoff eps_mach |A x| / eps ~ 1e-8 |u| (times the tableau weights, up to 144; EPIRK4s3's phi_4
+    # weights reach 34992 (R35): 243 x the noise): not 1e-11 as with the analytic remainder (R18)
+    bound = 1e-5 if method == "epirk4s3" else 3e-8
+    assert np.linalg.norm(r.u_high - ex) <= bound * np.linalg.norm(ex)
 
 
 @pytest.mark.parametrize("method,order", [("rosenbrock_euler", 2), ("exprb32", 3), ("exprb43", 4)])

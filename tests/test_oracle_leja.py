@@ -156,7 +156,7 @@ def test_leja_noconv_and_errors(xi300):
 
 # ---------------------------------------------------------------- integrators
 @pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3",
-                                    "exprb54s4", "epirk4s3b"])
+                                    "exprb54s4", "epirk4s3b", "epirk4s3"])
 def test_integrator_linear_exactness(xi300, method):
     # every exponential integrator is exact on linear homogeneous problems
     n = 64
@@ -194,7 +194,8 @@ def _allen_cahn_reference(pb, u0, T):
 
 
 @pytest.mark.parametrize("method,order", [("rosenbrock_euler", 2), ("exprb32", 3), ("exprb43", 4),
-                                          ("epirk4s3a", 4), ("exprb42", 4), ("epirk4s3b", 4)])
+                                          ("epirk4s3a", 4), ("exprb42", 4), ("epirk4s3b", 4),
+                                          ("epirk4s3", 4)])
 def test_integrator_convergence_order(xi300, method, order):
     n = 16
     pb = O.Problem((n, n), (2 / n, 2 / n), 2e-3, 0.0, 1.0)
@@ -342,7 +343,7 @@ def test_exprb53s3_orders(xi300):
 
 # ---------------------------------------------------------------- round-2 pins (VERDICT r1 "What's weak" #1)
 @pytest.mark.parametrize("method,order", [("exprb32", 2), ("exprb43", 3), ("epirk4s3a", 3), ("epirk5p1", 4),
-                                          ("epirk4s3b", 3)])
+                                          ("epirk4s3b", 3), ("epirk4s3", 3)])
 def test_embedded_solution_order(xi300, method, order):
     # The embedded (lower-order) solutions u_low that the error estimate ||u_high - u_low|| (P:252,
     # reading R20) compares against: EXPRB32 -> a (order 2), EXPRB43 / EPIRK4s3A -> u_3
@@ -537,7 +538,7 @@ def test_adaptive_linear_problem_grows_steps(xi300):
 
 
 @pytest.mark.parametrize("method,q", [("exprb32", 2), ("exprb43", 3), ("epirk4s3a", 3), ("exprb54s4", 4),
-                                      ("epirk5p1", 4), ("epirk4s3b", 3)])
+                                      ("epirk5p1", 4), ("epirk4s3b", 3), ("epirk4s3", 3)])
 def test_adaptive_controller_allen_cahn(xi300, method, q):
     # Allen-Cahn: the accept / reject decisions and the step sequence follow R32 exactly (replayed from the
     # logs), a too-large first step is rejected, and the global error at t_end shrinks with the tolerance
@@ -591,6 +592,23 @@ def test_epirk4s3b_local_error_order(xi300):
     for h in (0.0625, 0.03125, 0.015625):
         c, g = _cg(pb, u0)
         r = O.step(pb, "epirk4s3b", u0, h, c, g, 1e-14, 1e-14, xi300)
+        assert r.status == O.OK and r.err > 0.0
+        ex = _allen_cahn_reference(pb, u0, h)
+        errs.append(np.linalg.norm(r.u_high - ex) / np.linalg.norm(ex))
+    orders = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+    assert abs(orders[-1] - 5.0) < 0.3 and np.all(orders > 4.6), (errs, orders)
+
+
+def test_epirk4s3_local_error_order(xi300):
+    # EPIRK4s3 (reading R35): one step's error falls like h^5; changing a phi_4 weight (27648 -> 27000)
+    # drops the local order to 3 (dense-matrix check during the reconstruction, DESIGN R35)
+    n = 16
+    pb = O.Problem((n, n), (2 / n, 2 / n), 2e-3, 0.0, 1.0)
+    u0 = W.ic_allen_cahn_2d(n)
+    errs = []
+    for h in (0.0625, 0.03125, 0.015625):
+        c, g = _cg(pb, u0)
+        r = O.step(pb, "epirk4s3", u0, h, c, g, 1e-14, 1e-14, xi300)
         assert r.status == O.OK and r.err > 0.0
         ex = _allen_cahn_reference(pb, u0, h)
         errs.append(np.linalg.norm(r.u_high - ex) / np.linalg.norm(ex))
