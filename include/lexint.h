@@ -291,9 +291,12 @@ typedef enum {
     LX_EPIRK5P1 = 5,      /* Tokman et al. 2012 (cited at P:83, Table 2), 5th order, embedded 4th (R26, R33) */
     LX_EXPRB53S3 = 6,     /* Luan & Ostermann 2014 (cited at P:83), 5th order, embedded 3rd (R27)      */
     LX_EXPRB54S4 = 7,     /* Luan & Ostermann 2014 (cited at P:83), 5th order, embedded 4th (R31)      */
-    LX_EPIRK4S3B = 8      /* Rainwater & Tokman 2016 (cited at P:83), 4th order, embedded 3rd (R34):
+    LX_EPIRK4S3B = 8,     /* Rainwater & Tokman 2016 (cited at P:83), 4th order, embedded 3rd (R34):
                              a = u + 2/3 hphi_2(hJ/2) f, b = u + hphi_2(3hJ/4) f, u3 = u + hphi_1(hJ) f +
                              phi_3(hJ)(54 D_a - 16 D_b), u4 = u3 + phi_4(hJ)(-324 D_a + 144 D_b)          */
+    LX_EPIRK4S3 = 9       /* cited at P:83, 4th order, embedded 3rd (R35): a = u + 1/8 hphi_1(hJ/8) f,
+                             b = u + 1/9 hphi_1(hJ/9) f, u3 = u + hphi_1(hJ) f + phi_3(hJ)(-1024 D_a + 1458 D_b),
+                             u4 = u3 + phi_4(hJ)(27648 D_a - 34992 D_b)                                    */
 } lx_method;
 
 /* Rosenbrock-Euler: u_out = u + phi_1(dt J(u)) f(u) dt (alg:Ros_Eu). */

@@ -33,9 +33,9 @@ STATUS_NAMES = {0: "LX_OK", 1: "LX_ERR_ARG", 2: "LX_ERR_DIM", 3: "LX_ERR_ALIAS",
                 5: "LX_ERR_NOCONV", 6: "LX_ERR_NONFINITE", 7: "LX_ERR_UNKNOWN_INTEGRATOR", 8: "LX_ERR_CUDA",
                 9: "LX_ERR_NCCL", 10: "LX_ERR_TIMEOUT"}
 (LX_ROSENBROCK_EULER, LX_EXPRB32, LX_EXPRB43, LX_EPIRK4S3A, LX_EXPRB42, LX_EPIRK5P1, LX_EXPRB53S3, LX_EXPRB54S4,
- LX_EPIRK4S3B) = range(9)
+ LX_EPIRK4S3B, LX_EPIRK4S3) = range(10)
 METHODS = {"rosenbrock_euler": 0, "exprb32": 1, "exprb43": 2, "epirk4s3a": 3, "exprb42": 4, "epirk5p1": 5,
-           "exprb53s3": 6, "exprb54s4": 7, "epirk4s3b": 8}
+           "exprb53s3": 6, "exprb54s4": 7, "epirk4s3b": 8, "epirk4s3": 9}
 
 # Every symbol include/lexint.h declares (checked by tests/test_abi.py).
 EXPORTS = ("lx_last_error", "lx_version", "lx_leja_points", "lx_phi_scalar", "lx_divided_differences",

@@ -1402,30 +1402,35 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
         A.x0 = u; A.x1 = S3; A.x2 = S1; A.x3 = S2; A.a0 = b1; A.a1 = b2; A.a2 = b3; A.y0 = hi; A.y1 = u4;
         return run_stage(ctx, ST_LIN4_ERR, A);
     }
-    // EXPRB43 / EPIRK4s3A (reading R17) / EPIRK4s3B (reading R34)
+    // EXPRB43 / EPIRK4s3A (reading R17) / EPIRK4s3B (reading R34) / EPIRK4s3 (reading R35)
     const bool epb = method == LX_EPIRK4S3B;
-    const bool epirk = method == LX_EPIRK4S3A || epb;   // two independent stages a, b
+    const bool e4s3 = method == LX_EPIRK4S3;
+    const bool epirk = method == LX_EPIRK4S3A || epb || e4s3;   // two independent stages a, b
     double* S1 = scratch(ctx, 1);
     double* S2 = scratch(ctx, 2);
     double* S3 = epirk ? scratch(ctx, 3) : nullptr;
     if (!S1 || !S2 || (epirk && !S3)) return fail(LX_ERR_CUDA, "scratch allocation failed");
     const double cf2[2] = {0.5, 1.0}, cf3[3] = {0.5, 2.0 / 3.0, 1.0}, cfb[2] = {0.5, 0.75};
-    double* pv[3] = {S1, S2, S3};
+    const double cf9[3] = {1.0 / 9.0, 1.0 / 8.0, 1.0};
+    // EPIRK4s3: stage a uses the 1/8 output, stage b the 1/9 output (vertical coefficients increase)
+    double* pv[3] = {e4s3 ? S2 : S1, e4s3 ? S1 : S2, S3};
     if (epb) {
         // phi_2(hJ/2) f dt, phi_2(3hJ/4) f dt (vertical), phi_1(hJ) f dt
         LX_TRY(leja_device(ctx, pb, ul, S0, pv, cfb, 2, dt, c, gamma, 2, rtol, atol, rec));
         double* o1[1] = {S3};
         LX_TRY(leja_device(ctx, pb, ul, S0, o1, &one, 1, dt, c, gamma, 1, rtol, atol, rec));
     } else {
-        LX_TRY(leja_device(ctx, pb, ul, S0, pv, epirk ? cf3 : cf2, epirk ? 3 : 2, dt, c, gamma, 1, rtol, atol, rec));
+        LX_TRY(leja_device(ctx, pb, ul, S0, pv, e4s3 ? cf9 : epirk ? cf3 : cf2, epirk ? 3 : 2, dt, c, gamma, 1, rtol,
+                           atol, rec));
     }
     double* p_one = epirk ? S3 : S2;
-    // D_a = dt F(u + w_a p_a) - dt F(u)  -> S0   (w_a = 1/2; EPIRK4s3B: 2/3 on the phi_2 vector)
-    LX_TRY(stage_remainder(ctx, pb, rec, u, u, S1, epb ? 2.0 / 3.0 : 0.5, nullptr, 0.0, 1.0, dt, S0, hi));
+    // D_a = dt F(u + w_a p_a) - dt F(u)  -> S0   (w_a = 1/2; EPIRK4s3B: 2/3 on the phi_2 vector; EPIRK4s3: 1/8)
+    LX_TRY(stage_remainder(ctx, pb, rec, u, u, S1, epb ? 2.0 / 3.0 : e4s3 ? 0.125 : 0.5, nullptr, 0.0, 1.0, dt, S0, hi));
     double* Db;
     if (epirk) {
-        // D_b = dt F(u + w_b p_b) - dt F(u) -> S1   (w_b = 2/3; EPIRK4s3B: 1)
-        LX_TRY(stage_remainder(ctx, pb, rec, u, u, S2, epb ? 1.0 : 2.0 / 3.0, nullptr, 0.0, 1.0, dt, S1, hi));
+        // D_b = dt F(u + w_b p_b) - dt F(u) -> S1   (w_b = 2/3; EPIRK4s3B: 1; EPIRK4s3: 1/9)
+        LX_TRY(stage_remainder(ctx, pb, rec, u, u, S2, epb ? 1.0 : e4s3 ? 1.0 / 9.0 : 2.0 / 3.0, nullptr, 0.0, 1.0, dt,
+                               S1, hi));
         Db = S1;
     } else {
         // phi_1(hJ) D_a -> S1 ; b = u + p_one + S1 ; D_b -> lo
@@ -1438,8 +1443,10 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
     double* w3 = epirk ? S2 : S1;
     A = stage_args(ctx, pb, rec);
     A.x0 = S0; A.x1 = Db; A.y0 = w3; A.y1 = hi;
-    A.a0 = epb ? 54.0 : epirk ? 32.0 : 16.0; A.a1 = epb ? -16.0 : epirk ? -13.5 : -2.0;
-    A.a2 = epb ? -324.0 : epirk ? -144.0 : -48.0; A.a3 = epb ? 144.0 : epirk ? 81.0 : 12.0;
+    A.a0 = epb ? 54.0 : e4s3 ? -1024.0 : epirk ? 32.0 : 16.0;
+    A.a1 = epb ? -16.0 : e4s3 ? 1458.0 : epirk ? -13.5 : -2.0;
+    A.a2 = epb ? -324.0 : e4s3 ? 27648.0 : epirk ? -144.0 : -48.0;
+    A.a3 = epb ? 144.0 : e4s3 ? -34992.0 : epirk ? 81.0 : 12.0;
     LX_TRY(run_stage(ctx, ST_COMBINE2, A));
     // q3 -> S0 (D_a consumed); q4 -> S1 (EPIRK: D_b consumed) / lo (EXPRB43: D_b consumed)
     double* q3 = S0;
@@ -1461,7 +1468,7 @@ lx_status lx_step(lx_ctx* ctx, lx_method method, const lx_problem* pb0, const do
     const lx_problem* pb = &pbs;
     if (!ctx) return fail(LX_ERR_ARG, "ctx is NULL");
     LX_TRY(check_problem(ctx, pb));
-    if ((int)method < 0 || (int)method > 8) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
+    if ((int)method < 0 || (int)method > 9) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
     if (!u || !u_high) return fail(LX_ERR_ARG, "NULL argument");
     if (!nonembedded(method) && method != LX_EPIRK5P1 && !u_low)   // EPIRK5P1: u_low optional (R33)
         return fail(LX_ERR_ARG, "u_low required for embedded methods");
@@ -1501,6 +1508,7 @@ static int embedded_order(lx_method m) {
         case LX_EXPRB53S3: return 3;
         case LX_EPIRK5P1: return 4;   // reading R33
         case LX_EPIRK4S3B: return 3;  // reading R34
+        case LX_EPIRK4S3: return 3;   // reading R35
         case LX_EXPRB54S4: return 4;
         default: return 0;
     }
@@ -1572,7 +1580,7 @@ lx_status lx_integrate(lx_ctx* ctx, lx_method method, const lx_problem* pb0, dou
     lx_problem pbs = *pb0;
     const lx_problem* pb = &pbs;
     LX_TRY(check_problem(ctx, pb));
-    if ((int)method < 0 || (int)method > 8) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
+    if ((int)method < 0 || (int)method > 9) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
     if (nsteps < 0) return fail(LX_ERR_ARG, "nsteps < 0");
     if (!std::isfinite(dt)) return fail(LX_ERR_ARG, "dt not finite");
     Staging sg(ctx);
@@ -1992,27 +2000,29 @@ static lx_status bb_step(BbRun& R, lx_method method, const double* u, double* lo
         ctx->launches++;
         return LX_OK;
     }
-    // EXPRB43 / EPIRK4s3A (reading R17) / EPIRK4s3B (reading R34)
+    // EXPRB43 / EPIRK4s3A (reading R17) / EPIRK4s3B (reading R34) / EPIRK4s3 (reading R35)
     const bool epb = method == LX_EPIRK4S3B;
-    const bool epirk = method == LX_EPIRK4S3A || epb;
+    const bool e4s3 = method == LX_EPIRK4S3;
+    const bool epirk = method == LX_EPIRK4S3A || epb || e4s3;
     const double cf2[2] = {0.5, 1.0}, cf3[3] = {0.5, 2.0 / 3.0, 1.0}, cfb[2] = {0.5, 0.75};
-    double* pv[3] = {t[1], t[2], t[3]};
+    const double cf9[3] = {1.0 / 9.0, 1.0 / 8.0, 1.0};
+    double* pv[3] = {e4s3 ? t[2] : t[1], e4s3 ? t[1] : t[2], t[3]};   // EPIRK4s3: t1 <- 1/8, t2 <- 1/9
     if (epb) {
         LX_TRY(R.leja(f_u, pv, cfb, 2, dt, c, gamma, 2, rtol, atol));   // phi_2 {1/2, 3/4}
         double* o1[1] = {t[3]};
         LX_TRY(R.leja(f_u, o1, &one, 1, dt, c, gamma, 1, rtol, atol));
     } else {
-        LX_TRY(R.leja(f_u, pv, epirk ? cf3 : cf2, epirk ? 3 : 2, dt, c, gamma, 1, rtol, atol));
+        LX_TRY(R.leja(f_u, pv, e4s3 ? cf9 : epirk ? cf3 : cf2, epirk ? 3 : 2, dt, c, gamma, 1, rtol, atol));
     }
     double* p_half = t[1];
     double* p_one = epirk ? t[3] : t[2];
     double *NLu = t[4], *Da = t[5], *Db = t[6], *tmp = t[7];
     LX_TRY(R.remainder(u, NLu));
-    LX_TRY(R.comb(lo, 1.0, u, epb ? 2.0 / 3.0 : 0.5, p_half));   // a
+    LX_TRY(R.comb(lo, 1.0, u, epb ? 2.0 / 3.0 : e4s3 ? 0.125 : 0.5, p_half));   // a
     LX_TRY(R.remainder(lo, tmp));
     LX_TRY(R.comb(Da, dt, tmp, -dt, NLu));
     if (epirk) {
-        LX_TRY(R.comb(lo, 1.0, u, epb ? 1.0 : 2.0 / 3.0, t[2]));  // b
+        LX_TRY(R.comb(lo, 1.0, u, epb ? 1.0 : e4s3 ? 1.0 / 9.0 : 2.0 / 3.0, t[2]));  // b
     } else {
         double* o[1] = {hi};
         LX_TRY(R.leja(Da, o, &one, 1, dt, c, gamma, 1, rtol, atol));
@@ -2020,8 +2030,10 @@ static lx_status bb_step(BbRun& R, lx_method method, const double* u, double* lo
     }
     LX_TRY(R.remainder(lo, tmp));
     LX_TRY(R.comb(Db, dt, tmp, -dt, NLu));
-    const double a3 = epb ? 54.0 : epirk ? 32.0 : 16.0, b3 = epb ? -16.0 : epirk ? -13.5 : -2.0;
-    const double a4 = epb ? -324.0 : epirk ? -144.0 : -48.0, b4 = epb ? 144.0 : epirk ? 81.0 : 12.0;
+    const double a3 = epb ? 54.0 : e4s3 ? -1024.0 : epirk ? 32.0 : 16.0;
+    const double b3 = epb ? -16.0 : e4s3 ? 1458.0 : epirk ? -13.5 : -2.0;
+    const double a4 = epb ? -324.0 : e4s3 ? 27648.0 : epirk ? -144.0 : -48.0;
+    const double b4 = epb ? 144.0 : e4s3 ? -34992.0 : epirk ? 81.0 : 12.0;
     LX_TRY(R.comb(tmp, a3, Da, b3, Db));              // w3
     LX_TRY(R.comb(NLu, a4, Da, b4, Db));              // w4
     double* o3[1] = {Da};
@@ -2095,7 +2107,7 @@ lx_status lx_step_cb(lx_ctx* ctx, lx_method method, lx_rhs_fn f, void* user, con
                      double* u_high, double* err_out, double dt, double c, double gamma, double rtol, double atol,
                      int* iters_out) {
     if (!ctx || !f || !u || !u_high) return fail(LX_ERR_ARG, "NULL argument");
-    if ((int)method < 0 || (int)method > 8) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
+    if ((int)method < 0 || (int)method > 9) return fail(LX_ERR_UNKNOWN_INTEGRATOR, "unknown integrator %d", (int)method);
     if (!nonembedded(method) && method != LX_EPIRK5P1 && !u_low)   // EPIRK5P1: u_low optional (R33)
         return fail(LX_ERR_ARG, "u_low required for embedded methods");
     if (u_low == u || u_high == u) return fail(LX_ERR_ALIAS, "outputs must not alias u");

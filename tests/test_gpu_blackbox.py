@@ -121,7 +121,7 @@ def test_fd_leja_torch_callback(xi300):
 
 
 @pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3", "exprb54s4",
-                                    "epirk4s3b"])
+                                    "epirk4s3b", "epirk4s3"])
 def test_fd_steps_allen_cahn(xi300, method):
     n = 64
     pb, ob = _pair((n, n), diff=1e-4, nu=0.0, react=1.0)
@@ -188,5 +188,5 @@ def test_blackbox_errors():
             lx.lx_real_leja_phi_cb(ctx, lx.Rhs.builtin(ctx), v, [v], [1.0], 1e-4, -1.0, 1.0, 1, TOL, TOL)
         assert e.value.status == lx.LX_ERR_ALIAS
         with pytest.raises(lx.LxError) as e:
-            lx.lx_step_cb(ctx, 9, lx.Rhs.builtin(ctx), v, out, out, 1e-4, -1.0, 1.0, TOL, TOL)
+            lx.lx_step_cb(ctx, 10, lx.Rhs.builtin(ctx), v, out, out, 1e-4, -1.0, 1.0, TOL, TOL)
         assert e.value.status == lx.LX_ERR_UNKNOWN_INTEGRATOR

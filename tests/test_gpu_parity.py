@@ -148,7 +148,7 @@ def test_argument_errors():
             lx.lx_real_leja_phi(ctx, v, torch.empty_like(v), 1e-3, -1.0, -1.0, 1, TOL, TOL)
         assert e.value.status == lx.LX_ERR_ARG
         with pytest.raises(lx.LxError) as e:
-            lx.lx_step(ctx, 9, v, torch.empty_like(v), torch.empty_like(v), 1e-3, -1.0, 1.0, TOL, TOL)
+            lx.lx_step(ctx, 10, v, torch.empty_like(v), torch.empty_like(v), 1e-3, -1.0, 1.0, TOL, TOL)
         assert e.value.status == lx.LX_ERR_UNKNOWN_INTEGRATOR
     with pytest.raises(lx.LxError) as e:
         lx.Context(lx.Problem((16, 15), (0.1, 0.1)))
@@ -209,7 +209,7 @@ def test_power_iteration_and_rhs(xi300):
 
 # ---------------------------------------------------------------- integrators
 @pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3", "exprb54s4",
-                                    "epirk4s3b"])
+                                    "epirk4s3b", "epirk4s3"])
 def test_steps_linear_advdiff(xi300, method):
     n = 64
     pb, ob = _pair((n, n))
@@ -228,7 +228,7 @@ def test_steps_linear_advdiff(xi300, method):
 
 
 @pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3", "exprb54s4",
-                                    "epirk4s3b"])
+                                    "epirk4s3b", "epirk4s3"])
 def test_steps_allen_cahn(xi300, method):
     n = 128
     pb, ob = _pair((n, n), diff=1e-4, nu=0.0, react=1.0)
@@ -308,7 +308,7 @@ def test_leja_3d(xi300, shape):
         assert est == pytest.approx(O.power_iteration(ob, None, 20), rel=1e-10)
 
 
-@pytest.mark.parametrize("method", ["epirk4s3a", "exprb43", "epirk4s3b"])
+@pytest.mark.parametrize("method", ["epirk4s3a", "exprb43", "epirk4s3b", "epirk4s3"])
 def test_steps_3d(xi300, method):
     n = 32
     shape = (n, n, n)
@@ -339,7 +339,7 @@ def test_steps_3d(xi300, method):
 
 
 @pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3", "exprb54s4",
-                                    "epirk4s3b"])
+                                    "epirk4s3b", "epirk4s3"])
 def test_integrate_device_spectrum(xi300, method):
     # lx_integrate: the paper's time loop with (c, gamma) recomputed ON THE DEVICE every
     # step; the oracle recomputes them from its own state with the same formula (R16).
@@ -399,7 +399,7 @@ def _burgers_pair(n, beta=10.0):
 
 
 @pytest.mark.parametrize("method", ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3", "exprb54s4",
-                                    "epirk4s3b"])
+                                    "epirk4s3b", "epirk4s3"])
 def test_burgers_steps(xi300, method):
     n = 128
     pb, ob = _burgers_pair(n)
@@ -739,7 +739,7 @@ def test_pinned_host_pipelined_leja_calls(xi300):
 
 
 @pytest.mark.parametrize("method", ["exprb32", "exprb43", "epirk4s3a", "exprb53s3", "exprb54s4", "epirk5p1",
-                                    "epirk4s3b"])
+                                    "epirk4s3b", "epirk4s3"])
 def test_adaptive_step_size_control(xi300, method):
     # lx_integrate_adaptive vs the oracle's controller (reading R32): the same accept / reject sequence, the
     # same step sizes (they depend on err^(1/(q+1)); err agrees to rounding), the same final state
@@ -753,9 +753,12 @@ def test_adaptive_step_size_control(xi300, method):
         u = _dev(u0)
         acc, rej, dts, errs, its = lx.lx_integrate_adaptive(ctx, method, u, t_end, dt0, tol, 1e-12, 1e-12)
     assert (acc, rej) == (ref.accepted, ref.rejected)
-    np.testing.assert_allclose(dts, ref.dts, rtol=1e-8)
+    # EPIRK4s3's embedded error is phi_4 of 27648 D_a - 34992 D_b (R35): the cancellation turns rounding-level
+    # differences of D into ~1e-7 relative differences of err (~2e-8 of the step sizes, err^(1/4))
+    big = method == "epirk4s3"
+    np.testing.assert_allclose(dts, ref.dts, rtol=1e-7 if big else 1e-8)
     fin = np.isfinite(ref.errs)
     assert np.array_equal(np.isfinite(errs), fin)
-    np.testing.assert_allclose(errs[fin], ref.errs[fin], rtol=1e-6, atol=1e-15)
+    np.testing.assert_allclose(errs[fin], ref.errs[fin], rtol=1e-5 if big else 1e-6, atol=1e-15)
     assert its == ref.iters
     assert _rel(u, ref.u) <= 1e-9

@@ -96,7 +96,7 @@ def test_slab_leja_matches_oracle_and_single_domain(xi300, P, shape):
 
 
 @pytest.mark.parametrize("method", ["exprb32", "exprb43", "epirk4s3a", "epirk5p1", "exprb53s3", "exprb54s4",
-                                    "epirk4s3b"])
+                                    "epirk4s3b", "epirk4s3"])
 def test_slab_steps_allen_cahn(xi300, method):
     P, shape = 2, (96, 64)
     dx = tuple(2.0 / n for n in shape)
