@@ -1424,13 +1424,35 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
                            atol, rec));
     }
     double* p_one = epirk ? S3 : S2;
+    const double wa = epb ? 2.0 / 3.0 : e4s3 ? 0.125 : 0.5, wb = epb ? 1.0 : e4s3 ? 1.0 / 9.0 : 2.0 / 3.0;
+    const double c3a = epb ? 54.0 : e4s3 ? -1024.0 : epirk ? 32.0 : 16.0;
+    const double c3b = epb ? -16.0 : e4s3 ? 1458.0 : epirk ? -13.5 : -2.0;
+    const double c4a = epb ? -324.0 : e4s3 ? 27648.0 : epirk ? -144.0 : -48.0;
+    const double c4b = epb ? 144.0 : e4s3 ? -34992.0 : epirk ? 81.0 : 12.0;
+    if (epirk && pb->flux == 0.0) {
+        // independent stages a, b: both remainders and the final stage's two combinations in ONE pointwise
+        // kernel (D_a, D_b stay in registers): w3 -> S0 (f dt consumed), w4 -> hi
+        A = stage_args(ctx, pb, rec);
+        A.dt = dt;
+        A.u = u;
+        A.x1 = S1; A.x2 = S2; A.a0 = wa; A.a1 = wb;
+        A.a2 = c3a; A.a3 = c3b; A.a4 = c4a; A.a5 = c4b;
+        A.y0 = S0; A.y1 = hi;
+        LX_TRY(run_stage(ctx, ST_REM2_W34, A));
+        double* o3[1] = {S1};   // q3 (p_a consumed)
+        LX_TRY(leja_device(ctx, pb, ul, S0, o3, &one, 1, dt, c, gamma, 3, rtol, atol, rec));
+        double* o4[1] = {S2};   // q4 (p_b consumed)
+        LX_TRY(leja_device(ctx, pb, ul, hi, o4, &one, 1, dt, c, gamma, 4, rtol, atol, rec));
+        A = stage_args(ctx, pb, rec);   // u3 = u + p_one + q3 -> lo ; u4 = u3 + q4 -> hi ; err = ||u4 - u3||
+        A.x0 = u; A.x1 = p_one; A.x2 = S1; A.x3 = S2; A.y0 = lo; A.y1 = hi;
+        return run_stage(ctx, ST_FINAL4, A);
+    }
     // D_a = dt F(u + w_a p_a) - dt F(u)  -> S0   (w_a = 1/2; EPIRK4s3B: 2/3 on the phi_2 vector; EPIRK4s3: 1/8)
-    LX_TRY(stage_remainder(ctx, pb, rec, u, u, S1, epb ? 2.0 / 3.0 : e4s3 ? 0.125 : 0.5, nullptr, 0.0, 1.0, dt, S0, hi));
+    LX_TRY(stage_remainder(ctx, pb, rec, u, u, S1, wa, nullptr, 0.0, 1.0, dt, S0, hi));
     double* Db;
     if (epirk) {
         // D_b = dt F(u + w_b p_b) - dt F(u) -> S1   (w_b = 2/3; EPIRK4s3B: 1; EPIRK4s3: 1/9)
-        LX_TRY(stage_remainder(ctx, pb, rec, u, u, S2, epb ? 1.0 : e4s3 ? 1.0 / 9.0 : 2.0 / 3.0, nullptr, 0.0, 1.0, dt,
-                               S1, hi));
+        LX_TRY(stage_remainder(ctx, pb, rec, u, u, S2, wb, nullptr, 0.0, 1.0, dt, S1, hi));
         Db = S1;
     } else {
         // phi_1(hJ) D_a -> S1 ; b = u + p_one + S1 ; D_b -> lo
@@ -1443,10 +1465,7 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
     double* w3 = epirk ? S2 : S1;
     A = stage_args(ctx, pb, rec);
     A.x0 = S0; A.x1 = Db; A.y0 = w3; A.y1 = hi;
-    A.a0 = epb ? 54.0 : e4s3 ? -1024.0 : epirk ? 32.0 : 16.0;
-    A.a1 = epb ? -16.0 : e4s3 ? 1458.0 : epirk ? -13.5 : -2.0;
-    A.a2 = epb ? -324.0 : e4s3 ? 27648.0 : epirk ? -144.0 : -48.0;
-    A.a3 = epb ? 144.0 : e4s3 ? -34992.0 : epirk ? 81.0 : 12.0;
+    A.a0 = c3a; A.a1 = c3b; A.a2 = c4a; A.a3 = c4b;
     LX_TRY(run_stage(ctx, ST_COMBINE2, A));
     // q3 -> S0 (D_a consumed); q4 -> S1 (EPIRK: D_b consumed) / lo (EXPRB43: D_b consumed)
     double* q3 = S0;

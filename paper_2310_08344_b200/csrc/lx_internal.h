@@ -223,7 +223,7 @@ struct StageArgs {
     const double* u;      // state
     const double* x0; const double* x1; const double* x2; const double* x3;
     double* y0; double* y1;
-    double a0, a1, a2, a3;
+    double a0, a1, a2, a3, a4, a5;
     double dt;
     double* partials;     // [grid][kSlot]
     Ctrl* ctrl;
@@ -246,6 +246,8 @@ enum StageOp {
     ST_LIN3,              // y0 = x0 + a0*x1 + a1*x2
     ST_LIN4,              // y0 = x0 + a0*x1 + a1*x2 + a2*x3
     ST_LIN4_ERR,          // y0 = x0 + a0*x1 + a1*x2 + a2*x3 ; err = ||y0 - y1|| (y1 read: the embedded solution)
+    ST_REM2_W34,          // D_a = dt F(u + a0 x1) - dt F(u), D_b = dt F(u + a1 x2) - dt F(u) (not stored);
+                          // y0 = a2 D_a + a3 D_b, y1 = a4 D_a + a5 D_b  (two-stage EPIRK final-stage inputs)
 };
 cudaError_t launch_stage(int op, const StageArgs& A, cudaStream_t s);
 cudaError_t launch_rhs(const LejaParams& P, double scale, cudaStream_t s);
