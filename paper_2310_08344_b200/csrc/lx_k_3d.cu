@@ -339,27 +339,27 @@ __device__ __forceinline__ void bar_a() { asm volatile("bar.sync 1, 256;" ::: "m
 // A y (before the alpha / beta scaling) at the two columns of a pair, k_leja3d_smem's FMA order
 __device__ __forceinline__ double2 b3_apply(const Stencil& S, double2 yc, double2 up, double2 dn1, double2 dn2,
                                             double2 wm, double2 wp1, double2 wp2, double left, double2 rt) {
-    double ax = S.c0 * yc.x;
-    ax = fma(S.m1[0], up.x, ax);
-    ax = fma(S.p1[0], dn1.x, ax);
-    ax = fma(S.p2[0], dn2.x, ax);
-    ax = fma(S.m1[1], wm.x, ax);
-    ax = fma(S.p1[1], wp1.x, ax);
-    ax = fma(S.p2[1], wp2.x, ax);
-    ax = fma(S.m1[2], left, ax);
-    ax = fma(S.p1[2], yc.y, ax);
-    ax = fma(S.p2[2], rt.x, ax);
-    double ay = S.c0 * yc.y;
-    ay = fma(S.m1[0], up.y, ay);
-    ay = fma(S.p1[0], dn1.y, ay);
-    ay = fma(S.p2[0], dn2.y, ay);
-    ay = fma(S.m1[1], wm.y, ay);
-    ay = fma(S.p1[1], wp1.y, ay);
-    ay = fma(S.p2[1], wp2.y, ay);
-    ay = fma(S.m1[2], yc.x, ay);
-    ay = fma(S.p1[2], rt.x, ay);
-    ay = fma(S.p2[2], rt.y, ay);
-    return make_double2(ax, ay);
+    // the 10 stencil terms summed per direction, then the three direction sums (dependent chain 6 deep
+    // instead of 10: stage B, the kernel's critical path, is latency-bound on it)
+    double x0 = fma(S.m1[0], up.x, S.c0 * yc.x);
+    x0 = fma(S.p1[0], dn1.x, x0);
+    x0 = fma(S.p2[0], dn2.x, x0);
+    double x1 = S.m1[1] * wm.x;
+    x1 = fma(S.p1[1], wp1.x, x1);
+    x1 = fma(S.p2[1], wp2.x, x1);
+    double x2 = S.m1[2] * left;
+    x2 = fma(S.p1[2], yc.y, x2);
+    x2 = fma(S.p2[2], rt.x, x2);
+    double y0 = fma(S.m1[0], up.y, S.c0 * yc.y);
+    y0 = fma(S.p1[0], dn1.y, y0);
+    y0 = fma(S.p2[0], dn2.y, y0);
+    double y1 = S.m1[1] * wm.y;
+    y1 = fma(S.p1[1], wp1.y, y1);
+    y1 = fma(S.p2[1], wp2.y, y1);
+    double y2 = S.m1[2] * yc.x;
+    y2 = fma(S.p1[2], rt.x, y2);
+    y2 = fma(S.p2[2], rt.y, y2);
+    return make_double2(x0 + (x1 + x2), y0 + (y1 + y2));
 }
 
 // Per-pass coefficients (shared memory): d_m, d_{m+1}, d_0 (first pass), d_{m-1} (rollback)
