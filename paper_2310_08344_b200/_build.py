@@ -37,6 +37,8 @@ def _nccl_dir():
 def _flags():
     f = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+    # build-time extras (the bounds-checked debug build of tools/debug_bounds.sh: -DLX_DEBUG_BOUNDS)
+    f += [x for x in os.environ.get("NVCC_EXTRA", "").split() if x]
     nccl = _nccl_dir()
     if nccl:
         f += ["-I", nccl[0], "-DLX_HAVE_NCCL=1"]

@@ -13,6 +13,23 @@ namespace lx {
 
 #define FULL_MASK 0xffffffffu
 
+// Bounds checks of the debug build (-DLX_DEBUG_BOUNDS; tools/debug_bounds.sh): a failed check prints the
+// site and traps.  Compiled out of the product build.
+#ifdef LX_DEBUG_BOUNDS
+#define LX_DCHECK(cond, what)                                                                              \
+    do {                                                                                                   \
+        if (!(cond)) {                                                                                     \
+            printf("LX_DCHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__, blockIdx.x, \
+                   threadIdx.x);                                                                           \
+            __trap();                                                                                      \
+        }                                                                                                  \
+    } while (0)
+#else
+#define LX_DCHECK(cond, what) \
+    do {                      \
+    } while (0)
+#endif
+
 __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 __device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
 __device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }

@@ -469,9 +469,12 @@ __device__ __forceinline__ void b3_stage_b(const LejaParams& P, const B3Coef<K>&
         yn.x = fma(alpha, ax.x, bb * yc.x);
         yn.y = fma(alpha, ax.y, bb * yc.y);
         const long long off = off0 + r * rstride;
+        LX_DCHECK(off >= 0 && off + 2 <= (long long)P.n_loc * P.n1 * P.n2, "stage B output offset");
         if (!two) yn = yc;   // one-iteration pass: y_m is the next pass's input
         st2(dst + off, yn);
         if (SLAB) {   // a boundary plane of y_{m+1}: also into the neighbour's ghost block (peer memory)
+            LX_DCHECK(!x1 || off < 4 * (long long)P.n1 * P.n2, "ghost delivery up: plane < 4");
+            LX_DCHECK(!x2 || off >= ((long long)P.n_loc - 2) * P.n1 * P.n2, "ghost delivery down: plane >= n-2");
             if (x1) st2(x1 + off, yn);
             if (x2) st2(x2 + off, yn);
         }
@@ -571,12 +574,16 @@ __device__ __forceinline__ void b3_unit(const LejaParams& P, const double* __res
             const double* base;
             if (SLAB && (unsigned)pl >= (unsigned)n0) base = gsrc + (long long)(pl < 0 ? pl + 2 : pl - n0 + 2) * plane;
             else base = src + (long long)pl * plane;
+            LX_DCHECK(SLAB ? (pl >= -2 && pl < n0 + 4) : (pl >= 0 && pl < n0), "stage A plane index");
             const uint32_t sb = b1 + (uint32_t)slot * SL1;
+            LX_DCHECK(slot >= 0 && slot < kB3D, "stage A ring slot");
 #pragma unroll
             for (int q = 0; q < kB3PPT; q++)
-                if (goff[q] >= 0)
+                if (goff[q] >= 0) {
+                    LX_DCHECK(goff[q] + 2 <= plane && soff[q] + 16 <= SL1, "stage A piece offsets");
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + soff[q]), "l"(base + goff[q])
                                  : "memory");
+                }
             pl = SLAB ? pl + 1 : b3_inc(pl, n0);
         };
 #pragma unroll 1
@@ -649,6 +656,7 @@ __device__ __forceinline__ void b3_unit(const LejaParams& P, const double* __res
 #pragma unroll
             for (int r = 0; r < 2; r++) {
                 const long long o = off + r * rstride;
+                LX_DCHECK(o >= 0 && o + 2 <= (long long)n0 * plane, "stage B staging offset");
                 if (FIRST || rbm)
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + (uint32_t)((r * (K + 1) + K) * 4096)),
                                  "l"(src + o)
@@ -818,6 +826,7 @@ __device__ __forceinline__ void b3_slab_prologue(const LejaParams& P, unsigned g
         const int pr = (int)(t / half);
         const long long o = 2 * (t - pr * half);
         const int src = pr < 4 ? pr : n - 6 + pr;
+        LX_DCHECK(src >= 0 && src < n && o + 2 <= plane, "slab prologue plane");
         double* g = pr < 4 ? P.hup_v + (2 + pr) * plane : P.hdn_v + (pr - 4) * plane;
         st2(g + o, ld2(P.v.base + src * plane + o));
     }
