@@ -304,7 +304,8 @@ __device__ __forceinline__ unsigned long long tb2_wait_dec(const LejaParams& P, 
     if (dec_tag(w) == tag) return w;
     const unsigned long long t0 = globaltimer_ns();
     for (int spins = 0;; spins++) {
-        __nanosleep(64);
+        // back off (64 ns .. 512 ns): idle waiters leave issue slots and L2 to the warps still working
+        __nanosleep(spins < 8 ? 64 : 512);
         w = ld_acquire64(&tc->dec[q & 1]);
         if (dec_tag(w) == tag) return w;
         if ((spins & 15) == 15 && tb2_ended_before(P, pbase, q)) return kDecStop;
