@@ -274,6 +274,20 @@ lx_status lx_real_leja_phi_vertical(lx_ctx *ctx, const lx_problem *pb, const dou
                                     int K, double dt, double c, double gamma, int l, double rtol,
                                     double atol, int *iters_out);
 
+/* Several phi functions of one vector in one interpolation: outs[k] ~= phi_{ls[k]}(coeffs[k] dt J(u)) v.
+ * The Newton basis y_m ((J - cI)/gamma - xi_m I applied to v, Eq. (2)) does not depend on l,
+ * so K accumulators with their own divided differences (h(xi) = phi_{l_k}(a_k dt (c +
+ * gamma xi))) share it, exactly as the vertical interpolation shares it across coefficients: each
+ * accumulator stops at the iteration P:155 gives it, bitwise the output and iteration count of its own
+ * lx_real_leja_phi / _vertical call; *iters_out = steps until all K converged.  Typical use: phi_0 .. phi_3
+ * of the same v, or an EPIRK stage's phi_2 {1/2, 3/4} and phi_1 {1} on the same f (R34).
+ * ls[k] in [0, 4], coeffs[k] in (0, 1], (ls[k], coeffs[k]) pairs distinct, K in [1, 4]; otherwise as
+ * lx_real_leja_phi_vertical (host buffers staged, NULL iters_out = asynchronous).
+ * Errors: LX_ERR_ARG, LX_ERR_UNSUPPORTED, LX_ERR_ALIAS, LX_ERR_NOCONV, LX_ERR_NONFINITE, LX_ERR_CUDA. */
+lx_status lx_real_leja_phi_multi(lx_ctx *ctx, const lx_problem *pb, const double *u_lin, const double *v,
+                                 double *const *outs, const int *ls, const double *coeffs, int K, double dt,
+                                 double c, double gamma, double rtol, double atol, int *iters_out);
+
 /* ------------------------------------------------------------------------ */
 /* Exponential integrator steps (listings alg:Ros_Eu, alg:exprb32; */
 /* EXPRB43 / EPIRK4s3A tableaux from the papers cited at P:83).              */

@@ -46,7 +46,8 @@ EXPORTS = ("lx_last_error", "lx_version", "lx_leja_points", "lx_phi_scalar", "lx
            "lx_step_exprb42", "lx_step_epirk5p1",
            "lx_step", "lx_rhs", "lx_integrate", "lx_local_group_create", "lx_local_group_destroy", "lx_ctx_set_comm_local",
            "lx_real_leja_phi_cb", "lx_step_cb", "lx_builtin_rhs", "lx_ctx_set_comm_ex", "lx_ctx_set_comm_local_ex",
-           "lx_ctx_ipc_handle", "lx_ctx_set_comm_ipc", "lx_ctx_set_kernel", "lx_slab_halo_plan", "lx_integrate_adaptive")
+           "lx_ctx_ipc_handle", "lx_ctx_set_comm_ipc", "lx_ctx_set_kernel", "lx_slab_halo_plan", "lx_integrate_adaptive",
+           "lx_real_leja_phi_multi")
 
 # void f(const double* in, double* out, void* user, void* cuda_stream)  (include/lexint.h lx_rhs_fn)
 RHS_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
@@ -125,6 +126,8 @@ def lib() -> ctypes.CDLL:
             "lx_real_leja_phi": (ctypes.c_int, [vp, pbp, vp, vp, vp, d, d, d, ctypes.c_int, d, d, ip]),
             "lx_real_leja_phi_vertical": (ctypes.c_int, [vp, pbp, vp, vp, ctypes.POINTER(vp), dp, ctypes.c_int,
                                                          d, d, d, ctypes.c_int, d, d, ip]),
+            "lx_real_leja_phi_multi": (ctypes.c_int, [vp, pbp, vp, vp, ctypes.POINTER(vp), ip, dp, ctypes.c_int,
+                                                      d, d, d, d, d, ip]),
             "lx_step": (ctypes.c_int, [vp, ctypes.c_int, pbp, vp, vp, vp, dp, d, d, d, d, d, ip]),
             "lx_step_rosenbrock_euler": (ctypes.c_int, [vp, pbp, vp, vp, d, d, d, d, d, ip]),
             "lx_step_exprb32": (ctypes.c_int, [vp, pbp, vp, vp, vp, dp, d, d, d, d, d, ip]),
@@ -372,6 +375,21 @@ def lx_real_leja_phi_vertical(ctx: Context, v, outs: Sequence, coeffs: Sequence[
     st = lib().lx_real_leja_phi_vertical(ctx.handle, _pb(ctx, problem), _ptr(u_lin), _ptr(v), arr, cf, K,
                                          float(dt), float(c), float(gamma), int(l), float(rtol), float(atol),
                                          ctypes.byref(it) if sync else None)
+    _check(st, it.value)
+    return it.value if sync else None
+
+
+def lx_real_leja_phi_multi(ctx: Context, v, outs: Sequence, ls: Sequence[int], coeffs: Sequence[float], dt, c, gamma,
+                           rtol, atol, u_lin=None, problem: Problem | None = None, sync: bool = True):
+    """outs[k] = phi_{ls[k]}(coeffs[k] dt J) v, one shared Newton basis (lexint.h)."""
+    K = len(outs)
+    arr = (ctypes.c_void_p * K)(*[_ptr(o) for o in outs])
+    li = (ctypes.c_int * K)(*[int(x) for x in ls])
+    cf = (ctypes.c_double * K)(*[float(a) for a in coeffs])
+    it = ctypes.c_int(0)
+    st = lib().lx_real_leja_phi_multi(ctx.handle, _pb(ctx, problem), _ptr(u_lin), _ptr(v), arr, li, cf, K,
+                                      float(dt), float(c), float(gamma), float(rtol), float(atol),
+                                      ctypes.byref(it) if sync else None)
     _check(st, it.value)
     return it.value if sync else None
 

@@ -110,7 +110,7 @@ __device__ __forceinline__ double P_alpha(const LejaParams& P) {
 }
 
 __device__ __forceinline__ double coef_h(const LejaParams& P, int k, int j) {
-    return phi_dev(P.l, coef_arg(P.ak[k], P.cdt, P_c(P), P_g(P), P.xi[j]));
+    return phi_dev(P.lk[k], coef_arg(P.ak[k], P.cdt, P_c(P), P_g(P), P.xi[j]));
 }
 
 // one step of the recurrence: (d - d_i) * 1/(xi_j - xi_i), explicitly rounded
@@ -1001,6 +1001,8 @@ __device__ __forceinline__ unsigned long long tb2_call_key(const LejaParams& P) 
     };
     mix((unsigned long long)P.l | ((unsigned long long)K << 8) | ((unsigned long long)P.max_nodes << 16) |
         ((unsigned long long)P.active0 << 40));
+#pragma unroll
+    for (int k = 0; k < K; k++) mix((unsigned long long)P.lk[k]);
     mix((unsigned long long)__double_as_longlong(P.cdt));
     mix((unsigned long long)__double_as_longlong(P_c(P)));
     mix((unsigned long long)__double_as_longlong(P_g(P)));

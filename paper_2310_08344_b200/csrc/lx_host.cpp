@@ -411,10 +411,11 @@ static lx_status tb2_setup(lx_ctx* ctx, LejaParams& P, int K, bool diag) {
 // The 3D kernels read the Newton coefficients from a table built by one k_coef_tables launch.
 static lx_status leja3d_table(lx_ctx* ctx, LejaParams& P, int K, int l, const double* coeffs, double dt, double c,
                               double gamma, int rec) {
+    (void)l;
     if (!P.coef_gen) return LX_OK;
     CoefJobs jobs;
     std::memset(&jobs, 0, sizeof jobs);
-    for (int k = 0; k < K; k++) jobs.j[jobs.n++] = CoefJob{P.table, coeffs[k], l, K, k};
+    for (int k = 0; k < K; k++) jobs.j[jobs.n++] = CoefJob{P.table, coeffs[k], P.lk[k], K, k};
     CUDA_TRY(launch_coef_tables(ctx->xi_dev, ctx->rcp_dev, ctx->max_nodes, jobs, dt, c, gamma, ctx->cg_active,
                                 &ctx->rec_dev[rec].status, ctx->stream));
     ctx->launches++;
@@ -424,12 +425,13 @@ static lx_status leja3d_table(lx_ctx* ctx, LejaParams& P, int K, int l, const do
 
 static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u, const double* v, double* const* outs,
                              const double* coeffs, int K, double dt, double c, double gamma, int l, double rtol,
-                             double atol, int rec, const double* table = nullptr) {
+                             double atol, int rec, const double* table = nullptr, const int* ls = nullptr) {
     const double* coef = table;
     LejaParams P = base_params(ctx, pb);
     const bool diag = pb->react != 0.0;
-    // coefficient description (read by the prologue of every Leja kernel)
+    // coefficient description (read by the prologue of every Leja kernel); ls: one phi index per accumulator
     P.l = l;
+    for (int k = 0; k < kMaxK; k++) P.lk[k] = (ls && k < K) ? ls[k] : l;
     P.cdt = dt;
     P.cc = c;
     P.cgamma = gamma;
@@ -512,15 +514,20 @@ static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u,
 }
 
 static lx_status validate_leja(const lx_problem* pb, const double* u, const double* v, double* const* outs,
-                               const double* coeffs, int K, double dt, double gamma, int l) {
+                               const double* coeffs, int K, double dt, double gamma, int l, const int* ls = nullptr) {
     if (!v || !outs || !coeffs) return fail(LX_ERR_ARG, "NULL argument");
     if (K < 1 || K > kMaxK) return fail(LX_ERR_UNSUPPORTED, "K = %d not in [1, 4]", K);
-    if (l < 0 || l > 4) return fail(LX_ERR_UNSUPPORTED, "phi_%d not supported (l <= 4)", l);
+    for (int k = 0; k < (ls ? K : 1); k++) {
+        const int lk = ls ? ls[k] : l;
+        if (lk < 0 || lk > 4) return fail(LX_ERR_UNSUPPORTED, "phi_%d not supported (l <= 4)", lk);
+    }
     if (!(gamma > 0.0) && dt != 0.0) return fail(LX_ERR_ARG, "gamma must be > 0 (got %g)", gamma);
     if (!std::isfinite(dt)) return fail(LX_ERR_ARG, "dt not finite");
     for (int k = 0; k < K; k++) {
         if (!(coeffs[k] > 0.0 && coeffs[k] <= 1.0)) return fail(LX_ERR_ARG, "coeffs[%d] not in (0, 1]", k);
-        if (k > 0 && !(coeffs[k] > coeffs[k - 1])) return fail(LX_ERR_ARG, "coeffs not strictly increasing");
+        if (!ls && k > 0 && !(coeffs[k] > coeffs[k - 1])) return fail(LX_ERR_ARG, "coeffs not strictly increasing");
+        for (int j = 0; ls && j < k; j++)
+            if (ls[j] == ls[k] && coeffs[j] == coeffs[k]) return fail(LX_ERR_ARG, "(l, coeff) pairs must be distinct");
         if (!outs[k]) return fail(LX_ERR_ARG, "outs[%d] is NULL", k);
         if (outs[k] == v || (u && outs[k] == u)) return fail(LX_ERR_ALIAS, "out must not alias v or u_lin");
         for (int j = 0; j < k; j++)
@@ -941,7 +948,7 @@ lx_status lx_ctx_set_kernel(lx_ctx* ctx, int iterations_per_pass, int kernel3d) 
 // returns at once -- the caller must not touch its host buffers before lx_ctx_synchronize.
 static lx_status leja_pipelined(lx_ctx* ctx, const lx_problem* pb, const double* ud, const double* v,
                                 double* const* outs, const double* coeffs, int K, double dt, double c, double gamma,
-                                int l, double rtol, double atol, int* iters_out) {
+                                int l, double rtol, double atol, int* iters_out, const int* ls = nullptr) {
     const size_t bytes = ctx->N_loc * sizeof(double);
     if (!ctx->s_in) {
         CUDA_TRY(cudaStreamCreateWithFlags(&ctx->s_in, cudaStreamNonBlocking));
@@ -990,7 +997,7 @@ static lx_status leja_pipelined(lx_ctx* ctx, const lx_problem* pb, const double*
     const bool sync = iters_out != nullptr;
     const int rec = sync ? 0 : 1;
     if (sync) LX_TRY(reset_record(ctx, 0));
-    LX_TRY(leja_device(ctx, pb, ud, vd, od, coeffs, K, dt, c, gamma, l, rtol, atol, rec));
+    LX_TRY(leja_device(ctx, pb, ud, vd, od, coeffs, K, dt, c, gamma, l, rtol, atol, rec, nullptr, ls));
     CUDA_TRY(cudaEventRecord(ctx->ev_comp[sl], ctx->stream));
     if (vhost) CUDA_TRY(cudaEventRecord(ctx->ev_comp[ctx->pin_key_slot], ctx->stream));   // input slot in use
     CUDA_TRY(cudaStreamWaitEvent(ctx->s_out, ctx->ev_comp[sl], 0));
@@ -1006,12 +1013,11 @@ static lx_status leja_pipelined(lx_ctx* ctx, const lx_problem* pb, const double*
     return status_of(r);
 }
 
-lx_status lx_real_leja_phi_vertical(lx_ctx* ctx, const lx_problem* pb, const double* u_lin, const double* v,
-                                    double* const* outs, const double* coeffs, int K, double dt, double c,
-                                    double gamma, int l, double rtol, double atol, int* iters_out) {
-    if (!ctx) return fail(LX_ERR_ARG, "ctx is NULL");
-    LX_TRY(check_problem(ctx, pb));
-    LX_TRY(validate_leja(pb, u_lin, v, outs, coeffs, K, dt, gamma, l));
+// Leja call on a validated request: host-buffer pipelining, staging, one device call, record read-back.
+// ls: per-accumulator phi index (lx_real_leja_phi_multi) or NULL (every accumulator phi_l).
+static lx_status leja_api(lx_ctx* ctx, const lx_problem* pb, const double* u_lin, const double* v, double* const* outs,
+                          const double* coeffs, int K, double dt, double c, double gamma, int l, double rtol,
+                          double atol, int* iters_out, const int* ls) {
     if (pb->react == 0.0 && pb->flux == 0.0) u_lin = nullptr;
     {
         // host buffers in PINNED memory (v and/or outputs; u_lin on the device): pipelined staging --
@@ -1023,7 +1029,7 @@ lx_status lx_real_leja_phi_vertical(lx_ctx* ctx, const lx_problem* pb, const dou
             pinned = pinned && (!h || is_pinned_host_ptr(outs[k]));
         }
         if (host && pinned && (!u_lin || is_device_ptr(u_lin)))
-            return leja_pipelined(ctx, pb, u_lin, v, outs, coeffs, K, dt, c, gamma, l, rtol, atol, iters_out);
+            return leja_pipelined(ctx, pb, u_lin, v, outs, coeffs, K, dt, c, gamma, l, rtol, atol, iters_out, ls);
     }
     Staging sg(ctx);
     const double *vd, *ud;
@@ -1034,13 +1040,31 @@ lx_status lx_real_leja_phi_vertical(lx_ctx* ctx, const lx_problem* pb, const dou
     const bool sync = iters_out != nullptr || sg.any_host;
     const int rec = sync ? 0 : 1;
     if (sync) LX_TRY(reset_record(ctx, 0));
-    LX_TRY(leja_device(ctx, pb, ud, vd, od, coeffs, K, dt, c, gamma, l, rtol, atol, rec));
+    LX_TRY(leja_device(ctx, pb, ud, vd, od, coeffs, K, dt, c, gamma, l, rtol, atol, rec, nullptr, ls));
     LX_TRY(sg.finish());
     if (!sync) return LX_OK;
     Record r;
     LX_TRY(read_record(ctx, 0, &r));
     if (iters_out) *iters_out = r.iters;
     return status_of(r);
+}
+
+lx_status lx_real_leja_phi_vertical(lx_ctx* ctx, const lx_problem* pb, const double* u_lin, const double* v,
+                                    double* const* outs, const double* coeffs, int K, double dt, double c,
+                                    double gamma, int l, double rtol, double atol, int* iters_out) {
+    if (!ctx) return fail(LX_ERR_ARG, "ctx is NULL");
+    LX_TRY(check_problem(ctx, pb));
+    LX_TRY(validate_leja(pb, u_lin, v, outs, coeffs, K, dt, gamma, l));
+    return leja_api(ctx, pb, u_lin, v, outs, coeffs, K, dt, c, gamma, l, rtol, atol, iters_out, nullptr);
+}
+
+lx_status lx_real_leja_phi_multi(lx_ctx* ctx, const lx_problem* pb, const double* u_lin, const double* v,
+                                 double* const* outs, const int* ls, const double* coeffs, int K, double dt, double c,
+                                 double gamma, double rtol, double atol, int* iters_out) {
+    if (!ctx || !ls) return fail(LX_ERR_ARG, "NULL argument");
+    LX_TRY(check_problem(ctx, pb));
+    LX_TRY(validate_leja(pb, u_lin, v, outs, coeffs, K, dt, gamma, ls[0], ls));
+    return leja_api(ctx, pb, u_lin, v, outs, coeffs, K, dt, c, gamma, ls[0], rtol, atol, iters_out, ls);
 }
 
 lx_status lx_real_leja_phi(lx_ctx* ctx, const lx_problem* pb, const double* u_lin, const double* v, double* out,

@@ -158,6 +158,7 @@ struct LejaParams {
     // d_m^(k)) itself, two iterations ahead, on a dedicated coefficient warp (CTA 0, warp 0).
     int coef_gen;
     int l;
+    int lk[kMaxK];        // phi index of accumulator k (= l, or per accumulator: lx_real_leja_phi_multi)
     double cdt, cc, cgamma;
     double ak[kMaxK];
     const double* xi;     // [max_nodes] Leja points

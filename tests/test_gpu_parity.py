@@ -762,3 +762,39 @@ def test_adaptive_step_size_control(xi300, method):
     np.testing.assert_allclose(errs[fin], ref.errs[fin], rtol=1e-5 if big else 1e-6, atol=1e-15)
     assert its == ref.iters
     assert _rel(u, ref.u) <= 1e-9
+
+
+@pytest.mark.parametrize("shape,kern,ls,coeffs", [((96, 130), 1, (0, 1, 2, 3), (1.0,) * 4),
+                                                  ((96, 130), 2, (0, 1, 2, 3), (1.0,) * 4),
+                                                  ((128, 128), 2, (2, 2, 1), (0.5, 0.75, 1.0)),
+                                                  ((40, 16, 64), 2, (0, 1, 3), (1.0,) * 3),
+                                                  ((24, 16, 64), 1, (2, 2, 1), (0.5, 0.75, 1.0))])
+def test_multi_phi_shared_basis(xi300, shape, kern, ls, coeffs):
+    # lx_real_leja_phi_multi: several phi_l of one vector on one Newton basis (the basis does not depend on l):
+    # every output equals its own call (a few ulp: a single-accumulator call may end on a predicted
+    # one-iteration pass where the shared call rolls back) and the oracle (1e-10), and the shared call runs
+    # until the slowest accumulator converged
+    pb, ob = _pair(shape)
+    v = W.ic_random(shape, seed=8, amp=0.2)
+    dt = (10 if len(shape) == 2 else 5) * min(W.dt_cfl(n, 10.0, len(shape)) for n in shape)
+    with lx.Context(pb) as ctx:
+        ctx.set_kernel(kern)
+        c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+        outs = [torch.full(shape, float("nan"), dtype=torch.float64, device="cuda") for _ in ls]
+        it = lx.lx_real_leja_phi_multi(ctx, _dev(v), outs, ls, coeffs, dt, c, g, TOL, TOL)
+        its = []
+        for k, (l, a) in enumerate(zip(ls, coeffs)):
+            o = torch.empty(shape, dtype=torch.float64, device="cuda")
+            its.append(lx.lx_real_leja_phi(ctx, _dev(v), o, a * dt, c, g, l, TOL, TOL))
+            np.testing.assert_allclose(outs[k].cpu().numpy(), o.cpu().numpy(), rtol=0,
+                                       atol=8 * np.finfo(float).eps * float(o.abs().max()))
+            r = O.real_leja_phi(ob, v, a * dt, c, g, l, TOL, TOL, xi300)
+            assert its[-1] == r.iters
+            assert _rel(outs[k], r.outs[0]) <= TOL
+        assert it == max(its)
+        with pytest.raises(lx.LxError) as e:
+            lx.lx_real_leja_phi_multi(ctx, _dev(v), outs[:2], (1, 1), (1.0, 1.0), dt, c, g, TOL, TOL)
+        assert e.value.status == lx.LX_ERR_ARG
+        with pytest.raises(lx.LxError) as e:
+            lx.lx_real_leja_phi_multi(ctx, _dev(v), outs[:1], (5,), (1.0,), dt, c, g, TOL, TOL)
+        assert e.value.status == lx.LX_ERR_UNSUPPORTED
