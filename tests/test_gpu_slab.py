@@ -391,3 +391,33 @@ def test_peer_slab_3d_kernel_two_processes_ipc(xi300):
             one = torch.empty(shape, dtype=torch.float64, device="cuda")
             lx.lx_real_leja_phi(ctx1, torch.from_numpy(v).cuda(), one, dt, c, g, l, TOL, TOL)
             np.testing.assert_array_equal(full, one.cpu().numpy())
+
+
+@pytest.mark.parametrize("shape", [(96, 130), (32, 16, 64)])
+def test_slab_multi_phi(xi300, shape):
+    # lx_real_leja_phi_multi on 2 virtual ranks (2D / 3D peer-memory slab kernels, per-accumulator phi index
+    # in the in-kernel coefficients and in the prebuilt tables) against the oracle's separate calls
+    P, ls, coeffs = 2, (0, 1, 3), (1.0, 1.0, 1.0)
+    dx = tuple(2.0 / n for n in shape)
+    pb = lx.Problem(shape, dx, 1.0, 10.0, 0.0)
+    ob = O.Problem(shape, dx, 1.0, 10.0, 0.0)
+    v = W.ic_random(shape, seed=12, amp=0.2)
+    dt = (10 if len(shape) == 2 else 5) * min(W.dt_cfl(n, 10.0, len(shape)) for n in shape)
+    c, g = O.shift_scale(O.spectrum_bound(ob))
+
+    def rank_fn(r, group, s):
+        ctx = lx.Context(pb, stream=s)
+        ctx.set_comm_local(group, r)
+        b, e, _ = ctx.local()
+        vl = torch.from_numpy(v[b:e]).cuda()
+        outs = [torch.empty_like(vl) for _ in ls]
+        it = lx.lx_real_leja_phi_multi(ctx, vl, outs, ls, coeffs, dt, c, g, TOL, TOL)
+        ctx.close()
+        return it, [o.cpu().numpy() for o in outs]
+
+    res = _run_ranks(P, rank_fn)
+    refs_ = [O.real_leja_phi(ob, v, dt, c, g, l, TOL, TOL, xi300) for l in ls]
+    assert {r[0] for r in res} == {max(x.iters for x in refs_)}
+    for k, ref in enumerate(refs_):
+        full = np.concatenate([res[r][1][k] for r in range(P)], axis=0)
+        assert np.linalg.norm(full - ref.outs[0]) <= TOL * np.linalg.norm(ref.outs[0])
