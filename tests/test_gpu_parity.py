@@ -798,3 +798,41 @@ def test_multi_phi_shared_basis(xi300, shape, kern, ls, coeffs):
         with pytest.raises(lx.LxError) as e:
             lx.lx_real_leja_phi_multi(ctx, _dev(v), outs[:1], (5,), (1.0,), dt, c, g, TOL, TOL)
         assert e.value.status == lx.LX_ERR_UNSUPPORTED
+
+
+def _fuzz_cases(n, seed):
+    rng = np.random.default_rng(seed)
+    cases = []
+    for _ in range(n):
+        nd = int(rng.integers(2, 4))
+        if nd == 2:
+            shape = (int(rng.integers(16, 200)), 2 * int(rng.integers(32, 100)))
+        else:
+            shape = (int(rng.integers(4, 40)), 16 * int(rng.integers(1, 4)), 64 * int(rng.integers(1, 3)))
+        K = int(rng.integers(1, 5))
+        coeffs = tuple(sorted(rng.choice(np.array([0.125, 0.25, 1 / 3, 0.5, 2 / 3, 0.75, 0.9, 1.0]), K,
+                                         replace=False)))
+        # 3D at <= 5 x CFL: coarse 3D grids at 10 x CFL reach the real-Leja limit of R28 (NOCONV on both sides)
+        cases.append((shape, K, coeffs, int(rng.integers(0, 5)), float(rng.choice([1.0, 5.0, 10.0] if nd == 2 else [1.0, 5.0])),
+                      int(rng.integers(0, 3)), int(rng.integers(0, 1 << 30))))
+    return cases
+
+
+@pytest.mark.parametrize("case", _fuzz_cases(40, 2026))
+def test_leja_fuzz(xi300, case):
+    # seeded random shapes (2D ragged rows / even columns, 3D on and off the two-step kernel's shape), K = 1..4
+    # vertical coefficients, phi_0..phi_4, dt = 1 / 5 / 10 x CFL and kernel choice (auto, one pass, two
+    # steps): same iteration count as the oracle and 1e-10
+    shape, K, coeffs, l, mult, kern, seed = case
+    pb, ob = _pair(shape)
+    v = W.ic_random(shape, seed=seed % 100000, amp=0.3)
+    dt = mult * min(W.dt_cfl(n, 10.0, len(shape)) for n in shape)
+    with lx.Context(pb) as ctx:
+        ctx.set_kernel(kern)
+        c, g = lx.lx_shift_scale(lx.lx_spectrum_bound(ctx))
+        outs = [torch.full(shape, float("nan"), dtype=torch.float64, device="cuda") for _ in range(K)]
+        it = lx.lx_real_leja_phi_vertical(ctx, _dev(v), outs, coeffs, dt, c, g, l, TOL, TOL)
+    r = O.real_leja_phi(ob, v, dt, c, g, l, TOL, TOL, xi300, coeffs=coeffs)
+    assert it == r.iters, (case, it, r.iters)
+    for o, ref in zip(outs, r.outs):
+        assert _rel(o, ref) <= TOL, case
