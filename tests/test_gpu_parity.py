@@ -836,3 +836,32 @@ def test_leja_fuzz(xi300, case):
     assert it == r.iters, (case, it, r.iters)
     for o, ref in zip(outs, r.outs):
         assert _rel(o, ref) <= TOL, case
+
+
+_METHODS = ["rosenbrock_euler", "exprb32", "exprb43", "epirk4s3a", "exprb42", "epirk5p1", "exprb53s3", "exprb54s4",
+            "epirk4s3b", "epirk4s3"]
+
+
+@pytest.mark.parametrize("case", [(m, s) for s, m in enumerate(_METHODS)] + [(m, 100 + s) for s, m in enumerate(_METHODS)])
+def test_step_fuzz_allen_cahn(xi300, case):
+    # every integrator on a seeded random Allen-Cahn grid (ragged rows, even columns) and step size, on the
+    # auto kernel choice: same total iterations as the oracle, u_high / u_low / err to 1e-10
+    method, seed = case
+    rng = np.random.default_rng(seed)
+    shape = (int(rng.integers(16, 140)), 2 * int(rng.integers(32, 80)))
+    pb, ob = _pair(shape, diff=1e-3, nu=0.0, react=1.0)
+    u = W.ic_random(shape, seed=seed, amp=0.8)
+    h = float(rng.choice([0.002, 0.005, 0.01]))
+    bound = O.spectrum_bound(ob, u)
+    c, g = O.shift_scale(bound)
+    ref = O.step(ob, method, u, h, c, g, TOL, TOL, xi300)
+    assert ref.status == O.OK
+    with lx.Context(pb) as ctx:
+        lo, hi = torch.empty(shape, dtype=torch.float64, device="cuda"), torch.empty(shape, dtype=torch.float64,
+                                                                                        device="cuda")
+        it, err = lx.lx_step(ctx, method, _dev(u), lo, hi, h, c, g, TOL, TOL)
+    assert it == ref.iters, (case, it, ref.iters)
+    assert _rel(hi, ref.u_high) <= TOL
+    if method not in ("rosenbrock_euler", "exprb42"):
+        assert _rel(lo, ref.u_low) <= TOL
+        assert err == pytest.approx(ref.err, rel=1e-6, abs=1e-14)
