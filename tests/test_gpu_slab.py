@@ -421,3 +421,47 @@ def test_slab_multi_phi(xi300, shape):
     for k, ref in enumerate(refs_):
         full = np.concatenate([res[r][1][k] for r in range(P)], axis=0)
         assert np.linalg.norm(full - ref.outs[0]) <= TOL * np.linalg.norm(ref.outs[0])
+
+
+@pytest.mark.parametrize("method", ["exprb43", "epirk4s3a"])
+def test_slab_integrate_and_adaptive(xi300, method):
+    # the paper's time loop on 2 virtual ranks: lx_integrate (device spectrum bound with the cross-rank max,
+    # (c, gamma) on the device every step) and lx_integrate_adaptive (R32: the cross-rank embedded error
+    # drives identical accept / reject decisions on every rank) against the oracle's single-domain loops
+    P, shape = 2, (96, 64)
+    dx = tuple(2.0 / n for n in shape)
+    pb = lx.Problem(shape, dx, 1e-3, 0.0, 1.0)
+    ob = O.Problem(shape, dx, 1e-3, 0.0, 1.0)
+    u = W.ic_allen_cahn_2d(*shape)
+    dt, nsteps = 0.01, 3
+    t_end, dt0, tol = 0.2, 0.2, 1e-7
+
+    def rank_fn(r, group, s):
+        ctx = lx.Context(pb, stream=s)
+        ctx.set_comm_local(group, r)
+        b, e, _ = ctx.local()
+        ul = torch.from_numpy(u[b:e]).cuda()
+        it, err = lx.lx_integrate(ctx, method, ul, dt, nsteps, TOL, TOL)
+        ua = torch.from_numpy(u[b:e]).cuda()
+        acc, rej, dts, errs, its = lx.lx_integrate_adaptive(ctx, method, ua, t_end, dt0, tol, 1e-12, 1e-12)
+        ctx.close()
+        return it, err, ul.cpu().numpy(), (acc, rej, list(dts), its), ua.cpu().numpy()
+
+    res = _run_ranks(P, rank_fn)
+    uo, tot = u.copy(), 0
+    for _ in range(nsteps):
+        c, g = O.shift_scale(O.spectrum_bound(ob, uo))
+        r = O.step(ob, method, uo, dt, c, g, TOL, TOL, xi300)
+        tot += r.iters
+        uo = r.u_high
+    assert {x[0] for x in res} == {tot}
+    full = np.concatenate([x[2] for x in res])
+    assert np.linalg.norm(full - uo) <= TOL * np.linalg.norm(uo)
+    ref = O.integrate_adaptive(ob, method, u, t_end, dt0, tol, 1e-12, 1e-12, xi300)
+    assert ref.status == O.OK
+    for x in res:
+        acc, rej, dts, its = x[3]
+        assert (acc, rej, its) == (ref.accepted, ref.rejected, ref.iters)
+        np.testing.assert_allclose(dts, ref.dts, rtol=1e-8)
+    fa = np.concatenate([x[4] for x in res])
+    assert np.linalg.norm(fa - ref.u) <= 1e-9 * np.linalg.norm(ref.u)
