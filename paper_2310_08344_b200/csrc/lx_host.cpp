@@ -1184,6 +1184,11 @@ static lx_status rhs_device(lx_ctx* ctx, const lx_problem* pb, const double* u, 
     P.v = RowSrc{u, nullptr, ctx->row, ctx->n_loc, 0};
     P.ydst[0] = f;
     if (ctx->comm) return comm_rhs(ctx->comm, P, scale, ctx->stream, &ctx->launches) ? fail(LX_ERR_NCCL, "rhs halo: %s", comm_error()) : LX_OK;
+    if (P.ndim == 3 && ctx->k3d != 1 && P.n1 % 16 == 0 && P.n2 % 64 == 0) {
+        CUDA_TRY(launch_rhs3d_smem(P, scale, ctx->stream, ctx->device));
+        ctx->launches++;
+        return LX_OK;
+    }
     P.grid = (P.nunits + kWarps - 1) / kWarps;
     if (P.grid > ctx->nsm * 4) P.grid = ctx->nsm * 4;
     CUDA_TRY(launch_rhs(P, scale, ctx->stream));

@@ -252,6 +252,8 @@ enum StageOp {
 };
 cudaError_t launch_stage(int op, const StageArgs& A, cudaStream_t s);
 cudaError_t launch_rhs(const LejaParams& P, double scale, cudaStream_t s);
+// f(u) dt on 3D grids with the smem kernel's plane tiles (single domain, n1 % 16 == 0, n2 % 64 == 0)
+cudaError_t launch_rhs3d_smem(const LejaParams& P, double scale, cudaStream_t s, int device);
 // Burgers remainder difference (stencil): y = a2 * (dt F(x) - dt F(u)), x = P.v (with halo), u = P.u
 cudaError_t launch_rem_flux(const LejaParams& P, double dt, double a2, double* out, cudaStream_t s);
 cudaError_t launch_fill_start(double* v, long long n, bool add_e0, cudaStream_t s);

@@ -249,6 +249,117 @@ static void* leja3d_smem_ptr(int K, bool diag) {
 
 int leja3d_smem_units(int n0, int n1, int n2) { return (n1 / kS3J) * (n2 / 64) * ((n0 + kTI3 - 1) / kTI3); }
 
+// ---------------------------------------------------------------------------
+// f(u) dt on 3D grids (single domain, the smem kernel's shape) with the same shared-memory plane tiles as
+// k_leja3d_smem (each u value read from L2 / HBM ~1.2 times instead of ~5.5 by the warp-tile k_rhs2d<3>):
+// f(u) scale = scale (A u + react (u - u^3) [+ S]), the stencil in the FMA order of tile3d's M_RHS (16 B/pt,
+// +8 with a source).  No grid-wide synchronisation: a plain launch over the CTA units.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 2) k_rhs3d_smem(const __grid_constant__ LejaParams P, double scale) {
+    extern __shared__ double s3_rhs_ring[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int n0 = P.n_loc, n1 = P.n1, n2 = P.n2;
+    const int njb = n1 / kS3J, nkb = n2 >> 6;
+    const int ncu = njb * nkb * ((n0 + kTI3 - 1) / kTI3);
+    const Stencil& S = P.st;
+    constexpr int RW = kS3J / kWarps;
+    const double* src = P.v.base;
+    double* dst = P.ydst[0];
+    for (int cu = blockIdx.x; cu < ncu; cu += gridDim.x) {
+        const int jb = cu % njb, t0 = cu / njb, kb = t0 % nkb, ir = t0 / nkb;
+        const int j0 = jb * kS3J, k0 = kb * 64;
+        const int i0 = ir * kTI3, i1 = min(n0, i0 + kTI3);
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            s3_issue(src, s3_rhs_ring, i0 - 1 + q, q, j0, k0, n0, n1, n2);
+            cp_async_commit();
+        }
+        const int kc = k0 + 2 * lane;
+        for (int i = i0; i < i1; i++) {
+            const int rel = i - i0 + 1;
+            if (i + 3 <= i1 + 1) s3_issue(src, s3_rhs_ring, i + 3, (rel + 3) % kS3Depth, j0, k0, n0, n1, n2);
+            cp_async_commit();
+            cp_async_wait<1>();
+            __syncthreads();
+            const uint32_t base = smem_u32(s3_rhs_ring);
+            auto at = [&](int pos, int row, int col) {
+                return lds2(base + (uint32_t)(((pos % kS3Depth) * kS3Plane + row * kS3Cols + col) * 8));
+            };
+            const int cc = 2 + 2 * lane;
+#pragma unroll
+            for (int r = 0; r < RW; r++) {
+                const int row = warp + r * kWarps + 1;
+                const int j = j0 + row - 1;
+                const double2 yc = at(rel, row, cc);
+                const double2 up = at(rel - 1 + kS3Depth, row, cc);
+                const double2 dn1 = at(rel + 1, row, cc);
+                const double2 dn2 = at(rel + 2, row, cc);
+                const double2 wm = at(rel, row - 1, cc);
+                const double2 wp1 = at(rel, row + 1, cc);
+                const double2 wp2 = at(rel, row + 2, cc);
+                const double2 lf = at(rel, row, cc - 2);
+                const double2 rt = at(rel, row, cc + 2);
+                const double left = lf.y, r1 = rt.x, r2 = rt.y;
+                double ax = S.c0 * yc.x;
+                ax = fma(S.m1[0], up.x, ax);
+                ax = fma(S.p1[0], dn1.x, ax);
+                ax = fma(S.p2[0], dn2.x, ax);
+                ax = fma(S.m1[1], wm.x, ax);
+                ax = fma(S.p1[1], wp1.x, ax);
+                ax = fma(S.p2[1], wp2.x, ax);
+                ax = fma(S.m1[2], left, ax);
+                ax = fma(S.p1[2], yc.y, ax);
+                ax = fma(S.p2[2], r1, ax);
+                double ay = S.c0 * yc.y;
+                ay = fma(S.m1[0], up.y, ay);
+                ay = fma(S.p1[0], dn1.y, ay);
+                ay = fma(S.p2[0], dn2.y, ay);
+                ay = fma(S.m1[1], wm.y, ay);
+                ay = fma(S.p1[1], wp1.y, ay);
+                ay = fma(S.p2[1], wp2.y, ay);
+                ay = fma(S.m1[2], yc.x, ay);
+                ay = fma(S.p1[2], r1, ay);
+                ay = fma(S.p2[2], r2, ay);
+                double fx = fma(S.react, yc.x - yc.x * yc.x * yc.x, ax);
+                double fy = fma(S.react, yc.y - yc.y * yc.y * yc.y, ay);
+                const long long off = ((long long)i * n1 + j) * n2 + kc;
+                if (P.source) {
+                    const double2 sv = ldg2(P.source + off);
+                    fx += sv.x;
+                    fy += sv.y;
+                }
+                st2(dst + off, make_double2(scale * fx, scale * fy));
+            }
+        }
+        cp_async_wait<0>();
+        __syncthreads();   // the ring is reused by the next unit
+    }
+}
+
+cudaError_t launch_rhs3d_smem(const LejaParams& P, double scale, cudaStream_t s, int device) {
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    int g;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = cache.find(device);
+        if (it != cache.end()) {
+            g = it->second;
+        } else {
+            int nsm = 0, per = 0;
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+            cudaFuncSetAttribute((const void*)k_rhs3d_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, kS3Smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void*)k_rhs3d_smem, kThreads, kS3Smem);
+            g = nsm * (per < 1 ? 1 : per);
+            cache[device] = g;
+        }
+    }
+    const int ncu = leja3d_smem_units(P.n_loc, P.n1, P.n2);
+    if (g > ncu) g = ncu;
+    k_rhs3d_smem<<<g, kThreads, kS3Smem, s>>>(P, scale);
+    return cudaGetLastError();
+}
+
 int leja3d_smem_grid_size(int device, int K, bool diag, int ncu) {
     void* kern = leja3d_smem_ptr(K, diag);
     if (!kern) return 0;
@@ -1026,6 +1137,10 @@ cudaError_t launch_leja3d_tb2(const LejaParams& P, cudaStream_t s, bool slab) {
 }
 
 cudaError_t preload_3d() {
+    {
+        cudaFuncAttributes a;
+        if (cudaFuncGetAttributes(&a, (const void*)k_rhs3d_smem) != cudaSuccess) return cudaGetLastError();
+    }
     for (int K = 1; K <= kMaxK; K++) {
         cudaFuncAttributes a;
         for (int sl = 0; sl < 2; sl++)

@@ -865,3 +865,28 @@ def test_step_fuzz_allen_cahn(xi300, case):
     if method not in ("rosenbrock_euler", "exprb42"):
         assert _rel(lo, ref.u_low) <= TOL
         assert err == pytest.approx(ref.err, rel=1e-6, abs=1e-14)
+
+
+@pytest.mark.parametrize("shape,react,src", [((24, 16, 64), 0.0, False), ((70, 32, 128), 1.0, False),
+                                             ((9, 16, 64), 1.0, True)])
+def test_rhs_3d_kernels(xi300, shape, react, src):
+    # f(u) dt on 3D grids: the shared-memory plane-tile kernel (default on n1 % 16 == 0, n2 % 64 == 0) and the
+    # warp-tile kernel (lx_ctx_set_kernel(., ., 1)) against the oracle's f (runs of 64 planes, a ragged last
+    # run, runs shorter than the stencil reach, reaction and source terms)
+    dx = tuple(2.0 / m for m in shape)
+    diff, nu = (0.01, 0.0) if react else (1.0, 10.0)
+    S = W.ic_random(shape, seed=22, amp=0.3) if src else None
+    pb = lx.Problem(shape, dx, diff, nu, react, source=_dev(S) if src else None)
+    ob = O.Problem(shape, dx, diff, nu, react, source=S)
+    u = W.ic_random(shape, seed=21, amp=0.7)
+    ref = 0.125 * O.rhs(ob, u)
+    outs = []
+    for k3d in (0, 1):
+        with lx.Context(pb) as ctx:
+            ctx.set_kernel(0, k3d)
+            f = torch.empty(shape, dtype=torch.float64, device="cuda")
+            lx.lx_rhs(ctx, _dev(u), f, 0.125)
+            outs.append(f.cpu().numpy())
+    for o in outs:
+        assert np.abs(o - ref).max() <= 1e-12 * np.abs(ref).max()
+    np.testing.assert_array_equal(outs[0], outs[1])   # same FMA order in both kernels
