@@ -88,6 +88,7 @@ struct lx_ctx {
     size_t coef_stride = 0;
     cudaEvent_t coef_ev[kCoefSlots] = {};
     int coef_next = 0;
+    unsigned long long slot_key[kCoefSlots] = {};   // key of the prebuilt table in each ring slot (0: none)
     int64_t launches = 0;
     std::vector<double> xi;
     double* xi_dev = nullptr;             // Leja points on the device
@@ -294,6 +295,7 @@ static lx_status build_tables(lx_ctx* ctx, const TableSpec* specs, int n, double
     for (int t = 0; t < n; t++) {
         const int slot = ctx->coef_next;
         ctx->coef_next = (slot + 1) % kCoefSlots;
+        ctx->slot_key[slot] = 0;
         double* dev = ctx->coef_dev + slot * ctx->coef_stride;
         tables_out[t] = dev;
         for (int k = 0; k < specs[t].K; k++) {
@@ -413,12 +415,45 @@ static lx_status leja3d_table(lx_ctx* ctx, LejaParams& P, int K, int l, const do
                               double gamma, int rec) {
     (void)l;
     if (!P.coef_gen) return LX_OK;
+    // a table depends only on (K, l_k, a_k, dt, c, gamma): a repeated call (fixed dt and spectrum: every step
+    // of a linear problem) reuses the ring slot that still holds it instead of rebuilding it (host-known
+    // (c, gamma) only; lx_integrate's device-side (c, gamma) always rebuild)
+    unsigned long long key = 0;
+    if (!ctx->cg_active) {
+        unsigned long long h = 1469598103934665603ull;
+        auto mix = [&h](unsigned long long x) {
+            h ^= x;
+            h *= 1099511628211ull;
+        };
+        auto bits = [](double x) {
+            unsigned long long b;
+            std::memcpy(&b, &x, sizeof b);
+            return b;
+        };
+        mix((unsigned long long)K | ((unsigned long long)ctx->max_nodes << 8));
+        for (int k = 0; k < K; k++) {
+            mix((unsigned long long)P.lk[k]);
+            mix(bits(coeffs[k]));
+        }
+        mix(bits(dt));
+        mix(bits(c));
+        mix(bits(gamma));
+        key = h | 1ull;
+        for (int sl = 0; sl < kCoefSlots; sl++)
+            if (ctx->slot_key[sl] == key) {
+                P.table = ctx->coef_dev + sl * ctx->coef_stride;
+                P.coef = P.table;
+                P.coef_gen = 0;
+                return LX_OK;
+            }
+    }
     CoefJobs jobs;
     std::memset(&jobs, 0, sizeof jobs);
     for (int k = 0; k < K; k++) jobs.j[jobs.n++] = CoefJob{P.table, coeffs[k], P.lk[k], K, k};
     CUDA_TRY(launch_coef_tables(ctx->xi_dev, ctx->rcp_dev, ctx->max_nodes, jobs, dt, c, gamma, ctx->cg_active,
                                 &ctx->rec_dev[rec].status, ctx->stream));
     ctx->launches++;
+    if (key) ctx->slot_key[(P.table - ctx->coef_dev) / ctx->coef_stride] = key;
     P.coef_gen = 0;
     return LX_OK;
 }
@@ -444,6 +479,7 @@ static lx_status leja_device(lx_ctx* ctx, const lx_problem* pb, const double* u,
         // the Leja kernels compute their own Newton coefficients (coefficient warp) into a ring slot
         const int slot = ctx->coef_next;
         ctx->coef_next = (slot + 1) % kCoefSlots;
+        ctx->slot_key[slot] = 0;
         double* tab = ctx->coef_dev + slot * ctx->coef_stride;
         P.coef_gen = 1;
         P.table = tab;
