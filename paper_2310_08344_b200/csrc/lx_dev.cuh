@@ -1003,9 +1003,16 @@ __device__ __forceinline__ unsigned long long tb2_call_key(const LejaParams& P) 
         ((unsigned long long)P.active0 << 40));
 #pragma unroll
     for (int k = 0; k < K; k++) mix((unsigned long long)P.lk[k]);
+    // the spectrum enters through dt*gamma and c/gamma, bucketed (1/32 octave): a time loop whose (c, gamma)
+    // drift from step to step (lx_integrate, the Gershgorin bound of a nonlinear problem) keeps its
+    // predictions; they steer only the scheduling (results never depend on them)
+    auto bucket = [](double x) -> unsigned long long {
+        if (!(x > 0.0) || !isfinite(x)) return 0x8000000000000000ull | (unsigned long long)__double_as_longlong(x);
+        return (unsigned long long)(long long)floor(32.0 * log2(x));
+    };
     mix((unsigned long long)__double_as_longlong(P.cdt));
-    mix((unsigned long long)__double_as_longlong(P_c(P)));
-    mix((unsigned long long)__double_as_longlong(P_g(P)));
+    mix(bucket(P.cdt * P_g(P)));
+    mix(bucket(-P_c(P) / P_g(P)));
     mix((unsigned long long)__double_as_longlong(P.rtol));
     mix((unsigned long long)__double_as_longlong(P.atol));
 #pragma unroll
