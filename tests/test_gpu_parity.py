@@ -890,3 +890,27 @@ def test_rhs_3d_kernels(xi300, shape, react, src):
     for o in outs:
         assert np.abs(o - ref).max() <= 1e-12 * np.abs(ref).max()
     np.testing.assert_array_equal(outs[0], outs[1])   # same FMA order in both kernels
+
+
+@pytest.mark.parametrize("method", ["epirk4s3a", "exprb43"])
+def test_integrate_3d_two_step_kernel(xi300, method):
+    # the time loop on a 3D grid through the two-step plane-sweep kernel: repeated calls with the same
+    # parameters every step (predicted final iterations, reused coefficient tables) must keep the oracle's
+    # iteration counts and results step after step
+    shape = (32, 16, 64)
+    pb, ob = _pair(shape)
+    u = W.ic_random(shape, seed=31, amp=0.3)
+    dt, nsteps = 5 * min(W.dt_cfl(n, 10.0, 3) for n in shape), 4
+    ud = _dev(u)
+    with lx.Context(pb) as ctx:
+        ctx.set_kernel(2)
+        assert ctx.iterations_per_pass == 2
+        it, err = lx.lx_integrate(ctx, method, ud, dt, nsteps, TOL, TOL)
+    tot = 0
+    for _ in range(nsteps):
+        c, g = O.shift_scale(O.spectrum_bound(ob, u))
+        r = O.step(ob, method, u, dt, c, g, TOL, TOL, xi300)
+        tot += r.iters
+        u = r.u_high
+    assert it == tot
+    assert _rel(ud, u) <= TOL
