@@ -1523,6 +1523,23 @@ static lx_status step_device(lx_ctx* ctx, lx_method method, const lx_problem* pb
         // phi_1(hJ) D_a -> S1 ; b = u + p_one + S1 ; D_b -> lo
         double* o[1] = {S1};
         LX_TRY(leja_device(ctx, pb, ul, S0, o, &one, 1, dt, c, gamma, 1, rtol, atol, rec));
+        if (pb->flux == 0.0) {
+            // D_b and the final stage's two combinations in one pointwise kernel: w3 -> S1, w4 -> hi
+            A = stage_args(ctx, pb, rec);
+            A.dt = dt;
+            A.u = u;
+            A.x1 = p_one; A.x2 = S1; A.x3 = S0; A.a0 = 1.0; A.a1 = 1.0;
+            A.a2 = c3a; A.a3 = c3b; A.a4 = c4a; A.a5 = c4b;
+            A.y0 = S1; A.y1 = hi;
+            LX_TRY(run_stage(ctx, ST_REMB_W34, A));
+            double* o3[1] = {S0};   // q3 (D_a consumed)
+            LX_TRY(leja_device(ctx, pb, ul, S1, o3, &one, 1, dt, c, gamma, 3, rtol, atol, rec));
+            double* o4[1] = {lo};   // q4
+            LX_TRY(leja_device(ctx, pb, ul, hi, o4, &one, 1, dt, c, gamma, 4, rtol, atol, rec));
+            A = stage_args(ctx, pb, rec);   // u3 = u + p_one + q3 -> lo ; u4 = u3 + q4 -> hi ; err
+            A.x0 = u; A.x1 = p_one; A.x2 = S0; A.x3 = lo; A.y0 = lo; A.y1 = hi;
+            return run_stage(ctx, ST_FINAL4, A);
+        }
         LX_TRY(stage_remainder(ctx, pb, rec, u, u, p_one, 1.0, S1, 1.0, 1.0, dt, lo, hi));
         Db = lo;
     }

@@ -249,6 +249,8 @@ enum StageOp {
     ST_LIN4_ERR,          // y0 = x0 + a0*x1 + a1*x2 + a2*x3 ; err = ||y0 - y1|| (y1 read: the embedded solution)
     ST_REM2_W34,          // D_a = dt F(u + a0 x1) - dt F(u), D_b = dt F(u + a1 x2) - dt F(u) (not stored);
                           // y0 = a2 D_a + a3 D_b, y1 = a4 D_a + a5 D_b  (two-stage EPIRK final-stage inputs)
+    ST_REMB_W34,          // D_b = dt F(u + a0 x1 + a1 x2) - dt F(u) (not stored), D_a = x3;
+                          // y0 = a2 D_a + a3 D_b, y1 = a4 D_a + a5 D_b  (EXPRB43 final-stage inputs)
 };
 cudaError_t launch_stage(int op, const StageArgs& A, cudaStream_t s);
 cudaError_t launch_rhs(const LejaParams& P, double scale, cudaStream_t s);

@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kThreads) k_stage_pointwise(const __grid_const
     // before any store (outputs may alias inputs element-wise, which blocks the compiler from
     // overlapping trips on its own), so every thread keeps UN x (inputs) 16-byte loads in flight.
     constexpr int UN = 4;
-    constexpr int NIN = (OP == ST_LIN4_ERR) ? 5 : (OP == ST_FINAL4 || OP == ST_LIN4) ? 4 : (OP == ST_STAGE_REMAINDER) ? 4
+    constexpr int NIN = (OP == ST_LIN4_ERR) ? 5 : (OP == ST_FINAL4 || OP == ST_LIN4 || OP == ST_REMB_W34) ? 4 : (OP == ST_STAGE_REMAINDER) ? 4
                         : (OP == ST_SUM3 || OP == ST_LIN3 || OP == ST_REM2_W34) ? 3 : (OP == ST_MAXSQ) ? 1 : 2;
     __shared__ double s_red[kWarps][kSlot];
     __shared__ int s_last;
@@ -168,6 +168,7 @@ __global__ void __launch_bounds__(kThreads) k_stage_pointwise(const __grid_const
     if (OP == ST_REMAINDER_DIFF) { in[0] = A.x0; in[1] = A.u; }
     else if (OP == ST_STAGE_REMAINDER) { in[0] = A.x0; in[1] = A.u; in[2] = A.x1; in[3] = A.x2; }
     else if (OP == ST_REM2_W34) { in[0] = A.u; in[1] = A.x1; in[2] = A.x2; }
+    else if (OP == ST_REMB_W34) { in[0] = A.u; in[1] = A.x1; in[2] = A.x2; in[3] = A.x3; }
     else if (OP == ST_EXPRB32_A) { in[0] = A.x0; in[1] = A.x1; }
     else { in[0] = A.x0; in[1] = A.x1; in[2] = A.x2; in[3] = A.x3; }
     if (OP == ST_LIN4_ERR) in[4] = A.y1;
@@ -214,6 +215,15 @@ __global__ void __launch_bounds__(kThreads) k_stage_pointwise(const __grid_const
                 const double dby = dt * nl_rem(react, sby, u.y) + (-dt) * nl_rem(react, u.y, u.y);
                 st2(A.y0 + o, make_double2(A.a2 * dax + A.a3 * dbx, A.a2 * day + A.a3 * dby));
                 st2(A.y1 + o, make_double2(A.a4 * dax + A.a5 * dbx, A.a4 * day + A.a5 * dby));
+            } else if (OP == ST_REMB_W34) {
+                // ST_STAGE_REMAINDER (a2 = 1) for D_b and ST_COMBINE2 with D_a read back, in one pass
+                const double2 u = v[q][0], p = v[q][1], r = v[q][2], da = v[q][3];
+                const double sx = u.x + A.a0 * p.x + A.a1 * r.x;
+                const double sy = u.y + A.a0 * p.y + A.a1 * r.y;
+                const double dbx = dt * nl_rem(react, sx, u.x) + (-dt) * nl_rem(react, u.x, u.x);
+                const double dby = dt * nl_rem(react, sy, u.y) + (-dt) * nl_rem(react, u.y, u.y);
+                st2(A.y0 + o, make_double2(A.a2 * da.x + A.a3 * dbx, A.a2 * da.y + A.a3 * dby));
+                st2(A.y1 + o, make_double2(A.a4 * da.x + A.a5 * dbx, A.a4 * da.y + A.a5 * dby));
             } else if (OP == ST_EXPRB32_A) {
                 const double2 u = v[q][0], p = v[q][1];
                 const double2 a = make_double2(u.x + p.x, u.y + p.y);
@@ -309,6 +319,7 @@ static void* stage_kernel_ptr(int op) {
         case ST_LIN4: return (void*)k_stage_pointwise<ST_LIN4>;
         case ST_LIN4_ERR: return (void*)k_stage_pointwise<ST_LIN4_ERR>;
         case ST_REM2_W34: return (void*)k_stage_pointwise<ST_REM2_W34>;
+        case ST_REMB_W34: return (void*)k_stage_pointwise<ST_REMB_W34>;
     }
     return nullptr;
 }
@@ -358,6 +369,7 @@ cudaError_t launch_stage(int op, const StageArgs& A, cudaStream_t s) {
         case ST_LIN4: k_stage_pointwise<ST_LIN4><<<g, b, 0, s>>>(A); break;
         case ST_LIN4_ERR: k_stage_pointwise<ST_LIN4_ERR><<<g, b, 0, s>>>(A); break;
         case ST_REM2_W34: k_stage_pointwise<ST_REM2_W34><<<g, b, 0, s>>>(A); break;
+        case ST_REMB_W34: k_stage_pointwise<ST_REMB_W34><<<g, b, 0, s>>>(A); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
