@@ -503,6 +503,61 @@ __device__ __forceinline__ void tile3d(const LejaParams& P, const RowSrc& src, d
 }
 
 
+// Output of one row of the flux-form tile: y_m (or f, remainder, power iterate) at (i, j0..j0+1), its
+// norm, and the Newton accumulators p_m = p_{m-1} + d_m y_m (Leja mode).
+template <int K, bool FIRST, int MODE>
+__device__ __forceinline__ void tile2d_flux_out(const LejaParams& P, double* __restrict__ dst, int i, int j0,
+                                                bool valid, double2 yc, const double* res, const double2* pv,
+                                                double beta, const double* d0, const double* dm, int active,
+                                                double scale, double& sy, double* sp) {
+    constexpr int KK = K > 0 ? K : 1;
+    const int n1 = P.n1;
+    double2 yn;
+    if (MODE == M_POWER) {
+        yn.x = scale * res[0];
+        yn.y = scale * res[1];
+    } else if (MODE == M_RHS) {
+        double fx = res[0], fy = res[1];
+        if (P.source && valid) {
+            const double2 sv = ldg2(P.source + (long long)i * n1 + j0);
+            fx += sv.x;
+            fy += sv.y;
+        }
+        yn.x = scale * fx;
+        yn.y = scale * fy;
+    } else if (MODE == M_REM) {
+        yn.x = res[0];
+        yn.y = res[1];
+    } else {
+        yn.x = fma(scale, res[0], beta * yc.x);
+        yn.y = fma(scale, res[1], beta * yc.y);
+    }
+    if (valid) {
+        const long long off = (long long)i * n1 + j0;
+        st2(dst + off, yn);
+        sy = fma(yn.x, yn.x, sy);
+        sy = fma(yn.y, yn.y, sy);
+        if (MODE == M_LEJA) {
+#pragma unroll
+            for (int k = 0; k < KK; k++) {
+                if ((active >> k) & 1) {
+                    double2 pn;
+                    if (FIRST) {
+                        pn.x = fma(dm[k], yn.x, d0[k] * yc.x);
+                        pn.y = fma(dm[k], yn.y, d0[k] * yc.y);
+                    } else {
+                        pn.x = fma(dm[k], yn.x, pv[k].x);
+                        pn.y = fma(dm[k], yn.y, pv[k].y);
+                    }
+                    st2(P.p[k] + off, pn);
+                    sp[k] = fma(pn.x, pn.x, sp[k]);
+                    sp[k] = fma(pn.y, pn.y, sp[k]);
+                }
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Flux-form 2D tile (Problem III, viscous Burgers; exact Jacobian R13):
 //   M_LEJA/M_POWER: A y = diff lap(y) + sum_d D_d((nu + beta u) y)      (J(u) y)
@@ -523,26 +578,26 @@ __device__ __forceinline__ void tile2d_flux(const LejaParams& P, const RowSrc& s
     const int j0 = b * 64 + 2 * lane;
     const bool valid = j0 < n1;
     const int last = min(31, ((n1 - b * 64) >> 1) - 1);
-    const int i0 = rb * kRT;
-    const int nout = min(kRT, P.n_loc - i0);
+    const int i0 = rb * kRTF;
+    const int nout = min(kRTF, P.n_loc - i0);
     const Stencil& S = P.st;
     const RowSrc us{P.u, nullptr, (long long)n1, P.n_loc, 0};
     auto LD2 = [&](const double* q) { return RO ? ldg2(q) : ld2(q); };
     auto LD1 = [&](const double* q) { return RO ? __ldg(q) : *q; };
 
-    double2 w[kRT + 3], uw[kRT + 3];
+    double2 w[kRTF + 3], uw[kRTF + 3];
 #pragma unroll
-    for (int t = 0; t < kRT + 3; t++) {
+    for (int t = 0; t < kRTF + 3; t++) {
         w[t] = uw[t] = make_double2(0.0, 0.0);
         if (valid && t < nout + 3) {
             w[t] = LD2(rowp(src, i0 - 1 + t) + j0);
             if (TWO) uw[t] = ldg2(rowp(us, i0 - 1 + t) + j0);
         }
     }
-    double hl[kRT], uhl[kRT];
-    double2 hr[kRT], uhr[kRT];
+    double hl[kRTF], uhl[kRTF];
+    double2 hr[kRTF], uhr[kRTF];
 #pragma unroll
-    for (int t = 0; t < kRT; t++) {
+    for (int t = 0; t < kRTF; t++) {
         hl[t] = uhl[t] = 0.0;
         hr[t] = uhr[t] = make_double2(0.0, 0.0);
         if (t < nout) {
@@ -562,9 +617,9 @@ __device__ __forceinline__ void tile2d_flux(const LejaParams& P, const RowSrc& s
         }
     }
     constexpr int KK = K > 0 ? K : 1;
-    double2 pv[kRT][KK];
+    double2 pv[kRTF][KK];
 #pragma unroll
-    for (int t = 0; t < kRT; t++) {
+    for (int t = 0; t < kRTF; t++) {
         const long long off = (long long)(i0 + t) * n1 + j0;
         if (MODE == M_LEJA && !FIRST) {
 #pragma unroll
@@ -575,9 +630,80 @@ __device__ __forceinline__ void tile2d_flux(const LejaParams& P, const RowSrc& s
         }
     }
     const double nu = S.nu, bt = S.flux;
+    // J y (Leja / power modes): the flux field G = (nu + beta u) y is evaluated once per point of the
+    // window (in place of u) and its halo, instead of once per stencil use (7x); the same expression,
+    // so the result is bitwise that of evaluating it at each use.  The reaction diagonal
+    // qb u^2 + qa is kept for the output rows.
+    constexpr bool PRE = (MODE == M_LEJA || MODE == M_POWER);
+    double2 qd[kRTF];
+    if (PRE) {
 #pragma unroll
-    for (int t = 0; t < kRT; t++) {
-        if (t < nout) {
+        for (int t = 0; t < kRTF; t++) {
+            qd[t] = make_double2(0.0, 0.0);
+            if (S.react != 0.0) {
+                qd[t].x = fma(S.qb, uw[t + 1].x * uw[t + 1].x, S.qa);
+                qd[t].y = fma(S.qb, uw[t + 1].y * uw[t + 1].y, S.qa);
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < kRTF + 3; t++) {
+            uw[t].x = (nu + bt * uw[t].x) * w[t].x;
+            uw[t].y = (nu + bt * uw[t].y) * w[t].y;
+        }
+#pragma unroll
+        for (int t = 0; t < kRTF; t++) {
+            uhl[t] = (nu + bt * uhl[t]) * hl[t];
+            uhr[t].x = (nu + bt * uhr[t].x) * hr[t].x;
+            uhr[t].y = (nu + bt * uhr[t].y) * hr[t].y;
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < kRTF; t++) {
+        if (PRE && t < nout) {
+            const double2 yc = w[t + 1], up = w[t], dn1 = w[t + 2];
+            const double2 gc = uw[t + 1], gu = uw[t], gd1 = uw[t + 2], gd2 = uw[t + 3];
+            double yl = __shfl_up_sync(FULL_MASK, yc.y, 1);
+            double yr1 = __shfl_down_sync(FULL_MASK, yc.x, 1);
+            double gl = __shfl_up_sync(FULL_MASK, gc.y, 1);
+            double gr1 = __shfl_down_sync(FULL_MASK, gc.x, 1);
+            double gr2 = __shfl_down_sync(FULL_MASK, gc.y, 1);
+            if (lane == 0) {
+                yl = hl[t];
+                gl = uhl[t];
+            }
+            if (lane == last) {
+                yr1 = hr[t].x;
+                gr1 = uhr[t].x;
+                gr2 = uhr[t].y;
+            }
+            double res[2];
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const double y0 = h ? yc.y : yc.x;
+                const double ymr = h ? up.y : up.x, ypr = h ? dn1.y : dn1.x;
+                const double ymc = h ? yc.x : yl, ypc = h ? yr1 : yc.y;
+                const double g0 = h ? gc.y : gc.x;
+                const double gmr = h ? gu.y : gu.x, gpr = h ? gd1.y : gd1.x, gp2r = h ? gd2.y : gd2.x;
+                const double gmc = h ? gc.x : gl, gpc = h ? gr1 : gc.y, gp2c = h ? gr2 : gr1;
+                double adv = (S.a0[0] + S.a0[1]) * g0;
+                adv = fma(S.am1[0], gmr, adv);
+                adv = fma(S.ap1[0], gpr, adv);
+                adv = fma(S.ap2[0], gp2r, adv);
+                adv = fma(S.am1[1], gmc, adv);
+                adv = fma(S.ap1[1], gpc, adv);
+                adv = fma(S.ap2[1], gp2c, adv);
+                double lap = S.dd0 * y0;
+                lap = fma(S.dm1[0], ymr, lap);
+                lap = fma(S.dp1[0], ypr, lap);
+                lap = fma(S.dm1[1], ymc, lap);
+                lap = fma(S.dp1[1], ypc, lap);
+                double a = lap + adv;
+                if (S.react != 0.0) a = fma(h ? qd[t].y : qd[t].x, y0, a);
+                res[h] = a;
+            }
+            tile2d_flux_out<K, FIRST, MODE>(P, dst, i0 + t, j0, valid, yc, res, pv[t], beta, d0, dm, active,
+                                            scale, sy, sp);
+        } else if (!PRE && t < nout) {
             const double2 yc = w[t + 1], up = w[t], dn1 = w[t + 2], dn2 = w[t + 3];
             const double2 uc = TWO ? uw[t + 1] : yc, uu = TWO ? uw[t] : up;
             const double2 ud1 = TWO ? uw[t + 2] : dn1, ud2 = TWO ? uw[t + 3] : dn2;
@@ -646,50 +772,8 @@ __device__ __forceinline__ void tile2d_flux(const LejaParams& P, const RowSrc& s
                     res[h] = a;
                 }
             }
-            double2 yn;
-            if (MODE == M_POWER) {
-                yn.x = scale * res[0];
-                yn.y = scale * res[1];
-            } else if (MODE == M_RHS) {
-                double fx = res[0], fy = res[1];
-                if (P.source && valid) {
-                    const double2 sv = ldg2(P.source + (long long)(i0 + t) * n1 + j0);
-                    fx += sv.x;
-                    fy += sv.y;
-                }
-                yn.x = scale * fx;
-                yn.y = scale * fy;
-            } else if (MODE == M_REM) {
-                yn.x = res[0];
-                yn.y = res[1];
-            } else {
-                yn.x = fma(scale, res[0], beta * yc.x);
-                yn.y = fma(scale, res[1], beta * yc.y);
-            }
-            if (valid) {
-                const long long off = (long long)(i0 + t) * n1 + j0;
-                st2(dst + off, yn);
-                sy = fma(yn.x, yn.x, sy);
-                sy = fma(yn.y, yn.y, sy);
-                if (MODE == M_LEJA) {
-#pragma unroll
-                    for (int k = 0; k < KK; k++) {
-                        if ((active >> k) & 1) {
-                            double2 pn;
-                            if (FIRST) {
-                                pn.x = fma(dm[k], yn.x, d0[k] * yc.x);
-                                pn.y = fma(dm[k], yn.y, d0[k] * yc.y);
-                            } else {
-                                pn.x = fma(dm[k], yn.x, pv[t][k].x);
-                                pn.y = fma(dm[k], yn.y, pv[t][k].y);
-                            }
-                            st2(P.p[k] + off, pn);
-                            sp[k] = fma(pn.x, pn.x, sp[k]);
-                            sp[k] = fma(pn.y, pn.y, sp[k]);
-                        }
-                    }
-                }
-            }
+            tile2d_flux_out<K, FIRST, MODE>(P, dst, i0 + t, j0, valid, yc, res, pv[t], beta, d0, dm, active,
+                                            scale, sy, sp);
         }
     }
 }

@@ -327,7 +327,11 @@ static LejaParams base_params(lx_ctx* ctx, const lx_problem* pb) {
     }
     P.N_glob = ctx->N_glob;
     P.st = make_stencil(pb);
-    if (pb->flux != 0.0) P.ndim = 4;   // flux-form (Burgers) tile variant of the 2D kernels
+    if (pb->flux != 0.0) {
+        P.ndim = 4;   // flux-form (Burgers) tile variant of the 2D kernels
+        P.nrb = (P.n_loc + kRTF - 1) / kRTF;
+        P.nunits = P.nb * P.nrb;
+    }
     P.ctrl = ctx->ctrl;
     P.partials = ctx->partials;
     P.timeout_spins = 1 << 24;

@@ -6,7 +6,7 @@
 namespace lx {
 
 template <int NDIM, int K, bool DIAG>
-__global__ void __launch_bounds__(kThreads, (NDIM == 4 ? 1 : 2)) k_leja2d(const __grid_constant__ LejaParams P) {
+__global__ void __launch_bounds__(kThreads, 2) k_leja2d(const __grid_constant__ LejaParams P) {
     __shared__ double s_red[kWarps][kSlot];
     __shared__ int s_flags[4];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kThreads, (NDIM == 4 ? 1 : 2)) k_leja2d(const 
 }
 
 template <int NDIM, bool DIAG>
-__global__ void __launch_bounds__(kThreads, (NDIM == 4 ? 1 : 2)) k_power2d(const __grid_constant__ LejaParams P) {
+__global__ void __launch_bounds__(kThreads, 2) k_power2d(const __grid_constant__ LejaParams P) {
     __shared__ double s_red[kWarps][kSlot];
     __shared__ int s_flags[4];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
