@@ -452,6 +452,40 @@ def test_burgers_leja_power_rhs_integrate(xi300):
     assert it2 == tot and _rel(ud, u) <= TOL
 
 
+@pytest.mark.parametrize("shape", [(67, 90), (33, 130), (5, 64), (7, 62)])
+def test_burgers_ragged(xi300, shape):
+    # flux-form tile on ragged shapes: 2-row units with an odd row count (a last unit of one row),
+    # n1 not a multiple of the 64-column band, the smallest allowed grids; vertical K = 3, f, the spectrum
+    # estimate and a two-stage step (its remainders) against the oracle
+    n0, n1 = shape
+    dx = (2 / n0, 2 / n1)
+    pb, ob = lx.Problem(shape, dx, 1.0, 0.0, 0.0, None, 10.0), O.Problem(shape, dx, 1.0, 0.0, 0.0, None, 10.0)
+    u = W.ic_burgers_2d(n0, n1)
+    v = W.random_vector(shape, seed=31, scale=0.01)
+    dt = 10 * W.dt_cfl(max(shape), 20.0)
+    c, g = O.shift_scale(O.spectrum_bound(ob, u))
+    with lx.Context(pb) as ctx:
+        ud = _dev(u)
+        outs = [torch.empty_like(ud) for _ in range(3)]
+        it = lx.lx_real_leja_phi_vertical(ctx, _dev(v), outs, (0.25, 0.5, 1.0), dt, c, g, 1, TOL, TOL, u_lin=ud)
+        r = O.real_leja_phi(ob, v, dt, c, g, 1, TOL, TOL, xi300, u_lin=u, coeffs=(0.25, 0.5, 1.0))
+        assert it == r.iters
+        for k in range(3):
+            assert _rel(outs[k], r.outs[k]) <= TOL
+        f = torch.empty_like(ud)
+        lx.lx_rhs(ctx, ud, f, 0.25)
+        ref = 0.25 * O.rhs(ob, u)
+        assert np.abs(f.cpu().numpy() - ref).max() <= 1e-12 * np.abs(ref).max()
+        est = lx.lx_spectrum_estimate(ctx, ud, 20)
+        assert est == pytest.approx(O.power_iteration(ob, u, 20), rel=1e-10)
+        lo = torch.empty_like(ud)
+        hi = torch.empty_like(ud)
+        its, err = lx.lx_step(ctx, "epirk4s3a", ud, lo, hi, dt, c, g, TOL, TOL)
+        rs = O.step(ob, "epirk4s3a", u, dt, c, g, TOL, TOL, xi300)
+        assert its == rs.iters
+        assert _rel(hi, rs.u_high) <= TOL and _rel(lo, rs.u_low) <= TOL
+
+
 @pytest.mark.parametrize("shape,K,react,l", [((64, 64), 1, 0.0, 0), ((66, 62), 2, 0.0, 1), ((7, 24), 1, 0.0, 2),
                                              ((130, 122), 3, 1.0, 1), ((131, 182), 4, 0.0, 1),
                                              ((200, 60), 4, 1.0, 3), ((4096, 256), 1, 1.0, 0)])
