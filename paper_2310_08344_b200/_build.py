@@ -55,10 +55,15 @@ def build(verbose: bool = False, force: bool = False) -> str:
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
     hdr_mtime = max([os.path.getmtime(h) for h in _deps()] + [0])
     src_mtime = max([os.path.getmtime(x) for x in srcs] + [hdr_mtime, os.path.getmtime(__file__)])
+    flags = _flags()
+    # objects compiled with other flags (e.g. an NVCC_EXTRA variant build) are stale: rebuild everything
+    stamp = os.path.join(BUILD, "flags.txt")
+    key = " ".join(ARCH + flags)
+    if os.path.exists(stamp) and open(stamp).read() != key:
+        force = True
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= src_mtime:
         return LIB   # up to date (objects may be absent, e.g. on a gpurun box)
     objs = []
-    flags = _flags()
     cmds = []
     for s in srcs:
         o = os.path.join(BUILD, os.path.basename(s) + ".o")
@@ -85,6 +90,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
             print(" ".join(link), file=sys.stderr)
         subprocess.check_call(link)
         os.replace(LIB + ".tmp", LIB)
+    with open(stamp, "w") as fh:
+        fh.write(key)
     return LIB
 
 

@@ -332,46 +332,69 @@ __global__ void __launch_bounds__(kThreads) k_bb_norm(BbLin L) {
 // black-box path reproducible bit for bit wherever its inputs are (SURVEY 8(f) f-1 "FMA-off").
 __device__ __forceinline__ int lit_wrap(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
 
-// value of the input at offset o along dimension d from (i0, i1, i2); squared for the Burgers flux field
-__device__ __forceinline__ double lit_at(const RhsLit& R, int i0, int i1, int i2, int d, int o, bool sq) {
-    if (d == 0) i0 = lit_wrap(i0 + o, (int)R.n[0]);
-    else if (d == 1) i1 = lit_wrap(i1 + o, (int)R.n[1]);
-    else i2 = lit_wrap(i2 + o, (int)R.n[2]);
-    const double v = R.in[((size_t)i0 * R.n[1] + i1) * R.n[2] + i2];
-    return sq ? __dmul_rn(v, v) : v;
-}
-
-__device__ __forceinline__ double lit_upwind(double wm1, double w0, double w1, double w2, double h) {
+__device__ __forceinline__ double lit_upwind(double wm1, double w0, double w1, double w2, double h6) {
     return __ddiv_rn(__dsub_rn(__dsub_rn(__dadd_rn(-w2, __dmul_rn(6.0, w1)), __dmul_rn(3.0, w0)), __dmul_rn(2.0, wm1)),
-                     __dmul_rn(6.0, h));
+                     h6);
 }
 
-// grid: x over the contiguous dimension, y over the rows (i0, i1) -- no 64-bit index division
+// grid: x over the contiguous dimension, y over the rows (i0, i1) -- no 64-bit index division.  The
+// dimension loop is unrolled over NDIM, the four values per dimension are gathered from 32-bit row /
+// column offsets, and h h, 6 h are rounded once per thread: the same rounded operations in the same
+// order as the formula above, only the address arithmetic is cheaper.
+template <int NDIM, bool FLUX>
 __global__ void __launch_bounds__(kThreads) k_rhs_literal(RhsLit R) {
     // rows = all but the contiguous dimension (2D: dim 0; 3D: dims 0, 1)
-    const bool d3 = R.ndim == 3;
-    const int nrow = d3 ? (int)(R.n[0] * R.n[1]) : (int)R.n[0];
-    const int ninner = d3 ? (int)R.n[2] : (int)R.n[1];
+    constexpr bool d3 = NDIM == 3;
+    const int n0 = (int)R.n[0], n1 = (int)R.n[1];
+    const int nrow = d3 ? n0 * n1 : n0;
+    const int ninner = d3 ? (int)R.n[2] : n1;
+    double hh[NDIM], h6[NDIM];
+#pragma unroll
+    for (int d = 0; d < NDIM; d++) {
+        hh[d] = __dmul_rn(R.dx[d], R.dx[d]);
+        h6[d] = __dmul_rn(6.0, R.dx[d]);
+    }
+    const double* __restrict__ in = R.in;
     for (int row = blockIdx.y; row < nrow; row += gridDim.y) {
-        const int r0 = d3 ? row / (int)R.n[1] : row, r1 = d3 ? row - r0 * (int)R.n[1] : 0;
-        for (int in = blockIdx.x * kThreads + threadIdx.x; in < ninner; in += gridDim.x * kThreads) {
-            const int i0 = r0, i1 = d3 ? r1 : in, i2 = d3 ? in : 0;
-            double lap = 0.0, adv = 0.0, flx = 0.0;
-            for (int d = 0; d < R.ndim; d++) {
-                const double h = R.dx[d];
-                const double um1 = lit_at(R, i0, i1, i2, d, -1, false), u0 = lit_at(R, i0, i1, i2, d, 0, false);
-                const double up1 = lit_at(R, i0, i1, i2, d, 1, false), up2 = lit_at(R, i0, i1, i2, d, 2, false);
-                lap = __dadd_rn(lap, __ddiv_rn(__dadd_rn(__dsub_rn(up1, __dmul_rn(2.0, u0)), um1), __dmul_rn(h, h)));
-                adv = __dadd_rn(adv, lit_upwind(um1, u0, up1, up2, h));
-                if (R.flux != 0.0)
-                    flx = __dadd_rn(flx, lit_upwind(lit_at(R, i0, i1, i2, d, -1, true), lit_at(R, i0, i1, i2, d, 0, true),
-                                                    lit_at(R, i0, i1, i2, d, 1, true), lit_at(R, i0, i1, i2, d, 2, true), h));
+        const int r0 = d3 ? row / n1 : row, r1 = d3 ? row - r0 * n1 : 0;
+        // neighbour rows along the non-contiguous dimensions: row index of offset o = -1, +1, +2
+        int rows[NDIM - 1][3];
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+            const int o = q == 0 ? -1 : q;
+            rows[0][q] = d3 ? lit_wrap(r0 + o, n0) * n1 + r1 : lit_wrap(r0 + o, n0);
+            if (d3) rows[NDIM - 2][q] = r0 * n1 + lit_wrap(r1 + o, n1);
+        }
+        const size_t base = (size_t)row * ninner;
+        for (int c = blockIdx.x * kThreads + threadIdx.x; c < ninner; c += gridDim.x * kThreads) {
+            // v[d] = (w_{-1}, w_0, w_{+1}, w_{+2}) along dimension d
+            double v[NDIM][4];
+            const double u0 = __ldg(in + base + c);
+#pragma unroll
+            for (int d = 0; d < NDIM - 1; d++) {
+                v[d][0] = __ldg(in + (size_t)rows[d][0] * ninner + c);
+                v[d][1] = u0;
+                v[d][2] = __ldg(in + (size_t)rows[d][1] * ninner + c);
+                v[d][3] = __ldg(in + (size_t)rows[d][2] * ninner + c);
             }
-            const size_t idx = (size_t)row * ninner + in;
+            v[NDIM - 1][0] = __ldg(in + base + lit_wrap(c - 1, ninner));
+            v[NDIM - 1][1] = u0;
+            v[NDIM - 1][2] = __ldg(in + base + lit_wrap(c + 1, ninner));
+            v[NDIM - 1][3] = __ldg(in + base + lit_wrap(c + 2, ninner));
+            double lap = 0.0, adv = 0.0, flx = 0.0;
+#pragma unroll
+            for (int d = 0; d < NDIM; d++) {
+                const double um1 = v[d][0], uc = v[d][1], up1 = v[d][2], up2 = v[d][3];
+                lap = __dadd_rn(lap, __ddiv_rn(__dadd_rn(__dsub_rn(up1, __dmul_rn(2.0, uc)), um1), hh[d]));
+                adv = __dadd_rn(adv, lit_upwind(um1, uc, up1, up2, h6[d]));
+                if (FLUX)
+                    flx = __dadd_rn(flx, lit_upwind(__dmul_rn(um1, um1), __dmul_rn(uc, uc), __dmul_rn(up1, up1),
+                                                    __dmul_rn(up2, up2), h6[d]));
+            }
+            const size_t idx = base + c;
             double f = __dadd_rn(__dmul_rn(R.diff, lap), __dmul_rn(R.nu, adv));
-            if (R.flux != 0.0) f = __dadd_rn(f, __dmul_rn(__dmul_rn(R.flux, 0.5), flx));
-            const double u = R.in[idx];
-            if (R.react != 0.0) f = __dadd_rn(f, __dmul_rn(R.react, __dsub_rn(u, __dmul_rn(__dmul_rn(u, u), u))));
+            if (FLUX) f = __dadd_rn(f, __dmul_rn(__dmul_rn(R.flux, 0.5), flx));
+            if (R.react != 0.0) f = __dadd_rn(f, __dmul_rn(R.react, __dsub_rn(u0, __dmul_rn(__dmul_rn(u0, u0), u0))));
             if (R.src) f = __dadd_rn(f, R.src[idx]);
             R.out[idx] = f;
         }
@@ -418,7 +441,14 @@ cudaError_t launch_rhs_literal(const RhsLit& R, int grid, cudaStream_t s) {
     const int gx = (int)((ninner + kThreads - 1) / kThreads);
     const int gy = (int)(nrow < 65535 ? nrow : 65535);
     (void)grid;
-    k_rhs_literal<<<dim3(gx, gy), kThreads, 0, s>>>(R);
+    const dim3 g(gx, gy);
+    if (R.ndim == 3) {
+        if (R.flux != 0.0) k_rhs_literal<3, true><<<g, kThreads, 0, s>>>(R);
+        else k_rhs_literal<3, false><<<g, kThreads, 0, s>>>(R);
+    } else {
+        if (R.flux != 0.0) k_rhs_literal<2, true><<<g, kThreads, 0, s>>>(R);
+        else k_rhs_literal<2, false><<<g, kThreads, 0, s>>>(R);
+    }
     return cudaGetLastError();
 }
 cudaError_t launch_bb_norm(const BbLin& L, cudaStream_t s) {
@@ -430,7 +460,8 @@ cudaError_t preload_bb_kernels() {
     const void* ks[] = {(const void*)k_bb_init, (const void*)k_bb_perturb, (const void*)k_bb_update<1>,
                         (const void*)k_bb_update<2>, (const void*)k_bb_update<3>, (const void*)k_bb_update<4>,
                         (const void*)k_bb_maxabs, (const void*)k_bb_fdpiece, (const void*)k_bb_lincomb,
-                        (const void*)k_bb_norm, (const void*)k_rhs_literal};
+                        (const void*)k_bb_norm, (const void*)k_rhs_literal<2, false>, (const void*)k_rhs_literal<2, true>,
+                        (const void*)k_rhs_literal<3, false>, (const void*)k_rhs_literal<3, true>};
     for (const void* k : ks) {
         cudaFuncAttributes a;
         const cudaError_t e = cudaFuncGetAttributes(&a, k);

@@ -121,7 +121,7 @@ struct lx_ctx {
     BbCtrl* bb = nullptr;                 // device control block
     int* bb_done_host = nullptr;          // mapped pinned word written by the deciding CTA
     int* bb_done_dev = nullptr;           // its device alias
-    cudaEvent_t bb_ev[2] = {};
+    cudaEvent_t bb_ev[4] = {};
     double* B[kBb] = {};                  // black-box vectors: f(u), f_u dt, t1..t7, w, f(w)
 };
 
@@ -1913,10 +1913,11 @@ struct BbRun {
             }
             CUDA_TRY(launch_bb_update(A, m, ctx->stream));
             ctx->launches += u ? 2 : 1;
-            CUDA_TRY(cudaEventRecord(ctx->bb_ev[m & 1], ctx->stream));
-            // one iteration in flight: wait for the decision of m - 1 while m runs
-            if (m >= 2) {
-                CUDA_TRY(cudaEventSynchronize(ctx->bb_ev[(m - 1) & 1]));
+            CUDA_TRY(cudaEventRecord(ctx->bb_ev[m & 3], ctx->stream));
+            // kBbLag iterations in flight: wait for the decision of m - kBbLag while the later ones run
+            // (their kernels return at entry once the decision says done; f still runs on an unchanged w)
+            if (m > kBbLag) {
+                CUDA_TRY(cudaEventSynchronize(ctx->bb_ev[(m - kBbLag) & 3]));
                 if (*(volatile int*)ctx->bb_done_host) break;
             }
         }

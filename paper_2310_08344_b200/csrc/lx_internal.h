@@ -15,6 +15,10 @@ constexpr int kRT = 4;            // rows per warp work unit (2D)
 // rows per warp work unit of the flux-form (Burgers) 2D tile: two, so the kernel fits two CTAs per SM
 // (measured at 4096^2: phi_1 0.60 -> 0.72 of the copy peak vs four rows at one CTA per SM)
 constexpr int kRTF = 2;
+// black-box Leja: iterations enqueued ahead of the decision the host reads (<= 3).  Measured (4096^2 FD / linear):
+// 2 or 3 in flight are 2-4 % slower than 1 -- the extra f evaluations after convergence cost more than the
+// host's wake-up latency they hide.
+constexpr int kBbLag = 1;
 constexpr int kRT3 = LX_KRT3;         // planes per warp work unit (3D)
 // two-step (temporally blocked) kernel: rows per chunk, bytes of one staged chunk, ring depth
 // (chunks per warp ring; 8 warps x depth x stage <= 110 KB so that two CTAs fit on an SM)
