@@ -100,9 +100,26 @@ __global__ void __launch_bounds__(kThreads) k_bb_perturb(BbArgs A, int m) {
     const double eps = fd_eps(c, (m - 1) & 1);
     const long long N = A.N;
     const long long npair = N >> 1;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < npair; i += (long long)gridDim.x * blockDim.x) {
-        const double2 u = ld2g(A.u + 2 * i), y = ld2g(A.y_in + 2 * i);
-        st2g(A.w + 2 * i, make_double2(__dadd_rn(u.x, __dmul_rn(eps, y.x)), __dadd_rn(u.y, __dmul_rn(eps, y.y))));
+    // 4 element pairs per trip, all loads issued before the stores (bytes in flight for a 2-CTA/SM grid)
+    constexpr int UN = 4;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < npair; i0 += UN * stride) {
+        double2 u[UN], y[UN];
+#pragma unroll
+        for (int q = 0; q < UN; q++) {
+            const long long i = i0 + q * stride;
+            if (i < npair) {
+                u[q] = ld2g(A.u + 2 * i);
+                y[q] = ld2g(A.y_in + 2 * i);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < UN; q++) {
+            const long long i = i0 + q * stride;
+            if (i < npair)
+                st2g(A.w + 2 * i, make_double2(__dadd_rn(u[q].x, __dmul_rn(eps, y[q].x)),
+                                               __dadd_rn(u[q].y, __dmul_rn(eps, y[q].y))));
+        }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (N & 1) A.w[N - 1] = __dadd_rn(A.u[N - 1], __dmul_rn(eps, A.y_in[N - 1]));
