@@ -1230,7 +1230,7 @@ static lx_status rhs_device(lx_ctx* ctx, const lx_problem* pb, const double* u, 
         return LX_OK;
     }
     P.grid = (P.nunits + kWarps - 1) / kWarps;
-    if (P.grid > ctx->nsm * 4) P.grid = ctx->nsm * 4;
+    if (P.grid > ctx->nsm * 3) P.grid = ctx->nsm * 3;   // one wave at 3 CTAs per SM (k_rhs2d's launch bounds)
     CUDA_TRY(launch_rhs(P, scale, ctx->stream));
     ctx->launches++;
     return LX_OK;
